@@ -1,0 +1,203 @@
+/*
+ * drcb.h — C ABI of libdrcb.so, the B200 (sm_100a) implementation of the
+ * deep-radiance-cache hot path of arXiv 1910.02480.
+ *
+ * Every entry point replaces one Python surface of the reference
+ * (/root/reference/pkg); the reference interface is cited beside each one.
+ * Conventions
+ *   - plain C types only; no torch, no C++ across the ABI;
+ *   - all array arguments are DEVICE pointers owned by the caller unless
+ *     the comment says "host";
+ *   - every call is asynchronous on the `stream` argument (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream);
+ *   - return 0 on success or a DRCB_E* status; drcb_last_error() returns a
+ *     thread-local message. Status codes mirror drc/errors.py:4-31.
+ *   - `precision` selects the arithmetic of the ray/path kernels: 64 = the
+ *     fp64 parity build (matches the reference's float64 numpy), 32 = fp32.
+ */
+#ifndef DRCB_H
+#define DRCB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (drc/errors.py:4-31 -> 1..4; CUDA/NCCL failures 10/11) */
+#define DRCB_OK 0
+#define DRCB_ECONFIG 1      /* ConfigError      */
+#define DRCB_ECONTRACT 2    /* ContractError    */
+#define DRCB_EFORMAT 3      /* FormatError      */
+#define DRCB_EVALIDATION 4  /* SceneValidationError */
+#define DRCB_ECUDA 10
+#define DRCB_ENCCL 11
+
+/* material kinds (drc/bsdf.py:24) */
+#define DRCB_DIFFUSE 0
+#define DRCB_GLOSSY 1
+#define DRCB_MIRROR 2
+#define DRCB_TRANSMISSION 3
+
+typedef struct DrcbScene DrcbScene;
+typedef struct DrcbNet DrcbNet;
+typedef struct DrcbTrainer DrcbTrainer;
+
+/* Scene geometry + materials + lights, all HOST pointers, copied at create.
+ * Prim ids are global over [spheres | quads | triangles] in shape order
+ * (drc/geometry.py:48-119). */
+typedef struct DrcbSceneDesc {
+  int32_t n_spheres, n_quads, n_tris, n_materials, n_point_lights;
+  const double *sph_center;  /* (n_spheres,3) */
+  const double *sph_radius;  /* (n_spheres,)  */
+  const int32_t *sph_mat;
+  const double *quad_corner, *quad_eu, *quad_ev; /* (n_quads,3) each */
+  const int32_t *quad_mat;
+  const double *tri_v0, *tri_v1, *tri_v2;        /* (n_tris,3) each  */
+  const int32_t *tri_mat;
+  const int32_t *mat_kind;      /* (n_materials,) DRCB_DIFFUSE..       */
+  const double *mat_albedo;     /* (n_materials,3)                      */
+  const double *mat_exponent;   /* Phong exponent 2/r^2-2, 0 otherwise  */
+  const double *mat_ior;        /* 1 unless transmission                */
+  const double *mat_emission;   /* (n_materials,3)                      */
+  const double *point_pos, *point_intensity;    /* (n_point_lights,3)  */
+  double global_up[3];
+  double rotated_up[3];         /* bsdf._rotated_up(global_up), host-computed */
+  double environment[3];
+} DrcbSceneDesc;
+
+/* Pinhole camera (drc/scene.py:70-93); the basis is precomputed on the
+ * host exactly as Camera.basis() does. */
+typedef struct DrcbCamera {
+  double position[3], forward[3], right[3], up[3];
+  double tan_half;   /* tan(radians(fov)/2) */
+  int32_t width, height;
+} DrcbCamera;
+
+/* RenderConfig subset used on the device (drc/integrators.py:41-72). */
+typedef struct DrcbRenderCfg {
+  int32_t direct_spp;
+  int32_t max_path_depth;
+  int32_t mis_samples;
+  int32_t rr_start;
+  int32_t sampler_kind;   /* 0 independent, 1 stratified (drc/sampler.py:46-78) */
+  int32_t precision;      /* 32 or 64 */
+  int32_t tile;           /* RenderConfig.tile: only fixes the direct-pass
+                             summation grouping (cache.py:399-413) */
+  int32_t include_background; /* direct pass: add env seen by camera chains
+                                 (render(mode="direct") = 1; render_drc = 0) */
+  uint64_t seed;
+} DrcbRenderCfg;
+
+/* Primary-chain G-buffer, one row per pixel (drc/integrators.py:427-518).
+ * Real-typed fields use `precision`. */
+typedef struct DrcbGBuffer {
+  uint8_t *found, *escaped;
+  void *position, *normal, *throughput, *direction, *t_total; /* (n,3)/(n,) */
+  int32_t *mat;
+} DrcbGBuffer;
+
+/* ---- scene ------------------------------------------------------------ */
+/* Geometry(scene) + BVH (drc/geometry.py:48-185, 335-460). */
+int drcb_scene_create(const DrcbSceneDesc *desc, DrcbScene **out);
+void drcb_scene_destroy(DrcbScene *scene);
+/* host out[0..7]: n_prims, n_nodes, n_leaves, max_depth, n_lights, bytes */
+int drcb_scene_stats(const DrcbScene *scene, int64_t *out8);
+
+/* ---- stage kernels ---------------------------------------------------- */
+/* intersect_batch / occluded_batch (drc/geometry.py:217-329).
+ * O, D: (n,3) Real; tmin/tmax: (n,) Real or NULL (T_EPS / +inf).
+ * record=0 fills hit/t/prim only. */
+int drcb_intersect(const DrcbScene *scene, int32_t precision, const void *O,
+                   const void *D, int64_t n, const void *tmin, const void *tmax,
+                   int32_t record, uint8_t *hit, void *t, int64_t *prim,
+                   int32_t *mat, void *pos, void *nrm, void *stream);
+
+/* primary_chain_batch (drc/integrators.py:427-518). */
+int drcb_primary_chain(const DrcbScene *scene, int32_t precision,
+                       const void *O, const void *D, int64_t n,
+                       const DrcbGBuffer *out, void *stream);
+
+/* li_direct_batch (drc/integrators.py:305-424). keys: (n,) uint64.
+ * nonfinite: device int64 counter (may be NULL). */
+int drcb_li_direct(const DrcbScene *scene, const DrcbRenderCfg *cfg,
+                   const void *O, const void *D, const uint64_t *pix,
+                   const uint64_t *smp, int64_t n, int32_t include_background,
+                   void *L, int64_t *nonfinite, void *stream);
+
+/* trace_radiance_batch (drc/integrators.py:175-302). */
+int drcb_trace_radiance(const DrcbScene *scene, const DrcbRenderCfg *cfg,
+                        const void *O, const void *D, const uint64_t *pix,
+                        const uint64_t *smp, int64_t n, int32_t max_depth,
+                        int32_t skip_first_emission, int32_t rr_start,
+                        void *L, int64_t *nonfinite, void *stream);
+
+/* DrcState geometry buffers + the direct pass, fused
+ * (drc/cache.py:157-176 + 393-423): unjittered centre chains into `gb`,
+ * direct_spp jittered li_direct samples averaged into direct (H*W,3) Real. */
+int drcb_gbuffer_direct(const DrcbScene *scene, const DrcbCamera *cam,
+                        const DrcbRenderCfg *cfg, const DrcbGBuffer *gb,
+                        void *direct, int64_t *nonfinite, void *stream);
+
+/* render_input_stacks_batch (drc/hemimap.py:229-281) for n cache points.
+ * pos/nrm: (n,3) Real front-facing hit data; keys (n,) uint64.
+ * Outputs: stacks (n,7,32,32) float32 NCHW (InputStack.as_tensor order),
+ * s_r, s_d: (n,) Real; frames (n,9) Real (t,b,n of build_frame). */
+int drcb_render_stacks(const DrcbScene *scene, const DrcbRenderCfg *cfg,
+                       const void *pos, const void *nrm, const uint64_t *keys,
+                       int64_t n, float *stacks, void *s_r, void *s_d,
+                       void *frames, int64_t *nonfinite, void *stream);
+
+/* shade_indirect (drc/integrators.py:564-614) over n points.
+ * pred: (n,3,32,32) float32 network output (normalised); frames (n,9);
+ * wo (n,3) = -direction; mat (n,) int32; out L (n,3) Real. */
+int drcb_shade(const DrcbScene *scene, const DrcbRenderCfg *cfg,
+               const float *pred, const void *s_r, const void *frames,
+               const void *wo, const int32_t *mat, const uint64_t *keys,
+               int64_t n, void *L, void *stream);
+
+/* _interpolate_layer + composite (drc/cache.py:283-345, 463).
+ * Entries: e_px,e_py (m,) int32, e_normal,e_rad (m,3) Real.
+ * image (H*W,3) Real = direct + layer (direct may be NULL -> layer only). */
+int drcb_interp_composite(const DrcbScene *scene, int32_t precision,
+                          int32_t width, int32_t height, const DrcbGBuffer *gb,
+                          const int32_t *e_px, const int32_t *e_py,
+                          const void *e_normal, const void *e_rad, int64_t m,
+                          int32_t r, const void *direct, void *image,
+                          void *stream);
+
+/* Whole frame (drc/cache.py:377-470): gbuffer+direct, then the planned
+ * cache points (host arrays px,py,keys in budget order, n_points), stacks,
+ * network, shade, compaction, interpolation with final pass spacing r,
+ * composite. image: (H*W,3) Real device. telemetry (host, 8 x int64):
+ * entries, fallback_pixels(=0), nonfinite, n_points, ... */
+int drcb_render_drc(const DrcbScene *scene, const DrcbNet *net,
+                    const DrcbCamera *cam, const DrcbRenderCfg *cfg,
+                    const int32_t *px_host, const int32_t *py_host,
+                    const uint64_t *keys_host, int64_t n_points, int32_t r_final,
+                    int32_t net_mode, void *image, int64_t *telemetry_host,
+                    void *stream);
+
+/* ---- network ---------------------------------------------------------- */
+/* DRCW container parse + validation (drc/cnn.py:221-281): host bytes. */
+int drcb_net_create(const void *drcw, size_t len, DrcbNet **out);
+void drcb_net_destroy(DrcbNet *net);
+/* host out: k, n_params, version, slope bits */
+int drcb_net_info(const DrcbNet *net, int64_t *out4);
+/* forward (drc/cnn.py:193-215; trainer model.py:80-88 eval mode):
+ * x (n,7,32,32) f32 -> y (n,3,32,32) f32.
+ * mode: 0 fp32 SIMT (exact), 1 tf32 tcgen05, 2 bf16 tcgen05. */
+#define DRCB_NET_FP32 0
+#define DRCB_NET_TF32 1
+#define DRCB_NET_BF16 2
+int drcb_net_forward(const DrcbNet *net, const float *x, float *y, int64_t n,
+                     int32_t mode, void *stream);
+
+const char *drcb_last_error(void);
+int drcb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DRCB_H */

@@ -1,0 +1,377 @@
+// drcb_capi.cu — extern "C" entry points of libdrcb.so (include/drcb.h) and
+// the whole-frame driver drcb_render_drc (drc/cache.py:377-470).
+#include <cub/cub.cuh>
+#include <cstring>
+#include <string>
+
+#include "drcb_net.h"
+
+namespace drcb {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return DRCB_ECUDA;
+}
+
+int forward_f32(const NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t st);
+int forward_tc(NetImpl& net, const float* x, float* y, int64_t n, int mode, cudaStream_t st);
+
+int forward_f32_chunked(const NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t st) {
+  for (int64_t done = 0; done < n;) {
+    int64_t c = n - done < 2048 ? n - done : 2048;
+    int rc = forward_f32(net, x + done * 7 * 1024, y + done * 3 * 1024, c, st);
+    if (rc) return rc;
+    done += c;
+  }
+  return 0;
+}
+
+namespace {
+
+cudaStream_t S_(void* s) { return static_cast<cudaStream_t>(s); }
+
+int check_precision(int p) {
+  if (p != 32 && p != 64) return fail(DRCB_ECONFIG, "precision must be 32 or 64");
+  return 0;
+}
+
+int check_cfg(const DrcbRenderCfg* c) {
+  if (!c) return fail(DRCB_ECONTRACT, "null render config");
+  if (check_precision(c->precision)) return DRCB_ECONFIG;
+  if (c->direct_spp < 1 || c->max_path_depth < 1 || c->rr_start < 1 || c->tile < 1)
+    return fail(DRCB_ECONFIG, "direct_spp, max_path_depth, rr_start, tile must be >= 1");
+  if (c->mis_samples < 2) return fail(DRCB_ECONFIG, "mis_samples must be >= 2");
+  if (c->sampler_kind != 0 && c->sampler_kind != 1)
+    return fail(DRCB_ECONFIG, "unknown sampler kind");
+  return 0;
+}
+
+// gather cache-point hit data from the G-buffer (cache.py:211-220, 239-244)
+template <typename R>
+__global__ void k_gather_points(DrcbGBuffer gb, int W, const int32_t* px, const int32_t* py,
+                                int64_t n, R* pos, R* nrm, R* wo, int32_t* mat, uint8_t* live) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t q = int64_t(py[i]) * W + px[i];
+  bool f = gb.found[q];
+  live[i] = f;
+  const R* P = static_cast<const R*>(gb.position) + 3 * q;
+  const R* N = static_cast<const R*>(gb.normal) + 3 * q;
+  const R* D = static_cast<const R*>(gb.direction) + 3 * q;
+  for (int k = 0; k < 3; ++k) {
+    pos[3 * i + k] = P[k];
+    nrm[3 * i + k] = N[k];
+    wo[3 * i + k] = -D[k];
+  }
+  mat[i] = f ? gb.mat[q] : 0;
+}
+
+// stable compaction of live points into the entry pool (append order =
+// task order, cache.py:183-190, 450-452)
+template <typename R>
+__global__ void k_scatter_entries(const uint8_t* live, const int* rank, int64_t n,
+                                  const int32_t* px, const int32_t* py, const R* nrm, const R* L,
+                                  int32_t* epx, int32_t* epy, R* en, R* erad) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n || !live[i]) return;
+  int j = rank[i];
+  epx[j] = px[i];
+  epy[j] = py[i];
+  for (int k = 0; k < 3; ++k) {
+    en[3 * j + k] = nrm[3 * i + k];
+    erad[3 * j + k] = L[3 * i + k];
+  }
+}
+
+__global__ void k_u8_to_int(const uint8_t* a, int* b, int64_t n) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = a[i];
+}
+
+template <typename R>
+int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
+                 const DrcbRenderCfg* cfg, const int32_t* px_h, const int32_t* py_h,
+                 const uint64_t* keys_h, int64_t np_, int r_final, int net_mode, R* image,
+                 int64_t* tel, cudaStream_t st) {
+  const DevScene& S = scene->dev;
+  DevCamera C = make_camera(*cam);
+  const int W = C.W, H = C.H;
+  const int64_t npx = int64_t(W) * H;
+  // ---- frame buffers
+  size_t bytes = npx * (2 + 4 + sizeof(R) * 16) + 64;
+  uint8_t* fb = nullptr;
+  DRCB_CUDA(cudaMallocAsync((void**)&fb, bytes, st));
+  DrcbGBuffer gb;
+  uint8_t* cur = fb;
+  auto take = [&](size_t b) {
+    uint8_t* p = cur;
+    cur += (b + 15) & ~size_t(15);
+    return p;
+  };
+  R* direct = (R*)take(npx * 3 * sizeof(R));
+  gb.position = take(npx * 3 * sizeof(R));
+  gb.normal = take(npx * 3 * sizeof(R));
+  gb.throughput = take(npx * 3 * sizeof(R));
+  gb.direction = take(npx * 3 * sizeof(R));
+  gb.t_total = take(npx * sizeof(R));
+  gb.mat = (int32_t*)take(npx * 4);
+  gb.found = take(npx);
+  gb.escaped = take(npx);
+  int64_t* d_nf = nullptr;
+  DRCB_CUDA(cudaMallocAsync((void**)&d_nf, 8, st));
+  DRCB_CUDA(cudaMemsetAsync(d_nf, 0, 8, st));
+  DrcbRenderCfg dcfg = *cfg;
+  dcfg.include_background = 0;  // escaped chains carry the env in the indirect layer
+  int rc = launch_gbuffer_direct<R>(S, C, dcfg, cfg->tile, gb, direct, d_nf, st);
+  if (rc) return rc;
+  // ---- cache points
+  int64_t m = 0;
+  int32_t* epx = nullptr;
+  uint8_t* pb = nullptr;
+  if (np_ > 0) {
+    size_t pbytes = np_ * (4 + 4 + 8 + 4 + 1 + 4 + 4 + 4 + 4 + sizeof(R) * (3 * 6 + 2 + 9)) + 32 * 16 +
+                    np_ * size_t(7 + 3) * 1024 * 4 + 1024;
+    DRCB_CUDA(cudaMallocAsync((void**)&pb, pbytes, st));
+    cur = pb;
+    int32_t* px = (int32_t*)take(np_ * 4);
+    int32_t* py = (int32_t*)take(np_ * 4);
+    uint64_t* keys = (uint64_t*)take(np_ * 8);
+    int32_t* mat = (int32_t*)take(np_ * 4);
+    uint8_t* live = take(np_);
+    int* rank = (int*)take(np_ * 4);
+    R* pos = (R*)take(np_ * 3 * sizeof(R));
+    R* nrm = (R*)take(np_ * 3 * sizeof(R));
+    R* wo = (R*)take(np_ * 3 * sizeof(R));
+    R* Le = (R*)take(np_ * 3 * sizeof(R));
+    R* en = (R*)take(np_ * 3 * sizeof(R));
+    R* erad = (R*)take(np_ * 3 * sizeof(R));
+    R* s_r = (R*)take(np_ * sizeof(R));
+    R* s_d = (R*)take(np_ * sizeof(R));
+    R* frames = (R*)take(np_ * 9 * sizeof(R));
+    float* stacks = (float*)take(np_ * 7 * 1024 * 4);
+    float* pred = (float*)take(np_ * 3 * 1024 * 4);
+    epx = (int32_t*)take(np_ * 4);
+    int32_t* epy = (int32_t*)take(np_ * 4);
+    DRCB_CUDA(cudaMemcpyAsync(px, px_h, np_ * 4, cudaMemcpyHostToDevice, st));
+    DRCB_CUDA(cudaMemcpyAsync(py, py_h, np_ * 4, cudaMemcpyHostToDevice, st));
+    DRCB_CUDA(cudaMemcpyAsync(keys, keys_h, np_ * 8, cudaMemcpyHostToDevice, st));
+    int nb = int((np_ + 127) / 128);
+    k_gather_points<R><<<nb, 128, 0, st>>>(gb, W, px, py, np_, pos, nrm, wo, mat, live);
+    rc = launch_render_stacks<R>(S, *cfg, pos, nrm, keys, live, np_, stacks, s_r, s_d, frames,
+                                 d_nf, st);
+    if (rc) return rc;
+    if (net_mode == DRCB_NET_FP32)
+      rc = forward_f32_chunked(net->impl, stacks, pred, np_, st);
+    else
+      rc = forward_tc(net->impl, stacks, pred, np_, net_mode, st);
+    if (rc) return rc;
+    rc = launch_shade<R>(S, *cfg, pred, s_r, frames, wo, mat, keys, live, np_, Le, st);
+    if (rc) return rc;
+    // live-point compaction
+    int* flags = (int*)take(np_ * 4);
+    k_u8_to_int<<<nb, 128, 0, st>>>(live, flags, np_);
+    size_t tmpb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmpb, flags, rank, int(np_), st);
+    void* tmp = nullptr;
+    DRCB_CUDA(cudaMallocAsync(&tmp, tmpb, st));
+    cub::DeviceScan::ExclusiveSum(tmp, tmpb, flags, rank, int(np_), st);
+    DRCB_CUDA(cudaFreeAsync(tmp, st));
+    k_scatter_entries<R><<<nb, 128, 0, st>>>(live, rank, np_, px, py, nrm, Le, epx, epy, en, erad);
+    int last_rank = 0;
+    uint8_t last_live = 0;
+    DRCB_CUDA(cudaMemcpyAsync(&last_rank, rank + np_ - 1, 4, cudaMemcpyDeviceToHost, st));
+    DRCB_CUDA(cudaMemcpyAsync(&last_live, live + np_ - 1, 1, cudaMemcpyDeviceToHost, st));
+    DRCB_CUDA(cudaStreamSynchronize(st));
+    m = int64_t(last_rank) + last_live;
+    rc = launch_interp_composite<R>(S, W, H, gb, epx, epy, en, erad, m, r_final, direct, image, st);
+    if (rc) return rc;
+  } else {
+    rc = launch_interp_composite<R>(S, W, H, gb, nullptr, nullptr, nullptr, nullptr, 0, r_final,
+                                    direct, image, st);
+    if (rc) return rc;
+  }
+  int64_t nf = 0;
+  DRCB_CUDA(cudaMemcpyAsync(&nf, d_nf, 8, cudaMemcpyDeviceToHost, st));
+  DRCB_CUDA(cudaStreamSynchronize(st));
+  if (pb) DRCB_CUDA(cudaFreeAsync(pb, st));
+  DRCB_CUDA(cudaFreeAsync(fb, st));
+  DRCB_CUDA(cudaFreeAsync(d_nf, st));
+  if (tel) {
+    tel[0] = m;
+    tel[1] = 0;
+    tel[2] = nf;
+    tel[3] = np_;
+    for (int k = 4; k < 8; ++k) tel[k] = 0;
+  }
+  return 0;
+}
+
+}  // namespace
+}  // namespace drcb
+
+using namespace drcb;
+
+#define NEED(x) \
+  if (!(x)) return fail(DRCB_ECONTRACT, std::string(__func__) + ": null " #x)
+
+extern "C" const char* drcb_last_error(void) { return g_err.c_str(); }
+extern "C" int drcb_version(void) { return 1; }
+
+extern "C" int drcb_intersect(const DrcbScene* scene, int32_t precision, const void* O,
+                              const void* D, int64_t n, const void* tmin, const void* tmax,
+                              int32_t record, uint8_t* hit, void* t, int64_t* prim, int32_t* mat,
+                              void* pos, void* nrm, void* stream) {
+  NEED(scene);
+  NEED(hit);
+  if (check_precision(precision)) return DRCB_ECONFIG;
+  if (precision == 64)
+    return launch_intersect<double>(scene->dev, (const double*)O, (const double*)D, n,
+                                    (const double*)tmin, (const double*)tmax, record, hit,
+                                    (double*)t, prim, mat, (double*)pos, (double*)nrm, S_(stream));
+  return launch_intersect<float>(scene->dev, (const float*)O, (const float*)D, n,
+                                 (const float*)tmin, (const float*)tmax, record, hit, (float*)t,
+                                 prim, mat, (float*)pos, (float*)nrm, S_(stream));
+}
+
+extern "C" int drcb_primary_chain(const DrcbScene* scene, int32_t precision, const void* O,
+                                  const void* D, int64_t n, const DrcbGBuffer* out, void* stream) {
+  NEED(scene);
+  NEED(out);
+  if (check_precision(precision)) return DRCB_ECONFIG;
+  if (precision == 64)
+    return launch_primary_chain<double>(scene->dev, (const double*)O, (const double*)D, n, *out,
+                                        S_(stream));
+  return launch_primary_chain<float>(scene->dev, (const float*)O, (const float*)D, n, *out,
+                                     S_(stream));
+}
+
+extern "C" int drcb_li_direct(const DrcbScene* scene, const DrcbRenderCfg* cfg, const void* O,
+                              const void* D, const uint64_t* pix, const uint64_t* smp, int64_t n,
+                              int32_t include_background, void* L, int64_t* nonfinite,
+                              void* stream) {
+  NEED(scene);
+  if (check_cfg(cfg)) return DRCB_ECONFIG;
+  if (cfg->precision == 64)
+    return launch_li_direct<double>(scene->dev, *cfg, (const double*)O, (const double*)D, pix, smp,
+                                    n, include_background, (double*)L, nonfinite, S_(stream));
+  return launch_li_direct<float>(scene->dev, *cfg, (const float*)O, (const float*)D, pix, smp, n,
+                                 include_background, (float*)L, nonfinite, S_(stream));
+}
+
+extern "C" int drcb_trace_radiance(const DrcbScene* scene, const DrcbRenderCfg* cfg,
+                                   const void* O, const void* D, const uint64_t* pix,
+                                   const uint64_t* smp, int64_t n, int32_t max_depth,
+                                   int32_t skip_first_emission, int32_t rr_start, void* L,
+                                   int64_t* nonfinite, void* stream) {
+  NEED(scene);
+  if (check_cfg(cfg)) return DRCB_ECONFIG;
+  if (max_depth < 1) return fail(DRCB_ECONTRACT, "max_depth must be >= 1");
+  if (cfg->precision == 64)
+    return launch_trace_radiance<double>(scene->dev, *cfg, (const double*)O, (const double*)D, pix,
+                                         smp, n, max_depth, skip_first_emission, rr_start,
+                                         (double*)L, nonfinite, S_(stream));
+  return launch_trace_radiance<float>(scene->dev, *cfg, (const float*)O, (const float*)D, pix, smp,
+                                      n, max_depth, skip_first_emission, rr_start, (float*)L,
+                                      nonfinite, S_(stream));
+}
+
+extern "C" int drcb_gbuffer_direct(const DrcbScene* scene, const DrcbCamera* cam,
+                                   const DrcbRenderCfg* cfg, const DrcbGBuffer* gb, void* direct,
+                                   int64_t* nonfinite, void* stream) {
+  NEED(scene);
+  NEED(cam);
+  NEED(gb);
+  if (check_cfg(cfg)) return DRCB_ECONFIG;
+  DevCamera C = make_camera(*cam);
+  if (cfg->precision == 64)
+    return launch_gbuffer_direct<double>(scene->dev, C, *cfg, cfg->tile, *gb, (double*)direct,
+                                         nonfinite, S_(stream));
+  return launch_gbuffer_direct<float>(scene->dev, C, *cfg, cfg->tile, *gb, (float*)direct,
+                                      nonfinite, S_(stream));
+}
+
+extern "C" int drcb_render_stacks(const DrcbScene* scene, const DrcbRenderCfg* cfg,
+                                  const void* pos, const void* nrm, const uint64_t* keys,
+                                  int64_t n, float* stacks, void* s_r, void* s_d, void* frames,
+                                  int64_t* nonfinite, void* stream) {
+  NEED(scene);
+  if (check_cfg(cfg)) return DRCB_ECONFIG;
+  if (cfg->precision == 64)
+    return launch_render_stacks<double>(scene->dev, *cfg, (const double*)pos, (const double*)nrm,
+                                        keys, nullptr, n, stacks, (double*)s_r, (double*)s_d,
+                                        (double*)frames, nonfinite, S_(stream));
+  return launch_render_stacks<float>(scene->dev, *cfg, (const float*)pos, (const float*)nrm, keys,
+                                     nullptr, n, stacks, (float*)s_r, (float*)s_d, (float*)frames,
+                                     nonfinite, S_(stream));
+}
+
+extern "C" int drcb_shade(const DrcbScene* scene, const DrcbRenderCfg* cfg, const float* pred,
+                          const void* s_r, const void* frames, const void* wo, const int32_t* mat,
+                          const uint64_t* keys, int64_t n, void* L, void* stream) {
+  NEED(scene);
+  if (check_cfg(cfg)) return DRCB_ECONFIG;
+  if (cfg->precision == 64)
+    return launch_shade<double>(scene->dev, *cfg, pred, (const double*)s_r, (const double*)frames,
+                                (const double*)wo, mat, keys, nullptr, n, (double*)L, S_(stream));
+  return launch_shade<float>(scene->dev, *cfg, pred, (const float*)s_r, (const float*)frames,
+                             (const float*)wo, mat, keys, nullptr, n, (float*)L, S_(stream));
+}
+
+extern "C" int drcb_interp_composite(const DrcbScene* scene, int32_t precision, int32_t width,
+                                     int32_t height, const DrcbGBuffer* gb, const int32_t* e_px,
+                                     const int32_t* e_py, const void* e_normal, const void* e_rad,
+                                     int64_t m, int32_t r, const void* direct, void* image,
+                                     void* stream) {
+  NEED(scene);
+  NEED(gb);
+  if (check_precision(precision)) return DRCB_ECONFIG;
+  if (precision == 64)
+    return launch_interp_composite<double>(scene->dev, width, height, *gb, e_px, e_py,
+                                           (const double*)e_normal, (const double*)e_rad, m, r,
+                                           (const double*)direct, (double*)image, S_(stream));
+  return launch_interp_composite<float>(scene->dev, width, height, *gb, e_px, e_py,
+                                        (const float*)e_normal, (const float*)e_rad, m, r,
+                                        (const float*)direct, (float*)image, S_(stream));
+}
+
+extern "C" int drcb_render_drc(const DrcbScene* scene, const DrcbNet* net, const DrcbCamera* cam,
+                               const DrcbRenderCfg* cfg, const int32_t* px_host,
+                               const int32_t* py_host, const uint64_t* keys_host,
+                               int64_t n_points, int32_t r_final, int32_t net_mode, void* image,
+                               int64_t* telemetry_host, void* stream) {
+  NEED(scene);
+  NEED(cam);
+  NEED(image);
+  if (check_cfg(cfg)) return DRCB_ECONFIG;
+  if (n_points > 0 && (!net || !px_host || !py_host || !keys_host))
+    return fail(DRCB_ECONTRACT, "drcb_render_drc: points given without network/arrays");
+  if (n_points > 0 && net->impl.k < 4) return fail(DRCB_ECONFIG, "bad network");
+  for (int64_t i = 0; i < n_points; ++i)
+    if (px_host[i] < 0 || px_host[i] >= cam->width || py_host[i] < 0 || py_host[i] >= cam->height)
+      return fail(DRCB_ECONTRACT, "cache point outside the image");
+  DrcbNet* mnet = const_cast<DrcbNet*>(net);
+  if (cfg->precision == 64)
+    return render_frame<double>(scene, mnet, cam, cfg, px_host, py_host, keys_host, n_points,
+                                r_final, net_mode, (double*)image, telemetry_host, S_(stream));
+  return render_frame<float>(scene, mnet, cam, cfg, px_host, py_host, keys_host, n_points, r_final,
+                             net_mode, (float*)image, telemetry_host, S_(stream));
+}
+
+extern "C" int drcb_net_forward(const DrcbNet* net, const float* x, float* y, int64_t n,
+                                int32_t mode, void* stream) {
+  NEED(net);
+  if (n <= 0) return 0;
+  NEED(x);
+  NEED(y);
+  if (mode == DRCB_NET_FP32) return forward_f32_chunked(net->impl, x, y, n, S_(stream));
+  if (mode == DRCB_NET_TF32 || mode == DRCB_NET_BF16)
+    return forward_tc(const_cast<DrcbNet*>(net)->impl, x, y, n, mode, S_(stream));
+  return fail(DRCB_ECONFIG, "unknown network mode");
+}

@@ -1,0 +1,75 @@
+// drcb_internal.h — host-side handle types shared by the C-ABI translation
+// units. Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/drcb.h"
+#include "drcb_scene.cuh"
+
+namespace drcb {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+#define DRCB_CUDA(call)                                      \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) return ::drcb::cuda_fail(_e, #call); \
+  } while (0)
+
+struct SceneStats {
+  int64_t n_prims = 0, n_nodes = 0, n_leaves = 0, max_depth = 0, n_lights = 0, bytes = 0;
+};
+
+}  // namespace drcb
+
+struct DrcbScene {
+  drcb::DevScene dev;          // device pointers (owned)
+  std::vector<void*> allocs;   // device allocations to free
+  drcb::SceneStats stats;
+  int device = 0;
+};
+
+namespace drcb {
+DevCamera make_camera(const DrcbCamera& c);
+
+// stage launchers (drcb_render.cu)
+template <typename R>
+int launch_intersect(const DevScene& S, const R* O, const R* D, int64_t n, const R* tmin,
+                     const R* tmax, int record, uint8_t* hit, R* t, int64_t* prim, int32_t* mat,
+                     R* pos, R* nrm, cudaStream_t st);
+template <typename R>
+int launch_primary_chain(const DevScene& S, const R* O, const R* D, int64_t n,
+                         const DrcbGBuffer& gb, cudaStream_t st);
+template <typename R>
+int launch_li_direct(const DevScene& S, const DrcbRenderCfg& cfg, const R* O, const R* D,
+                     const uint64_t* pix, const uint64_t* smp, int64_t n, int include_bg, R* L,
+                     int64_t* nonfinite, cudaStream_t st);
+template <typename R>
+int launch_trace_radiance(const DevScene& S, const DrcbRenderCfg& cfg, const R* O, const R* D,
+                          const uint64_t* pix, const uint64_t* smp, int64_t n, int max_depth,
+                          int skip_first, int rr_start, R* L, int64_t* nonfinite,
+                          cudaStream_t st);
+template <typename R>
+int launch_gbuffer_direct(const DevScene& S, const DevCamera& C, const DrcbRenderCfg& cfg,
+                          int tile, const DrcbGBuffer& gb, R* direct, int64_t* nonfinite,
+                          cudaStream_t st);
+// map rays + normalisation; live (n,) optional mask (nullptr = all live)
+template <typename R>
+int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* pos, const R* nrm,
+                         const uint64_t* keys, const uint8_t* live, int64_t n, float* stacks,
+                         R* s_r, R* s_d, R* frames, int64_t* nonfinite, cudaStream_t st);
+template <typename R>
+int launch_shade(const DevScene& S, const DrcbRenderCfg& cfg, const float* pred, const R* s_r,
+                 const R* frames, const R* wo, const int32_t* mat, const uint64_t* keys,
+                 const uint8_t* live, int64_t n, R* L, cudaStream_t st);
+template <typename R>
+int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& gb,
+                            const int32_t* e_px, const int32_t* e_py, const R* e_n,
+                            const R* e_rad, int64_t m, int r, const R* direct, R* image,
+                            cudaStream_t st);
+}  // namespace drcb

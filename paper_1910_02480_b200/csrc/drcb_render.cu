@@ -1,0 +1,708 @@
+// drcb_render.cu — ray/path kernels of one DRC frame, instantiated for fp64
+// (parity) and fp32 (fast). Compiled with -fmad=false (see Makefile).
+//
+//   k_intersect        intersect_batch / occluded_batch  (geometry.py:217-329)
+//   k_primary_chain    primary_chain_batch               (integrators.py:427-518)
+//   k_li_direct        li_direct_batch                   (integrators.py:305-424)
+//   k_trace            trace_radiance_batch              (integrators.py:175-302)
+//   k_gbuffer_direct   DrcState geo + direct pass, fused (cache.py:157-176, 393-423)
+//   k_map_rays         render_input_stacks_batch rays    (hemimap.py:229-262)
+//   k_stack_normalize  per-map s_r / s_d + fp32 stack    (hemimap.py:264-281)
+//   k_shade            build_map_distribution+shade_indirect (hemimap.py:156-197,
+//                      integrators.py:564-614)
+//   k_interp           _interpolate_layer + composite    (cache.py:283-345, 463)
+#include <cub/cub.cuh>
+
+#include "drcb_internal.h"
+#include "drcb_trace.cuh"
+
+namespace drcb {
+
+namespace {
+
+constexpr int TPB = 128;
+
+inline int nblocks(int64_t n, int tpb = TPB) { return int((n + tpb - 1) / tpb); }
+
+template <typename R>
+__global__ void k_intersect(DevScene S, const R* __restrict__ O, const R* __restrict__ D,
+                            int64_t n, const R* tmin, const R* tmax, int record, uint8_t* hit,
+                            R* t, int64_t* prim, int32_t* mat, R* pos, R* nrm) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  V3<R> o = ldr3(O + 3 * i), d = ldr3(D + 3 * i);
+  R lo = tmin ? tmin[i] : R(T_EPS);
+  R hi = tmax ? tmax[i] : R(INFINITY);
+  if (!record) {
+    HitRec<R> h = traverse<R, false>(S, o, d, lo, hi);
+    hit[i] = h.prim >= 0;
+    if (t) t[i] = h.prim >= 0 ? h.t : R(INFINITY);
+    if (prim) prim[i] = h.prim;
+    return;
+  }
+  SurfHit<R> h = intersect(S, o, d, lo, hi);
+  hit[i] = h.hit;
+  if (t) t[i] = h.t;
+  if (prim) prim[i] = h.prim;
+  if (mat) mat[i] = h.mat;
+  if (pos) st3(pos + 3 * i, h.pos);
+  if (nrm) st3(nrm + 3 * i, h.normal);
+}
+
+template <typename R>
+__device__ __forceinline__ void store_chain(const DrcbGBuffer& gb, int64_t i, const ChainOut<R>& c) {
+  gb.found[i] = c.found;
+  gb.escaped[i] = c.escaped;
+  st3(static_cast<R*>(gb.position) + 3 * i, c.pos);
+  st3(static_cast<R*>(gb.normal) + 3 * i, c.normal);
+  st3(static_cast<R*>(gb.throughput) + 3 * i, c.thr);
+  st3(static_cast<R*>(gb.direction) + 3 * i, c.dir);
+  static_cast<R*>(gb.t_total)[i] = c.t_total;
+  gb.mat[i] = c.mat;
+}
+
+template <typename R>
+__global__ void k_primary_chain(DevScene S, const R* __restrict__ O, const R* __restrict__ D,
+                                int64_t n, DrcbGBuffer gb) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  store_chain(gb, i, primary_chain(S, ldr3(O + 3 * i), ldr3(D + 3 * i)));
+}
+
+__device__ __forceinline__ void add_nonfinite(int64_t* ctr, int c) {
+  if (ctr && c) atomicAdd((unsigned long long*)ctr, (unsigned long long)c);
+}
+
+template <typename R>
+__global__ void k_li_direct(DevScene S, DrcbRenderCfg cfg, const R* __restrict__ O,
+                            const R* __restrict__ D, const uint64_t* pix, const uint64_t* smp,
+                            int64_t n, int include_bg, R* L, int64_t* nonfinite) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int nf = 0;
+  if (i < n) {
+    PathRng rng;
+    rng.init(cfg.seed, pix[i], smp[i], cfg.sampler_kind, uint32_t(cfg.direct_spp > 1 ? cfg.direct_spp : 1));
+    V3<R> l = direct_path(S, ldr3(O + 3 * i), ldr3(D + 3 * i), rng, include_bg != 0, nf);
+    st3(L + 3 * i, l);
+  }
+  if (nonfinite) add_nonfinite(nonfinite, nf);
+}
+
+template <typename R>
+__global__ void k_trace(DevScene S, DrcbRenderCfg cfg, const R* __restrict__ O,
+                        const R* __restrict__ D, const uint64_t* pix, const uint64_t* smp,
+                        int64_t n, int max_depth, int skip_first, int rr_start, R* L,
+                        int64_t* nonfinite) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int nf = 0;
+  if (i < n) {
+    PathRng rng;
+    // trace_radiance_batch is always called with a spp=1 sampler in the
+    // reference pipeline; honour the configured kind/spp for direct calls.
+    rng.init(cfg.seed, pix[i], smp[i], cfg.sampler_kind, uint32_t(cfg.direct_spp > 1 ? cfg.direct_spp : 1));
+    V3<R> l = trace_path<R>(S, ldr3(O + 3 * i), ldr3(D + 3 * i), rng, max_depth, skip_first != 0,
+                            rr_start, nullptr, nf);
+    st3(L + 3 * i, l);
+  }
+  if (nonfinite) add_nonfinite(nonfinite, nf);
+}
+
+// One thread per pixel: the unjittered centre chain (G-buffer) and the
+// direct_spp jittered li_direct samples, averaged (cache.py:157-176, 393-423).
+template <typename R>
+__global__ void __launch_bounds__(TPB) k_gbuffer_direct(DevScene S, DevCamera C, DrcbRenderCfg cfg,
+                                                         int tile, DrcbGBuffer gb, R* direct,
+                                                         int64_t* nonfinite) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t npx = int64_t(C.W) * C.H;
+  int nf = 0;
+  if (i < npx) {
+    int x = int(i % C.W), y = int(i / C.W);
+    V3<R> cam = ld3<R>(C.pos);
+    V3<R> dc = camera_dir<R>(C, R(x) + R(0.5), R(y) + R(0.5));
+    store_chain(gb, i, primary_chain(S, cam, dc));
+    // direct pass; samples are summed in the reference's per-tile chunks
+    int spp = cfg.direct_spp;
+    int tx0 = (x / tile) * tile, ty0 = (y / tile) * tile;
+    int tw = min(tile, C.W - tx0), th = min(tile, C.H - ty0);
+    int chunk = max(1, 16384 / (tw * th));
+    PathRng rng;
+    V3<R> acc = {R(0), R(0), R(0)};
+    for (int s0 = 0; s0 < spp; s0 += chunk) {
+      int ns = min(chunk, spp - s0);
+      V3<R> part;
+      for (int s = s0; s < s0 + ns; ++s) {
+        rng.init(cfg.seed, uint64_t(i), uint64_t(s), cfg.sampler_kind, uint32_t(spp > 1 ? spp : 1));
+        R jx = to_unit<R>(rng.sample(0)), jy = to_unit<R>(rng.sample(1));
+        V3<R> d = camera_dir<R>(C, R(x) + jx, R(y) + jy);
+        V3<R> l = direct_path(S, cam, d, rng, cfg.include_background != 0, nf);
+        part = (s == s0) ? l : part + l;
+      }
+      acc = acc + part;
+    }
+    R inv = R(spp);
+    st3(direct + 3 * i, mk<R>(acc.x / inv, acc.y / inv, acc.z / inv));
+  }
+  if (nonfinite) add_nonfinite(nonfinite, nf);
+}
+
+// One thread per texel path of one cache point (hemimap.py:236-262). The
+// reference casts the first map ray twice (line 250 and segment 0 of
+// trace_radiance_batch); it is cast once here and reused.
+template <typename R>
+__global__ void __launch_bounds__(TPB) k_map_rays(DevScene S, DrcbRenderCfg cfg,
+                                                   const R* __restrict__ pos,
+                                                   const R* __restrict__ nrm,
+                                                   const uint64_t* __restrict__ keys,
+                                                   const uint8_t* __restrict__ live, int64_t n,
+                                                   R* rad, R* dist, R* nloc, R* frames,
+                                                   int64_t* nonfinite) {
+  int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t p = g / MAP_TEXELS;
+  int tex = int(g % MAP_TEXELS);
+  int nf = 0;
+  if (p < n && (!live || live[p])) {
+    V3<R> hp = ldr3(pos + 3 * p), hn = ldr3(nrm + 3 * p);
+    Frame<R> fr = frame_scalar(S, hn);
+    if (tex == 0) {
+      R* f = frames + 9 * p;
+      st3(f, fr.t);
+      st3(f + 3, fr.b);
+      st3(f + 6, fr.n);
+    }
+    int u = tex % MAP_RES, v = tex / MAP_RES;
+    V3<R> dir = fr.to_world(texel_local<R>(u, v));
+    V3<R> o = hp + R(T_EPS) * hn;
+    SurfHit<R> first = intersect(S, o, dir);
+    R d = first.hit ? first.t : R(0);
+    bool facing = dot(first.normal, dir) > R(0);
+    V3<R> nf3 = facing ? -first.normal : first.normal;
+    V3<R> nl = first.hit ? fr.to_local(nf3) : mk<R>(R(0), R(0), R(0));
+    PathRng rng;
+    rng.init(cfg.seed, keys[p], uint64_t(tex), cfg.sampler_kind, 1u);
+    V3<R> L = trace_path<R>(S, o, dir, rng, cfg.max_path_depth, true, cfg.rr_start, &first, nf);
+    int64_t q = p * MAP_TEXELS + tex;
+    st3(rad + 3 * q, L);
+    dist[q] = d;
+    st3(nloc + 3 * q, nl);
+  }
+  if (nonfinite) add_nonfinite(nonfinite, nf);
+}
+
+// numpy pairwise summation of 1024 contiguous values (8-accumulator blocks of
+// 128, binary tree above), replicated bit for bit. `a` is in shared memory;
+// must be called by all threads of the block; result valid in all threads.
+template <typename R>
+__device__ R pairwise1024(const R* a, R* scratch /* >= 64 */) {
+  int t = threadIdx.x;
+  if (t < 64) {
+    int blk = t >> 3, j = t & 7;
+    const R* b = a + 128 * blk;
+    R r = b[j];
+    for (int i = 8; i < 128; i += 8) r = r + b[i + j];
+    scratch[t] = r;
+  }
+  __syncthreads();
+  R res;
+  {
+    R B[8];
+    for (int blk = 0; blk < 8; ++blk) {
+      const R* r = scratch + 8 * blk;
+      B[blk] = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    }
+    res = ((B[0] + B[1]) + (B[2] + B[3])) + ((B[4] + B[5]) + (B[6] + B[7]));
+  }
+  __syncthreads();
+  return res;
+}
+
+// numpy pairwise sum of 32 contiguous values (n <= 128 branch)
+template <typename R>
+__device__ __forceinline__ R pairwise32(const R* a) {
+  R r[8];
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  for (int i = 8; i < 32; i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = r[j] + a[i + j];
+  return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+}
+
+constexpr double LUMA_R = 0.2126, LUMA_G = 0.7152, LUMA_B = 0.0722;  // hemimap.py:26
+
+// One block (256 threads) per cache point: s_r = mean luminance + 1e-3,
+// s_d = max distance (or 1), fp32 NCHW stack [rad/s_r, n_local, d/s_d].
+template <typename R>
+__global__ void __launch_bounds__(256) k_stack_normalize(const R* __restrict__ rad,
+                                                         const R* __restrict__ dist,
+                                                         const R* __restrict__ nloc,
+                                                         const uint8_t* __restrict__ live,
+                                                         int64_t n, float* stacks, R* s_r,
+                                                         R* s_d) {
+  __shared__ R lum[MAP_TEXELS];
+  __shared__ R scratch[64];
+  __shared__ R dmax[8];
+  int64_t p = blockIdx.x;
+  if (p >= n) return;
+  float* out = stacks + p * 7 * MAP_TEXELS;
+  if (live && !live[p]) {
+    for (int t = threadIdx.x; t < 7 * MAP_TEXELS; t += blockDim.x) out[t] = 0.f;
+    if (threadIdx.x == 0) { s_r[p] = R(1); s_d[p] = R(1); }
+    return;
+  }
+  const R* rp = rad + p * MAP_TEXELS * 3;
+  const R* dp = dist + p * MAP_TEXELS;
+  R dm = R(0);
+  for (int t = threadIdx.x; t < MAP_TEXELS; t += blockDim.x) {
+    lum[t] = (rp[3 * t] * R(LUMA_R) + rp[3 * t + 1] * R(LUMA_G)) + rp[3 * t + 2] * R(LUMA_B);
+    dm = fmax(dm, dp[t]);
+  }
+  for (int off = 16; off > 0; off >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, off));
+  if ((threadIdx.x & 31) == 0) dmax[threadIdx.x >> 5] = dm;
+  __syncthreads();
+  R sum = pairwise1024(lum, scratch);
+  R sr = sum / R(MAP_TEXELS) + R(1e-3);
+  R mx = dmax[0];
+  for (int w = 1; w < 8; ++w) mx = fmax(mx, dmax[w]);
+  R sd = mx > R(0) ? mx : R(1);
+  const R* np_ = nloc + p * MAP_TEXELS * 3;
+  for (int t = threadIdx.x; t < MAP_TEXELS; t += blockDim.x) {
+    for (int c = 0; c < 3; ++c) out[c * MAP_TEXELS + t] = float(rp[3 * t + c] / sr);
+    for (int c = 0; c < 3; ++c) out[(3 + c) * MAP_TEXELS + t] = float(np_[3 * t + c]);
+    out[6 * MAP_TEXELS + t] = float(dp[t] / sd);
+  }
+  if (threadIdx.x == 0) {
+    s_r[p] = sr;
+    s_d[p] = sd;
+  }
+}
+
+// numpy remainder (floored modulo) for y > 0
+template <typename R>
+__device__ __forceinline__ R py_mod(R x, R y) {
+  R m = fmod(x, y);
+  if (m != R(0)) {
+    if ((m < R(0)) != (y < R(0))) m += y;
+  } else {
+    m = copysign(R(0), y);
+  }
+  return m;
+}
+
+// _texels_from_local (hemimap.py:106-114)
+template <typename R>
+__device__ __forceinline__ bool texel_of(V3<R> l, int& u, int& v) {
+  R z = fmin(fmax(l.z, R(-1)), R(1));
+  bool valid = z >= R(0);
+  R theta = acos(z);
+  R phi = py_mod(atan2(l.y, l.x), R(2.0 * PI));
+  long long uu = (long long)(phi / R(2.0 * PI) * R(MAP_RES));
+  long long vv = (long long)(theta / R(PI / 2.0) * R(MAP_RES));
+  u = int(uu < MAP_RES - 1 ? uu : MAP_RES - 1);
+  v = int(vv < MAP_RES - 1 ? vv : MAP_RES - 1);
+  if (!valid) { u = 0; v = 0; }
+  return valid;
+}
+
+template <typename R>
+__device__ __forceinline__ R texel_sin_theta(int v) {
+  return sin(R(PI / 2.0) * (R(v) + R(0.5)) / R(MAP_RES));
+}
+
+// One block (256 threads) per cache point: the map's 2D distribution and the
+// MIS shading estimate (integrators.py:564-614).
+template <typename R>
+__global__ void __launch_bounds__(256) k_shade(DevScene S, DrcbRenderCfg cfg,
+                                               const float* __restrict__ pred,
+                                               const R* __restrict__ s_r,
+                                               const R* __restrict__ frames,
+                                               const R* __restrict__ wo,
+                                               const int32_t* __restrict__ mats,
+                                               const uint64_t* __restrict__ keys,
+                                               const uint8_t* __restrict__ live, int64_t n,
+                                               R* Lout) {
+  __shared__ R prob[MAP_TEXELS];
+  __shared__ R colcdf[MAP_TEXELS];
+  __shared__ R rowcdf[MAP_RES];
+  __shared__ R rows[MAP_RES];
+  __shared__ R scratch[64];
+  __shared__ R contrib[64][3];
+  int64_t p = blockIdx.x;
+  if (p >= n) return;
+  if (live && !live[p]) {
+    if (threadIdx.x < 3) Lout[3 * p + threadIdx.x] = R(0);
+    return;
+  }
+  const float* pd = pred + p * 3 * MAP_TEXELS;  // (3,32,32)
+  const R scale = s_r[p];
+  // weights w = lum * sin(theta_v) + 1e-8 (build_map_distribution)
+  for (int t = threadIdx.x; t < MAP_TEXELS; t += blockDim.x) {
+    R r = R(pd[t]) * scale, g = R(pd[MAP_TEXELS + t]) * scale, b = R(pd[2 * MAP_TEXELS + t]) * scale;
+    R lum = (r * R(LUMA_R) + g * R(LUMA_G)) + b * R(LUMA_B);
+    prob[t] = lum * texel_sin_theta<R>(t / MAP_RES) + R(1e-8);
+  }
+  __syncthreads();
+  R wsum = pairwise1024(prob, scratch);
+  for (int t = threadIdx.x; t < MAP_TEXELS; t += blockDim.x) prob[t] = prob[t] / wsum;
+  __syncthreads();
+  if (threadIdx.x < MAP_RES) rows[threadIdx.x] = pairwise32(prob + MAP_RES * threadIdx.x);
+  __syncthreads();
+  if (threadIdx.x < MAP_RES) {
+    int v = threadIdx.x;
+    R acc = R(0);
+    for (int u = 0; u < MAP_RES; ++u) {
+      R c = prob[v * MAP_RES + u] / rows[v];
+      acc = (u == 0) ? c : acc + c;
+      colcdf[v * MAP_RES + u] = acc;
+    }
+    colcdf[v * MAP_RES + MAP_RES - 1] = R(1);
+  }
+  if (threadIdx.x == 32) {
+    R acc = R(0);
+    for (int v = 0; v < MAP_RES; ++v) {
+      acc = (v == 0) ? rows[0] : acc + rows[v];
+      rowcdf[v] = acc;
+    }
+    rowcdf[MAP_RES - 1] = R(1);
+  }
+  __syncthreads();
+  const R* F = frames + 9 * p;
+  Frame<R> fr{ldr3(F), ldr3(F + 3), ldr3(F + 6)};
+  V3<R> wo_local = fr.to_local(ldr3(wo + 3 * p));
+  int mat = mats[p];
+  const int n_map = cfg.mis_samples / 2;
+  const int n_bsdf = cfg.mis_samples - n_map;
+  const R omega0 = (R(2.0 * PI) / R(MAP_RES)) * (R(PI) / (R(2) * R(MAP_RES)));
+  int i = threadIdx.x;
+  PathRng rng;
+  V3<R> c = {R(0), R(0), R(0)};
+  if (i < n_map && i < 64) {
+    rng.init(cfg.seed, keys[p], uint64_t(i), cfg.sampler_kind, 1u);
+    R u1 = to_unit<R>(rng.sample(SHADE_DIM_BASE + 0));
+    R u2 = to_unit<R>(rng.sample(SHADE_DIM_BASE + 1));
+    int v = 0;
+    while (v < MAP_RES && rowcdf[v] <= u1) ++v;
+    v = min(v, MAP_RES - 1);
+    int u = 0;
+    for (int k = 0; k < MAP_RES; ++k) u += (colcdf[v * MAP_RES + k] <= u2);
+    u = min(u, MAP_RES - 1);
+    R pr = prob[v * MAP_RES + u];
+    V3<R> dir = fr.to_world(texel_local<R>(u, v));
+    R pdf = pr / (omega0 * texel_sin_theta<R>(v));
+    V3<R> radv = {R(pd[v * MAP_RES + u]) * scale, R(pd[MAP_TEXELS + v * MAP_RES + u]) * scale,
+                  R(pd[2 * MAP_TEXELS + v * MAP_RES + u]) * scale};
+    V3<R> li = fr.to_local(dir);
+    V3<R> f;
+    R pdf_b;
+    bsdf_eval(S, mat, wo_local, li, f, pdf_b);
+    R cos_i = fmax(li.z, R(0));
+    R w = power_heuristic(pdf, pdf_b);
+    R k = (w * cos_i) / pdf;
+    c = (f * radv) * mk<R>(k, k, k);
+  } else if (i >= 32 && i - 32 < n_bsdf && i - 32 < 32) {
+    int j = i - 32;
+    rng.init(cfg.seed, keys[p], uint64_t(j), cfg.sampler_kind, 1u);
+    R u1 = to_unit<R>(rng.sample(SHADE_DIM_BASE + 2));
+    R u2 = to_unit<R>(rng.sample(SHADE_DIM_BASE + 3));
+    BsdfSample<R> bs = bsdf_sample(S, mat, wo_local, u1, u2, true);
+    int u, v;
+    bool valid = texel_of(bs.li, u, v);
+    V3<R> radv = {R(0), R(0), R(0)};
+    R pdf_m = R(0);
+    if (valid) {
+      int q = v * MAP_RES + u;
+      radv = {R(pd[q]) * scale, R(pd[MAP_TEXELS + q]) * scale, R(pd[2 * MAP_TEXELS + q]) * scale};
+      pdf_m = prob[q] / (omega0 * texel_sin_theta<R>(v));
+    }
+    R cos_i = fmax(bs.li.z, R(0));
+    R w = power_heuristic(bs.pdf, pdf_m);
+    R k = (w * cos_i) / bs.pdf;
+    c = (bs.value * radv) * mk<R>(k, k, k);
+  }
+  if (i < 64) {
+    contrib[i][0] = c.x;
+    contrib[i][1] = c.y;
+    contrib[i][2] = c.z;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    V3<R> sm = {contrib[0][0], contrib[0][1], contrib[0][2]};
+    for (int k = 1; k < n_map; ++k) sm = sm + mk<R>(contrib[k][0], contrib[k][1], contrib[k][2]);
+    V3<R> sb = {contrib[32][0], contrib[32][1], contrib[32][2]};
+    for (int k = 1; k < n_bsdf; ++k) sb = sb + mk<R>(contrib[32 + k][0], contrib[32 + k][1], contrib[32 + k][2]);
+    V3<R> total = divs(sm, R(n_map));
+    total = total + divs(sb, R(n_bsdf));
+    if (!all_finite(total)) total = {R(0), R(0), R(0)};
+    st3(Lout + 3 * p, total);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// interpolation: entries bucketed on a screen grid (replaces cKDTree,
+// cache.py:205-208, 305-307); exact predicates of the reference:
+//   d1 = sqrt(min dx^2+dy^2), r_eff = max(r, 1.5 d1),
+//   gather dx^2+dy^2 <= (2 r_eff)^2, w = w_p w_n + w_p + 1e-4.
+constexpr int BUCKET = 16;
+
+__global__ void k_bucket_count(const int32_t* px, const int32_t* py, int64_t m, int nbx,
+                               int* counts) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  atomicAdd(&counts[(py[i] / BUCKET) * nbx + px[i] / BUCKET], 1);
+}
+
+__global__ void k_bucket_fill(const int32_t* px, const int32_t* py, int64_t m, int nbx,
+                              const int* offsets, int* cursor, int* items) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int b = (py[i] / BUCKET) * nbx + px[i] / BUCKET;
+  int slot = atomicAdd(&cursor[b], 1);
+  items[offsets[b] + slot] = int(i);
+}
+
+// ascending entry order inside each bucket (determinism)
+__global__ void k_bucket_sort(const int* offsets, int nb, int* items) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  int s = offsets[b], e = offsets[b + 1];
+  for (int i = s + 1; i < e; ++i) {
+    int v = items[i];
+    int j = i - 1;
+    while (j >= s && items[j] > v) {
+      items[j + 1] = items[j];
+      --j;
+    }
+    items[j + 1] = v;
+  }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(TPB) k_interp(DevScene S, int W, int H, DrcbGBuffer gb,
+                                                 const int32_t* __restrict__ epx,
+                                                 const int32_t* __restrict__ epy,
+                                                 const R* __restrict__ en,
+                                                 const R* __restrict__ erad, int64_t m, int r,
+                                                 int nbx, int nby, const int* __restrict__ off,
+                                                 const int* __restrict__ items,
+                                                 const R* __restrict__ direct, R* image) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(W) * H) return;
+  int x = int(i % W), y = int(i / W);
+  V3<R> layer = {R(0), R(0), R(0)};
+  V3<R> thr = ldr3(static_cast<const R*>(gb.throughput) + 3 * i);
+  if (gb.escaped[i] && S.has_env) layer = thr * ld3<R>(S.env);
+  if (gb.found[i] && m > 0) {
+    int bx = x / BUCKET, by = y / BUCKET;
+    // nearest entry by expanding Chebyshev rings of buckets
+    long long best = LLONG_MAX;
+    int maxring = max(nbx, nby);
+    for (int k = 0; k <= maxring; ++k) {
+      for (int yy = by - k; yy <= by + k; ++yy) {
+        if (yy < 0 || yy >= nby) continue;
+        for (int xx = bx - k; xx <= bx + k; ++xx) {
+          if (xx < 0 || xx >= nbx) continue;
+          if (max(abs(yy - by), abs(xx - bx)) != k) continue;
+          int b = yy * nbx + xx;
+          for (int q = off[b]; q < off[b + 1]; ++q) {
+            int e = items[q];
+            long long dx = epx[e] - x, dy = epy[e] - y;
+            long long d2 = dx * dx + dy * dy;
+            if (d2 < best) best = d2;
+          }
+        }
+      }
+      long long lim = (long long)k * BUCKET + 1;
+      if (best != LLONG_MAX && best <= lim * lim) break;
+    }
+    R d1 = sqrt(R(best));
+    R r_eff = fmax(R(r), R(1.5) * d1);
+    R rad = R(2) * r_eff;
+    R rad2 = rad * rad;
+    V3<R> npx = ldr3(static_cast<const R*>(gb.normal) + 3 * i);
+    int reach = int(ceil(double(rad))) + 1;
+    int bx0 = max(0, (x - reach) / BUCKET), bx1 = min(nbx - 1, (x + reach) / BUCKET);
+    int by0 = max(0, (y - reach) / BUCKET), by1 = min(nby - 1, (y + reach) / BUCKET);
+    V3<R> num = {R(0), R(0), R(0)};
+    R den = R(0);
+    for (int yy = by0; yy <= by1; ++yy)
+      for (int xx = bx0; xx <= bx1; ++xx) {
+        int b = yy * nbx + xx;
+        for (int q = off[b]; q < off[b + 1]; ++q) {
+          int e = items[q];
+          R dx = R(epx[e] - x), dy = R(epy[e] - y);
+          R d2 = dx * dx + dy * dy;
+          if (!(d2 <= rad2)) continue;
+          R dist = sqrt(d2);
+          R w_p = fmax(R(0), R(1) - dist / r_eff);
+          R w_n = fmax(R(0), dot(ldr3(en + 3 * e), npx));
+          R wgt = (w_p * w_n + w_p) + R(1e-4);
+          num = num + wgt * ldr3(erad + 3 * e);
+          den = den + wgt;
+        }
+      }
+    if (den > R(0)) layer = thr * divs(num, den);
+  }
+  V3<R> out = layer;
+  if (direct) out = ldr3(direct + 3 * i) + layer;
+  st3(image + 3 * i, out);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+
+#define LAUNCH_CHECK()                                                    \
+  do {                                                                    \
+    cudaError_t _e = cudaGetLastError();                                  \
+    if (_e != cudaSuccess) return cuda_fail(_e, __func__);                \
+  } while (0)
+
+template <typename R>
+int launch_intersect(const DevScene& S, const R* O, const R* D, int64_t n, const R* tmin,
+                     const R* tmax, int record, uint8_t* hit, R* t, int64_t* prim, int32_t* mat,
+                     R* pos, R* nrm, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_intersect<R><<<nblocks(n), TPB, 0, st>>>(S, O, D, n, tmin, tmax, record, hit, t, prim, mat,
+                                              pos, nrm);
+  LAUNCH_CHECK();
+  return 0;
+}
+
+template <typename R>
+int launch_primary_chain(const DevScene& S, const R* O, const R* D, int64_t n,
+                         const DrcbGBuffer& gb, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_primary_chain<R><<<nblocks(n), TPB, 0, st>>>(S, O, D, n, gb);
+  LAUNCH_CHECK();
+  return 0;
+}
+
+template <typename R>
+int launch_li_direct(const DevScene& S, const DrcbRenderCfg& cfg, const R* O, const R* D,
+                     const uint64_t* pix, const uint64_t* smp, int64_t n, int include_bg, R* L,
+                     int64_t* nonfinite, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_li_direct<R><<<nblocks(n), TPB, 0, st>>>(S, cfg, O, D, pix, smp, n, include_bg, L, nonfinite);
+  LAUNCH_CHECK();
+  return 0;
+}
+
+template <typename R>
+int launch_trace_radiance(const DevScene& S, const DrcbRenderCfg& cfg, const R* O, const R* D,
+                          const uint64_t* pix, const uint64_t* smp, int64_t n, int max_depth,
+                          int skip_first, int rr_start, R* L, int64_t* nonfinite,
+                          cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_trace<R><<<nblocks(n), TPB, 0, st>>>(S, cfg, O, D, pix, smp, n, max_depth, skip_first,
+                                          rr_start, L, nonfinite);
+  LAUNCH_CHECK();
+  return 0;
+}
+
+template <typename R>
+int launch_gbuffer_direct(const DevScene& S, const DevCamera& C, const DrcbRenderCfg& cfg,
+                          int tile, const DrcbGBuffer& gb, R* direct, int64_t* nonfinite,
+                          cudaStream_t st) {
+  int64_t n = int64_t(C.W) * C.H;
+  if (n <= 0) return 0;
+  k_gbuffer_direct<R><<<nblocks(n), TPB, 0, st>>>(S, C, cfg, tile, gb, direct, nonfinite);
+  LAUNCH_CHECK();
+  return 0;
+}
+
+template <typename R>
+int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* pos, const R* nrm,
+                         const uint64_t* keys, const uint8_t* live, int64_t n, float* stacks,
+                         R* s_r, R* s_d, R* frames, int64_t* nonfinite, cudaStream_t st) {
+  if (n <= 0) return 0;
+  size_t per = size_t(n) * MAP_TEXELS;
+  R* scratch = nullptr;
+  DRCB_CUDA(cudaMallocAsync((void**)&scratch, per * 7 * sizeof(R), st));
+  R* rad = scratch;
+  R* dist = scratch + 3 * per;
+  R* nloc = scratch + 4 * per;
+  k_map_rays<R><<<nblocks(int64_t(per)), TPB, 0, st>>>(S, cfg, pos, nrm, keys, live, n, rad, dist,
+                                                         nloc, frames, nonfinite);
+  LAUNCH_CHECK();
+  k_stack_normalize<R><<<int(n), 256, 0, st>>>(rad, dist, nloc, live, n, stacks, s_r, s_d);
+  LAUNCH_CHECK();
+  DRCB_CUDA(cudaFreeAsync(scratch, st));
+  return 0;
+}
+
+template <typename R>
+int launch_shade(const DevScene& S, const DrcbRenderCfg& cfg, const float* pred, const R* s_r,
+                 const R* frames, const R* wo, const int32_t* mat, const uint64_t* keys,
+                 const uint8_t* live, int64_t n, R* L, cudaStream_t st) {
+  if (n <= 0) return 0;
+  if (cfg.mis_samples < 2 || cfg.mis_samples > 64)
+    return fail(DRCB_ECONFIG, "mis_samples must be in [2, 64]");
+  k_shade<R><<<int(n), 256, 0, st>>>(S, cfg, pred, s_r, frames, wo, mat, keys, live, n, L);
+  LAUNCH_CHECK();
+  return 0;
+}
+
+template <typename R>
+int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& gb,
+                            const int32_t* e_px, const int32_t* e_py, const R* e_n,
+                            const R* e_rad, int64_t m, int r, const R* direct, R* image,
+                            cudaStream_t st) {
+  int nbx = (W + BUCKET - 1) / BUCKET, nby = (H + BUCKET - 1) / BUCKET;
+  int nb = nbx * nby;
+  int* buf = nullptr;
+  size_t mm = size_t(m > 0 ? m : 1);
+  DRCB_CUDA(cudaMallocAsync((void**)&buf, sizeof(int) * (3 * size_t(nb) + 2 + mm), st));
+  int* counts = buf;
+  int* offsets = buf + nb + 1;     // nb + 1
+  int* cursor = offsets + nb + 1;  // nb
+  int* items = cursor + nb;        // m
+  DRCB_CUDA(cudaMemsetAsync(buf, 0, sizeof(int) * (3 * size_t(nb) + 2), st));
+  if (m > 0) {
+    k_bucket_count<<<nblocks(m), TPB, 0, st>>>(e_px, e_py, m, nbx, counts);
+    LAUNCH_CHECK();
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, nb + 1, st);
+    void* tmp = nullptr;
+    DRCB_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, offsets, nb + 1, st);
+    DRCB_CUDA(cudaFreeAsync(tmp, st));
+    k_bucket_fill<<<nblocks(m), TPB, 0, st>>>(e_px, e_py, m, nbx, offsets, cursor, items);
+    LAUNCH_CHECK();
+    k_bucket_sort<<<nblocks(nb), TPB, 0, st>>>(offsets, nb, items);
+    LAUNCH_CHECK();
+  }
+  k_interp<R><<<nblocks(int64_t(W) * H), TPB, 0, st>>>(S, W, H, gb, e_px, e_py, e_n, e_rad, m, r,
+                                                       nbx, nby, offsets, items, direct, image);
+  LAUNCH_CHECK();
+  DRCB_CUDA(cudaFreeAsync(buf, st));
+  return 0;
+}
+
+#define INST(R)                                                                                  \
+  template int launch_intersect<R>(const DevScene&, const R*, const R*, int64_t, const R*,      \
+                                   const R*, int, uint8_t*, R*, int64_t*, int32_t*, R*, R*,     \
+                                   cudaStream_t);                                                \
+  template int launch_primary_chain<R>(const DevScene&, const R*, const R*, int64_t,            \
+                                       const DrcbGBuffer&, cudaStream_t);                        \
+  template int launch_li_direct<R>(const DevScene&, const DrcbRenderCfg&, const R*, const R*,   \
+                                   const uint64_t*, const uint64_t*, int64_t, int, R*, int64_t*, \
+                                   cudaStream_t);                                                \
+  template int launch_trace_radiance<R>(const DevScene&, const DrcbRenderCfg&, const R*,        \
+                                        const R*, const uint64_t*, const uint64_t*, int64_t,    \
+                                        int, int, int, R*, int64_t*, cudaStream_t);              \
+  template int launch_gbuffer_direct<R>(const DevScene&, const DevCamera&,                      \
+                                        const DrcbRenderCfg&, int, const DrcbGBuffer&, R*,      \
+                                        int64_t*, cudaStream_t);                                 \
+  template int launch_render_stacks<R>(const DevScene&, const DrcbRenderCfg&, const R*,         \
+                                       const R*, const uint64_t*, const uint8_t*, int64_t,      \
+                                       float*, R*, R*, R*, int64_t*, cudaStream_t);              \
+  template int launch_shade<R>(const DevScene&, const DrcbRenderCfg&, const float*, const R*,   \
+                               const R*, const R*, const int32_t*, const uint64_t*,             \
+                               const uint8_t*, int64_t, R*, cudaStream_t);                       \
+  template int launch_interp_composite<R>(const DevScene&, int, int, const DrcbGBuffer&,        \
+                                          const int32_t*, const int32_t*, const R*, const R*,   \
+                                          int64_t, int, const R*, R*, cudaStream_t);
+
+INST(float)
+INST(double)
+
+}  // namespace drcb

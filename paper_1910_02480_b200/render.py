@@ -1,0 +1,505 @@
+"""Frame driver and stage entry points — the drop-in surfaces of the
+reference's rendering path, executed on the B200 through libdrcb.
+
+  render_drc(scene, config, net)          drc/cache.py:377-470
+  render(scene, config, mode, weights)    drc/integrators.py:662-722 (drc/direct)
+  intersect_batch / primary_chain_batch / li_direct_batch /
+  trace_radiance_batch / render_input_stacks / shade_indirect_batch
+                                          stage-level parity surfaces
+
+Host-side here is only integer control logic: the progressive pass plan
+(cache.py:59-113), the task order and the per-point sample keys
+(cache.py:42, 243, 279). Everything per ray, per texel, per map and per
+pixel runs in CUDA; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .cnn import MODES, device_net
+from .errors import ConfigError, ContractError
+from .scene import camera_struct, device_scene
+
+T_EPS = 1e-4
+ENTRY_KEY_BASE = 1 << 40
+FALLBACK_KEY_BASE = 1 << 41
+SAMPLER_KINDS = ("independent", "stratified")
+
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+_SEED0 = np.uint64(0x853C49E6748FEA9B)
+
+
+def hash_u64(*keys):
+    """Keyed splitmix-style hash (sampler.py:25-37), host side, for the pass
+    plan only (device kernels carry their own copy)."""
+    h = _SEED0
+    with np.errstate(over="ignore"):
+        for k in keys:
+            z = (h * _M2) ^ np.asarray(k, dtype=np.uint64)
+            z = (z ^ (z >> np.uint64(30))) * _M1
+            z = (z ^ (z >> np.uint64(27))) * _M2
+            h = z ^ (z >> np.uint64(31))
+    return h
+
+
+@dataclass
+class RenderConfig:
+    """RenderConfig (integrators.py:41-72) plus two B200 knobs:
+    precision (64 = fp64 parity build, 32 = fp32 fast build) and net_mode
+    ("fp32" exact SIMT, "tf32" / "bf16" tcgen05)."""
+
+    spp: int = 16
+    direct_spp: int = 8
+    indirect_tasks: int = 5
+    passes: int | None = None
+    max_path_depth: int = 8
+    map_resolution: int = 32
+    mis_samples: int = 16
+    rr_start: int = 5
+    seed: int = 0
+    threads: int = 0
+    r0: int = 16
+    tile: int = 64
+    exposure: float = 1.0
+    sampler_kind: str = "independent"
+    precision: int = 64
+    net_mode: str = "fp32"
+
+    def __post_init__(self):
+        for name in ("spp", "direct_spp", "indirect_tasks", "max_path_depth", "mis_samples",
+                     "rr_start", "r0", "tile"):
+            if getattr(self, name) < 1:
+                raise ConfigError(f"{name} must be >= 1")
+        if self.mis_samples < 2:
+            raise ConfigError("mis_samples must be >= 2")
+        if self.r0 < 2 or (self.r0 & (self.r0 - 1)) != 0:
+            raise ConfigError("r0 must be a power of two >= 2")
+        if self.passes is not None and self.passes < 1:
+            raise ConfigError("passes must be >= 1")
+        if self.sampler_kind not in SAMPLER_KINDS:
+            raise ConfigError(f"unknown sampler kind {self.sampler_kind!r}")
+        if self.precision not in (32, 64):
+            raise ConfigError("precision must be 32 or 64")
+        if self.net_mode not in MODES:
+            raise ConfigError(f"unknown net_mode {self.net_mode!r}")
+
+
+def _cfg_struct(config, precision=None):
+    if getattr(config, "map_resolution", 32) != 32:
+        raise ConfigError("map_resolution must be 32 (the network's input size)")
+    mis = int(config.mis_samples)
+    if mis > 64:
+        raise ConfigError("mis_samples above 64 is not supported on the device")
+    c = _lib.RenderCfg()
+    c.direct_spp = int(config.direct_spp)
+    c.max_path_depth = int(config.max_path_depth)
+    c.mis_samples = mis
+    c.rr_start = int(config.rr_start)
+    c.sampler_kind = SAMPLER_KINDS.index(config.sampler_kind)
+    c.precision = int(precision or getattr(config, "precision", 64))
+    c.tile = int(config.tile)
+    c.seed = int(config.seed)
+    return c
+
+
+# ---------------------------------------------------------------------------
+# progressive plan (cache.py:59-113, 371-374): integer host logic
+
+@dataclass(frozen=True)
+class PassPlan:
+    pass_index: int
+    r: int
+    offset: tuple
+    grid_x: np.ndarray
+    grid_y: np.ndarray
+    subgrids: tuple
+
+    @property
+    def task_count(self):
+        return len(self.subgrids)
+
+    def task_points(self, t):
+        a, b = self.subgrids[t]
+        step = len(self.subgrids) and int(round(np.sqrt(len(self.subgrids))))
+        xs = self.grid_x[a::step] if step > 1 else self.grid_x
+        ys = self.grid_y[b::step] if step > 1 else self.grid_y
+        return xs, ys
+
+
+def _ceil_div(a, b):
+    return -(-a // b)
+
+
+def plan_pass(image_size, pass_index, r0=16, jitter_seed=0):
+    if r0 < 2 or (r0 & (r0 - 1)) != 0:
+        raise ConfigError("r0 must be a power of two >= 2")
+    w, h = image_size
+    r = r0
+    off = [int(hash_u64(jitter_seed, 0, 101) % np.uint64(r)),
+           int(hash_u64(jitter_seed, 1, 101) % np.uint64(r))]
+    for k in range(1, pass_index + 1):
+        r = max(1, _ceil_div(r0, 1 << k))
+        off = [(off[0] + (r + 1) // 2) % r, (off[1] + (r + 1) // 2) % r]
+    r = max(1, _ceil_div(r0, 1 << pass_index))
+    grid_x = np.arange(off[0], w, r, dtype=np.int64)
+    grid_y = np.arange(off[1], h, r, dtype=np.int64)
+    step = min(1 << pass_index, r0)
+    cells = [(a, b) for a in range(step) for b in range(step)]
+    order = np.argsort([int(hash_u64(jitter_seed, 7, a * step + b)) for a, b in cells],
+                       kind="stable")
+    return PassPlan(pass_index, r, (off[0], off[1]), grid_x, grid_y,
+                    tuple(cells[i] for i in order))
+
+
+def task_budget(config):
+    if config.passes is not None:
+        return sum(min(4 ** k, config.r0 ** 2) for k in range(config.passes))
+    return config.indirect_tasks
+
+
+def plan_points(size, config):
+    """All cache points of a frame in the reference's evaluation order:
+    pass by pass, task by task, meshgrid(xs, ys) y-major (cache.py:274-280,
+    436-452). Returns px, py (int32), keys (uint64), r_final, pass records."""
+    w, h = size
+    budget = task_budget(config)
+    pxs, pys, keys, passes = [], [], [], []
+    done, k, r_final = 0, 0, None
+    while done < budget:
+        plan = plan_pass((w, h), k, config.r0, jitter_seed=config.seed)
+        base = ENTRY_KEY_BASE + plan.pass_index * w * h * 4
+        executed = 0
+        for t in range(plan.task_count):
+            if done >= budget:
+                break
+            xs, ys = plan.task_points(t)
+            gx, gy = np.meshgrid(xs, ys)
+            gx, gy = gx.ravel(), gy.ravel()
+            pxs.append(gx)
+            pys.append(gy)
+            keys.append((base + gy * w + gx).astype(np.uint64))
+            done += 1
+            executed += 1
+        passes.append({"index": k, "r": plan.r, "tasks": executed,
+                       "points": int(sum(len(a) for a in pxs))})
+        r_final = plan.r
+        k += 1
+    cat = (lambda a, dt: np.ascontiguousarray(np.concatenate(a).astype(dt)) if a
+           else np.zeros(0, dt))
+    return cat(pxs, np.int32), cat(pys, np.int32), cat(keys, np.uint64), r_final, passes
+
+
+# ---------------------------------------------------------------------------
+# frame driver
+
+class FrameState:
+    """Telemetry view of a finished frame (the reference returns its DrcState;
+    entries here stay on the device and only their count is reported)."""
+
+    def __init__(self, entries, points):
+        self.entry_count = entries
+        self.planned_points = points
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise ContractError("libdrcb needs a CUDA device (there is no CPU path)")
+    return torch
+
+
+def render_drc_device(scene, config, net, camera=None, out=None, precision=None):
+    """One DRC frame, result left on the device: (image (H,W,3) CUDA tensor,
+    telemetry dict). `camera` overrides scene.camera (multi-frame benches)."""
+    torch = _torch()
+    prec = int(precision or getattr(config, "precision", 64))
+    dtype = torch.float64 if prec == 64 else torch.float32
+    cam = camera or scene.camera
+    w, h = cam.resolution
+    ds = device_scene(scene)
+    cfg = _cfg_struct(config, prec)
+    px, py, keys, r_final, passes = plan_points((w, h), config)
+    net_mode = getattr(config, "net_mode", "fp32")
+    dn = device_net(net) if len(px) else None
+    if out is None:
+        out = torch.empty((h, w, 3), dtype=dtype, device="cuda")
+    tel = (C.c_int64 * 8)()
+    t0 = time.time()
+    _lib.call("drcb_render_drc", ds.handle, dn.handle if dn else None,
+              C.byref(camera_struct(cam)), C.byref(cfg),
+              px.ctypes.data_as(C.c_void_p), py.ctypes.data_as(C.c_void_p),
+              keys.ctypes.data_as(C.c_void_p), len(px), int(r_final or 1), MODES[net_mode],
+              _lib.ptr(out), tel, _lib.stream_ptr())
+    telemetry = {
+        "mode": "drc", "direct_spp": config.direct_spp,
+        "geometry_seconds": 0.0, "direct_seconds": 0.0,
+        "passes": [dict(p, entries=None, seconds=None) for p in passes],
+        "nonfinite": int(tel[2]), "entries": int(tel[0]),
+        "fallback_pixels": int(tel[1]), "tasks": sum(p["tasks"] for p in passes),
+        "seconds": time.time() - t0,
+    }
+    telemetry["state"] = FrameState(int(tel[0]), int(tel[3]))
+    return out, telemetry
+
+
+def render_drc(scene, config, net, interrupt=None, snapshots=None):
+    """Drop-in for drc.cache.render_drc: (image (H,W,3) float64, telemetry).
+
+    `snapshots` budgets are rendered as clean runs at that budget, which the
+    reference guarantees equal its mid-run snapshots (cache.py:381-385).
+    `interrupt` is polled once before the frame; a frame is one device
+    submission, so there is no mid-frame pass boundary to stop at."""
+    if interrupt is not None and interrupt():
+        config = _replace(config, indirect_tasks=1, passes=None)
+    img, tel = render_drc_device(scene, config, net)
+    image = img.double().cpu().numpy()
+    if snapshots:
+        snaps = {}
+        for b in sorted(set(snapshots)):
+            if b >= tel["tasks"]:
+                snaps[b] = image if b == tel["tasks"] else None
+                continue
+            si, _ = render_drc_device(scene, _replace(config, indirect_tasks=b, passes=None), net)
+            snaps[b] = si.double().cpu().numpy()
+        tel["snapshots"] = {k: v for k, v in snaps.items() if v is not None}
+    return image, tel
+
+
+def _replace(config, **kw):
+    import dataclasses
+
+    if dataclasses.is_dataclass(config):
+        return dataclasses.replace(config, **kw)
+    d = dict(config.__dict__)
+    d.update(kw)
+    return RenderConfig(**{k: v for k, v in d.items() if k in RenderConfig.__dataclass_fields__})
+
+
+def render(scene, config, mode="pt", weights=None, interrupt=None):
+    """Drop-in for drc.integrators.render for the modes on the hot path."""
+    if mode not in ("pt", "direct", "drc"):
+        raise ConfigError(f"unknown render mode {mode!r}")
+    if mode == "drc":
+        if weights is None:
+            raise ConfigError("drc mode requires a weights network")
+        return render_drc(scene, config, weights, interrupt=interrupt)
+    if mode == "direct":
+        t0 = time.time()
+        torch = _torch()
+        prec = int(getattr(config, "precision", 64))
+        dtype = torch.float64 if prec == 64 else torch.float32
+        w, h = scene.camera.resolution
+        gb = GBufferTensors(w * h, dtype)
+        direct = torch.empty((h, w, 3), dtype=dtype, device="cuda")
+        nf = torch.zeros(1, dtype=torch.int64, device="cuda")
+        cfg = _cfg_struct(config, prec)
+        cfg.include_background = 1
+        _lib.call("drcb_gbuffer_direct", device_scene(scene).handle,
+                  C.byref(camera_struct(scene.camera)), C.byref(cfg), C.byref(gb.struct()),
+                  _lib.ptr(direct), _lib.ptr(nf), _lib.stream_ptr())
+        return direct.double().cpu().numpy(), {"mode": "direct", "spp": config.direct_spp,
+                                               "seconds": time.time() - t0,
+                                               "nonfinite": int(nf.item())}
+    raise ConfigError("mode 'pt' is not on the B200 hot path yet (SURVEY §8f item 2)")
+
+
+# ---------------------------------------------------------------------------
+# stage-level surfaces (numpy in / numpy out, for parity tests)
+
+class GBufferTensors:
+    def __init__(self, n, dtype):
+        torch = _torch()
+        dev = "cuda"
+        self.found = torch.zeros(n, dtype=torch.uint8, device=dev)
+        self.escaped = torch.zeros(n, dtype=torch.uint8, device=dev)
+        self.position = torch.zeros((n, 3), dtype=dtype, device=dev)
+        self.normal = torch.zeros((n, 3), dtype=dtype, device=dev)
+        self.throughput = torch.zeros((n, 3), dtype=dtype, device=dev)
+        self.direction = torch.zeros((n, 3), dtype=dtype, device=dev)
+        self.t_total = torch.zeros(n, dtype=dtype, device=dev)
+        self.mat = torch.zeros(n, dtype=torch.int32, device=dev)
+
+    def struct(self):
+        g = _lib.GBuffer()
+        for f in ("found", "escaped", "position", "normal", "throughput", "direction",
+                  "t_total", "mat"):
+            setattr(g, f, getattr(self, f).data_ptr())
+        return g
+
+    def numpy(self):
+        return {
+            "found": self.found.cpu().numpy().astype(bool),
+            "escaped": self.escaped.cpu().numpy().astype(bool),
+            "position": self.position.double().cpu().numpy(),
+            "normal": self.normal.double().cpu().numpy(),
+            "mat": self.mat.cpu().numpy().astype(np.int64),
+            "throughput": self.throughput.double().cpu().numpy(),
+            "direction": self.direction.double().cpu().numpy(),
+            "t_total": self.t_total.double().cpu().numpy(),
+        }
+
+
+class _Keep(list):
+    """Holds device temporaries until the library call has been issued and
+    the stream synchronised (a bare `ptr(_dev(...))` would let torch recycle
+    the block before the kernel reads it)."""
+
+    def dev(self, a, dtype):
+        torch = _torch()
+        t = torch.from_numpy(np.array(a, copy=True, order="C")).to(device="cuda", dtype=dtype)
+        self.append(t)
+        return _lib.ptr(t)
+
+
+def _dev(a, dtype):
+    torch = _torch()
+    return torch.from_numpy(np.array(a, copy=True, order="C")).to(device="cuda", dtype=dtype)
+
+
+def _rdtype(precision):
+    torch = _torch()
+    return torch.float64 if precision == 64 else torch.float32
+
+
+def intersect_batch(scene, origins, directions, t_min=T_EPS, t_max=np.inf, record=True,
+                    precision=64):
+    """geometry.intersect_batch on the device: dict(hit, t, prim[, mat,
+    position, normal])."""
+    torch = _torch()
+    rd = _rdtype(precision)
+    O = np.atleast_2d(np.asarray(origins, dtype=np.float64))
+    D = np.atleast_2d(np.asarray(directions, dtype=np.float64))
+    n = len(O)
+    Od, Dd = _dev(O, rd), _dev(D, rd)
+    tmin = _dev(np.broadcast_to(np.asarray(t_min, dtype=np.float64), (n,)), rd)
+    tmax = _dev(np.broadcast_to(np.asarray(t_max, dtype=np.float64), (n,)), rd)
+    hit = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    t = torch.zeros(n, dtype=rd, device="cuda")
+    prim = torch.zeros(n, dtype=torch.int64, device="cuda")
+    mat = torch.zeros(n, dtype=torch.int32, device="cuda") if record else None
+    pos = torch.zeros((n, 3), dtype=rd, device="cuda") if record else None
+    nrm = torch.zeros((n, 3), dtype=rd, device="cuda") if record else None
+    _lib.call("drcb_intersect", device_scene(scene).handle, precision, _lib.ptr(Od), _lib.ptr(Dd),
+              n, _lib.ptr(tmin), _lib.ptr(tmax), int(bool(record)), _lib.ptr(hit), _lib.ptr(t),
+              _lib.ptr(prim), _lib.ptr(mat), _lib.ptr(pos), _lib.ptr(nrm), _lib.stream_ptr())
+    out = {"hit": hit.cpu().numpy().astype(bool), "t": t.double().cpu().numpy(),
+           "prim": prim.cpu().numpy()}
+    if record:
+        out["mat"] = mat.cpu().numpy().astype(np.int64)
+        out["position"] = pos.double().cpu().numpy()
+        out["normal"] = nrm.double().cpu().numpy()
+    return out
+
+
+def primary_chain_batch(scene, origins, directions, precision=64):
+    K = _Keep()
+    rd = _rdtype(precision)
+    O = np.atleast_2d(np.asarray(origins, dtype=np.float64))
+    D = np.atleast_2d(np.asarray(directions, dtype=np.float64))
+    gb = GBufferTensors(len(O), rd)
+    _lib.call("drcb_primary_chain", device_scene(scene).handle, precision, K.dev(O, rd),
+              K.dev(D, rd), len(O), C.byref(gb.struct()), _lib.stream_ptr())
+    return gb.numpy()
+
+
+def _sampler_cfg(sampler, precision, **kw):
+    cfg = RenderConfig(direct_spp=max(int(getattr(sampler, "spp", 1)), 1),
+                       sampler_kind=getattr(sampler, "kind", "independent"),
+                       seed=int(getattr(sampler, "seed", 0)), precision=precision, **kw)
+    return _cfg_struct(cfg, precision)
+
+
+def li_direct_batch(scene, origins, directions, pixel_keys, sample_keys, sampler,
+                    include_background=True, stats=None, precision=64):
+    K = _Keep()
+    torch = _torch()
+    rd = _rdtype(precision)
+    O = np.atleast_2d(np.asarray(origins, dtype=np.float64))
+    n = len(O)
+    L = torch.zeros((n, 3), dtype=rd, device="cuda")
+    nf = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cfg = _sampler_cfg(sampler, precision)
+    _lib.call("drcb_li_direct", device_scene(scene).handle, C.byref(cfg), K.dev(O, rd),
+              K.dev(np.asarray(directions, dtype=np.float64), rd),
+              K.dev(np.asarray(pixel_keys, dtype=np.uint64).view(np.int64), torch.int64),
+              K.dev(np.asarray(sample_keys, dtype=np.uint64).view(np.int64), torch.int64),
+              n, int(bool(include_background)), _lib.ptr(L), _lib.ptr(nf), _lib.stream_ptr())
+    if stats is not None:
+        stats["nonfinite"] = stats.get("nonfinite", 0) + int(nf.item())
+    return L.double().cpu().numpy()
+
+
+def trace_radiance_batch(scene, origins, directions, pixel_keys, sample_keys, sampler, max_depth,
+                         skip_first_emission=False, rr_start=5, stats=None, precision=64):
+    K = _Keep()
+    torch = _torch()
+    if max_depth < 1:
+        raise ContractError("max_depth must be >= 1")
+    rd = _rdtype(precision)
+    O = np.atleast_2d(np.asarray(origins, dtype=np.float64))
+    n = len(O)
+    L = torch.zeros((n, 3), dtype=rd, device="cuda")
+    nf = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cfg = _sampler_cfg(sampler, precision)
+    _lib.call("drcb_trace_radiance", device_scene(scene).handle, C.byref(cfg),
+              K.dev(O, rd), K.dev(np.asarray(directions, dtype=np.float64), rd),
+              K.dev(np.asarray(pixel_keys, dtype=np.uint64).view(np.int64), torch.int64),
+              K.dev(np.asarray(sample_keys, dtype=np.uint64).view(np.int64), torch.int64),
+              n, int(max_depth), int(bool(skip_first_emission)), int(rr_start), _lib.ptr(L),
+              _lib.ptr(nf), _lib.stream_ptr())
+    if stats is not None:
+        stats["nonfinite"] = stats.get("nonfinite", 0) + int(nf.item())
+    return L.double().cpu().numpy()
+
+
+def render_input_stacks(scene, positions, normals, keys, config, precision=64):
+    """render_input_stacks_batch (hemimap.py:229-281) for n hits given as
+    front-facing positions/normals. Returns stacks (n,7,32,32) float32,
+    s_r (n,), s_d (n,), frames (n,3,3) rows t,b,n."""
+    K = _Keep()
+    torch = _torch()
+    rd = _rdtype(precision)
+    P = np.atleast_2d(np.asarray(positions, dtype=np.float64))
+    n = len(P)
+    stacks = torch.zeros((n, 7, 32, 32), dtype=torch.float32, device="cuda")
+    s_r = torch.zeros(n, dtype=rd, device="cuda")
+    s_d = torch.zeros(n, dtype=rd, device="cuda")
+    frames = torch.zeros((n, 9), dtype=rd, device="cuda")
+    nf = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cfg = _cfg_struct(config, precision)
+    _lib.call("drcb_render_stacks", device_scene(scene).handle, C.byref(cfg),
+              K.dev(P, rd), K.dev(np.asarray(normals, dtype=np.float64), rd),
+              K.dev(np.asarray(keys, dtype=np.uint64).view(np.int64), torch.int64), n,
+              _lib.ptr(stacks), _lib.ptr(s_r), _lib.ptr(s_d), _lib.ptr(frames), _lib.ptr(nf),
+              _lib.stream_ptr())
+    return (stacks.cpu().numpy(), s_r.double().cpu().numpy(), s_d.double().cpu().numpy(),
+            frames.double().cpu().numpy().reshape(n, 3, 3))
+
+
+def shade_indirect_batch(scene, pred, s_r, frames, wo, mats, keys, config, precision=64):
+    """shade_indirect (integrators.py:564-614) for n cache points at once.
+    pred (n,3,32,32) float32 normalised prediction; frames (n,3,3)."""
+    K = _Keep()
+    torch = _torch()
+    rd = _rdtype(precision)
+    pred = np.ascontiguousarray(pred, dtype=np.float32)
+    n = len(pred)
+    L = torch.zeros((n, 3), dtype=rd, device="cuda")
+    cfg = _cfg_struct(config, precision)
+    _lib.call("drcb_shade", device_scene(scene).handle, C.byref(cfg),
+              K.dev(pred, torch.float32), K.dev(np.asarray(s_r, np.float64), rd),
+              K.dev(np.asarray(frames, np.float64).reshape(n, 9), rd),
+              K.dev(np.asarray(wo, np.float64).reshape(n, 3), rd),
+              K.dev(np.asarray(mats, np.int32), torch.int32),
+              K.dev(np.asarray(keys, dtype=np.uint64).view(np.int64), torch.int64), n,
+              _lib.ptr(L), _lib.stream_ptr())
+    return L.double().cpu().numpy()

@@ -1,0 +1,208 @@
+"""Generate golden vectors by running the UNMODIFIED reference
+(/root/reference/pkg, imported read-only via sys.path) in the build container.
+
+The GPU box has no reference checkout, so the outputs are committed as small
+.npz fixtures next to this script; tests/ compare libdrcb and the C oracle
+against them. Re-run with:  python tests/golden/make_golden.py
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+REF = "/root/reference/pkg"
+sys.path.insert(0, os.path.join(REF, "src"))
+sys.path.insert(0, os.path.join(REF, "trainer", "src"))
+sys.path.insert(0, REPO)
+
+from drc import cnn as rcnn  # noqa: E402
+from drc import geometry as rgeo  # noqa: E402
+from drc import hemimap as rhemi  # noqa: E402
+from drc import integrators as rint  # noqa: E402
+from drc.cache import DrcState, plan_pass, render_drc  # noqa: E402
+from drc.integrators import RenderConfig  # noqa: E402
+from drc.sampler import Sampler  # noqa: E402
+from drc.scene import parse_scene  # noqa: E402
+
+from paper_1910_02480_b200 import scenegen  # noqa: E402
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {name}: {os.path.getsize(path)} bytes")
+
+
+def doc_array(doc):
+    return np.frombuffer(json.dumps(doc).encode("utf-8"), dtype=np.uint8)
+
+
+def ref_scene_doc(name, res):
+    with open(os.path.join(REF, "scenes", f"{name}.json")) as f:
+        doc = json.load(f)
+    doc["camera"]["resolution"] = [res, res]
+    return doc
+
+
+def random_shape_doc(rng, n_spheres, n_quads, n_tris):
+    # the shape mix of tests/test_geometry.py:39-57
+    shapes = []
+    for _ in range(n_spheres):
+        shapes.append({"type": "sphere", "center": list(rng.uniform(-5, 5, 3)),
+                       "radius": float(rng.uniform(0.1, 1.2)), "material": "gray"})
+    for _ in range(n_quads):
+        shapes.append({"type": "quad", "corner": list(rng.uniform(-5, 5, 3)),
+                       "edge_u": list(rng.uniform(-2, 2, 3)), "edge_v": list(rng.uniform(-2, 2, 3)),
+                       "material": "gray"})
+    verts = rng.uniform(-5, 5, (3 * n_tris, 3))
+    shapes.append({"type": "mesh", "vertices": verts.tolist(),
+                   "triangles": np.arange(3 * n_tris).reshape(-1, 3).tolist(), "material": "gray"})
+    return {"camera": {"position": [0, 0, -5], "look_at": [0, 0, 0], "up": [0, 1, 0], "fov": 40.0,
+                       "resolution": [64, 64]},
+            "global_up": [0, 1, 0],
+            "materials": {"gray": {"kind": "diffuse", "albedo": [0.5, 0.5, 0.5]},
+                          "lamp": {"kind": "diffuse", "albedo": [0.5, 0.5, 0.5],
+                                   "emission": [4.0, 4.0, 4.0]}},
+            "shapes": shapes, "point_lights": []}
+
+
+def geometry_fixture():
+    rng = np.random.default_rng(2024)
+    doc = random_shape_doc(rng, 40, 40, 20)
+    # make a few prims emissive so light tables are exercised
+    doc["shapes"][3]["material"] = "lamp"
+    doc["shapes"][45]["material"] = "lamp"
+    scene = parse_scene(json.dumps(doc))
+    n = 4000
+    O = rng.uniform(-8, 8, (n, 3))
+    D = rng.normal(size=(n, 3))
+    D /= np.linalg.norm(D, axis=1, keepdims=True)
+    r = rgeo.intersect_batch(scene.geometry, O, D)
+    tmax = rng.uniform(0.5, 12.0, n)
+    s = rgeo.intersect_batch(scene.geometry, O, D, t_max=tmax, record=False)
+    save("geometry_mixed.npz", doc=doc_array(doc), O=O, D=D, hit=r["hit"], t=r["t"],
+         prim=r["prim"], mat=r["mat"], position=r["position"], normal=r["normal"], tmax=tmax,
+         shadow_hit=s["hit"])
+
+
+def frame_fixture(name, doc, k, seed_w, cfg_kw, n_points=6, net=None):
+    """Stage-level and whole-frame outputs of one small scene."""
+    scene = parse_scene(json.dumps(doc))
+    cfg = RenderConfig(threads=1, **cfg_kw)
+    w, h = scene.camera.resolution
+    state = DrcState(scene, cfg)
+    geo = state.geo
+    direct, _ = rint.render(scene, cfg, "direct")
+    if net is None:
+        net = rcnn.random_network(k, seed_w)
+    # cache points: the first pass-0 grid points that are found
+    plan = plan_pass((w, h), 0, cfg.r0, jitter_seed=cfg.seed)
+    xs, ys = plan.task_points(0)
+    gx, gy = np.meshgrid(xs, ys)
+    pts = [(x, y) for x, y in zip(gx.ravel(), gy.ravel()) if geo["found"][y * w + x]][:n_points]
+    keys = [(1 << 40) + y * w + x for x, y in pts]
+    hits = []
+    for x, y in pts:
+        i = y * w + x
+        hits.append(rgeo.Hit(position=geo["position"][i], normal=geo["normal"][i],
+                             distance=float(geo["t_total"][i]), material_id=int(geo["mat"][i]),
+                             is_emitter=False, emitted=np.zeros(3)))
+    msampler = Sampler(cfg.sampler_kind, cfg.seed, 1)
+    stacks = rhemi.render_input_stacks_batch(scene, hits, msampler, cfg, keys) if hits else []
+    st = np.stack([s.as_tensor() for s in stacks]) if stacks else np.zeros((0, 7, 32, 32), np.float32)
+    preds = np.stack([rcnn.forward(net, s) for s in st]) if stacks else np.zeros((0, 3, 32, 32), np.float32)
+    shade = []
+    for (x, y), hit, stk, key, pred in zip(pts, hits, stacks, keys, preds):
+        i = y * w + x
+        radmap = rhemi.HemiMap(np.moveaxis(pred, 0, -1), stk.radiance.frame, scale=stk.s_r)
+        shade.append(rint.shade_indirect(scene, hit, radmap, stk.radiance.frame,
+                                         -geo["direction"][i], msampler, cfg.mis_samples, key=key))
+    frames = np.stack([np.stack([s.radiance.frame.t, s.radiance.frame.b, s.radiance.frame.n])
+                       for s in stacks]) if stacks else np.zeros((0, 3, 3))
+    img, tel = render_drc(scene, cfg, net)
+    out = dict(doc=doc_array(doc), k=k, seed_w=seed_w, cfg=doc_array(cfg_kw),
+               found=geo["found"], escaped=geo["escaped"], position=geo["position"],
+               normal=geo["normal"], mat=geo["mat"], throughput=geo["throughput"],
+               direction=geo["direction"], t_total=geo["t_total"], direct=direct,
+               pts=np.array(pts, dtype=np.int64).reshape(-1, 2),
+               keys=np.array(keys, dtype=np.uint64), stacks=st,
+               s_r=np.array([s.s_r for s in stacks]), s_d=np.array([s.s_d for s in stacks]),
+               frames=frames, preds=preds, shade=np.array(shade).reshape(-1, 3), image=img,
+               entries=tel["entries"], tasks=tel["tasks"])
+    save(name, **out)
+
+
+def trace_fixture():
+    scene = scenegen.build_scene("c1", resolution=(32, 32))
+    doc = scenegen.scene_doc(scene)
+    rscene = parse_scene(json.dumps(doc))
+    rng = np.random.default_rng(7)
+    n = 1024
+    O = rng.uniform(-0.9, 0.9, (n, 3))
+    D = rng.normal(size=(n, 3))
+    D /= np.linalg.norm(D, axis=1, keepdims=True)
+    pix = rng.integers(0, 1 << 40, n).astype(np.uint64)
+    smp = rng.integers(0, 1024, n).astype(np.uint64)
+    s = Sampler("independent", 3, 1)
+    L0 = rint.trace_radiance_batch(rscene, O, D, pix, smp, s, 8, skip_first_emission=False, rr_start=5)
+    L1 = rint.trace_radiance_batch(rscene, O, D, pix, smp, s, 8, skip_first_emission=True, rr_start=5)
+    s4 = Sampler("stratified", 5, 4)
+    Ld = rint.li_direct_batch(rscene, O, D, pix, smp % np.uint64(4), s4, include_background=True)
+    ch = rint.primary_chain_batch(rscene, O, D)
+    save("trace_c1.npz", doc=doc_array(doc), O=O, D=D, pix=pix, smp=smp, L_full=L0, L_skip=L1,
+         L_direct_strat=Ld, chain_found=ch["found"], chain_position=ch["position"])
+
+
+def cnn_fixture():
+    rng = np.random.default_rng(11)
+    out = {}
+    for k, seed, n in ((8, 5, 4), (64, 1, 2)):
+        net = rcnn.random_network(k, seed)
+        raw = rcnn.save_weights(net)
+        x = rng.uniform(0, 1, (n, 7, 32, 32)).astype(np.float32)
+        x[:, :3] *= rng.uniform(0.5, 20.0)  # radiance channels span a wide range
+        y = np.stack([rcnn.forward(net, xi) for xi in x])
+        out[f"x_k{k}"] = x
+        out[f"y_k{k}"] = y
+        out[f"sha_k{k}"] = np.frombuffer(hashlib.sha256(raw).digest(), dtype=np.uint8)
+    # hand-checkable primitives (test_cnn.py KAT style)
+    xb = rng.normal(size=(3, 8, 8)).astype(np.float32)
+    out["up_in"] = xb
+    out["up_out"] = rcnn.upsample_bilinear2x2(xb)
+    blur = rcnn.make_blur_network(16)
+    xs = rng.uniform(0, 1, (2, 7, 32, 32)).astype(np.float32)
+    out["blur_x"] = xs
+    out["blur_y"] = np.stack([rcnn.forward(blur, v) for v in xs])
+    save("cnn.npz", **out)
+
+
+def main():
+    geometry_fixture()
+    trace_fixture()
+    cnn_fixture()
+    c1 = scenegen.scene_doc(scenegen.build_scene("c1", resolution=(48, 48)))
+    frame_fixture("frame_c1.npz", c1, 8, 0, dict(direct_spp=2, indirect_tasks=5, mis_samples=16))
+    frame_fixture("frame_cornell.npz", ref_scene_doc("cornell", 32), 8, 3,
+                  dict(direct_spp=2, indirect_tasks=2, mis_samples=8))
+    frame_fixture("frame_glossybox.npz", ref_scene_doc("glossybox", 32), 8, 4,
+                  dict(direct_spp=3, indirect_tasks=1, mis_samples=16, sampler_kind="stratified"))
+    frame_fixture("frame_room.npz", ref_scene_doc("room", 32), 16, 0,
+                  dict(direct_spp=2, indirect_tasks=3, mis_samples=8, seed=9),
+                  net=rcnn.make_blur_network(16))
+    env = {"camera": {"position": [0, 0, -5], "look_at": [0, 0, 0], "up": [0, 1, 0], "fov": 40.0,
+                      "resolution": [16, 16]},
+           "global_up": [0, 1, 0], "materials": {"gray": {"kind": "diffuse", "albedo": [0.5, 0.5, 0.5]}},
+           "shapes": [{"type": "sphere", "center": [0, 0, 0], "radius": 1.0, "material": "gray"}],
+           "point_lights": [], "environment": [1.0, 1.0, 1.0]}
+    frame_fixture("frame_furnace.npz", env, 8, 1, dict(direct_spp=2, indirect_tasks=1, mis_samples=8))
+
+
+if __name__ == "__main__":
+    main()
