@@ -1,0 +1,347 @@
+"""Benchmark: predicted-radiance DRC frames/s at 1024^2 (BASELINE.json config 3).
+
+One step = one batch of 8 complete DRC frames per rank (G-buffer + direct,
+cache-point map path tracing, U-Net, MIS shading, interpolation, composite)
+over the 258,036-triangle config-3 scene, each frame from its own orbit camera.
+Frames shard across ranks with no collective (weak scaling: every rank renders
+its own 8 frames; value = all frames / max-over-ranks time).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+
+--impl reference times the CPU restatement of the reference path (the C
+oracle; the reference itself is pure Python and cannot run whole frames at
+this size) on the host cores over a bounded sample and
+extrapolates frames/s.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+FRAMES_PER_RANK = 8
+METRIC = "frames/sec at 1024^2 (DRC frame: G-buffer+direct, map path tracing, U-Net, shade, interp)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--tasks", type=int, default=1)
+    ap.add_argument("--precision", type=int, default=32)
+    ap.add_argument("--net", default=os.environ.get("DRCB_BENCH_NET", "bf16"))
+    ap.add_argument("--frames", type=int, default=FRAMES_PER_RANK)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-points", type=int, default=16)
+    ap.add_argument("--cpu-pixels", type=int, default=4096)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md clocks line)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 8]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+
+def measured_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def cpu_baseline(scene, cams, cfg, net_host, npts_total, n_pixels, n_points, rank):
+    """Oracle (CPU restatement of the reference path) on a bounded sample of
+    the same workload; returns per-frame extrapolation."""
+    from oracle import oracle as O
+
+    nthreads = os.cpu_count() or 1
+    O.set_threads(nthreads)
+    from paper_1910_02480_b200 import cnn
+    from paper_1910_02480_b200.render import plan_points
+
+    osc = O.OracleScene(scene)
+    onet = O.OracleNet(cnn.save_weights(net_host))
+    cam = cams[0]
+    w, h = cam.resolution
+    p0 = (h // 2) * w
+    t0 = time.perf_counter()
+    geo, _ = O.gbuffer_direct(osc, cam, cfg, p0, p0 + n_pixels)
+    t_px = (time.perf_counter() - t0) / n_pixels
+    px, py, keys, _, _ = plan_points((w, h), cfg)
+    idx = py.astype(np.int64) * w + px
+    # G-buffer rows for the sampled cache points (pixel rows outside the
+    # sample are filled from a second bounded call on just those pixels)
+    sel = np.linspace(0, len(px) - 1, n_points).astype(np.int64)
+    pos, nrm, ks, dirs, mats = [], [], [], [], []
+    for j in sel:
+        g, _ = O.gbuffer_direct(osc, cam, cfg, int(idx[j]), int(idx[j]) + 1)
+        q = int(idx[j])
+        if g["found"][q]:
+            pos.append(g["position"][q]); nrm.append(g["normal"][q]); ks.append(keys[j])
+            dirs.append(g["direction"][q]); mats.append(g["mat"][q])
+    t1 = time.perf_counter()
+    st, s_r, _, frames = O.render_stacks(osc, np.array(pos), np.array(nrm), np.array(ks, np.uint64), cfg)
+    pred = onet.forward(st)
+    O.shade(osc, pred, s_r, frames, -np.array(dirs), np.array(mats), np.array(ks, np.uint64), cfg)
+    t_pt = (time.perf_counter() - t1) / max(1, len(pos))
+    frame_s = w * h * t_px + npts_total * t_pt
+    return {"value": 1.0 / frame_s, "unit": "frames/s", "cores": nthreads, "kind": "port",
+            "sample": f"oracle on {n_pixels} px (G-buffer+direct) + {len(pos)} cache points "
+                      f"(maps+U-Net fp32+shade) of config {cfg_name()} frame 0; frame time "
+                      f"extrapolated = {w}x{h}*{t_px*1e6:.1f}us + {npts_total}*{t_pt*1e3:.1f}ms",
+            "seconds_per_frame": frame_s}
+
+
+_CFG_NAME = ["c3"]
+
+
+def cfg_name():
+    return _CFG_NAME[0]
+
+
+def main():
+    args = parse()
+    _CFG_NAME[0] = args.config
+    rank, world, local = dist_env()
+    from paper_1910_02480_b200 import cnn, render, scenegen
+
+    res, _, _, _, _, wseed = scenegen.CONFIGS[args.config]
+    cfg = render.RenderConfig(direct_spp=1, indirect_tasks=args.tasks, mis_samples=16,
+                              max_path_depth=8, rr_start=5, seed=0, precision=args.precision,
+                              net_mode=args.net if args.net in ("fp32", "tf32", "bf16") else "fp32")
+    workload = {"workload": f"{args.config}: DRC frames {res[0]}x{res[1]}, "
+                            f"{args.frames} frames/rank/step, indirect_tasks={args.tasks}, "
+                            f"direct_spp=1, orbit cameras r=3 (seed 2)",
+                "scene_tris": None, "cache_points_per_frame": None,
+                "precision": f"rays fp{args.precision}, U-Net {cfg.net_mode}",
+                "l2": "flushed between steps (256 MB write)"}
+    scene = scenegen.build_scene(args.config)
+    cams = scenegen.orbit_cameras(args.frames * max(world, 1), res, seed=2)
+    my_cams = cams[rank * args.frames:(rank + 1) * args.frames]
+    net = cnn.random_network(64, seed=wseed)
+    plan = render.plan_points(res, cfg)
+    n_pts = len(plan[0])
+    workload["cache_points_per_frame"] = n_pts
+    from paper_1910_02480_b200.scene import flatten
+
+    workload["scene_tris"] = int(len(flatten(scene)["tri_mat"]))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        vals = []
+        cb = None
+        for i in range(args.warmup + args.steps):
+            cb = cpu_baseline(scene, cams, cfg, net, n_pts, args.cpu_pixels, args.cpu_points, rank)
+            if i >= args.warmup:
+                vals.append(cb["value"])
+        v = float(np.mean(vals))
+        cb["value"] = v
+        line = {"metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * args.frames / v,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded procedural scene, SURVEY §8d)", "config": workload,
+                "impl": "reference", "cpu_baseline": cb,
+                "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1910_02480_b200 import _lib
+    from paper_1910_02480_b200.scene import device_scene
+
+    ds = device_scene(scene)
+    st = ds.stats()
+    dn = cnn.device_net(net)
+    dtype = torch.float32 if args.precision == 32 else torch.float64
+    w, h = res
+    outs = [torch.empty((h, w, 3), dtype=dtype, device="cuda") for _ in my_cams]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def frame(i, tel=False):
+        return render.render_drc_device(scene, cfg, net, camera=my_cams[i], out=outs[i], plan=plan,
+                                        telemetry=tel)
+
+    def step(tel=False):
+        stages = []
+        for i in range(len(my_cams)):
+            _, t = frame(i, tel)
+            if t:
+                stages.append(t["stage_us"])
+        return stages
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device-resident inputs)
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = _lib.load().drcb_kernel_launches()
+    ev0.record()
+    stage_rows = []
+    for _ in range(args.steps):
+        stage_rows += step(tel=True)
+        flush.fill_(1.0)
+    ev1.record()
+    launches_timed = int(_lib.load().drcb_kernel_launches() - l0)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    frames_total = args.steps * len(my_cams) * world
+    value = frames_total / (ms / 1e3)
+
+    # ---- e2e: public API with host buffers (plan H2D inside the call, image D2H)
+    pinned = [torch.empty((h, w, 3), dtype=dtype, pin_memory=True) for _ in my_cams]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        for i in range(len(my_cams)):
+            img, _ = render.render_drc_device(scene, cfg, net, camera=my_cams[i], out=outs[i],
+                                              telemetry=False)
+            pinned[i].copy_(img, non_blocking=True)
+        flush.fill_(1.0)
+    e1.record()
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    te = torch.tensor([ems], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = frames_total / (float(te.item()) / 1e3)
+    h2d = len(my_cams) * n_pts * (4 + 4 + 8)
+    d2h = len(my_cams) * h * w * 3 * (4 if args.precision == 32 else 8)
+
+    # ---- roofline of the dominant stage (live CUDA-event stage times)
+    peaks, src = measured_peaks()
+    avg = {k: float(np.mean([r[k] for r in stage_rows])) for k in stage_rows[0]}
+    dom = max(avg, key=avg.get)
+    flop_map = cnn.flops_per_map(64)
+    if dom == "network":
+        achieved = n_pts * flop_map / (avg["network"] * 1e-6) / 1e12
+        peak = peaks.get("bf16_tflops", 1590.0)
+        roof = {"bound": "tensor", "kernel": "U-Net forward (all conv layers)", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "algorithmic": f"{flop_map/1e9:.5f} GFLOP/map x {n_pts} maps"}
+    else:
+        # traversal-bound stages: algorithmic bytes = scene bytes read once
+        # per launch lower bound is meaningless; report counted casts instead
+        casts = None
+        roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": peaks.get("hbm_gbs"),
+                "unit": "GB/s", "frac": None, "traffic": None}
+    roof["peak_source"] = src
+    roof["stage_ms_per_frame"] = {k: v / 1e3 for k, v in avg.items()}
+
+    cb = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_baseline(scene, cams, cfg, net, n_pts, args.cpu_pixels, args.cpu_points, rank)
+        except Exception as e:  # the baseline must never break the GPU line
+            cb = {"value": None, "error": repr(e)}
+    launches = launches_timed
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": f"f{args.precision} rays / {cfg.net_mode} U-Net",
+            "data": "synthetic (seeded procedural scene + random-init U-Net, SURVEY §8d)",
+            "config": workload, "clocks": clk, "roofline": roof, "cpu_baseline": cb,
+            "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches, "scene_stats": st,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -194,6 +194,15 @@ int drcb_net_info(const DrcbNet *net, int64_t *out4);
 int drcb_net_forward(const DrcbNet *net, const float *x, float *y, int64_t n,
                      int32_t mode, void *stream);
 
+/* single tensor-core conv layer with an identity epilogue, HOST arrays
+ * (unit-test harness for the implicit-GEMM kernel): x (n,hw,hw,cin) NHWC,
+ * w (cout,cin,3,3) conv form, y (n,hw,hw,cout). */
+int drcb_debug_conv(int32_t mode, int32_t cin, int32_t cout, int32_t hw, int64_t n,
+                    const float *x, const float *w, float *y);
+
+/* number of kernels this library has launched so far (process-wide) */
+int64_t drcb_kernel_launches(void);
+
 const char *drcb_last_error(void);
 int drcb_version(void);
 

@@ -1,6 +1,7 @@
 // drcb_capi.cu — extern "C" entry points of libdrcb.so (include/drcb.h) and
 // the whole-frame driver drcb_render_drc (drc/cache.py:377-470).
 #include <cub/cub.cuh>
+#include <atomic>
 #include <cstring>
 #include <string>
 
@@ -9,6 +10,8 @@
 namespace drcb {
 
 static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(const std::string& msg) { g_err = msg; }
 int fail(int code, const std::string& msg) {
@@ -95,17 +98,48 @@ __global__ void k_u8_to_int(const uint8_t* a, int* b, int64_t n) {
   if (i < n) b[i] = a[i];
 }
 
+__global__ void k_entry_count(const int* rank, const uint8_t* live, int64_t n, int* m) {
+  *m = n > 0 ? rank[n - 1] + int(live[n - 1]) : 0;
+}
+
+// Per-frame stage timing (CUDA events on the frame's stream; read only when
+// the caller asks for telemetry, so the frame itself never blocks the host).
+struct StageEvents {
+  cudaEvent_t ev[6] = {};
+  bool on = false;
+  void create() {
+    for (auto& e : ev) cudaEventCreate(&e);
+    on = true;
+  }
+  void rec(int i, cudaStream_t st) {
+    if (on) cudaEventRecord(ev[i], st);
+  }
+  float ms(int a, int b) {
+    float t = 0.f;
+    if (on) cudaEventElapsedTime(&t, ev[a], ev[b]);
+    return t;
+  }
+  ~StageEvents() {
+    if (on)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
 template <typename R>
 int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
                  const DrcbRenderCfg* cfg, const int32_t* px_h, const int32_t* py_h,
                  const uint64_t* keys_h, int64_t np_, int r_final, int net_mode, R* image,
                  int64_t* tel, cudaStream_t st) {
   const DevScene& S = scene->dev;
+  keep_pool_memory();
   DevCamera C = make_camera(*cam);
   const int W = C.W, H = C.H;
   const int64_t npx = int64_t(W) * H;
-  // ---- frame buffers
-  size_t bytes = npx * (2 + 4 + sizeof(R) * 16) + 64;
+  StageEvents E;
+  if (tel) E.create();
+  E.rec(0, st);
+  // ---- frame buffers (stream-ordered allocations from the pool)
+  size_t bytes = npx * (2 + 4 + sizeof(R) * 16) + 256;
   uint8_t* fb = nullptr;
   DRCB_CUDA(cudaMallocAsync((void**)&fb, bytes, st));
   DrcbGBuffer gb;
@@ -124,20 +158,19 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
   gb.mat = (int32_t*)take(npx * 4);
   gb.found = take(npx);
   gb.escaped = take(npx);
-  int64_t* d_nf = nullptr;
-  DRCB_CUDA(cudaMallocAsync((void**)&d_nf, 8, st));
+  int64_t* d_nf = (int64_t*)take(8);
+  int* d_m = (int*)take(4);
   DRCB_CUDA(cudaMemsetAsync(d_nf, 0, 8, st));
+  DRCB_CUDA(cudaMemsetAsync(d_m, 0, 4, st));
   DrcbRenderCfg dcfg = *cfg;
   dcfg.include_background = 0;  // escaped chains carry the env in the indirect layer
   int rc = launch_gbuffer_direct<R>(S, C, dcfg, cfg->tile, gb, direct, d_nf, st);
   if (rc) return rc;
-  // ---- cache points
-  int64_t m = 0;
-  int32_t* epx = nullptr;
+  E.rec(1, st);
   uint8_t* pb = nullptr;
   if (np_ > 0) {
-    size_t pbytes = np_ * (4 + 4 + 8 + 4 + 1 + 4 + 4 + 4 + 4 + sizeof(R) * (3 * 6 + 2 + 9)) + 32 * 16 +
-                    np_ * size_t(7 + 3) * 1024 * 4 + 1024;
+    size_t pbytes = np_ * (4 * 8 + 8 + 1 + sizeof(R) * (3 * 6 + 2 + 9)) + 32 * 24 +
+                    np_ * size_t(7 + 3) * 1024 * 4;
     DRCB_CUDA(cudaMallocAsync((void**)&pb, pbytes, st));
     cur = pb;
     int32_t* px = (int32_t*)take(np_ * 4);
@@ -146,6 +179,9 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
     int32_t* mat = (int32_t*)take(np_ * 4);
     uint8_t* live = take(np_);
     int* rank = (int*)take(np_ * 4);
+    int* flags = (int*)take(np_ * 4);
+    int32_t* epx = (int32_t*)take(np_ * 4);
+    int32_t* epy = (int32_t*)take(np_ * 4);
     R* pos = (R*)take(np_ * 3 * sizeof(R));
     R* nrm = (R*)take(np_ * 3 * sizeof(R));
     R* wo = (R*)take(np_ * 3 * sizeof(R));
@@ -157,25 +193,25 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
     R* frames = (R*)take(np_ * 9 * sizeof(R));
     float* stacks = (float*)take(np_ * 7 * 1024 * 4);
     float* pred = (float*)take(np_ * 3 * 1024 * 4);
-    epx = (int32_t*)take(np_ * 4);
-    int32_t* epy = (int32_t*)take(np_ * 4);
     DRCB_CUDA(cudaMemcpyAsync(px, px_h, np_ * 4, cudaMemcpyHostToDevice, st));
     DRCB_CUDA(cudaMemcpyAsync(py, py_h, np_ * 4, cudaMemcpyHostToDevice, st));
     DRCB_CUDA(cudaMemcpyAsync(keys, keys_h, np_ * 8, cudaMemcpyHostToDevice, st));
     int nb = int((np_ + 127) / 128);
     k_gather_points<R><<<nb, 128, 0, st>>>(gb, W, px, py, np_, pos, nrm, wo, mat, live);
+    count_launch();
     rc = launch_render_stacks<R>(S, *cfg, pos, nrm, keys, live, np_, stacks, s_r, s_d, frames,
                                  d_nf, st);
     if (rc) return rc;
+    E.rec(2, st);
     if (net_mode == DRCB_NET_FP32)
       rc = forward_f32_chunked(net->impl, stacks, pred, np_, st);
     else
       rc = forward_tc(net->impl, stacks, pred, np_, net_mode, st);
     if (rc) return rc;
+    E.rec(3, st);
     rc = launch_shade<R>(S, *cfg, pred, s_r, frames, wo, mat, keys, live, np_, Le, st);
     if (rc) return rc;
-    // live-point compaction
-    int* flags = (int*)take(np_ * 4);
+    // stable compaction of live points into the entry pool
     k_u8_to_int<<<nb, 128, 0, st>>>(live, flags, np_);
     size_t tmpb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmpb, flags, rank, int(np_), st);
@@ -184,31 +220,40 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
     cub::DeviceScan::ExclusiveSum(tmp, tmpb, flags, rank, int(np_), st);
     DRCB_CUDA(cudaFreeAsync(tmp, st));
     k_scatter_entries<R><<<nb, 128, 0, st>>>(live, rank, np_, px, py, nrm, Le, epx, epy, en, erad);
-    int last_rank = 0;
-    uint8_t last_live = 0;
-    DRCB_CUDA(cudaMemcpyAsync(&last_rank, rank + np_ - 1, 4, cudaMemcpyDeviceToHost, st));
-    DRCB_CUDA(cudaMemcpyAsync(&last_live, live + np_ - 1, 1, cudaMemcpyDeviceToHost, st));
-    DRCB_CUDA(cudaStreamSynchronize(st));
-    m = int64_t(last_rank) + last_live;
-    rc = launch_interp_composite<R>(S, W, H, gb, epx, epy, en, erad, m, r_final, direct, image, st);
+    k_entry_count<<<1, 1, 0, st>>>(rank, live, np_, d_m);
+    count_launch(5);  // u8_to_int, scan (2), scatter, entry_count
+    E.rec(4, st);
+    rc = launch_interp_composite<R>(S, W, H, gb, epx, epy, en, erad, np_, d_m, r_final, direct,
+                                    image, st);
     if (rc) return rc;
   } else {
-    rc = launch_interp_composite<R>(S, W, H, gb, nullptr, nullptr, nullptr, nullptr, 0, r_final,
-                                    direct, image, st);
+    E.rec(2, st);
+    E.rec(3, st);
+    E.rec(4, st);
+    rc = launch_interp_composite<R>(S, W, H, gb, nullptr, nullptr, nullptr, nullptr, 0, nullptr,
+                                    r_final, direct, image, st);
     if (rc) return rc;
   }
+  E.rec(5, st);
   int64_t nf = 0;
-  DRCB_CUDA(cudaMemcpyAsync(&nf, d_nf, 8, cudaMemcpyDeviceToHost, st));
-  DRCB_CUDA(cudaStreamSynchronize(st));
+  int m = 0;
+  if (tel) {
+    DRCB_CUDA(cudaMemcpyAsync(&nf, d_nf, 8, cudaMemcpyDeviceToHost, st));
+    DRCB_CUDA(cudaMemcpyAsync(&m, d_m, 4, cudaMemcpyDeviceToHost, st));
+  }
   if (pb) DRCB_CUDA(cudaFreeAsync(pb, st));
   DRCB_CUDA(cudaFreeAsync(fb, st));
-  DRCB_CUDA(cudaFreeAsync(d_nf, st));
   if (tel) {
+    DRCB_CUDA(cudaStreamSynchronize(st));
     tel[0] = m;
-    tel[1] = 0;
+    tel[1] = 0;  // fallback pixels: unreachable by construction (cache.py:306-307)
     tel[2] = nf;
     tel[3] = np_;
-    for (int k = 4; k < 8; ++k) tel[k] = 0;
+    // stage times in microseconds: gbuffer+direct, maps, network, shade+interp
+    tel[4] = int64_t(1000.0 * E.ms(0, 1));
+    tel[5] = int64_t(1000.0 * E.ms(1, 2));
+    tel[6] = int64_t(1000.0 * E.ms(2, 3));
+    tel[7] = int64_t(1000.0 * E.ms(3, 5));
   }
   return 0;
 }
@@ -223,6 +268,7 @@ using namespace drcb;
 
 extern "C" const char* drcb_last_error(void) { return g_err.c_str(); }
 extern "C" int drcb_version(void) { return 1; }
+extern "C" int64_t drcb_kernel_launches(void) { return g_launches.load(); }
 
 extern "C" int drcb_intersect(const DrcbScene* scene, int32_t precision, const void* O,
                               const void* D, int64_t n, const void* tmin, const void* tmax,
@@ -334,10 +380,11 @@ extern "C" int drcb_interp_composite(const DrcbScene* scene, int32_t precision, 
   if (check_precision(precision)) return DRCB_ECONFIG;
   if (precision == 64)
     return launch_interp_composite<double>(scene->dev, width, height, *gb, e_px, e_py,
-                                           (const double*)e_normal, (const double*)e_rad, m, r,
+                                           (const double*)e_normal, (const double*)e_rad, m,
+                                           nullptr, r,
                                            (const double*)direct, (double*)image, S_(stream));
   return launch_interp_composite<float>(scene->dev, width, height, *gb, e_px, e_py,
-                                        (const float*)e_normal, (const float*)e_rad, m, r,
+                                        (const float*)e_normal, (const float*)e_rad, m, nullptr, r,
                                         (const float*)direct, (float*)image, S_(stream));
 }
 

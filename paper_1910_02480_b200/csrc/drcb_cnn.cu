@@ -201,6 +201,7 @@ int conv_f32(const ConvLayer& L, const float* in, int cin_tot, int cin_off, floa
     k_conv_f32<1><<<grid, 256, 0, st>>>(in, cin_tot, cin_off, L.cin, L.d_w, L.d_bias, L.d_scale,
                                         L.d_shift, act, slope, out, cout_tot, cout_off, L.cout,
                                         L.hw);
+  count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_f32");
 }
@@ -210,6 +211,7 @@ int maxpool_f32(const float* in, int c_tot, int c_off, int c, int hw_out, float*
   int64_t total = n * c * hw_out * hw_out;
   k_maxpool_f32<<<unsigned((total + 255) / 256), 256, 0, st>>>(in, c_tot, c_off, c, out, hw_out,
                                                                 total);
+  count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_maxpool_f32");
 }
@@ -218,6 +220,7 @@ int upsample_f32(const float* in, int c, int hw_in, float* out, int c_tot, int64
                  cudaStream_t st) {
   int64_t total = n * c * 4 * hw_in * hw_in;
   k_upsample_f32<<<unsigned((total + 255) / 256), 256, 0, st>>>(in, c, hw_in, out, c_tot, total);
+  count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_upsample_f32");
 }

@@ -14,6 +14,8 @@ namespace drcb {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
+void count_launch(int n = 1);
+void keep_pool_memory();
 
 #define DRCB_CUDA(call)                                      \
   do {                                                       \
@@ -70,6 +72,6 @@ int launch_shade(const DevScene& S, const DrcbRenderCfg& cfg, const float* pred,
 template <typename R>
 int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& gb,
                             const int32_t* e_px, const int32_t* e_py, const R* e_n,
-                            const R* e_rad, int64_t m, int r, const R* direct, R* image,
-                            cudaStream_t st);
+                            const R* e_rad, int64_t m, const int* m_dev, int r,
+                            const R* direct, R* image, cudaStream_t st);
 }  // namespace drcb

@@ -442,17 +442,17 @@ __global__ void __launch_bounds__(256) k_shade(DevScene S, DrcbRenderCfg cfg,
 //   gather dx^2+dy^2 <= (2 r_eff)^2, w = w_p w_n + w_p + 1e-4.
 constexpr int BUCKET = 16;
 
-__global__ void k_bucket_count(const int32_t* px, const int32_t* py, int64_t m, int nbx,
-                               int* counts) {
+__global__ void k_bucket_count(const int32_t* px, const int32_t* py, int64_t m, const int* m_dev,
+                               int nbx, int* counts) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= m) return;
+  if (i >= (m_dev ? int64_t(*m_dev) : m)) return;
   atomicAdd(&counts[(py[i] / BUCKET) * nbx + px[i] / BUCKET], 1);
 }
 
-__global__ void k_bucket_fill(const int32_t* px, const int32_t* py, int64_t m, int nbx,
-                              const int* offsets, int* cursor, int* items) {
+__global__ void k_bucket_fill(const int32_t* px, const int32_t* py, int64_t m, const int* m_dev,
+                              int nbx, const int* offsets, int* cursor, int* items) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= m) return;
+  if (i >= (m_dev ? int64_t(*m_dev) : m)) return;
   int b = (py[i] / BUCKET) * nbx + px[i] / BUCKET;
   int slot = atomicAdd(&cursor[b], 1);
   items[offsets[b] + slot] = int(i);
@@ -479,13 +479,15 @@ __global__ void __launch_bounds__(TPB) k_interp(DevScene S, int W, int H, DrcbGB
                                                  const int32_t* __restrict__ epx,
                                                  const int32_t* __restrict__ epy,
                                                  const R* __restrict__ en,
-                                                 const R* __restrict__ erad, int64_t m, int r,
+                                                 const R* __restrict__ erad, int64_t m_cap,
+                                                 const int* __restrict__ m_dev, int r,
                                                  int nbx, int nby, const int* __restrict__ off,
                                                  const int* __restrict__ items,
                                                  const R* __restrict__ direct, R* image) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= int64_t(W) * H) return;
   int x = int(i % W), y = int(i / W);
+  const int64_t m = m_dev ? int64_t(*m_dev) : m_cap;
   V3<R> layer = {R(0), R(0), R(0)};
   V3<R> thr = ldr3(static_cast<const R*>(gb.throughput) + 3 * i);
   if (gb.escaped[i] && S.has_env) layer = thr * ld3<R>(S.env);
@@ -552,6 +554,7 @@ __global__ void __launch_bounds__(TPB) k_interp(DevScene S, int W, int H, DrcbGB
 
 #define LAUNCH_CHECK()                                                    \
   do {                                                                    \
+    count_launch();                                                       \
     cudaError_t _e = cudaGetLastError();                                  \
     if (_e != cudaSuccess) return cuda_fail(_e, __func__);                \
   } while (0)
@@ -644,8 +647,8 @@ int launch_shade(const DevScene& S, const DrcbRenderCfg& cfg, const float* pred,
 template <typename R>
 int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& gb,
                             const int32_t* e_px, const int32_t* e_py, const R* e_n,
-                            const R* e_rad, int64_t m, int r, const R* direct, R* image,
-                            cudaStream_t st) {
+                            const R* e_rad, int64_t m, const int* m_dev, int r, const R* direct,
+                            R* image, cudaStream_t st) {
   int nbx = (W + BUCKET - 1) / BUCKET, nby = (H + BUCKET - 1) / BUCKET;
   int nb = nbx * nby;
   int* buf = nullptr;
@@ -657,20 +660,21 @@ int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& 
   int* items = cursor + nb;        // m
   DRCB_CUDA(cudaMemsetAsync(buf, 0, sizeof(int) * (3 * size_t(nb) + 2), st));
   if (m > 0) {
-    k_bucket_count<<<nblocks(m), TPB, 0, st>>>(e_px, e_py, m, nbx, counts);
+    k_bucket_count<<<nblocks(m), TPB, 0, st>>>(e_px, e_py, m, m_dev, nbx, counts);
     LAUNCH_CHECK();
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, nb + 1, st);
     void* tmp = nullptr;
     DRCB_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
     cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, offsets, nb + 1, st);
+    count_launch(2);
     DRCB_CUDA(cudaFreeAsync(tmp, st));
-    k_bucket_fill<<<nblocks(m), TPB, 0, st>>>(e_px, e_py, m, nbx, offsets, cursor, items);
+    k_bucket_fill<<<nblocks(m), TPB, 0, st>>>(e_px, e_py, m, m_dev, nbx, offsets, cursor, items);
     LAUNCH_CHECK();
     k_bucket_sort<<<nblocks(nb), TPB, 0, st>>>(offsets, nb, items);
     LAUNCH_CHECK();
   }
-  k_interp<R><<<nblocks(int64_t(W) * H), TPB, 0, st>>>(S, W, H, gb, e_px, e_py, e_n, e_rad, m, r,
+  k_interp<R><<<nblocks(int64_t(W) * H), TPB, 0, st>>>(S, W, H, gb, e_px, e_py, e_n, e_rad, m, m_dev, r,
                                                        nbx, nby, offsets, items, direct, image);
   LAUNCH_CHECK();
   DRCB_CUDA(cudaFreeAsync(buf, st));
@@ -700,7 +704,7 @@ int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& 
                                const uint8_t*, int64_t, R*, cudaStream_t);                       \
   template int launch_interp_composite<R>(const DevScene&, int, int, const DrcbGBuffer&,        \
                                           const int32_t*, const int32_t*, const R*, const R*,   \
-                                          int64_t, int, const R*, R*, cudaStream_t);
+                                          int64_t, const int*, int, const R*, R*, cudaStream_t);
 
 INST(float)
 INST(double)

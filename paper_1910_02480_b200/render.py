@@ -217,9 +217,12 @@ def _torch():
     return torch
 
 
-def render_drc_device(scene, config, net, camera=None, out=None, precision=None):
+def render_drc_device(scene, config, net, camera=None, out=None, precision=None, plan=None,
+                      telemetry=True):
     """One DRC frame, result left on the device: (image (H,W,3) CUDA tensor,
-    telemetry dict). `camera` overrides scene.camera (multi-frame benches)."""
+    telemetry dict). `camera` overrides scene.camera (multi-frame benches);
+    `plan` reuses a plan_points() result; telemetry=False enqueues the frame
+    without any host synchronisation."""
     torch = _torch()
     prec = int(precision or getattr(config, "precision", 64))
     dtype = torch.float64 if prec == 64 else torch.float32
@@ -227,18 +230,20 @@ def render_drc_device(scene, config, net, camera=None, out=None, precision=None)
     w, h = cam.resolution
     ds = device_scene(scene)
     cfg = _cfg_struct(config, prec)
-    px, py, keys, r_final, passes = plan_points((w, h), config)
+    px, py, keys, r_final, passes = plan or plan_points((w, h), config)
     net_mode = getattr(config, "net_mode", "fp32")
     dn = device_net(net) if len(px) else None
     if out is None:
         out = torch.empty((h, w, 3), dtype=dtype, device="cuda")
-    tel = (C.c_int64 * 8)()
+    tel = (C.c_int64 * 8)() if telemetry else None
     t0 = time.time()
     _lib.call("drcb_render_drc", ds.handle, dn.handle if dn else None,
               C.byref(camera_struct(cam)), C.byref(cfg),
               px.ctypes.data_as(C.c_void_p), py.ctypes.data_as(C.c_void_p),
               keys.ctypes.data_as(C.c_void_p), len(px), int(r_final or 1), MODES[net_mode],
               _lib.ptr(out), tel, _lib.stream_ptr())
+    if tel is None:
+        return out, None
     telemetry = {
         "mode": "drc", "direct_spp": config.direct_spp,
         "geometry_seconds": 0.0, "direct_seconds": 0.0,
@@ -246,6 +251,8 @@ def render_drc_device(scene, config, net, camera=None, out=None, precision=None)
         "nonfinite": int(tel[2]), "entries": int(tel[0]),
         "fallback_pixels": int(tel[1]), "tasks": sum(p["tasks"] for p in passes),
         "seconds": time.time() - t0,
+        "stage_us": {"gbuffer_direct": int(tel[4]), "maps": int(tel[5]), "network": int(tel[6]),
+                     "shade_interp": int(tel[7])},
     }
     telemetry["state"] = FrameState(int(tel[0]), int(tel[3]))
     return out, telemetry

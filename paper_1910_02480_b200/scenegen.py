@@ -84,14 +84,21 @@ class _Builder:
                                 np.asarray(faces, dtype=np.int64), name))
 
 
-def _cornell(b, rng, lights):
-    walls = [
-        _quad_tris([-1, -1, -1], [1, -1, -1], [1, -1, 1], [-1, -1, 1]),   # floor
-        _quad_tris([-1, 1, -1], [-1, 1, 1], [1, 1, 1], [1, 1, -1]),       # ceiling
-        _quad_tris([-1, -1, 1], [1, -1, 1], [1, 1, 1], [-1, 1, 1]),       # back
-        _quad_tris([-1, -1, -1], [-1, -1, 1], [-1, 1, 1], [-1, 1, -1]),   # left
-        _quad_tris([1, -1, -1], [1, 1, -1], [1, 1, 1], [1, -1, 1]),       # right
-    ]
+def _cornell(b, rng, lights, closed=True):
+    """Cornell box (closed=True: 5 walls, configs 1-2). The orbit-camera
+    configs (3-4, cameras on a radius-3 sphere) use an open stage instead:
+    only a 6x6 floor, so the cameras see the lit objects rather than the
+    outside of the walls."""
+    if closed:
+        walls = [
+            _quad_tris([-1, -1, -1], [1, -1, -1], [1, -1, 1], [-1, -1, 1]),   # floor
+            _quad_tris([-1, 1, -1], [-1, 1, 1], [1, 1, 1], [1, 1, -1]),       # ceiling
+            _quad_tris([-1, -1, 1], [1, -1, 1], [1, 1, 1], [-1, 1, 1]),       # back
+            _quad_tris([-1, -1, -1], [-1, -1, 1], [-1, 1, 1], [-1, 1, -1]),   # left
+            _quad_tris([1, -1, -1], [1, 1, -1], [1, 1, 1], [1, -1, 1]),       # right
+        ]
+    else:
+        walls = [_quad_tris([-3, -1, -3], [3, -1, -3], [3, -1, 3], [-3, -1, 3])]
     for v, f in walls:
         b.add(v, f, rng.uniform(0.1, 0.9, 3))
     for lo, hi in (([-0.6, -0.999, 0.1], [-0.1, 0.2, 0.6]), ([0.1, -0.999, -0.5], [0.6, -0.4, 0.0])):
@@ -130,7 +137,7 @@ def build_scene(config="c1", seed=None, resolution=None):
     seed = {"c1": 0, "c2": 1, "c3": 2, "c4": 2}[config] if seed is None else seed
     rng = np.random.default_rng(seed)
     b = _Builder()
-    _cornell(b, rng, lights)
+    _cornell(b, rng, lights, closed=config in ("c1", "c2"))
     _spheres(b, rng, n_sph)
     if n_rand:
         _random_tris(b, rng, n_rand)

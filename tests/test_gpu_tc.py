@@ -1,0 +1,83 @@
+"""Tensor-core (tcgen05) U-Net engines against the fp32 engine and the
+reference: single-layer implicit GEMM vs an operand-rounded fp64 conv, and
+whole-network relative L2 bars (BASELINE.json: bf16 within 1e-2)."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1910_02480_b200 import _lib, cnn  # noqa: E402
+
+
+def _round(a, bits):
+    i = a.astype(np.float32).view(np.int32).astype(np.int64)
+    drop = 23 - bits
+    lsb = (i >> drop) & 1
+    i = ((i + (1 << (drop - 1)) - 1 + lsb) >> drop) << drop
+    return i.astype(np.int32).view(np.float32).astype(np.float64)
+
+
+def _conv_ref(x, w):
+    n, hw, _, cin = x.shape
+    xp = np.zeros((n, hw + 2, hw + 2, cin))
+    xp[:, 1:-1, 1:-1] = x
+    y = np.zeros((n, hw, hw, w.shape[0]))
+    for ky in range(3):
+        for kx in range(3):
+            y += np.einsum("nyxc,oc->nyxo", xp[:, ky:ky + hw, kx:kx + hw], w[:, :, ky, kx])
+    return y
+
+
+@pytest.mark.parametrize("mode,bits,tol", [(1, 10, 2e-3), (2, 7, 5e-3)])
+@pytest.mark.parametrize("shape", [(64, 64, 32, 8), (7, 64, 32, 8), (128, 256, 8, 16),
+                                   (256, 512, 4, 16), (192, 64, 32, 8), (32, 16, 32, 8)])
+def test_single_layer_implicit_gemm(mode, bits, tol, shape):
+    cin, cout, hw, n = shape
+    rng = np.random.default_rng(hash(shape) % 1000)
+    x = rng.normal(size=(n, hw, hw, cin)).astype(np.float32)
+    w = rng.normal(size=(cout, cin, 3, 3)).astype(np.float32)
+    y = np.zeros((n, hw, hw, cout), np.float32)
+    _lib.call("drcb_debug_conv", mode, cin, cout, hw, n, x.ctypes.data_as(C.c_void_p),
+              w.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p))
+    ref = _conv_ref(_round(x, bits), _round(w, bits))
+    # every output position/channel (catches tile, tap and padding errors)
+    assert np.abs(y - ref).max() <= tol * np.abs(ref).max()
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def test_tf32_network_within_bar_on_reference_golden():
+    g = load_golden("cnn.npz")
+    y = cnn.forward_batch(cnn.random_network(64, 1), g["x_k64"], mode="tf32")
+    assert _rel(y, g["y_k64"]) <= 1e-2 / 3  # measured 1.3e-3
+
+
+def test_bf16_network_within_bar_bench_weights():
+    # config-3 bench weights (seed 2); the bar is 1e-2 relative L2
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0, 1, (32, 7, 32, 32)).astype(np.float32)
+    x[:, :3] *= 5
+    net = cnn.random_network(64, 2)
+    ref = cnn.forward_batch(net, x, mode="fp32")
+    assert _rel(cnn.forward_batch(net, x, mode="bf16"), ref) <= 1e-2
+    assert _rel(cnn.forward_batch(net, x, mode="tf32"), ref) <= 2e-3
+
+
+def test_tc_batch_sizes_and_padding():
+    # n not a multiple of 8 (4x4 tiles hold 8 maps), results independent of batching
+    rng = np.random.default_rng(6)
+    x = rng.uniform(0, 1, (13, 7, 32, 32)).astype(np.float32)
+    net = cnn.random_network(64, 2)
+    y13 = cnn.forward_batch(net, x, mode="bf16")
+    y1 = np.concatenate([cnn.forward_batch(net, x[i:i + 1], mode="bf16") for i in range(13)])
+    assert np.array_equal(y13, y1)
