@@ -24,7 +24,7 @@ void keep_pool_memory();
   } while (0)
 
 struct SceneStats {
-  int64_t n_prims = 0, n_nodes = 0, n_leaves = 0, max_depth = 0, n_lights = 0, bytes = 0;
+  int64_t n_prims = 0, n_nodes = 0, n_leaves = 0, max_depth = 0, n_lights = 0, bytes = 0, n_refs = 0;
 };
 
 }  // namespace drcb

@@ -146,47 +146,150 @@ __global__ void __launch_bounds__(TPB) k_gbuffer_direct(DevScene S, DevCamera C,
   if (nonfinite) add_nonfinite(nonfinite, nf);
 }
 
-// One thread per texel path of one cache point (hemimap.py:236-262). The
-// reference casts the first map ray twice (line 250 and segment 0 of
-// trace_radiance_batch); it is cast once here and reused.
+// Map paths of all cache points (hemimap.py:236-262 + integrators.py:175-302)
+// as a persistent kernel with per-lane path regeneration: a lane whose path
+// terminates (escape, RR, max depth) immediately takes the next texel from a
+// global counter, so warps stay full instead of idling behind the longest
+// path of the warp. The segment-0 cast doubles as the first-hit feature cast
+// (the reference casts it twice, hemimap.py:250 and segment 0).
+constexpr int MAP_TPB = 256;
+
 template <typename R>
-__global__ void __launch_bounds__(TPB) k_map_rays(DevScene S, DrcbRenderCfg cfg,
-                                                   const R* __restrict__ pos,
-                                                   const R* __restrict__ nrm,
-                                                   const uint64_t* __restrict__ keys,
-                                                   const uint8_t* __restrict__ live, int64_t n,
-                                                   R* rad, R* dist, R* nloc, R* frames,
-                                                   int64_t* nonfinite) {
-  int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  int64_t p = g / MAP_TEXELS;
-  int tex = int(g % MAP_TEXELS);
+__global__ void __launch_bounds__(MAP_TPB, 3) k_map_paths(DevScene S, DrcbRenderCfg cfg,
+                                                          const R* __restrict__ pos,
+                                                          const R* __restrict__ nrm,
+                                                          const uint64_t* __restrict__ keys,
+                                                          const uint8_t* __restrict__ live,
+                                                          int64_t total, unsigned long long* counter,
+                                                          R* rad, R* dist, R* nloc,
+                                                          int64_t* nonfinite) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  bool have = false, done_all = false;
+  int64_t job = 0;
+  int seg = 0;
+  bool prev_delta = true;
+  R prev_pdf = R(0);
+  V3<R> O, D, beta, L;
+  PathRng rng;
   int nf = 0;
-  if (p < n && (!live || live[p])) {
-    V3<R> hp = ldr3(pos + 3 * p), hn = ldr3(nrm + 3 * p);
-    Frame<R> fr = frame_scalar(S, hn);
-    if (tex == 0) {
-      R* f = frames + 9 * p;
-      st3(f, fr.t);
-      st3(f + 3, fr.b);
-      st3(f + 6, fr.n);
+  const V3<R> env = ld3<R>(S.env);
+  while (true) {
+    bool need = !have && !done_all;
+    unsigned m = __ballot_sync(FULL, need);
+    bool fresh = false;
+    if (m) {
+      int leader = __ffs(m) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
+      base = __shfl_sync(FULL, base, leader);
+      if (need) {
+        job = int64_t(base) + __popc(m & ((1u << lane) - 1u));
+        if (job >= total) {
+          done_all = true;
+        } else if (!live || live[job / MAP_TEXELS]) {
+          have = true;
+          fresh = true;
+        }
+      }
     }
-    int u = tex % MAP_RES, v = tex / MAP_RES;
-    V3<R> dir = fr.to_world(texel_local<R>(u, v));
-    V3<R> o = hp + R(T_EPS) * hn;
-    SurfHit<R> first = intersect(S, o, dir);
-    R d = first.hit ? first.t : R(0);
-    bool facing = dot(first.normal, dir) > R(0);
-    V3<R> nf3 = facing ? -first.normal : first.normal;
-    V3<R> nl = first.hit ? fr.to_local(nf3) : mk<R>(R(0), R(0), R(0));
-    PathRng rng;
-    rng.init(cfg.seed, keys[p], uint64_t(tex), cfg.sampler_kind, 1u);
-    V3<R> L = trace_path<R>(S, o, dir, rng, cfg.max_path_depth, true, cfg.rr_start, &first, nf);
-    int64_t q = p * MAP_TEXELS + tex;
-    st3(rad + 3 * q, L);
-    dist[q] = d;
-    st3(nloc + 3 * q, nl);
+    if (__all_sync(FULL, !have && done_all)) break;
+    if (!have) continue;
+    bool skip = false;
+    int64_t p = 0;
+    int tex = 0;
+    if (fresh) {
+      p = job / MAP_TEXELS;
+      tex = int(job % MAP_TEXELS);
+      V3<R> hp = ldr3(pos + 3 * p), hn = ldr3(nrm + 3 * p);
+      Frame<R> fr = frame_scalar(S, hn);
+      D = fr.to_world(texel_local<R>(tex % MAP_RES, tex / MAP_RES));
+      O = hp + R(T_EPS) * hn;
+    }
+    // single traversal call site for fresh and continuing lanes
+    SurfHit<R> h = intersect(S, O, D);
+    if (fresh) {
+      // first-hit features: distance and front-facing normal in the map frame
+      Frame<R> fr = frame_scalar(S, ldr3(nrm + 3 * p));
+      bool facing = dot(h.normal, D) > R(0);
+      V3<R> nf3 = facing ? -h.normal : h.normal;
+      dist[job] = h.hit ? h.t : R(0);
+      st3(nloc + 3 * job, h.hit ? fr.to_local(nf3) : mk<R>(R(0), R(0), R(0)));
+      rng.init(cfg.seed, keys[p], uint64_t(tex), cfg.sampler_kind, 1u);
+      L = mk<R>(R(0), R(0), R(0));
+      beta = mk<R>(R(1), R(1), R(1));
+      seg = 0;
+      prev_pdf = R(0);
+      prev_delta = true;
+      skip = true;  // skip_first_emission at segment 0
+    }
+    // ---- one segment of trace_radiance_batch
+    bool end = false;
+    if (!h.hit) {
+      if (S.has_env && !skip) L = L + beta * env;
+      end = true;
+    } else {
+      const int mat = h.mat;
+      const bool facing = dot(h.normal, D) < R(0);
+      if (S.mat_emitter[mat] && facing && !skip) {
+        R w = R(1);
+        if (seg > 0 && !prev_delta) {
+          R pdf_nee = nee_pdf_for_hit(S, h.prim, h.t, -dot(h.normal, D));
+          w = power_heuristic(prev_pdf, pdf_nee);
+        }
+        L = L + (beta * ld3<R>(S.mat_emis + 3 * mat)) * mk<R>(w, w, w);
+      }
+      if (seg == cfg.max_path_depth) {
+        end = true;
+      } else {
+        V3<R> n_front = facing ? h.normal : -h.normal;
+        Frame<R> fr = frame_batch(S, n_front);
+        V3<R> wo_local = fr.to_local(-D);
+        uint64_t base = 2 + 8 * (uint64_t)seg;
+        if (S.n_lights > 0 && !S.mat_spec[mat])
+          L = L + beta * nee(S, rng, base, h.pos, n_front, fr, mat, wo_local);
+        R u1 = sample_dim<R>(rng, base + 3), u2 = sample_dim<R>(rng, base + 4);
+        BsdfSample<R> bs = bsdf_sample(S, mat, wo_local, u1, u2, facing);
+        R cos_i = fabs(bs.li.z);
+        R k = cos_i / bs.pdf;
+        beta = beta * (bs.spec ? bs.value : bs.value * mk<R>(k, k, k));
+        R side = bs.li.z >= R(0) ? R(1) : R(-1);
+        O = h.pos + (R(T_EPS) * side) * n_front;
+        D = fr.to_world(bs.li);
+        prev_pdf = bs.pdf;
+        prev_delta = bs.spec;
+        bool alive = any_pos(beta) && all_finite(beta);
+        if (seg + 1 >= cfg.rr_start) {
+          R q = fmin(fmax(maxc(beta), R(RR_FLOOR)), R(1));
+          bool survive = sample_dim<R>(rng, base + 5) < q;
+          beta = divs(beta, q);
+          alive = alive && survive;
+        }
+        ++seg;
+        end = !alive;
+      }
+    }
+    if (end) {
+      if (!all_finite(L)) {
+        L = mk<R>(R(0), R(0), R(0));
+        ++nf;
+      }
+      st3(rad + 3 * job, L);
+      have = false;
+    }
   }
   if (nonfinite) add_nonfinite(nonfinite, nf);
+}
+
+// cache-point frames (build_frame of the front normal, hemimap.py:238)
+template <typename R>
+__global__ void k_point_frames(DevScene S, const R* __restrict__ nrm, int64_t n, R* frames) {
+  int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  Frame<R> fr = frame_scalar(S, ldr3(nrm + 3 * p));
+  st3(frames + 9 * p, fr.t);
+  st3(frames + 9 * p + 3, fr.b);
+  st3(frames + 9 * p + 6, fr.n);
 }
 
 // numpy pairwise summation of 1024 contiguous values (8-accumulator blocks of
@@ -619,12 +722,25 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
   if (n <= 0) return 0;
   size_t per = size_t(n) * MAP_TEXELS;
   R* scratch = nullptr;
-  DRCB_CUDA(cudaMallocAsync((void**)&scratch, per * 7 * sizeof(R), st));
+  DRCB_CUDA(cudaMallocAsync((void**)&scratch, per * 7 * sizeof(R) + 64, st));
   R* rad = scratch;
   R* dist = scratch + 3 * per;
   R* nloc = scratch + 4 * per;
-  k_map_rays<R><<<nblocks(int64_t(per)), TPB, 0, st>>>(S, cfg, pos, nrm, keys, live, n, rad, dist,
-                                                         nloc, frames, nonfinite);
+  unsigned long long* counter = reinterpret_cast<unsigned long long*>(scratch + 7 * per);
+  DRCB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+  k_point_frames<R><<<nblocks(n), TPB, 0, st>>>(S, nrm, n, frames);
+  LAUNCH_CHECK();
+  static int grid = 0;
+  if (!grid) {
+    int nsm = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_paths<R>, MAP_TPB, 0);
+    grid = nsm * (per_sm > 0 ? per_sm : 1);
+  }
+  int64_t total = int64_t(per);
+  int g = int(std::min<int64_t>(grid, (total + MAP_TPB - 1) / MAP_TPB));
+  k_map_paths<R><<<g, MAP_TPB, 0, st>>>(S, cfg, pos, nrm, keys, live, total, counter, rad, dist,
+                                         nloc, nonfinite);
   LAUNCH_CHECK();
   k_stack_normalize<R><<<int(n), 256, 0, st>>>(rad, dist, nloc, live, n, stacks, s_r, s_d);
   LAUNCH_CHECK();
@@ -710,3 +826,9 @@ INST(float)
 INST(double)
 
 }  // namespace drcb
+
+// arm (buf != NULL, 3 x u64 device counters) or disarm the traversal counters
+extern "C" int drcb_trav_stats(unsigned long long* buf) {
+  cudaError_t e = cudaMemcpyToSymbol(drcb::g_trav_stats, &buf, sizeof(buf));
+  return e == cudaSuccess ? 0 : drcb::cuda_fail(e, "drcb_trav_stats");
+}

@@ -7,6 +7,7 @@
 // leaf order as 48 B fp32 records (v0+id, e1, e2) and 72 B fp64 records so a
 // leaf's triangles are contiguous in memory.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -45,8 +46,9 @@ struct BuildNode {
 };
 
 struct Builder {
-  const std::vector<Box>& pb;
-  std::vector<double> cen;  // 3 per prim
+  const std::vector<Box>& pb;   // one box per reference
+  const std::vector<int>& ref_prim;  // reference -> prim id
+  std::vector<double> cen;  // 3 per reference
   std::vector<int> ids;
   std::vector<BuildNode> nodes;
   std::vector<int> order;  // leaf slots -> prim id
@@ -56,7 +58,7 @@ struct Builder {
   static constexpr int LEAF = 4;
   static constexpr int DEPTH_LIMIT = 56;
 
-  explicit Builder(const std::vector<Box>& b) : pb(b) {
+  Builder(const std::vector<Box>& b, const std::vector<int>& rp) : pb(b), ref_prim(rp) {
     cen.resize(3 * pb.size());
     for (size_t i = 0; i < pb.size(); ++i)
       for (int k = 0; k < 3; ++k) cen[3 * i + k] = 0.5 * (pb[i].lo[k] + pb[i].hi[k]);
@@ -72,7 +74,7 @@ struct Builder {
 
   int make_leaf(int b, int e) {
     int start = (int)order.size();
-    for (int i = b; i < e; ++i) order.push_back(ids[i]);
+    for (int i = b; i < e; ++i) order.push_back(ref_prim[ids[i]]);
     ++n_leaves;
     return ~((start << 3) | (e - b - 1));
   }
@@ -209,6 +211,90 @@ int upload(DrcbScene* s, const std::vector<T>& v, const T** out) {
   DRCB_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
   *out = static_cast<const T*>(p);
   return 0;
+}
+
+// Sutherland-Hodgman clip of a convex polygon to x[axis] <= pos (keep_le)
+// or >= pos
+void clip_poly(const std::vector<std::array<double, 3>>& in, int axis, double pos, bool keep_le,
+               std::vector<std::array<double, 3>>& out) {
+  out.clear();
+  size_t n = in.size();
+  for (size_t i = 0; i < n; ++i) {
+    const auto& a = in[i];
+    const auto& b = in[(i + 1) % n];
+    double da = keep_le ? pos - a[axis] : a[axis] - pos;
+    double db = keep_le ? pos - b[axis] : b[axis] - pos;
+    if (da >= 0) out.push_back(a);
+    if ((da >= 0) != (db >= 0)) {
+      double t = da / (da - db);
+      std::array<double, 3> c;
+      for (int k = 0; k < 3; ++k) c[k] = a[k] + t * (b[k] - a[k]);
+      c[axis] = pos;
+      out.push_back(c);
+    }
+  }
+}
+
+void split_rec(const std::vector<std::array<double, 3>>& poly, const Box& box, double target,
+               int depth, int prim, std::vector<Box>& rb, std::vector<int>& rp) {
+  int ax = 0;
+  double ext[3];
+  for (int k = 0; k < 3; ++k) ext[k] = box.hi[k] - box.lo[k];
+  for (int k = 1; k < 3; ++k)
+    if (ext[k] > ext[ax]) ax = k;
+  if (ext[ax] <= target || depth >= 7 || poly.size() < 3) {
+    rb.push_back(box);
+    rp.push_back(prim);
+    return;
+  }
+  double mid = 0.5 * (box.lo[ax] + box.hi[ax]);
+  std::vector<std::array<double, 3>> half;
+  for (int side = 0; side < 2; ++side) {
+    clip_poly(poly, ax, mid, side == 0, half);
+    if (half.size() < 3) continue;
+    Box hb;
+    for (const auto& v : half) hb.grow_pt(v.data());
+    // never let rounding shrink a piece outside the parent box
+    for (int k = 0; k < 3; ++k) {
+      hb.lo[k] = std::max(hb.lo[k], box.lo[k]);
+      hb.hi[k] = std::min(hb.hi[k], box.hi[k]);
+    }
+    split_rec(half, hb, target, depth + 1, prim, rb, rp);
+  }
+}
+
+void split_references(const std::vector<Box>& pb, const std::vector<double>& tri, int ns, int nq,
+                      int nt, std::vector<Box>& rb, std::vector<int>& rp) {
+  const int np = int(pb.size());
+  rb.reserve(np);
+  rp.reserve(np);
+  std::vector<double> ext(np);
+  for (int p = 0; p < np; ++p) {
+    double e = 0;
+    for (int k = 0; k < 3; ++k) e = std::max(e, pb[p].hi[k] - pb[p].lo[k]);
+    ext[p] = e;
+  }
+  double target = INFINITY;
+  if (nt >= 1024) {
+    std::vector<double> te(ext.begin() + ns + nq, ext.end());
+    std::nth_element(te.begin(), te.begin() + te.size() / 2, te.end());
+    target = 4.0 * te[te.size() / 2];
+  }
+  for (int p = 0; p < np; ++p) {
+    if (p < ns + nq || !(ext[p] > target)) {
+      rb.push_back(pb[p]);
+      rp.push_back(p);
+      continue;
+    }
+    const double* t = &tri[13 * (p - ns - nq)];
+    std::vector<std::array<double, 3>> poly(3);
+    for (int k = 0; k < 3; ++k) {
+      poly[0][k] = t[k];
+      poly[1][k] = t[k] + t[3 + k];
+      poly[2][k] = t[k] + t[6 + k];
+    }
+    split_rec(poly, pb[p], target, 0, p, rb, rp);
+  }
 }
 
 inline void cross3(const double* a, const double* b, double* o) {
@@ -357,10 +443,19 @@ extern "C" int drcb_scene_create(const DrcbSceneDesc* desc, DrcbScene** out) {
   D.n_area = (int)area_prim.size();
   D.n_lights = npl + D.n_area;
 
-  // --- BVH
-  Builder B(pb);
+  // --- BVH over primitive references. Early split clipping (Ernst &
+  // Greiner 2007): primitives whose box is much larger than the typical one
+  // (config 3/4's random triangles span the scene) are recursively cut at the
+  // mid-plane of their box's longest axis, the triangle is clipped to each
+  // half and each piece's tight box becomes a reference to the SAME prim.
+  // Duplicate references cannot change the result (same t, same id).
+  std::vector<Box> rb;
+  std::vector<int> rp;
+  split_references(pb, tri, ns, nq, nt, rb, rp);
+  Builder B(rb, rp);
   B.run();
   s->stats.n_prims = D.n_prims;
+  s->stats.n_refs = (int64_t)rb.size();
   s->stats.n_nodes = (int64_t)B.nodes.size();
   s->stats.n_leaves = B.n_leaves;
   s->stats.max_depth = B.max_depth;
@@ -481,7 +576,7 @@ extern "C" int drcb_scene_stats(const DrcbScene* s, int64_t* out) {
   out[3] = s->stats.max_depth;
   out[4] = s->stats.n_lights;
   out[5] = s->stats.bytes;
-  out[6] = 0;
+  out[6] = s->stats.n_refs;
   out[7] = 0;
   return 0;
 }

@@ -106,10 +106,61 @@ __device__ __forceinline__ bool improves(R t, int prim, R best_t, int best_prim)
 
 constexpr int TRAV_STACK = 64;
 
+// traversal counters (nodes visited, primitives tested, casts) for the
+// roofline's algorithmic-bytes figure; flushed only when a counting run
+// armed g_trav_stats (drcb_trav_stats), one predicated branch per cast.
+__device__ unsigned long long* g_trav_stats = nullptr;
+
 __device__ __forceinline__ float f_ru(double x) { return __double2float_ru(x); }
 __device__ __forceinline__ float f_ru(float x) { return x; }
 
+constexpr int TRAV_SENTINEL = 0x76543210;
+
+// leaf primitives tests; returns true on an any-hit termination
+template <typename R, bool ANY>
+__device__ __forceinline__ bool test_leaf(const DevScene& S, int leaf, V3<R> O, V3<R> D, R tmin,
+                                          R tmax, HitRec<R>& best, float& tbest,
+                                          unsigned& n_prims) {
+  constexpr float ROB = 1.0f + 4.0f * 5.97e-8f;
+  int code = ~leaf;
+  int start = code >> 3, count = (code & 7) + 1;
+  n_prims += count;
+  for (int s = start; s < start + count; ++s) {
+    V3<R> v0, e1, e2;
+    int id;
+    leaf_tri<R>(S, s, v0, e1, e2, id);
+    R t;
+    bool ok;
+    R bound = ANY ? tmax : best.t;
+    if (id >= S.n_s + S.n_q) {
+      ok = tri_t(v0, e1, e2, O, D, tmin, bound, t);
+    } else if (id >= S.n_s) {
+      ok = quad_t(S, id - S.n_s, O, D, tmin, bound, t);
+    } else {
+      ok = sphere_t(S, id, O, D, tmin, bound, t);
+    }
+    if (ok) {
+      if (ANY) {
+        best.t = t;
+        best.prim = id;
+        return true;
+      }
+      if (improves(t, id, best.t, best.prim)) {
+        best.t = t;
+        best.prim = id;
+        tbest = f_ru(t) * ROB;
+      }
+    }
+  }
+  return false;
+}
+
 // Closest hit (ANY=false) or any hit in (tmin, tmax] (ANY=true) over the BVH.
+// "While-while" traversal with speculative leaf postponement (Aila & Laine
+// 2009): lanes descend inner nodes until every active lane of the warp holds
+// a postponed leaf, then all lanes test leaves together, so inner-node and
+// leaf code do not alternate lane by lane. Result is traversal-order
+// independent (nearest t, ties -> lowest prim id).
 template <typename R, bool ANY>
 __device__ HitRec<R> traverse(const DevScene& S, V3<R> O, V3<R> D, R tmin, R tmax) {
   HitRec<R> best{tmax, -1};
@@ -125,75 +176,68 @@ __device__ HitRec<R> traverse(const DevScene& S, V3<R> O, V3<R> D, R tmin, R tma
   constexpr float ROB = 1.0f + 4.0f * 5.97e-8f;  // conservative slab (2*gamma(3))
   int stack[TRAV_STACK];
   int sp = 0;
+  stack[0] = TRAV_SENTINEL;
   int node = 0;
+  int leaf = 0;  // >= 0: no postponed leaf
+  unsigned n_nodes = 0, n_prims = 0;
   float tbest = isinf(float(tmax)) ? INFINITY : f_ru(tmax) * ROB;
-  while (true) {
-    if (node >= 0) {
+  while (node != TRAV_SENTINEL) {
+    // inner nodes until all lanes have a postponed leaf
+    while (unsigned(node) < unsigned(TRAV_SENTINEL)) {
+      ++n_nodes;
       const float4* nd = S.nodes + 4 * node;
       float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2), d = __ldg(nd + 3);
-      // child 0
       float tx0 = a.x * ix - oix, tx1 = a.y * ix - oix;
       float ty0 = a.z * iy - oiy, ty1 = a.w * iy - oiy;
       float tz0 = c.x * iz - oiz, tz1 = c.y * iz - oiz;
       float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
-      float f0 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fmaxf(tz0, tz1)) * ROB;
-      f0 = fminf(f0, tbest);
-      // child 1
+      float f0 = fminf(fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fmaxf(tz0, tz1)) * ROB, tbest);
       float sx0 = b.x * ix - oix, sx1 = b.y * ix - oix;
       float sy0 = b.z * iy - oiy, sy1 = b.w * iy - oiy;
       float sz0 = c.z * iz - oiz, sz1 = c.w * iz - oiz;
       float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), 0.0f));
-      float f1 = fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fmaxf(sz0, sz1)) * ROB;
-      f1 = fminf(f1, tbest);
+      float f1 = fminf(fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fmaxf(sz0, sz1)) * ROB, tbest);
       bool h0 = n0 <= f0, h1 = n1 <= f1;
       int c0 = __float_as_int(d.x), c1 = __float_as_int(d.y);
-      if (h0 && h1) {
-        int nearc = c0, farc = c1;
-        if (n1 < n0) { nearc = c1; farc = c0; }
-        if (sp < TRAV_STACK) stack[sp++] = farc;
-        node = nearc;
-      } else if (h0) {
-        node = c0;
-      } else if (h1) {
-        node = c1;
+      if (!h0 && !h1) {
+        node = stack[sp--];
       } else {
-        if (sp == 0) break;
-        node = stack[--sp];
-      }
-      continue;
-    }
-    // leaf
-    int code = ~node;
-    int start = code >> 3, count = (code & 7) + 1;
-    for (int s = start; s < start + count; ++s) {
-      V3<R> v0, e1, e2;
-      int id;
-      leaf_tri<R>(S, s, v0, e1, e2, id);
-      R t;
-      bool ok;
-      R bound = ANY ? tmax : best.t;
-      if (id >= S.n_s + S.n_q) {
-        ok = tri_t(v0, e1, e2, O, D, tmin, bound, t);
-      } else if (id >= S.n_s) {
-        ok = quad_t(S, id - S.n_s, O, D, tmin, bound, t);
-      } else {
-        ok = sphere_t(S, id, O, D, tmin, bound, t);
-      }
-      if (ok) {
-        if (ANY) {
-          best.t = t;
-          best.prim = id;
-          return best;
-        }
-        if (improves(t, id, best.t, best.prim)) {
-          best.t = t;
-          best.prim = id;
-          tbest = f_ru(t) * ROB;
+        node = h0 ? c0 : c1;
+        if (h0 && h1) {
+          int other = c1;
+          if (n1 < n0) {
+            node = c1;
+            other = c0;
+          }
+          if (sp + 1 < TRAV_STACK) stack[++sp] = other;
         }
       }
+      if (node < 0 && leaf >= 0) {  // first leaf: postpone, keep descending
+        leaf = node;
+        node = stack[sp--];
+      }
+      if (!__any_sync(__activemask(), leaf >= 0)) break;
     }
-    if (sp == 0) break;
-    node = stack[--sp];
+    // postponed leaves
+    while (leaf < 0) {
+      if (test_leaf<R, ANY>(S, leaf, O, D, tmin, tmax, best, tbest, n_prims)) {
+        node = TRAV_SENTINEL;
+        leaf = 0;
+        break;
+      }
+      leaf = node;
+      if (node < 0) node = stack[sp--];
+    }
+  }
+  if (g_trav_stats) {
+    atomicAdd(g_trav_stats + 0, n_nodes);
+    atomicAdd(g_trav_stats + 1, n_prims);
+    atomicAdd(g_trav_stats + 2, 1ull);
+    atomicMax(g_trav_stats + 3, (unsigned long long)n_nodes);
+    atomicMax(g_trav_stats + 4, (unsigned long long)n_prims);
+    // histogram of prims tested: [0,8) [8,32) [32,128) [128,512) [512,inf)
+    int b = n_prims < 8 ? 0 : n_prims < 32 ? 1 : n_prims < 128 ? 2 : n_prims < 512 ? 3 : 4;
+    atomicAdd(g_trav_stats + 5 + b, 1ull);
   }
   return best;
 }

@@ -378,7 +378,7 @@ class DeviceScene:
     def stats(self):
         out = (C.c_int64 * 8)()
         _lib.call("drcb_scene_stats", self.handle, out)
-        keys = ("n_prims", "n_nodes", "n_leaves", "max_depth", "n_lights", "bytes")
+        keys = ("n_prims", "n_nodes", "n_leaves", "max_depth", "n_lights", "bytes", "n_refs")
         return {k: int(out[i]) for i, k in enumerate(keys)}
 
     def close(self):
