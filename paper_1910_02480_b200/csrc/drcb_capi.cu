@@ -25,6 +25,9 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 int forward_f32(const NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t st);
 int forward_tc(NetImpl& net, const float* x, float* y, int64_t n, int mode, cudaStream_t st);
+int forward_tc_nhwc(NetImpl& net, const void* x_nhwc, float* y, int64_t n, int mode,
+                    cudaStream_t st);
+int tc_input_channels(int mode);
 
 int forward_f32_chunked(const NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t st) {
   for (int64_t done = 0; done < n;) {
@@ -199,14 +202,29 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
     int nb = int((np_ + 127) / 128);
     k_gather_points<R><<<nb, 128, 0, st>>>(gb, W, px, py, np_, pos, nrm, wo, mat, live);
     count_launch();
-    rc = launch_render_stacks<R>(S, *cfg, pos, nrm, keys, live, np_, stacks, s_r, s_d, frames,
-                                 d_nf, st);
+    const bool tc = net_mode != DRCB_NET_FP32;
+    const int64_t np8 = ((np_ + 7) / 8) * 8;
+    void* xin = nullptr;
+    int cpad = tc ? tc_input_channels(net_mode) : 0;
+    if (tc && np_ <= 8192) {
+      size_t xb = size_t(np8) * 1024 * cpad * (net_mode == DRCB_NET_BF16 ? 2 : 4);
+      DRCB_CUDA(cudaMallocAsync(&xin, xb, st));
+      if (np8 > np_)
+        DRCB_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(xin) + xb / np8 * np_, 0,
+                                  xb / np8 * (np8 - np_), st));
+    }
+    rc = launch_render_stacks<R>(S, *cfg, pos, nrm, keys, live, np_, xin ? nullptr : stacks, s_r,
+                                 s_d, frames, d_nf, st, xin,
+                                 xin ? (net_mode == DRCB_NET_BF16 ? 1 : 2) : 0, cpad);
     if (rc) return rc;
     E.rec(2, st);
-    if (net_mode == DRCB_NET_FP32)
+    if (!tc)
       rc = forward_f32_chunked(net->impl, stacks, pred, np_, st);
+    else if (xin)
+      rc = forward_tc_nhwc(net->impl, xin, pred, np_, net_mode, st);
     else
       rc = forward_tc(net->impl, stacks, pred, np_, net_mode, st);
+    if (xin) DRCB_CUDA(cudaFreeAsync(xin, st));
     if (rc) return rc;
     E.rec(3, st);
     rc = launch_shade<R>(S, *cfg, pred, s_r, frames, wo, mat, keys, live, np_, Le, st);

@@ -471,77 +471,144 @@ __global__ void k_stack_to_nhwc(const float* __restrict__ x, int64_t n, int64_t 
   for (int g = 0; g < cpad / V; ++g) o[g] = (g * V < 8) ? pack<T>(f + g * V) : z;
 }
 
-// 2x2 max-pool of channel slice [off, off+c) of an NHWC buffer
-// (cnn.py:152-156); one thread per (output pixel, 16-byte channel group)
-template <typename T>
-__global__ void k_pool_nhwc(const T* __restrict__ in, int c_tot, int off, int c, int hw_out,
-                            int64_t total, T* __restrict__ out) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// 2x2 max-pool of channel slice [off, off+C) of an NHWC buffer
+// (cnn.py:152-156); compile-time shapes, one thread per (output pixel,
+// 4 x 16 B channel groups)
+template <typename T, int HW_OUT, int C>
+__global__ void __launch_bounds__(256) k_pool_nhwc(const T* __restrict__ in, int c_tot, int off,
+                                                   T* __restrict__ out, int64_t nmaps) {
   constexpr int V = Vec<T>::N;
-  const int groups = c / V;
-  if (i >= total / V) return;
-  int g = int(i % groups);
-  int64_t px = i / groups;  // (n, y, x) over the output
-  int x = int(px % hw_out);
-  int64_t r = px / hw_out;
-  int y = int(r % hw_out);
-  int64_t n = r / hw_out;
-  int hi = 2 * hw_out;
-  const T* p = in + ((n * hi + 2 * y) * hi + 2 * x) * c_tot + off + g * V;
-  float a[V], b[V], cc[V], d[V], m[V];
-  unpack<T>(*reinterpret_cast<const uint4*>(p), a);
-  unpack<T>(*reinterpret_cast<const uint4*>(p + c_tot), b);
-  unpack<T>(*reinterpret_cast<const uint4*>(p + hi * c_tot), cc);
-  unpack<T>(*reinterpret_cast<const uint4*>(p + (hi + 1) * c_tot), d);
+  constexpr int G = C / V;          // 16 B groups per pixel
+  constexpr int GPT = G >= 4 ? 4 : G;  // groups per thread
+  constexpr int TPP = G / GPT;       // threads per pixel
+  constexpr int HI = 2 * HW_OUT;
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nmaps * HW_OUT * HW_OUT * TPP) return;
+  const int gq = int(i % TPP);
+  const int64_t px = i / TPP;
+  const int x = int(px % HW_OUT), y = int((px / HW_OUT) % HW_OUT);
+  const int64_t n = px / (HW_OUT * HW_OUT);
+  const T* p = in + ((n * HI + 2 * y) * HI + 2 * x) * c_tot + off;
+  T* o = out + px * C;
 #pragma unroll
-  for (int j = 0; j < V; ++j) m[j] = fmaxf(fmaxf(a[j], b[j]), fmaxf(cc[j], d[j]));
-  *reinterpret_cast<uint4*>(out + px * c + g * V) = pack<T>(m);
+  for (int k = 0; k < GPT; ++k) {
+    const int g = gq * GPT + k;
+    float a[V], b[V], cc[V], d[V], m[V];
+    unpack<T>(__ldg(reinterpret_cast<const uint4*>(p + g * V)), a);
+    unpack<T>(__ldg(reinterpret_cast<const uint4*>(p + c_tot + g * V)), b);
+    unpack<T>(__ldg(reinterpret_cast<const uint4*>(p + HI * c_tot + g * V)), cc);
+    unpack<T>(__ldg(reinterpret_cast<const uint4*>(p + (HI + 1) * c_tot + g * V)), d);
+#pragma unroll
+    for (int j = 0; j < V; ++j) m[j] = fmaxf(fmaxf(a[j], b[j]), fmaxf(cc[j], d[j]));
+    *reinterpret_cast<uint4*>(o + g * V) = pack<T>(m);
+  }
 }
 
+// src = max((o + 0.5)/2 - 0.5, 0) in closed form (no int<->float
+// conversions on the XU pipe): o = 0 -> (0, 1, 0); o = 2i (i >= 1) ->
+// (i-1, i, 0.75); o = 2i+1 -> (i, min(i+1, n-1), 0.25)
 __device__ __forceinline__ void up_w(int o, int n, int& i0, int& i1, float& fr) {
-  // src = max((o + 0.5)/2 - 0.5, 0) is exact in fp32 for these sizes
-  float src = fmaxf((float(o) + 0.5f) * 0.5f - 0.5f, 0.f);
-  int a = int(src);
-  i0 = a < n - 1 ? a : n - 1;
-  i1 = i0 + 1 < n - 1 ? i0 + 1 : n - 1;
-  fr = src - float(i0);
+  const int i = o >> 1;
+  if (o & 1) {
+    i0 = i;
+    i1 = min(i + 1, n - 1);
+    fr = 0.25f;
+  } else if (o == 0) {
+    i0 = 0;
+    i1 = min(1, n - 1);
+    fr = 0.f;
+  } else {
+    i0 = i - 1;
+    i1 = i;
+    fr = 0.75f;
+  }
 }
 
-// bilinear 2x (align_corners=False) of an NHWC buffer (c channels) into the
-// leading channel slice of the decoder concat buffer (cnn.py:159-174),
-// rows then columns like the reference; one thread per (pixel, 16 B group)
-template <typename T>
-__global__ void k_up_nhwc(const T* __restrict__ in, int c, int hw_in, T* __restrict__ out,
-                          int c_tot, int64_t total) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// bilinear 2x (align_corners=False) of an NHWC buffer (C channels) into the
+// leading channel slice of the decoder concat buffer (cnn.py:159-174), rows
+// then columns like the reference; compile-time shapes, one thread per
+// (output pixel, 4 x 16 B channel groups)
+template <typename T, int HW_IN, int C>
+__global__ void __launch_bounds__(256) k_up_nhwc(const T* __restrict__ in, T* __restrict__ out,
+                                                 int c_tot, int64_t nmaps) {
   constexpr int V = Vec<T>::N;
-  const int groups = c / V;
-  if (i >= total / V) return;
-  int g = int(i % groups);
-  int64_t px = i / groups;
-  int ho = 2 * hw_in;
-  int x = int(px % ho);
-  int64_t r = px / ho;
-  int y = int(r % ho);
-  int64_t n = r / ho;
+  constexpr int G = C / V;
+  constexpr int GPT = G >= 4 ? 4 : G;
+  constexpr int TPP = G / GPT;
+  constexpr int HO = 2 * HW_IN;
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nmaps * HO * HO * TPP) return;
+  const int gq = int(i % TPP);
+  const int64_t px = i / TPP;
+  const int x = int(px % HO), y = int((px / HO) % HO);
+  const int64_t n = px / (HO * HO);
   int r0, r1, c0, c1;
   float fr, fc;
-  up_w(y, hw_in, r0, r1, fr);
-  up_w(x, hw_in, c0, c1, fc);
-  const T* b = in + n * hw_in * hw_in * c + g * V;
-  float p00[V], p10[V], p01[V], p11[V], o[V];
-  unpack<T>(*reinterpret_cast<const uint4*>(b + (r0 * hw_in + c0) * c), p00);
-  unpack<T>(*reinterpret_cast<const uint4*>(b + (r1 * hw_in + c0) * c), p10);
-  unpack<T>(*reinterpret_cast<const uint4*>(b + (r0 * hw_in + c1) * c), p01);
-  unpack<T>(*reinterpret_cast<const uint4*>(b + (r1 * hw_in + c1) * c), p11);
+  up_w(y, HW_IN, r0, r1, fr);
+  up_w(x, HW_IN, c0, c1, fc);
   const float omr = 1.f - fr, omc = 1.f - fc;
+  const T* b = in + n * HW_IN * HW_IN * C;
+  T* o = out + px * c_tot;
 #pragma unroll
-  for (int j = 0; j < V; ++j) {
-    float t0 = p00[j] * omr + p10[j] * fr;
-    float t1 = p01[j] * omr + p11[j] * fr;
-    o[j] = t0 * omc + t1 * fc;
+  for (int k = 0; k < GPT; ++k) {
+    const int g = (gq * GPT + k) * V;
+    float p00[V], p10[V], p01[V], p11[V], v[V];
+    unpack<T>(__ldg(reinterpret_cast<const uint4*>(b + (r0 * HW_IN + c0) * C + g)), p00);
+    unpack<T>(__ldg(reinterpret_cast<const uint4*>(b + (r1 * HW_IN + c0) * C + g)), p10);
+    unpack<T>(__ldg(reinterpret_cast<const uint4*>(b + (r0 * HW_IN + c1) * C + g)), p01);
+    unpack<T>(__ldg(reinterpret_cast<const uint4*>(b + (r1 * HW_IN + c1) * C + g)), p11);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      float t0 = __fadd_rn(__fmul_rn(p00[j], omr), __fmul_rn(p10[j], fr));
+      float t1 = __fadd_rn(__fmul_rn(p01[j], omr), __fmul_rn(p11[j], fr));
+      v[j] = __fadd_rn(__fmul_rn(t0, omc), __fmul_rn(t1, fc));
+    }
+    *reinterpret_cast<uint4*>(o + g) = pack<T>(v);
   }
-  *reinterpret_cast<uint4*>(out + ((n * ho + y) * ho + x) * c_tot + g * V) = pack<T>(o);
+}
+
+template <typename T, int HW_OUT, int C>
+void launch_pool(const T* in, int c_tot, int off, T* out, int64_t nmaps, cudaStream_t st) {
+  constexpr int G = C / Vec<T>::N;
+  constexpr int TPP = G / (G >= 4 ? 4 : G);
+  int64_t tot = nmaps * HW_OUT * HW_OUT * TPP;
+  k_pool_nhwc<T, HW_OUT, C><<<unsigned((tot + 255) / 256), 256, 0, st>>>(in, c_tot, off, out, nmaps);
+  count_launch();
+}
+
+template <typename T, int HW_IN, int C>
+void launch_up(const T* in, T* out, int c_tot, int64_t nmaps, cudaStream_t st) {
+  constexpr int G = C / Vec<T>::N;
+  constexpr int TPP = G / (G >= 4 ? 4 : G);
+  int64_t tot = nmaps * 4 * HW_IN * HW_IN * TPP;
+  k_up_nhwc<T, HW_IN, C><<<unsigned((tot + 255) / 256), 256, 0, st>>>(in, out, c_tot, nmaps);
+  count_launch();
+}
+
+// shapes of the k = 64 / k = 32 U-Nets
+template <typename T>
+int pool_dispatch(const T* in, int c_tot, int off, int c, int hw_out, T* out, int64_t n,
+                  cudaStream_t st) {
+  if (hw_out == 16 && c == 64) launch_pool<T, 16, 64>(in, c_tot, off, out, n, st);
+  else if (hw_out == 8 && c == 128) launch_pool<T, 8, 128>(in, c_tot, off, out, n, st);
+  else if (hw_out == 4 && c == 256) launch_pool<T, 4, 256>(in, c_tot, off, out, n, st);
+  else if (hw_out == 16 && c == 32) launch_pool<T, 16, 32>(in, c_tot, off, out, n, st);
+  else if (hw_out == 8 && c == 64) launch_pool<T, 8, 64>(in, c_tot, off, out, n, st);
+  else if (hw_out == 4 && c == 128) launch_pool<T, 4, 128>(in, c_tot, off, out, n, st);
+  else return fail(DRCB_ECONFIG, "unsupported pool shape");
+  return 0;
+}
+
+template <typename T>
+int up_dispatch(const T* in, int c, int hw_in, T* out, int c_tot, int64_t n, cudaStream_t st) {
+  if (hw_in == 4 && c == 512) launch_up<T, 4, 512>(in, out, c_tot, n, st);
+  else if (hw_in == 8 && c == 256) launch_up<T, 8, 256>(in, out, c_tot, n, st);
+  else if (hw_in == 16 && c == 128) launch_up<T, 16, 128>(in, out, c_tot, n, st);
+  else if (hw_in == 4 && c == 256) launch_up<T, 4, 256>(in, out, c_tot, n, st);
+  else if (hw_in == 8 && c == 128) launch_up<T, 8, 128>(in, out, c_tot, n, st);
+  else if (hw_in == 16 && c == 64) launch_up<T, 16, 64>(in, out, c_tot, n, st);
+  else return fail(DRCB_ECONFIG, "unsupported upsample shape");
+  return 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -747,7 +814,8 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
 }
 
 template <int KIND>
-int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t st) {
+int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t st,
+                 const void* x_nhwc = nullptr) {
   using T = typename std::conditional<KIND == 0, __nv_bfloat16, float>::type;
   const int k = net.k;
   if (k % 32 != 0 || k / 4 > 16)
@@ -787,22 +855,19 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
   Buf B[NBUF];
   for (int i = 0; i < NBUF; ++i) B[i] = Buf{base + off[i], specs[i].c, specs[i].hw};
   int rc = 0;
-  // input stack -> NHWC padded
-  {
+  // input stack -> NHWC padded (skipped when the caller already wrote it)
+  if (x_nhwc) {
+    B[0].p = const_cast<void*>(x_nhwc);
+  } else {
     int64_t tot = np * 1024;
     k_stack_to_nhwc<T><<<unsigned((tot + 255) / 256), 256, 0, st>>>(x, n, np, B[0].c, (T*)B[0].p);
     count_launch();
   }
-  constexpr int V = 16 / sizeof(T);
   auto pool = [&](const Buf& in, int off_c, int c, const Buf& out) {
-    int64_t tot = np * out.hw * out.hw * c;
-    k_pool_nhwc<T><<<unsigned((tot / V + 255) / 256), 256, 0, st>>>((const T*)in.p, in.c, off_c, c, out.hw, tot, (T*)out.p);
-    count_launch();
+    rc |= pool_dispatch<T>((const T*)in.p, in.c, off_c, c, out.hw, (T*)out.p, np, st);
   };
   auto up = [&](const Buf& in, int c, const Buf& out) {
-    int64_t tot = np * out.hw * out.hw * c;
-    k_up_nhwc<T><<<unsigned((tot / V + 255) / 256), 256, 0, st>>>((const T*)in.p, c, in.hw, (T*)out.p, out.c, tot);
-    count_launch();
+    rc |= up_dispatch<T>((const T*)in.p, c, in.hw, (T*)out.p, out.c, np, st);
   };
   // encoder
   rc |= run_layer<KIND>(net, Ls[0], B[0], B[1], 0, np, st);
@@ -848,6 +913,17 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
 }
 
 }  // namespace tc
+
+// input already NHWC (n rounded up to 8 maps, channels padded to the K
+// granularity, zeros in the padding): used by the frame driver
+int forward_tc_nhwc(NetImpl& net, const void* x_nhwc, float* y, int64_t n, int mode,
+                    cudaStream_t st) {
+  keep_pool_memory();
+  return mode == DRCB_NET_BF16 ? tc::forward_kind<0>(net, nullptr, y, n, st, x_nhwc)
+                               : tc::forward_kind<1>(net, nullptr, y, n, st, x_nhwc);
+}
+
+int tc_input_channels(int mode) { return mode == DRCB_NET_BF16 ? 64 : 32; }
 
 int forward_tc(NetImpl& net, const float* x, float* y, int64_t n, int mode, cudaStream_t st) {
   if (n <= 0) return 0;

@@ -64,7 +64,8 @@ int launch_gbuffer_direct(const DevScene& S, const DevCamera& C, const DrcbRende
 template <typename R>
 int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* pos, const R* nrm,
                          const uint64_t* keys, const uint8_t* live, int64_t n, float* stacks,
-                         R* s_r, R* s_d, R* frames, int64_t* nonfinite, cudaStream_t st);
+                         R* s_r, R* s_d, R* frames, int64_t* nonfinite, cudaStream_t st,
+                         void* nhwc = nullptr, int nhwc_kind = 0, int cpad = 0);
 template <typename R>
 int launch_shade(const DevScene& S, const DrcbRenderCfg& cfg, const float* pred, const R* s_r,
                  const R* frames, const R* wo, const int32_t* mat, const uint64_t* keys,

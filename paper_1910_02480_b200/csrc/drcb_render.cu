@@ -12,6 +12,7 @@
 //                      integrators.py:564-614)
 //   k_interp           _interpolate_layer + composite    (cache.py:283-345, 463)
 #include <cub/cub.cuh>
+#include <cuda_bf16.h>
 
 #include "drcb_internal.h"
 #include "drcb_trace.cuh"
@@ -333,21 +334,30 @@ constexpr double LUMA_R = 0.2126, LUMA_G = 0.7152, LUMA_B = 0.0722;  // hemimap.
 
 // One block (256 threads) per cache point: s_r = mean luminance + 1e-3,
 // s_d = max distance (or 1), fp32 NCHW stack [rad/s_r, n_local, d/s_d].
+// nhwc_kind: 0 = none, 1 = bf16 NHWC (cpad channels), 2 = tf32-rounded fp32
+// NHWC: the tensor-core network's input layout, written here directly
 template <typename R>
 __global__ void __launch_bounds__(256) k_stack_normalize(const R* __restrict__ rad,
                                                          const R* __restrict__ dist,
                                                          const R* __restrict__ nloc,
                                                          const uint8_t* __restrict__ live,
                                                          int64_t n, float* stacks, R* s_r,
-                                                         R* s_d) {
+                                                         R* s_d, void* nhwc, int nhwc_kind,
+                                                         int cpad) {
   __shared__ R lum[MAP_TEXELS];
   __shared__ R scratch[64];
   __shared__ R dmax[8];
   int64_t p = blockIdx.x;
   if (p >= n) return;
-  float* out = stacks + p * 7 * MAP_TEXELS;
+  float* out = stacks ? stacks + p * 7 * MAP_TEXELS : nullptr;
   if (live && !live[p]) {
-    for (int t = threadIdx.x; t < 7 * MAP_TEXELS; t += blockDim.x) out[t] = 0.f;
+    if (stacks)
+      for (int t = threadIdx.x; t < 7 * MAP_TEXELS; t += blockDim.x) out[t] = 0.f;
+    if (nhwc_kind) {
+      int es = nhwc_kind == 1 ? 2 : 4;
+      uint4* o = reinterpret_cast<uint4*>(static_cast<uint8_t*>(nhwc) + size_t(p) * MAP_TEXELS * cpad * es);
+      for (int t = threadIdx.x; t < MAP_TEXELS * cpad * es / 16; t += blockDim.x) o[t] = make_uint4(0, 0, 0, 0);
+    }
     if (threadIdx.x == 0) { s_r[p] = R(1); s_d[p] = R(1); }
     return;
   }
@@ -368,9 +378,33 @@ __global__ void __launch_bounds__(256) k_stack_normalize(const R* __restrict__ r
   R sd = mx > R(0) ? mx : R(1);
   const R* np_ = nloc + p * MAP_TEXELS * 3;
   for (int t = threadIdx.x; t < MAP_TEXELS; t += blockDim.x) {
-    for (int c = 0; c < 3; ++c) out[c * MAP_TEXELS + t] = float(rp[3 * t + c] / sr);
-    for (int c = 0; c < 3; ++c) out[(3 + c) * MAP_TEXELS + t] = float(np_[3 * t + c]);
-    out[6 * MAP_TEXELS + t] = float(dp[t] / sd);
+    float v[8];
+    for (int c = 0; c < 3; ++c) v[c] = float(rp[3 * t + c] / sr);
+    for (int c = 0; c < 3; ++c) v[3 + c] = float(np_[3 * t + c]);
+    v[6] = float(dp[t] / sd);
+    v[7] = 0.f;
+    if (stacks)
+      for (int c = 0; c < 7; ++c) out[c * MAP_TEXELS + t] = v[c];
+    if (nhwc_kind == 1) {
+      uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(nhwc) + (p * MAP_TEXELS + t) * cpad);
+      uint32_t w[4];
+      for (int j = 0; j < 4; ++j) {
+        __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+        w[j] = *reinterpret_cast<uint32_t*>(&b);
+      }
+      o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      for (int g = 1; g < cpad / 8; ++g) o[g] = make_uint4(0, 0, 0, 0);
+    } else if (nhwc_kind == 2) {
+      float4* o = reinterpret_cast<float4*>(static_cast<float*>(nhwc) + (p * MAP_TEXELS + t) * cpad);
+      auto rt = [](float x) {
+        uint32_t r;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+        return __uint_as_float(r);
+      };
+      o[0] = make_float4(rt(v[0]), rt(v[1]), rt(v[2]), rt(v[3]));
+      o[1] = make_float4(rt(v[4]), rt(v[5]), rt(v[6]), 0.f);
+      for (int g = 2; g < cpad / 4; ++g) o[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
   if (threadIdx.x == 0) {
     s_r[p] = sr;
@@ -718,7 +752,8 @@ int launch_gbuffer_direct(const DevScene& S, const DevCamera& C, const DrcbRende
 template <typename R>
 int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* pos, const R* nrm,
                          const uint64_t* keys, const uint8_t* live, int64_t n, float* stacks,
-                         R* s_r, R* s_d, R* frames, int64_t* nonfinite, cudaStream_t st) {
+                         R* s_r, R* s_d, R* frames, int64_t* nonfinite, cudaStream_t st,
+                         void* nhwc, int nhwc_kind, int cpad) {
   if (n <= 0) return 0;
   size_t per = size_t(n) * MAP_TEXELS;
   R* scratch = nullptr;
@@ -742,7 +777,8 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
   k_map_paths<R><<<g, MAP_TPB, 0, st>>>(S, cfg, pos, nrm, keys, live, total, counter, rad, dist,
                                          nloc, nonfinite);
   LAUNCH_CHECK();
-  k_stack_normalize<R><<<int(n), 256, 0, st>>>(rad, dist, nloc, live, n, stacks, s_r, s_d);
+  k_stack_normalize<R><<<int(n), 256, 0, st>>>(rad, dist, nloc, live, n, stacks, s_r, s_d, nhwc,
+                                                nhwc_kind, cpad);
   LAUNCH_CHECK();
   DRCB_CUDA(cudaFreeAsync(scratch, st));
   return 0;
@@ -814,7 +850,8 @@ int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& 
                                         int64_t*, cudaStream_t);                                 \
   template int launch_render_stacks<R>(const DevScene&, const DrcbRenderCfg&, const R*,         \
                                        const R*, const uint64_t*, const uint8_t*, int64_t,      \
-                                       float*, R*, R*, R*, int64_t*, cudaStream_t);              \
+                                       float*, R*, R*, R*, int64_t*, cudaStream_t, void*, int,  \
+                                       int);                                                     \
   template int launch_shade<R>(const DevScene&, const DrcbRenderCfg&, const float*, const R*,   \
                                const R*, const R*, const int32_t*, const uint64_t*,             \
                                const uint8_t*, int64_t, R*, cudaStream_t);                       \
