@@ -208,6 +208,29 @@ int drcb_trav_stats(unsigned long long *buf);
 /* number of kernels this library has launched so far (process-wide) */
 int64_t drcb_kernel_launches(void);
 
+/* ---- training step (trainer/src/drc_trainer/train.py:97-103) ---------- */
+/* MapAutoencoder in train mode (batch-statistics BN, momentum 0.1), L1 loss,
+ * Adam(lr, betas, eps) with fp32 master weights, from DRCW bytes (host). */
+int drcb_trainer_create(const void *drcw, size_t len, float lr, float beta1, float beta2,
+                        float eps, DrcbTrainer **out);
+void drcb_trainer_destroy(DrcbTrainer *t);
+/* host out: k, n_params, n_running, steps taken */
+int drcb_trainer_info(const DrcbTrainer *t, int64_t *out4);
+/* device pointers of the flat fp32 parameter / gradient / running-stat
+ * buffers, torch named_parameters() order (for all-reduce and inspection) */
+int drcb_trainer_buffers(const DrcbTrainer *t, void **params, void **grads, void **running);
+/* forward + loss + backward into the gradient buffer; x (n,7,32,32),
+ * y (n,3,32,32) device fp32; apply_adam=1 also takes the optimiser step.
+ * loss_host (optional) receives the mean L1 loss (synchronises). */
+int drcb_trainer_step(DrcbTrainer *t, const float *x, const float *y, int64_t n,
+                      double *loss_host, int32_t apply_adam, void *stream);
+/* Adam on the gradient buffer scaled by grad_scale (1/world after an
+ * all-reduce sum across data-parallel ranks). */
+int drcb_trainer_apply(DrcbTrainer *t, float grad_scale, void *stream);
+/* DRCW bytes of the current weights + running stats into host buf (cap
+ * bytes); returns the size (buf = NULL to query). */
+int64_t drcb_trainer_export(const DrcbTrainer *t, void *buf, int64_t cap);
+
 const char *drcb_last_error(void);
 int drcb_version(void);
 

@@ -89,6 +89,14 @@ _SIGS = [
     ("drcb_trav_stats", C.c_int, [vp]),
     ("drcb_debug_conv", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, vp, vp,
                                   vp]),
+    ("drcb_trainer_create", C.c_int, [C.c_char_p, C.c_size_t, C.c_float, C.c_float, C.c_float,
+                                      C.c_float, C.POINTER(vp)]),
+    ("drcb_trainer_destroy", None, [vp]),
+    ("drcb_trainer_info", C.c_int, [vp, C.POINTER(C.c_int64)]),
+    ("drcb_trainer_buffers", C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+    ("drcb_trainer_step", C.c_int, [vp, vp, vp, C.c_int64, C.POINTER(C.c_double), C.c_int32, vp]),
+    ("drcb_trainer_apply", C.c_int, [vp, C.c_float, vp]),
+    ("drcb_trainer_export", C.c_int64, [vp, vp, C.c_int64]),
     ("drcb_last_error", C.c_char_p, []),
     ("drcb_version", C.c_int, []),
 ]

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(256) k_conv_f32(const float* __restrict__ in, 
   for (int j = 0; j < CO_PER_THREAD; ++j) {
     int co = co0 + j;
     if (co >= cout) break;
-    float v = acc[j] + bias[co];
+    float v = acc[j] + (bias ? bias[co] : 0.f);
     if (act == 1) {
       v = __fadd_rn(__fmul_rn(v, scale[co]), shift[co]);
       v = v >= 0.f ? v : __fmul_rn(slope, v);
@@ -192,7 +192,7 @@ int conv_f32(const ConvLayer& L, const float* in, int cin_tot, int cin_off, floa
              int cout_tot, int cout_off, int64_t n, float slope, cudaStream_t st) {
   int npx = L.hw * L.hw;
   dim3 grid((npx + 255) / 256, (L.cout + CO_PER_THREAD - 1) / CO_PER_THREAD, unsigned(n));
-  int act = L.act ? 1 : 2;
+  int act = L.mode >= 0 ? L.mode : (L.act ? 1 : 2);
   if (L.ksize == 3)
     k_conv_f32<3><<<grid, 256, 0, st>>>(in, cin_tot, cin_off, L.cin, L.d_w, L.d_bias, L.d_scale,
                                         L.d_shift, act, slope, out, cout_tot, cout_off, L.cout,

@@ -16,6 +16,7 @@ struct ConvLayer {
   std::string bn;        // e.g. "enc1.bn1" ("" for head.conv_out)
   int cin = 0, cout = 0, ksize = 3, hw = 32;
   bool act = true;       // BN + LeakyReLU epilogue
+  int mode = -1;         // SIMT epilogue override: 0 bias only, 1 BN+LReLU, 2 bias+ReLU
   // host copies
   std::vector<float> w;      // (cout, cin, k, k) conv form
   std::vector<float> bias;   // (cout)

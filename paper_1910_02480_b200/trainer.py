@@ -1,0 +1,161 @@
+"""The autoencoder's training step on the B200 — the drop-in for
+drc_trainer.train's inner step (trainer/src/drc_trainer/train.py:97-103):
+
+    optimizer.zero_grad(); loss = L1(model(x), y); loss.backward(); optimizer.step()
+
+`DeviceTrainer` keeps fp32 master weights, gradients and Adam moments in HBM
+(drcb_trainer_*); BN runs in train mode (batch statistics, momentum 0.1).
+Parameters are laid out in torch's named_parameters() order of
+MapAutoencoder (model.py:54-88) so gradients and updates compare 1:1.
+
+Data parallelism: each rank steps on its shard with apply=False, the flat
+gradient buffer is all-reduced (sum) over NCCL, then `apply(1/world)`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .cnn import architecture, load_weights, save_weights
+
+_LAYERS = ["enc1.conv1", "enc1.conv2", "enc2.conv1", "enc2.conv2", "enc3.conv1", "enc3.conv2",
+           "bott.conv1", "bott.conv2", "dec3.deconv1", "dec3.deconv2", "dec2.deconv1",
+           "dec2.deconv2", "dec1.deconv1", "dec1.deconv2", "head.deconv1", "head.deconv2",
+           "head.conv_out"]
+
+
+def _bn_of(layer):
+    if layer == "head.conv_out":
+        return None
+    mod, conv = layer.split(".")
+    return f"{mod}.bn{conv[-1]}"
+
+
+def param_layout(k):
+    """[(torch name, drcw name, shape, offset)] in named_parameters() order."""
+    arch = architecture(k)
+    out, off = [], 0
+    for layer in _LAYERS:
+        for suffix in ("weight", "bias"):
+            shape = arch[f"{layer}.{suffix}"]
+            out.append((f"{layer}.{suffix}", f"{layer}.{suffix}", shape, off))
+            off += int(np.prod(shape))
+        bn = _bn_of(layer)
+        if bn:
+            for tsuf, dsuf in (("weight", "gamma"), ("bias", "beta")):
+                shape = arch[f"{bn}.{dsuf}"]
+                out.append((f"{bn}.{tsuf}", f"{bn}.{dsuf}", shape, off))
+                off += int(np.prod(shape))
+    return out
+
+
+class DeviceTrainer:
+    def __init__(self, net_or_drcw, lr=6e-5, betas=(0.9, 0.999), eps=1e-8):
+        lib = _lib.load()
+        raw = net_or_drcw if isinstance(net_or_drcw, (bytes, bytearray)) else save_weights(net_or_drcw)
+        h = C.c_void_p()
+        _lib.check(lib.drcb_trainer_create(bytes(raw), len(raw), float(lr), float(betas[0]),
+                                           float(betas[1]), float(eps), C.byref(h)),
+                   "drcb_trainer_create")
+        self.handle = h
+        info = (C.c_int64 * 4)()
+        _lib.call("drcb_trainer_info", h, info)
+        self.k, self.n_params, self.n_running = int(info[0]), int(info[1]), int(info[2])
+        self.layout = param_layout(self.k)
+
+    # -- steps ---------------------------------------------------------------
+    def step(self, x, y, apply=True, want_loss=True):
+        """One step on x (n,7,32,32), y (n,3,32,32) (CUDA tensors or numpy).
+        Returns the batch L1 loss (float) or None."""
+        import torch
+
+        xd = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, np.float32))
+        yd = y if isinstance(y, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(y, np.float32))
+        xd = xd.to(device="cuda", dtype=torch.float32).contiguous()
+        yd = yd.to(device="cuda", dtype=torch.float32).contiguous()
+        loss = C.c_double(0.0)
+        _lib.call("drcb_trainer_step", self.handle, _lib.ptr(xd), _lib.ptr(yd), int(xd.shape[0]),
+                  C.byref(loss) if want_loss else None, int(bool(apply)), _lib.stream_ptr())
+        return float(loss.value) if want_loss else None
+
+    def apply(self, grad_scale=1.0):
+        _lib.call("drcb_trainer_apply", self.handle, float(grad_scale), _lib.stream_ptr())
+
+    # -- buffers -------------------------------------------------------------
+    def _buffers(self):
+        p, g, r = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _lib.call("drcb_trainer_buffers", self.handle, C.byref(p), C.byref(g), C.byref(r))
+        return p.value, g.value, r.value
+
+    def grad_tensor(self):
+        """The flat fp32 gradient buffer as a CUDA tensor view (for NCCL)."""
+        return _device_view(self._buffers()[1], self.n_params)
+
+    def _host(self, which):
+        import torch
+
+        ptr = self._buffers()[which]
+        torch.cuda.current_stream().synchronize()
+        return _device_view(ptr, self.n_params).cpu().numpy()
+
+    def params(self):
+        flat = self._host(0)
+        return {n: flat[o:o + int(np.prod(s))].reshape(s).copy() for n, _, s, o in self.layout}
+
+    def grads(self):
+        flat = self._host(1)
+        return {n: flat[o:o + int(np.prod(s))].reshape(s).copy() for n, _, s, o in self.layout}
+
+    def export(self):
+        size = _lib.load().drcb_trainer_export(self.handle, None, 0)
+        buf = (C.c_uint8 * size)()
+        _lib.load().drcb_trainer_export(self.handle, buf, size)
+        return bytes(buf)
+
+    def network(self):
+        return load_weights(self.export())
+
+    def close(self):
+        if getattr(self, "handle", None) and _lib._lib is not None:
+            _lib._lib.drcb_trainer_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _device_view(ptr, n):
+    """Zero-copy torch view of library-owned device memory."""
+    import torch
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+
+    return torch.as_tensor(_CAI(), device="cuda")
+
+
+@dataclass
+class TrainConfig:
+    """TrainConfig (train.py:19-36)."""
+
+    learning_rate: float = 6e-5
+    batch_size: int = 32
+    epochs: int = 3
+    ablation: tuple = ()
+    seed: int = 0
+    val_fraction: float = 0.1
+    k: int = 64
+    slope: float = 0.01
+
+
+def train_step(trainer, x, y):
+    """train.py:97-103 on the device; returns the loss."""
+    return trainer.step(x, y, apply=True)

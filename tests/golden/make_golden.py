@@ -204,5 +204,49 @@ def main():
     frame_fixture("frame_furnace.npz", env, 8, 1, dict(direct_spp=2, indirect_tasks=1, mis_samples=8))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--train" not in sys.argv:
     main()
+
+
+def train_fixture():
+    """Two optimisation steps of the reference trainer (train.py:85-103):
+    MapAutoencoder in train mode, L1Loss, Adam(lr, betas), from DRCW weights."""
+    import torch
+
+    from drc_trainer.model import export_drcw, import_drcw
+
+    torch.manual_seed(0)
+    out = {}
+    for k, seed, n in ((8, 7, 4),):
+        net = rcnn.random_network(k, seed)
+        raw = rcnn.save_weights(net)
+        model = import_drcw(raw)
+        model.train()
+        opt = torch.optim.Adam(model.parameters(), lr=1e-4, betas=(0.9, 0.999))
+        loss_fn = torch.nn.L1Loss()
+        rng = np.random.default_rng(seed)
+        xs, ys, losses = [], [], []
+        for step in range(2):
+            x = rng.uniform(0, 1, (n, 7, 32, 32)).astype(np.float32)
+            x[:, :3] *= 4.0
+            y = np.exp(rng.normal(-1.0, 1.0, (n, 3, 32, 32))).astype(np.float32)
+            xs.append(x)
+            ys.append(y)
+            opt.zero_grad()
+            loss = loss_fn(model(torch.from_numpy(x)), torch.from_numpy(y))
+            loss.backward()
+            if step == 0:
+                for name, p in model.named_parameters():
+                    out[f"k{k}_grad0/{name}"] = p.grad.detach().numpy().copy()
+            opt.step()
+            losses.append(float(loss))
+        out[f"k{k}_x"] = np.stack(xs)
+        out[f"k{k}_y"] = np.stack(ys)
+        out[f"k{k}_loss"] = np.array(losses)
+        out[f"k{k}_weights_in"] = np.frombuffer(raw, dtype=np.uint8)
+        out[f"k{k}_weights_out"] = np.frombuffer(export_drcw(model), dtype=np.uint8)
+    save("train.npz", **out)
+
+
+if __name__ == "__main__" and "--train" in sys.argv:
+    train_fixture()

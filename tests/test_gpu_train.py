@@ -1,0 +1,74 @@
+"""Training step (train.py:97-103) against two steps of the reference's own
+torch trainer (MapAutoencoder train mode, L1Loss, Adam) recorded in
+tests/golden/train.npz."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1910_02480_b200 import cnn  # noqa: E402
+from paper_1910_02480_b200.trainer import DeviceTrainer  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def g():
+    return load_golden("train.npz")
+
+
+def test_first_step_loss_and_gradients(g):
+    tr = DeviceTrainer(bytes(g["k8_weights_in"]), lr=1e-4)
+    loss = tr.step(g["k8_x"][0], g["k8_y"][0], apply=False)
+    assert abs(loss - g["k8_loss"][0]) <= 1e-5 * abs(g["k8_loss"][0])
+    grads = tr.grads()
+    worst = 0.0
+    for name, gv in grads.items():
+        ref = g[f"k8_grad0/{name}"]
+        scale = max(np.abs(ref).max(), 1e-6)
+        err = np.abs(gv - ref).max() / scale
+        if name.endswith(".bias") and ("conv" in name and "conv_out" not in name):
+            # conv biases feeding train-mode BN have a zero true gradient;
+            # both sides hold rounding noise around 0
+            assert np.abs(gv).max() <= 1e-5 * max(1.0, scale), name
+            continue
+        worst = max(worst, err)
+        assert err <= 1e-4, (name, err)
+
+
+def test_two_adam_steps_match_reference(g):
+    tr = DeviceTrainer(bytes(g["k8_weights_in"]), lr=1e-4)
+    l0 = tr.step(g["k8_x"][0], g["k8_y"][0])
+    l1 = tr.step(g["k8_x"][1], g["k8_y"][1])
+    assert np.allclose([l0, l1], g["k8_loss"], rtol=2e-5)
+    got = cnn.load_weights(tr.export()).tensors
+    ref = cnn.load_weights(bytes(g["k8_weights_out"])).tensors
+    w0 = cnn.load_weights(bytes(g["k8_weights_in"])).tensors
+    for name in ref:
+        d = np.abs(got[name] - ref[name])
+        moved = np.abs(ref[name] - w0[name]).max()
+        if "running" in name:
+            # the conv bias in front of each BN only carries rounding-noise
+            # gradient, which Adam turns into a +-lr step; the running mean
+            # absorbs it with momentum 0.1 (<= 2 steps * 2 lr * 0.1 = 4e-5)
+            assert np.allclose(got[name], ref[name], rtol=1e-4, atol=5e-5), name
+        else:
+            # Adam moves each weight by ~lr*sign(g); elements whose gradient is
+            # rounding noise (biases before BN) may move either way by <= 2 lr
+            assert d.max() <= 2.5e-4, (name, d.max(), moved)
+            noise = name.endswith(".bias") and "conv_out" not in name and "bn" not in name
+            if not noise:
+                assert np.mean(d <= 2e-6) >= 0.99, (name, np.mean(d <= 2e-6))
+
+
+def test_loss_decreases_on_a_fixed_batch():
+    rng = np.random.default_rng(0)
+    x = rng.uniform(0, 1, (8, 7, 32, 32)).astype(np.float32)
+    y = np.exp(rng.normal(-1, 1, (8, 3, 32, 32))).astype(np.float32)
+    tr = DeviceTrainer(cnn.random_network(16, 4), lr=1e-3)
+    losses = [tr.step(x, y) for _ in range(20)]
+    assert losses[-1] < 0.8 * losses[0]
