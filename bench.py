@@ -185,8 +185,10 @@ def main():
                 "precision": f"rays fp{args.precision}, U-Net {cfg.net_mode}",
                 "l2": "flushed between steps (256 MB write)"}
     scene = scenegen.build_scene(args.config)
+    from paper_1910_02480_b200.dist import frame_shard
+
     cams = scenegen.orbit_cameras(args.frames * max(world, 1), res, seed=2)
-    my_cams = cams[rank * args.frames:(rank + 1) * args.frames]
+    my_cams = [cams[i] for i in frame_shard(len(cams), rank, max(world, 1))]
     net = cnn.random_network(64, seed=wseed)
     plan = render.plan_points(res, cfg)
     n_pts = len(plan[0])

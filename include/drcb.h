@@ -227,6 +227,17 @@ int drcb_trainer_step(DrcbTrainer *t, const float *x, const float *y, int64_t n,
 /* Adam on the gradient buffer scaled by grad_scale (1/world after an
  * all-reduce sum across data-parallel ranks). */
 int drcb_trainer_apply(DrcbTrainer *t, float grad_scale, void *stream);
+/* Data-parallel communicator (NULL = single process). With a communicator
+ * the step uses SyncBN (batch statistics all-reduced over NVLink/NVSwitch)
+ * and all-reduces the gradient buffer; Adam averages by 1/world. */
+int drcb_trainer_set_comm(DrcbTrainer *t, void *nccl_comm, int32_t world);
+
+/* ---- NCCL plumbing (libnccl.so.2 opened at first use) ------------------ */
+int drcb_nccl_unique_id(void *out128);
+int drcb_nccl_comm_create(const void *id128, int32_t world, int32_t rank, void **comm);
+int drcb_nccl_comm_destroy(void *comm);
+int drcb_allreduce_sum_f32(void *comm, float *buf, int64_t n, void *stream);
+
 /* DRCW bytes of the current weights + running stats into host buf (cap
  * bytes); returns the size (buf = NULL to query). */
 int64_t drcb_trainer_export(const DrcbTrainer *t, void *buf, int64_t cap);

@@ -97,6 +97,11 @@ _SIGS = [
     ("drcb_trainer_step", C.c_int, [vp, vp, vp, C.c_int64, C.POINTER(C.c_double), C.c_int32, vp]),
     ("drcb_trainer_apply", C.c_int, [vp, C.c_float, vp]),
     ("drcb_trainer_export", C.c_int64, [vp, vp, C.c_int64]),
+    ("drcb_trainer_set_comm", C.c_int, [vp, vp, C.c_int32]),
+    ("drcb_nccl_unique_id", C.c_int, [vp]),
+    ("drcb_nccl_comm_create", C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(vp)]),
+    ("drcb_nccl_comm_destroy", C.c_int, [vp]),
+    ("drcb_allreduce_sum_f32", C.c_int, [vp, vp, C.c_int64, vp]),
     ("drcb_last_error", C.c_char_p, []),
     ("drcb_version", C.c_int, []),
 ]

@@ -16,6 +16,7 @@ int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
 void count_launch(int n = 1);
 void keep_pool_memory();
+int allreduce_sum(void* comm, void* buf, size_t count, int is_double, cudaStream_t st);
 
 #define DRCB_CUDA(call)                                      \
   do {                                                       \

@@ -646,8 +646,10 @@ int bn_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& out, cudaS
   dim3 g(std::min<int64_t>(64, nb(n * hw2)), t.cout);
   k_chan_stats<<<g, 256, 0, st>>>(W.z[l], t.cout, 0, hw2, n, W.acc);
   TCHECK("k_chan_stats");
-  // SyncBN across data-parallel ranks would all-reduce W.acc here
-  k_bn_finalize<<<nb(t.cout), 256, 0, st>>>(W.acc, t.cout, double(n) * hw2, W.mean[l],
+  // SyncBN: batch statistics over all data-parallel ranks (NVLink all-reduce)
+  int rc = allreduce_sum(T->comm, W.acc, size_t(2) * t.cout, 1, st);
+  if (rc) return rc;
+  k_bn_finalize<<<nb(t.cout), 256, 0, st>>>(W.acc, t.cout, double(n) * hw2 * T->world, W.mean[l],
                                                W.invstd[l], T->running + t.rm, T->running + t.rv);
   TCHECK("k_bn_finalize");
   k_bn_act<<<nb(n * t.cout * hw2), 256, 0, st>>>(W.z[l], t.cout, hw2, n, W.mean[l], W.invstd[l],
@@ -679,12 +681,19 @@ int layer_backward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, co
                                      W.mean[l], W.invstd[l], T->params + t.g, T->params + t.be,
                                      T->slope, W.acc);
   TCHECK("k_bn_bwd_stats");
+  // local gamma/beta gradients first (they join the gradient all-reduce)
   k_bn_param_grads<<<nb(t.cout), 256, 0, st>>>(W.acc, t.cout, T->grads + t.g, T->grads + t.be);
   TCHECK("k_bn_param_grads");
+  // SyncBN backward: global means of dyb and dyb * xhat
+  {
+    int rc = allreduce_sum(T->comm, W.acc, size_t(2) * t.cout, 1, st);
+    if (rc) return rc;
+  }
   k_bn_bwd_apply<<<nb(n * t.cout * hw2), 256, 0, st>>>(W.z[l], dout.p, dout.ctot, dout.coff,
                                                         t.cout, hw2, n, W.mean[l], W.invstd[l],
                                                         T->params + t.g, T->params + t.be,
-                                                        T->slope, W.acc, double(n) * hw2, W.dz);
+                                                        T->slope, W.acc, double(n) * hw2 * T->world,
+                                                        W.dz);
   TCHECK("k_bn_bwd_apply");
   k_chan_sum<<<t.cout, 256, 0, st>>>(W.dz, t.cout, hw2, n, T->grads + t.b);
   TCHECK("k_chan_sum");
@@ -830,8 +839,15 @@ extern "C" int drcb_trainer_step(DrcbTrainer* T, const float* x, const float* y,
   }
   // ---- data-parallel gradient average happens between here and Adam
   // (drcb_trainer_apply after an external all-reduce, or apply_adam below)
+  // gradient all-reduce over the data-parallel ranks (sum); the per-rank
+  // loss is a local mean, so the average is sum / world
+  rc = allreduce_sum(T->comm, T->grads, size_t(T->n_params), 0, st);
+  if (rc) {
+    cudaFreeAsync(W.base, st);
+    return rc;
+  }
   if (apply_adam) {
-    rc = drcb_trainer_apply(T, 1.0f, stream);
+    rc = drcb_trainer_apply(T, 1.0f / float(T->world), stream);
     if (rc) {
       cudaFreeAsync(W.base, st);
       return rc;
@@ -862,6 +878,15 @@ extern "C" int drcb_trainer_apply(DrcbTrainer* T, float grad_scale, void* stream
   k_adam<<<nb(T->n_params), 256, 0, st>>>(T->params, T->grads, T->m, T->v, T->n_params, step_size,
                                            T->b1, T->b2, T->eps, float(std::sqrt(bc2)), grad_scale);
   TCHECK("k_adam");
+  return 0;
+}
+
+// data-parallel communicator (ncclComm_t from drcb_nccl_comm_create; NULL =
+// single process): SyncBN statistics and the gradient all-reduce use it
+extern "C" int drcb_trainer_set_comm(DrcbTrainer* T, void* comm, int32_t world) {
+  if (!T || world < 1) return fail(DRCB_ECONTRACT, "drcb_trainer_set_comm: bad arguments");
+  T->comm = comm;
+  T->world = comm ? world : 1;
   return 0;
 }
 

@@ -72,3 +72,20 @@ def test_loss_decreases_on_a_fixed_batch():
     tr = DeviceTrainer(cnn.random_network(16, 4), lr=1e-3)
     losses = [tr.step(x, y) for _ in range(20)]
     assert losses[-1] < 0.8 * losses[0]
+
+
+def test_nccl_syncbn_path_single_rank_matches_plain_step(g):
+    # the in-library NCCL path (SyncBN statistics + gradient all-reduce) on a
+    # world-1 communicator must reproduce the single-process step exactly
+    from paper_1910_02480_b200.dist import attach_nccl
+
+    a = DeviceTrainer(bytes(g["k8_weights_in"]), lr=1e-4)
+    b = DeviceTrainer(bytes(g["k8_weights_in"]), lr=1e-4)
+    comm = attach_nccl(b)
+    la = a.step(g["k8_x"][0], g["k8_y"][0])
+    lb = b.step(g["k8_x"][0], g["k8_y"][0])
+    assert la == lb
+    pa, pb = a.params(), b.params()
+    for name in pa:
+        assert np.array_equal(pa[name], pb[name]), name
+    comm.close()
