@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "drcb_net.h"
@@ -199,6 +200,69 @@ struct Smem {
   static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// Epilogue of one 128 x BN accumulator tile held in TMEM: tcgen05.ld, folded
+// BN + LeakyReLU, NHWC store into the destination slice; for the head layer
+// the fused 1x1 conv_out + ReLU writes fp32 NCHW predictions.
+template <int KIND, int BN>
+__device__ __forceinline__ void epilogue_tile(const ConvArgs& p, uint32_t tbase, int64_t m, int nt) {
+      if (p.head) {
+    // head.deconv2 (BN == 16 channels) + BN + LeakyReLU, then the fused
+    // 1x1 conv_out + ReLU -> fp32 NCHW prediction (cnn.py:209-215)
+    uint32_t r[16];
+    tmem_ld16(tbase, r);
+    tmem_wait_ld();
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float x = __uint_as_float(r[j]) * __ldg(p.ep_a + j) + __ldg(p.ep_b + j);
+      v[j] = x >= 0.f ? x : p.slope * x;
+    }
+    int64_t n = m / 1024;
+    int pix = int(m % 1024);
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+      float s = p.hw_b[o];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) s += p.hw_w[o * 16 + j] * v[j];
+      p.pred[(n * 3 + o) * 1024 + pix] = fmaxf(s, 0.f);
+    }
+  } else {
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t r[16];
+      tmem_ld16(tbase + c0, r);
+      tmem_wait_ld();
+      const int cg = nt * BN + c0;
+      if (cg >= p.cout) break;
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float x = __uint_as_float(r[j]) * __ldg(p.ep_a + cg + j) + __ldg(p.ep_b + cg + j);
+        v[j] = x >= 0.f ? x : p.slope * x;
+      }
+      if constexpr (KIND == 0) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+          pk[j] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
+                                              m * p.cout_tot + p.cout_off + cg);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      } else {
+        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + m * p.cout_tot +
+                                                p.cout_off + cg);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_float4(round_tf32(v[4 * j]), round_tf32(v[4 * j + 1]),
+                               round_tf32(v[4 * j + 2]), round_tf32(v[4 * j + 3]));
+      }
+    }
+  }
+}
+
 template <int KIND, int BN, int STAGES>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
@@ -320,62 +384,175 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int64_t m = int64_t(mt) * BM + row;
       const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
-      if (p.head) {
-        // head.deconv2 (BN == 16 channels) + BN + LeakyReLU, then the fused
-        // 1x1 conv_out + ReLU -> fp32 NCHW prediction (cnn.py:209-215)
-        uint32_t r[16];
-        tmem_ld16(tbase, r);
-        tmem_wait_ld();
-        float v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float x = __uint_as_float(r[j]) * __ldg(p.ep_a + j) + __ldg(p.ep_b + j);
-          v[j] = x >= 0.f ? x : p.slope * x;
-        }
-        int64_t n = m / 1024;
-        int pix = int(m % 1024);
-#pragma unroll
-        for (int o = 0; o < 3; ++o) {
-          float s = p.hw_b[o];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) s += p.hw_w[o * 16 + j] * v[j];
-          p.pred[(n * 3 + o) * 1024 + pix] = fmaxf(s, 0.f);
-        }
-      } else {
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-          uint32_t r[16];
-          tmem_ld16(tbase + c0, r);
-          tmem_wait_ld();
-          const int cg = nt * BN + c0;
-          if (cg >= p.cout) break;
-          float v[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float x = __uint_as_float(r[j]) * __ldg(p.ep_a + cg + j) + __ldg(p.ep_b + cg + j);
-            v[j] = x >= 0.f ? x : p.slope * x;
-          }
-          if constexpr (KIND == 0) {
-            uint32_t pk[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-              pk[j] = *reinterpret_cast<uint32_t*>(&b2);
+      epilogue_tile<KIND, BN>(p, tbase, m, nt);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Row-halo variant for the 32x32 and 16x16 layers (one map covers whole
+// tiles). The 32x32/16x16 layers are L2-bandwidth-bound in the plain kernel
+// (A re-loaded for each of the 9 taps, weights re-streamed per tile). Here a
+// stage is one (channel chunk, dx) pair: a single TMA box of rows+2 image rows
+// serves the three dy taps, whose A operands are the same SMEM buffer at
+// descriptor offsets dy*W*128 B (a multiple of the 1024 B swizzle atom).
+// RES: the whole packed weight matrix (9 * cblocks K tiles) stays resident in
+// SMEM for the CTA's lifetime, loaded once.
+struct HaloArgs {
+  int a_bytes;      // (rows+2) * W * 128
+  int row_bytes;    // W * 128: one dy shift
+  int stages;
+  int res;
+};
+
+template <int KIND, int BN, bool RES>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_conv_halo(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                const __grid_constant__ ConvArgs p, const __grid_constant__ HaloArgs h) {
+  constexpr int B_TILE = BN * ROW_BYTES;
+  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int CEL = ROW_BYTES / ELEM;
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int n_wtiles = 9 * p.cblocks;
+  uint8_t* wres = smem;
+  uint8_t* stages = smem + (RES ? n_wtiles * B_TILE : 0);
+  const int stage_bytes = h.a_bytes + (RES ? 0 : 3 * B_TILE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + h.stages * stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + 8;
+  uint64_t* tfull = bars + 16;
+  uint64_t* tempty = bars + 18;
+  uint64_t* wfull = bars + 20;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&mapA);
+    prefetch_map(&mapB);
+    for (int st = 0; st < h.stages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    mbar_init(wfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+  const int kstages = p.cblocks * 3;  // (chunk, dx) pairs per tile
+  if (warp == 0) {
+    if (lane == 0) {
+      if (RES) {
+        mbar_expect_tx(wfull, uint32_t(n_wtiles * B_TILE));
+        for (int t = 0; t < n_wtiles; ++t) tma_load_2d(&mapB, wfull, wres + t * B_TILE, t * CEL, 0);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int mt = tile % p.num_m_tiles, nt = tile / p.num_m_tiles;
+        int n0 = mt / p.tiles_per_map;
+        int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
+        for (int ks = 0; ks < kstages; ++ks) {
+          int cb = ks / 3, dxi = ks % 3;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sA = stages + stage * stage_bytes;
+          mbar_expect_tx(&full[stage], uint32_t(stage_bytes));
+          tma_load_4d(&mapA, &full[stage], sA, cb * CEL, dxi - 1, y0 - 1, n0);
+          if (!RES) {
+            for (int dyi = 0; dyi < 3; ++dyi) {
+              int kb = (dyi * 3 + dxi) * p.cblocks + cb;
+              tma_load_2d(&mapB, &full[stage], sA + h.a_bytes + dyi * B_TILE, kb * CEL, nt * BN);
             }
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
-                                                  m * p.cout_tot + p.cout_off + cg);
-            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          } else {
-            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + m * p.cout_tot +
-                                                    p.cout_off + cg);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              dst[j] = make_float4(round_tf32(v[4 * j]), round_tf32(v[4 * j + 1]),
-                                   round_tf32(v[4 * j + 2]), round_tf32(v[4 * j + 3]));
+          }
+          if (++stage == h.stages) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(KIND, BM, BN);
+      if (RES) mbar_wait(wfull, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        uint32_t tmem_d = tmem_base + acc * BN;
+        bool first = true;
+        for (int ks = 0; ks < kstages; ++ks) {
+          int cb = ks / 3, dxi = ks % 3;
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          uint32_t a0 = smem_u32(stages + stage * stage_bytes);
+#pragma unroll
+          for (int dyi = 0; dyi < 3; ++dyi) {
+            uint32_t aa = a0 + dyi * h.row_bytes;
+            uint32_t bb = RES ? smem_u32(wres + ((dyi * 3 + dxi) * p.cblocks + cb) * B_TILE)
+                              : a0 + h.a_bytes + dyi * B_TILE;
+#pragma unroll
+            for (int k = 0; k < ROW_BYTES / 32; ++k) {
+              tc_mma<KIND>(tmem_d, sw128_desc(aa + 32 * k), sw128_desc(bb + 32 * k), idesc,
+                           first ? 0u : 1u);
+              first = false;
+            }
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == h.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int mt = tile % p.num_m_tiles, nt = tile / p.num_m_tiles;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t m = int64_t(mt) * BM + row;
+      const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
+      epilogue_tile<KIND, BN>(p, tbase, m, nt);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -744,6 +921,43 @@ int launch_bn(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, c
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_tc");
 }
 
+template <int KIND, int BN, bool RES>
+int launch_halo_bn(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a,
+                   const HaloArgs& h, size_t smem, cudaStream_t st) {
+  auto kern = k_conv_halo<KIND, BN, RES>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  int tiles = a.num_m_tiles * a.num_n_tiles;
+  int grid = tiles < nsm ? tiles : nsm;
+  kern<<<grid, NUM_THREADS, smem, st>>>(mA, mB, a, h);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_halo");
+}
+
+template <int KIND>
+int launch_halo(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, const HaloArgs& h,
+                size_t smem, cudaStream_t st) {
+#define HALO_CASE(BNV)                                                    \
+  case BNV:                                                               \
+    return h.res ? launch_halo_bn<KIND, BNV, true>(mA, mB, a, h, smem, st) \
+                 : launch_halo_bn<KIND, BNV, false>(mA, mB, a, h, smem, st);
+  switch (a.bn) {
+    HALO_CASE(16)
+    HALO_CASE(32)
+    HALO_CASE(64)
+    HALO_CASE(128)
+    HALO_CASE(256)
+  }
+#undef HALO_CASE
+  return fail(DRCB_ECONFIG, "unsupported N tile (halo)");
+}
+
 // stage counts keep smem <= ~200 KB: BN=256 -> 48 KB/stage
 template <int KIND>
 int launch_conv(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, cudaStream_t st) {
@@ -805,6 +1019,26 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     }
   }
   CUtensorMap mA, mB;
+  if (hw >= 16 && !getenv("DRCB_NO_HALO")) {
+    // row-halo kernel: box of rows+2 image rows per (chunk, dx) stage
+    HaloArgs hz;
+    hz.row_bytes = hw * ROW_BYTES;
+    hz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
+    const int b_tile = a.bn * ROW_BYTES;
+    const int w_bytes = 9 * a.cblocks * b_tile;
+    const int budget = 200 * 1024;
+    hz.res = (a.num_n_tiles == 1 && w_bytes + 3 * hz.a_bytes <= budget) ? 1 : 0;
+    int stage_bytes = hz.a_bytes + (hz.res ? 0 : 3 * b_tile);
+    hz.stages = std::min(8, (budget - (hz.res ? w_bytes : 0)) / stage_bytes);
+    if (hz.stages >= 2) {
+      rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, hw, a.rows_per_tile + 2, 1);
+      if (rc) return rc;
+      rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
+      if (rc) return rc;
+      size_t smem = 1024 + size_t(hz.res ? w_bytes : 0) + size_t(hz.stages) * stage_bytes + 256;
+      return launch_halo<KIND>(mA, mB, a, hz, smem, st);
+    }
+  }
   int box_w = hw, box_h = a.maps_per_tile == 1 ? a.rows_per_tile : hw, box_n = a.maps_per_tile;
   rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, box_w, box_h, box_n);
   if (rc) return rc;
