@@ -87,6 +87,9 @@ typedef struct DrcbRenderCfg {
                              summation grouping (cache.py:399-413) */
   int32_t include_background; /* direct pass: add env seen by camera chains
                                  (render(mode="direct") = 1; render_drc = 0) */
+  int32_t map_spp;        /* sampler spp of map paths (render_drc: 1; dataset
+                             reference mode: ref_spp, dataset.py:92) */
+  int32_t reserved;
   uint64_t seed;
 } DrcbRenderCfg;
 
@@ -178,6 +181,18 @@ int drcb_render_drc(const DrcbScene *scene, const DrcbNet *net,
                     const uint64_t *keys_host, int64_t n_points, int32_t r_final,
                     int32_t net_mode, void *image, int64_t *telemetry_host,
                     void *stream);
+
+/* render(mode="pt") (drc/integrators.py:678-722): spp = cfg->direct_spp
+ * jittered paths per pixel (max_path_depth, rr_start), image (H*W,3) Real. */
+int drcb_render_pt(const DrcbScene *scene, const DrcbCamera *cam, const DrcbRenderCfg *cfg,
+                   void *image, int64_t *nonfinite, void *stream);
+
+/* _reference_map (drc/dataset.py:107-127): ground-truth radiance map of one
+ * cache point (pos/nrm (3,) Real device, front-facing), ref_spp paths per
+ * texel with the cfg sampler; out (32*32,3) Real, texel order v*32+u. */
+int drcb_reference_map(const DrcbScene *scene, const DrcbRenderCfg *cfg, const void *pos,
+                       const void *nrm, uint64_t key, int32_t ref_spp, void *out,
+                       int64_t *nonfinite, void *stream);
 
 /* ---- network ---------------------------------------------------------- */
 /* DRCW container parse + validation (drc/cnn.py:221-281): host bytes. */

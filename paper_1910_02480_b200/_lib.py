@@ -48,7 +48,8 @@ class RenderCfg(C.Structure):
         ("direct_spp", C.c_int32), ("max_path_depth", C.c_int32),
         ("mis_samples", C.c_int32), ("rr_start", C.c_int32),
         ("sampler_kind", C.c_int32), ("precision", C.c_int32),
-        ("tile", C.c_int32), ("include_background", C.c_int32), ("seed", C.c_uint64),
+        ("tile", C.c_int32), ("include_background", C.c_int32),
+        ("map_spp", C.c_int32), ("reserved", C.c_int32), ("seed", C.c_uint64),
     ]
 
 
@@ -81,6 +82,9 @@ _SIGS = [
                                         vp, vp, vp, vp, C.c_int64, C.c_int32, vp, vp, vp]),
     ("drcb_render_drc", C.c_int, [vp, vp, C.POINTER(Camera), C.POINTER(RenderCfg), vp, vp, vp,
                                   C.c_int64, C.c_int32, C.c_int32, vp, vp, vp]),
+    ("drcb_render_pt", C.c_int, [vp, C.POINTER(Camera), C.POINTER(RenderCfg), vp, vp, vp]),
+    ("drcb_reference_map", C.c_int, [vp, C.POINTER(RenderCfg), vp, vp, C.c_uint64, C.c_int32, vp,
+                                     vp, vp]),
     ("drcb_net_create", C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(vp)]),
     ("drcb_net_destroy", None, [vp]),
     ("drcb_net_info", C.c_int, [vp, C.POINTER(C.c_int64)]),

@@ -429,6 +429,37 @@ extern "C" int drcb_render_drc(const DrcbScene* scene, const DrcbNet* net, const
                              net_mode, (float*)image, telemetry_host, S_(stream));
 }
 
+extern "C" int drcb_render_pt(const DrcbScene* scene, const DrcbCamera* cam,
+                              const DrcbRenderCfg* cfg, void* image, int64_t* nonfinite,
+                              void* stream) {
+  NEED(scene);
+  NEED(cam);
+  NEED(image);
+  if (check_cfg(cfg)) return DRCB_ECONFIG;
+  DevCamera C = make_camera(*cam);
+  if (cfg->precision == 64)
+    return launch_pt_frame<double>(scene->dev, C, *cfg, cfg->direct_spp, cfg->tile,
+                                   (double*)image, nonfinite, S_(stream));
+  return launch_pt_frame<float>(scene->dev, C, *cfg, cfg->direct_spp, cfg->tile, (float*)image,
+                                nonfinite, S_(stream));
+}
+
+extern "C" int drcb_reference_map(const DrcbScene* scene, const DrcbRenderCfg* cfg,
+                                  const void* pos, const void* nrm, uint64_t key, int32_t ref_spp,
+                                  void* out, int64_t* nonfinite, void* stream) {
+  NEED(scene);
+  NEED(pos);
+  NEED(nrm);
+  NEED(out);
+  if (check_cfg(cfg)) return DRCB_ECONFIG;
+  if (ref_spp < 1) return fail(DRCB_ECONFIG, "ref_spp must be >= 1");
+  if (cfg->precision == 64)
+    return launch_reference_map<double>(scene->dev, *cfg, (const double*)pos, (const double*)nrm,
+                                        key, ref_spp, (double*)out, nonfinite, S_(stream));
+  return launch_reference_map<float>(scene->dev, *cfg, (const float*)pos, (const float*)nrm, key,
+                                     ref_spp, (float*)out, nonfinite, S_(stream));
+}
+
 extern "C" int drcb_net_forward(const DrcbNet* net, const float* x, float* y, int64_t n,
                                 int32_t mode, void* stream) {
   NEED(net);

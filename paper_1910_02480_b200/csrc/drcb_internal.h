@@ -28,6 +28,12 @@ struct SceneStats {
   int64_t n_prims = 0, n_nodes = 0, n_leaves = 0, max_depth = 0, n_lights = 0, bytes = 0, n_refs = 0;
 };
 
+template <typename R>
+int launch_pt_frame(const DevScene& S, const DevCamera& C, const DrcbRenderCfg& cfg, int spp,
+                    int tile, R* image, int64_t* nonfinite, cudaStream_t st);
+template <typename R>
+int launch_reference_map(const DevScene& S, const DrcbRenderCfg& cfg, const R* pos, const R* nrm,
+                         uint64_t key, int ref_spp, R* out, int64_t* nonfinite, cudaStream_t st);
 }  // namespace drcb
 
 struct DrcbScene {
@@ -76,4 +82,10 @@ int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& 
                             const int32_t* e_px, const int32_t* e_py, const R* e_n,
                             const R* e_rad, int64_t m, const int* m_dev, int r,
                             const R* direct, R* image, cudaStream_t st);
+template <typename R>
+int launch_pt_frame(const DevScene& S, const DevCamera& C, const DrcbRenderCfg& cfg, int spp,
+                    int tile, R* image, int64_t* nonfinite, cudaStream_t st);
+template <typename R>
+int launch_reference_map(const DevScene& S, const DrcbRenderCfg& cfg, const R* pos, const R* nrm,
+                         uint64_t key, int ref_spp, R* out, int64_t* nonfinite, cudaStream_t st);
 }  // namespace drcb

@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(MAP_TPB, 3) k_map_paths(DevScene S, DrcbRender
       V3<R> nf3 = facing ? -h.normal : h.normal;
       dist[job] = h.hit ? h.t : R(0);
       st3(nloc + 3 * job, h.hit ? fr.to_local(nf3) : mk<R>(R(0), R(0), R(0)));
-      rng.init(cfg.seed, keys[p], uint64_t(tex), cfg.sampler_kind, 1u);
+      rng.init(cfg.seed, keys[p], uint64_t(tex), cfg.sampler_kind,
+               uint32_t(cfg.map_spp > 1 ? cfg.map_spp : 1));
       L = mk<R>(R(0), R(0), R(0));
       beta = mk<R>(R(1), R(1), R(1));
       seg = 0;
@@ -291,6 +292,83 @@ __global__ void k_point_frames(DevScene S, const R* __restrict__ nrm, int64_t n,
   st3(frames + 9 * p, fr.t);
   st3(frames + 9 * p + 3, fr.b);
   st3(frames + 9 * p + 6, fr.n);
+}
+
+// render(mode="pt") (integrators.py:678-722): spp jittered camera paths per
+// pixel through trace_radiance_batch, summed in the reference's per-tile
+// sample chunks, averaged. One thread per pixel.
+template <typename R>
+__global__ void __launch_bounds__(TPB) k_pt_frame(DevScene S, DevCamera C, DrcbRenderCfg cfg,
+                                                   int spp, int tile, R* image,
+                                                   int64_t* nonfinite) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int nf = 0;
+  if (i < int64_t(C.W) * C.H) {
+    int x = int(i % C.W), y = int(i / C.W);
+    V3<R> cam = ld3<R>(C.pos);
+    int tx0 = (x / tile) * tile, ty0 = (y / tile) * tile;
+    int tw = min(tile, C.W - tx0), th = min(tile, C.H - ty0);
+    int chunk = max(1, 16384 / (tw * th));
+    PathRng rng;
+    V3<R> acc = {R(0), R(0), R(0)};
+    for (int s0 = 0; s0 < spp; s0 += chunk) {
+      int ns = min(chunk, spp - s0);
+      V3<R> part;
+      for (int s = s0; s < s0 + ns; ++s) {
+        rng.init(cfg.seed, uint64_t(i), uint64_t(s), cfg.sampler_kind, uint32_t(spp > 1 ? spp : 1));
+        R jx = to_unit<R>(rng.sample(0)), jy = to_unit<R>(rng.sample(1));
+        V3<R> d = camera_dir<R>(C, R(x) + jx, R(y) + jy);
+        V3<R> l = trace_path<R>(S, cam, d, rng, cfg.max_path_depth, false, cfg.rr_start, nullptr, nf);
+        part = (s == s0) ? l : part + l;
+      }
+      acc = acc + part;
+    }
+    st3(image + 3 * i, divs(acc, R(spp)));
+  }
+  if (nonfinite) add_nonfinite(nonfinite, nf);
+}
+
+// _reference_map (dataset.py:107-127): ref_spp paths per texel of one cache
+// point (pixel key = texel + key * 4096, sample key = s), skip first emission;
+// one thread per (texel, 16-sample chunk) writes the chunk's sequential sum.
+template <typename R>
+__global__ void __launch_bounds__(TPB) k_reference_chunks(DevScene S, DrcbRenderCfg cfg,
+                                                           const R* __restrict__ pos,
+                                                           const R* __restrict__ nrm,
+                                                           uint64_t key, int ref_spp, int chunk,
+                                                           int nchunks, R* partial,
+                                                           int64_t* nonfinite) {
+  int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int nf = 0;
+  if (g < int64_t(nchunks) * MAP_TEXELS) {
+    int tex = int(g % MAP_TEXELS), c = int(g / MAP_TEXELS);
+    V3<R> hp = ldr3(pos), hn = ldr3(nrm);
+    Frame<R> fr = frame_scalar(S, hn);
+    V3<R> D = fr.to_world(texel_local<R>(tex % MAP_RES, tex / MAP_RES));
+    V3<R> O = hp + R(T_EPS) * hn;
+    uint64_t pix = uint64_t(tex) + key * uint64_t(1 << 12);
+    int s0 = c * chunk, ns = min(chunk, ref_spp - s0);
+    PathRng rng;
+    V3<R> part = {R(0), R(0), R(0)};
+    for (int s = s0; s < s0 + ns; ++s) {
+      rng.init(cfg.seed, pix, uint64_t(s), cfg.sampler_kind, uint32_t(ref_spp > 1 ? ref_spp : 1));
+      V3<R> l = trace_path<R>(S, O, D, rng, cfg.max_path_depth, true, cfg.rr_start, nullptr, nf);
+      part = (s == s0) ? l : part + l;
+    }
+    st3(partial + 3 * g, part);
+  }
+  if (nonfinite) add_nonfinite(nonfinite, nf);
+}
+
+// total = ((0 + chunk_0) + chunk_1) + ... ; map = total / ref_spp
+template <typename R>
+__global__ void k_reference_reduce(const R* __restrict__ partial, int nchunks, int ref_spp,
+                                   R* out) {
+  int tex = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tex >= MAP_TEXELS) return;
+  V3<R> tot = {R(0), R(0), R(0)};
+  for (int c = 0; c < nchunks; ++c) tot = tot + ldr3(partial + 3 * (int64_t(c) * MAP_TEXELS + tex));
+  st3(out + 3 * tex, divs(tot, R(ref_spp)));
 }
 
 // numpy pairwise summation of 1024 contiguous values (8-accumulator blocks of
@@ -833,6 +911,32 @@ int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& 
   return 0;
 }
 
+template <typename R>
+int launch_pt_frame(const DevScene& S, const DevCamera& C, const DrcbRenderCfg& cfg, int spp,
+                    int tile, R* image, int64_t* nonfinite, cudaStream_t st) {
+  int64_t n = int64_t(C.W) * C.H;
+  if (n <= 0) return 0;
+  k_pt_frame<R><<<nblocks(n), TPB, 0, st>>>(S, C, cfg, spp, tile, image, nonfinite);
+  LAUNCH_CHECK();
+  return 0;
+}
+
+template <typename R>
+int launch_reference_map(const DevScene& S, const DrcbRenderCfg& cfg, const R* pos, const R* nrm,
+                         uint64_t key, int ref_spp, R* out, int64_t* nonfinite, cudaStream_t st) {
+  const int chunk = std::max(1, (1 << 14) / MAP_TEXELS);  // dataset.py:114
+  const int nchunks = (ref_spp + chunk - 1) / chunk;
+  R* partial = nullptr;
+  DRCB_CUDA(cudaMallocAsync((void**)&partial, sizeof(R) * 3 * size_t(nchunks) * MAP_TEXELS, st));
+  k_reference_chunks<R><<<nblocks(int64_t(nchunks) * MAP_TEXELS), TPB, 0, st>>>(
+      S, cfg, pos, nrm, key, ref_spp, chunk, nchunks, partial, nonfinite);
+  LAUNCH_CHECK();
+  k_reference_reduce<R><<<nblocks(MAP_TEXELS), TPB, 0, st>>>(partial, nchunks, ref_spp, out);
+  LAUNCH_CHECK();
+  DRCB_CUDA(cudaFreeAsync(partial, st));
+  return 0;
+}
+
 #define INST(R)                                                                                  \
   template int launch_intersect<R>(const DevScene&, const R*, const R*, int64_t, const R*,      \
                                    const R*, int, uint8_t*, R*, int64_t*, int32_t*, R*, R*,     \
@@ -861,6 +965,16 @@ int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& 
 
 INST(float)
 INST(double)
+template int launch_pt_frame<float>(const DevScene&, const DevCamera&, const DrcbRenderCfg&, int,
+                                    int, float*, int64_t*, cudaStream_t);
+template int launch_pt_frame<double>(const DevScene&, const DevCamera&, const DrcbRenderCfg&, int,
+                                     int, double*, int64_t*, cudaStream_t);
+template int launch_reference_map<float>(const DevScene&, const DrcbRenderCfg&, const float*,
+                                         const float*, uint64_t, int, float*, int64_t*,
+                                         cudaStream_t);
+template int launch_reference_map<double>(const DevScene&, const DrcbRenderCfg&, const double*,
+                                          const double*, uint64_t, int, double*, int64_t*,
+                                          cudaStream_t);
 
 }  // namespace drcb
 

@@ -316,7 +316,21 @@ def render(scene, config, mode="pt", weights=None, interrupt=None):
         return direct.double().cpu().numpy(), {"mode": "direct", "spp": config.direct_spp,
                                                "seconds": time.time() - t0,
                                                "nonfinite": int(nf.item())}
-    raise ConfigError("mode 'pt' is not on the B200 hot path yet (SURVEY §8f item 2)")
+    # mode == "pt": spp jittered paths per pixel (integrators.py:678-722)
+    t0 = time.time()
+    torch = _torch()
+    prec = int(getattr(config, "precision", 64))
+    dtype = torch.float64 if prec == 64 else torch.float32
+    w, h = scene.camera.resolution
+    image = torch.empty((h, w, 3), dtype=dtype, device="cuda")
+    nf = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cfg = _cfg_struct(config, prec)
+    cfg.direct_spp = int(config.spp)
+    _lib.call("drcb_render_pt", device_scene(scene).handle, C.byref(camera_struct(scene.camera)),
+              C.byref(cfg), _lib.ptr(image), _lib.ptr(nf), _lib.stream_ptr())
+    return image.double().cpu().numpy(), {"mode": "pt", "spp": config.spp,
+                                          "seconds": time.time() - t0,
+                                          "nonfinite": int(nf.item())}
 
 
 # ---------------------------------------------------------------------------

@@ -16,8 +16,8 @@ def pytest_configure(config):
 
 def load_golden(name):
     d = dict(np.load(os.path.join(GOLDEN, name), allow_pickle=False))
-    for k in ("doc", "cfg"):
-        if k in d:
+    for k in list(d):
+        if k == "cfg" or k.startswith("doc"):
             d[k] = json.loads(bytes(d[k]).decode("utf-8"))
     return d
 

@@ -204,7 +204,7 @@ def main():
     frame_fixture("frame_furnace.npz", env, 8, 1, dict(direct_spp=2, indirect_tasks=1, mis_samples=8))
 
 
-if __name__ == "__main__" and "--train" not in sys.argv:
+if __name__ == "__main__" and not ({"--train", "--pt"} & set(sys.argv)):
     main()
 
 
@@ -250,3 +250,25 @@ def train_fixture():
 
 if __name__ == "__main__" and "--train" in sys.argv:
     train_fixture()
+
+
+def pt_dataset_fixture():
+    """render(mode="pt") and reference-mode examples (dataset.py:53-127)."""
+    from drc.dataset import generate_examples
+
+    doc = ref_scene_doc("cornell", 24)
+    scene = parse_scene(json.dumps(doc))
+    cfg = RenderConfig(threads=1, spp=3, max_path_depth=5, rr_start=3, seed=4)
+    img, _ = rint.render(scene, cfg, "pt")
+    doc2 = ref_scene_doc("glossybox", 16)
+    scene2 = parse_scene(json.dumps(doc2))
+    cfg2 = RenderConfig(threads=1, max_path_depth=4, rr_start=3)
+    ex = generate_examples(scene2, (2, 2), 256, seed=5, config=cfg2)
+    save("pt_dataset.npz", doc=doc_array(doc), pt=img, doc2=doc_array(doc2),
+         ex_input=np.stack([e.input for e in ex]), ex_target=np.stack([e.target for e in ex]),
+         ex_sr=np.array([e.s_r for e in ex]), ex_sd=np.array([e.s_d for e in ex]),
+         ex_pixel=np.array([e.pixel for e in ex]))
+
+
+if __name__ == "__main__" and "--pt" in sys.argv:
+    pt_dataset_fixture()
