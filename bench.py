@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--cpu-points", type=int, default=16)
     ap.add_argument("--cpu-pixels", type=int, default=4096)
     ap.add_argument("--streams", type=int, default=2)
+    ap.add_argument("--direct-spp", type=int, default=0)
     return ap.parse_args()
 
 
@@ -175,12 +176,13 @@ def main():
     from paper_1910_02480_b200 import cnn, render, scenegen
 
     res, _, _, _, _, wseed = scenegen.CONFIGS[args.config]
-    cfg = render.RenderConfig(direct_spp=1, indirect_tasks=args.tasks, mis_samples=16,
+    direct_spp = args.direct_spp or (4 if args.config == "c4" else 1)  # BASELINE config 4: 4 spp
+    cfg = render.RenderConfig(direct_spp=direct_spp, indirect_tasks=args.tasks, mis_samples=16,
                               max_path_depth=8, rr_start=5, seed=0, precision=args.precision,
                               net_mode=args.net if args.net in ("fp32", "tf32", "bf16") else "fp32")
     workload = {"workload": f"{args.config}: DRC frames {res[0]}x{res[1]}, "
                             f"{args.frames} frames/rank/step, indirect_tasks={args.tasks}, "
-                            f"direct_spp=1, orbit cameras r=3 (seed 2)",
+                            f"direct_spp={direct_spp}, orbit cameras r=3 (seed 2)",
                 "scene_tris": None, "cache_points_per_frame": None,
                 "precision": f"rays fp{args.precision}, U-Net {cfg.net_mode}",
                 "l2": "flushed between steps (256 MB write)"}

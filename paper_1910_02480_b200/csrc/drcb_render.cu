@@ -147,6 +147,60 @@ __global__ void __launch_bounds__(TPB) k_gbuffer_direct(DevScene S, DevCamera C,
   if (nonfinite) add_nonfinite(nonfinite, nf);
 }
 
+// Split form of the direct pass: one thread per pixel for the centre chain,
+// one thread per (pixel, sample) for the jittered li_direct paths, and an
+// ordered per-pixel reduction that sums samples in the reference's per-tile
+// chunks ((s0 + s1 + ...) per chunk, chunks accumulated from 0) and divides
+// by direct_spp (cache.py:399-413).
+template <typename R>
+__global__ void __launch_bounds__(TPB) k_gbuffer(DevScene S, DevCamera C, DrcbGBuffer gb) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(C.W) * C.H) return;
+  int x = int(i % C.W), y = int(i / C.W);
+  V3<R> dc = camera_dir<R>(C, R(x) + R(0.5), R(y) + R(0.5));
+  store_chain(gb, i, primary_chain(S, ld3<R>(C.pos), dc));
+}
+
+template <typename R>
+__global__ void __launch_bounds__(TPB) k_direct_samples(DevScene S, DevCamera C, DrcbRenderCfg cfg,
+                                                         R* samples, int64_t* nonfinite) {
+  const int spp = cfg.direct_spp;
+  const int64_t npx = int64_t(C.W) * C.H;
+  int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int nf = 0;
+  if (g < npx * spp) {
+    int64_t i = g % npx;  // sample-major: neighbouring threads trace neighbouring pixels
+    int s = int(g / npx);
+    int x = int(i % C.W), y = int(i / C.W);
+    PathRng rng;
+    rng.init(cfg.seed, uint64_t(i), uint64_t(s), cfg.sampler_kind, uint32_t(spp > 1 ? spp : 1));
+    R jx = to_unit<R>(rng.sample(0)), jy = to_unit<R>(rng.sample(1));
+    V3<R> d = camera_dir<R>(C, R(x) + jx, R(y) + jy);
+    st3(samples + 3 * g, direct_path(S, ld3<R>(C.pos), d, rng, cfg.include_background != 0, nf));
+  }
+  if (nonfinite) add_nonfinite(nonfinite, nf);
+}
+
+template <typename R>
+__global__ void k_direct_reduce(DevCamera C, int spp, int tile, const R* __restrict__ samples,
+                                R* direct) {
+  const int64_t npx = int64_t(C.W) * C.H;
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= npx) return;
+  int x = int(i % C.W), y = int(i / C.W);
+  int tx0 = (x / tile) * tile, ty0 = (y / tile) * tile;
+  int tw = min(tile, C.W - tx0), th = min(tile, C.H - ty0);
+  int chunk = max(1, 16384 / (tw * th));
+  V3<R> acc = {R(0), R(0), R(0)};
+  for (int s0 = 0; s0 < spp; s0 += chunk) {
+    int ns = min(chunk, spp - s0);
+    V3<R> part = ldr3(samples + 3 * (int64_t(s0) * npx + i));
+    for (int s = s0 + 1; s < s0 + ns; ++s) part = part + ldr3(samples + 3 * (int64_t(s) * npx + i));
+    acc = acc + part;
+  }
+  st3(direct + 3 * i, divs(acc, R(spp)));
+}
+
 // Map paths of all cache points (hemimap.py:236-262 + integrators.py:175-302)
 // as a persistent kernel with per-lane path regeneration: a lane whose path
 // terminates (escape, RR, max depth) immediately takes the next texel from a
@@ -822,8 +876,16 @@ int launch_gbuffer_direct(const DevScene& S, const DevCamera& C, const DrcbRende
                           cudaStream_t st) {
   int64_t n = int64_t(C.W) * C.H;
   if (n <= 0) return 0;
-  k_gbuffer_direct<R><<<nblocks(n), TPB, 0, st>>>(S, C, cfg, tile, gb, direct, nonfinite);
+  k_gbuffer<R><<<nblocks(n), TPB, 0, st>>>(S, C, gb);
   LAUNCH_CHECK();
+  const int spp = cfg.direct_spp;
+  R* samples = nullptr;
+  DRCB_CUDA(cudaMallocAsync((void**)&samples, sizeof(R) * 3 * size_t(n) * spp, st));
+  k_direct_samples<R><<<nblocks(n * spp), TPB, 0, st>>>(S, C, cfg, samples, nonfinite);
+  LAUNCH_CHECK();
+  k_direct_reduce<R><<<nblocks(n), TPB, 0, st>>>(C, spp, tile, samples, direct);
+  LAUNCH_CHECK();
+  DRCB_CUDA(cudaFreeAsync(samples, st));
   return 0;
 }
 
