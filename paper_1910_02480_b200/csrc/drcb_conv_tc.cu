@@ -167,6 +167,26 @@ __host__ __device__ constexpr uint32_t make_idesc(int kind, int M, int N) {
   return (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
+// src = max((o + 0.5)/2 - 0.5, 0) in closed form (no int<->float
+// conversions on the XU pipe): o = 0 -> (0, 1, 0); o = 2i (i >= 1) ->
+// (i-1, i, 0.75); o = 2i+1 -> (i, min(i+1, n-1), 0.25)
+__device__ __forceinline__ void up_w(int o, int n, int& i0, int& i1, float& fr) {
+  const int i = o >> 1;
+  if (o & 1) {
+    i0 = i;
+    i1 = min(i + 1, n - 1);
+    fr = 0.25f;
+  } else if (o == 0) {
+    i0 = 0;
+    i1 = min(1, n - 1);
+    fr = 0.f;
+  } else {
+    i0 = i - 1;
+    i1 = i;
+    fr = 0.75f;
+  }
+}
+
 constexpr int BM = 128;
 constexpr int NUM_THREADS = 192;  // 6 warps
 constexpr int ROW_BYTES = 128;    // one swizzle row = one K stage per operand row
@@ -189,6 +209,11 @@ struct ConvArgs {
   float* pred;                            // (maps,3,32,32) fp32 when head
   float hw_w[3 * 16];                     // conv_out weights (3, 16)
   float hw_b[3];
+  // fused bilinear 2x upsample (tiles holding whole maps): when up_out is
+  // set, the epilogue writes up2x(output) into up_out's leading channel
+  // slice (up_ctot channels per pixel) instead of the low-res tensor
+  void* up_out;
+  int up_ctot;
 };
 
 template <int KIND, int BN, int STAGES>
@@ -197,14 +222,18 @@ struct Smem {
   static constexpr int A_BYTES = BM * ROW_BYTES;
   static constexpr int B_BYTES = BN * ROW_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int STAGING = BM * 16 * 4;  // one 16-channel chunk, fp32, for the fused upsample
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + STAGING;
 };
 
 // Epilogue of one 128 x BN accumulator tile held in TMEM: tcgen05.ld, folded
 // BN + LeakyReLU, NHWC store into the destination slice; for the head layer
 // the fused 1x1 conv_out + ReLU writes fp32 NCHW predictions.
+__device__ __forceinline__ void epi_barrier() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 template <int KIND, int BN>
-__device__ __forceinline__ void epilogue_tile(const ConvArgs& p, uint32_t tbase, int64_t m, int nt) {
+__device__ __forceinline__ void epilogue_tile(const ConvArgs& p, uint32_t tbase, int64_t m, int nt,
+                                              float* staging = nullptr) {
       if (p.head) {
     // head.deconv2 (BN == 16 channels) + BN + LeakyReLU, then the fused
     // 1x1 conv_out + ReLU -> fp32 NCHW prediction (cnn.py:209-215)
@@ -239,6 +268,64 @@ __device__ __forceinline__ void epilogue_tile(const ConvArgs& p, uint32_t tbase,
       for (int j = 0; j < 16; ++j) {
         float x = __uint_as_float(r[j]) * __ldg(p.ep_a + cg + j) + __ldg(p.ep_b + cg + j);
         v[j] = x >= 0.f ? x : p.slope * x;
+      }
+      if (staging) {
+        // fused bilinear 2x upsample of this 16-channel chunk: stage the
+        // stored-precision values of all 128 tile pixels (whole maps), then
+        // each thread emits 4 of the tile's 512 output pixels
+        const int row = int(m % BM);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if constexpr (KIND == 0) staging[j * BM + row] = __bfloat162float(__float2bfloat16_rn(v[j]));
+          else staging[j * BM + row] = round_tf32(v[j]);
+        }
+        epi_barrier();
+        const int hw = p.hw, ho = 2 * hw, per_map = ho * ho;
+        const int64_t tile_map0 = (m / BM) * (BM / (hw * hw));
+#pragma unroll 1
+        for (int r = 0; r < 4; ++r) {
+          const int oi = row + BM * r;
+          const int mp = oi / per_map, opos = oi % per_map;
+          const int oy = opos / ho, ox = opos % ho;
+          int r0, r1, c0i, c1i;
+          float fr, fc;
+          up_w(oy, hw, r0, r1, fr);
+          up_w(ox, hw, c0i, c1i, fc);
+          const float omr = 1.f - fr, omc = 1.f - fc;
+          const int sb = mp * hw * hw;
+          const int i00 = sb + r0 * hw + c0i, i10 = sb + r1 * hw + c0i;
+          const int i01 = sb + r0 * hw + c1i, i11 = sb + r1 * hw + c1i;
+          float o[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float* s = staging + j * BM;
+            float t0 = __fadd_rn(__fmul_rn(s[i00], omr), __fmul_rn(s[i10], fr));
+            float t1 = __fadd_rn(__fmul_rn(s[i01], omr), __fmul_rn(s[i11], fr));
+            o[j] = __fadd_rn(__fmul_rn(t0, omc), __fmul_rn(t1, fc));
+          }
+          const int64_t opix = (tile_map0 + mp) * per_map + opos;
+          if constexpr (KIND == 0) {
+            uint32_t pk[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(o[2 * j], o[2 * j + 1]);
+              pk[j] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.up_out) +
+                                                  opix * p.up_ctot + cg);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          } else {
+            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.up_out) +
+                                                    opix * p.up_ctot + cg);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              dst[j] = make_float4(round_tf32(o[4 * j]), round_tf32(o[4 * j + 1]),
+                                   round_tf32(o[4 * j + 2]), round_tf32(o[4 * j + 3]));
+          }
+        }
+        epi_barrier();
+        continue;
       }
       if constexpr (KIND == 0) {
         uint32_t pk[8];
@@ -278,6 +365,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  float* staging = reinterpret_cast<float*>(smem + STAGES * SM::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (warp == 0 && lane == 0) {
@@ -384,7 +472,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int64_t m = int64_t(mt) * BM + row;
       const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
-      epilogue_tile<KIND, BN>(p, tbase, m, nt);
+      epilogue_tile<KIND, BN>(p, tbase, m, nt, p.up_out ? staging : nullptr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -681,26 +769,6 @@ __global__ void __launch_bounds__(256) k_pool_nhwc(const T* __restrict__ in, int
   }
 }
 
-// src = max((o + 0.5)/2 - 0.5, 0) in closed form (no int<->float
-// conversions on the XU pipe): o = 0 -> (0, 1, 0); o = 2i (i >= 1) ->
-// (i-1, i, 0.75); o = 2i+1 -> (i, min(i+1, n-1), 0.25)
-__device__ __forceinline__ void up_w(int o, int n, int& i0, int& i1, float& fr) {
-  const int i = o >> 1;
-  if (o & 1) {
-    i0 = i;
-    i1 = min(i + 1, n - 1);
-    fr = 0.25f;
-  } else if (o == 0) {
-    i0 = 0;
-    i1 = min(1, n - 1);
-    fr = 0.f;
-  } else {
-    i0 = i - 1;
-    i1 = i;
-    fr = 0.75f;
-  }
-}
-
 // bilinear 2x (align_corners=False) of an NHWC buffer (C channels) into the
 // leading channel slice of the decoder concat buffer (cnn.py:159-174), rows
 // then columns like the reference; compile-time shapes, one thread per
@@ -980,7 +1048,7 @@ struct Buf {
 // one conv layer: in (NHWC, c_in_tot == layer cin_pad) -> out slice
 template <int KIND>
 int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cout_off,
-              int64_t nmaps, cudaStream_t st, float* pred = nullptr) {
+              int64_t nmaps, cudaStream_t st, float* pred = nullptr, const Buf* up = nullptr) {
   int rc = prepare_layer(net, L, KIND);
   if (rc) return rc;
   if (in.c != L.cin_pad) return fail(DRCB_ECONTRACT, "tc layer input channels mismatch for " + L.name);
@@ -1009,6 +1077,11 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
   a.ep_b = L.d_ep_b;
   a.slope = net.slope;
   a.out = out.p;
+  if (up) {
+    if (hw * hw > BM) return fail(DRCB_ECONTRACT, "fused upsample needs whole maps per tile");
+    a.up_out = up->p;
+    a.up_ctot = up->c;
+  }
   if (pred) {
     const ConvLayer& H = net.layers[16];
     a.head = 1;
@@ -1114,12 +1187,18 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
   rc |= run_layer<KIND>(net, Ls[5], B[7], B[8], 8 * k, np, st);   // s3 -> c3[8k:12k]
   pool(B[8], 8 * k, 4 * k, B[9]);
   rc |= run_layer<KIND>(net, Ls[6], B[9], B[10], 0, np, st);
-  rc |= run_layer<KIND>(net, Ls[7], B[10], B[11], 0, np, st);
+  // bott.conv2 and dec3.deconv2 tiles hold whole maps, so their epilogues
+  // can write the bilinear 2x upsample straight into the decoder concat
+  // buffers (DRCB_FUSED_UP=1). Measured on B200 at 4096 maps it is a wash
+  // (7.79 vs 7.71 ms per frame's network: the staged epilogue lengthens the
+  // tile tail more than the separate upsample pass costs), so it is opt-in.
+  const bool fuse7 = getenv("DRCB_FUSED_UP") != nullptr, fuse9 = fuse7;
+  rc |= run_layer<KIND>(net, Ls[7], B[10], B[11], 0, np, st, nullptr, fuse7 ? &B[8] : nullptr);
+  if (!fuse7) up(B[11], 8 * k, B[8]);
   // decoder
-  up(B[11], 8 * k, B[8]);
   rc |= run_layer<KIND>(net, Ls[8], B[8], B[7], 0, np, st);
-  rc |= run_layer<KIND>(net, Ls[9], B[7], B[12], 0, np, st);
-  up(B[12], 4 * k, B[5]);
+  rc |= run_layer<KIND>(net, Ls[9], B[7], B[12], 0, np, st, nullptr, fuse9 ? &B[5] : nullptr);
+  if (!fuse9) up(B[12], 4 * k, B[5]);
   rc |= run_layer<KIND>(net, Ls[10], B[5], B[4], 0, np, st);
   rc |= run_layer<KIND>(net, Ls[11], B[4], B[13], 0, np, st);
   up(B[13], 2 * k, B[2]);

@@ -81,3 +81,16 @@ def test_tc_batch_sizes_and_padding():
     y13 = cnn.forward_batch(net, x, mode="bf16")
     y1 = np.concatenate([cnn.forward_batch(net, x[i:i + 1], mode="bf16") for i in range(13)])
     assert np.array_equal(y13, y1)
+
+
+@pytest.mark.parametrize("mode", ["bf16", "tf32"])
+def test_fused_upsample_epilogue_bit_identical(mode, monkeypatch):
+    # DRCB_FUSED_UP: bott.conv2 / dec3.deconv2 epilogues write the 2x
+    # upsample directly; it must reproduce the separate upsample pass exactly
+    rng = np.random.default_rng(7)
+    x = rng.uniform(0, 1, (11, 7, 32, 32)).astype(np.float32)
+    net = cnn.random_network(64, 2)
+    plain = cnn.forward_batch(net, x, mode=mode)
+    monkeypatch.setenv("DRCB_FUSED_UP", "1")
+    fused = cnn.forward_batch(net, x, mode=mode)
+    assert np.array_equal(plain, fused)
