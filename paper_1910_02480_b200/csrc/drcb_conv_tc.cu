@@ -80,6 +80,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1,
+                                             int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
                                             int c1, int c2, int c3) {
   asm volatile(
@@ -214,6 +225,7 @@ struct ConvArgs {
   // slice (up_ctot channels per pixel) instead of the low-res tensor
   void* up_out;
   int up_ctot;
+  int taps1;  // 1-tap (im2col input) GEMM: every K block uses the centre tap
 };
 
 template <int KIND, int BN, int STAGES>
@@ -231,21 +243,69 @@ struct Smem {
 // the fused 1x1 conv_out + ReLU writes fp32 NCHW predictions.
 __device__ __forceinline__ void epi_barrier() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-template <int KIND, int BN>
-__device__ __forceinline__ void epilogue_tile(const ConvArgs& p, uint32_t tbase, int64_t m, int nt,
-                                              float* staging = nullptr) {
-      if (p.head) {
-    // head.deconv2 (BN == 16 channels) + BN + LeakyReLU, then the fused
-    // 1x1 conv_out + ReLU -> fp32 NCHW prediction (cnn.py:209-215)
-    uint32_t r[16];
-    tmem_ld16(tbase, r);
+// 16 accumulator columns [c0, c0+16) of this thread's pixel. DX: the tile
+// holds three accumulators P_dx (dx = -1, 0, +1 at column offsets 0, BN, 2BN)
+// computed from the UNSHIFTED input row; the conv output is
+// P_-1(x-1) + P_0(x) + P_+1(x+1), the neighbours fetched from the adjacent
+// lanes (a warp's 32 TMEM lanes are 32 consecutive pixels of one or two
+// image rows) with zero beyond the row ends.
+template <int BN, bool DX>
+__device__ __forceinline__ void acc_chunk(uint32_t tbase, int c0, int x, int hw, float (&v)[16]) {
+  uint32_t r[16];
+  tmem_ld16(tbase + c0, r);
+  if constexpr (!DX) {
     tmem_wait_ld();
-    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+  } else {
+    uint32_t r0[16], r2[16];
+    tmem_ld16(tbase + BN + c0, r0);
+    tmem_ld16(tbase + 2 * BN + c0, r2);
+    tmem_wait_ld();
+    const bool has_l = x > 0, has_r = x < hw - 1;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      float x = __uint_as_float(r[j]) * __ldg(p.ep_a + j) + __ldg(p.ep_b + j);
-      v[j] = x >= 0.f ? x : p.slope * x;
+      float l = __shfl_up_sync(0xffffffffu, __uint_as_float(r[j]), 1);
+      float rt = __shfl_down_sync(0xffffffffu, __uint_as_float(r2[j]), 1);
+      float s = __uint_as_float(r0[j]);
+      if (has_l) s += l;
+      if (has_r) s += rt;
+      v[j] = s;
     }
+  }
+}
+
+// folded BN (scale a, shift b; 16-B aligned vectors) + LeakyReLU
+__device__ __forceinline__ void bn_lrelu16(const float (&acc)[16], const float* a, const float* b,
+                                           float slope, float (&v)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; j += 4) {
+    const float4 av = __ldg(reinterpret_cast<const float4*>(a + j));
+    const float4 bv = __ldg(reinterpret_cast<const float4*>(b + j));
+    const float aa[4] = {av.x, av.y, av.z, av.w}, bb[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      float x = acc[j + t] * aa[t] + bb[t];
+      v[j + t] = x >= 0.f ? x : slope * x;
+    }
+  }
+}
+
+// cbeg/cstep: the 16-column chunks this warp handles (several epilogue warps
+// may share one TMEM lane quarter)
+template <int KIND, int BN, bool DX = false>
+__device__ __forceinline__ void epilogue_tile(const ConvArgs& p, uint32_t tbase, int64_t m, int nt,
+                                              float* staging = nullptr, int cbeg = 0,
+                                              int cstep = 16) {
+  const int xpix = int(m % p.hw);
+  if (p.head) {
+    if (cbeg != 0) return;
+    // head.deconv2 (BN == 16 channels) + BN + LeakyReLU, then the fused
+    // 1x1 conv_out + ReLU -> fp32 NCHW prediction (cnn.py:209-215)
+    float acc[16];
+    acc_chunk<BN, DX>(tbase, 0, xpix, p.hw, acc);
+    float v[16];
+    bn_lrelu16(acc, p.ep_a, p.ep_b, p.slope, v);
     int64_t n = m / 1024;
     int pix = int(m % 1024);
 #pragma unroll
@@ -257,18 +317,13 @@ __device__ __forceinline__ void epilogue_tile(const ConvArgs& p, uint32_t tbase,
     }
   } else {
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t r[16];
-      tmem_ld16(tbase + c0, r);
-      tmem_wait_ld();
+    for (int c0 = cbeg; c0 < BN; c0 += cstep) {
       const int cg = nt * BN + c0;
       if (cg >= p.cout) break;
+      float acc[16];
+      acc_chunk<BN, DX>(tbase, c0, xpix, p.hw, acc);
       float v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        float x = __uint_as_float(r[j]) * __ldg(p.ep_a + cg + j) + __ldg(p.ep_b + cg + j);
-        v[j] = x >= 0.f ? x : p.slope * x;
-      }
+      bn_lrelu16(acc, p.ep_a + cg, p.ep_b + cg, p.slope, v);
       if (staging) {
         // fused bilinear 2x upsample of this 16-channel chunk: stage the
         // stored-precision values of all 128 tile pixels (whole maps), then
@@ -409,7 +464,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           y0 = 0;
         }
         for (int kb = 0; kb < p.num_kb; ++kb) {
-          int tap = kb / p.cblocks, cb = kb % p.cblocks;
+          int tap = p.taps1 ? 4 : kb / p.cblocks, cb = kb % p.cblocks;
           int dy = tap / 3 - 1, dx = tap % 3 - 1;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * SM::STAGE_BYTES;
@@ -660,6 +715,278 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// dx-in-N implicit GEMM for hw in {16, 32} (tiles = whole image rows).
+// One TMA box of rows+2 image rows per channel chunk is the ONLY activation
+// load (the (chunk, dx) halo kernel above loads it three times). For each dy
+// the A descriptor is shifted by dy*W*128 B and ONE MMA (two for BN = 128)
+// multiplies it by the three dx taps' weights stacked along N: the tile holds
+// three accumulators P_dx of the unshifted input, combined in the epilogue
+// (acc_chunk<BN, true>) as P_-1(x-1) + P_0(x) + P_+1(x+1). A ring and B ring
+// are separate: A stage = one chunk's halo box; B stage = one (chunk, dy)
+// triple of weight tiles (or the whole weight matrix resident, RES).
+// Epilogue into a SMEM staging tile for a TMA store: BN channels of 128
+// pixels as BN/CEL sub-tiles of [128 px][128 B], each in the SWIZZLE_128B
+// layout the output tensor map expects (16-B piece j of pixel r at
+// r*128 + ((j ^ (r & 7)) << 4)): the global write is one coalesced bulk
+// tensor store per sub-tile instead of 16-B scattered stores per thread.
+template <int KIND, int BN>
+__device__ __forceinline__ void epilogue_stage(const ConvArgs& p, uint32_t tbase, int64_t m, int nt,
+                                               uint8_t* ost, int cbeg, int cstep) {
+  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int CEL = ROW_BYTES / ELEM;
+  const int xpix = int(m % p.hw);
+  const int r = int(m % BM);
+#pragma unroll 1
+  for (int c0 = cbeg; c0 < BN; c0 += cstep) {
+    const int cg = nt * BN + c0;
+    float acc[16];
+    acc_chunk<BN, true>(tbase, c0, xpix, p.hw, acc);
+    float v[16];
+    bn_lrelu16(acc, p.ep_a + cg, p.ep_b + cg, p.slope, v);
+    uint8_t* sub = ost + (c0 / CEL) * (BM * ROW_BYTES) + r * ROW_BYTES;
+    const int jb = (c0 % CEL) * ELEM / 16;
+    if constexpr (KIND == 0) {
+      uint32_t pk[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+        pk[j] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      *reinterpret_cast<uint4*>(sub + (((jb + 0) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      *reinterpret_cast<uint4*>(sub + (((jb + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<float4*>(sub + (((jb + j) ^ (r & 7)) << 4)) =
+            make_float4(round_tf32(v[4 * j]), round_tf32(v[4 * j + 1]), round_tf32(v[4 * j + 2]),
+                        round_tf32(v[4 * j + 3]));
+    }
+  }
+}
+__device__ __forceinline__ void epi_bar256() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
+
+struct DxArgs {
+  int a_bytes;    // (rows+2) * W * 128
+  int row_bytes;  // W * 128: one dy shift
+  int sa, sb;     // A / B ring depths
+  int o_bytes;    // one output staging tile (BM * BN * elem); 0 = direct stores (head)
+};
+
+constexpr int DX_EPI_WARPS = 8;
+constexpr int DX_THREADS = 64 + 32 * DX_EPI_WARPS;
+
+template <int KIND, int BN, bool RES>
+__global__ void __launch_bounds__(DX_THREADS, 1)
+    k_conv_dx(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+              const __grid_constant__ CUtensorMap mapO, const __grid_constant__ ConvArgs p,
+              const __grid_constant__ DxArgs h) {
+  constexpr int B_TILE = BN * ROW_BYTES;
+  constexpr int B3 = 3 * B_TILE;               // the three dx tiles of one (chunk, dy)
+  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int CEL = ROW_BYTES / ELEM;
+  constexpr int NACC = 6 * BN <= 512 ? 2 : 1;   // TMEM accumulator buffers
+  constexpr int NSPLIT = 3 * BN <= 256 ? 1 : 2;
+  constexpr int NMMA = 3 * BN / NSPLIT;
+  constexpr uint32_t COLS = NACC * 3 * BN;
+  constexpr uint32_t TMEM_COLS = COLS <= 32 ? 32 : (COLS <= 64 ? 64 : (COLS <= 128 ? 128 : (COLS <= 256 ? 256 : 512)));
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int n_wtiles = 9 * p.cblocks;
+  uint8_t* wres = smem;  // RES: tiles ordered [chunk][dy][dx]
+  uint8_t* aring = smem + (RES ? n_wtiles * B_TILE : 0);
+  uint8_t* bring = aring + h.sa * h.a_bytes;
+  uint8_t* ostage = bring + (RES ? 0 : h.sb * B3);  // 2 x o_bytes, 1024-aligned
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ostage + 2 * h.o_bytes);
+  uint64_t* afull = bars;
+  uint64_t* aempty = bars + 8;
+  uint64_t* bfull = bars + 16;
+  uint64_t* bempty = bars + 24;
+  uint64_t* tfull = bars + 32;
+  uint64_t* tempty = bars + 34;
+  uint64_t* wfull = bars + 36;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 37);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&mapA);
+    prefetch_map(&mapB);
+    for (int s = 0; s < h.sa; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < h.sb; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], DX_EPI_WARPS);
+    }
+    mbar_init(wfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+  // N tiles of one M tile are adjacent in the schedule (the halo box is
+  // re-read from L2, not DRAM)
+  if (warp == 0) {
+    if (lane == 0) {
+      if (RES) {
+        mbar_expect_tx(wfull, uint32_t(n_wtiles * B_TILE));
+        for (int cb = 0; cb < p.cblocks; ++cb)
+          for (int t = 0; t < 9; ++t)
+            tma_load_2d(&mapB, wfull, wres + (cb * 9 + t) * B_TILE, (t * p.cblocks + cb) * CEL, 0);
+      }
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int nt = tile % p.num_n_tiles, mt = tile / p.num_n_tiles;
+        int n0 = mt / p.tiles_per_map;
+        int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
+        for (int cb = 0; cb < p.cblocks; ++cb) {
+          mbar_wait(&aempty[sa], pa ^ 1);
+          mbar_expect_tx(&afull[sa], uint32_t(h.a_bytes));
+          tma_load_4d(&mapA, &afull[sa], aring + sa * h.a_bytes, cb * CEL, 0, y0 - 1, n0);
+          if (++sa == h.sa) {
+            sa = 0;
+            pa ^= 1;
+          }
+          if (!RES) {
+            for (int dyi = 0; dyi < 3; ++dyi) {
+              mbar_wait(&bempty[sb], pb ^ 1);
+              mbar_expect_tx(&bfull[sb], uint32_t(B3));
+              uint8_t* dst = bring + sb * B3;
+              for (int dxi = 0; dxi < 3; ++dxi)
+                tma_load_2d(&mapB, &bfull[sb], dst + dxi * B_TILE,
+                            ((dyi * 3 + dxi) * p.cblocks + cb) * CEL, nt * BN);
+              if (++sb == h.sb) {
+                sb = 0;
+                pb ^= 1;
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(KIND, BM, NMMA);
+      if (RES) mbar_wait(wfull, 0);
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * 3 * BN;
+        bool first = true;
+        for (int cb = 0; cb < p.cblocks; ++cb) {
+          mbar_wait(&afull[sa], pa);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(aring + sa * h.a_bytes);
+#pragma unroll 1
+          for (int dyi = 0; dyi < 3; ++dyi) {
+            uint32_t bb;
+            if (RES) {
+              bb = smem_u32(wres + (cb * 9 + dyi * 3) * B_TILE);
+            } else {
+              mbar_wait(&bfull[sb], pb);
+              tc_fence_after();
+              bb = smem_u32(bring + sb * B3);
+            }
+            const uint32_t aa = a0 + dyi * h.row_bytes;
+#pragma unroll
+            for (int k = 0; k < ROW_BYTES / 32; ++k) {
+#pragma unroll
+              for (int sp = 0; sp < NSPLIT; ++sp)
+                tc_mma<KIND>(tmem_d + sp * NMMA, sw128_desc(aa + 32 * k),
+                             sw128_desc(bb + sp * NMMA * ROW_BYTES + 32 * k), idesc, first ? 0u : 1u);
+              first = false;
+            }
+            if (!RES) {
+              tc_commit(&bempty[sb]);
+              if (++sb == h.sb) {
+                sb = 0;
+                pb ^= 1;
+              }
+            }
+          }
+          tc_commit(&aempty[sa]);
+          if (++sa == h.sa) {
+            sa = 0;
+            pa ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == NACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int acc = 0, obuf = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int nt = tile % p.num_n_tiles, mt = tile / p.num_n_tiles;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t m = int64_t(mt) * BM + row;
+      const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + acc * 3 * BN;
+      // two warps per TMEM lane quarter split the 16-column chunks
+      const int half = (warp - 2) / 4;
+      if (h.o_bytes) {
+        uint8_t* ot = ostage + obuf * h.o_bytes;
+        if (threadIdx.x == 64) bulk_wait_read1();  // the store issued 2 tiles ago has read ot
+        epi_bar256();
+        epilogue_stage<KIND, BN>(p, tbase, m, nt, ot, 16 * half, 32);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        fence_proxy_async();
+        epi_bar256();
+        if (threadIdx.x == 64) {
+          const int n0 = mt / p.tiles_per_map;
+          const int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
+          for (int sb2 = 0; sb2 < BN / CEL; ++sb2)
+            tma_store_4d(&mapO, ot + sb2 * BM * ROW_BYTES, p.cout_off + nt * BN + sb2 * CEL, 0, y0, n0);
+          bulk_commit();
+        }
+        obuf ^= 1;
+      } else {
+        epilogue_tile<KIND, BN, true>(p, tbase, m, nt, nullptr, 16 * half, 32);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
+      if (++acc == NACC) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (threadIdx.x == 64 && h.o_bytes) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // NHWC helper kernels (element type T = bf16 or fp32)
 template <typename T>
 __device__ __forceinline__ float ldf(const T* p);
@@ -718,22 +1045,32 @@ __device__ __forceinline__ uint4 pack<float>(const float* f) {
                     __float_as_uint(round_tf32(f[2])), __float_as_uint(round_tf32(f[3])));
 }
 
-// NCHW fp32 stack (n,7,32,32) -> NHWC (n_pad,32,32,cpad), zero padded;
-// one thread per pixel
+// NCHW fp32 stack (n,7,32,32) -> im2col network input (n_pad,32,32,64):
+// K value k = tap * 7 + c of pixel (y, x) is channel c of pixel
+// (y + tap/3 - 1, x + tap%3 - 1), zero outside the map, k = 63 zero. One
+// thread per (pixel, 16-B piece): a warp writes 512 contiguous bytes.
 template <typename T>
-__global__ void k_stack_to_nhwc(const float* __restrict__ x, int64_t n, int64_t n_pad, int cpad,
+__global__ void k_stack_to_nhwc(const float* __restrict__ x, int64_t n, int64_t n_pad, int,
                                 T* __restrict__ out) {
+  constexpr int V = Vec<T>::N;   // K values per 16-B piece
+  constexpr int PP = 64 / V;     // pieces per pixel
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n_pad * 1024) return;
-  int64_t map = i / 1024;
-  int pix = int(i % 1024);
-  constexpr int V = Vec<T>::N;
-  float f[16];
+  if (i >= n_pad * 1024 * PP) return;
+  const int piece = int(i % PP);
+  const int64_t px = i / PP;
+  const int64_t map = px / 1024;
+  const int pix = int(px % 1024), y = pix >> 5, xx = pix & 31;
+  float f[V];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) f[c] = (map < n && c < 7) ? __ldg(x + (map * 7 + c) * 1024 + pix) : 0.f;
-  uint4* o = reinterpret_cast<uint4*>(out + i * cpad);
-  const uint4 z = make_uint4(0, 0, 0, 0);
-  for (int g = 0; g < cpad / V; ++g) o[g] = (g * V < 8) ? pack<T>(f + g * V) : z;
+  for (int j = 0; j < V; ++j) {
+    const int k = piece * V + j;
+    const int tap = k / 7, c = k % 7;
+    const int yy = y + tap / 3 - 1, xs = xx + tap % 3 - 1;
+    f[j] = (k < 63 && map < n && yy >= 0 && yy < 32 && xs >= 0 && xs < 32)
+               ? __ldg(x + (map * 7 + c) * 1024 + yy * 32 + xs)
+               : 0.f;
+  }
+  reinterpret_cast<uint4*>(out)[i] = pack<T>(f);
 }
 
 // 2x2 max-pool of channel slice [off, off+C) of an NHWC buffer
@@ -757,7 +1094,7 @@ __global__ void __launch_bounds__(256) k_pool_nhwc(const T* __restrict__ in, int
   T* o = out + px * C;
 #pragma unroll
   for (int k = 0; k < GPT; ++k) {
-    const int g = gq * GPT + k;
+    const int g = k * TPP + gq;  // a pixel's threads cover adjacent 16-B groups (full sectors)
     float a[V], b[V], cc[V], d[V], m[V];
     unpack<T>(__ldg(reinterpret_cast<const uint4*>(p + g * V)), a);
     unpack<T>(__ldg(reinterpret_cast<const uint4*>(p + c_tot + g * V)), b);
@@ -796,7 +1133,7 @@ __global__ void __launch_bounds__(256) k_up_nhwc(const T* __restrict__ in, T* __
   T* o = out + px * c_tot;
 #pragma unroll
   for (int k = 0; k < GPT; ++k) {
-    const int g = (gq * GPT + k) * V;
+    const int g = (k * TPP + gq) * V;  // adjacent 16-B groups per instruction
     float p00[V], p10[V], p01[V], p11[V], v[V];
     unpack<T>(__ldg(reinterpret_cast<const uint4*>(b + (r0 * HW_IN + c0) * C + g)), p00);
     unpack<T>(__ldg(reinterpret_cast<const uint4*>(b + (r1 * HW_IN + c0) * C + g)), p10);
@@ -922,7 +1259,8 @@ int pad_c(int c, int kind) {
 // pack conv-form weights (cout, cin, 3, 3) into K-major (cout_pad, 9*cin_pad)
 int prepare_layer(NetImpl& net, ConvLayer& L, int kind) {
   if (L.tc_kind == kind) return 0;
-  const int cinp = pad_c(L.cin, kind);
+  L.im2col = (L.name == "enc1.conv1" && L.cin == 7);
+  const int cinp = L.im2col ? 64 : pad_c(L.cin, kind);
   // output channels are padded to the next layer's K granularity; padded
   // channels get zero weights and zero epilogue vectors, so they hold exact
   // zeros (head.deconv1's k/2 outputs feed a K-padded input). The fused head
@@ -930,7 +1268,9 @@ int prepare_layer(NetImpl& net, ConvLayer& L, int kind) {
   const int coutp = (L.name == "head.deconv2") ? 16 : pad_c(L.cout, kind);
   L.cin_pad = cinp;
   L.cout_pad = coutp;
-  const int64_t ktot = int64_t(9) * cinp;
+  const int64_t ktot = L.im2col ? 64 : int64_t(9) * cinp;
+  // K index of (input channel ci, tap t) in the packed operand
+  auto kidx = [&](int ci, int t) -> int64_t { return L.im2col ? t * 7 + ci : int64_t(t) * cinp + ci; };
   std::vector<float> a(coutp, 0.f), b(coutp, 0.f);
   for (int c = 0; c < L.cout; ++c) {
     a[c] = L.scale[c];
@@ -943,7 +1283,7 @@ int prepare_layer(NetImpl& net, ConvLayer& L, int kind) {
     for (int co = 0; co < L.cout; ++co)
       for (int ci = 0; ci < L.cin; ++ci)
         for (int t = 0; t < 9; ++t)
-          w[size_t(co) * ktot + size_t(t) * cinp + ci] = __float2bfloat16(L.w[(size_t(co) * L.cin + ci) * 9 + t]);
+          w[size_t(co) * ktot + kidx(ci, t)] = __float2bfloat16(L.w[(size_t(co) * L.cin + ci) * 9 + t]);
     if (cudaMalloc(&dw, nel * 2) != cudaSuccess) return fail(DRCB_ECUDA, "cudaMalloc weights");
     cudaMemcpy(dw, w.data(), nel * 2, cudaMemcpyHostToDevice);
   } else {
@@ -951,7 +1291,7 @@ int prepare_layer(NetImpl& net, ConvLayer& L, int kind) {
     for (int co = 0; co < L.cout; ++co)
       for (int ci = 0; ci < L.cin; ++ci)
         for (int t = 0; t < 9; ++t)
-          w[size_t(co) * ktot + size_t(t) * cinp + ci] = host_round_tf32(L.w[(size_t(co) * L.cin + ci) * 9 + t]);
+          w[size_t(co) * ktot + kidx(ci, t)] = host_round_tf32(L.w[(size_t(co) * L.cin + ci) * 9 + t]);
     if (cudaMalloc(&dw, nel * 4) != cudaSuccess) return fail(DRCB_ECUDA, "cudaMalloc weights");
     cudaMemcpy(dw, w.data(), nel * 4, cudaMemcpyHostToDevice);
   }
@@ -1026,6 +1366,42 @@ int launch_halo(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a,
   return fail(DRCB_ECONFIG, "unsupported N tile (halo)");
 }
 
+template <int KIND, int BN, bool RES>
+int launch_dx_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
+                 const ConvArgs& a, const DxArgs& h, size_t smem, cudaStream_t st) {
+  auto kern = k_conv_dx<KIND, BN, RES>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  int tiles = a.num_m_tiles * a.num_n_tiles;
+  int grid = tiles < nsm ? tiles : nsm;
+  kern<<<grid, DX_THREADS, smem, st>>>(mA, mB, mO, a, h);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_dx");
+}
+
+template <int KIND>
+int launch_dx(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO, const ConvArgs& a,
+              const DxArgs& h, bool res, size_t smem, cudaStream_t st) {
+#define DX_CASE(BNV)                                                         \
+  case BNV:                                                                  \
+    return res ? launch_dx_bn<KIND, BNV, true>(mA, mB, mO, a, h, smem, st)   \
+               : launch_dx_bn<KIND, BNV, false>(mA, mB, mO, a, h, smem, st);
+  switch (a.bn) {
+    DX_CASE(16)
+    DX_CASE(32)
+    DX_CASE(64)
+    DX_CASE(128)
+  }
+#undef DX_CASE
+  return fail(DRCB_ECONFIG, "unsupported N tile (dx)");
+}
+
 // stage counts keep smem <= ~200 KB: BN=256 -> 48 KB/stage
 template <int KIND>
 int launch_conv(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, cudaStream_t st) {
@@ -1067,7 +1443,8 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
   }
   a.num_m_tiles = int(nmaps * hw * hw / BM);
   a.cblocks = L.cin_pad / (ROW_BYTES / (KIND == 0 ? 2 : 4));
-  a.num_kb = 9 * a.cblocks;
+  a.num_kb = (L.im2col ? 1 : 9) * a.cblocks;
+  a.taps1 = L.im2col ? 1 : 0;
   a.bn = L.cout_pad >= 256 ? 256 : L.cout_pad;
   a.num_n_tiles = L.cout_pad / a.bn;
   a.cout = pred ? L.cout_pad : L.cout_pad;  // padded channels carry exact zeros
@@ -1092,7 +1469,46 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     }
   }
   CUtensorMap mA, mB;
-  if (hw >= 16 && !getenv("DRCB_NO_HALO")) {
+  if (hw >= 16 && !L.im2col && !getenv("DRCB_NO_DX")) {
+    // dx-in-N kernel: one rows+2 halo box per chunk; BN <= 128
+    static const char* bn_env = getenv("DRCB_DX_BN");
+    const int bn_cap = bn_env ? atoi(bn_env) : (KIND == 0 ? 128 : 64);
+    while (a.bn > bn_cap || a.bn > 128) a.bn /= 2;
+    a.num_n_tiles = L.cout_pad / a.bn;
+    DxArgs dz;
+    dz.row_bytes = hw * ROW_BYTES;
+    dz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
+    const int b_tile = a.bn * ROW_BYTES;
+    const int w_bytes = 9 * a.cblocks * b_tile;
+    dz.o_bytes = (pred || getenv("DRCB_NO_TMA_STORE")) ? 0 : BM * a.bn * (KIND == 0 ? 2 : 4);
+    const int budget = 200 * 1024 - 2 * dz.o_bytes;
+    const bool res = a.num_n_tiles == 1 && w_bytes + 3 * dz.a_bytes <= budget;
+    if (res) {
+      dz.sb = 1;
+      dz.sa = std::min(8, (budget - w_bytes) / dz.a_bytes);
+    } else {
+      // B triples are consumed three per A box
+      dz.sa = std::min(4, std::max(2, budget / (4 * dz.a_bytes)));
+      dz.sb = std::min(8, (budget - dz.sa * dz.a_bytes) / (3 * b_tile));
+    }
+    if (dz.sa >= 2 && (res || dz.sb >= 2)) {
+      rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, hw, a.rows_per_tile + 2, 1);
+      if (rc) return rc;
+      rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
+      if (rc) return rc;
+      CUtensorMap mO;
+      if (dz.o_bytes) {
+        rc = encode_act(&mO, out.p, KIND, out.c, hw, nmaps, hw, a.rows_per_tile, 1);
+        if (rc) return rc;
+      }
+      size_t smem = 1024 + size_t(res ? w_bytes : 0) + size_t(dz.sa) * dz.a_bytes +
+                    size_t(res ? 0 : dz.sb * 3 * b_tile) + 2 * size_t(dz.o_bytes) + 512;
+      return launch_dx<KIND>(mA, mB, mO, a, dz, res, smem, st);
+    }
+    a.bn = L.cout_pad >= 256 ? 256 : L.cout_pad;
+    a.num_n_tiles = L.cout_pad / a.bn;
+  }
+  if (hw >= 16 && !L.im2col && !getenv("DRCB_NO_HALO")) {
     // row-halo kernel: box of rows+2 image rows per (chunk, dx) stage
     HaloArgs hz;
     hz.row_bytes = hw * ROW_BYTES;
@@ -1115,7 +1531,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
   int box_w = hw, box_h = a.maps_per_tile == 1 ? a.rows_per_tile : hw, box_n = a.maps_per_tile;
   rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, box_w, box_h, box_n);
   if (rc) return rc;
-  rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
+  rc = encode_w(&mB, L.d_wtc, KIND, int64_t(L.im2col ? 1 : 9) * L.cin_pad, L.cout_pad, a.bn);
   if (rc) return rc;
   return launch_conv<KIND>(mA, mB, a, st);
 }
@@ -1133,7 +1549,7 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
   // buffer plan (elements per map): channels padded to the K granularity
   struct Spec { int c, hw; };
   const Spec specs[] = {
-      {P(7), 32},       // 0 x0
+      {64, 32},         // 0 x0: im2col input (k = tap * 7 + c)
       {P(k), 32},       // 1 e32
       {3 * k, 32},      // 2 c1 [up(2k) | s1(k)]
       {P(k), 16},       // 3 p1
@@ -1166,7 +1582,7 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
   if (x_nhwc) {
     B[0].p = const_cast<void*>(x_nhwc);
   } else {
-    int64_t tot = np * 1024;
+    int64_t tot = np * 1024 * (64 / Vec<T>::N);
     k_stack_to_nhwc<T><<<unsigned((tot + 255) / 256), 256, 0, st>>>(x, n, np, B[0].c, (T*)B[0].p);
     count_launch();
   }
@@ -1236,7 +1652,7 @@ int forward_tc_nhwc(NetImpl& net, const void* x_nhwc, float* y, int64_t n, int m
                                : tc::forward_kind<1>(net, nullptr, y, n, st, x_nhwc);
 }
 
-int tc_input_channels(int mode) { return mode == DRCB_NET_BF16 ? 64 : 32; }
+int tc_input_channels(int) { return 64; }  // im2col K values per pixel
 
 int forward_tc(NetImpl& net, const float* x, float* y, int64_t n, int mode, cudaStream_t st) {
   if (n <= 0) return 0;

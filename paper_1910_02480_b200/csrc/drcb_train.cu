@@ -481,7 +481,6 @@ int alloc_work(DrcbTrainer* T, int64_t n, Work& W, cudaStream_t st) {
   add(&W.dc1, 3 * k * 1024); add(&W.dc2, 6 * k * 256); add(&W.dc3, 12 * k * 64);
   add(&W.dpre, 3 * 1024); add(&W.dz, size_t(k) * 1024 * 3);
   for (auto& r : req) per += (r.second + 63) / 64 * 64;
-  size_t fixed = 0;
   int64_t maxw = 0;
   for (const auto& l : T->L) maxw = std::max(maxw, l.nw);
   size_t bytes = per * n * 4 + size_t(maxw) * 4 + (16 * 2 * 1024 + 4096) * 8 + 1024 * 1024;
@@ -504,7 +503,7 @@ int alloc_work(DrcbTrainer* T, int64_t n, Work& W, cudaStream_t st) {
   uintptr_t a = (reinterpret_cast<uintptr_t>(cur) + 7) & ~uintptr_t(7);
   W.acc = reinterpret_cast<double*>(a);
   W.loss = W.acc + 2 * 1024;
-  (void)fixed;
+
   return 0;
 }
 
