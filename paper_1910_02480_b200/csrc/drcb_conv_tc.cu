@@ -90,6 +90,10 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
                                             int c1, int c2, int c3) {
@@ -297,7 +301,7 @@ template <int KIND, int BN, bool DX = false>
 __device__ __forceinline__ void epilogue_tile(const ConvArgs& p, uint32_t tbase, int64_t m, int nt,
                                               float* staging = nullptr, int cbeg = 0,
                                               int cstep = 16) {
-  const int xpix = int(m % p.hw);
+  const int xpix = int(m & int64_t(p.hw - 1));  // hw is a power of two
   if (p.head) {
     if (cbeg != 0) return;
     // head.deconv2 (BN == 16 channels) + BN + LeakyReLU, then the fused
@@ -547,203 +551,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Row-halo variant for the 32x32 and 16x16 layers (one map covers whole
-// tiles). The 32x32/16x16 layers are L2-bandwidth-bound in the plain kernel
-// (A re-loaded for each of the 9 taps, weights re-streamed per tile). Here a
-// stage is one (channel chunk, dx) pair: a single TMA box of rows+2 image rows
-// serves the three dy taps, whose A operands are the same SMEM buffer at
-// descriptor offsets dy*W*128 B (a multiple of the 1024 B swizzle atom).
-// RES: the whole packed weight matrix (9 * cblocks K tiles) stays resident in
-// SMEM for the CTA's lifetime, loaded once.
-struct HaloArgs {
-  int a_bytes;      // (rows+2) * W * 128
-  int row_bytes;    // W * 128: one dy shift
-  int stages;
-  int res;
-};
-
-template <int KIND, int BN, bool RES>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_conv_halo(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                const __grid_constant__ ConvArgs p, const __grid_constant__ HaloArgs h) {
-  constexpr int B_TILE = BN * ROW_BYTES;
-  constexpr int ELEM = KIND == 0 ? 2 : 4;
-  constexpr int CEL = ROW_BYTES / ELEM;
-  constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int n_wtiles = 9 * p.cblocks;
-  uint8_t* wres = smem;
-  uint8_t* stages = smem + (RES ? n_wtiles * B_TILE : 0);
-  const int stage_bytes = h.a_bytes + (RES ? 0 : 3 * B_TILE);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + h.stages * stage_bytes);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + 8;
-  uint64_t* tfull = bars + 16;
-  uint64_t* tempty = bars + 18;
-  uint64_t* wfull = bars + 20;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (warp == 0 && lane == 0) {
-    prefetch_map(&mapA);
-    prefetch_map(&mapB);
-    for (int st = 0; st < h.stages; ++st) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
-    }
-    mbar_init(wfull, 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
-  const int kstages = p.cblocks * 3;  // (chunk, dx) pairs per tile
-  if (warp == 0) {
-    if (lane == 0) {
-      if (RES) {
-        mbar_expect_tx(wfull, uint32_t(n_wtiles * B_TILE));
-        for (int t = 0; t < n_wtiles; ++t) tma_load_2d(&mapB, wfull, wres + t * B_TILE, t * CEL, 0);
-      }
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int mt = tile % p.num_m_tiles, nt = tile / p.num_m_tiles;
-        int n0 = mt / p.tiles_per_map;
-        int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
-        for (int ks = 0; ks < kstages; ++ks) {
-          int cb = ks / 3, dxi = ks % 3;
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sA = stages + stage * stage_bytes;
-          mbar_expect_tx(&full[stage], uint32_t(stage_bytes));
-          tma_load_4d(&mapA, &full[stage], sA, cb * CEL, dxi - 1, y0 - 1, n0);
-          if (!RES) {
-            for (int dyi = 0; dyi < 3; ++dyi) {
-              int kb = (dyi * 3 + dxi) * p.cblocks + cb;
-              tma_load_2d(&mapB, &full[stage], sA + h.a_bytes + dyi * B_TILE, kb * CEL, nt * BN);
-            }
-          }
-          if (++stage == h.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(KIND, BM, BN);
-      if (RES) mbar_wait(wfull, 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        uint32_t tmem_d = tmem_base + acc * BN;
-        bool first = true;
-        for (int ks = 0; ks < kstages; ++ks) {
-          int cb = ks / 3, dxi = ks % 3;
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          uint32_t a0 = smem_u32(stages + stage * stage_bytes);
-#pragma unroll
-          for (int dyi = 0; dyi < 3; ++dyi) {
-            uint32_t aa = a0 + dyi * h.row_bytes;
-            uint32_t bb = RES ? smem_u32(wres + ((dyi * 3 + dxi) * p.cblocks + cb) * B_TILE)
-                              : a0 + h.a_bytes + dyi * B_TILE;
-#pragma unroll
-            for (int k = 0; k < ROW_BYTES / 32; ++k) {
-              tc_mma<KIND>(tmem_d, sw128_desc(aa + 32 * k), sw128_desc(bb + 32 * k), idesc,
-                           first ? 0u : 1u);
-              first = false;
-            }
-          }
-          tc_commit(&empty[stage]);
-          if (++stage == h.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        tc_commit(&tfull[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
-        }
-      }
-    }
-  } else {
-    const int q = warp & 3;
-    const int row = q * 32 + lane;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      int mt = tile % p.num_m_tiles, nt = tile / p.num_m_tiles;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const int64_t m = int64_t(mt) * BM + row;
-      const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
-      epilogue_tile<KIND, BN>(p, tbase, m, nt);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
-  }
-}
-
-// ---------------------------------------------------------------------------
-// dx-in-N implicit GEMM for hw in {16, 32} (tiles = whole image rows).
-// One TMA box of rows+2 image rows per channel chunk is the ONLY activation
-// load (the (chunk, dx) halo kernel above loads it three times). For each dy
-// the A descriptor is shifted by dy*W*128 B and ONE MMA (two for BN = 128)
-// multiplies it by the three dx taps' weights stacked along N: the tile holds
-// three accumulators P_dx of the unshifted input, combined in the epilogue
-// (acc_chunk<BN, true>) as P_-1(x-1) + P_0(x) + P_+1(x+1). A ring and B ring
-// are separate: A stage = one chunk's halo box; B stage = one (chunk, dy)
-// triple of weight tiles (or the whole weight matrix resident, RES).
 // Epilogue into a SMEM staging tile for a TMA store: BN channels of 128
 // pixels as BN/CEL sub-tiles of [128 px][128 B], each in the SWIZZLE_128B
 // layout the output tensor map expects (16-B piece j of pixel r at
 // r*128 + ((j ^ (r & 7)) << 4)): the global write is one coalesced bulk
 // tensor store per sub-tile instead of 16-B scattered stores per thread.
-template <int KIND, int BN>
+template <int KIND, int BN, bool DX, int CSTEP>
 __device__ __forceinline__ void epilogue_stage(const ConvArgs& p, uint32_t tbase, int64_t m, int nt,
-                                               uint8_t* ost, int cbeg, int cstep) {
+                                               uint8_t* ost, int cbeg) {
   constexpr int ELEM = KIND == 0 ? 2 : 4;
   constexpr int CEL = ROW_BYTES / ELEM;
-  const int xpix = int(m % p.hw);
-  const int r = int(m % BM);
-#pragma unroll 1
-  for (int c0 = cbeg; c0 < BN; c0 += cstep) {
+  const int xpix = int(m & int64_t(p.hw - 1));  // hw is a power of two
+  const int r = int(m & (BM - 1));
+  const uint32_t ost_s = smem_u32(ost);
+  // unrolled so the next chunk's TMEM loads overlap this chunk's math
+#pragma unroll
+  for (int i = 0; i < (BN + CSTEP - 1) / CSTEP; ++i) {
+    const int c0 = cbeg + i * CSTEP;
+    if (c0 >= BN) break;
     const int cg = nt * BN + c0;
     float acc[16];
-    acc_chunk<BN, true>(tbase, c0, xpix, p.hw, acc);
+    acc_chunk<BN, DX>(tbase, c0, xpix, p.hw, acc);
     float v[16];
     bn_lrelu16(acc, p.ep_a + cg, p.ep_b + cg, p.slope, v);
-    uint8_t* sub = ost + (c0 / CEL) * (BM * ROW_BYTES) + r * ROW_BYTES;
+    const uint32_t sub = ost_s + (c0 / CEL) * (BM * ROW_BYTES) + r * ROW_BYTES;
     const int jb = (c0 % CEL) * ELEM / 16;
     if constexpr (KIND == 0) {
       uint32_t pk[8];
@@ -752,42 +583,61 @@ __device__ __forceinline__ void epilogue_stage(const ConvArgs& p, uint32_t tbase
         __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
         pk[j] = *reinterpret_cast<uint32_t*>(&b2);
       }
-      *reinterpret_cast<uint4*>(sub + (((jb + 0) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-      *reinterpret_cast<uint4*>(sub + (((jb + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      sts128(sub + (((jb + 0) ^ (r & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+      sts128(sub + (((jb + 1) ^ (r & 7)) << 4), pk[4], pk[5], pk[6], pk[7]);
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        *reinterpret_cast<float4*>(sub + (((jb + j) ^ (r & 7)) << 4)) =
-            make_float4(round_tf32(v[4 * j]), round_tf32(v[4 * j + 1]), round_tf32(v[4 * j + 2]),
-                        round_tf32(v[4 * j + 3]));
+        sts128(sub + (((jb + j) ^ (r & 7)) << 4), __float_as_uint(round_tf32(v[4 * j])),
+               __float_as_uint(round_tf32(v[4 * j + 1])), __float_as_uint(round_tf32(v[4 * j + 2])),
+               __float_as_uint(round_tf32(v[4 * j + 3])));
     }
   }
 }
-__device__ __forceinline__ void epi_bar256() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
+constexpr int RT_EPI_WARPS = 8;
+constexpr int RT_THREADS = 64 + 32 * RT_EPI_WARPS;
+__device__ __forceinline__ void epi_bar_rt() {
+  asm volatile("bar.sync 2, %0;" ::"r"(32 * RT_EPI_WARPS) : "memory");
+}
 
-struct DxArgs {
+struct RowArgs {
   int a_bytes;    // (rows+2) * W * 128
   int row_bytes;  // W * 128: one dy shift
   int sa, sb;     // A / B ring depths
   int o_bytes;    // one output staging tile (BM * BN * elem); 0 = direct stores (head)
 };
 
-constexpr int DX_EPI_WARPS = 8;
-constexpr int DX_THREADS = 64 + 32 * DX_EPI_WARPS;
-
-template <int KIND, int BN, bool RES>
-__global__ void __launch_bounds__(DX_THREADS, 1)
-    k_conv_dx(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-              const __grid_constant__ CUtensorMap mapO, const __grid_constant__ ConvArgs p,
-              const __grid_constant__ DxArgs h) {
+// Row-tile implicit GEMM for hw in {16, 32}: an M tile is BM/W whole image
+// rows, its activation operand one TMA box of rows+2 rows (OOB rows zero =
+// the conv's padding), and the three dy taps read that box at descriptor
+// offsets dy*W*128 B (a multiple of the 1024-B swizzle atom).
+//   DX = false ("halo"): one box per (channel chunk, dx) loaded at x offset
+//     dx-1 (OOB columns zero); per dy one MMA with N = BN into the single
+//     accumulator. B stage = the three dy weight tiles of that (chunk, dx).
+//   DX = true ("dx-in-N"): one box per chunk; per dy ONE MMA multiplies it by
+//     the three dx taps' weights stacked along N (N = 3 BN, split in two for
+//     BN = 128) into accumulators P_-1, P_0, P_+1 of the unshifted input,
+//     combined in the epilogue as P_-1(x-1) + P_0(x) + P_+1(x+1) by lane
+//     shuffles (acc_chunk<BN, true>). 1/3 of the activation traffic for 3x
+//     the TMEM reads + shuffles in the epilogue.
+// RES: the whole weight matrix stays resident in SMEM ([chunk][dy][dx]
+// tiles). 8 epilogue warps (two per TMEM lane quarter) stage the tile in
+// SMEM in the output map's swizzled layout; one thread TMA-stores it.
+template <int KIND, int BN, bool RES, bool DX>
+__global__ void __launch_bounds__(RT_THREADS, 1)
+    k_conv_rows(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                const __grid_constant__ CUtensorMap mapO, const __grid_constant__ ConvArgs p,
+                const __grid_constant__ RowArgs h) {
   constexpr int B_TILE = BN * ROW_BYTES;
-  constexpr int B3 = 3 * B_TILE;               // the three dx tiles of one (chunk, dy)
+  constexpr int B3 = 3 * B_TILE;                       // one B stage: three weight tiles
   constexpr int ELEM = KIND == 0 ? 2 : 4;
   constexpr int CEL = ROW_BYTES / ELEM;
-  constexpr int NACC = 6 * BN <= 512 ? 2 : 1;   // TMEM accumulator buffers
-  constexpr int NSPLIT = 3 * BN <= 256 ? 1 : 2;
-  constexpr int NMMA = 3 * BN / NSPLIT;
-  constexpr uint32_t COLS = NACC * 3 * BN;
+  constexpr int NACCW = DX ? 3 * BN : BN;              // TMEM columns per accumulator
+  constexpr int NACC = 2 * NACCW <= 512 ? 2 : 1;       // TMEM accumulator buffers
+  constexpr int NSPLIT = NACCW <= 256 ? 1 : 2;
+  constexpr int NMMA = NACCW / NSPLIT;
+  constexpr int BPA = DX ? 3 : 1;                      // B stages per A stage
+  constexpr uint32_t COLS = NACC * NACCW;
   constexpr uint32_t TMEM_COLS = COLS <= 32 ? 32 : (COLS <= 64 ? 64 : (COLS <= 128 ? 128 : (COLS <= 256 ? 256 : 512)));
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -819,7 +669,7 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], DX_EPI_WARPS);
+      mbar_init(&tempty[a], RT_EPI_WARPS);
     }
     mbar_init(wfull, 1);
     fence_barrier_init();
@@ -835,7 +685,8 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int num_tiles = p.num_m_tiles * p.num_n_tiles;
-  // N tiles of one M tile are adjacent in the schedule (the halo box is
+  const int astages = DX ? p.cblocks : 3 * p.cblocks;  // A boxes per tile
+  // N tiles of one M tile are adjacent in the schedule (the boxes are
   // re-read from L2, not DRAM)
   if (warp == 0) {
     if (lane == 0) {
@@ -851,22 +702,26 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
         int nt = tile % p.num_n_tiles, mt = tile / p.num_n_tiles;
         int n0 = mt / p.tiles_per_map;
         int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
-        for (int cb = 0; cb < p.cblocks; ++cb) {
+        for (int as = 0; as < astages; ++as) {
+          const int cb = DX ? as : as / 3, dxi = DX ? 1 : as % 3;
           mbar_wait(&aempty[sa], pa ^ 1);
           mbar_expect_tx(&afull[sa], uint32_t(h.a_bytes));
-          tma_load_4d(&mapA, &afull[sa], aring + sa * h.a_bytes, cb * CEL, 0, y0 - 1, n0);
+          tma_load_4d(&mapA, &afull[sa], aring + sa * h.a_bytes, cb * CEL, dxi - 1, y0 - 1, n0);
           if (++sa == h.sa) {
             sa = 0;
             pa ^= 1;
           }
           if (!RES) {
-            for (int dyi = 0; dyi < 3; ++dyi) {
+            for (int bs = 0; bs < BPA; ++bs) {
               mbar_wait(&bempty[sb], pb ^ 1);
               mbar_expect_tx(&bfull[sb], uint32_t(B3));
               uint8_t* dst = bring + sb * B3;
-              for (int dxi = 0; dxi < 3; ++dxi)
-                tma_load_2d(&mapB, &bfull[sb], dst + dxi * B_TILE,
-                            ((dyi * 3 + dxi) * p.cblocks + cb) * CEL, nt * BN);
+              // DX: the three dx tiles of (cb, dy = bs); halo: the three dy
+              // tiles of (cb, dx)
+              for (int j = 0; j < 3; ++j) {
+                const int tap = DX ? bs * 3 + j : j * 3 + dxi;
+                tma_load_2d(&mapB, &bfull[sb], dst + j * B_TILE, (tap * p.cblocks + cb) * CEL, nt * BN);
+              }
               if (++sb == h.sb) {
                 sb = 0;
                 pb ^= 1;
@@ -887,21 +742,30 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * 3 * BN;
+        const uint32_t tmem_d = tmem_base + acc * NACCW;
         bool first = true;
-        for (int cb = 0; cb < p.cblocks; ++cb) {
+        for (int as = 0; as < astages; ++as) {
+          const int cb = DX ? as : as / 3, dxi = DX ? 1 : as % 3;
           mbar_wait(&afull[sa], pa);
           tc_fence_after();
           const uint32_t a0 = smem_u32(aring + sa * h.a_bytes);
+          uint32_t bstage = 0;
+          if (!RES && !DX) {
+            mbar_wait(&bfull[sb], pb);
+            tc_fence_after();
+            bstage = smem_u32(bring + sb * B3);
+          }
 #pragma unroll 1
           for (int dyi = 0; dyi < 3; ++dyi) {
             uint32_t bb;
             if (RES) {
-              bb = smem_u32(wres + (cb * 9 + dyi * 3) * B_TILE);
-            } else {
+              bb = smem_u32(wres + (cb * 9 + dyi * 3 + (DX ? 0 : dxi)) * B_TILE);
+            } else if (DX) {
               mbar_wait(&bfull[sb], pb);
               tc_fence_after();
               bb = smem_u32(bring + sb * B3);
+            } else {
+              bb = bstage + dyi * B_TILE;
             }
             const uint32_t aa = a0 + dyi * h.row_bytes;
 #pragma unroll
@@ -912,12 +776,19 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
                              sw128_desc(bb + sp * NMMA * ROW_BYTES + 32 * k), idesc, first ? 0u : 1u);
               first = false;
             }
-            if (!RES) {
+            if (!RES && DX) {
               tc_commit(&bempty[sb]);
               if (++sb == h.sb) {
                 sb = 0;
                 pb ^= 1;
               }
+            }
+          }
+          if (!RES && !DX) {
+            tc_commit(&bempty[sb]);
+            if (++sb == h.sb) {
+              sb = 0;
+              pb ^= 1;
             }
           }
           tc_commit(&aempty[sa]);
@@ -936,6 +807,9 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
   } else {
     const int q = warp & 3;
     const int row = q * 32 + lane;
+    // RT_EPI_WARPS / 4 warps per TMEM lane quarter split the 16-column chunks
+    const int grp = (warp - 2) / 4;
+    constexpr int CSTEP = 16 * (RT_EPI_WARPS / 4);
     int acc = 0, obuf = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -943,19 +817,17 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t m = int64_t(mt) * BM + row;
-      const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + acc * 3 * BN;
-      // two warps per TMEM lane quarter split the 16-column chunks
-      const int half = (warp - 2) / 4;
+      const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + acc * NACCW;
       if (h.o_bytes) {
         uint8_t* ot = ostage + obuf * h.o_bytes;
         if (threadIdx.x == 64) bulk_wait_read1();  // the store issued 2 tiles ago has read ot
-        epi_bar256();
-        epilogue_stage<KIND, BN>(p, tbase, m, nt, ot, 16 * half, 32);
+        epi_bar_rt();
+        epilogue_stage<KIND, BN, DX, CSTEP>(p, tbase, m, nt, ot, 16 * grp);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
         fence_proxy_async();
-        epi_bar256();
+        epi_bar_rt();
         if (threadIdx.x == 64) {
           const int n0 = mt / p.tiles_per_map;
           const int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
@@ -965,7 +837,7 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
         }
         obuf ^= 1;
       } else {
-        epilogue_tile<KIND, BN, true>(p, tbase, m, nt, nullptr, 16 * half, 32);
+        epilogue_tile<KIND, BN, DX>(p, tbase, m, nt, nullptr, 16 * grp, CSTEP);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -1329,10 +1201,10 @@ int launch_bn(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, c
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_tc");
 }
 
-template <int KIND, int BN, bool RES>
-int launch_halo_bn(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a,
-                   const HaloArgs& h, size_t smem, cudaStream_t st) {
-  auto kern = k_conv_halo<KIND, BN, RES>;
+template <int KIND, int BN, bool RES, bool DX>
+int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
+                   const ConvArgs& a, const RowArgs& h, size_t smem, cudaStream_t st) {
+  auto kern = k_conv_rows<KIND, BN, RES, DX>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1342,64 +1214,27 @@ int launch_halo_bn(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs&
   if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   int tiles = a.num_m_tiles * a.num_n_tiles;
   int grid = tiles < nsm ? tiles : nsm;
-  kern<<<grid, NUM_THREADS, smem, st>>>(mA, mB, a, h);
+  kern<<<grid, RT_THREADS, smem, st>>>(mA, mB, mO, a, h);
   count_launch();
   cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_halo");
+  return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_rows");
 }
 
-template <int KIND>
-int launch_halo(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, const HaloArgs& h,
-                size_t smem, cudaStream_t st) {
-#define HALO_CASE(BNV)                                                    \
-  case BNV:                                                               \
-    return h.res ? launch_halo_bn<KIND, BNV, true>(mA, mB, a, h, smem, st) \
-                 : launch_halo_bn<KIND, BNV, false>(mA, mB, a, h, smem, st);
+template <int KIND, bool DX>
+int launch_rows(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO, const ConvArgs& a,
+                const RowArgs& h, bool res, size_t smem, cudaStream_t st) {
+#define ROWS_CASE(BNV)                                                              \
+  case BNV:                                                                         \
+    return res ? launch_rows_bn<KIND, BNV, true, DX>(mA, mB, mO, a, h, smem, st)    \
+               : launch_rows_bn<KIND, BNV, false, DX>(mA, mB, mO, a, h, smem, st);
   switch (a.bn) {
-    HALO_CASE(16)
-    HALO_CASE(32)
-    HALO_CASE(64)
-    HALO_CASE(128)
-    HALO_CASE(256)
+    ROWS_CASE(16)
+    ROWS_CASE(32)
+    ROWS_CASE(64)
+    ROWS_CASE(128)
   }
-#undef HALO_CASE
-  return fail(DRCB_ECONFIG, "unsupported N tile (halo)");
-}
-
-template <int KIND, int BN, bool RES>
-int launch_dx_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
-                 const ConvArgs& a, const DxArgs& h, size_t smem, cudaStream_t st) {
-  auto kern = k_conv_dx<KIND, BN, RES>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  int tiles = a.num_m_tiles * a.num_n_tiles;
-  int grid = tiles < nsm ? tiles : nsm;
-  kern<<<grid, DX_THREADS, smem, st>>>(mA, mB, mO, a, h);
-  count_launch();
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_dx");
-}
-
-template <int KIND>
-int launch_dx(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO, const ConvArgs& a,
-              const DxArgs& h, bool res, size_t smem, cudaStream_t st) {
-#define DX_CASE(BNV)                                                         \
-  case BNV:                                                                  \
-    return res ? launch_dx_bn<KIND, BNV, true>(mA, mB, mO, a, h, smem, st)   \
-               : launch_dx_bn<KIND, BNV, false>(mA, mB, mO, a, h, smem, st);
-  switch (a.bn) {
-    DX_CASE(16)
-    DX_CASE(32)
-    DX_CASE(64)
-    DX_CASE(128)
-  }
-#undef DX_CASE
-  return fail(DRCB_ECONFIG, "unsupported N tile (dx)");
+#undef ROWS_CASE
+  return fail(DRCB_ECONFIG, "unsupported N tile (row-tile kernel)");
 }
 
 // stage counts keep smem <= ~200 KB: BN=256 -> 48 KB/stage
@@ -1422,6 +1257,12 @@ struct Buf {
 };
 
 // one conv layer: in (NHWC, c_in_tot == layer cin_pad) -> out slice
+// dx-in-N vs halo for a row-tile layer (measured on B200)
+bool rows_use_dx(const ConvLayer& L, int kind) {
+  (void)kind;
+  return L.hw == 32 || L.cin_pad >= 256;
+}
+
 template <int KIND>
 int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cout_off,
               int64_t nmaps, cudaStream_t st, float* pred = nullptr, const Buf* up = nullptr) {
@@ -1469,64 +1310,48 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     }
   }
   CUtensorMap mA, mB;
-  if (hw >= 16 && !L.im2col && !getenv("DRCB_NO_DX")) {
-    // dx-in-N kernel: one rows+2 halo box per chunk; BN <= 128
-    static const char* bn_env = getenv("DRCB_DX_BN");
-    const int bn_cap = bn_env ? atoi(bn_env) : (KIND == 0 ? 128 : 64);
-    while (a.bn > bn_cap || a.bn > 128) a.bn /= 2;
+  if (hw >= 16 && !L.im2col && !getenv("DRCB_NO_ROWS")) {
+    // row-tile kernel (hw 16/32); DRCB_ROWS=dx|halo overrides the variant
+    static const char* mode_env = getenv("DRCB_ROWS");
+    const bool dx = mode_env ? std::strcmp(mode_env, "dx") == 0 : rows_use_dx(L, KIND);
+    const int bn_cap = KIND == 0 ? 128 : 64;
+    while (a.bn > bn_cap) a.bn /= 2;
     a.num_n_tiles = L.cout_pad / a.bn;
-    DxArgs dz;
-    dz.row_bytes = hw * ROW_BYTES;
-    dz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
+    RowArgs rz;
+    rz.row_bytes = hw * ROW_BYTES;
+    rz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
     const int b_tile = a.bn * ROW_BYTES;
     const int w_bytes = 9 * a.cblocks * b_tile;
-    dz.o_bytes = (pred || getenv("DRCB_NO_TMA_STORE")) ? 0 : BM * a.bn * (KIND == 0 ? 2 : 4);
-    const int budget = 200 * 1024 - 2 * dz.o_bytes;
-    const bool res = a.num_n_tiles == 1 && w_bytes + 3 * dz.a_bytes <= budget;
+    rz.o_bytes = pred ? 0 : BM * a.bn * (KIND == 0 ? 2 : 4);
+    const int budget = 200 * 1024 - 2 * rz.o_bytes;
+    const bool res = a.num_n_tiles == 1 && w_bytes + 3 * rz.a_bytes <= budget;
     if (res) {
-      dz.sb = 1;
-      dz.sa = std::min(8, (budget - w_bytes) / dz.a_bytes);
-    } else {
+      rz.sb = 1;
+      rz.sa = std::min(8, (budget - w_bytes) / rz.a_bytes);
+    } else if (dx) {
       // B triples are consumed three per A box
-      dz.sa = std::min(4, std::max(2, budget / (4 * dz.a_bytes)));
-      dz.sb = std::min(8, (budget - dz.sa * dz.a_bytes) / (3 * b_tile));
+      rz.sa = std::min(4, std::max(2, budget / (4 * rz.a_bytes)));
+      rz.sb = std::min(8, (budget - rz.sa * rz.a_bytes) / (3 * b_tile));
+    } else {
+      rz.sa = rz.sb = std::min(8, budget / (rz.a_bytes + 3 * b_tile));
     }
-    if (dz.sa >= 2 && (res || dz.sb >= 2)) {
+    if (rz.sa >= 2 && (res || rz.sb >= 2)) {
       rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, hw, a.rows_per_tile + 2, 1);
       if (rc) return rc;
       rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
       if (rc) return rc;
       CUtensorMap mO;
-      if (dz.o_bytes) {
+      if (rz.o_bytes) {
         rc = encode_act(&mO, out.p, KIND, out.c, hw, nmaps, hw, a.rows_per_tile, 1);
         if (rc) return rc;
       }
-      size_t smem = 1024 + size_t(res ? w_bytes : 0) + size_t(dz.sa) * dz.a_bytes +
-                    size_t(res ? 0 : dz.sb * 3 * b_tile) + 2 * size_t(dz.o_bytes) + 512;
-      return launch_dx<KIND>(mA, mB, mO, a, dz, res, smem, st);
+      size_t smem = 1024 + size_t(res ? w_bytes : 0) + size_t(rz.sa) * rz.a_bytes +
+                    size_t(res ? 0 : rz.sb * 3 * b_tile) + 2 * size_t(rz.o_bytes) + 512;
+      return dx ? launch_rows<KIND, true>(mA, mB, mO, a, rz, res, smem, st)
+                : launch_rows<KIND, false>(mA, mB, mO, a, rz, res, smem, st);
     }
     a.bn = L.cout_pad >= 256 ? 256 : L.cout_pad;
     a.num_n_tiles = L.cout_pad / a.bn;
-  }
-  if (hw >= 16 && !L.im2col && !getenv("DRCB_NO_HALO")) {
-    // row-halo kernel: box of rows+2 image rows per (chunk, dx) stage
-    HaloArgs hz;
-    hz.row_bytes = hw * ROW_BYTES;
-    hz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
-    const int b_tile = a.bn * ROW_BYTES;
-    const int w_bytes = 9 * a.cblocks * b_tile;
-    const int budget = 200 * 1024;
-    hz.res = (a.num_n_tiles == 1 && w_bytes + 3 * hz.a_bytes <= budget) ? 1 : 0;
-    int stage_bytes = hz.a_bytes + (hz.res ? 0 : 3 * b_tile);
-    hz.stages = std::min(8, (budget - (hz.res ? w_bytes : 0)) / stage_bytes);
-    if (hz.stages >= 2) {
-      rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, hw, a.rows_per_tile + 2, 1);
-      if (rc) return rc;
-      rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
-      if (rc) return rc;
-      size_t smem = 1024 + size_t(hz.res ? w_bytes : 0) + size_t(hz.stages) * stage_bytes + 256;
-      return launch_halo<KIND>(mA, mB, a, hz, smem, st);
-    }
   }
   int box_w = hw, box_h = a.maps_per_tile == 1 ? a.rows_per_tile : hw, box_n = a.maps_per_tile;
   rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, box_w, box_h, box_n);
