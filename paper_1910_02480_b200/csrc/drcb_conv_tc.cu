@@ -980,44 +980,54 @@ __global__ void __launch_bounds__(256) k_pool_nhwc(const T* __restrict__ in, int
 
 // bilinear 2x (align_corners=False) of an NHWC buffer (C channels) into the
 // leading channel slice of the decoder concat buffer (cnn.py:159-174), rows
-// then columns like the reference; compile-time shapes, one thread per
-// (output pixel, 4 x 16 B channel groups)
+// then columns like the reference. One thread per (2x2 output block, 16-B
+// channel group), groups fastest: the 3x3 input neighbourhood is loaded once
+// for four outputs and a warp's stores cover whole 32-B sectors.
 template <typename T, int HW_IN, int C>
 __global__ void __launch_bounds__(256) k_up_nhwc(const T* __restrict__ in, T* __restrict__ out,
                                                  int c_tot, int64_t nmaps) {
   constexpr int V = Vec<T>::N;
   constexpr int G = C / V;
-  constexpr int GPT = G >= 4 ? 4 : G;
-  constexpr int TPP = G / GPT;
   constexpr int HO = 2 * HW_IN;
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= nmaps * HO * HO * TPP) return;
-  const int gq = int(i % TPP);
-  const int64_t px = i / TPP;
-  const int x = int(px % HO), y = int((px / HO) % HO);
-  const int64_t n = px / (HO * HO);
-  int r0, r1, c0, c1;
-  float fr, fc;
-  up_w(y, HW_IN, r0, r1, fr);
-  up_w(x, HW_IN, c0, c1, fc);
-  const float omr = 1.f - fr, omc = 1.f - fc;
-  const T* b = in + n * HW_IN * HW_IN * C;
-  T* o = out + px * c_tot;
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nmaps * HW_IN * HW_IN * G) return;
+  const int g = int(t % G) * V;
+  const int64_t blk = t / G;
+  const int j = int(blk % HW_IN), i = int((blk / HW_IN) % HW_IN);
+  const int64_t n = blk / (HW_IN * HW_IN);
+  const T* b = in + n * HW_IN * HW_IN * C + g;
+  // neighbourhood rows/cols i-1, i, i+1 (clamped; up_w only selects in-range ones)
+  float nb[3][3][V];
 #pragma unroll
-  for (int k = 0; k < GPT; ++k) {
-    const int g = (k * TPP + gq) * V;  // adjacent 16-B groups per instruction
-    float p00[V], p10[V], p01[V], p11[V], v[V];
-    unpack<T>(__ldg(reinterpret_cast<const uint4*>(b + (r0 * HW_IN + c0) * C + g)), p00);
-    unpack<T>(__ldg(reinterpret_cast<const uint4*>(b + (r1 * HW_IN + c0) * C + g)), p10);
-    unpack<T>(__ldg(reinterpret_cast<const uint4*>(b + (r0 * HW_IN + c1) * C + g)), p01);
-    unpack<T>(__ldg(reinterpret_cast<const uint4*>(b + (r1 * HW_IN + c1) * C + g)), p11);
+  for (int dr = 0; dr < 3; ++dr) {
+    const int r = min(max(i + dr - 1, 0), HW_IN - 1);
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      float t0 = __fadd_rn(__fmul_rn(p00[j], omr), __fmul_rn(p10[j], fr));
-      float t1 = __fadd_rn(__fmul_rn(p01[j], omr), __fmul_rn(p11[j], fr));
-      v[j] = __fadd_rn(__fmul_rn(t0, omc), __fmul_rn(t1, fc));
+    for (int dc = 0; dc < 3; ++dc) {
+      const int c = min(max(j + dc - 1, 0), HW_IN - 1);
+      unpack<T>(__ldg(reinterpret_cast<const uint4*>(b + (r * HW_IN + c) * C)), nb[dr][dc]);
     }
-    *reinterpret_cast<uint4*>(o + g) = pack<T>(v);
+  }
+  // up_w in neighbourhood coordinates with compile-time indices: even
+  // output 2i -> rows (i-1, i), weight 0.75 (0 at i = 0, where the clamped
+  // row i-1 is row 0 and the result is row 0 exactly as in the reference);
+  // odd 2i+1 -> rows (i, i+1 clamped), weight 0.25
+  const float fr_even = i == 0 ? 0.f : 0.75f, fc_even = j == 0 ? 0.f : 0.75f;
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const float fr = a ? 0.25f : fr_even, omr = 1.f - fr;
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb) {
+      const float fc = bb ? 0.25f : fc_even, omc = 1.f - fc;
+      float v[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        float t0 = __fadd_rn(__fmul_rn(nb[a][bb][e], omr), __fmul_rn(nb[a + 1][bb][e], fr));
+        float t1 = __fadd_rn(__fmul_rn(nb[a][bb + 1][e], omr), __fmul_rn(nb[a + 1][bb + 1][e], fr));
+        v[e] = __fadd_rn(__fmul_rn(t0, omc), __fmul_rn(t1, fc));
+      }
+      const int64_t px = (n * HO + 2 * i + a) * HO + 2 * j + bb;
+      *reinterpret_cast<uint4*>(out + px * c_tot + g) = pack<T>(v);
+    }
   }
 }
 
@@ -1032,9 +1042,7 @@ void launch_pool(const T* in, int c_tot, int off, T* out, int64_t nmaps, cudaStr
 
 template <typename T, int HW_IN, int C>
 void launch_up(const T* in, T* out, int c_tot, int64_t nmaps, cudaStream_t st) {
-  constexpr int G = C / Vec<T>::N;
-  constexpr int TPP = G / (G >= 4 ? 4 : G);
-  int64_t tot = nmaps * 4 * HW_IN * HW_IN * TPP;
+  int64_t tot = nmaps * HW_IN * HW_IN * (C / Vec<T>::N);
   k_up_nhwc<T, HW_IN, C><<<unsigned((tot + 255) / 256), 256, 0, st>>>(in, out, c_tot, nmaps);
   count_launch();
 }
