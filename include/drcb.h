@@ -215,9 +215,11 @@ int drcb_net_forward(const DrcbNet *net, const float *x, float *y, int64_t n,
 int drcb_debug_conv(int32_t mode, int32_t cin, int32_t cout, int32_t hw, int64_t n,
                     const float *x, const float *w, float *y);
 
-/* traversal counters for roofline accounting: buf = device u64[10]
- * {inner nodes visited, primitives tested, casts}, accumulated by every
- * cast until disarmed with NULL (adds one atomic per cast when armed). */
+/* traversal counters for roofline accounting: buf = device u64[12]
+ * {inner nodes visited, primitives tested, casts, max nodes, max prims,
+ * prims-tested histogram [5], sum of converged lanes at cast entry, any-hit
+ * casts}, accumulated by every cast until disarmed with NULL (adds a few
+ * atomics per cast when armed). */
 int drcb_trav_stats(unsigned long long *buf);
 
 /* number of kernels this library has launched so far (process-wide) */

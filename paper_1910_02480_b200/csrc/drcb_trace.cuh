@@ -116,55 +116,33 @@ __device__ __forceinline__ float f_ru(float x) { return x; }
 
 constexpr int TRAV_SENTINEL = 0x76543210;
 
-// leaf primitives tests; returns true on an any-hit termination
-template <typename R, bool ANY>
-__device__ __forceinline__ bool test_leaf(const DevScene& S, int leaf, V3<R> O, V3<R> D, R tmin,
-                                          R tmax, HitRec<R>& best, float& tbest,
-                                          unsigned& n_prims) {
-  constexpr float ROB = 1.0f + 4.0f * 5.97e-8f;
-  int code = ~leaf;
-  int start = code >> 3, count = (code & 7) + 1;
-  n_prims += count;
-  for (int s = start; s < start + count; ++s) {
-    V3<R> v0, e1, e2;
-    int id;
-    leaf_tri<R>(S, s, v0, e1, e2, id);
-    R t;
-    bool ok;
-    R bound = ANY ? tmax : best.t;
-    if (id >= S.n_s + S.n_q) {
-      ok = tri_t(v0, e1, e2, O, D, tmin, bound, t);
-    } else if (id >= S.n_s) {
-      ok = quad_t(S, id - S.n_s, O, D, tmin, bound, t);
-    } else {
-      ok = sphere_t(S, id, O, D, tmin, bound, t);
-    }
-    if (ok) {
-      if (ANY) {
-        best.t = t;
-        best.prim = id;
-        return true;
-      }
-      if (improves(t, id, best.t, best.prim)) {
-        best.t = t;
-        best.prim = id;
-        tbest = f_ru(t) * ROB;
-      }
-    }
-  }
-  return false;
+// one primitive test; returns whether it hit inside (tmin, bound)
+template <typename R>
+__device__ __forceinline__ bool test_prim(const DevScene& S, int slot, V3<R> O, V3<R> D, R tmin,
+                                          R bound, R& t, int& id) {
+  V3<R> v0, e1, e2;
+  leaf_tri<R>(S, slot, v0, e1, e2, id);
+  if (id >= S.n_s + S.n_q) return tri_t(v0, e1, e2, O, D, tmin, bound, t);
+  if (id >= S.n_s) return quad_t(S, id - S.n_s, O, D, tmin, bound, t);
+  return sphere_t(S, id, O, D, tmin, bound, t);
 }
 
 // Closest hit (ANY=false) or any hit in (tmin, tmax] (ANY=true) over the BVH.
-// "While-while" traversal with speculative leaf postponement (Aila & Laine
-// 2009): lanes descend inner nodes until every active lane of the warp holds
-// a postponed leaf, then all lanes test leaves together, so inner-node and
-// leaf code do not alternate lane by lane. Result is traversal-order
-// independent (nearest t, ties -> lowest prim id).
+// Warp-synchronous while-while traversal with speculative leaf postponement
+// (Aila & Laine 2009): every lane that entered runs every iteration of ONE
+// loop whose phase is warp-uniform. INNER phase: lanes step one node; a lane
+// reaching a leaf postpones it and keeps descending speculatively until it
+// meets a second leaf. The warp switches to the LEAF phase when no lane is
+// still searching for its first leaf, and stays there while any lane has
+// primitives left: each iteration tests ONE primitive per lane, so leaf work
+// of different lanes is done side by side instead of lane after lane. The
+// result is traversal-order independent (nearest t, ties -> lowest prim id).
 template <typename R, bool ANY>
 __device__ HitRec<R> traverse(const DevScene& S, V3<R> O, V3<R> D, R tmin, R tmax) {
   HitRec<R> best{tmax, -1};
   if (S.n_prims == 0) return best;
+  const unsigned tmask = __activemask();
+  const int entry_lanes = __popc(tmask);
   const float ox = float(O.x), oy = float(O.y), oz = float(O.z);
   auto safe_inv = [](R d) -> float {
     float f = float(d);
@@ -177,56 +155,85 @@ __device__ HitRec<R> traverse(const DevScene& S, V3<R> O, V3<R> D, R tmin, R tma
   int stack[TRAV_STACK];
   int sp = 0;
   stack[0] = TRAV_SENTINEL;
-  int node = 0;
-  int leaf = 0;  // >= 0: no postponed leaf
+  int node = 0;        // >= 0 inner node, < 0 leaf code, SENTINEL = stack empty
+  int postponed = 0;   // < 0: a leaf found while searching
+  int pcur = 0, pend = 0;  // primitive cursor of the leaf under test
+  bool leaf_phase = false;
   unsigned n_nodes = 0, n_prims = 0;
   float tbest = isinf(float(tmax)) ? INFINITY : f_ru(tmax) * ROB;
-  while (node != TRAV_SENTINEL) {
-    // inner nodes until all lanes have a postponed leaf
-    while (unsigned(node) < unsigned(TRAV_SENTINEL)) {
-      ++n_nodes;
-      const float4* nd = S.nodes + 4 * node;
-      float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2), d = __ldg(nd + 3);
-      float tx0 = a.x * ix - oix, tx1 = a.y * ix - oix;
-      float ty0 = a.z * iy - oiy, ty1 = a.w * iy - oiy;
-      float tz0 = c.x * iz - oiz, tz1 = c.y * iz - oiz;
-      float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
-      float f0 = fminf(fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fmaxf(tz0, tz1)) * ROB, tbest);
-      float sx0 = b.x * ix - oix, sx1 = b.y * ix - oix;
-      float sy0 = b.z * iy - oiy, sy1 = b.w * iy - oiy;
-      float sz0 = c.z * iz - oiz, sz1 = c.w * iz - oiz;
-      float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), 0.0f));
-      float f1 = fminf(fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fmaxf(sz0, sz1)) * ROB, tbest);
-      bool h0 = n0 <= f0, h1 = n1 <= f1;
-      int c0 = __float_as_int(d.x), c1 = __float_as_int(d.y);
-      if (!h0 && !h1) {
-        node = stack[sp--];
-      } else {
-        node = h0 ? c0 : c1;
-        if (h0 && h1) {
-          int other = c1;
-          if (n1 < n0) {
-            node = c1;
-            other = c0;
+  while (true) {
+    const bool inner = node >= 0 && node != TRAV_SENTINEL;
+    const bool leafwork = pcur < pend || postponed < 0 || node < 0;
+    const bool searching = inner && postponed >= 0 && pcur >= pend;
+    const unsigned any_search = __ballot_sync(tmask, searching);
+    const unsigned any_leaf = __ballot_sync(tmask, leafwork);
+    if (!any_search && !any_leaf) break;
+    leaf_phase = any_leaf && (leaf_phase || !any_search);
+    if (!leaf_phase) {
+      if (inner && pcur >= pend) {
+        ++n_nodes;
+        const float4* nd = S.nodes + 4 * node;
+        float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2), d = __ldg(nd + 3);
+        float tx0 = a.x * ix - oix, tx1 = a.y * ix - oix;
+        float ty0 = a.z * iy - oiy, ty1 = a.w * iy - oiy;
+        float tz0 = c.x * iz - oiz, tz1 = c.y * iz - oiz;
+        float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+        float f0 = fminf(fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fmaxf(tz0, tz1)) * ROB, tbest);
+        float sx0 = b.x * ix - oix, sx1 = b.y * ix - oix;
+        float sy0 = b.z * iy - oiy, sy1 = b.w * iy - oiy;
+        float sz0 = c.z * iz - oiz, sz1 = c.w * iz - oiz;
+        float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), 0.0f));
+        float f1 = fminf(fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fmaxf(sz0, sz1)) * ROB, tbest);
+        bool h0 = n0 <= f0, h1 = n1 <= f1;
+        int c0 = __float_as_int(d.x), c1 = __float_as_int(d.y);
+        if (!h0 && !h1) {
+          node = stack[sp--];
+        } else {
+          node = h0 ? c0 : c1;
+          if (h0 && h1) {
+            int other = c1;
+            if (n1 < n0) {
+              node = c1;
+              other = c0;
+            }
+            if (sp + 1 < TRAV_STACK) stack[++sp] = other;
           }
-          if (sp + 1 < TRAV_STACK) stack[++sp] = other;
+        }
+        if (node < 0 && postponed >= 0) {  // first leaf: postpone, keep descending
+          postponed = node;
+          node = stack[sp--];
         }
       }
-      if (node < 0 && leaf >= 0) {  // first leaf: postpone, keep descending
-        leaf = node;
-        node = stack[sp--];
+    } else if (leafwork) {
+      if (pcur >= pend) {  // next leaf: the postponed one, then the current node
+        int code;
+        if (postponed < 0) {
+          code = ~postponed;
+          postponed = 0;
+        } else {
+          code = ~node;
+          node = stack[sp--];
+        }
+        pcur = code >> 3;
+        pend = pcur + (code & 7) + 1;
+        n_prims += pend - pcur;
       }
-      if (!__any_sync(__activemask(), leaf >= 0)) break;
-    }
-    // postponed leaves
-    while (leaf < 0) {
-      if (test_leaf<R, ANY>(S, leaf, O, D, tmin, tmax, best, tbest, n_prims)) {
-        node = TRAV_SENTINEL;
-        leaf = 0;
-        break;
+      R t;
+      int id;
+      if (test_prim<R>(S, pcur, O, D, tmin, ANY ? tmax : best.t, t, id)) {
+        if (ANY) {
+          best.t = t;
+          best.prim = id;
+          node = TRAV_SENTINEL;
+          postponed = 0;
+          pend = pcur;
+        } else if (improves(t, id, best.t, best.prim)) {
+          best.t = t;
+          best.prim = id;
+          tbest = f_ru(t) * ROB;
+        }
       }
-      leaf = node;
-      if (node < 0) node = stack[sp--];
+      ++pcur;
     }
   }
   if (g_trav_stats) {
@@ -238,6 +245,8 @@ __device__ HitRec<R> traverse(const DevScene& S, V3<R> O, V3<R> D, R tmin, R tma
     // histogram of prims tested: [0,8) [8,32) [32,128) [128,512) [512,inf)
     int b = n_prims < 8 ? 0 : n_prims < 32 ? 1 : n_prims < 128 ? 2 : n_prims < 512 ? 3 : 4;
     atomicAdd(g_trav_stats + 5 + b, 1ull);
+    atomicAdd(g_trav_stats + 10, (unsigned long long)entry_lanes);
+    if (ANY) atomicAdd(g_trav_stats + 11, 1ull);
   }
   return best;
 }
