@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(MAP_TPB, 3) k_map_paths(DevScene S, DrcbRender
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   bool have = false, done_all = false;
-  int64_t job = 0;
+  int64_t job = 0, slot = 0;
   int seg = 0;
   bool prev_delta = true;
   R prev_pdf = R(0);
@@ -255,7 +255,11 @@ __global__ void __launch_bounds__(MAP_TPB, 3) k_map_paths(DevScene S, DrcbRender
     int tex = 0;
     if (fresh) {
       p = job / MAP_TEXELS;
-      tex = int(job % MAP_TEXELS);
+      // 32 consecutive jobs = an 8x4 texel block (a compact solid angle)
+      // rather than a 32-texel row: coherent first-bounce rays per warp
+      const int k = int(job % MAP_TEXELS), blk = k >> 5, w = k & 31;
+      tex = ((blk >> 2) * 4 + (w >> 3)) * MAP_RES + (blk & 3) * 8 + (w & 7);
+      slot = p * MAP_TEXELS + tex;
       V3<R> hp = ldr3(pos + 3 * p), hn = ldr3(nrm + 3 * p);
       Frame<R> fr = frame_scalar(S, hn);
       D = fr.to_world(texel_local<R>(tex % MAP_RES, tex / MAP_RES));
@@ -268,8 +272,8 @@ __global__ void __launch_bounds__(MAP_TPB, 3) k_map_paths(DevScene S, DrcbRender
       Frame<R> fr = frame_scalar(S, ldr3(nrm + 3 * p));
       bool facing = dot(h.normal, D) > R(0);
       V3<R> nf3 = facing ? -h.normal : h.normal;
-      dist[job] = h.hit ? h.t : R(0);
-      st3(nloc + 3 * job, h.hit ? fr.to_local(nf3) : mk<R>(R(0), R(0), R(0)));
+      dist[slot] = h.hit ? h.t : R(0);
+      st3(nloc + 3 * slot, h.hit ? fr.to_local(nf3) : mk<R>(R(0), R(0), R(0)));
       rng.init(cfg.seed, keys[p], uint64_t(tex), cfg.sampler_kind,
                uint32_t(cfg.map_spp > 1 ? cfg.map_spp : 1));
       L = mk<R>(R(0), R(0), R(0));
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(MAP_TPB, 3) k_map_paths(DevScene S, DrcbRender
         L = mk<R>(R(0), R(0), R(0));
         ++nf;
       }
-      st3(rad + 3 * job, L);
+      st3(rad + 3 * slot, L);
       have = false;
     }
   }
