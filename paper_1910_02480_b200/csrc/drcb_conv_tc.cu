@@ -229,7 +229,6 @@ struct ConvArgs {
   // slice (up_ctot channels per pixel) instead of the low-res tensor
   void* up_out;
   int up_ctot;
-  int taps1;  // 1-tap (im2col input) GEMM: every K block uses the centre tap
 };
 
 template <int KIND, int BN, int STAGES>
@@ -468,7 +467,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           y0 = 0;
         }
         for (int kb = 0; kb < p.num_kb; ++kb) {
-          int tap = p.taps1 ? 4 : kb / p.cblocks, cb = kb % p.cblocks;
+          int tap = kb / p.cblocks, cb = kb % p.cblocks;
           int dy = tap / 3 - 1, dx = tap % 3 - 1;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * SM::STAGE_BYTES;
@@ -859,6 +858,226 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// enc1.conv1 (7 -> 64 channels @ 32x32) from the compact network input: NHWC
+// with 8 channels per pixel (7 + one zero), 16 B (bf16) / 32 B (tf32) per
+// pixel, 1/8 of a channel-padded layout's bytes. The im2col operand is built
+// in SMEM: K value tap*8 + c of pixel (y, x) is channel c of pixel
+// (y + tap/3 - 1, x + tap%3 - 1); 9 taps x 8 = 72 K values, zero-padded to
+// whole 128-B swizzle rows (bf16: 2 K chunks, tf32: 3).
+//   warp 0: TMA of the tile's input rows y0-1 .. y0+4 (OOB rows = 0)
+//   warp 1: tcgen05.mma (M = 128, N = 64) into double-buffered TMEM
+//   warps 2-5: build the im2col tile (one pixel per thread, 9 x 16-B pieces
+//              per tap group; the x border is zeroed here)
+//   warps 6-9: folded BN + LeakyReLU epilogue staged in SMEM, TMA store
+constexpr int IN8_THREADS = 320;
+constexpr int IN8_SI = 4, IN8_SA = 2;
+
+template <int KIND>
+__global__ void __launch_bounds__(IN8_THREADS, 1)
+    k_conv_in8(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapB,
+               const __grid_constant__ CUtensorMap mapO, const __grid_constant__ ConvArgs p) {
+  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int PX_BYTES = 8 * ELEM;                  // one input pixel
+  constexpr int PPT = PX_BYTES / 16;                  // 16-B pieces per tap
+  constexpr int NCH = (72 * ELEM + ROW_BYTES - 1) / ROW_BYTES;  // K chunks
+  constexpr int BN = 64;
+  constexpr int IN_BYTES = 6 * 32 * PX_BYTES;         // rows y0-1 .. y0+4
+  constexpr int A_BYTES = NCH * BM * ROW_BYTES;
+  constexpr int W_BYTES = NCH * BN * ROW_BYTES;
+  constexpr int O_BYTES = BM * BN * ELEM;
+  constexpr int CEL = ROW_BYTES / ELEM;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;                          // IN8_SA x A_BYTES
+  uint8_t* sw = sa + IN8_SA * A_BYTES;         // W_BYTES
+  uint8_t* so = sw + W_BYTES;                  // 2 x O_BYTES
+  uint8_t* si = so + 2 * O_BYTES;              // IN8_SI x IN_BYTES
+  uint64_t* bars = reinterpret_cast<uint64_t*>(si + IN8_SI * IN_BYTES);
+  uint64_t* ifull = bars;
+  uint64_t* iempty = bars + IN8_SI;
+  uint64_t* afull = bars + 2 * IN8_SI;
+  uint64_t* aempty = afull + IN8_SA;
+  uint64_t* tfull = aempty + IN8_SA;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* wfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfull + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&mapX);
+    prefetch_map(&mapB);
+    for (int i = 0; i < IN8_SI; ++i) {
+      mbar_init(&ifull[i], 1);
+      mbar_init(&iempty[i], 4);
+    }
+    for (int i = 0; i < IN8_SA; ++i) {
+      mbar_init(&afull[i], 4);
+      mbar_init(&aempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    mbar_init(wfull, 1);
+    fence_barrier_init();
+  }
+  if (warp >= 2 && warp < 6) {
+    // K padding pieces (never rewritten): zero them once in every A stage
+    const int r = threadIdx.x - 64;
+    for (int st = 0; st < IN8_SA; ++st)
+      for (int j = 9 * PPT; j < NCH * 8; ++j)
+        sts128(smem_u32(sa + st * A_BYTES + (j >> 3) * (BM * ROW_BYTES) + r * ROW_BYTES) +
+                   (((j & 7) ^ (r & 7)) << 4),
+               0u, 0u, 0u, 0u);
+    fence_proxy_async();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(128u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = p.num_m_tiles;
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(wfull, uint32_t(W_BYTES));
+      for (int c = 0; c < NCH; ++c) tma_load_2d(&mapB, wfull, sw + c * BN * ROW_BYTES, c * CEL, 0);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&iempty[st], ph ^ 1);
+        mbar_expect_tx(&ifull[st], uint32_t(IN_BYTES));
+        tma_load_4d(&mapX, &ifull[st], si + st * IN_BYTES, 0, 0, (tile & 7) * 4 - 1, tile >> 3);
+        if (++st == IN8_SI) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(KIND, BM, BN);
+      mbar_wait(wfull, 0);
+      int st = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        mbar_wait(&afull[st], ph);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sa + st * A_BYTES), b0 = smem_u32(sw);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int k = 0; k < ROW_BYTES / 32; ++k)
+            tc_mma<KIND>(tmem_base + acc * BN, sw128_desc(a0 + c * BM * ROW_BYTES + 32 * k),
+                         sw128_desc(b0 + c * BN * ROW_BYTES + 32 * k), idesc, (c | k) ? 1u : 0u);
+        tc_commit(&aempty[st]);
+        tc_commit(&tfull[acc]);
+        if (++st == IN8_SA) {
+          st = 0;
+          ph ^= 1;
+        }
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // im2col builders: thread r = tile pixel (row r / 32, column r % 32)
+    const int r = threadIdx.x - 64, ry = r >> 5, x = r & 31;
+    int ist = 0, ast = 0;
+    uint32_t iph = 0, aph = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      mbar_wait(&ifull[ist], iph);
+      mbar_wait(&aempty[ast], aph ^ 1);
+      const uint32_t src = smem_u32(si + ist * IN_BYTES);
+      const uint32_t dst = smem_u32(sa + ast * A_BYTES) + r * ROW_BYTES;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        const int xs = x + t % 3 - 1;
+        const bool ok = xs >= 0 && xs < 32;
+        const uint32_t a = src + ((ry + t / 3) * 32 + (ok ? xs : 0)) * PX_BYTES;
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) {
+          uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+          if (ok)
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                         : "r"(a + 16 * q));
+          const int j = t * PPT + q;
+          sts128(dst + (j >> 3) * (BM * ROW_BYTES) + (((j & 7) ^ (r & 7)) << 4), v0, v1, v2, v3);
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&iempty[ist]);
+        mbar_arrive(&afull[ast]);
+      }
+      if (++ist == IN8_SI) {
+        ist = 0;
+        iph ^= 1;
+      }
+      if (++ast == IN8_SA) {
+        ast = 0;
+        aph ^= 1;
+      }
+    }
+  } else {
+    // epilogue warps 6..9 -> TMEM lane quarter warp % 4
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int acc = 0, obuf = 0;
+    uint32_t aph = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int64_t m = int64_t(tile) * BM + row;
+      uint8_t* ot = so + obuf * O_BYTES;
+      if (threadIdx.x == 192) bulk_wait_read1();
+      asm volatile("bar.sync 3, 128;" ::: "memory");
+      epilogue_stage<KIND, BN, false, 16>(p, tmem_base + (uint32_t(q * 32) << 16) + acc * BN, m, 0,
+                                          ot, 0);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      fence_proxy_async();
+      asm volatile("bar.sync 3, 128;" ::: "memory");
+      if (threadIdx.x == 192) {
+        for (int sb = 0; sb < BN / CEL; ++sb)
+          tma_store_4d(&mapO, ot + sb * BM * ROW_BYTES, p.cout_off + sb * CEL, 0, (tile & 7) * 4,
+                       tile >> 3);
+        bulk_commit();
+      }
+      obuf ^= 1;
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
+      }
+    }
+    if (threadIdx.x == 192) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(128u));
+  }
+}
+
+template <int KIND>
+constexpr size_t in8_smem() {
+  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int NCH = (72 * ELEM + ROW_BYTES - 1) / ROW_BYTES;
+  return 1024 + size_t(IN8_SA) * NCH * BM * ROW_BYTES + size_t(NCH) * 64 * ROW_BYTES +
+         2 * size_t(BM) * 64 * ELEM + size_t(IN8_SI) * 6 * 32 * 8 * ELEM + 256;
+}
+
+// ---------------------------------------------------------------------------
 // NHWC helper kernels (element type T = bf16 or fp32)
 template <typename T>
 __device__ __forceinline__ float ldf(const T* p);
@@ -917,30 +1136,24 @@ __device__ __forceinline__ uint4 pack<float>(const float* f) {
                     __float_as_uint(round_tf32(f[2])), __float_as_uint(round_tf32(f[3])));
 }
 
-// NCHW fp32 stack (n,7,32,32) -> im2col network input (n_pad,32,32,64):
-// K value k = tap * 7 + c of pixel (y, x) is channel c of pixel
-// (y + tap/3 - 1, x + tap%3 - 1), zero outside the map, k = 63 zero. One
-// thread per (pixel, 16-B piece): a warp writes 512 contiguous bytes.
+// NCHW fp32 stack (n,7,32,32) -> compact NHWC network input (n_pad,32,32,8),
+// channel 7 and padding maps zero; one thread per (pixel, 16-B piece)
 template <typename T>
 __global__ void k_stack_to_nhwc(const float* __restrict__ x, int64_t n, int64_t n_pad, int,
                                 T* __restrict__ out) {
-  constexpr int V = Vec<T>::N;   // K values per 16-B piece
-  constexpr int PP = 64 / V;     // pieces per pixel
+  constexpr int V = Vec<T>::N;   // channels per 16-B piece
+  constexpr int PP = 8 / V;      // pieces per pixel
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n_pad * 1024 * PP) return;
   const int piece = int(i % PP);
   const int64_t px = i / PP;
   const int64_t map = px / 1024;
-  const int pix = int(px % 1024), y = pix >> 5, xx = pix & 31;
+  const int pix = int(px % 1024);
   float f[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
-    const int k = piece * V + j;
-    const int tap = k / 7, c = k % 7;
-    const int yy = y + tap / 3 - 1, xs = xx + tap % 3 - 1;
-    f[j] = (k < 63 && map < n && yy >= 0 && yy < 32 && xs >= 0 && xs < 32)
-               ? __ldg(x + (map * 7 + c) * 1024 + yy * 32 + xs)
-               : 0.f;
+    const int c = piece * V + j;
+    f[j] = (c < 7 && map < n) ? __ldg(x + (map * 7 + c) * 1024 + pix) : 0.f;
   }
   reinterpret_cast<uint4*>(out)[i] = pack<T>(f);
 }
@@ -1139,8 +1352,10 @@ int pad_c(int c, int kind) {
 // pack conv-form weights (cout, cin, 3, 3) into K-major (cout_pad, 9*cin_pad)
 int prepare_layer(NetImpl& net, ConvLayer& L, int kind) {
   if (L.tc_kind == kind) return 0;
-  L.im2col = (L.name == "enc1.conv1" && L.cin == 7);
-  const int cinp = L.im2col ? 64 : pad_c(L.cin, kind);
+  L.in8 = (L.name == "enc1.conv1" && L.cin <= 8);
+  // in8: K = 9 taps x 8 channels rounded up to whole 128-B rows
+  const int cinp = L.in8 ? ((72 * (kind == 0 ? 2 : 4) + ROW_BYTES - 1) / ROW_BYTES) * (ROW_BYTES / (kind == 0 ? 2 : 4))
+                         : pad_c(L.cin, kind);
   // output channels are padded to the next layer's K granularity; padded
   // channels get zero weights and zero epilogue vectors, so they hold exact
   // zeros (head.deconv1's k/2 outputs feed a K-padded input). The fused head
@@ -1148,9 +1363,9 @@ int prepare_layer(NetImpl& net, ConvLayer& L, int kind) {
   const int coutp = (L.name == "head.deconv2") ? 16 : pad_c(L.cout, kind);
   L.cin_pad = cinp;
   L.cout_pad = coutp;
-  const int64_t ktot = L.im2col ? 64 : int64_t(9) * cinp;
+  const int64_t ktot = L.in8 ? cinp : int64_t(9) * cinp;
   // K index of (input channel ci, tap t) in the packed operand
-  auto kidx = [&](int ci, int t) -> int64_t { return L.im2col ? t * 7 + ci : int64_t(t) * cinp + ci; };
+  auto kidx = [&](int ci, int t) -> int64_t { return L.in8 ? t * 8 + ci : int64_t(t) * cinp + ci; };
   std::vector<float> a(coutp, 0.f), b(coutp, 0.f);
   for (int c = 0; c < L.cout; ++c) {
     a[c] = L.scale[c];
@@ -1271,11 +1486,67 @@ bool rows_use_dx(const ConvLayer& L, int kind) {
   return L.hw == 32 || L.cin_pad >= 256;
 }
 
+// enc1.conv1 through k_conv_in8 (input: 8-channel NHWC, out: BN + LeakyReLU)
+template <int KIND>
+int run_in8(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cout_off, int64_t nmaps,
+            cudaStream_t st) {
+  if (in.c != 8 || L.hw != 32 || L.cout_pad != 64)
+    return fail(DRCB_ECONTRACT, "enc1.conv1 expects the 8-channel 32x32 input and 64 outputs");
+  ConvArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.hw = 32;
+  a.maps_per_tile = 1;
+  a.rows_per_tile = 4;
+  a.tiles_per_map = 8;
+  a.num_m_tiles = int(nmaps * 8);
+  a.num_n_tiles = 1;
+  a.bn = 64;
+  a.cout = 64;
+  a.cout_tot = out.c;
+  a.cout_off = cout_off;
+  a.ep_a = L.d_ep_a;
+  a.ep_b = L.d_ep_b;
+  a.slope = net.slope;
+  a.out = out.p;
+  auto enc = get_encode();
+  if (!enc) return fail(DRCB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const int es = KIND == 0 ? 2 : 4;
+  CUtensorMap mX, mB, mO;
+  cuuint64_t dims[4] = {8, 32, 32, cuuint64_t(nmaps)};
+  cuuint64_t strides[3] = {cuuint64_t(8 * es), cuuint64_t(8 * es * 32), cuuint64_t(8 * es * 1024)};
+  cuuint32_t box[4] = {8, 32, 6, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(&mX, KIND == 0 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                   in.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DRCB_ECUDA, "cuTensorMapEncodeTiled(in8) failed: " + std::to_string(int(r)));
+  int rc = encode_w(&mB, L.d_wtc, KIND, L.cin_pad, 64, 64);
+  if (rc) return rc;
+  rc = encode_act(&mO, out.p, KIND, out.c, 32, nmaps, 32, 4, 1);
+  if (rc) return rc;
+  auto kern = k_conv_in8<KIND>;
+  constexpr size_t smem = in8_smem<KIND>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  int grid = a.num_m_tiles < nsm ? a.num_m_tiles : nsm;
+  kern<<<grid, IN8_THREADS, smem, st>>>(mX, mB, mO, a);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_in8");
+}
+
 template <int KIND>
 int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cout_off,
               int64_t nmaps, cudaStream_t st, float* pred = nullptr, const Buf* up = nullptr) {
   int rc = prepare_layer(net, L, KIND);
   if (rc) return rc;
+  if (L.in8) return run_in8<KIND>(net, L, in, out, cout_off, nmaps, st);
   if (in.c != L.cin_pad) return fail(DRCB_ECONTRACT, "tc layer input channels mismatch for " + L.name);
   const int hw = L.hw;
   ConvArgs a;
@@ -1292,8 +1563,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
   }
   a.num_m_tiles = int(nmaps * hw * hw / BM);
   a.cblocks = L.cin_pad / (ROW_BYTES / (KIND == 0 ? 2 : 4));
-  a.num_kb = (L.im2col ? 1 : 9) * a.cblocks;
-  a.taps1 = L.im2col ? 1 : 0;
+  a.num_kb = 9 * a.cblocks;
   a.bn = L.cout_pad >= 256 ? 256 : L.cout_pad;
   a.num_n_tiles = L.cout_pad / a.bn;
   a.cout = pred ? L.cout_pad : L.cout_pad;  // padded channels carry exact zeros
@@ -1318,7 +1588,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     }
   }
   CUtensorMap mA, mB;
-  if (hw >= 16 && !L.im2col && !getenv("DRCB_NO_ROWS")) {
+  if (hw >= 16 && !getenv("DRCB_NO_ROWS")) {
     // row-tile kernel (hw 16/32); DRCB_ROWS=dx|halo overrides the variant
     static const char* mode_env = getenv("DRCB_ROWS");
     const bool dx = mode_env ? std::strcmp(mode_env, "dx") == 0 : rows_use_dx(L, KIND);
@@ -1364,7 +1634,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
   int box_w = hw, box_h = a.maps_per_tile == 1 ? a.rows_per_tile : hw, box_n = a.maps_per_tile;
   rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, box_w, box_h, box_n);
   if (rc) return rc;
-  rc = encode_w(&mB, L.d_wtc, KIND, int64_t(L.im2col ? 1 : 9) * L.cin_pad, L.cout_pad, a.bn);
+  rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
   if (rc) return rc;
   return launch_conv<KIND>(mA, mB, a, st);
 }
@@ -1382,7 +1652,7 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
   // buffer plan (elements per map): channels padded to the K granularity
   struct Spec { int c, hw; };
   const Spec specs[] = {
-      {64, 32},         // 0 x0: im2col input (k = tap * 7 + c)
+      {8, 32},          // 0 x0: compact input, 7 channels + 1 zero
       {P(k), 32},       // 1 e32
       {3 * k, 32},      // 2 c1 [up(2k) | s1(k)]
       {P(k), 16},       // 3 p1
@@ -1415,7 +1685,7 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
   if (x_nhwc) {
     B[0].p = const_cast<void*>(x_nhwc);
   } else {
-    int64_t tot = np * 1024 * (64 / Vec<T>::N);
+    int64_t tot = np * 1024 * (8 / Vec<T>::N);
     k_stack_to_nhwc<T><<<unsigned((tot + 255) / 256), 256, 0, st>>>(x, n, np, B[0].c, (T*)B[0].p);
     count_launch();
   }
@@ -1485,7 +1755,7 @@ int forward_tc_nhwc(NetImpl& net, const void* x_nhwc, float* y, int64_t n, int m
                                : tc::forward_kind<1>(net, nullptr, y, n, st, x_nhwc);
 }
 
-int tc_input_channels(int) { return 64; }  // im2col K values per pixel
+int tc_input_channels(int) { return 8; }  // compact NHWC input (7 + 1 zero channel)
 
 int forward_tc(NetImpl& net, const float* x, float* y, int64_t n, int mode, cudaStream_t st) {
   if (n <= 0) return 0;

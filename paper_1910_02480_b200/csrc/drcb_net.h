@@ -29,9 +29,9 @@ struct ConvLayer {
   float *d_ep_a = nullptr, *d_ep_b = nullptr;  // y = acc * a + b, then LeakyReLU
   int cin_pad = 0, cout_pad = 0;
   int tc_kind = -1;          // which operand format d_wtc holds
-  // enc1.conv1 on the tensor cores reads an im2col input (64 K values per
-  // pixel: k = tap * 7 + c, k = 63 zero) and runs as a 1-tap GEMM
-  bool im2col = false;
+  // enc1.conv1 on the tensor cores reads the compact 8-channel NHWC input and
+  // builds its im2col operand in SMEM (k_conv_in8): K value tap * 8 + c
+  bool in8 = false;
 };
 
 struct NetImpl {

@@ -470,8 +470,8 @@ constexpr double LUMA_R = 0.2126, LUMA_G = 0.7152, LUMA_B = 0.0722;  // hemimap.
 
 // One block (256 threads) per cache point: s_r = mean luminance + 1e-3,
 // s_d = max distance (or 1), fp32 NCHW stack [rad/s_r, n_local, d/s_d].
-// nhwc_kind: 0 = none, 1 = bf16, 2 = tf32-rounded fp32 im2col input of the
-// tensor-core network (cpad = 64 K values per texel), written here directly
+// nhwc_kind: 0 = none, 1 = bf16, 2 = tf32-rounded fp32 compact NHWC input of
+// the tensor-core network (cpad = 8: 7 channels + 1 zero), written here directly
 template <typename R>
 __global__ void __launch_bounds__(256) k_stack_normalize(const R* __restrict__ rad,
                                                          const R* __restrict__ dist,
@@ -513,46 +513,27 @@ __global__ void __launch_bounds__(256) k_stack_normalize(const R* __restrict__ r
   for (int w = 1; w < 8; ++w) mx = fmax(mx, dmax[w]);
   R sd = mx > R(0) ? mx : R(1);
   const R* np_ = nloc + p * MAP_TEXELS * 3;
-  __shared__ float sv[7][MAP_TEXELS];
   for (int t = threadIdx.x; t < MAP_TEXELS; t += blockDim.x) {
-    float v[7];
+    float v[8];
     for (int c = 0; c < 3; ++c) v[c] = float(rp[3 * t + c] / sr);
     for (int c = 0; c < 3; ++c) v[3 + c] = float(np_[3 * t + c]);
     v[6] = float(dp[t] / sd);
+    v[7] = 0.f;
     if (stacks)
       for (int c = 0; c < 7; ++c) out[c * MAP_TEXELS + t] = v[c];
-    if (nhwc_kind)
-      for (int c = 0; c < 7; ++c) sv[c][t] = v[c];
-  }
-  if (nhwc_kind) {
-    // im2col network input (cpad == 64 K values per texel): k = tap * 7 + c
-    // is channel c of the texel at (y + tap/3 - 1, x + tap%3 - 1), zero
-    // outside the map, k = 63 zero; (texel, 16-B piece) per thread so a warp
-    // writes 512 contiguous bytes
-    __syncthreads();
-    const int V = nhwc_kind == 1 ? 8 : 4, PP = cpad / V;
-    uint4* o = reinterpret_cast<uint4*>(static_cast<uint8_t*>(nhwc) +
-                                        size_t(p) * MAP_TEXELS * cpad * (nhwc_kind == 1 ? 2 : 4));
-    for (int i = threadIdx.x; i < MAP_TEXELS * PP; i += blockDim.x) {
-      const int t = i / PP, piece = i % PP, y = t >> 5, x = t & 31;
-      float f[8];
-      for (int j = 0; j < V; ++j) {
-        const int k = piece * V + j, tap = k / 7, c = k % 7;
-        const int yy = y + tap / 3 - 1, xx = x + tap % 3 - 1;
-        f[j] = (k < 63 && yy >= 0 && yy < 32 && xx >= 0 && xx < 32) ? sv[c][yy * 32 + xx] : 0.f;
+    if (nhwc_kind == 1) {
+      uint32_t w[4];
+      for (int j = 0; j < 4; ++j) {
+        __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+        w[j] = *reinterpret_cast<uint32_t*>(&b);
       }
-      if (nhwc_kind == 1) {
-        uint32_t w[4];
-        for (int j = 0; j < 4; ++j) {
-          __nv_bfloat162 b = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
-          w[j] = *reinterpret_cast<uint32_t*>(&b);
-        }
-        o[i] = make_uint4(w[0], w[1], w[2], w[3]);
-      } else {
-        uint32_t w[4];
-        for (int j = 0; j < 4; ++j) asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(w[j]) : "f"(f[j]));
-        o[i] = make_uint4(w[0], w[1], w[2], w[3]);
-      }
+      reinterpret_cast<uint4*>(nhwc)[p * MAP_TEXELS + t] = make_uint4(w[0], w[1], w[2], w[3]);
+    } else if (nhwc_kind == 2) {
+      uint32_t w[8];
+      for (int j = 0; j < 8; ++j) asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(w[j]) : "f"(v[j]));
+      uint4* o = reinterpret_cast<uint4*>(nhwc) + 2 * (p * MAP_TEXELS + t);
+      o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      o[1] = make_uint4(w[4], w[5], w[6], w[7]);
     }
   }
   if (threadIdx.x == 0) {
