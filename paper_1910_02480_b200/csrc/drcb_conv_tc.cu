@@ -593,6 +593,31 @@ __device__ __forceinline__ void epilogue_stage(const ConvArgs& p, uint32_t tbase
     }
   }
 }
+// elementwise max of four 16-B vectors of stored values (bf16x8 / fp32x4)
+template <int KIND>
+__device__ __forceinline__ uint4 max4(uint4 a, uint4 b, uint4 c, uint4 d) {
+  uint4 r;
+  uint32_t* ra = reinterpret_cast<uint32_t*>(&a);
+  uint32_t* rb = reinterpret_cast<uint32_t*>(&b);
+  uint32_t* rc = reinterpret_cast<uint32_t*>(&c);
+  uint32_t* rd = reinterpret_cast<uint32_t*>(&d);
+  uint32_t* rr = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if constexpr (KIND == 0) {
+      __nv_bfloat162 x = __hmax2(__hmax2(*reinterpret_cast<__nv_bfloat162*>(&ra[i]),
+                                         *reinterpret_cast<__nv_bfloat162*>(&rb[i])),
+                                 __hmax2(*reinterpret_cast<__nv_bfloat162*>(&rc[i]),
+                                         *reinterpret_cast<__nv_bfloat162*>(&rd[i])));
+      rr[i] = *reinterpret_cast<uint32_t*>(&x);
+    } else {
+      rr[i] = __float_as_uint(fmaxf(fmaxf(__uint_as_float(ra[i]), __uint_as_float(rb[i])),
+                                    fmaxf(__uint_as_float(rc[i]), __uint_as_float(rd[i]))));
+    }
+  }
+  return r;
+}
+
 constexpr int RT_EPI_WARPS = 8;
 constexpr int RT_THREADS = 64 + 32 * RT_EPI_WARPS;
 __device__ __forceinline__ void epi_bar_rt() {
@@ -604,6 +629,7 @@ struct RowArgs {
   int row_bytes;  // W * 128: one dy shift
   int sa, sb;     // A / B ring depths
   int o_bytes;    // one output staging tile (BM * BN * elem); 0 = direct stores (head)
+  int p_bytes;    // fused 2x2 max-pool staging tile (BM/4 * BN * elem); 0 = no pool
 };
 
 // Row-tile implicit GEMM for hw in {16, 32}: an M tile is BM/W whole image
@@ -625,8 +651,8 @@ struct RowArgs {
 template <int KIND, int BN, bool RES, bool DX>
 __global__ void __launch_bounds__(RT_THREADS, 1)
     k_conv_rows(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                const __grid_constant__ CUtensorMap mapO, const __grid_constant__ ConvArgs p,
-                const __grid_constant__ RowArgs h) {
+                const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapP,
+                const __grid_constant__ ConvArgs p, const __grid_constant__ RowArgs h) {
   constexpr int B_TILE = BN * ROW_BYTES;
   constexpr int B3 = 3 * B_TILE;                       // one B stage: three weight tiles
   constexpr int ELEM = KIND == 0 ? 2 : 4;
@@ -645,7 +671,8 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   uint8_t* aring = smem + (RES ? n_wtiles * B_TILE : 0);
   uint8_t* bring = aring + h.sa * h.a_bytes;
   uint8_t* ostage = bring + (RES ? 0 : h.sb * B3);  // 2 x o_bytes, 1024-aligned
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ostage + 2 * h.o_bytes);
+  uint8_t* pstage = ostage + 2 * h.o_bytes;          // 2 x p_bytes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pstage + 2 * h.p_bytes);
   uint64_t* afull = bars;
   uint64_t* aempty = bars + 8;
   uint64_t* bfull = bars + 16;
@@ -827,13 +854,43 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
         if (lane == 0) mbar_arrive(&tempty[acc]);
         fence_proxy_async();
         epi_bar_rt();
+        const int n0 = mt / p.tiles_per_map;
+        const int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
         if (threadIdx.x == 64) {
-          const int n0 = mt / p.tiles_per_map;
-          const int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
           for (int sb2 = 0; sb2 < BN / CEL; ++sb2)
             tma_store_4d(&mapO, ot + sb2 * BM * ROW_BYTES, p.cout_off + nt * BN + sb2 * CEL, 0, y0, n0);
-          bulk_commit();
         }
+        if (h.p_bytes) {
+          // fused 2x2 max-pool (cnn.py:152-156) of the staged, already rounded
+          // tile: BM/4 pooled pixels x BN channels, same swizzled layout
+          uint8_t* pt = pstage + obuf * h.p_bytes;
+          const int hw = p.hw, ho = hw >> 1;
+          constexpr int PPR = ROW_BYTES / 16;  // 16-B pieces per sub-tile row
+          for (int e = threadIdx.x - 64; e < (BM / 4) * (BN * ELEM / 16); e += 32 * RT_EPI_WARPS) {
+            const int pr = e / (BN * ELEM / 16), pc = e % (BN * ELEM / 16);
+            const int sub = pc / PPR, jj = pc % PPR;
+            const int py = pr / ho, px = pr % ho;
+            const int r00 = (2 * py) * hw + 2 * px;
+            const uint32_t base = smem_u32(ot + sub * BM * ROW_BYTES);
+            uint4 v[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              const int rr = r00 + (w >> 1) * hw + (w & 1);
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(v[w].x), "=r"(v[w].y), "=r"(v[w].z), "=r"(v[w].w)
+                           : "r"(base + rr * ROW_BYTES + ((jj ^ (rr & 7)) << 4)));
+            }
+            uint4 m4 = max4<KIND>(v[0], v[1], v[2], v[3]);
+            sts128(smem_u32(pt + sub * (BM / 4) * ROW_BYTES) + pr * ROW_BYTES + ((jj ^ (pr & 7)) << 4),
+                   m4.x, m4.y, m4.z, m4.w);
+          }
+          fence_proxy_async();
+          epi_bar_rt();
+          if (threadIdx.x == 64)
+            for (int sb2 = 0; sb2 < BN / CEL; ++sb2)
+              tma_store_4d(&mapP, pt + sb2 * (BM / 4) * ROW_BYTES, nt * BN + sb2 * CEL, 0, y0 >> 1, n0);
+        }
+        if (threadIdx.x == 64) bulk_commit();
         obuf ^= 1;
       } else {
         epilogue_tile<KIND, BN, DX>(p, tbase, m, nt, nullptr, 16 * grp, CSTEP);
@@ -1426,7 +1483,8 @@ int launch_bn(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, c
 
 template <int KIND, int BN, bool RES, bool DX>
 int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
-                   const ConvArgs& a, const RowArgs& h, size_t smem, cudaStream_t st) {
+                   const CUtensorMap& mP, const ConvArgs& a, const RowArgs& h, size_t smem,
+                   cudaStream_t st) {
   auto kern = k_conv_rows<KIND, BN, RES, DX>;
   static bool attr = false;
   if (!attr) {
@@ -1437,19 +1495,20 @@ int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorM
   if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   int tiles = a.num_m_tiles * a.num_n_tiles;
   int grid = tiles < nsm ? tiles : nsm;
-  kern<<<grid, RT_THREADS, smem, st>>>(mA, mB, mO, a, h);
+  kern<<<grid, RT_THREADS, smem, st>>>(mA, mB, mO, mP, a, h);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_rows");
 }
 
 template <int KIND, bool DX>
-int launch_rows(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO, const ConvArgs& a,
-                const RowArgs& h, bool res, size_t smem, cudaStream_t st) {
-#define ROWS_CASE(BNV)                                                              \
-  case BNV:                                                                         \
-    return res ? launch_rows_bn<KIND, BNV, true, DX>(mA, mB, mO, a, h, smem, st)    \
-               : launch_rows_bn<KIND, BNV, false, DX>(mA, mB, mO, a, h, smem, st);
+int launch_rows(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
+                const CUtensorMap& mP, const ConvArgs& a, const RowArgs& h, bool res, size_t smem,
+                cudaStream_t st) {
+#define ROWS_CASE(BNV)                                                                  \
+  case BNV:                                                                             \
+    return res ? launch_rows_bn<KIND, BNV, true, DX>(mA, mB, mO, mP, a, h, smem, st)    \
+               : launch_rows_bn<KIND, BNV, false, DX>(mA, mB, mO, mP, a, h, smem, st);
   switch (a.bn) {
     ROWS_CASE(16)
     ROWS_CASE(32)
@@ -1543,7 +1602,8 @@ int run_in8(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cout_
 
 template <int KIND>
 int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cout_off,
-              int64_t nmaps, cudaStream_t st, float* pred = nullptr, const Buf* up = nullptr) {
+              int64_t nmaps, cudaStream_t st, float* pred = nullptr, const Buf* up = nullptr,
+              const Buf* pool = nullptr) {
   int rc = prepare_layer(net, L, KIND);
   if (rc) return rc;
   if (L.in8) return run_in8<KIND>(net, L, in, out, cout_off, nmaps, st);
@@ -1601,7 +1661,8 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     const int b_tile = a.bn * ROW_BYTES;
     const int w_bytes = 9 * a.cblocks * b_tile;
     rz.o_bytes = pred ? 0 : BM * a.bn * (KIND == 0 ? 2 : 4);
-    const int budget = 200 * 1024 - 2 * rz.o_bytes;
+    rz.p_bytes = (pool && rz.o_bytes) ? rz.o_bytes / 4 : 0;
+    const int budget = 216 * 1024 - 2 * rz.o_bytes - 2 * rz.p_bytes;  // of 227 KB
     const bool res = a.num_n_tiles == 1 && w_bytes + 3 * rz.a_bytes <= budget;
     if (res) {
       rz.sb = 1;
@@ -1618,15 +1679,22 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       if (rc) return rc;
       rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
       if (rc) return rc;
-      CUtensorMap mO;
+      CUtensorMap mO, mP;
       if (rz.o_bytes) {
         rc = encode_act(&mO, out.p, KIND, out.c, hw, nmaps, hw, a.rows_per_tile, 1);
         if (rc) return rc;
       }
+      if (rz.p_bytes) {
+        rc = encode_act(&mP, pool->p, KIND, pool->c, hw / 2, nmaps, hw / 2, a.rows_per_tile / 2, 1);
+        if (rc) return rc;
+      } else {
+        mP = mO;
+      }
       size_t smem = 1024 + size_t(res ? w_bytes : 0) + size_t(rz.sa) * rz.a_bytes +
-                    size_t(res ? 0 : rz.sb * 3 * b_tile) + 2 * size_t(rz.o_bytes) + 512;
-      return dx ? launch_rows<KIND, true>(mA, mB, mO, a, rz, res, smem, st)
-                : launch_rows<KIND, false>(mA, mB, mO, a, rz, res, smem, st);
+                    size_t(res ? 0 : rz.sb * 3 * b_tile) + 2 * size_t(rz.o_bytes) +
+                    2 * size_t(rz.p_bytes) + 512;
+      return dx ? launch_rows<KIND, true>(mA, mB, mO, mP, a, rz, res, smem, st)
+                : launch_rows<KIND, false>(mA, mB, mO, mP, a, rz, res, smem, st);
     }
     a.bn = L.cout_pad >= 256 ? 256 : L.cout_pad;
     a.num_n_tiles = L.cout_pad / a.bn;
@@ -1636,7 +1704,12 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
   if (rc) return rc;
   rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
   if (rc) return rc;
-  return launch_conv<KIND>(mA, mB, a, st);
+  rc = launch_conv<KIND>(mA, mB, a, st);
+  if (rc || !pool) return rc;
+  // this path has no fused pool: run the separate pass
+  using T = typename std::conditional<KIND == 0, __nv_bfloat16, float>::type;
+  return pool_dispatch<T>(static_cast<const T*>(out.p), out.c, cout_off, L.cout_pad, hw / 2,
+                          static_cast<T*>(pool->p), nmaps, st);
 }
 
 template <int KIND>
@@ -1697,11 +1770,15 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
   };
   // encoder
   rc |= run_layer<KIND>(net, Ls[0], B[0], B[1], 0, np, st);
-  rc |= run_layer<KIND>(net, Ls[1], B[1], B[2], 2 * k, np, st);   // s1 -> c1[2k:3k]
-  pool(B[2], 2 * k, k, B[3]);
+  // the 32x32 / 16x16 skip convs also write their 2x2 max-pool (fused)
+  const bool fpool = getenv("DRCB_NO_FUSED_POOL") == nullptr;
+  rc |= run_layer<KIND>(net, Ls[1], B[1], B[2], 2 * k, np, st, nullptr, nullptr,
+                        fpool ? &B[3] : nullptr);                   // s1 -> c1[2k:3k]
+  if (!fpool) pool(B[2], 2 * k, k, B[3]);
   rc |= run_layer<KIND>(net, Ls[2], B[3], B[4], 0, np, st);
-  rc |= run_layer<KIND>(net, Ls[3], B[4], B[5], 4 * k, np, st);   // s2 -> c2[4k:6k]
-  pool(B[5], 4 * k, 2 * k, B[6]);
+  rc |= run_layer<KIND>(net, Ls[3], B[4], B[5], 4 * k, np, st, nullptr, nullptr,
+                        fpool ? &B[6] : nullptr);                   // s2 -> c2[4k:6k]
+  if (!fpool) pool(B[5], 4 * k, 2 * k, B[6]);
   rc |= run_layer<KIND>(net, Ls[4], B[6], B[7], 0, np, st);
   rc |= run_layer<KIND>(net, Ls[5], B[7], B[8], 8 * k, np, st);   // s3 -> c3[8k:12k]
   pool(B[8], 8 * k, 4 * k, B[9]);
