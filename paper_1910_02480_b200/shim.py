@@ -6,7 +6,7 @@
 rebinds the reference's hot-path surfaces to the B200 implementation:
 
   drc.cache.render_drc                      -> render.render_drc
-  drc.integrators.render (drc/direct modes) -> render.render
+  drc.integrators.render (drc/direct/pt)    -> render.render
   drc.cnn.forward                           -> cnn.forward
   drc_trainer.model.forward_reference       -> batched device forward
 
@@ -42,7 +42,7 @@ def install(net_mode="fp32", precision=64):
         return render.render_drc(scene, cfg, net, interrupt=interrupt, snapshots=snapshots)
 
     def render_any(scene, config, mode="pt", weights=None, interrupt=None):
-        if mode in ("drc", "direct"):
+        if mode in ("drc", "direct", "pt"):
             return render.render(scene, _with_b200_fields(config, net_mode, precision), mode,
                                  weights, interrupt)
         return _INSTALLED["drc.integrators.render"](scene, config, mode, weights, interrupt)
