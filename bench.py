@@ -169,6 +169,20 @@ def cfg_name():
     return _CFG_NAME[0]
 
 
+def network_traffic(n_maps):
+    """DRAM bytes (read + write) of one U-Net forward over n_maps, scaled from
+    the committed ncu capture (profiles/*_network_traffic.json, 4,096 maps);
+    None when no capture is committed."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                          "profiles", "*_network_traffic.json")))
+    if not files:
+        return None
+    d = json.load(open(files[-1]))
+    return int(d["dram_bytes_total"] * n_maps / d["maps"])
+
+
 def main():
     args = parse()
     _CFG_NAME[0] = args.config
@@ -334,7 +348,8 @@ def main():
         achieved = n_pts * flop_map / (avg["network"] * 1e-6) / 1e12
         peak = peaks.get("bf16_tflops", 1590.0)
         roof = {"bound": "tensor", "kernel": "U-Net forward (all conv layers)", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": network_traffic(n_pts),
                 "algorithmic": f"{flop_map/1e9:.5f} GFLOP/map x {n_pts} maps"}
     else:
         # traversal-bound stages: algorithmic bytes = scene bytes read once
