@@ -563,6 +563,12 @@ __device__ __forceinline__ void epilogue_stage(const ConvArgs& p, uint32_t tbase
   const int xpix = int(m & int64_t(p.hw - 1));  // hw is a power of two
   const int r = int(m & (BM - 1));
   const uint32_t ost_s = smem_u32(ost);
+  if constexpr (BN < CEL) {
+    // channels [BN, CEL) of the stored row are the next layer's K padding
+    if (cbeg == 0)
+#pragma unroll
+      for (int j = BN * ELEM / 16; j < 8; ++j) sts128(ost_s + r * ROW_BYTES + ((j ^ (r & 7)) << 4), 0u, 0u, 0u, 0u);
+  }
   // unrolled so the next chunk's TMEM loads overlap this chunk's math
 #pragma unroll
   for (int i = 0; i < (BN + CSTEP - 1) / CSTEP; ++i) {
@@ -857,7 +863,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
         const int n0 = mt / p.tiles_per_map;
         const int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
         if (threadIdx.x == 64) {
-          for (int sb2 = 0; sb2 < BN / CEL; ++sb2)
+          for (int sb2 = 0; sb2 < (BN + CEL - 1) / CEL; ++sb2)
             tma_store_4d(&mapO, ot + sb2 * BM * ROW_BYTES, p.cout_off + nt * BN + sb2 * CEL, 0, y0, n0);
         }
         if (h.p_bytes) {
@@ -1417,7 +1423,13 @@ int prepare_layer(NetImpl& net, ConvLayer& L, int kind) {
   // channels get zero weights and zero epilogue vectors, so they hold exact
   // zeros (head.deconv1's k/2 outputs feed a K-padded input). The fused head
   // layer only needs the UMMA minimum N of 16.
-  const int coutp = (L.name == "head.deconv2") ? 16 : pad_c(L.cout, kind);
+  // A row-tile layer (hw >= 16) with fewer outputs than one 128-B row
+  // (bf16 head.deconv1: 32) computes N = cout rounded to 16 and its epilogue
+  // zero-fills the rest of the row, which the next layer's K padding reads.
+  const int cel = kind == 0 ? 64 : 32;
+  const int coutp = (L.name == "head.deconv2") ? 16
+                    : (L.hw >= 16 && L.cout < cel && L.name != "enc1.conv1") ? (L.cout + 15) / 16 * 16
+                                                    : pad_c(L.cout, kind);
   L.cin_pad = cinp;
   L.cout_pad = coutp;
   const int64_t ktot = L.in8 ? cinp : int64_t(9) * cinp;
@@ -1660,7 +1672,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     rz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
     const int b_tile = a.bn * ROW_BYTES;
     const int w_bytes = 9 * a.cblocks * b_tile;
-    rz.o_bytes = pred ? 0 : BM * a.bn * (KIND == 0 ? 2 : 4);
+    rz.o_bytes = pred ? 0 : BM * std::max(a.bn, ROW_BYTES / (KIND == 0 ? 2 : 4)) * (KIND == 0 ? 2 : 4);
     rz.p_bytes = (pool && rz.o_bytes) ? rz.o_bytes / 4 : 0;
     const int budget = 216 * 1024 - 2 * rz.o_bytes - 2 * rz.p_bytes;  // of 227 KB
     const bool res = a.num_n_tiles == 1 && w_bytes + 3 * rz.a_bytes <= budget;
@@ -1717,8 +1729,8 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
                  const void* x_nhwc = nullptr) {
   using T = typename std::conditional<KIND == 0, __nv_bfloat16, float>::type;
   const int k = net.k;
-  if (k % 32 != 0 || k / 4 > 16)
-    return fail(DRCB_ECONFIG, "tensor-core path supports k in {32, 64}");
+  if (k != 64)  // buffer plan: concat/skip slices are whole 64-channel rows only at k = 64
+    return fail(DRCB_ECONFIG, "tensor-core path supports k = 64 (use net_mode fp32 for other k)");
   auto& Ls = net.layers;
   const int64_t np = ((n + 7) / 8) * 8;  // 4x4 tiles hold 8 maps
   auto P = [&](int c) { return pad_c(c, KIND); };
