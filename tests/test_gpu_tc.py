@@ -94,3 +94,29 @@ def test_fused_upsample_epilogue_bit_identical(mode, monkeypatch):
     monkeypatch.setenv("DRCB_FUSED_UP", "1")
     fused = cnn.forward_batch(net, x, mode=mode)
     assert np.array_equal(plain, fused)
+
+
+@pytest.mark.parametrize("mode", ["bf16", "tf32"])
+def test_fused_pool_bit_identical(mode, monkeypatch):
+    # the encoder pools fused into the skip convs' epilogues must reproduce
+    # the separate pool pass exactly (max of the stored, rounded values)
+    rng = np.random.default_rng(8)
+    x = rng.uniform(0, 1, (9, 7, 32, 32)).astype(np.float32)
+    net = cnn.random_network(64, 2)
+    fused = cnn.forward_batch(net, x, mode=mode)
+    monkeypatch.setenv("DRCB_NO_FUSED_POOL", "1")
+    plain = cnn.forward_batch(net, x, mode=mode)
+    assert np.array_equal(plain, fused)
+
+
+@pytest.mark.parametrize("mode,bar", [("bf16", 5e-3), ("tf32", 1e-3)])
+def test_row_tile_kernels_agree_with_per_tap_kernel(mode, bar, monkeypatch):
+    # the 16x16 / 32x32 row-tile kernels (halo, dx-in-N) vs the plain per-tap
+    # implicit GEMM: same products, different fp32 summation order
+    rng = np.random.default_rng(9)
+    x = rng.uniform(0, 1, (9, 7, 32, 32)).astype(np.float32)
+    net = cnn.random_network(64, 2)
+    rows = cnn.forward_batch(net, x, mode=mode)
+    monkeypatch.setenv("DRCB_NO_ROWS", "1")
+    tap = cnn.forward_batch(net, x, mode=mode)
+    assert _rel(rows, tap) <= bar
