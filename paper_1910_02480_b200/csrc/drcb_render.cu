@@ -152,10 +152,21 @@ __global__ void __launch_bounds__(TPB) k_gbuffer_direct(DevScene S, DevCamera C,
 // ordered per-pixel reduction that sums samples in the reference's per-tile
 // chunks ((s0 + s1 + ...) per chunk, chunks accumulated from 0) and divides
 // by direct_spp (cache.py:399-413).
+// thread k of a frame -> pixel: 32 consecutive threads cover an 8x4 pixel
+// block (coherent primary and shadow rays per warp) when the frame tiles
+// evenly, row-major otherwise
+__device__ __forceinline__ int64_t pixel_of(const DevCamera& C, int64_t k) {
+  if ((C.W & 7) || (C.H & 3)) return k;
+  const int64_t b = k >> 5;
+  const int w = int(k & 31), bpr = C.W >> 3;
+  return (int64_t(b / bpr) * 4 + (w >> 3)) * C.W + int64_t(b % bpr) * 8 + (w & 7);
+}
+
 template <typename R>
 __global__ void __launch_bounds__(TPB) k_gbuffer(DevScene S, DevCamera C, DrcbGBuffer gb) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= int64_t(C.W) * C.H) return;
+  int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= int64_t(C.W) * C.H) return;
+  const int64_t i = pixel_of(C, k);
   int x = int(i % C.W), y = int(i / C.W);
   V3<R> dc = camera_dir<R>(C, R(x) + R(0.5), R(y) + R(0.5));
   store_chain(gb, i, primary_chain(S, ld3<R>(C.pos), dc));
@@ -169,14 +180,16 @@ __global__ void __launch_bounds__(TPB) k_direct_samples(DevScene S, DevCamera C,
   int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   int nf = 0;
   if (g < npx * spp) {
-    int64_t i = g % npx;  // sample-major: neighbouring threads trace neighbouring pixels
+    // sample-major: neighbouring threads trace neighbouring pixels (8x4 blocks)
+    const int64_t i = pixel_of(C, g % npx);
     int s = int(g / npx);
     int x = int(i % C.W), y = int(i / C.W);
     PathRng rng;
     rng.init(cfg.seed, uint64_t(i), uint64_t(s), cfg.sampler_kind, uint32_t(spp > 1 ? spp : 1));
     R jx = to_unit<R>(rng.sample(0)), jy = to_unit<R>(rng.sample(1));
     V3<R> d = camera_dir<R>(C, R(x) + jx, R(y) + jy);
-    st3(samples + 3 * g, direct_path(S, ld3<R>(C.pos), d, rng, cfg.include_background != 0, nf));
+    st3(samples + 3 * (int64_t(s) * npx + i),
+        direct_path(S, ld3<R>(C.pos), d, rng, cfg.include_background != 0, nf));
   }
   if (nonfinite) add_nonfinite(nonfinite, nf);
 }
