@@ -225,6 +225,23 @@ int drcb_trav_stats(unsigned long long *buf);
 /* number of kernels this library has launched so far (process-wide) */
 int64_t drcb_kernel_launches(void);
 
+/* ---- trainer input pipeline (trainer/src/drc_trainer/data.py:77-121) -- */
+/* numpy cos/sin of 2*pi*shift/32 for shift = 0, 8, 16, 24 (host-computed so
+ * the float64 normal re-expression matches _rotate_normals_xy bit for bit) */
+typedef struct DrcbAugmentTrig {
+  double cos_a[4], sin_a[4];
+} DrcbAugmentTrig;
+
+/* Gather n examples from a resident base set (x_base (N,7,32,32), y_base
+ * (N,3,32,32) fp32 device) by base[i] and apply variant[i] (NULL = 0):
+ * shift = 8*(v>>1) columns (np.roll by -shift), flip = v&1, normals
+ * re-expressed (transform_example, data.py:86-100); ablate bit 0 = normals,
+ * bit 1 = distance (ablate, data.py:106-117). augment() order is
+ * v = 2*shift_index + flip (data.py:103-104). */
+int drcb_augment_gather(const float *x_base, const float *y_base, const int64_t *base,
+                        const int32_t *variant, int64_t n, const DrcbAugmentTrig *trig,
+                        int32_t ablate, float *x_out, float *y_out, void *stream);
+
 /* ---- training step (trainer/src/drc_trainer/train.py:97-103) ---------- */
 /* MapAutoencoder in train mode (batch-statistics BN, momentum 0.1), L1 loss,
  * Adam(lr, betas, eps) with fp32 master weights, from DRCW bytes (host). */

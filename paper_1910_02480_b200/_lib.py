@@ -53,6 +53,10 @@ class RenderCfg(C.Structure):
     ]
 
 
+class AugmentTrig(C.Structure):
+    _fields_ = [("cos_a", C.c_double * 4), ("sin_a", C.c_double * 4)]
+
+
 class GBuffer(C.Structure):
     _fields_ = [
         ("found", vp), ("escaped", vp), ("position", vp), ("normal", vp),
@@ -99,6 +103,7 @@ _SIGS = [
     ("drcb_trainer_info", C.c_int, [vp, C.POINTER(C.c_int64)]),
     ("drcb_trainer_buffers", C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     ("drcb_trainer_step", C.c_int, [vp, vp, vp, C.c_int64, C.POINTER(C.c_double), C.c_int32, vp]),
+    ("drcb_augment_gather", C.c_int, [vp, vp, vp, vp, C.c_int64, vp, C.c_int32, vp, vp, vp]),
     ("drcb_trainer_apply", C.c_int, [vp, C.c_float, vp]),
     ("drcb_trainer_export", C.c_int64, [vp, vp, C.c_int64]),
     ("drcb_trainer_set_comm", C.c_int, [vp, vp, C.c_int32]),

@@ -727,7 +727,7 @@ extern "C" int drcb_trainer_apply(DrcbTrainer* T, float grad_scale, void* stream
 extern "C" int drcb_trainer_step(DrcbTrainer* T, const float* x, const float* y, int64_t n,
                                  double* loss_host, int32_t apply_adam, void* stream) {
   if (!T || !x || !y) return fail(DRCB_ECONTRACT, "drcb_trainer_step: null argument");
-  if (n < 2) return fail(DRCB_ECONFIG, "batch norm training needs n >= 2 examples");
+  if (n < 1) return fail(DRCB_ECONFIG, "training step needs n >= 1 examples");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   keep_pool_memory();
   const int k = T->k;

@@ -9,6 +9,9 @@ rebinds the reference's hot-path surfaces to the B200 implementation:
   drc.integrators.render (drc/direct/pt)    -> render.render
   drc.cnn.forward                           -> cnn.forward
   drc_trainer.model.forward_reference       -> batched device forward
+  drc_trainer.data.{read_drcd, augment, transform_example, ablate,
+                    split_by_scene}         -> data (device augmentation)
+  drc_trainer.train.train                   -> trainer.train (device loop)
 
 The reference objects (Scene, RenderConfig, Network) are accepted as-is
 (duck typing). Nothing falls back to the CPU: if libdrcb.so or the GPU is
@@ -80,6 +83,30 @@ def install(net_mode="fp32", precision=64):
     if "drc_trainer.model.forward_reference" not in _INSTALLED:
         _INSTALLED["drc_trainer.model.forward_reference"] = model.forward_reference
     model.forward_reference = forward_reference
+
+    # the trainer's input pipeline and loop (data.py, train.py:65-116)
+    from . import data as bdata
+    from . import trainer as btrainer
+
+    def train(examples, config, weights_out, curves_out=None, log=print):
+        trainer, history = btrainer.train(examples, config, weights_out, curves_out, log)
+        m = model.import_drcw(trainer.export())
+        m.eval()
+        return m, history
+
+    tmods = {
+        "drc_trainer.data": {"read_drcd": bdata.read_drcd, "augment": bdata.augment,
+                             "transform_example": bdata.transform_example,
+                             "ablate": bdata.ablate, "split_by_scene": bdata.split_by_scene},
+        "drc_trainer.train": {"train": train},
+    }
+    for modname, attrs in tmods.items():
+        mod = importlib.import_module(modname)
+        for name, fn in attrs.items():
+            key = f"{modname}.{name}"
+            if key not in _INSTALLED:
+                _INSTALLED[key] = getattr(mod, name)
+            setattr(mod, name, fn)
 
 
 def uninstall():

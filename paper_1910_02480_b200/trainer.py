@@ -159,3 +159,132 @@ class TrainConfig:
 def train_step(trainer, x, y):
     """train.py:97-103 on the device; returns the loss."""
     return trainer.step(x, y, apply=True)
+
+
+def torch_default_network(k=64, slope=0.01):
+    """The initial weights of a freshly constructed MapAutoencoder
+    (model.py:20-88) under the current torch RNG state: the same torch modules
+    (default Kaiming-uniform conv init, unit/zero batch norm) built in the same
+    order, exported to a DRCW Network. Weight initialisation only; nothing here
+    runs on the training path."""
+    import torch
+    from torch import nn
+
+    from .cnn import Network
+
+    tensors = {}
+
+    def conv(name, cin, cout, transposed, ks=3):
+        if transposed:
+            m = nn.ConvTranspose2d(cin, cout, ks, stride=1, padding=1)
+        else:
+            m = nn.Conv2d(cin, cout, ks, padding=1 if ks == 3 else 0)
+        tensors[f"{name}.weight"] = m.weight.detach().numpy().astype(np.float32)
+        tensors[f"{name}.bias"] = m.bias.detach().numpy().astype(np.float32)
+
+    def bn(name, c):
+        m = nn.BatchNorm2d(c, eps=1e-5)
+        tensors[f"{name}.gamma"] = m.weight.detach().numpy().astype(np.float32)
+        tensors[f"{name}.beta"] = m.bias.detach().numpy().astype(np.float32)
+        tensors[f"{name}.running_mean"] = m.running_mean.numpy().astype(np.float32)
+        tensors[f"{name}.running_var"] = m.running_var.numpy().astype(np.float32)
+
+    with torch.no_grad():
+        for name, cin, cout, tr in (("enc1", 7, k, False), ("enc2", k, 2 * k, False),
+                                    ("enc3", 2 * k, 4 * k, False), ("bott", 4 * k, 8 * k, False),
+                                    ("dec3", 12 * k, 4 * k, True), ("dec2", 6 * k, 2 * k, True),
+                                    ("dec1", 3 * k, k, True)):
+            kind = "deconv" if tr else "conv"
+            conv(f"{name}.{kind}1", cin, cout, tr)
+            bn(f"{name}.bn1", cout)
+            conv(f"{name}.{kind}2", cout, cout, tr)
+            bn(f"{name}.bn2", cout)
+        conv("head.deconv1", k, k // 2, True)
+        bn("head.bn1", k // 2)
+        conv("head.deconv2", k // 2, k // 4, True)
+        bn("head.bn2", k // 4)
+        conv("head.conv_out", k // 4, 3, False, ks=1)
+    return Network(tensors=tensors, k=k, slope=float(np.float32(slope)))
+
+
+def evaluate(trainer, dev_examples, batch_size, ablation=()):
+    """_evaluate (train.py:56-64): eval-mode (running statistics) L1 over
+    batches, weighted by batch length."""
+    import torch
+
+    from .cnn import DeviceNet
+
+    net = DeviceNet(trainer.export())
+    total, count = 0.0, 0
+    for b0 in range(0, dev_examples.n, batch_size):
+        idx = list(range(b0, min(b0 + batch_size, dev_examples.n)))
+        x, y = dev_examples.gather(idx, None, ablation)
+        pred = net.forward_device(x, mode="fp32")
+        total += float(torch.nn.functional.l1_loss(pred, y)) * len(idx)
+        count += len(idx)
+    net.close()
+    return total / max(count, 1)
+
+
+def train(examples, config, weights_out=None, curves_out=None, log=print):
+    """drc_trainer.train.train (train.py:65-116) on the device: by-scene
+    split, 8 augmentation variants per training example gathered and
+    transformed per batch by the device pipeline (data.DeviceExamples), the
+    reference's shuffling (torch.randperm with the seeded loader generator),
+    one DeviceTrainer step per batch, validation once per epoch. Returns
+    (trainer, history) with history rows (step, split, loss)."""
+    import csv
+    import os
+
+    import torch
+
+    from . import data
+
+    if config.learning_rate <= 0:
+        raise ValueError("learning rate must be > 0")
+    if config.batch_size < 1 or config.epochs < 1:
+        raise ValueError("batch size and epochs must be >= 1")
+    if set(config.ablation) - {"normals", "distance"}:
+        raise ValueError("ablation mask must be within {normals, distance}")
+    torch.manual_seed(config.seed)
+    np.random.seed(config.seed)
+    train_ex, val_ex = data.split_by_scene(examples, config.val_fraction, config.seed)
+    if not val_ex:  # single-scene corpus: fall back to an example split
+        cut = max(1, len(examples) // 10)
+        train_ex, val_ex = examples[cut:], examples[:cut]
+    trainer = DeviceTrainer(torch_default_network(config.k, config.slope), lr=config.learning_rate)
+    dtrain, dval = data.DeviceExamples(train_ex), data.DeviceExamples(val_ex)
+    n_items = 8 * len(train_ex)
+    gen = torch.Generator().manual_seed(config.seed)
+    history = []
+    step = 0
+    val0 = evaluate(trainer, dval, config.batch_size, config.ablation)
+    history.append((step, "val", val0))
+    log(f"initial val L1 {val0:.5f} ({n_items} augmented train, {len(val_ex)} val examples)")
+    for epoch in range(config.epochs):
+        # the DataLoader's draws per epoch: the iterator's base seed, the
+        # RandomSampler permutation, and the sampler's trailing (empty-slice)
+        # randperm when it is exhausted (torch/utils/data/sampler.py)
+        torch.empty((), dtype=torch.int64).random_(generator=gen)
+        perm = torch.randperm(n_items, generator=gen).tolist()
+        torch.randperm(n_items, generator=gen)
+        for b0 in range(0, n_items, config.batch_size):
+            items = perm[b0:b0 + config.batch_size]
+            x, y = dtrain.gather([i // 8 for i in items], [i % 8 for i in items], config.ablation)
+            loss = trainer.step(x, y, apply=True)
+            step += 1
+            history.append((step, "train", loss))
+        val = evaluate(trainer, dval, config.batch_size, config.ablation)
+        history.append((step, "val", val))
+        log(f"epoch {epoch + 1}/{config.epochs}: val L1 {val:.5f}")
+    if curves_out:
+        with open(curves_out, "w", newline="") as f:
+            w = csv.writer(f)
+            w.writerow(["step", "split", "loss"])
+            w.writerows(history)
+    if weights_out:
+        tmp = f"{weights_out}.tmp"
+        with open(tmp, "wb") as f:
+            f.write(trainer.export())
+        os.replace(tmp, weights_out)
+    return trainer, history

@@ -204,7 +204,7 @@ def main():
     frame_fixture("frame_furnace.npz", env, 8, 1, dict(direct_spp=2, indirect_tasks=1, mis_samples=8))
 
 
-if __name__ == "__main__" and not ({"--train", "--pt"} & set(sys.argv)):
+if __name__ == "__main__" and not ({"--train", "--pt", "--data"} & set(sys.argv)):
     main()
 
 
@@ -272,3 +272,59 @@ def pt_dataset_fixture():
 
 if __name__ == "__main__" and "--pt" in sys.argv:
     pt_dataset_fixture()
+
+
+def data_fixture():
+    """The trainer's input pipeline and loop (trainer/src/drc_trainer/data.py,
+    train.py:65-116): augment/ablate variants, split_by_scene, DRCD bytes and a
+    short train() run (k = 8) with its initial/final weights and history."""
+    import torch
+
+    from drc.dataset import TrainingExample, write_dataset
+    from drc_trainer import data as rdata
+    from drc_trainer import train as rtrain
+    from drc_trainer.model import export_drcw
+
+    rng = np.random.default_rng(11)
+    scenes = ["alpha", "beta", "gamma", "delta", "eps"]
+    exs = []
+    for i in range(15):
+        x = rng.uniform(0, 1, (7, 32, 32)).astype(np.float32)
+        x[:3] *= 3.0
+        nv = rng.normal(size=(3, 32, 32))
+        nv /= np.linalg.norm(nv, axis=0, keepdims=True)
+        x[3:6] = nv.astype(np.float32)
+        x[3:5, 5, 7] = 0.0  # exact zeros in the normal pair
+        y = np.exp(rng.normal(-1.0, 1.0, (3, 32, 32))).astype(np.float32)
+        exs.append(TrainingExample(input=x, target=y, s_r=float(rng.uniform(0.1, 2)),
+                                   s_d=float(rng.uniform(0.5, 3)), scene_id=scenes[i % 5],
+                                   pixel=(i, 2 * i)))
+    raw = write_dataset(exs)
+    rex = rdata.read_drcd(raw)
+    aug = [v for e in rex[:2] for v in rdata.augment(e)]
+    abl_n = rdata.ablate(rex[0], ("normals",))
+    abl_nd = [rdata.transform_example(rdata.ablate(rex[1], ("normals", "distance")), s, f)
+              for s in (8, 24) for f in (False, True)]
+    splits = {}
+    for seed in (0, 1, 5):
+        tr, va = rdata.split_by_scene(rex, 0.2, seed)
+        splits[f"split{seed}_val"] = np.array([i for i, e in enumerate(rex) if any(e is v for v in va)])
+    cfg = rtrain.TrainConfig(learning_rate=1e-3, batch_size=8, epochs=2, k=8, seed=3,
+                             val_fraction=0.2, ablation=("distance",))
+    model, hist = rtrain.train(rex, cfg, None, log=lambda *a: None)
+    torch.manual_seed(cfg.seed)
+    from drc_trainer.model import MapAutoencoder
+    init = MapAutoencoder(k=8)
+    save("data.npz", drcd=np.frombuffer(raw, dtype=np.uint8),
+         aug_input=np.stack([e.input for e in aug]), aug_target=np.stack([e.target for e in aug]),
+         abl_n=abl_n.input, abl_nd_input=np.stack([e.input for e in abl_nd]),
+         **splits,
+         hist_step=np.array([h[0] for h in hist]),
+         hist_split=np.array([0 if h[1] == "train" else 1 for h in hist]),
+         hist_loss=np.array([h[2] for h in hist]),
+         init_weights=np.frombuffer(export_drcw(init), dtype=np.uint8),
+         final_weights=np.frombuffer(export_drcw(model), dtype=np.uint8))
+
+
+if __name__ == "__main__" and "--data" in sys.argv:
+    data_fixture()
