@@ -182,6 +182,23 @@ int drcb_render_drc(const DrcbScene *scene, const DrcbNet *net,
                     int32_t net_mode, void *image, int64_t *telemetry_host,
                     void *stream);
 
+/* The frame's entry pool (DrcState.entries, drc/cache.py:183-201): device
+ * buffers with room for n_points entries; the first telemetry[0] are valid,
+ * in the reference's append order. Real arrays use cfg->precision. */
+typedef struct DrcbEntries {
+  int32_t *px, *py;
+  void *position, *normal, *radiance, *throughput; /* (n,3) each */
+} DrcbEntries;
+
+/* drcb_render_drc that also copies the entry pool out (the `--cache-out`
+ * DRCC dump of cli.py:130-132 and DrcState.entries()). */
+int drcb_render_drc_entries(const DrcbScene *scene, const DrcbNet *net,
+                            const DrcbCamera *cam, const DrcbRenderCfg *cfg,
+                            const int32_t *px_host, const int32_t *py_host,
+                            const uint64_t *keys_host, int64_t n_points, int32_t r_final,
+                            int32_t net_mode, void *image, int64_t *telemetry_host,
+                            const DrcbEntries *entries, void *stream);
+
 /* render(mode="pt") (drc/integrators.py:678-722): spp = cfg->direct_spp
  * jittered paths per pixel (max_path_depth, rr_start), image (H*W,3) Real. */
 int drcb_render_pt(const DrcbScene *scene, const DrcbCamera *cam, const DrcbRenderCfg *cfg,

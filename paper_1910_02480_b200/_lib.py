@@ -53,6 +53,11 @@ class RenderCfg(C.Structure):
     ]
 
 
+class Entries(C.Structure):
+    _fields_ = [("px", C.c_void_p), ("py", C.c_void_p), ("position", C.c_void_p),
+                ("normal", C.c_void_p), ("radiance", C.c_void_p), ("throughput", C.c_void_p)]
+
+
 class AugmentTrig(C.Structure):
     _fields_ = [("cos_a", C.c_double * 4), ("sin_a", C.c_double * 4)]
 
@@ -103,6 +108,9 @@ _SIGS = [
     ("drcb_trainer_info", C.c_int, [vp, C.POINTER(C.c_int64)]),
     ("drcb_trainer_buffers", C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     ("drcb_trainer_step", C.c_int, [vp, vp, vp, C.c_int64, C.POINTER(C.c_double), C.c_int32, vp]),
+    ("drcb_render_drc_entries", C.c_int, [vp, vp, C.POINTER(Camera), C.POINTER(RenderCfg), vp, vp,
+                                          vp, C.c_int64, C.c_int32, C.c_int32, vp, vp,
+                                          C.POINTER(Entries), vp]),
     ("drcb_augment_gather", C.c_int, [vp, vp, vp, vp, C.c_int64, vp, C.c_int32, vp, vp, vp]),
     ("drcb_trainer_apply", C.c_int, [vp, C.c_float, vp]),
     ("drcb_trainer_export", C.c_int64, [vp, vp, C.c_int64]),

@@ -84,7 +84,8 @@ __global__ void k_gather_points(DrcbGBuffer gb, int W, const int32_t* px, const 
 template <typename R>
 __global__ void k_scatter_entries(const uint8_t* live, const int* rank, int64_t n,
                                   const int32_t* px, const int32_t* py, const R* nrm, const R* L,
-                                  int32_t* epx, int32_t* epy, R* en, R* erad) {
+                                  int32_t* epx, int32_t* epy, R* en, R* erad, const R* pos,
+                                  const R* gthr, int W, DrcbEntries dump) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n || !live[i]) return;
   int j = rank[i];
@@ -93,6 +94,17 @@ __global__ void k_scatter_entries(const uint8_t* live, const int* rank, int64_t 
   for (int k = 0; k < 3; ++k) {
     en[3 * j + k] = nrm[3 * i + k];
     erad[3 * j + k] = L[3 * i + k];
+  }
+  if (dump.px) {  // entry pool copy-out (DrcState.entries, cache.py:196-201)
+    const int64_t pix = int64_t(py[i]) * W + px[i];
+    dump.px[j] = px[i];
+    dump.py[j] = py[i];
+    for (int k = 0; k < 3; ++k) {
+      static_cast<R*>(dump.position)[3 * j + k] = pos[3 * i + k];
+      static_cast<R*>(dump.normal)[3 * j + k] = nrm[3 * i + k];
+      static_cast<R*>(dump.radiance)[3 * j + k] = L[3 * i + k];
+      static_cast<R*>(dump.throughput)[3 * j + k] = gthr[3 * pix + k];
+    }
   }
 }
 
@@ -132,7 +144,7 @@ template <typename R>
 int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
                  const DrcbRenderCfg* cfg, const int32_t* px_h, const int32_t* py_h,
                  const uint64_t* keys_h, int64_t np_, int r_final, int net_mode, R* image,
-                 int64_t* tel, cudaStream_t st) {
+                 int64_t* tel, cudaStream_t st, const DrcbEntries* dump = nullptr) {
   const DevScene& S = scene->dev;
   keep_pool_memory();
   DevCamera C = make_camera(*cam);
@@ -237,7 +249,10 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
     DRCB_CUDA(cudaMallocAsync(&tmp, tmpb, st));
     cub::DeviceScan::ExclusiveSum(tmp, tmpb, flags, rank, int(np_), st);
     DRCB_CUDA(cudaFreeAsync(tmp, st));
-    k_scatter_entries<R><<<nb, 128, 0, st>>>(live, rank, np_, px, py, nrm, Le, epx, epy, en, erad);
+    DrcbEntries dz{};
+    if (dump) dz = *dump;
+    k_scatter_entries<R><<<nb, 128, 0, st>>>(live, rank, np_, px, py, nrm, Le, epx, epy, en, erad,
+                                             pos, static_cast<const R*>(gb.throughput), W, dz);
     k_entry_count<<<1, 1, 0, st>>>(rank, live, np_, d_m);
     count_launch(5);  // u8_to_int, scan (2), scatter, entry_count
     E.rec(4, st);
@@ -427,6 +442,35 @@ extern "C" int drcb_render_drc(const DrcbScene* scene, const DrcbNet* net, const
                                 r_final, net_mode, (double*)image, telemetry_host, S_(stream));
   return render_frame<float>(scene, mnet, cam, cfg, px_host, py_host, keys_host, n_points, r_final,
                              net_mode, (float*)image, telemetry_host, S_(stream));
+}
+
+extern "C" int drcb_render_drc_entries(const DrcbScene* scene, const DrcbNet* net,
+                                       const DrcbCamera* cam, const DrcbRenderCfg* cfg,
+                                       const int32_t* px_host, const int32_t* py_host,
+                                       const uint64_t* keys_host, int64_t n_points,
+                                       int32_t r_final, int32_t net_mode, void* image,
+                                       int64_t* telemetry_host, const DrcbEntries* entries,
+                                       void* stream) {
+  NEED(entries);
+  if (n_points > 0 && (!entries->px || !entries->py || !entries->position || !entries->normal ||
+                       !entries->radiance || !entries->throughput))
+    return fail(DRCB_ECONTRACT, "drcb_render_drc_entries: null entry buffer");
+  NEED(scene);
+  NEED(cam);
+  NEED(image);
+  if (check_cfg(cfg)) return DRCB_ECONFIG;
+  if (n_points > 0 && (!net || !px_host || !py_host || !keys_host))
+    return fail(DRCB_ECONTRACT, "drcb_render_drc_entries: points given without network/arrays");
+  for (int64_t i = 0; i < n_points; ++i)
+    if (px_host[i] < 0 || px_host[i] >= cam->width || py_host[i] < 0 || py_host[i] >= cam->height)
+      return fail(DRCB_ECONTRACT, "cache point outside the image");
+  DrcbNet* mnet = const_cast<DrcbNet*>(net);
+  if (cfg->precision == 64)
+    return render_frame<double>(scene, mnet, cam, cfg, px_host, py_host, keys_host, n_points,
+                                r_final, net_mode, (double*)image, telemetry_host, S_(stream),
+                                entries);
+  return render_frame<float>(scene, mnet, cam, cfg, px_host, py_host, keys_host, n_points, r_final,
+                             net_mode, (float*)image, telemetry_host, S_(stream), entries);
 }
 
 extern "C" int drcb_render_pt(const DrcbScene* scene, const DrcbCamera* cam,

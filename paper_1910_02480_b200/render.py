@@ -15,6 +15,8 @@ pixel runs in CUDA; there is no CPU fallback.
 
 from __future__ import annotations
 
+import dataclasses
+
 import ctypes as C
 import os
 import time
@@ -24,7 +26,7 @@ import numpy as np
 
 from . import _lib
 from .cnn import MODES, device_net
-from .errors import ConfigError, ContractError
+from .errors import ConfigError, ContractError, FormatError
 from .scene import camera_struct, device_scene
 
 T_EPS = 1e-4
@@ -200,13 +202,78 @@ def plan_points(size, config):
 # ---------------------------------------------------------------------------
 # frame driver
 
-class FrameState:
-    """Telemetry view of a finished frame (the reference returns its DrcState;
-    entries here stay on the device and only their count is reported)."""
+@dataclasses.dataclass(frozen=True)
+class CacheEntry:
+    """drc.cache.CacheEntry (cache.py:50-55)."""
 
-    def __init__(self, entries, points):
+    pixel: tuple
+    position: np.ndarray
+    normal: np.ndarray
+    indirect_radiance: np.ndarray
+    specular_throughput: np.ndarray
+
+
+class FrameState:
+    """Telemetry view of a finished frame (the reference returns its DrcState).
+    The entry pool is copied out only when the frame was rendered with
+    entries=True (render_drc does); otherwise only its size is known."""
+
+    def __init__(self, entries, points, pool=None):
         self.entry_count = entries
         self.planned_points = points
+        self._pool = pool
+
+    def entries(self):
+        """DrcState.entries (cache.py:196-201), in append (task) order."""
+        if self._pool is None:
+            raise ContractError("entry pool not collected (render with entries=True)")
+        px, py, pos, nrm, rad, thr = self._pool
+        return [CacheEntry(pixel=(int(px[i]), int(py[i])), position=pos[i], normal=nrm[i],
+                           indirect_radiance=rad[i], specular_throughput=thr[i])
+                for i in range(self.entry_count)]
+
+
+DRCC_MAGIC = b"DRCC"
+DRCC_VERSION = 1
+
+
+def write_cache_dump(entries, path):
+    """Little-endian entry records: pixel, position, normal, radiance
+    (cache.py:476-485)."""
+    import struct
+
+    with open(path, "wb") as f:
+        f.write(DRCC_MAGIC)
+        f.write(struct.pack("<II", DRCC_VERSION, len(entries)))
+        for e in entries:
+            f.write(struct.pack("<II", int(e.pixel[0]), int(e.pixel[1])))
+            f.write(np.asarray(e.position, dtype="<f4").tobytes())
+            f.write(np.asarray(e.normal, dtype="<f4").tobytes())
+            f.write(np.asarray(e.indirect_radiance, dtype="<f4").tobytes())
+
+
+def read_cache_dump(path):
+    """cache.py:488-507 (FormatError with byte offsets)."""
+    import struct
+
+    with open(path, "rb") as f:
+        raw = f.read()
+    if raw[:4] != DRCC_MAGIC:
+        raise FormatError("bad magic, not a DRCC dump", offset=0)
+    version, count = struct.unpack("<II", raw[4:12])
+    if version != DRCC_VERSION:
+        raise FormatError(f"unsupported DRCC version {version}", offset=4)
+    rec = 8 + 9 * 4
+    if len(raw) != 12 + count * rec:
+        raise FormatError("truncated cache dump", offset=len(raw))
+    out = []
+    for i in range(count):
+        o = 12 + i * rec
+        x, y = struct.unpack("<II", raw[o:o + 8])
+        vals = np.frombuffer(raw[o + 8:o + rec], dtype="<f4").astype(np.float64)
+        out.append(CacheEntry(pixel=(x, y), position=vals[0:3], normal=vals[3:6],
+                              indirect_radiance=vals[6:9], specular_throughput=np.ones(3)))
+    return out
 
 
 def _torch():
@@ -218,7 +285,7 @@ def _torch():
 
 
 def render_drc_device(scene, config, net, camera=None, out=None, precision=None, plan=None,
-                      telemetry=True):
+                      telemetry=True, entries=False):
     """One DRC frame, result left on the device: (image (H,W,3) CUDA tensor,
     telemetry dict). `camera` overrides scene.camera (multi-frame benches);
     `plan` reuses a plan_points() result; telemetry=False enqueues the frame
@@ -235,13 +302,23 @@ def render_drc_device(scene, config, net, camera=None, out=None, precision=None,
     dn = device_net(net) if len(px) else None
     if out is None:
         out = torch.empty((h, w, 3), dtype=dtype, device="cuda")
-    tel = (C.c_int64 * 8)() if telemetry else None
+    tel = (C.c_int64 * 8)() if (telemetry or entries) else None
     t0 = time.time()
-    _lib.call("drcb_render_drc", ds.handle, dn.handle if dn else None,
-              C.byref(camera_struct(cam)), C.byref(cfg),
-              px.ctypes.data_as(C.c_void_p), py.ctypes.data_as(C.c_void_p),
-              keys.ctypes.data_as(C.c_void_p), len(px), int(r_final or 1), MODES[net_mode],
-              _lib.ptr(out), tel, _lib.stream_ptr())
+    args = (ds.handle, dn.handle if dn else None, C.byref(camera_struct(cam)), C.byref(cfg),
+            px.ctypes.data_as(C.c_void_p), py.ctypes.data_as(C.c_void_p),
+            keys.ctypes.data_as(C.c_void_p), len(px), int(r_final or 1), MODES[net_mode],
+            _lib.ptr(out), tel)
+    pool = None
+    if entries:
+        n = max(len(px), 1)
+        bufs = [torch.zeros(n, dtype=torch.int32, device="cuda") for _ in range(2)] + \
+               [torch.zeros((n, 3), dtype=dtype, device="cuda") for _ in range(4)]
+        ent = _lib.Entries(*[C.c_void_p(b.data_ptr()) for b in bufs])
+        _lib.call("drcb_render_drc_entries", *args, C.byref(ent), _lib.stream_ptr())
+        m = int(tel[0])
+        pool = [b[:m].cpu().numpy().astype(np.float64 if b.dim() == 2 else np.int64) for b in bufs]
+    else:
+        _lib.call("drcb_render_drc", *args, _lib.stream_ptr())
     if tel is None:
         return out, None
     telemetry = {
@@ -254,7 +331,7 @@ def render_drc_device(scene, config, net, camera=None, out=None, precision=None,
         "stage_us": {"gbuffer_direct": int(tel[4]), "maps": int(tel[5]), "network": int(tel[6]),
                      "shade_interp": int(tel[7])},
     }
-    telemetry["state"] = FrameState(int(tel[0]), int(tel[3]))
+    telemetry["state"] = FrameState(int(tel[0]), int(tel[3]), pool)
     return out, telemetry
 
 
@@ -267,7 +344,7 @@ def render_drc(scene, config, net, interrupt=None, snapshots=None):
     submission, so there is no mid-frame pass boundary to stop at."""
     if interrupt is not None and interrupt():
         config = _replace(config, indirect_tasks=1, passes=None)
-    img, tel = render_drc_device(scene, config, net)
+    img, tel = render_drc_device(scene, config, net, entries=True)
     image = img.double().cpu().numpy()
     if snapshots:
         snaps = {}

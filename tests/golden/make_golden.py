@@ -204,7 +204,7 @@ def main():
     frame_fixture("frame_furnace.npz", env, 8, 1, dict(direct_spp=2, indirect_tasks=1, mis_samples=8))
 
 
-if __name__ == "__main__" and not ({"--train", "--pt", "--data"} & set(sys.argv)):
+if __name__ == "__main__" and not ({"--train", "--pt", "--data", "--drcc"} & set(sys.argv)):
     main()
 
 
@@ -328,3 +328,30 @@ def data_fixture():
 
 if __name__ == "__main__" and "--data" in sys.argv:
     data_fixture()
+
+
+def drcc_fixture():
+    """The entry pool of the frame_c1 frame (DrcState.entries, cache.py:196-201)
+    and its DRCC dump bytes (write_cache_dump, cache.py:476-485)."""
+    import tempfile
+
+    from drc.cache import write_cache_dump
+
+    c1 = scenegen.scene_doc(scenegen.build_scene("c1", resolution=(48, 48)))
+    scene = parse_scene(json.dumps(c1))
+    cfg = RenderConfig(threads=1, direct_spp=2, indirect_tasks=5, mis_samples=16)
+    net = rcnn.random_network(8, 0)
+    _, tel = render_drc(scene, cfg, net)
+    ents = tel["state"].entries()
+    with tempfile.NamedTemporaryFile(suffix=".drcc") as f:
+        write_cache_dump(ents, f.name)
+        raw = open(f.name, "rb").read()
+    save("drcc.npz", doc=doc_array(c1), drcc=np.frombuffer(raw, dtype=np.uint8),
+         e_px=np.array([e.pixel[0] for e in ents]), e_py=np.array([e.pixel[1] for e in ents]),
+         e_pos=np.stack([e.position for e in ents]), e_normal=np.stack([e.normal for e in ents]),
+         e_rad=np.stack([e.indirect_radiance for e in ents]),
+         e_thr=np.stack([e.specular_throughput for e in ents]))
+
+
+if __name__ == "__main__" and "--drcc" in sys.argv:
+    drcc_fixture()
