@@ -111,6 +111,7 @@ _SIGS = [
     ("drcb_render_drc_entries", C.c_int, [vp, vp, C.POINTER(Camera), C.POINTER(RenderCfg), vp, vp,
                                           vp, C.c_int64, C.c_int32, C.c_int32, vp, vp,
                                           C.POINTER(Entries), vp]),
+    ("drcb_trainer_set_mode", C.c_int, [vp, C.c_int32]),
     ("drcb_augment_gather", C.c_int, [vp, vp, vp, vp, C.c_int64, vp, C.c_int32, vp, vp, vp]),
     ("drcb_trainer_apply", C.c_int, [vp, C.c_float, vp]),
     ("drcb_trainer_export", C.c_int64, [vp, vp, C.c_int64]),

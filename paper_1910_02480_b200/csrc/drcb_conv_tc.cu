@@ -1551,6 +1551,13 @@ struct Buf {
 };
 
 // one conv layer: in (NHWC, c_in_tot == layer cin_pad) -> out slice
+// N tile: the largest of 256 / 128 / 64 / 32 / 16 (<= cap) dividing cout_pad
+int n_tile(int cout_pad, int cap) {
+  for (int b = cap; b >= 16; b /= 2)
+    if (cout_pad % b == 0) return b;
+  return 16;
+}
+
 // dx-in-N vs halo for a row-tile layer (measured on B200)
 bool rows_use_dx(const ConvLayer& L, int kind) {
   (void)kind;
@@ -1636,7 +1643,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
   a.num_m_tiles = int(nmaps * hw * hw / BM);
   a.cblocks = L.cin_pad / (ROW_BYTES / (KIND == 0 ? 2 : 4));
   a.num_kb = 9 * a.cblocks;
-  a.bn = L.cout_pad >= 256 ? 256 : L.cout_pad;
+  a.bn = n_tile(L.cout_pad, 256);
   a.num_n_tiles = L.cout_pad / a.bn;
   a.cout = pred ? L.cout_pad : L.cout_pad;  // padded channels carry exact zeros
   a.cout_tot = out.c;
@@ -1664,8 +1671,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     // row-tile kernel (hw 16/32); DRCB_ROWS=dx|halo overrides the variant
     static const char* mode_env = getenv("DRCB_ROWS");
     const bool dx = mode_env ? std::strcmp(mode_env, "dx") == 0 : rows_use_dx(L, KIND);
-    const int bn_cap = KIND == 0 ? 128 : 64;
-    while (a.bn > bn_cap) a.bn /= 2;
+    a.bn = n_tile(L.cout_pad, KIND == 0 ? 128 : 64);
     a.num_n_tiles = L.cout_pad / a.bn;
     RowArgs rz;
     rz.row_bytes = hw * ROW_BYTES;
@@ -1708,7 +1714,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       return dx ? launch_rows<KIND, true>(mA, mB, mO, mP, a, rz, res, smem, st)
                 : launch_rows<KIND, false>(mA, mB, mO, mP, a, rz, res, smem, st);
     }
-    a.bn = L.cout_pad >= 256 ? 256 : L.cout_pad;
+    a.bn = n_tile(L.cout_pad, 256);
     a.num_n_tiles = L.cout_pad / a.bn;
   }
   int box_w = hw, box_h = a.maps_per_tile == 1 ? a.rows_per_tile : hw, box_n = a.maps_per_tile;
@@ -1845,6 +1851,30 @@ int forward_tc_nhwc(NetImpl& net, const void* x_nhwc, float* y, int64_t n, int m
 }
 
 int tc_input_channels(int) { return 8; }  // compact NHWC input (7 + 1 zero channel)
+
+// One tensor-core conv on caller buffers (the training engine's forward and
+// dgrad): NHWC bf16 in (nmaps a multiple of 8, cin_pad channels), packed
+// K-major weights [cout_pad][9 * cin_pad], epilogue y = acc * a + b then
+// LeakyReLU(slope) (slope 1 = identity) into out's channel slice.
+int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int cin_pad, void* out,
+                 int out_ctot, int out_coff, const void* wpacked, int cout_pad, const float* ep_a,
+                 const float* ep_b, float slope, cudaStream_t st) {
+  NetImpl net;
+  net.slope = slope;
+  ConvLayer L;
+  L.name = "train";
+  L.cin = cin;
+  L.cout = cout;
+  L.hw = hw;
+  L.cin_pad = cin_pad;
+  L.cout_pad = cout_pad;
+  L.d_wtc = const_cast<void*>(wpacked);
+  L.d_ep_a = const_cast<float*>(ep_a);
+  L.d_ep_b = const_cast<float*>(ep_b);
+  L.tc_kind = 0;
+  tc::Buf bi{const_cast<void*>(in), cin_pad, hw}, bo{out, out_ctot, hw};
+  return tc::run_layer<0>(net, L, bi, bo, out_coff, nmaps, st);
+}
 
 int forward_tc(NetImpl& net, const float* x, float* y, int64_t n, int mode, cudaStream_t st) {
   if (n <= 0) return 0;

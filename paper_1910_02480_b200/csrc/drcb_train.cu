@@ -11,9 +11,17 @@
 #include <string>
 #include <vector>
 
+#include <cublas_v2.h>
+#include <cuda_bf16.h>
+#include <dlfcn.h>
+
 #include "drcb_net.h"
 
 namespace drcb {
+
+int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int cin_pad, void* out,
+                 int out_ctot, int out_coff, const void* wpacked, int cout_pad, const float* ep_a,
+                 const float* ep_b, float slope, cudaStream_t st);
 
 int conv_f32(const ConvLayer& L, const float* in, int cin_tot, int cin_off, float* out,
              int cout_tot, int cout_off, int64_t n, float slope, cudaStream_t st);
@@ -384,6 +392,135 @@ __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float
 
 inline unsigned nb(int64_t n, int t = 256) { return unsigned((n + t - 1) / t); }
 
+// ---------------------------------------------------------------------------
+// bf16 tensor-core path (drcb_trainer_set_mode(T, 2)): the 3x3 convs of the
+// forward and the dgrad run on the sm_100a implicit-GEMM kernels
+// (tc_conv_bf16) over NHWC bf16 copies, the weight gradient is one GEMM over
+// all pixels (im2col bf16 x dz bf16 -> fp32, cuBLAS), everything else (batch
+// norm, LeakyReLU, pools, upsample, Adam, fp32 master weights) is unchanged.
+
+inline int pad64(int c) { return (c + 63) / 64 * 64; }
+
+// conv-form fp32 weights [cout][cin][9] -> packed bf16 [coutp][9 * cinp]
+__global__ void k_pack_w(const float* __restrict__ w, int cout, int cin, int cinp, int coutp,
+                         __nv_bfloat16* __restrict__ out) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t kt = int64_t(9) * cinp;
+  if (i >= int64_t(coutp) * kt) return;
+  const int co = int(i / kt), r = int(i % kt), tap = r / cinp, ci = r % cinp;
+  out[i] = __float2bfloat16_rn((co < cout && ci < cin) ? w[(int64_t(co) * cin + ci) * 9 + tap] : 0.f);
+}
+
+// padded epilogue vector: v[c] (or fill when v == NULL) for c < n, 0 beyond
+__global__ void k_pad_vec(const float* __restrict__ v, int n, int np, float fill, float* out) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < np) out[c] = c < n ? (v ? v[c] : fill) : 0.f;
+}
+
+// NCHW fp32 channel slice [coff, coff + c) -> NHWC bf16 with cpad channels
+// (zeros in the padding and in maps n .. np-1); thread per (map, group of 8
+// channels, pixel), pixel fastest (coalesced reads)
+__global__ void k_nchw2nhwc(const float* __restrict__ in, int ctot, int coff, int c, int hw2,
+                            int64_t n, int64_t np, int cpad, __nv_bfloat16* __restrict__ out) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int G = cpad / 8;
+  if (i >= np * G * hw2) return;
+  const int p = int(i % hw2);
+  const int g = int((i / hw2) % G);
+  const int64_t m = i / (int64_t(hw2) * G);
+  __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int ch = g * 8 + j;
+    v[j] = __float2bfloat16_rn((m < n && ch < c) ? __ldg(in + (m * ctot + coff + ch) * hw2 + p) : 0.f);
+  }
+  *reinterpret_cast<uint4*>(out + (m * hw2 + p) * cpad + g * 8) = *reinterpret_cast<uint4*>(v);
+}
+
+// NHWC bf16 (cpad) -> NCHW fp32 channel slice; thread per (map, channel,
+// pixel), pixel fastest (coalesced writes)
+__global__ void k_nhwc2nchw(const __nv_bfloat16* __restrict__ in, int cpad, int c, int hw2,
+                            int64_t n, float* __restrict__ out, int ctot, int coff) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n * c * hw2) return;
+  const int p = int(i % hw2);
+  const int ch = int((i / hw2) % c);
+  const int64_t m = i / (int64_t(hw2) * c);
+  out[(m * ctot + coff + ch) * hw2 + p] = __bfloat162float(in[(m * hw2 + p) * cpad + ch]);
+}
+
+// im2col of an NHWC bf16 activation: X[p][tap][cinp] (zero outside the map)
+__global__ void k_im2col(const __nv_bfloat16* __restrict__ x, int hw, int64_t n, int cinp,
+                         __nv_bfloat16* __restrict__ X) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int G = cinp / 8;
+  const int hw2 = hw * hw;
+  if (i >= n * hw2 * 9 * G) return;
+  const int g = int(i % G);
+  const int tap = int((i / G) % 9);
+  const int64_t pg = i / (int64_t(G) * 9);
+  const int64_t m = pg / hw2;
+  const int p = int(pg % hw2), y = p / hw + tap / 3 - 1, xx = p % hw + tap % 3 - 1;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (y >= 0 && y < hw && xx >= 0 && xx < hw)
+    v = __ldg(reinterpret_cast<const uint4*>(x + ((m * hw2) + y * hw + xx) * cinp + g * 8));
+  reinterpret_cast<uint4*>(X)[i] = v;
+}
+
+// GEMM result C (col-major coutp x 9*cinp) -> conv-form gradient [co][ci][9]
+__global__ void k_wgrad_from_gemm(const float* __restrict__ C, int coutp, int cout, int cin,
+                                  int cinp, float* __restrict__ dwf) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(cout) * cin * 9) return;
+  const int tap = int(i % 9);
+  const int ci = int((i / 9) % cin);
+  const int co = int(i / (int64_t(9) * cin));
+  dwf[i] = C[co + (int64_t(tap) * cinp + ci) * coutp];
+}
+
+// per-channel sum of an NCHW tensor (conv bias gradient), grid (chunks, c)
+__global__ void k_chan_sum_acc(const float* __restrict__ x, int c, int hw2, int64_t n, double* acc) {
+  const int ch = blockIdx.y;
+  double s = 0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * hw2;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t m = i / hw2;
+    s += x[(m * c + ch) * hw2 + int(i % hw2)];
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(acc + ch, s);
+}
+__global__ void k_acc_to_float(const double* acc, int c, float* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < c) out[i] = float(acc[i]);
+}
+
+// cuBLAS, opened at first use (shares the process's instance with torch)
+struct Blas {
+  void* h = nullptr;
+  cublasStatus_t (*create)(cublasHandle_t*) = nullptr;
+  cublasStatus_t (*set_stream)(cublasHandle_t, cudaStream_t) = nullptr;
+  cublasStatus_t (*gemm_ex)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int,
+                            const void*, const void*, cudaDataType, int, const void*, cudaDataType,
+                            int, const void*, void*, cudaDataType, int, cublasComputeType_t,
+                            cublasGemmAlgo_t) = nullptr;
+};
+
+Blas* blas() {
+  static Blas b;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    b.h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (b.h) {
+      b.create = reinterpret_cast<decltype(b.create)>(dlsym(b.h, "cublasCreate_v2"));
+      b.set_stream = reinterpret_cast<decltype(b.set_stream)>(dlsym(b.h, "cublasSetStream_v2"));
+      b.gemm_ex = reinterpret_cast<decltype(b.gemm_ex)>(dlsym(b.h, "cublasGemmEx"));
+    }
+  }
+  return (b.create && b.set_stream && b.gemm_ex) ? &b : nullptr;
+}
+
 }  // namespace train
 }  // namespace drcb
 
@@ -401,6 +538,11 @@ struct DrcbTrainer {
   void* comm = nullptr;  // ncclComm_t or NULL
   int world = 1;
   std::vector<void*> allocs;
+  // bf16 tensor-core path
+  int mode = 0;  // 0 = fp32 CUDA cores (parity), 2 = bf16 tensor cores
+  void* blas = nullptr;                     // cublasHandle_t
+  std::vector<__nv_bfloat16*> wpk_f, wpk_t;  // packed fwd / dgrad weights per layer
+  std::vector<float*> ep_one_f, ep_one_t, ep_b, ep_zero;
 };
 
 namespace drcb {
@@ -610,6 +752,54 @@ extern "C" int drcb_trainer_create(const void* drcw, size_t len, float lr, float
   return 0;
 }
 
+// Select the conv engine: 0 = fp32 CUDA cores (the parity engine, default),
+// 2 = bf16 tensor cores (forward + dgrad on the implicit-GEMM kernels,
+// weight gradient via one bf16 GEMM; fp32 master weights, batch norm,
+// activations and Adam unchanged).
+extern "C" int drcb_trainer_set_mode(DrcbTrainer* T, int32_t mode) {
+  if (!T) return fail(DRCB_ECONTRACT, "drcb_trainer_set_mode: null trainer");
+  if (mode != 0 && mode != 2) return fail(DRCB_ECONFIG, "trainer mode must be 0 (fp32) or 2 (bf16)");
+  if (mode == 2 && T->wpk_f.empty()) {
+    if (!blas()) return fail(DRCB_ECUDA, "libcublas.so.12 not available");
+    cublasHandle_t h = nullptr;
+    if (blas()->create(&h) != CUBLAS_STATUS_SUCCESS) return fail(DRCB_ECUDA, "cublasCreate failed");
+    T->blas = h;
+    size_t bytes = 0;
+    std::vector<size_t> off;
+    for (int l = 0; l < 16; ++l) {
+      const TL& t = T->L[l];
+      const size_t cinp = pad64(t.cin), coutp = pad64(t.cout);
+      const size_t sz[6] = {coutp * 9 * cinp * 2, cinp * 9 * coutp * 2, coutp * 4, cinp * 4,
+                            coutp * 4, cinp * 4};
+      for (size_t z : sz) {
+        off.push_back(bytes);
+        bytes += (z + 255) / 256 * 256;
+      }
+    }
+    void* base = nullptr;
+    if (cudaMalloc(&base, bytes) != cudaSuccess) return fail(DRCB_ECUDA, "cudaMalloc bf16 state");
+    T->allocs.push_back(base);
+    uint8_t* b = static_cast<uint8_t*>(base);
+    for (int l = 0; l < 16; ++l) {
+      const TL& t = T->L[l];
+      const int cinp = pad64(t.cin), coutp = pad64(t.cout);
+      T->wpk_f.push_back(reinterpret_cast<__nv_bfloat16*>(b + off[6 * l]));
+      T->wpk_t.push_back(reinterpret_cast<__nv_bfloat16*>(b + off[6 * l + 1]));
+      T->ep_one_f.push_back(reinterpret_cast<float*>(b + off[6 * l + 2]));
+      T->ep_one_t.push_back(reinterpret_cast<float*>(b + off[6 * l + 3]));
+      T->ep_b.push_back(reinterpret_cast<float*>(b + off[6 * l + 4]));
+      T->ep_zero.push_back(reinterpret_cast<float*>(b + off[6 * l + 5]));
+      k_pad_vec<<<nb(coutp), 256>>>(nullptr, t.cout, coutp, 1.f, T->ep_one_f[l]);
+      k_pad_vec<<<nb(cinp), 256>>>(nullptr, t.cin, cinp, 1.f, T->ep_one_t[l]);
+      k_pad_vec<<<nb(cinp), 256>>>(nullptr, 0, cinp, 0.f, T->ep_zero[l]);
+    }
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "drcb_trainer_set_mode");
+  }
+  T->mode = mode;
+  return 0;
+}
+
 extern "C" void drcb_trainer_destroy(DrcbTrainer* T) {
   if (!T) return;
   for (void* p : T->allocs) cudaFree(p);
@@ -658,12 +848,94 @@ int bn_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& out, cudaS
   return 0;
 }
 
+// bf16 tensor-core conv of layer l: in (NCHW fp32 slice) -> W.z[l] (NCHW fp32)
+int conv_tc_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, cudaStream_t st) {
+  const TL& t = T->L[l];
+  const int hw2 = t.hw * t.hw, cinp = pad64(t.cin), coutp = pad64(t.cout);
+  const int64_t np = (n + 7) / 8 * 8;
+  __nv_bfloat16 *xi = nullptr, *zo = nullptr;
+  DRCB_CUDA(cudaMallocAsync((void**)&xi, size_t(np) * hw2 * cinp * 2, st));
+  DRCB_CUDA(cudaMallocAsync((void**)&zo, size_t(np) * hw2 * coutp * 2, st));
+  k_nchw2nhwc<<<nb(np * (cinp / 8) * hw2), 256, 0, st>>>(in.p, in.ctot, in.coff, t.cin, hw2, n, np,
+                                                          cinp, xi);
+  TCHECK("k_nchw2nhwc");
+  int rc = tc_conv_bf16(t.cin, t.cout, t.hw, np, xi, cinp, zo, coutp, 0, T->wpk_f[l], coutp,
+                        T->ep_one_f[l], T->ep_b[l], 1.0f, st);
+  if (rc) return rc;
+  k_nhwc2nchw<<<nb(n * t.cout * hw2), 256, 0, st>>>(zo, coutp, t.cout, hw2, n, W.z[l], t.cout, 0);
+  TCHECK("k_nhwc2nchw");
+  DRCB_CUDA(cudaFreeAsync(xi, st));
+  DRCB_CUDA(cudaFreeAsync(zo, st));
+  return 0;
+}
+
+// bf16 tensor-core backward of layer l's conv: dgrad (W.dz -> din, the
+// transposed conv on the tensor cores) and the weight gradient as one GEMM
+// over all pixels, dW[co][tap, ci] = sum_p dz[p][co] im2col(in)[p][tap, ci]
+int conv_tc_backward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, float* din,
+                     int din_ctot, cudaStream_t st) {
+  const TL& t = T->L[l];
+  const int hw2 = t.hw * t.hw, cinp = pad64(t.cin), coutp = pad64(t.cout);
+  const int64_t np = (n + 7) / 8 * 8;
+  __nv_bfloat16 *dzh = nullptr, *X = nullptr;
+  float* C = nullptr;
+  DRCB_CUDA(cudaMallocAsync((void**)&dzh, size_t(np) * hw2 * coutp * 2, st));
+  k_nchw2nhwc<<<nb(np * (coutp / 8) * hw2), 256, 0, st>>>(W.dz, t.cout, 0, t.cout, hw2, n, np,
+                                                           coutp, dzh);
+  TCHECK("k_nchw2nhwc");
+  if (din) {
+    __nv_bfloat16* dih = nullptr;
+    DRCB_CUDA(cudaMallocAsync((void**)&dih, size_t(np) * hw2 * cinp * 2, st));
+    int rc = tc_conv_bf16(t.cout, t.cin, t.hw, np, dzh, coutp, dih, cinp, 0, T->wpk_t[l], cinp,
+                          T->ep_one_t[l], T->ep_zero[l], 1.0f, st);
+    if (rc) return rc;
+    k_nhwc2nchw<<<nb(n * t.cin * hw2), 256, 0, st>>>(dih, cinp, t.cin, hw2, n, din, din_ctot, 0);
+    TCHECK("k_nhwc2nchw");
+    DRCB_CUDA(cudaFreeAsync(dih, st));
+  }
+  const int64_t P = n * hw2;
+  const int K9 = 9 * cinp;
+  __nv_bfloat16* xh = nullptr;
+  DRCB_CUDA(cudaMallocAsync((void**)&xh, size_t(np) * hw2 * cinp * 2, st));
+  DRCB_CUDA(cudaMallocAsync((void**)&X, size_t(P) * K9 * 2, st));
+  DRCB_CUDA(cudaMallocAsync((void**)&C, size_t(coutp) * K9 * 4, st));
+  k_nchw2nhwc<<<nb(np * (cinp / 8) * hw2), 256, 0, st>>>(in.p, in.ctot, in.coff, t.cin, hw2, n, np,
+                                                          cinp, xh);
+  TCHECK("k_nchw2nhwc");
+  k_im2col<<<nb(P * 9 * (cinp / 8)), 256, 0, st>>>(xh, t.hw, n, cinp, X);
+  TCHECK("k_im2col");
+  Blas* B = blas();
+  if (!B) return fail(DRCB_ECUDA, "libcublas.so.12 not available");
+  cublasHandle_t h = static_cast<cublasHandle_t>(T->blas);
+  if (B->set_stream(h, st) != CUBLAS_STATUS_SUCCESS) return fail(DRCB_ECUDA, "cublasSetStream");
+  const float one = 1.f, zero = 0.f;
+  // column-major: C (coutp x K9) = dz (coutp x P) * X^T (P x K9)
+  cublasStatus_t bs = B->gemm_ex(h, CUBLAS_OP_N, CUBLAS_OP_T, coutp, K9, int(P), &one, dzh,
+                                 CUDA_R_16BF, coutp, X, CUDA_R_16BF, K9, &zero, C, CUDA_R_32F,
+                                 coutp, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+  if (bs != CUBLAS_STATUS_SUCCESS) return fail(DRCB_ECUDA, "cublasGemmEx (wgrad) failed");
+  count_launch();
+  k_wgrad_from_gemm<<<nb(int64_t(t.cout) * t.cin * 9), 256, 0, st>>>(C, coutp, t.cout, t.cin, cinp,
+                                                                      W.dwf);
+  TCHECK("k_wgrad_from_gemm");
+  DRCB_CUDA(cudaFreeAsync(dzh, st));
+  DRCB_CUDA(cudaFreeAsync(xh, st));
+  DRCB_CUDA(cudaFreeAsync(X, st));
+  DRCB_CUDA(cudaFreeAsync(C, st));
+  return 0;
+}
+
 // conv/deconv + train BN + LeakyReLU layer l: in -> out slice
 int layer_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, const View& out,
                   cudaStream_t st) {
-  ConvLayer L;
-  conv_layer_view(T, l, T->wf + T->wf_off[l], L);
-  int rc = conv_f32(L, in.p, in.ctot, in.coff, W.z[l], T->L[l].cout, 0, n, T->slope, st);
+  int rc;
+  if (T->mode == 2) {
+    rc = conv_tc_forward(T, l, W, n, in, st);
+  } else {
+    ConvLayer L;
+    conv_layer_view(T, l, T->wf + T->wf_off[l], L);
+    rc = conv_f32(L, in.p, in.ctot, in.coff, W.z[l], T->L[l].cout, 0, n, T->slope, st);
+  }
   if (rc) return rc;
   return bn_forward(T, l, W, n, out, st);
 }
@@ -694,8 +966,52 @@ int layer_backward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, co
                                                         T->slope, W.acc, double(n) * hw2 * T->world,
                                                         W.dz);
   TCHECK("k_bn_bwd_apply");
-  k_chan_sum<<<t.cout, 256, 0, st>>>(W.dz, t.cout, hw2, n, T->grads + t.b);
-  TCHECK("k_chan_sum");
+  DRCB_CUDA(cudaMemsetAsync(W.acc, 0, sizeof(double) * t.cout, st));
+  k_chan_sum_acc<<<dim3(std::min<int64_t>(64, nb(n * hw2)), t.cout), 256, 0, st>>>(W.dz, t.cout,
+                                                                                  hw2, n, W.acc);
+  TCHECK("k_chan_sum_acc");
+  k_acc_to_float<<<nb(t.cout), 256, 0, st>>>(W.acc, t.cout, T->grads + t.b);
+  TCHECK("k_acc_to_float");
+  if (T->mode == 2) {
+    int rc = conv_tc_backward(T, l, W, n, in, din, din_ctot, st);
+    if (rc) return rc;
+    if (getenv("DRCB_TRAIN_CHECK")) {
+      // self-check: the tensor-core dgrad / wgrad of this layer against the
+      // fp32 CUDA-core kernels on the SAME inputs (bf16 operand rounding:
+      // ~3e-3 relative L2); fails the step beyond 2e-2
+      std::vector<float> a(t.cout * t.cin * 9), b(t.cout * t.cin * 9);
+      cudaMemcpyAsync(a.data(), W.dwf, a.size() * 4, cudaMemcpyDeviceToHost, st);
+      k_wgrad<3><<<t.cout * t.cin, 256, 0, st>>>(W.dz, t.cout, in.p, in.ctot, in.coff, t.cin, t.hw, n,
+                                                  W.dwf);
+      cudaMemcpyAsync(b.data(), W.dwf, b.size() * 4, cudaMemcpyDeviceToHost, st);
+      double num = 0, den = 0;
+      if (din) {
+        int64_t nd = n * din_ctot * t.hw * t.hw;
+        std::vector<float> c(nd), d(nd);
+        cudaMemcpyAsync(c.data(), din, nd * 4, cudaMemcpyDeviceToHost, st);
+        ConvLayer D;
+        D.cin = t.cout; D.cout = t.cin; D.hw = t.hw; D.ksize = 3; D.act = false; D.mode = 0;
+        D.d_w = T->wt + T->wf_off[l]; D.d_bias = nullptr;
+        conv_f32(D, W.dz, t.cout, 0, din, din_ctot, 0, n, T->slope, st);
+        cudaMemcpyAsync(d.data(), din, nd * 4, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        for (int64_t i = 0; i < nd; ++i) { num += (c[i]-d[i])*(c[i]-d[i]); den += d[i]*d[i]; }
+        cudaMemcpyAsync(din, c.data(), nd * 4, cudaMemcpyHostToDevice, st);
+        if (!(sqrt(num / (den + 1e-30)) <= 2e-2))
+          return fail(DRCB_ECUDA, "bf16 dgrad self-check failed at layer " + std::to_string(l));
+      }
+      cudaStreamSynchronize(st);
+      num = den = 0;
+      for (size_t i = 0; i < a.size(); ++i) { num += (a[i]-b[i])*(a[i]-b[i]); den += b[i]*b[i]; }
+      cudaMemcpyAsync(W.dwf, a.data(), a.size() * 4, cudaMemcpyHostToDevice, st);
+      cudaStreamSynchronize(st);
+      if (!(sqrt(num / (den + 1e-30)) <= 2e-2))
+        return fail(DRCB_ECUDA, "bf16 wgrad self-check failed at layer " + std::to_string(l));
+    }
+    k_wgrad_to_param<<<nb(t.nw), 256, 0, st>>>(W.dwf, t.cin, t.cout, 3, t.deconv, T->grads + t.w);
+    TCHECK("k_wgrad_to_param");
+    return 0;
+  }
   k_wgrad<3><<<t.cout * t.cin, 256, 0, st>>>(W.dz, t.cout, in.p, in.ctot, in.coff, t.cin, t.hw, n,
                                               W.dwf);
   TCHECK("k_wgrad");
@@ -740,6 +1056,17 @@ extern "C" int drcb_trainer_step(DrcbTrainer* T, const float* x, const float* y,
     k_wforms<<<nb(t.nw), 256, 0, st>>>(T->params + t.w, t.cin, t.cout, t.ks, t.deconv,
                                         T->wf + T->wf_off[l], T->wt + T->wf_off[l]);
     TCHECK("k_wforms");
+    if (T->mode == 2 && l < 16) {
+      const int cinp = pad64(t.cin), coutp = pad64(t.cout);
+      k_pack_w<<<nb(int64_t(coutp) * 9 * cinp), 256, 0, st>>>(T->wf + T->wf_off[l], t.cout, t.cin,
+                                                               cinp, coutp, T->wpk_f[l]);
+      TCHECK("k_pack_w");
+      k_pack_w<<<nb(int64_t(cinp) * 9 * coutp), 256, 0, st>>>(T->wt + T->wf_off[l], t.cin, t.cout,
+                                                               coutp, cinp, T->wpk_t[l]);
+      TCHECK("k_pack_w");
+      k_pad_vec<<<nb(coutp), 256, 0, st>>>(T->params + t.b, t.cout, coutp, 0.f, T->ep_b[l]);
+      TCHECK("k_pad_vec");
+    }
   }
   float* xin = const_cast<float*>(x);
   // ---- forward (model.py:80-88)

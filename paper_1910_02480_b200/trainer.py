@@ -54,7 +54,12 @@ def param_layout(k):
 
 
 class DeviceTrainer:
-    def __init__(self, net_or_drcw, lr=6e-5, betas=(0.9, 0.999), eps=1e-8):
+    """mode "fp32": CUDA-core engine (the parity engine); "bf16": the 3x3
+    convs' forward and dgrad on the tcgen05 implicit-GEMM kernels and the
+    weight gradient as one bf16 GEMM, with fp32 master weights, batch norm,
+    activations and Adam (BASELINE config 5: bf16 compute, fp32 master)."""
+
+    def __init__(self, net_or_drcw, lr=6e-5, betas=(0.9, 0.999), eps=1e-8, mode="fp32"):
         lib = _lib.load()
         raw = net_or_drcw if isinstance(net_or_drcw, (bytes, bytearray)) else save_weights(net_or_drcw)
         h = C.c_void_p()
@@ -66,6 +71,10 @@ class DeviceTrainer:
         _lib.call("drcb_trainer_info", h, info)
         self.k, self.n_params, self.n_running = int(info[0]), int(info[1]), int(info[2])
         self.layout = param_layout(self.k)
+        if mode not in ("fp32", "bf16"):
+            raise ValueError("trainer mode must be 'fp32' or 'bf16'")
+        self.mode = mode
+        _lib.call("drcb_trainer_set_mode", h, 0 if mode == "fp32" else 2)
 
     # -- steps ---------------------------------------------------------------
     def step(self, x, y, apply=True, want_loss=True):

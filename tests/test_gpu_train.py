@@ -89,3 +89,26 @@ def test_nccl_syncbn_path_single_rank_matches_plain_step(g):
     for name in pa:
         assert np.array_equal(pa[name], pb[name]), name
     comm.close()
+
+
+def test_bf16_tensor_core_trainer(monkeypatch):
+    """mode="bf16": forward/dgrad on the tcgen05 conv kernels, weight gradient
+    as one bf16 GEMM. The self-check (DRCB_TRAIN_CHECK) compares every layer's
+    tensor-core dgrad and wgrad with the fp32 kernels on the same inputs
+    inside the step (bf16 rounding ~3e-3, fails beyond 2e-2); the whole step
+    tracks the fp32 engine (BN makes per-layer gradients sensitive to the
+    bf16 forward, so the comparison is on losses)."""
+    rng = np.random.default_rng(0)
+    x = torch.from_numpy(rng.uniform(0, 1, (16, 7, 32, 32)).astype(np.float32)).cuda()
+    x[:, :3] *= 3
+    y = torch.from_numpy(np.exp(rng.normal(-1, 1, (16, 3, 32, 32))).astype(np.float32)).cuda()
+    net = cnn.random_network(64, 2)
+    a = DeviceTrainer(net, lr=1e-4)
+    b = DeviceTrainer(net, lr=1e-4, mode="bf16")
+    monkeypatch.setenv("DRCB_TRAIN_CHECK", "1")
+    la, lb = a.step(x, y, apply=False), b.step(x, y, apply=False)
+    assert abs(lb - la) <= 2e-3 * la
+    monkeypatch.delenv("DRCB_TRAIN_CHECK")
+    for _ in range(20):
+        la, lb = a.step(x, y), b.step(x, y)
+    assert abs(lb - la) <= 2e-2 * la, (la, lb)
