@@ -273,6 +273,12 @@ int drcb_trainer_buffers(const DrcbTrainer *t, void **params, void **grads, void
 /* forward + loss + backward into the gradient buffer; x (n,7,32,32),
  * y (n,3,32,32) device fp32; apply_adam=1 also takes the optimiser step.
  * loss_host (optional) receives the mean L1 loss (synchronises). */
+/* conv engine: 0 = fp32 CUDA cores (the parity engine, default), 2 = bf16
+ * tensor cores (forward + dgrad on the tcgen05 implicit-GEMM conv kernels,
+ * weight gradient as one bf16 GEMM over all pixels; fp32 master weights,
+ * batch norm, activations and Adam). Env DRCB_TRAIN_CHECK=1 makes every bf16
+ * step compare each layer's dgrad/wgrad with the fp32 kernels (fails > 2e-2). */
+int drcb_trainer_set_mode(DrcbTrainer *t, int32_t mode);
 int drcb_trainer_step(DrcbTrainer *t, const float *x, const float *y, int64_t n,
                       double *loss_host, int32_t apply_adam, void *stream);
 /* Adam on the gradient buffer scaled by grad_scale (1/world after an
