@@ -417,55 +417,75 @@ __global__ void k_pad_vec(const float* __restrict__ v, int n, int np, float fill
   if (c < np) out[c] = c < n ? (v ? v[c] : fill) : 0.f;
 }
 
-// NCHW fp32 channel slice [coff, coff + c) -> NHWC bf16 with cpad channels
-// (zeros in the padding and in maps n .. np-1); thread per (map, group of 8
-// channels, pixel), pixel fastest (coalesced reads)
-__global__ void k_nchw2nhwc(const float* __restrict__ in, int ctot, int coff, int c, int hw2,
-                            int64_t n, int64_t np, int cpad, __nv_bfloat16* __restrict__ out) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int G = cpad / 8;
-  if (i >= np * G * hw2) return;
-  const int p = int(i % hw2);
-  const int g = int((i / hw2) % G);
-  const int64_t m = i / (int64_t(hw2) * G);
+
+
+// Tiled layout conversions (32 pixels x 64 channels per block through SMEM,
+// both sides coalesced). Pixels are flattened over (map, pixel); `pad` = 1
+// writes the (hw+2)^2 zero-bordered layout used by the weight-gradient GEMMs
+// (its border is cleared by the caller), `mbase` shifts by a margin.
+__global__ void __launch_bounds__(256) k_nchw2nhwc_t(const float* __restrict__ in, int ctot, int coff,
+                                                     int c, int hw, int64_t n, int cpad, int pad,
+                                                     int64_t mbase, __nv_bfloat16* __restrict__ out) {
+  __shared__ float tile[64][33];
+  const int hw2 = hw * hw;
+  const int64_t P0 = int64_t(blockIdx.x) * 32;
+  const int c0 = blockIdx.y * 64;
+  for (int k = 0; k < 8; ++k) {
+    const int idx = threadIdx.x + 256 * k, ch = idx >> 5, px = idx & 31;
+    const int64_t P = P0 + px, m = P / hw2;
+    const int p = int(P % hw2);
+    float v = 0.f;
+    if (m < n && c0 + ch < c) v = __ldg(in + (m * ctot + coff + c0 + ch) * hw2 + p);
+    tile[ch][px] = v;
+  }
+  __syncthreads();
+  const int px = threadIdx.x >> 3, piece = threadIdx.x & 7;
+  const int64_t P = P0 + px, m = P / hw2;
+  const int p = int(P % hw2);
   __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int ch = g * 8 + j;
-    v[j] = __float2bfloat16_rn((m < n && ch < c) ? __ldg(in + (m * ctot + coff + ch) * hw2 + p) : 0.f);
+  for (int j = 0; j < 8; ++j) v[j] = __float2bfloat16_rn(tile[piece * 8 + j][px]);
+  const int64_t q = pad ? mbase + (m * (hw + 2) + p / hw + 1) * (hw + 2) + p % hw + 1 : P;
+  *reinterpret_cast<uint4*>(out + q * cpad + c0 + piece * 8) = *reinterpret_cast<uint4*>(v);
+}
+
+__global__ void __launch_bounds__(256) k_nhwc2nchw_t(const __nv_bfloat16* __restrict__ in, int cpad,
+                                                     int c, int hw2, int64_t n,
+                                                     float* __restrict__ out, int ctot, int coff) {
+  __shared__ float tile[64][33];
+  const int64_t P0 = int64_t(blockIdx.x) * 32;
+  const int c0 = blockIdx.y * 64;
+  {
+    const int px = threadIdx.x >> 3, piece = threadIdx.x & 7;
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(in + (P0 + px) * cpad + c0 + piece * 8));
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tile[piece * 8 + j][px] = __bfloat162float(b[j]);
   }
-  *reinterpret_cast<uint4*>(out + (m * hw2 + p) * cpad + g * 8) = *reinterpret_cast<uint4*>(v);
+  __syncthreads();
+  for (int k = 0; k < 8; ++k) {
+    const int idx = threadIdx.x + 256 * k, ch = idx >> 5, px = idx & 31;
+    const int64_t P = P0 + px, m = P / hw2;
+    if (m < n && c0 + ch < c) out[(m * ctot + coff + c0 + ch) * hw2 + int(P % hw2)] = tile[ch][px];
+  }
 }
 
-// NHWC bf16 (cpad) -> NCHW fp32 channel slice; thread per (map, channel,
-// pixel), pixel fastest (coalesced writes)
-__global__ void k_nhwc2nchw(const __nv_bfloat16* __restrict__ in, int cpad, int c, int hw2,
-                            int64_t n, float* __restrict__ out, int ctot, int coff) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n * c * hw2) return;
-  const int p = int(i % hw2);
-  const int ch = int((i / hw2) % c);
-  const int64_t m = i / (int64_t(hw2) * c);
-  out[(m * ctot + coff + ch) * hw2 + p] = __bfloat162float(in[(m * hw2 + p) * cpad + ch]);
+// 1x1 conv weight gradient (head.conv_out): dW[co][ci] = sum_p dz x, grid
+// (chunks, cout * cin), double accumulation
+__global__ void k_wgrad1_acc(const float* __restrict__ dz, int cout, const float* __restrict__ in,
+                             int cin, int hw2, int64_t n, double* acc) {
+  const int co = blockIdx.y / cin, ci = blockIdx.y % cin;
+  double s = 0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * hw2;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t m = i / hw2;
+    const int p = int(i % hw2);
+    s += double(dz[(m * cout + co) * hw2 + p]) * in[(m * cin + ci) * hw2 + p];
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(acc + blockIdx.y, s);
 }
 
-// im2col of an NHWC bf16 activation: X[p][tap][cinp] (zero outside the map)
-__global__ void k_im2col(const __nv_bfloat16* __restrict__ x, int hw, int64_t n, int cinp,
-                         __nv_bfloat16* __restrict__ X) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int G = cinp / 8;
-  const int hw2 = hw * hw;
-  if (i >= n * hw2 * 9 * G) return;
-  const int g = int(i % G);
-  const int tap = int((i / G) % 9);
-  const int64_t pg = i / (int64_t(G) * 9);
-  const int64_t m = pg / hw2;
-  const int p = int(pg % hw2), y = p / hw + tap / 3 - 1, xx = p % hw + tap % 3 - 1;
-  uint4 v = make_uint4(0, 0, 0, 0);
-  if (y >= 0 && y < hw && xx >= 0 && xx < hw)
-    v = __ldg(reinterpret_cast<const uint4*>(x + ((m * hw2) + y * hw + xx) * cinp + g * 8));
-  reinterpret_cast<uint4*>(X)[i] = v;
-}
 
 // GEMM result C (col-major coutp x 9*cinp) -> conv-form gradient [co][ci][9]
 __global__ void k_wgrad_from_gemm(const float* __restrict__ C, int coutp, int cout, int cin,
@@ -848,6 +868,26 @@ int bn_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& out, cudaS
   return 0;
 }
 
+// NCHW fp32 slice -> NHWC bf16 (np maps, cpad channels); pad = 1: the
+// zero-bordered (hw+2)^2 layout with `margin` zero pixels before the first map
+int to_nhwc(const View& in, int c, int hw, int64_t n, int64_t np, int cpad, int pad, int64_t margin,
+            __nv_bfloat16* out, cudaStream_t st) {
+  dim3 g(unsigned(np * hw * hw / 32), unsigned(cpad / 64));
+  k_nchw2nhwc_t<<<g, 256, 0, st>>>(in.p, in.ctot, in.coff, c, hw, n, cpad, pad, margin, out);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : cuda_fail(e, "k_nchw2nhwc_t");
+}
+
+int to_nchw(const __nv_bfloat16* in, int cpad, int c, int hw, int64_t n, int64_t np, float* out,
+            int ctot, int coff, cudaStream_t st) {
+  dim3 g(unsigned(np * hw * hw / 32), unsigned(cpad / 64));
+  k_nhwc2nchw_t<<<g, 256, 0, st>>>(in, cpad, c, hw * hw, n, out, ctot, coff);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : cuda_fail(e, "k_nhwc2nchw_t");
+}
+
 // bf16 tensor-core conv of layer l: in (NCHW fp32 slice) -> W.z[l] (NCHW fp32)
 int conv_tc_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, cudaStream_t st) {
   const TL& t = T->L[l];
@@ -856,71 +896,76 @@ int conv_tc_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, c
   __nv_bfloat16 *xi = nullptr, *zo = nullptr;
   DRCB_CUDA(cudaMallocAsync((void**)&xi, size_t(np) * hw2 * cinp * 2, st));
   DRCB_CUDA(cudaMallocAsync((void**)&zo, size_t(np) * hw2 * coutp * 2, st));
-  k_nchw2nhwc<<<nb(np * (cinp / 8) * hw2), 256, 0, st>>>(in.p, in.ctot, in.coff, t.cin, hw2, n, np,
-                                                          cinp, xi);
-  TCHECK("k_nchw2nhwc");
-  int rc = tc_conv_bf16(t.cin, t.cout, t.hw, np, xi, cinp, zo, coutp, 0, T->wpk_f[l], coutp,
-                        T->ep_one_f[l], T->ep_b[l], 1.0f, st);
+  int rc = to_nhwc(in, t.cin, t.hw, n, np, cinp, 0, 0, xi, st);
+  if (!rc)
+    rc = tc_conv_bf16(t.cin, t.cout, t.hw, np, xi, cinp, zo, coutp, 0, T->wpk_f[l], coutp,
+                      T->ep_one_f[l], T->ep_b[l], 1.0f, st);
+  if (!rc) rc = to_nchw(zo, coutp, t.cout, t.hw, n, np, W.z[l], t.cout, 0, st);
   if (rc) return rc;
-  k_nhwc2nchw<<<nb(n * t.cout * hw2), 256, 0, st>>>(zo, coutp, t.cout, hw2, n, W.z[l], t.cout, 0);
-  TCHECK("k_nhwc2nchw");
   DRCB_CUDA(cudaFreeAsync(xi, st));
   DRCB_CUDA(cudaFreeAsync(zo, st));
   return 0;
 }
 
-// bf16 tensor-core backward of layer l's conv: dgrad (W.dz -> din, the
-// transposed conv on the tensor cores) and the weight gradient as one GEMM
-// over all pixels, dW[co][tap, ci] = sum_p dz[p][co] im2col(in)[p][tap, ci]
+// bf16 tensor-core backward of layer l's conv. dgrad: the transposed conv on
+// the tensor cores (W.dz -> din). Weight gradient without an im2col buffer:
+// with dz and x in the zero-bordered (hw+2)^2 layout, every tap is a constant
+// offset s = (ky-1)(hw+2) + (kx-1) in the flattened padded pixel index, so
+//   dW_tap[co][ci] = sum_q dz_pad[q][co] * x_pad[q + s][ci]
+// is one plain GEMM per tap over all padded pixels (dz is zero on the border,
+// so border rows add nothing and shifted rows never leave x's zero margins).
 int conv_tc_backward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, float* din,
                      int din_ctot, cudaStream_t st) {
   const TL& t = T->L[l];
-  const int hw2 = t.hw * t.hw, cinp = pad64(t.cin), coutp = pad64(t.cout);
+  const int hw = t.hw, hw2 = hw * hw, cinp = pad64(t.cin), coutp = pad64(t.cout);
   const int64_t np = (n + 7) / 8 * 8;
-  __nv_bfloat16 *dzh = nullptr, *X = nullptr;
-  float* C = nullptr;
-  DRCB_CUDA(cudaMallocAsync((void**)&dzh, size_t(np) * hw2 * coutp * 2, st));
-  k_nchw2nhwc<<<nb(np * (coutp / 8) * hw2), 256, 0, st>>>(W.dz, t.cout, 0, t.cout, hw2, n, np,
-                                                           coutp, dzh);
-  TCHECK("k_nchw2nhwc");
+  const View dzv{W.dz, t.cout, 0};
+  int rc = 0;
   if (din) {
-    __nv_bfloat16* dih = nullptr;
+    __nv_bfloat16 *dzh = nullptr, *dih = nullptr;
+    DRCB_CUDA(cudaMallocAsync((void**)&dzh, size_t(np) * hw2 * coutp * 2, st));
     DRCB_CUDA(cudaMallocAsync((void**)&dih, size_t(np) * hw2 * cinp * 2, st));
-    int rc = tc_conv_bf16(t.cout, t.cin, t.hw, np, dzh, coutp, dih, cinp, 0, T->wpk_t[l], cinp,
-                          T->ep_one_t[l], T->ep_zero[l], 1.0f, st);
+    rc = to_nhwc(dzv, t.cout, hw, n, np, coutp, 0, 0, dzh, st);
+    if (!rc)
+      rc = tc_conv_bf16(t.cout, t.cin, hw, np, dzh, coutp, dih, cinp, 0, T->wpk_t[l], cinp,
+                        T->ep_one_t[l], T->ep_zero[l], 1.0f, st);
+    if (!rc) rc = to_nchw(dih, cinp, t.cin, hw, n, np, din, din_ctot, 0, st);
     if (rc) return rc;
-    k_nhwc2nchw<<<nb(n * t.cin * hw2), 256, 0, st>>>(dih, cinp, t.cin, hw2, n, din, din_ctot, 0);
-    TCHECK("k_nhwc2nchw");
+    DRCB_CUDA(cudaFreeAsync(dzh, st));
     DRCB_CUDA(cudaFreeAsync(dih, st));
   }
-  const int64_t P = n * hw2;
-  const int K9 = 9 * cinp;
-  __nv_bfloat16* xh = nullptr;
-  DRCB_CUDA(cudaMallocAsync((void**)&xh, size_t(np) * hw2 * cinp * 2, st));
-  DRCB_CUDA(cudaMallocAsync((void**)&X, size_t(P) * K9 * 2, st));
-  DRCB_CUDA(cudaMallocAsync((void**)&C, size_t(coutp) * K9 * 4, st));
-  k_nchw2nhwc<<<nb(np * (cinp / 8) * hw2), 256, 0, st>>>(in.p, in.ctot, in.coff, t.cin, hw2, n, np,
-                                                          cinp, xh);
-  TCHECK("k_nchw2nhwc");
-  k_im2col<<<nb(P * 9 * (cinp / 8)), 256, 0, st>>>(xh, t.hw, n, cinp, X);
-  TCHECK("k_im2col");
+  const int wp = hw + 2;
+  const int64_t Q = np * wp * wp, margin = wp + 1;
+  __nv_bfloat16 *dzp = nullptr, *xp = nullptr;
+  float* C = nullptr;
+  DRCB_CUDA(cudaMallocAsync((void**)&dzp, size_t(Q) * coutp * 2, st));
+  DRCB_CUDA(cudaMallocAsync((void**)&xp, size_t(Q + 2 * margin) * cinp * 2, st));
+  DRCB_CUDA(cudaMallocAsync((void**)&C, size_t(9) * coutp * cinp * 4, st));
+  DRCB_CUDA(cudaMemsetAsync(dzp, 0, size_t(Q) * coutp * 2, st));
+  DRCB_CUDA(cudaMemsetAsync(xp, 0, size_t(Q + 2 * margin) * cinp * 2, st));
+  rc = to_nhwc(dzv, t.cout, hw, n, np, coutp, 1, 0, dzp, st);
+  if (!rc) rc = to_nhwc(in, t.cin, hw, n, np, cinp, 1, margin, xp, st);
+  if (rc) return rc;
   Blas* B = blas();
   if (!B) return fail(DRCB_ECUDA, "libcublas.so.12 not available");
   cublasHandle_t h = static_cast<cublasHandle_t>(T->blas);
   if (B->set_stream(h, st) != CUBLAS_STATUS_SUCCESS) return fail(DRCB_ECUDA, "cublasSetStream");
   const float one = 1.f, zero = 0.f;
-  // column-major: C (coutp x K9) = dz (coutp x P) * X^T (P x K9)
-  cublasStatus_t bs = B->gemm_ex(h, CUBLAS_OP_N, CUBLAS_OP_T, coutp, K9, int(P), &one, dzh,
-                                 CUDA_R_16BF, coutp, X, CUDA_R_16BF, K9, &zero, C, CUDA_R_32F,
-                                 coutp, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-  if (bs != CUBLAS_STATUS_SUCCESS) return fail(DRCB_ECUDA, "cublasGemmEx (wgrad) failed");
-  count_launch();
+  for (int tap = 0; tap < 9; ++tap) {
+    const int64_t shift = int64_t(tap / 3 - 1) * wp + (tap % 3 - 1);
+    // column-major: C_tap (coutp x cinp) = dz_pad (coutp x Q) * x_pad[+s]^T (Q x cinp)
+    cublasStatus_t bs = B->gemm_ex(h, CUBLAS_OP_N, CUBLAS_OP_T, coutp, cinp, int(Q), &one, dzp,
+                                   CUDA_R_16BF, coutp, xp + (margin + shift) * cinp, CUDA_R_16BF,
+                                   cinp, &zero, C + int64_t(tap) * coutp * cinp, CUDA_R_32F, coutp,
+                                   CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    if (bs != CUBLAS_STATUS_SUCCESS) return fail(DRCB_ECUDA, "cublasGemmEx (wgrad) failed");
+    count_launch();
+  }
   k_wgrad_from_gemm<<<nb(int64_t(t.cout) * t.cin * 9), 256, 0, st>>>(C, coutp, t.cout, t.cin, cinp,
                                                                       W.dwf);
   TCHECK("k_wgrad_from_gemm");
-  DRCB_CUDA(cudaFreeAsync(dzh, st));
-  DRCB_CUDA(cudaFreeAsync(xh, st));
-  DRCB_CUDA(cudaFreeAsync(X, st));
+  DRCB_CUDA(cudaFreeAsync(dzp, st));
+  DRCB_CUDA(cudaFreeAsync(xp, st));
   DRCB_CUDA(cudaFreeAsync(C, st));
   return 0;
 }
@@ -1111,10 +1156,17 @@ extern "C" int drcb_trainer_step(DrcbTrainer* T, const float* x, const float* y,
   {
     const TL& t = T->L[16];
     // conv_out: dW, db, d(a15)
-    k_chan_sum<<<3, 256, 0, st>>>(W.dpre, 3, 1024, n, T->grads + t.b);
-    TCHECK("k_chan_sum");
-    k_wgrad<1><<<3 * t.cin, 256, 0, st>>>(W.dpre, 3, W.a15, k / 4, 0, t.cin, 32, n, W.dwf);
-    TCHECK("k_wgrad");
+    DRCB_CUDA(cudaMemsetAsync(W.acc, 0, sizeof(double) * (3 + 3 * t.cin), st));
+    k_chan_sum_acc<<<dim3(std::min<int64_t>(64, nb(n * 1024)), 3), 256, 0, st>>>(W.dpre, 3, 1024, n,
+                                                                                 W.acc);
+    TCHECK("k_chan_sum_acc");
+    k_acc_to_float<<<1, 32, 0, st>>>(W.acc, 3, T->grads + t.b);
+    TCHECK("k_acc_to_float");
+    k_wgrad1_acc<<<dim3(std::min<int64_t>(32, nb(n * 1024)), 3 * t.cin), 256, 0, st>>>(
+        W.dpre, 3, W.a15, t.cin, 1024, n, W.acc + 3);
+    TCHECK("k_wgrad1_acc");
+    k_acc_to_float<<<nb(3 * t.cin), 256, 0, st>>>(W.acc + 3, 3 * t.cin, W.dwf);
+    TCHECK("k_acc_to_float");
     k_wgrad_to_param<<<nb(t.nw), 256, 0, st>>>(W.dwf, t.cin, 3, 1, 0, T->grads + t.w);
     TCHECK("k_wgrad_to_param");
     ConvLayer D;
