@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--cpu-pixels", type=int, default=4096)
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--direct-spp", type=int, default=0)
+    ap.add_argument("--no-train", action="store_true",
+                    help="skip the secondary training-step measurement")
     return ap.parse_args()
 
 
@@ -167,6 +169,38 @@ _CFG_NAME = ["c3"]
 
 def cfg_name():
     return _CFG_NAME[0]
+
+
+def train_throughput(cnn, batches=(64, 256), steps=5, warmup=2):
+    """Secondary figure (BASELINE config 5 is not the metric's config): the
+    autoencoder's training step (train-mode BN, L1, Adam, fp32 master
+    weights) on synthetic (B,7,32,32) batches, bf16 tensor-core engine and the
+    fp32 parity engine, CUDA-event timed on device-resident batches."""
+    import torch
+
+    from paper_1910_02480_b200.trainer import DeviceTrainer
+
+    net = cnn.random_network(64, seed=3)
+    out = {"model": "MapAutoencoder k=64 (7,32,32)->(3,32,32)", "unit": "samples/s"}
+    for mode in ("bf16", "fp32"):
+        tr = DeviceTrainer(net, lr=1e-4, mode=mode)
+        for b in batches if mode == "bf16" else batches[:1]:
+            g = torch.Generator(device="cuda").manual_seed(3)
+            x = torch.rand((b, 7, 32, 32), device="cuda", generator=g)
+            y = torch.rand((b, 3, 32, 32), device="cuda", generator=g)
+            for _ in range(warmup):
+                tr.step(x, y, want_loss=False)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(steps):
+                tr.step(x, y, want_loss=False)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            out[f"{mode}_b{b}"] = {"samples_per_s": b / (ms / 1e3), "ms_per_step": ms}
+        tr.close()
+    return out
 
 
 def network_traffic(n_maps):
@@ -367,6 +401,12 @@ def main():
         except Exception as e:  # the baseline must never break the GPU line
             cb = {"value": None, "error": repr(e)}
     launches = launches_timed
+    train = None
+    if rank == 0 and not args.no_train:
+        try:
+            train = train_throughput(cnn)
+        except Exception as e:  # secondary figure; never breaks the GPU line
+            train = {"error": repr(e)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
@@ -378,6 +418,7 @@ def main():
             "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "scene_stats": st,
+            "train": train,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
