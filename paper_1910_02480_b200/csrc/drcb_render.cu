@@ -163,7 +163,7 @@ __device__ __forceinline__ int64_t pixel_of(const DevCamera& C, int64_t k) {
 }
 
 template <typename R>
-__global__ void __launch_bounds__(TPB) k_gbuffer(DevScene S, DevCamera C, DrcbGBuffer gb) {
+__global__ void __launch_bounds__(TPB, 8) k_gbuffer(DevScene S, DevCamera C, DrcbGBuffer gb) {
   int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= int64_t(C.W) * C.H) return;
   const int64_t i = pixel_of(C, k);
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(TPB) k_gbuffer(DevScene S, DevCamera C, DrcbGB
 }
 
 template <typename R>
-__global__ void __launch_bounds__(TPB) k_direct_samples(DevScene S, DevCamera C, DrcbRenderCfg cfg,
+__global__ void __launch_bounds__(TPB, 8) k_direct_samples(DevScene S, DevCamera C, DrcbRenderCfg cfg,
                                                          R* samples, int64_t* nonfinite) {
   const int spp = cfg.direct_spp;
   const int64_t npx = int64_t(C.W) * C.H;
@@ -223,7 +223,7 @@ __global__ void k_direct_reduce(DevCamera C, int spp, int tile, const R* __restr
 constexpr int MAP_TPB = 256;
 
 template <typename R>
-__global__ void __launch_bounds__(MAP_TPB, 3) k_map_paths(DevScene S, DrcbRenderCfg cfg,
+__global__ void __launch_bounds__(MAP_TPB, 4) k_map_paths(DevScene S, DrcbRenderCfg cfg,
                                                           const R* __restrict__ pos,
                                                           const R* __restrict__ nrm,
                                                           const uint64_t* __restrict__ keys,
