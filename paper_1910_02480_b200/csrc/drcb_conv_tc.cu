@@ -654,7 +654,7 @@ struct RowArgs {
 // RES: the whole weight matrix stays resident in SMEM ([chunk][dy][dx]
 // tiles). 8 epilogue warps (two per TMEM lane quarter) stage the tile in
 // SMEM in the output map's swizzled layout; one thread TMA-stores it.
-template <int KIND, int BN, bool RES, bool DX>
+template <int KIND, int BN, bool RES, bool DX, int MH>
 __global__ void __launch_bounds__(RT_THREADS, 1)
     k_conv_rows(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapP,
@@ -663,12 +663,15 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   constexpr int B3 = 3 * B_TILE;                       // one B stage: three weight tiles
   constexpr int ELEM = KIND == 0 ? 2 : 4;
   constexpr int CEL = ROW_BYTES / ELEM;
-  constexpr int NACCW = DX ? 3 * BN : BN;              // TMEM columns per accumulator
-  constexpr int NACC = 2 * NACCW <= 512 ? 2 : 1;       // TMEM accumulator buffers
+  constexpr int NACCW = DX ? 3 * BN : BN;              // TMEM columns per M block
+  // MH = 2: a work tile is two M blocks (BM rows each) sharing every A and B
+  // stage (half the weight traffic per pixel for streamed-weight layers)
+  constexpr int NACC = 2 * MH * NACCW <= 512 ? 2 : 1;  // TMEM accumulator buffers
+  static_assert(MH == 1 || (BN <= CEL && DX), "two-block tiles: one staging sub-tile, dx-in-N");
   constexpr int NSPLIT = NACCW <= 256 ? 1 : 2;
   constexpr int NMMA = NACCW / NSPLIT;
   constexpr int BPA = DX ? 3 : 1;                      // B stages per A stage
-  constexpr uint32_t COLS = NACC * NACCW;
+  constexpr uint32_t COLS = NACC * MH * NACCW;
   constexpr uint32_t TMEM_COLS = COLS <= 32 ? 32 : (COLS <= 64 ? 64 : (COLS <= 128 ? 128 : (COLS <= 256 ? 256 : 512)));
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -774,7 +777,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * NACCW;
+        const uint32_t tmem_d = tmem_base + acc * MH * NACCW;
         bool first = true;
         for (int as = 0; as < astages; ++as) {
           const int cb = DX ? as : as / 3, dxi = DX ? 1 : as % 3;
@@ -803,9 +806,13 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < ROW_BYTES / 32; ++k) {
 #pragma unroll
-              for (int sp = 0; sp < NSPLIT; ++sp)
-                tc_mma<KIND>(tmem_d + sp * NMMA, sw128_desc(aa + 32 * k),
-                             sw128_desc(bb + sp * NMMA * ROW_BYTES + 32 * k), idesc, first ? 0u : 1u);
+              for (int mh = 0; mh < MH; ++mh)
+#pragma unroll
+                for (int sp = 0; sp < NSPLIT; ++sp)
+                  tc_mma<KIND>(tmem_d + mh * NACCW + sp * NMMA,
+                               sw128_desc(aa + mh * BM * ROW_BYTES + 32 * k),
+                               sw128_desc(bb + sp * NMMA * ROW_BYTES + 32 * k), idesc,
+                               first ? 0u : 1u);
               first = false;
             }
             if (!RES && DX) {
@@ -848,13 +855,15 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
       int nt = tile % p.num_n_tiles, mt = tile / p.num_n_tiles;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t m = int64_t(mt) * BM + row;
-      const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + acc * NACCW;
+      const uint32_t tbase0 = tmem_base + (uint32_t(q * 32) << 16) + acc * MH * NACCW;
       if (h.o_bytes) {
         uint8_t* ot = ostage + obuf * h.o_bytes;
         if (threadIdx.x == 64) bulk_wait_read1();  // the store issued 2 tiles ago has read ot
         epi_bar_rt();
-        epilogue_stage<KIND, BN, DX, CSTEP>(p, tbase, m, nt, ot, 16 * grp);
+#pragma unroll
+        for (int mh = 0; mh < MH; ++mh)
+          epilogue_stage<KIND, BN, DX, CSTEP>(p, tbase0 + mh * NACCW, (int64_t(mt) * MH + mh) * BM + row,
+                                              nt, ot + mh * BM * ROW_BYTES, 16 * grp);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -864,7 +873,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
         const int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
         if (threadIdx.x == 64) {
           for (int sb2 = 0; sb2 < (BN + CEL - 1) / CEL; ++sb2)
-            tma_store_4d(&mapO, ot + sb2 * BM * ROW_BYTES, p.cout_off + nt * BN + sb2 * CEL, 0, y0, n0);
+            tma_store_4d(&mapO, ot + sb2 * MH * BM * ROW_BYTES, p.cout_off + nt * BN + sb2 * CEL, 0, y0, n0);
         }
         if (h.p_bytes) {
           // fused 2x2 max-pool (cnn.py:152-156) of the staged, already rounded
@@ -899,7 +908,10 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
         if (threadIdx.x == 64) bulk_commit();
         obuf ^= 1;
       } else {
-        epilogue_tile<KIND, BN, DX>(p, tbase, m, nt, nullptr, 16 * grp, CSTEP);
+#pragma unroll
+        for (int mh = 0; mh < MH; ++mh)
+          epilogue_tile<KIND, BN, DX>(p, tbase0 + mh * NACCW, (int64_t(mt) * MH + mh) * BM + row, nt,
+                                      nullptr, 16 * grp, CSTEP);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -1493,11 +1505,11 @@ int launch_bn(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, c
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_tc");
 }
 
-template <int KIND, int BN, bool RES, bool DX>
+template <int KIND, int BN, bool RES, bool DX, int MH = 1>
 int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
                    const CUtensorMap& mP, const ConvArgs& a, const RowArgs& h, size_t smem,
                    cudaStream_t st) {
-  auto kern = k_conv_rows<KIND, BN, RES, DX>;
+  auto kern = k_conv_rows<KIND, BN, RES, DX, MH>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1676,7 +1688,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     RowArgs rz;
     rz.row_bytes = hw * ROW_BYTES;
     rz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
-    const int b_tile = a.bn * ROW_BYTES;
+    int b_tile = a.bn * ROW_BYTES;
     const int w_bytes = 9 * a.cblocks * b_tile;
     rz.o_bytes = pred ? 0 : BM * std::max(a.bn, ROW_BYTES / (KIND == 0 ? 2 : 4)) * (KIND == 0 ? 2 : 4);
     rz.p_bytes = (pool && rz.o_bytes) ? rz.o_bytes / 4 : 0;
@@ -1691,6 +1703,25 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       rz.sb = std::min(8, (budget - rz.sa * rz.a_bytes) / (3 * b_tile));
     } else {
       rz.sa = rz.sb = std::min(8, budget / (rz.a_bytes + 3 * b_tile));
+    }
+    // streamed-weight dx layers (dec1.deconv1, dec2.deconv1): two M blocks per
+    // work tile share each weight stage (half the L2 weight traffic per
+    // pixel; at 16x16 the tile is the whole map)
+    const bool two = dx && !res && KIND == 0 && a.bn <= 128 && L.cout_pad % 64 == 0 &&
+                     rz.o_bytes && !rz.p_bytes && getenv("DRCB_NO_MH2") == nullptr;
+    if (two) {
+      a.bn = 64;  // two M blocks x 3 dx accumulators of 64 columns = 384 TMEM columns
+      a.num_n_tiles = L.cout_pad / 64;
+      b_tile = 64 * ROW_BYTES;
+      rz.o_bytes = BM * 64 * 2;
+      a.rows_per_tile = 2 * BM / hw;
+      a.tiles_per_map = hw * hw / (2 * BM);
+      a.num_m_tiles = int(nmaps * a.tiles_per_map);
+      rz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
+      rz.o_bytes *= 2;
+      const int bud2 = 216 * 1024 - 2 * rz.o_bytes;
+      rz.sa = 2;
+      rz.sb = std::min(8, (bud2 - rz.sa * rz.a_bytes) / (3 * b_tile));
     }
     if (rz.sa >= 2 && (res || rz.sb >= 2)) {
       rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, hw, a.rows_per_tile + 2, 1);
@@ -1711,6 +1742,8 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       size_t smem = 1024 + size_t(res ? w_bytes : 0) + size_t(rz.sa) * rz.a_bytes +
                     size_t(res ? 0 : rz.sb * 3 * b_tile) + 2 * size_t(rz.o_bytes) +
                     2 * size_t(rz.p_bytes) + 512;
+      if constexpr (KIND == 0)
+        if (two) return launch_rows_bn<KIND, 64, false, true, 2>(mA, mB, mO, mP, a, rz, smem, st);
       return dx ? launch_rows<KIND, true>(mA, mB, mO, mP, a, rz, res, smem, st)
                 : launch_rows<KIND, false>(mA, mB, mO, mP, a, rz, res, smem, st);
     }
