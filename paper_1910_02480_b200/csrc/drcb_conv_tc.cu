@@ -1573,7 +1573,11 @@ int n_tile(int cout_pad, int cap) {
 // dx-in-N vs halo for a row-tile layer (measured on B200)
 bool rows_use_dx(const ConvLayer& L, int kind) {
   (void)kind;
-  return L.hw == 32 || L.cin_pad >= 256;
+  const bool pooled = L.name.rfind("enc", 0) == 0;  // encoder convs feed a max-pool
+  // 16x16: dx (with two-block tiles) wins once the streamed weights dominate
+  // (cin >= 128) unless the epilogue also pools (dec2.deconv2: 289 vs 302 us;
+  // enc2.conv1: halo 178 vs 196 us; enc2.conv2 + pool: halo 302 vs 318 us)
+  return L.hw == 32 || L.cin_pad >= 256 || (L.hw == 16 && L.cin_pad >= 128 && !pooled);
 }
 
 // enc1.conv1 through k_conv_in8 (input: 8-channel NHWC, out: BN + LeakyReLU)
