@@ -77,6 +77,13 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        """Spawn the sampler and wait for its first row: nvidia-smi's start-up
+        stalls the GPU for ~0.1 s, which must not land in the timed region
+        (measured: a 200 ms first step when it did)."""
+        self.t_from = None
+        if os.environ.get("BENCH_NO_SMI"):  # A/B switch for the sampler's own cost
+            self.proc = None
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
@@ -84,12 +91,19 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while len(self.rows) < 2 and time.time() - t0 < 10:
+                time.sleep(0.05)
         except Exception:
             self.proc = None
 
+    def mark(self):
+        """Only rows read after this call count (the timed region)."""
+        self.t_from = time.time()
+
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
 
     def stop(self):
         if self.proc is None:
@@ -99,7 +113,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        rows = [r for r in self.rows if len(r) >= 8]
+        rows = [r for t, r in self.rows if len(r) >= 8 and (self.t_from is None or t >= self.t_from)]
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -294,41 +308,67 @@ def main():
         return render.render_drc_device(scene, cfg, net, camera=my_cams[i], out=outs[i], plan=plan,
                                         telemetry=tel)
 
+    frame_cpu = []
+
     def step(tel=False):
         stages = []
         ev = main.record_event()
         for s_ in streams:
             s_.wait_event(ev)
         for i in range(len(my_cams)):
+            t0 = time.time()
             with torch.cuda.stream(streams[i % len(streams)]):
                 _, t = frame(i, tel)
+            if os.environ.get("BENCH_DEBUG"):
+                frame_cpu.append(round(1e3 * (time.time() - t0), 1))
             if t:
                 stages.append(t["stage_us"])
         for s_ in streams:
             main.wait_stream(s_)
         return stages
 
+    clocks = ClockSampler(local)
+    clocks.start()  # before the warm-up: its start-up stall stays out of the timed region
+    # host-side housekeeping before the warm-up: the GPU must not sit idle
+    # between the warm-up and the timed steps (an idle gap lets the clocks
+    # drop and the first timed step ran up to 0.5 s instead of 80 ms)
+    import gc
+
+    gc.collect()
+    gc.disable()
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
 
     # ---- timed region (device-resident inputs)
-    clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
-    time.sleep(0.3)
+    clocks.mark()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = _lib.load().drcb_kernel_launches()
     ev0.record()
     stage_rows = []
+    dbg = os.environ.get("BENCH_DEBUG")
+    step_ev = []
+    cpu_t = []
     for _ in range(args.steps):
+        if dbg:
+            step_ev.append(torch.cuda.Event(enable_timing=True))
+            step_ev[-1].record()
+            cpu_t.append(time.time())
         step()
         flush.fill_(1.0)
     ev1.record()
+    if dbg:
+        cpu_t.append(time.time())
+        torch.cuda.synchronize()
+        step_ev.append(ev1)
+        print("per-step ms", [round(a.elapsed_time(b), 1) for a, b in zip(step_ev, step_ev[1:])],
+              "cpu enqueue ms", [round(1e3 * (b - a), 1) for a, b in zip(cpu_t, cpu_t[1:])],
+              "frame cpu ms (last 48)", frame_cpu[-48:], file=sys.stderr)
     launches_timed = int(_lib.load().drcb_kernel_launches() - l0)
     torch.cuda.synchronize()
+    gc.enable()
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
