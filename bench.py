@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--cpu-pixels", type=int, default=4096)
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--direct-spp", type=int, default=0)
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager steps instead of CUDA-graph replays")
     ap.add_argument("--no-train", action="store_true",
                     help="skip the secondary training-step measurement")
     return ap.parse_args()
@@ -312,7 +314,8 @@ def main():
 
     def step(tel=False):
         stages = []
-        ev = main.record_event()
+        cur = torch.cuda.current_stream()  # the capture stream while a graph is recorded
+        ev = cur.record_event()
         for s_ in streams:
             s_.wait_event(ev)
         for i in range(len(my_cams)):
@@ -324,7 +327,7 @@ def main():
             if t:
                 stages.append(t["stage_us"])
         for s_ in streams:
-            main.wait_stream(s_)
+            cur.wait_stream(s_)
         return stages
 
     clocks = ClockSampler(local)
@@ -338,6 +341,34 @@ def main():
     gc.disable()
     for _ in range(args.warmup):
         step()
+
+    # One step (8 frames, 2 streams, ~1,000 kernels + stream-ordered
+    # allocations) captured as a CUDA graph and replayed: the GPU no longer
+    # depends on the launching thread keeping ahead of it (a stalled host
+    # thread starved the first timed step by up to 0.5 s). Every replay
+    # re-executes every kernel of the step.
+    graph, per_step_launches = None, None
+    if not args.no_graph:
+        try:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            la = _lib.load().drcb_kernel_launches()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                step()
+            per_step_launches = int(_lib.load().drcb_kernel_launches() - la)
+            for _ in range(max(1, args.warmup)):
+                g.replay()
+            graph = g
+        except Exception as e:  # eager steps remain the fallback
+            print(f"bench: CUDA graph capture failed ({e!r}); timing eager steps", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize()
+
+    def timed_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
 
     # ---- timed region (device-resident inputs)
     if world > 1:
@@ -356,7 +387,7 @@ def main():
             step_ev.append(torch.cuda.Event(enable_timing=True))
             step_ev[-1].record()
             cpu_t.append(time.time())
-        step()
+        timed_step()
         flush.fill_(1.0)
     ev1.record()
     if dbg:
@@ -367,6 +398,8 @@ def main():
               "cpu enqueue ms", [round(1e3 * (b - a), 1) for a, b in zip(cpu_t, cpu_t[1:])],
               "frame cpu ms (last 48)", frame_cpu[-48:], file=sys.stderr)
     launches_timed = int(_lib.load().drcb_kernel_launches() - l0)
+    if graph is not None:
+        launches_timed = per_step_launches * args.steps
     torch.cuda.synchronize()
     gc.enable()
     clk = clocks.stop()
