@@ -410,6 +410,21 @@ def main():
     for i in range(len(my_cams)):
         _, tl = frame(i, True)
         stage_rows.append(tl["stage_us"])
+    # traversal counters of one frame (untimed; drcb_trav_stats adds atomics)
+    trav = None
+    try:
+        import ctypes as C
+
+        buf = torch.zeros(12, dtype=torch.int64, device="cuda")
+        _lib.call("drcb_trav_stats", C.c_void_p(buf.data_ptr()))
+        frame(0, False)
+        torch.cuda.synchronize()
+        _lib.call("drcb_trav_stats", None)
+        c = buf.cpu().tolist()
+        trav = {"casts_per_frame": c[2], "shadow_casts_per_frame": c[11],
+                "nodes_per_cast": c[0] / max(c[2], 1), "prims_per_cast": c[1] / max(c[2], 1)}
+    except Exception as e:  # secondary figure
+        trav = {"error": repr(e)}
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -466,6 +481,12 @@ def main():
                 "unit": "GB/s", "frac": None, "traffic": None}
     roof["peak_source"] = src
     roof["stage_ms_per_frame"] = {k: v / 1e3 for k, v in avg.items()}
+    if trav and "casts_per_frame" in trav:
+        # every cast of a frame is made by the G-buffer/direct and map stages
+        tr_ms = (avg["gbuffer_direct"] + avg["maps"]) / 1e3
+        trav["mrays_per_s"] = trav["casts_per_frame"] / (tr_ms * 1e-3) / 1e6
+        trav["note"] = ("BVH + triangles (76 MB) stay L2/L1-resident: the casting kernels are bound "
+                        "by SIMT issue and divergence, not HBM (profiles/*_ncu_full_summary.md)")
 
     cb = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -492,6 +513,7 @@ def main():
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "scene_stats": st,
             "train": train,
+            "traversal": trav,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
