@@ -406,7 +406,11 @@ def main():
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    # stage split from an untimed single-stream pass (CUDA events per stage)
+    # stage split from an untimed single-stream pass (CUDA events per stage),
+    # after one eager frame (the graph replays used the graph's own memory
+    # pool; the first eager frame refills the stream-ordered pool)
+    frame(0, False)
+    torch.cuda.synchronize()
     for i in range(len(my_cams)):
         _, tl = frame(i, True)
         stage_rows.append(tl["stage_us"])

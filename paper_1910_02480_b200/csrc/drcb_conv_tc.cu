@@ -88,6 +88,7 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -224,11 +225,6 @@ struct ConvArgs {
   float* pred;                            // (maps,3,32,32) fp32 when head
   float hw_w[3 * 16];                     // conv_out weights (3, 16)
   float hw_b[3];
-  // fused bilinear 2x upsample (tiles holding whole maps): when up_out is
-  // set, the epilogue writes up2x(output) into up_out's leading channel
-  // slice (up_ctot channels per pixel) instead of the low-res tensor
-  void* up_out;
-  int up_ctot;
 };
 
 template <int KIND, int BN, int STAGES>
@@ -237,14 +233,12 @@ struct Smem {
   static constexpr int A_BYTES = BM * ROW_BYTES;
   static constexpr int B_BYTES = BN * ROW_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGING = BM * 16 * 4;  // one 16-channel chunk, fp32, for the fused upsample
-  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + STAGING;
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 // Epilogue of one 128 x BN accumulator tile held in TMEM: tcgen05.ld, folded
 // BN + LeakyReLU, NHWC store into the destination slice; for the head layer
 // the fused 1x1 conv_out + ReLU writes fp32 NCHW predictions.
-__device__ __forceinline__ void epi_barrier() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // 16 accumulator columns [c0, c0+16) of this thread's pixel. DX: the tile
 // holds three accumulators P_dx (dx = -1, 0, +1 at column offsets 0, BN, 2BN)
@@ -298,7 +292,7 @@ __device__ __forceinline__ void bn_lrelu16(const float (&acc)[16], const float* 
 // may share one TMEM lane quarter)
 template <int KIND, int BN, bool DX = false>
 __device__ __forceinline__ void epilogue_tile(const ConvArgs& p, uint32_t tbase, int64_t m, int nt,
-                                              float* staging = nullptr, int cbeg = 0,
+                                              int cbeg = 0,
                                               int cstep = 16) {
   const int xpix = int(m & int64_t(p.hw - 1));  // hw is a power of two
   if (p.head) {
@@ -327,64 +321,6 @@ __device__ __forceinline__ void epilogue_tile(const ConvArgs& p, uint32_t tbase,
       acc_chunk<BN, DX>(tbase, c0, xpix, p.hw, acc);
       float v[16];
       bn_lrelu16(acc, p.ep_a + cg, p.ep_b + cg, p.slope, v);
-      if (staging) {
-        // fused bilinear 2x upsample of this 16-channel chunk: stage the
-        // stored-precision values of all 128 tile pixels (whole maps), then
-        // each thread emits 4 of the tile's 512 output pixels
-        const int row = int(m % BM);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if constexpr (KIND == 0) staging[j * BM + row] = __bfloat162float(__float2bfloat16_rn(v[j]));
-          else staging[j * BM + row] = round_tf32(v[j]);
-        }
-        epi_barrier();
-        const int hw = p.hw, ho = 2 * hw, per_map = ho * ho;
-        const int64_t tile_map0 = (m / BM) * (BM / (hw * hw));
-#pragma unroll 1
-        for (int r = 0; r < 4; ++r) {
-          const int oi = row + BM * r;
-          const int mp = oi / per_map, opos = oi % per_map;
-          const int oy = opos / ho, ox = opos % ho;
-          int r0, r1, c0i, c1i;
-          float fr, fc;
-          up_w(oy, hw, r0, r1, fr);
-          up_w(ox, hw, c0i, c1i, fc);
-          const float omr = 1.f - fr, omc = 1.f - fc;
-          const int sb = mp * hw * hw;
-          const int i00 = sb + r0 * hw + c0i, i10 = sb + r1 * hw + c0i;
-          const int i01 = sb + r0 * hw + c1i, i11 = sb + r1 * hw + c1i;
-          float o[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float* s = staging + j * BM;
-            float t0 = __fadd_rn(__fmul_rn(s[i00], omr), __fmul_rn(s[i10], fr));
-            float t1 = __fadd_rn(__fmul_rn(s[i01], omr), __fmul_rn(s[i11], fr));
-            o[j] = __fadd_rn(__fmul_rn(t0, omc), __fmul_rn(t1, fc));
-          }
-          const int64_t opix = (tile_map0 + mp) * per_map + opos;
-          if constexpr (KIND == 0) {
-            uint32_t pk[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(o[2 * j], o[2 * j + 1]);
-              pk[j] = *reinterpret_cast<uint32_t*>(&b2);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.up_out) +
-                                                  opix * p.up_ctot + cg);
-            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          } else {
-            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.up_out) +
-                                                    opix * p.up_ctot + cg);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              dst[j] = make_float4(round_tf32(o[4 * j]), round_tf32(o[4 * j + 1]),
-                                   round_tf32(o[4 * j + 2]), round_tf32(o[4 * j + 3]));
-          }
-        }
-        epi_barrier();
-        continue;
-      }
       if constexpr (KIND == 0) {
         uint32_t pk[8];
 #pragma unroll
@@ -423,7 +359,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
-  float* staging = reinterpret_cast<float*>(smem + STAGES * SM::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (warp == 0 && lane == 0) {
@@ -530,7 +465,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int64_t m = int64_t(mt) * BM + row;
       const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
-      epilogue_tile<KIND, BN>(p, tbase, m, nt, p.up_out ? staging : nullptr);
+      epilogue_tile<KIND, BN>(p, tbase, m, nt);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -599,6 +534,36 @@ __device__ __forceinline__ void epilogue_stage(const ConvArgs& p, uint32_t tbase
     }
   }
 }
+__device__ __forceinline__ void unpack8_bf16(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(b[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+// bilinear mix of four 16-B bf16 vectors (p00, p10, p01, p11) in packed bf16x2
+// arithmetic: t0 = p00*omr + p10*fr, t1 = p01*omr + p11*fr, v = t0*omc + t1*fc
+// (the weights 0, 0.25, 0.75, 1 are exact in bf16)
+__device__ __forceinline__ void up_mix_bf16x2(const uint4 (&q)[4], float omr, float fr, float omc,
+                                              float fc, uint32_t (&out)[4]) {
+  const __nv_bfloat162 wr0 = __float2bfloat162_rn(omr), wr1 = __float2bfloat162_rn(fr);
+  const __nv_bfloat162 wc0 = __float2bfloat162_rn(omc), wc1 = __float2bfloat162_rn(fc);
+  const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&q[0]);
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q[1]);
+  const __nv_bfloat162* c = reinterpret_cast<const __nv_bfloat162*>(&q[2]);
+  const __nv_bfloat162* d = reinterpret_cast<const __nv_bfloat162*>(&q[3]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 t0 = __hadd2(__hmul2(a[i], wr0), __hmul2(b[i], wr1));
+    const __nv_bfloat162 t1 = __hadd2(__hmul2(c[i], wr0), __hmul2(d[i], wr1));
+    const __nv_bfloat162 v = __hadd2(__hmul2(t0, wc0), __hmul2(t1, wc1));
+    out[i] = *reinterpret_cast<const uint32_t*>(&v);
+  }
+}
+
 // elementwise max of four 16-B vectors of stored values (bf16x8 / fp32x4)
 template <int KIND>
 __device__ __forceinline__ uint4 max4(uint4 a, uint4 b, uint4 c, uint4 d) {
@@ -636,6 +601,7 @@ struct RowArgs {
   int sa, sb;     // A / B ring depths
   int o_bytes;    // one output staging tile (BM * BN * elem); 0 = direct stores (head)
   int p_bytes;    // fused 2x2 max-pool staging tile (BM/4 * BN * elem); 0 = no pool
+  int up2;        // MH = 2 at 16x16 (a tile = one whole map): store up2x(out) at 32x32 instead
 };
 
 // Row-tile implicit GEMM for hw in {16, 32}: an M tile is BM/W whole image
@@ -680,7 +646,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   uint8_t* aring = smem + (RES ? n_wtiles * B_TILE : 0);
   uint8_t* bring = aring + h.sa * h.a_bytes;
   uint8_t* ostage = bring + (RES ? 0 : h.sb * B3);  // 2 x o_bytes, 1024-aligned
-  uint8_t* pstage = ostage + 2 * h.o_bytes;          // 2 x p_bytes
+  uint8_t* pstage = ostage + (h.up2 ? 3 : 2) * h.o_bytes;  // 2 x p_bytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(pstage + 2 * h.p_bytes);
   uint64_t* afull = bars;
   uint64_t* aempty = bars + 8;
@@ -856,7 +822,58 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase0 = tmem_base + (uint32_t(q * 32) << 16) + acc * MH * NACCW;
-      if (h.o_bytes) {
+      if (MH == 2 && h.up2) {
+        // The tile is one whole 16x16 map: stage it (stored, rounded values),
+        // then write its bilinear 2x upsample (cnn.py:159-174, the operation
+        // order of k_up_nhwc) straight into the 32x32 concat buffer in four
+        // 8-row chunks; the 16x16 output itself is never stored.
+        uint8_t* lowb = ostage;  // + two 8-row output chunk buffers (3 x o_bytes)
+        if (threadIdx.x == 64) bulk_wait_read0();
+        epi_bar_rt();
+#pragma unroll
+        for (int mh = 0; mh < MH; ++mh)
+          epilogue_stage<KIND, BN, DX, CSTEP>(p, tbase0 + mh * NACCW, (int64_t(mt) * MH + mh) * BM + row,
+                                              nt, lowb + mh * BM * ROW_BYTES, 16 * grp);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        epi_bar_rt();
+        const uint32_t L0 = smem_u32(lowb);
+        const int et = threadIdx.x - 64;
+        for (int chk = 0; chk < 4; ++chk) {
+          uint8_t* upb = ostage + (1 + (chk & 1)) * h.o_bytes;
+          const uint32_t U0 = smem_u32(upb);
+          if (chk > 1) {  // the store of chunk chk-2 has read this buffer
+            if (threadIdx.x == 64) bulk_wait_read1();
+            epi_bar_rt();
+          }
+          for (int e = et; e < 256 * 8; e += 32 * RT_EPI_WARPS) {
+            const int opx = e >> 3, j = e & 7;
+            const int oy = 8 * chk + (opx >> 5), ox = opx & 31;
+            int r0, r1, c0, c1;
+            float fr, fc;
+            up_w(oy, 16, r0, r1, fr);
+            up_w(ox, 16, c0, c1, fc);
+            const float omr = 1.f - fr, omc = 1.f - fc;
+            uint4 q[4];
+            const int rr[4] = {r0 * 16 + c0, r1 * 16 + c0, r0 * 16 + c1, r1 * 16 + c1};
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(q[w].x), "=r"(q[w].y), "=r"(q[w].z), "=r"(q[w].w)
+                           : "r"(L0 + rr[w] * ROW_BYTES + ((j ^ (rr[w] & 7)) << 4)));
+            uint32_t pk[4];
+            up_mix_bf16x2(q, omr, fr, omc, fc, pk);
+            sts128(U0 + opx * ROW_BYTES + ((j ^ (opx & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+          }
+          fence_proxy_async();
+          epi_bar_rt();
+          if (threadIdx.x == 64) {
+            tma_store_4d(&mapO, upb, nt * BN, 0, 8 * chk, mt);
+            bulk_commit();
+          }
+        }
+      } else if (h.o_bytes) {
         uint8_t* ot = ostage + obuf * h.o_bytes;
         if (threadIdx.x == 64) bulk_wait_read1();  // the store issued 2 tiles ago has read ot
         epi_bar_rt();
@@ -911,7 +928,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
 #pragma unroll
         for (int mh = 0; mh < MH; ++mh)
           epilogue_tile<KIND, BN, DX>(p, tbase0 + mh * NACCW, (int64_t(mt) * MH + mh) * BM + row, nt,
-                                      nullptr, 16 * grp, CSTEP);
+                                      16 * grp, CSTEP);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -1284,6 +1301,34 @@ __global__ void __launch_bounds__(256) k_up_nhwc(const T* __restrict__ in, T* __
   const int j = int(blk % HW_IN), i = int((blk / HW_IN) % HW_IN);
   const int64_t n = blk / (HW_IN * HW_IN);
   const T* b = in + n * HW_IN * HW_IN * C + g;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    // bf16: packed bf16x2 mixing (up_mix_bf16x2), the same arithmetic as the
+    // upsample fused into dec2.deconv2's epilogue
+    uint4 nbq[3][3];
+#pragma unroll
+    for (int dr = 0; dr < 3; ++dr) {
+      const int r = min(max(i + dr - 1, 0), HW_IN - 1);
+#pragma unroll
+      for (int dc = 0; dc < 3; ++dc) {
+        const int c = min(max(j + dc - 1, 0), HW_IN - 1);
+        nbq[dr][dc] = __ldg(reinterpret_cast<const uint4*>(b + (r * HW_IN + c) * C));
+      }
+    }
+    const float fr_even = i == 0 ? 0.f : 0.75f, fc_even = j == 0 ? 0.f : 0.75f;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const float fr = a ? 0.25f : fr_even;
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb) {
+        const float fc = bb ? 0.25f : fc_even;
+        const uint4 q[4] = {nbq[a][bb], nbq[a + 1][bb], nbq[a][bb + 1], nbq[a + 1][bb + 1]};
+        uint32_t o[4];
+        up_mix_bf16x2(q, 1.f - fr, fr, 1.f - fc, fc, o);
+        const int64_t px = (n * HO + 2 * i + a) * HO + 2 * j + bb;
+        *reinterpret_cast<uint4*>(out + px * c_tot + g) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  } else {
   // neighbourhood rows/cols i-1, i, i+1 (clamped; up_w only selects in-range ones)
   float nb[3][3][V];
 #pragma unroll
@@ -1316,6 +1361,7 @@ __global__ void __launch_bounds__(256) k_up_nhwc(const T* __restrict__ in, T* __
       const int64_t px = (n * HO + 2 * i + a) * HO + 2 * j + bb;
       *reinterpret_cast<uint4*>(out + px * c_tot + g) = pack<T>(v);
     }
+  }
   }
 }
 
@@ -1668,11 +1714,6 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
   a.ep_b = L.d_ep_b;
   a.slope = net.slope;
   a.out = out.p;
-  if (up) {
-    if (hw * hw > BM) return fail(DRCB_ECONTRACT, "fused upsample needs whole maps per tile");
-    a.up_out = up->p;
-    a.up_ctot = up->c;
-  }
   if (pred) {
     const ConvLayer& H = net.layers[16];
     a.head = 1;
@@ -1690,6 +1731,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     a.bn = n_tile(L.cout_pad, KIND == 0 ? 128 : 64);
     a.num_n_tiles = L.cout_pad / a.bn;
     RowArgs rz;
+    rz.up2 = 0;
     rz.row_bytes = hw * ROW_BYTES;
     rz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
     int b_tile = a.bn * ROW_BYTES;
@@ -1727,13 +1769,23 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       rz.sa = 2;
       rz.sb = std::min(8, (bud2 - rz.sa * rz.a_bytes) / (3 * b_tile));
     }
+    // 16x16 two-block tiles hold whole maps: the epilogue can write the 2x
+    // upsample of the output into the next level's concat buffer itself
+    const bool up_after = up && !(two && hw == 16);  // no whole-map tile: separate pass
+    if (up && !up_after) {
+      rz.up2 = 1;
+      rz.sb = 2;  // room for the low-res tile + two output chunk buffers
+    }
     if (rz.sa >= 2 && (res || rz.sb >= 2)) {
       rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, hw, a.rows_per_tile + 2, 1);
       if (rc) return rc;
       rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
       if (rc) return rc;
       CUtensorMap mO, mP;
-      if (rz.o_bytes) {
+      if (rz.up2) {
+        rc = encode_act(&mO, up->p, KIND, up->c, 2 * hw, nmaps, 2 * hw, 8, 1);
+        if (rc) return rc;
+      } else if (rz.o_bytes) {
         rc = encode_act(&mO, out.p, KIND, out.c, hw, nmaps, hw, a.rows_per_tile, 1);
         if (rc) return rc;
       }
@@ -1744,12 +1796,17 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
         mP = mO;
       }
       size_t smem = 1024 + size_t(res ? w_bytes : 0) + size_t(rz.sa) * rz.a_bytes +
-                    size_t(res ? 0 : rz.sb * 3 * b_tile) + 2 * size_t(rz.o_bytes) +
+                    size_t(res ? 0 : rz.sb * 3 * b_tile) + (rz.up2 ? 3 : 2) * size_t(rz.o_bytes) +
                     2 * size_t(rz.p_bytes) + 512;
       if constexpr (KIND == 0)
-        if (two) return launch_rows_bn<KIND, 64, false, true, 2>(mA, mB, mO, mP, a, rz, smem, st);
-      return dx ? launch_rows<KIND, true>(mA, mB, mO, mP, a, rz, res, smem, st)
+        if (two) rc = launch_rows_bn<KIND, 64, false, true, 2>(mA, mB, mO, mP, a, rz, smem, st);
+      if (!two || KIND != 0)
+        rc = dx ? launch_rows<KIND, true>(mA, mB, mO, mP, a, rz, res, smem, st)
                 : launch_rows<KIND, false>(mA, mB, mO, mP, a, rz, res, smem, st);
+      if (rc || !up_after) return rc;
+      using T = typename std::conditional<KIND == 0, __nv_bfloat16, float>::type;
+      return up_dispatch<T>(static_cast<const T*>(out.p), L.cout_pad, hw, static_cast<T*>(up->p),
+                            up->c, nmaps, st);
     }
     a.bn = n_tile(L.cout_pad, 256);
     a.num_n_tiles = L.cout_pad / a.bn;
@@ -1838,21 +1895,17 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
   rc |= run_layer<KIND>(net, Ls[5], B[7], B[8], 8 * k, np, st);   // s3 -> c3[8k:12k]
   pool(B[8], 8 * k, 4 * k, B[9]);
   rc |= run_layer<KIND>(net, Ls[6], B[9], B[10], 0, np, st);
-  // bott.conv2 and dec3.deconv2 tiles hold whole maps, so their epilogues
-  // can write the bilinear 2x upsample straight into the decoder concat
-  // buffers (DRCB_FUSED_UP=1). Measured on B200 at 4096 maps it is a wash
-  // (7.79 vs 7.71 ms per frame's network: the staged epilogue lengthens the
-  // tile tail more than the separate upsample pass costs), so it is opt-in.
-  const bool fuse7 = getenv("DRCB_FUSED_UP") != nullptr, fuse9 = fuse7;
-  rc |= run_layer<KIND>(net, Ls[7], B[10], B[11], 0, np, st, nullptr, fuse7 ? &B[8] : nullptr);
-  if (!fuse7) up(B[11], 8 * k, B[8]);
+  rc |= run_layer<KIND>(net, Ls[7], B[10], B[11], 0, np, st);
+  up(B[11], 8 * k, B[8]);
   // decoder
   rc |= run_layer<KIND>(net, Ls[8], B[8], B[7], 0, np, st);
-  rc |= run_layer<KIND>(net, Ls[9], B[7], B[12], 0, np, st, nullptr, fuse9 ? &B[5] : nullptr);
-  if (!fuse9) up(B[12], 4 * k, B[5]);
+  rc |= run_layer<KIND>(net, Ls[9], B[7], B[12], 0, np, st);
+  up(B[12], 4 * k, B[5]);
   rc |= run_layer<KIND>(net, Ls[10], B[5], B[4], 0, np, st);
-  rc |= run_layer<KIND>(net, Ls[11], B[4], B[13], 0, np, st);
-  up(B[13], 2 * k, B[2]);
+  // dec2.deconv2's whole-map tiles write up2x straight into c1 (k_conv_rows up2)
+  const bool fup16 = KIND == 0 && getenv("DRCB_NO_UP16") == nullptr;
+  rc |= run_layer<KIND>(net, Ls[11], B[4], B[13], 0, np, st, nullptr, fup16 ? &B[2] : nullptr);
+  if (!fup16) up(B[13], 2 * k, B[2]);
   rc |= run_layer<KIND>(net, Ls[12], B[2], B[1], 0, np, st);
   rc |= run_layer<KIND>(net, Ls[13], B[1], B[14], 0, np, st);
   rc |= run_layer<KIND>(net, Ls[14], B[14], B[15], 0, np, st);

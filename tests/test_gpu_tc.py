@@ -84,27 +84,16 @@ def test_tc_batch_sizes_and_padding():
 
 
 @pytest.mark.parametrize("mode", ["bf16", "tf32"])
-def test_fused_upsample_epilogue_bit_identical(mode, monkeypatch):
-    # DRCB_FUSED_UP: bott.conv2 / dec3.deconv2 epilogues write the 2x
-    # upsample directly; it must reproduce the separate upsample pass exactly
-    rng = np.random.default_rng(7)
-    x = rng.uniform(0, 1, (11, 7, 32, 32)).astype(np.float32)
-    net = cnn.random_network(64, 2)
-    plain = cnn.forward_batch(net, x, mode=mode)
-    monkeypatch.setenv("DRCB_FUSED_UP", "1")
-    fused = cnn.forward_batch(net, x, mode=mode)
-    assert np.array_equal(plain, fused)
-
-
-@pytest.mark.parametrize("mode", ["bf16", "tf32"])
-def test_fused_pool_bit_identical(mode, monkeypatch):
-    # the encoder pools fused into the skip convs' epilogues must reproduce
-    # the separate pool pass exactly (max of the stored, rounded values)
+@pytest.mark.parametrize("env", ["DRCB_NO_FUSED_POOL", "DRCB_NO_UP16"])
+def test_fused_pool_and_upsample_bit_identical(mode, env, monkeypatch):
+    # the encoder pools fused into the skip convs' epilogues and the 16 -> 32
+    # upsample fused into dec2.deconv2's whole-map epilogue must reproduce
+    # the separate passes exactly (they act on the stored, rounded values)
     rng = np.random.default_rng(8)
     x = rng.uniform(0, 1, (9, 7, 32, 32)).astype(np.float32)
     net = cnn.random_network(64, 2)
     fused = cnn.forward_batch(net, x, mode=mode)
-    monkeypatch.setenv("DRCB_NO_FUSED_POOL", "1")
+    monkeypatch.setenv(env, "1")
     plain = cnn.forward_batch(net, x, mode=mode)
     assert np.array_equal(plain, fused)
 
