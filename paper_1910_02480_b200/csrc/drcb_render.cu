@@ -17,9 +17,19 @@
 #include "drcb_internal.h"
 #include "drcb_trace.cuh"
 
+#ifndef DRCB_RENDER_PREC
+#define DRCB_RENDER_PREC 64
+#endif
+// kernels live in a per-build namespace: both objects define them
+#if DRCB_RENDER_PREC == 32
+#define DRCB_RENDER_NS render_f32
+#else
+#define DRCB_RENDER_NS render_f64
+#endif
+
 namespace drcb {
 
-namespace {
+namespace DRCB_RENDER_NS {
 
 constexpr int TPB = 128;
 
@@ -827,7 +837,8 @@ __global__ void __launch_bounds__(TPB) k_interp(DevScene S, int W, int H, DrcbGB
   st3(image + 3 * i, out);
 }
 
-}  // namespace
+}  // namespace DRCB_RENDER_NS
+using namespace DRCB_RENDER_NS;
 
 // ---------------------------------------------------------------------------
 // launchers
@@ -1036,23 +1047,38 @@ int launch_reference_map(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
                                           const int32_t*, const int32_t*, const R*, const R*,   \
                                           int64_t, const int*, int, const R*, R*, cudaStream_t);
 
+// One source, two objects (Makefile): the fp64 parity build with -fmad=false
+// (numpy's unfused arithmetic, bit-exact against the reference) and the fp32
+// build with the compiler's FMA contraction.
+#if DRCB_RENDER_PREC == 32
 INST(float)
-INST(double)
 template int launch_pt_frame<float>(const DevScene&, const DevCamera&, const DrcbRenderCfg&, int,
                                     int, float*, int64_t*, cudaStream_t);
-template int launch_pt_frame<double>(const DevScene&, const DevCamera&, const DrcbRenderCfg&, int,
-                                     int, double*, int64_t*, cudaStream_t);
 template int launch_reference_map<float>(const DevScene&, const DrcbRenderCfg&, const float*,
                                          const float*, uint64_t, int, float*, int64_t*,
                                          cudaStream_t);
+
+// the fp32 module's copy of the traversal-counter pointer
+int set_trav_stats_f32(unsigned long long* buf) {
+  cudaError_t e = cudaMemcpyToSymbol(g_trav_stats, &buf, sizeof(buf));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "drcb_trav_stats");
+}
+}  // namespace drcb
+#else
+INST(double)
+template int launch_pt_frame<double>(const DevScene&, const DevCamera&, const DrcbRenderCfg&, int,
+                                     int, double*, int64_t*, cudaStream_t);
 template int launch_reference_map<double>(const DevScene&, const DrcbRenderCfg&, const double*,
                                           const double*, uint64_t, int, double*, int64_t*,
                                           cudaStream_t);
-
+int set_trav_stats_f32(unsigned long long* buf);
 }  // namespace drcb
 
-// arm (buf != NULL, 3 x u64 device counters) or disarm the traversal counters
+// arm (buf != NULL, device u64[12] counters) or disarm the traversal counters
+// of both arithmetic builds
 extern "C" int drcb_trav_stats(unsigned long long* buf) {
   cudaError_t e = cudaMemcpyToSymbol(drcb::g_trav_stats, &buf, sizeof(buf));
-  return e == cudaSuccess ? 0 : drcb::cuda_fail(e, "drcb_trav_stats");
+  if (e != cudaSuccess) return drcb::cuda_fail(e, "drcb_trav_stats");
+  return drcb::set_trav_stats_f32(buf);
 }
+#endif

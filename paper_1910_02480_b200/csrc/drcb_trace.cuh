@@ -174,14 +174,16 @@ __device__ HitRec<R> traverse(const DevScene& S, V3<R> O, V3<R> D, R tmin, R tma
         ++n_nodes;
         const float4* nd = S.nodes + 4 * node;
         float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2), d = __ldg(nd + 3);
-        float tx0 = a.x * ix - oix, tx1 = a.y * ix - oix;
-        float ty0 = a.z * iy - oiy, ty1 = a.w * iy - oiy;
-        float tz0 = c.x * iz - oiz, tz1 = c.y * iz - oiz;
+        // explicit FMAs (this TU builds with -fmad=false for the fp64 parity
+        // path; one rounding instead of two stays inside the ROB slack)
+        float tx0 = __fmaf_rn(a.x, ix, -oix), tx1 = __fmaf_rn(a.y, ix, -oix);
+        float ty0 = __fmaf_rn(a.z, iy, -oiy), ty1 = __fmaf_rn(a.w, iy, -oiy);
+        float tz0 = __fmaf_rn(c.x, iz, -oiz), tz1 = __fmaf_rn(c.y, iz, -oiz);
         float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
         float f0 = fminf(fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fmaxf(tz0, tz1)) * ROB, tbest);
-        float sx0 = b.x * ix - oix, sx1 = b.y * ix - oix;
-        float sy0 = b.z * iy - oiy, sy1 = b.w * iy - oiy;
-        float sz0 = c.z * iz - oiz, sz1 = c.w * iz - oiz;
+        float sx0 = __fmaf_rn(b.x, ix, -oix), sx1 = __fmaf_rn(b.y, ix, -oix);
+        float sy0 = __fmaf_rn(b.z, iy, -oiy), sy1 = __fmaf_rn(b.w, iy, -oiy);
+        float sz0 = __fmaf_rn(c.z, iz, -oiz), sz1 = __fmaf_rn(c.w, iz, -oiz);
         float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), 0.0f));
         float f1 = fminf(fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fmaxf(sz0, sz1)) * ROB, tbest);
         bool h0 = n0 <= f0, h1 = n1 <= f1;
