@@ -231,9 +231,14 @@ __global__ void k_direct_reduce(DevCamera C, int spp, int tile, const R* __restr
 // path of the warp. The segment-0 cast doubles as the first-hit feature cast
 // (the reference casts it twice, hemimap.py:250 and segment 0).
 constexpr int MAP_TPB = 256;
+// CTAs per SM the path kernel's registers are sized for (fp32 build: 5,
+// measured 3.42 / 3.18 / 3.08 / 3.22 / 3.58 ms for 3 / 4 / 5 / 6 / 8)
+#ifndef MAP_CTAS
+#define MAP_CTAS 4
+#endif
 
 template <typename R>
-__global__ void __launch_bounds__(MAP_TPB, 4) k_map_paths(DevScene S, DrcbRenderCfg cfg,
+__global__ void __launch_bounds__(MAP_TPB, MAP_CTAS) k_map_paths(DevScene S, DrcbRenderCfg cfg,
                                                           const R* __restrict__ pos,
                                                           const R* __restrict__ nrm,
                                                           const uint64_t* __restrict__ keys,
