@@ -32,6 +32,9 @@ namespace drcb {
 namespace DRCB_RENDER_NS {
 
 constexpr int TPB = 128;
+#ifndef DIRECT_CTAS
+#define DIRECT_CTAS 8  // CTAs/SM the direct-pass kernel's registers are sized for
+#endif
 
 inline int nblocks(int64_t n, int tpb = TPB) { return int((n + tpb - 1) / tpb); }
 
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(TPB, 8) k_gbuffer(DevScene S, DevCamera C, Drc
 }
 
 template <typename R>
-__global__ void __launch_bounds__(TPB, 8) k_direct_samples(DevScene S, DevCamera C, DrcbRenderCfg cfg,
+__global__ void __launch_bounds__(TPB, DIRECT_CTAS) k_direct_samples(DevScene S, DevCamera C, DrcbRenderCfg cfg,
                                                          R* samples, int64_t* nonfinite) {
   const int spp = cfg.direct_spp;
   const int64_t npx = int64_t(C.W) * C.H;
