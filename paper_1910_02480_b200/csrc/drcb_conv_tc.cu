@@ -632,7 +632,9 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   constexpr int NACCW = DX ? 3 * BN : BN;              // TMEM columns per M block
   // MH = 2: a work tile is two M blocks (BM rows each) sharing every A and B
   // stage (half the weight traffic per pixel for streamed-weight layers)
-  constexpr int NACC = 2 * MH * NACCW <= 512 ? 2 : 1;  // TMEM accumulator buffers
+  // TMEM accumulator buffers: four when they fit (small-N layers, whose
+  // per-tile epilogue latency is long next to their MMA time), else two / one
+  constexpr int NACC = 4 * MH * NACCW <= 512 ? 4 : (2 * MH * NACCW <= 512 ? 2 : 1);
   static_assert(MH == 1 || (BN <= CEL && DX), "two-block tiles: one staging sub-tile, dx-in-N");
   constexpr int NSPLIT = NACCW <= 256 ? 1 : 2;
   constexpr int NMMA = NACCW / NSPLIT;
@@ -653,9 +655,13 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   uint64_t* bfull = bars + 16;
   uint64_t* bempty = bars + 24;
   uint64_t* tfull = bars + 32;
-  uint64_t* tempty = bars + 34;
-  uint64_t* wfull = bars + 36;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 37);
+  uint64_t* tempty = bars + 36;
+  uint64_t* wfull = bars + 40;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 41);
+  // the fused head epilogue (16 channels -> 3) is one 16-column chunk: the two
+  // epilogue warp groups take alternate tiles (accumulator buffer = group)
+  // instead of one group idling
+  const bool HEAD_SPLIT = p.head && h.o_bytes == 0 && NACC % 2 == 0 && RT_EPI_WARPS == 8;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (warp == 0 && lane == 0) {
     prefetch_map(&mapA);
@@ -668,9 +674,9 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
       mbar_init(&bfull[s], 1);
       mbar_init(&bempty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], RT_EPI_WARPS);
+      mbar_init(&tempty[a], HEAD_SPLIT ? RT_EPI_WARPS / 2 : RT_EPI_WARPS);
     }
     mbar_init(wfull, 1);
     fence_barrier_init();
@@ -819,6 +825,13 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       int nt = tile % p.num_n_tiles, mt = tile / p.num_n_tiles;
+      if (HEAD_SPLIT && (acc & 1) != grp) {
+        if (++acc == NACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase0 = tmem_base + (uint32_t(q * 32) << 16) + acc * MH * NACCW;
@@ -847,24 +860,39 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
             if (threadIdx.x == 64) bulk_wait_read1();
             epi_bar_rt();
           }
-          for (int e = et; e < 256 * 8; e += 32 * RT_EPI_WARPS) {
-            const int opx = e >> 3, j = e & 7;
-            const int oy = 8 * chk + (opx >> 5), ox = opx & 31;
-            int r0, r1, c0, c1;
-            float fr, fc;
-            up_w(oy, 16, r0, r1, fr);
-            up_w(ox, 16, c0, c1, fc);
-            const float omr = 1.f - fr, omc = 1.f - fc;
-            uint4 q[4];
-            const int rr[4] = {r0 * 16 + c0, r1 * 16 + c0, r0 * 16 + c1, r1 * 16 + c1};
+          // one item = a 2x2 output block from its 3x3 low-res neighbourhood
+          // (k_up_nhwc's blocking: 9 SMEM reads per 4 outputs, not 16)
+          for (int e = et; e < 64 * 8; e += 32 * RT_EPI_WARPS) {
+            const int j = e & 7, blk = e >> 3;
+            const int bi = 4 * chk + (blk >> 4), bj = blk & 15;  // low-res pixel
+            uint4 nbq[3][3];
 #pragma unroll
-            for (int w = 0; w < 4; ++w)
-              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                           : "=r"(q[w].x), "=r"(q[w].y), "=r"(q[w].z), "=r"(q[w].w)
-                           : "r"(L0 + rr[w] * ROW_BYTES + ((j ^ (rr[w] & 7)) << 4)));
-            uint32_t pk[4];
-            up_mix_bf16x2(q, omr, fr, omc, fc, pk);
-            sts128(U0 + opx * ROW_BYTES + ((j ^ (opx & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+            for (int dr = 0; dr < 3; ++dr) {
+              const int r = min(max(bi + dr - 1, 0), 15);
+#pragma unroll
+              for (int dc = 0; dc < 3; ++dc) {
+                const int c = min(max(bj + dc - 1, 0), 15);
+                const int rr = r * 16 + c;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(nbq[dr][dc].x), "=r"(nbq[dr][dc].y), "=r"(nbq[dr][dc].z),
+                               "=r"(nbq[dr][dc].w)
+                             : "r"(L0 + rr * ROW_BYTES + ((j ^ (rr & 7)) << 4)));
+              }
+            }
+            const float fr_even = bi == 0 ? 0.f : 0.75f, fc_even = bj == 0 ? 0.f : 0.75f;
+#pragma unroll
+            for (int a2 = 0; a2 < 2; ++a2) {
+              const float fr = a2 ? 0.25f : fr_even;
+#pragma unroll
+              for (int b2 = 0; b2 < 2; ++b2) {
+                const float fc = b2 ? 0.25f : fc_even;
+                const uint4 q[4] = {nbq[a2][b2], nbq[a2 + 1][b2], nbq[a2][b2 + 1], nbq[a2 + 1][b2 + 1]};
+                uint32_t pk[4];
+                up_mix_bf16x2(q, 1.f - fr, fr, 1.f - fc, fc, pk);
+                const int opx = ((2 * bi + a2) & 7) * 32 + 2 * bj + b2;  // pixel in the chunk
+                sts128(U0 + opx * ROW_BYTES + ((j ^ (opx & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+              }
+            }
           }
           fence_proxy_async();
           epi_bar_rt();
@@ -928,7 +956,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
 #pragma unroll
         for (int mh = 0; mh < MH; ++mh)
           epilogue_tile<KIND, BN, DX>(p, tbase0 + mh * NACCW, (int64_t(mt) * MH + mh) * BM + row, nt,
-                                      16 * grp, CSTEP);
+                                      HEAD_SPLIT ? 0 : 16 * grp, CSTEP);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -1769,6 +1797,28 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       rz.sa = 2;
       rz.sb = std::min(8, (bud2 - rz.sa * rz.a_bytes) / (3 * b_tile));
     }
+    // resident-weight 32x32 dx layers: two M blocks (8 rows) per work tile
+    // halve the per-tile fixed costs and the halo re-reads (10 rows loaded
+    // per 8 computed instead of 6 per 4)
+    // (head.deconv1 / head.deconv2; at BN = 64 the 40 KB A stages leave too
+    // few of them and the layer slows down)
+    bool two_res = !two && dx && res && KIND == 0 && a.bn <= 32 && hw == 32 && !rz.p_bytes &&
+                   !up && getenv("DRCB_NO_MH2") == nullptr;
+    if (two_res) {
+      const int a2 = (2 * BM / hw + 2) * hw * ROW_BYTES;
+      const int bud2 = 216 * 1024 - 4 * rz.o_bytes;
+      const int sa2 = std::min(8, (bud2 - w_bytes) / a2);
+      if (sa2 >= 2) {
+        a.rows_per_tile = 2 * BM / hw;
+        a.tiles_per_map = hw * hw / (2 * BM);
+        a.num_m_tiles = int(nmaps * a.tiles_per_map);
+        rz.a_bytes = a2;
+        rz.o_bytes *= 2;
+        rz.sa = sa2;
+      } else {
+        two_res = false;
+      }
+    }
     // 16x16 two-block tiles hold whole maps: the epilogue can write the 2x
     // upsample of the output into the next level's concat buffer itself
     const bool up_after = up && !(two && hw == 16);  // no whole-map tile: separate pass
@@ -1798,9 +1848,16 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       size_t smem = 1024 + size_t(res ? w_bytes : 0) + size_t(rz.sa) * rz.a_bytes +
                     size_t(res ? 0 : rz.sb * 3 * b_tile) + (rz.up2 ? 3 : 2) * size_t(rz.o_bytes) +
                     2 * size_t(rz.p_bytes) + 512;
-      if constexpr (KIND == 0)
+      if constexpr (KIND == 0) {
         if (two) rc = launch_rows_bn<KIND, 64, false, true, 2>(mA, mB, mO, mP, a, rz, smem, st);
-      if (!two || KIND != 0)
+        if (two_res) {
+          switch (a.bn) {
+            case 16: rc = launch_rows_bn<KIND, 16, true, true, 2>(mA, mB, mO, mP, a, rz, smem, st); break;
+            default: rc = launch_rows_bn<KIND, 32, true, true, 2>(mA, mB, mO, mP, a, rz, smem, st); break;
+          }
+        }
+      }
+      if ((!two && !two_res) || KIND != 0)
         rc = dx ? launch_rows<KIND, true>(mA, mB, mO, mP, a, rz, res, smem, st)
                 : launch_rows<KIND, false>(mA, mB, mO, mP, a, rz, res, smem, st);
       if (rc || !up_after) return rc;
