@@ -978,6 +978,280 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair row-tile conv (tcgen05.mma.cta_group::2, M = 256): the
+// streamed-weight dx layers (dec1.deconv1 @32x32, dec2.deconv1 @16x16).
+// A work tile is 256 output pixels; CTA rank r of the pair owns M rows
+// [128 r, 128 r + 128) (its A box, its TMEM accumulator, its epilogue and
+// store), and half of the N = 3 BN stacked dx weight rows ([1.5 BN r,
+// 1.5 BN (r + 1))). Per SM that is the single-CTA kernel's A traffic with half
+// its B traffic and B operand reads, and an accumulator of 3 BN columns per
+// CTA, so two of them fit in TMEM: the epilogue of tile i overlaps the MMAs
+// of tile i + 1 (the one-CTA MH = 2 kernel holds 6 BN columns per tile and
+// must drain before the next tile starts).
+//   both CTAs, warp 0: TMA producer (its own A box and B half; completion
+//                      is signalled on the LEADER's full barriers)
+//   leader, warp 1:    MMA issue (one thread), commits multicast to both
+//   both CTAs, 2-9:    epilogue (arrive on the leader's TMEM-empty barrier)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_4d_cg2(const CUtensorMap* map, uint32_t bar_cluster, void* dst,
+                                                int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* map, uint32_t bar_cluster, void* dst,
+                                                int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// arrive on the barrier at the same SMEM offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_cg2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
+               : "memory");
+}
+
+template <int BN, bool RES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RT_THREADS, 1)
+    k_conv_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                const __grid_constant__ CUtensorMap mapO, const __grid_constant__ ConvArgs p,
+                const __grid_constant__ RowArgs h) {
+  constexpr int KIND = 0;
+  constexpr int ELEM = 2;
+  constexpr int CEL = ROW_BYTES / ELEM;
+  static_assert(BN == CEL, "one 128-B staging sub-tile per pixel");
+  constexpr int N = 3 * BN;                  // stacked dx accumulators per CTA row
+  constexpr int BHALF = N / 2 * ROW_BYTES;   // this CTA's half of a (cb, dy) triple
+  constexpr int BCH = BN / 2;                // rows per B box
+  constexpr uint32_t TMEM_COLS = 2 * N <= 256 ? 256 : 512;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // RES: this CTA's weight half stays resident, [cb][dy] triples
+  uint8_t* wres = smem;
+  uint8_t* aring = smem + (RES ? p.cblocks * 3 * BHALF : 0);
+  uint8_t* bring = aring + h.sa * h.a_bytes;
+  uint8_t* ostage = bring + (RES ? 0 : h.sb * BHALF);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ostage + 2 * h.o_bytes);
+  uint64_t* afull = bars;
+  uint64_t* aempty = bars + 8;
+  uint64_t* bfull = bars + 16;
+  uint64_t* bempty = bars + 24;
+  uint64_t* tfull = bars + 32;
+  uint64_t* tempty = bars + 34;
+  uint64_t* wfull = bars + 36;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 37);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&mapA);
+    prefetch_map(&mapB);
+    for (int s = 0; s < h.sa; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < h.sb; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * RT_EPI_WARPS);  // both CTAs' epilogue warps
+    }
+    mbar_init(wfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = p.num_m_tiles;  // one N tile (cout = BN)
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+  const int rows_cta = BM / p.hw;
+  if (warp == 0) {
+    if (lane == 0) {
+      if (RES) {
+        if (leader) mbar_expect_tx(wfull, uint32_t(2 * p.cblocks * 3 * BHALF));
+        const uint32_t fw = mapa_rank(smem_u32(wfull), 0);
+        for (int cb = 0; cb < p.cblocks; ++cb)
+          for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              const int s = int(rank) * (N / 2) + j * BCH;
+              const int tap = dy * 3 + s / BN;
+              tma_load_2d_cg2(&mapB, fw, wres + (cb * 3 + dy) * BHALF + j * BCH * ROW_BYTES,
+                              (tap * p.cblocks + cb) * CEL, s % BN);
+            }
+      }
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        const int n0 = tile / p.tiles_per_map;
+        const int y0 = (tile % p.tiles_per_map) * p.rows_per_tile + int(rank) * rows_cta;
+        for (int cb = 0; cb < p.cblocks; ++cb) {
+          mbar_wait(&aempty[sa], pa ^ 1);
+          if (leader) mbar_expect_tx(&afull[sa], uint32_t(2 * h.a_bytes));
+          tma_load_4d_cg2(&mapA, mapa_rank(smem_u32(&afull[sa]), 0), aring + sa * h.a_bytes, cb * CEL, 0,
+                          y0 - 1, n0);
+          if (++sa == h.sa) {
+            sa = 0;
+            pa ^= 1;
+          }
+          if (!RES)
+          for (int dy = 0; dy < 3; ++dy) {
+            mbar_wait(&bempty[sb], pb ^ 1);
+            if (leader) mbar_expect_tx(&bfull[sb], uint32_t(2 * BHALF));
+            const uint32_t fb = mapa_rank(smem_u32(&bfull[sb]), 0);
+            uint8_t* dst = bring + sb * BHALF;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              const int s = int(rank) * (N / 2) + j * BCH;  // stacked row: dx * BN + co
+              const int tap = dy * 3 + s / BN;
+              tma_load_2d_cg2(&mapB, fb, dst + j * BCH * ROW_BYTES, (tap * p.cblocks + cb) * CEL, s % BN);
+            }
+            if (++sb == h.sb) {
+              sb = 0;
+              pb ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = make_idesc(KIND, 2 * BM, N);
+      if (RES) mbar_wait(wfull, 0);
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * N;
+        bool first = true;
+        for (int cb = 0; cb < p.cblocks; ++cb) {
+          mbar_wait(&afull[sa], pa);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(aring + sa * h.a_bytes);
+#pragma unroll 1
+          for (int dy = 0; dy < 3; ++dy) {
+            uint32_t bb;
+            if (RES) {
+              bb = smem_u32(wres + (cb * 3 + dy) * BHALF);
+            } else {
+              mbar_wait(&bfull[sb], pb);
+              tc_fence_after();
+              bb = smem_u32(bring + sb * BHALF);
+            }
+            const uint32_t aa = a0 + dy * h.row_bytes;
+#pragma unroll
+            for (int k = 0; k < ROW_BYTES / 32; ++k) {
+              tc_mma_cg2(tmem_d, sw128_desc(aa + 32 * k), sw128_desc(bb + 32 * k), idesc, first ? 0u : 1u);
+              first = false;
+            }
+            if (!RES) {
+              tc_commit_cg2(&bempty[sb]);
+              if (++sb == h.sb) {
+                sb = 0;
+                pb ^= 1;
+              }
+            }
+          }
+          tc_commit_cg2(&aempty[sa]);
+          if (++sa == h.sa) {
+            sa = 0;
+            pa ^= 1;
+          }
+        }
+        tc_commit_cg2(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int grp = (warp - 2) / 4;
+    constexpr int CSTEP = 16 * (RT_EPI_WARPS / 4);
+    int acc = 0, obuf = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs) {
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase0 = tmem_base + (uint32_t(q * 32) << 16) + acc * N;
+      uint8_t* ot = ostage + obuf * h.o_bytes;
+      if (threadIdx.x == 64) bulk_wait_read1();  // the store issued 2 tiles ago has read ot
+      epi_bar_rt();
+      epilogue_stage<KIND, BN, true, CSTEP>(p, tbase0, (int64_t(tile) * 2 + rank) * BM + row, 0, ot,
+                                            16 * grp);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_rank(smem_u32(&tempty[acc]), 0));
+      fence_proxy_async();
+      epi_bar_rt();
+      if (threadIdx.x == 64) {
+        const int n0 = tile / p.tiles_per_map;
+        const int y0 = (tile % p.tiles_per_map) * p.rows_per_tile + int(rank) * rows_cta;
+        tma_store_4d(&mapO, ot, p.cout_off, 0, y0, n0);
+        bulk_commit();
+      }
+      obuf ^= 1;
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (threadIdx.x == 64) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // enc1.conv1 (7 -> 64 channels @ 32x32) from the compact network input: NHWC
 // with 8 channels per pixel (7 + one zero), 16 B (bf16) / 32 B (tf32) per
 // pixel, 1/8 of a channel-padded layout's bytes. The im2col operand is built
@@ -1599,6 +1873,24 @@ int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorM
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_rows");
 }
 
+template <bool RES>
+int launch_pair64(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
+                  const ConvArgs& a, const RowArgs& h, size_t smem, cudaStream_t st) {
+  auto kern = k_conv_pair<64, RES>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int pairs = std::min(a.num_m_tiles, nsm / 2);
+  kern<<<2 * pairs, RT_THREADS, smem, st>>>(mA, mB, mO, a, h);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_pair");
+}
+
 template <int KIND, bool DX>
 int launch_rows(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
                 const CUtensorMap& mP, const ConvArgs& a, const RowArgs& h, bool res, size_t smem,
@@ -1796,6 +2088,46 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       const int bud2 = 216 * 1024 - 2 * rz.o_bytes;
       rz.sa = 2;
       rz.sb = std::min(8, (bud2 - rz.sa * rz.a_bytes) / (3 * b_tile));
+    }
+    // streamed-weight dx layers without a fused upsample: CTA-pair kernel
+    // (M = 256 across two SMs, double-buffered TMEM)
+    if (KIND == 0 && dx && !res && L.cout_pad == 64 && rz.o_bytes && !rz.p_bytes && !up &&
+        getenv("DRCB_NO_PAIR") == nullptr) {
+      RowArgs pz = rz;
+      ConvArgs pa = a;
+      pa.bn = 64;
+      pa.num_n_tiles = 1;
+      pa.rows_per_tile = 2 * BM / hw;           // per pair tile
+      pa.tiles_per_map = hw * hw / (2 * BM);
+      pa.num_m_tiles = int(nmaps * pa.tiles_per_map);
+      pz.a_bytes = (BM / hw + 2) * hw * ROW_BYTES;
+      pz.o_bytes = BM * 64 * 2;
+      pz.p_bytes = 0;
+      pz.up2 = 0;
+      const int bhalf = 96 * ROW_BYTES;
+      // this CTA's half of the weights resident when it fits next to three
+      // A stages (dec1.deconv1: 3 x 3 x 12 KB)
+      const int wbytes = a.cblocks * 3 * bhalf;
+      const bool pres = wbytes + 3 * pz.a_bytes + 2 * pz.o_bytes <= 216 * 1024 &&
+                        getenv("DRCB_PAIR_STREAM") == nullptr;
+      if (pres) {
+        pz.sb = 1;
+        pz.sa = std::min(8, (216 * 1024 - 2 * pz.o_bytes - wbytes) / pz.a_bytes);
+      } else {
+        pz.sa = 4;
+        pz.sb = std::min(8, (216 * 1024 - 2 * pz.o_bytes - pz.sa * pz.a_bytes) / bhalf);
+      }
+      CUtensorMap pA, pB, pO;
+      rc = encode_act(&pA, in.p, KIND, in.c, hw, nmaps, hw, BM / hw + 2, 1);
+      if (rc) return rc;
+      rc = encode_w(&pB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, 32);
+      if (rc) return rc;
+      rc = encode_act(&pO, out.p, KIND, out.c, hw, nmaps, hw, BM / hw, 1);
+      if (rc) return rc;
+      const size_t smem = 1024 + (pres ? size_t(wbytes) : size_t(pz.sb) * bhalf) + size_t(pz.sa) * pz.a_bytes +
+                          2 * size_t(pz.o_bytes) + 512;
+      return pres ? launch_pair64<true>(pA, pB, pO, pa, pz, smem, st)
+                  : launch_pair64<false>(pA, pB, pO, pa, pz, smem, st);
     }
     // resident-weight 32x32 dx layers: two M blocks (8 rows) per work tile
     // halve the per-tile fixed costs and the halo re-reads (10 rows loaded
