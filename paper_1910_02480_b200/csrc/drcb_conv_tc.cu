@@ -283,8 +283,37 @@ __device__ __forceinline__ void bn_lrelu16(const float (&acc)[16], const float* 
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       float x = acc[j + t] * aa[t] + bb[t];
-      v[j + t] = x >= 0.f ? x : slope * x;
+      v[j + t] = fmaxf(x, slope * x);  // LeakyReLU, 0 < slope < 1 (x >= 0 ? x : slope x)
     }
+  }
+}
+// the same with the folded vectors staged in SMEM (sa / sb: SMEM addresses
+// of the chunk's first channel)
+__device__ __forceinline__ void bn_lrelu16_s(const float (&acc)[16], uint32_t sa, uint32_t sb,
+                                             float slope, float (&v)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; j += 4) {
+    float aa[4], bb[4];
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(aa[0]), "=f"(aa[1]), "=f"(aa[2]), "=f"(aa[3])
+                 : "r"(sa + 4 * j));
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(bb[0]), "=f"(bb[1]), "=f"(bb[2]), "=f"(bb[3])
+                 : "r"(sb + 4 * j));
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      float x = acc[j + t] * aa[t] + bb[t];
+      v[j + t] = fmaxf(x, slope * x);
+    }
+  }
+}
+// folded BN vectors of channels [0, EP_MAX) staged in SMEM: a at sep, b at
+// sep + 4 * EP_MAX
+constexpr int EP_MAX = 256;
+__device__ __forceinline__ void stage_ep(const ConvArgs& p, int ncout, float* sep, int t0, int nthr) {
+  for (int i = t0; i < ncout; i += nthr) {
+    sep[i] = p.ep_a[i];
+    sep[EP_MAX + i] = p.ep_b[i];
   }
 }
 
@@ -492,7 +521,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // tensor store per sub-tile instead of 16-B scattered stores per thread.
 template <int KIND, int BN, bool DX, int CSTEP>
 __device__ __forceinline__ void epilogue_stage(const ConvArgs& p, uint32_t tbase, int64_t m, int nt,
-                                               uint8_t* ost, int cbeg) {
+                                               uint8_t* ost, int cbeg, uint32_t sep = 0) {
   constexpr int ELEM = KIND == 0 ? 2 : 4;
   constexpr int CEL = ROW_BYTES / ELEM;
   const int xpix = int(m & int64_t(p.hw - 1));  // hw is a power of two
@@ -513,7 +542,10 @@ __device__ __forceinline__ void epilogue_stage(const ConvArgs& p, uint32_t tbase
     float acc[16];
     acc_chunk<BN, DX>(tbase, c0, xpix, p.hw, acc);
     float v[16];
-    bn_lrelu16(acc, p.ep_a + cg, p.ep_b + cg, p.slope, v);
+    if (sep)
+      bn_lrelu16_s(acc, sep + 4 * cg, sep + 4 * (EP_MAX + cg), p.slope, v);
+    else
+      bn_lrelu16(acc, p.ep_a + cg, p.ep_b + cg, p.slope, v);
     const uint32_t sub = ost_s + (c0 / CEL) * (BM * ROW_BYTES) + r * ROW_BYTES;
     const int jb = (c0 % CEL) * ELEM / 16;
     if constexpr (KIND == 0) {
@@ -821,6 +853,14 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
     // RT_EPI_WARPS / 4 warps per TMEM lane quarter split the 16-column chunks
     const int grp = (warp - 2) / 4;
     constexpr int CSTEP = 16 * (RT_EPI_WARPS / 4);
+    // folded BN vectors in SMEM for the staged epilogue
+    float* s_ep = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);
+    const int ncout = p.num_n_tiles * BN;
+    const uint32_t sep = (h.o_bytes && ncout <= EP_MAX) ? smem_u32(s_ep) : 0u;
+    if (sep) {
+      stage_ep(p, ncout, s_ep, threadIdx.x - 64, 32 * RT_EPI_WARPS);
+      epi_bar_rt();
+    }
     int acc = 0, obuf = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -846,7 +886,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
 #pragma unroll
         for (int mh = 0; mh < MH; ++mh)
           epilogue_stage<KIND, BN, DX, CSTEP>(p, tbase0 + mh * NACCW, (int64_t(mt) * MH + mh) * BM + row,
-                                              nt, lowb + mh * BM * ROW_BYTES, 16 * grp);
+                                              nt, lowb + mh * BM * ROW_BYTES, 16 * grp, sep);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -908,7 +948,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
 #pragma unroll
         for (int mh = 0; mh < MH; ++mh)
           epilogue_stage<KIND, BN, DX, CSTEP>(p, tbase0 + mh * NACCW, (int64_t(mt) * MH + mh) * BM + row,
-                                              nt, ot + mh * BM * ROW_BYTES, 16 * grp);
+                                              nt, ot + mh * BM * ROW_BYTES, 16 * grp, sep);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -1212,6 +1252,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RT_THREADS, 1)
     const int row = q * 32 + lane;
     const int grp = (warp - 2) / 4;
     constexpr int CSTEP = 16 * (RT_EPI_WARPS / 4);
+    float* s_ep = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);
+    stage_ep(p, BN, s_ep, threadIdx.x - 64, 32 * RT_EPI_WARPS);
+    epi_bar_rt();
+    const uint32_t sep = smem_u32(s_ep);
     int acc = 0, obuf = 0;
     uint32_t acc_phase = 0;
     for (int tile = pair; tile < num_tiles; tile += npairs) {
@@ -1222,7 +1266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RT_THREADS, 1)
       if (threadIdx.x == 64) bulk_wait_read1();  // the store issued 2 tiles ago has read ot
       epi_bar_rt();
       epilogue_stage<KIND, BN, true, CSTEP>(p, tbase0, (int64_t(tile) * 2 + rank) * BM + row, 0, ot,
-                                            16 * grp);
+                                            16 * grp, sep);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_rank(smem_u32(&tempty[acc]), 0));
@@ -2125,7 +2169,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       rc = encode_act(&pO, out.p, KIND, out.c, hw, nmaps, hw, BM / hw, 1);
       if (rc) return rc;
       const size_t smem = 1024 + (pres ? size_t(wbytes) : size_t(pz.sb) * bhalf) + size_t(pz.sa) * pz.a_bytes +
-                          2 * size_t(pz.o_bytes) + 512;
+                          2 * size_t(pz.o_bytes) + 512 + 8 * EP_MAX;
       return pres ? launch_pair64<true>(pA, pB, pO, pa, pz, smem, st)
                   : launch_pair64<false>(pA, pB, pO, pa, pz, smem, st);
     }
@@ -2179,7 +2223,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       }
       size_t smem = 1024 + size_t(res ? w_bytes : 0) + size_t(rz.sa) * rz.a_bytes +
                     size_t(res ? 0 : rz.sb * 3 * b_tile) + (rz.up2 ? 3 : 2) * size_t(rz.o_bytes) +
-                    2 * size_t(rz.p_bytes) + 512;
+                    2 * size_t(rz.p_bytes) + 512 + 8 * EP_MAX;
       if constexpr (KIND == 0) {
         if (two) rc = launch_rows_bn<KIND, 64, false, true, 2>(mA, mB, mO, mP, a, rz, smem, st);
         if (two_res) {
