@@ -283,7 +283,7 @@ __device__ __forceinline__ void bn_lrelu16(const float (&acc)[16], const float* 
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       float x = acc[j + t] * aa[t] + bb[t];
-      v[j + t] = fmaxf(x, slope * x);  // LeakyReLU, 0 < slope < 1 (x >= 0 ? x : slope x)
+      v[j + t] = x >= 0.f ? x : slope * x;
     }
   }
 }
@@ -303,7 +303,7 @@ __device__ __forceinline__ void bn_lrelu16_s(const float (&acc)[16], uint32_t sa
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       float x = acc[j + t] * aa[t] + bb[t];
-      v[j + t] = fmaxf(x, slope * x);
+      v[j + t] = x >= 0.f ? x : slope * x;
     }
   }
 }
@@ -623,6 +623,10 @@ __device__ __forceinline__ uint4 max4(uint4 a, uint4 b, uint4 c, uint4 d) {
 
 constexpr int RT_EPI_WARPS = 8;
 constexpr int RT_THREADS = 64 + 32 * RT_EPI_WARPS;
+// the two epilogue warps of TMEM lane quarter q (32 pixel rows)
+__device__ __forceinline__ void quarter_bar(int q) {
+  asm volatile("bar.sync %0, 64;" ::"r"(8 + q) : "memory");
+}
 __device__ __forceinline__ void epi_bar_rt() {
   asm volatile("bar.sync 2, %0;" ::"r"(32 * RT_EPI_WARPS) : "memory");
 }
@@ -941,6 +945,33 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
             bulk_commit();
           }
         }
+      } else if (h.o_bytes && !h.p_bytes) {
+        // per lane quarter: its two warps stage their 32 pixel rows and one
+        // thread stores them (mapP: 32-pixel boxes); no CTA-wide barrier
+        uint8_t* ot = ostage + obuf * h.o_bytes;
+        const bool issuer = grp == 0 && lane == 0;
+        if (issuer) bulk_wait_read1();  // this quarter's store of 2 tiles ago has read ot
+        quarter_bar(q);
+#pragma unroll
+        for (int mh = 0; mh < MH; ++mh)
+          epilogue_stage<KIND, BN, DX, CSTEP>(p, tbase0 + mh * NACCW, (int64_t(mt) * MH + mh) * BM + row,
+                                              nt, ot + mh * BM * ROW_BYTES, 16 * grp, sep);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        fence_proxy_async();
+        quarter_bar(q);
+        if (issuer) {
+          const int n0 = mt / p.tiles_per_map;
+          const int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
+#pragma unroll
+          for (int mh = 0; mh < MH; ++mh)
+            for (int sb2 = 0; sb2 < (BN + CEL - 1) / CEL; ++sb2)
+              tma_store_4d(&mapP, ot + (sb2 * MH * BM + mh * BM + q * 32) * ROW_BYTES,
+                           p.cout_off + nt * BN + sb2 * CEL, 0, y0 + (mh * BM + q * 32) / p.hw, n0);
+          bulk_commit();
+        }
+        obuf ^= 1;
       } else if (h.o_bytes) {
         uint8_t* ot = ostage + obuf * h.o_bytes;
         if (threadIdx.x == 64) bulk_wait_read1();  // the store issued 2 tiles ago has read ot
@@ -1006,7 +1037,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
         acc_phase ^= 1;
       }
     }
-    if (threadIdx.x == 64 && h.o_bytes) bulk_wait_all();
+    if (lane == 0 && grp == 0 && h.o_bytes) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -2217,6 +2248,10 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       }
       if (rz.p_bytes) {
         rc = encode_act(&mP, pool->p, KIND, pool->c, hw / 2, nmaps, hw / 2, a.rows_per_tile / 2, 1);
+        if (rc) return rc;
+      } else if (rz.o_bytes && !rz.up2) {
+        // per-quarter stores: 32-pixel boxes
+        rc = encode_act(&mP, out.p, KIND, out.c, hw, nmaps, hw, 32 / hw, 1);
         if (rc) return rc;
       } else {
         mP = mO;
