@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
 #pragma unroll
           for (int mh = 0; mh < MH; ++mh)
             for (int sb2 = 0; sb2 < (BN + CEL - 1) / CEL; ++sb2)
-              tma_store_4d(&mapP, ot + (sb2 * MH * BM + mh * BM + q * 32) * ROW_BYTES,
+              tma_store_4d(&mapO, ot + (sb2 * MH * BM + mh * BM + q * 32) * ROW_BYTES,
                            p.cout_off + nt * BN + sb2 * CEL, 0, y0 + (mh * BM + q * 32) / p.hw, n0);
           bulk_commit();
         }
@@ -1294,19 +1294,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RT_THREADS, 1)
       tc_fence_after();
       const uint32_t tbase0 = tmem_base + (uint32_t(q * 32) << 16) + acc * N;
       uint8_t* ot = ostage + obuf * h.o_bytes;
-      if (threadIdx.x == 64) bulk_wait_read1();  // the store issued 2 tiles ago has read ot
-      epi_bar_rt();
+      const bool issuer = grp == 0 && lane == 0;  // per lane quarter (32 pixel rows)
+      if (issuer) bulk_wait_read1();  // this quarter's store of 2 tiles ago has read ot
+      quarter_bar(q);
       epilogue_stage<KIND, BN, true, CSTEP>(p, tbase0, (int64_t(tile) * 2 + rank) * BM + row, 0, ot,
                                             16 * grp, sep);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_rank(smem_u32(&tempty[acc]), 0));
       fence_proxy_async();
-      epi_bar_rt();
-      if (threadIdx.x == 64) {
+      quarter_bar(q);
+      if (issuer) {
         const int n0 = tile / p.tiles_per_map;
         const int y0 = (tile % p.tiles_per_map) * p.rows_per_tile + int(rank) * rows_cta;
-        tma_store_4d(&mapO, ot, p.cout_off, 0, y0, n0);
+        tma_store_4d(&mapO, ot + q * 32 * ROW_BYTES, p.cout_off, 0, y0 + q * 32 / p.hw, n0);
         bulk_commit();
       }
       obuf ^= 1;
@@ -1315,7 +1316,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RT_THREADS, 1)
         acc_phase ^= 1;
       }
     }
-    if (threadIdx.x == 64) bulk_wait_all();
+    if (lane == 0 && grp == 0) bulk_wait_all();
   }
   tc_fence_before();
   cluster_sync_all();
@@ -2197,7 +2198,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       if (rc) return rc;
       rc = encode_w(&pB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, 32);
       if (rc) return rc;
-      rc = encode_act(&pO, out.p, KIND, out.c, hw, nmaps, hw, BM / hw, 1);
+      rc = encode_act(&pO, out.p, KIND, out.c, hw, nmaps, hw, 32 / hw, 1);  // per-quarter boxes
       if (rc) return rc;
       const size_t smem = 1024 + (pres ? size_t(wbytes) : size_t(pz.sb) * bhalf) + size_t(pz.sa) * pz.a_bytes +
                           2 * size_t(pz.o_bytes) + 512 + 8 * EP_MAX;
@@ -2243,15 +2244,12 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
         rc = encode_act(&mO, up->p, KIND, up->c, 2 * hw, nmaps, 2 * hw, 8, 1);
         if (rc) return rc;
       } else if (rz.o_bytes) {
-        rc = encode_act(&mO, out.p, KIND, out.c, hw, nmaps, hw, a.rows_per_tile, 1);
+        // whole-tile boxes with the fused pool, else per-lane-quarter (32 px)
+        rc = encode_act(&mO, out.p, KIND, out.c, hw, nmaps, hw, rz.p_bytes ? a.rows_per_tile : 32 / hw, 1);
         if (rc) return rc;
       }
       if (rz.p_bytes) {
         rc = encode_act(&mP, pool->p, KIND, pool->c, hw / 2, nmaps, hw / 2, a.rows_per_tile / 2, 1);
-        if (rc) return rc;
-      } else if (rz.o_bytes && !rz.up2) {
-        // per-quarter stores: 32-pixel boxes
-        rc = encode_act(&mP, out.p, KIND, out.c, hw, nmaps, hw, 32 / hw, 1);
         if (rc) return rc;
       } else {
         mP = mO;
