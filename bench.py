@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--direct-spp", type=int, default=0)
     ap.add_argument("--no-graph", action="store_true",
                     help="time eager steps instead of CUDA-graph replays")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the secondary c4 (1080p) and tasks=16 frame rates")
     ap.add_argument("--no-train", action="store_true",
                     help="skip the secondary training-step measurement")
     return ap.parse_args()
@@ -187,36 +189,129 @@ def cfg_name():
     return _CFG_NAME[0]
 
 
-def train_throughput(cnn, batches=(64, 256), steps=5, warmup=2):
+def train_throughput(cnn, world=1, batches=(64, 256, 1024), global_batch=4096, steps=5, warmup=2):
     """Secondary figure (BASELINE config 5 is not the metric's config): the
     autoencoder's training step (train-mode BN, L1, Adam, fp32 master
-    weights) on synthetic (B,7,32,32) batches, bf16 tensor-core engine and the
-    fp32 parity engine, CUDA-event timed on device-resident batches."""
+    weights) on synthetic (B,7,32,32) batches, CUDA-event timed on
+    device-resident batches. Every rank runs it: with world > 1 the trainer
+    gets a libdrcb NCCL communicator (SyncBN statistics + the 7.8M-float
+    gradient all-reduce inside the step), the per-rank batch is
+    fixed (weak scaling; `global_batch` is split over the ranks: strong) and
+    the step time is the max over ranks. The fp32 parity engine is timed on a
+    single rank only."""
     import torch
+    import torch.distributed as dist
 
+    from paper_1910_02480_b200.dist import attach_nccl
     from paper_1910_02480_b200.trainer import DeviceTrainer
 
     net = cnn.random_network(64, seed=3)
-    out = {"model": "MapAutoencoder k=64 (7,32,32)->(3,32,32)", "unit": "samples/s"}
-    for mode in ("bf16", "fp32"):
-        tr = DeviceTrainer(net, lr=1e-4, mode=mode)
-        for b in batches if mode == "bf16" else batches[:1]:
-            g = torch.Generator(device="cuda").manual_seed(3)
-            x = torch.rand((b, 7, 32, 32), device="cuda", generator=g)
-            y = torch.rand((b, 3, 32, 32), device="cuda", generator=g)
-            for _ in range(warmup):
-                tr.step(x, y, want_loss=False)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record()
-            for _ in range(steps):
-                tr.step(x, y, want_loss=False)
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / steps
-            out[f"{mode}_b{b}"] = {"samples_per_s": b / (ms / 1e3), "ms_per_step": ms}
+    out = {"model": "MapAutoencoder k=64 (7,32,32)->(3,32,32)", "unit": "samples/s",
+           "world": world, "allreduce": "libdrcb NCCL (grads + SyncBN)" if world > 1 else None}
+    runs = [("bf16", b, f"bf16_b{b}") for b in batches]
+    if global_batch and global_batch % world == 0:
+        runs.append(("bf16", global_batch // world, f"bf16_global{global_batch}"))
+    if world == 1:
+        runs.append(("fp32", batches[0], f"fp32_b{batches[0]}"))
+    trainers = {}
+    for mode, b, key in runs:
+        if mode not in trainers:
+            tr = DeviceTrainer(net, lr=1e-4, mode=mode)
+            if world > 1:
+                attach_nccl(tr)
+            trainers[mode] = tr
+        tr = trainers[mode]
+        g = torch.Generator(device="cuda").manual_seed(3)
+        x = torch.rand((b, 7, 32, 32), device="cuda", generator=g)
+        y = torch.rand((b, 3, 32, 32), device="cuda", generator=g)
+        for _ in range(warmup):
+            tr.step(x, y, want_loss=False)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record()
+        for _ in range(steps):
+            tr.step(x, y, want_loss=False)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        out[key] = {"samples_per_s": b * world / (ms / 1e3), "ms_per_step": ms,
+                    "batch_per_rank": b, "global_batch": b * world}
+        del x, y
+    for tr in trainers.values():
         tr.close()
     return out
+
+
+def secondary_frames(config, tasks, frames, rank, world, steps=2, warmup=1, streams=2):
+    """Secondary frames/s figure for another BASELINE configuration (eager
+    multi-stream steps, CUDA-event timed, max over ranks, weak scaling: every
+    rank renders `frames` frames of its own). c4 = 1920x1080 with the 1.04M-
+    triangle scene, two lights and 4 jittered direct samples per pixel; c3
+    with tasks=16 = the paper's operating point (65,536 cache points/frame)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1910_02480_b200 import cnn, render, scenegen
+    from paper_1910_02480_b200.dist import frame_shard
+    from paper_1910_02480_b200.scene import device_scene, flatten
+
+    res, _, _, _, _, wseed = scenegen.CONFIGS[config]
+    spp = 4 if config == "c4" else 1
+    cfg = render.RenderConfig(direct_spp=spp, indirect_tasks=tasks, mis_samples=16,
+                              max_path_depth=8, rr_start=5, seed=0, precision=32, net_mode="bf16")
+    scene = scenegen.build_scene(config)
+    cams = scenegen.orbit_cameras(frames * world, res, seed=2)
+    mine = [cams[i] for i in frame_shard(len(cams), rank, world)]
+    net = cnn.random_network(64, seed=wseed)
+    t_build = time.perf_counter()
+    ds = device_scene(scene)
+    t_build = time.perf_counter() - t_build
+    plan = render.plan_points(res, cfg)
+    w, h = res
+    outs = [torch.empty((h, w, 3), dtype=torch.float32, device="cuda") for _ in mine]
+    sts = [torch.cuda.Stream() for _ in range(streams)]
+    cur = torch.cuda.current_stream()
+
+    def step():
+        ev = cur.record_event()
+        for s_ in sts:
+            s_.wait_event(ev)
+        for i, cam in enumerate(mine):
+            with torch.cuda.stream(sts[i % streams]):
+                render.render_drc_device(scene, cfg, net, camera=cam, out=outs[i], plan=plan,
+                                         telemetry=False)
+        for s_ in sts:
+            cur.wait_stream(s_)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    _, tel = render.render_drc_device(scene, cfg, net, camera=mine[0], out=outs[0], plan=plan)
+    st = ds.stats()
+    return {"workload": f"{config}: {w}x{h}, {len(mine)} frames/rank/step, indirect_tasks={tasks}, "
+                        f"direct_spp={spp}, bf16 U-Net, fp32 rays",
+            "frames_per_s": steps * len(mine) * world / (ms / 1e3), "ms_per_frame_per_rank":
+            ms / (steps * len(mine)), "cache_points_per_frame": int(len(plan[0])),
+            "scene_tris": int(len(flatten(scene)["tri_mat"])), "bvh_refs": st.get("n_refs"),
+            "scene_build_s": t_build,
+            "stage_ms_per_frame": {k: v / 1e3 for k, v in tel["stage_us"].items()}}
 
 
 def network_traffic(n_maps):
@@ -411,9 +506,11 @@ def main():
     # pool; the first eager frame refills the stream-ordered pool)
     frame(0, False)
     torch.cuda.synchronize()
+    sub_rows = []
     for i in range(len(my_cams)):
         _, tl = frame(i, True)
         stage_rows.append(tl["stage_us"])
+        sub_rows.append(tl["substage_us"])
     # traversal counters of one frame (untimed; drcb_trav_stats adds atomics)
     trav = None
     try:
@@ -485,6 +582,21 @@ def main():
                 "unit": "GB/s", "frac": None, "traffic": None}
     roof["peak_source"] = src
     roof["stage_ms_per_frame"] = {k: v / 1e3 for k, v in avg.items()}
+    # the HBM-bound elementwise stages against the measured HBM peak:
+    # algorithmic bytes = every distinct tensor read once + written once
+    sub = {k: float(np.mean([r[k] for r in sub_rows])) for k in sub_rows[0]}
+    rb = 4 if args.precision == 32 else 8
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    px_bytes = w * h * (2 + 4 * 3 * rb)  # found+escaped, throughput, normal, direct, image
+    pt_bytes = n_pts * (3 * 1024 * 4 + 13 * rb + 4 + 8 + 1)  # pred map, s_r, frame, wo, L; mat, key, live
+    roof["elementwise"] = {
+        "interp_composite": {"bytes_per_frame": px_bytes, "us": sub["interp"],
+                             "achieved_gbs": px_bytes / (sub["interp"] * 1e3),
+                             "frac_hbm": px_bytes / (sub["interp"] * 1e3) / hbm},
+        "shade": {"bytes_per_frame": pt_bytes, "us": sub["shade"],
+                  "achieved_gbs": pt_bytes / (sub["shade"] * 1e3),
+                  "frac_hbm": pt_bytes / (sub["shade"] * 1e3) / hbm},
+    }
     if trav and "casts_per_frame" in trav:
         # every cast of a frame is made by the G-buffer/direct and map stages
         tr_ms = (avg["gbuffer_direct"] + avg["maps"]) / 1e3
@@ -500,11 +612,19 @@ def main():
             cb = {"value": None, "error": repr(e)}
     launches = launches_timed
     train = None
-    if rank == 0 and not args.no_train:
+    if not args.no_train:
         try:
-            train = train_throughput(cnn)
+            train = train_throughput(cnn, world=max(world, 1))
         except Exception as e:  # secondary figure; never breaks the GPU line
             train = {"error": repr(e)}
+    secondary = {}
+    if not args.no_secondary:
+        for key, c_, tk in (("c4_1080p", "c4", 1), ("c3_tasks16", "c3", 16)):
+            try:
+                secondary[key] = secondary_frames(c_, tk, 8 if c_ == "c4" else 1, rank,
+                                                  max(world, 1))
+            except Exception as e:  # secondary figure; never breaks the GPU line
+                secondary[key] = {"error": repr(e)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
@@ -518,6 +638,7 @@ def main():
             "gpu_launches": launches, "scene_stats": st,
             "train": train,
             "traversal": trav,
+            "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -173,8 +173,11 @@ int drcb_interp_composite(const DrcbScene *scene, int32_t precision,
 /* Whole frame (drc/cache.py:377-470): gbuffer+direct, then the planned
  * cache points (host arrays px,py,keys in budget order, n_points), stacks,
  * network, shade, compaction, interpolation with final pass spacing r,
- * composite. image: (H*W,3) Real device. telemetry (host, 8 x int64):
- * entries, fallback_pixels(=0), nonfinite, n_points, ... */
+ * composite. image: (H*W,3) Real device. telemetry (host, 10 x int64, or
+ * NULL): entries, fallback_pixels(=0), nonfinite, n_points, then stage times
+ * in microseconds from CUDA events on `stream`: gbuffer+direct, maps (paths
+ * + stacks), network, shade+interp, and the split of the last one: shade +
+ * entry compaction, interpolation + composite. */
 int drcb_render_drc(const DrcbScene *scene, const DrcbNet *net,
                     const DrcbCamera *cam, const DrcbRenderCfg *cfg,
                     const int32_t *px_host, const int32_t *py_host,

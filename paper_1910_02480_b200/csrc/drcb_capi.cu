@@ -287,6 +287,8 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
     tel[5] = int64_t(1000.0 * E.ms(1, 2));
     tel[6] = int64_t(1000.0 * E.ms(2, 3));
     tel[7] = int64_t(1000.0 * E.ms(3, 5));
+    tel[8] = int64_t(1000.0 * E.ms(3, 4));  // shade + entry compaction
+    tel[9] = int64_t(1000.0 * E.ms(4, 5));  // interpolation + composite
   }
   return 0;
 }

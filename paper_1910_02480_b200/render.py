@@ -302,7 +302,7 @@ def render_drc_device(scene, config, net, camera=None, out=None, precision=None,
     dn = device_net(net) if len(px) else None
     if out is None:
         out = torch.empty((h, w, 3), dtype=dtype, device="cuda")
-    tel = (C.c_int64 * 8)() if (telemetry or entries) else None
+    tel = (C.c_int64 * 10)() if (telemetry or entries) else None
     t0 = time.time()
     args = (ds.handle, dn.handle if dn else None, C.byref(camera_struct(cam)), C.byref(cfg),
             px.ctypes.data_as(C.c_void_p), py.ctypes.data_as(C.c_void_p),
@@ -330,6 +330,7 @@ def render_drc_device(scene, config, net, camera=None, out=None, precision=None,
         "seconds": time.time() - t0,
         "stage_us": {"gbuffer_direct": int(tel[4]), "maps": int(tel[5]), "network": int(tel[6]),
                      "shade_interp": int(tel[7])},
+        "substage_us": {"shade": int(tel[8]), "interp": int(tel[9])},
     }
     telemetry["state"] = FrameState(int(tel[0]), int(tel[3]), pool)
     return out, telemetry
