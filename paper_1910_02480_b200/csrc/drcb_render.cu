@@ -605,86 +605,122 @@ __device__ __forceinline__ R texel_sin_theta(int v) {
   return sin(R(PI / 2.0) * (R(v) + R(0.5)) / R(MAP_RES));
 }
 
-// One block (256 threads) per cache point: the map's 2D distribution and the
-// MIS shading estimate (integrators.py:564-614).
+// One WARP per cache point (SHADE_WARPS maps per block): the map's 2D
+// distribution and the MIS shading estimate (integrators.py:564-614,
+// hemimap.py:156-197). Arithmetic and summation orders are those of the
+// reference's numpy calls: numpy's pairwise sum for the normaliser and the
+// row masses, sequential cumsums for the row and column CDFs. The column CDF
+// of a row is only needed for the rows that are sampled, so each map-sampling
+// lane rebuilds its own row's CDF on the fly (the same divisions and adds the
+// full table would hold) instead of storing 1,024 CDF values per map.
+constexpr int SHADE_PITCH = MAP_RES + 1;  // padded rows: lane v reads row v conflict-free
+
 template <typename R>
-__global__ void __launch_bounds__(256) k_shade(DevScene S, DrcbRenderCfg cfg,
-                                               const float* __restrict__ pred,
-                                               const R* __restrict__ s_r,
-                                               const R* __restrict__ frames,
-                                               const R* __restrict__ wo,
-                                               const int32_t* __restrict__ mats,
-                                               const uint64_t* __restrict__ keys,
-                                               const uint8_t* __restrict__ live, int64_t n,
-                                               R* Lout) {
-  __shared__ R prob[MAP_TEXELS];
-  __shared__ R colcdf[MAP_TEXELS];
-  __shared__ R rowcdf[MAP_RES];
-  __shared__ R rows[MAP_RES];
-  __shared__ R scratch[64];
-  __shared__ R contrib[64][3];
-  int64_t p = blockIdx.x;
+struct ShadeSmem {
+  R prob[MAP_RES * SHADE_PITCH];
+  R rows[MAP_RES];
+  R sin_v[MAP_RES];
+  R part[64];
+};
+
+template <typename R>
+constexpr int shade_warps() { return sizeof(R) == 4 ? 8 : 4; }
+
+template <typename R>
+__global__ void __launch_bounds__(32 * shade_warps<R>()) k_shade(
+    DevScene S, DrcbRenderCfg cfg, const float* __restrict__ pred, const R* __restrict__ s_r,
+    const R* __restrict__ frames, const R* __restrict__ wo, const int32_t* __restrict__ mats,
+    const uint64_t* __restrict__ keys, const uint8_t* __restrict__ live, int64_t n, R* Lout) {
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ ShadeSmem<R> sm_all[shade_warps<R>()];
+  const int lane = threadIdx.x & 31;
+  ShadeSmem<R>& sm = sm_all[threadIdx.x >> 5];
+  const int64_t p = int64_t(blockIdx.x) * shade_warps<R>() + (threadIdx.x >> 5);
   if (p >= n) return;
   if (live && !live[p]) {
-    if (threadIdx.x < 3) Lout[3 * p + threadIdx.x] = R(0);
+    if (lane < 3) Lout[3 * p + lane] = R(0);
     return;
   }
   const float* pd = pred + p * 3 * MAP_TEXELS;  // (3,32,32)
   const R scale = s_r[p];
-  // weights w = lum * sin(theta_v) + 1e-8 (build_map_distribution)
-  for (int t = threadIdx.x; t < MAP_TEXELS; t += blockDim.x) {
+  sm.sin_v[lane] = texel_sin_theta<R>(lane);
+  __syncwarp();
+  // weights w = lum * sin(theta_v) + 1e-8 (build_map_distribution); lane =
+  // column u, so the loads of a row are coalesced
+  for (int v = 0; v < MAP_RES; ++v) {
+    const int t = v * MAP_RES + lane;
     R r = R(pd[t]) * scale, g = R(pd[MAP_TEXELS + t]) * scale, b = R(pd[2 * MAP_TEXELS + t]) * scale;
     R lum = (r * R(LUMA_R) + g * R(LUMA_G)) + b * R(LUMA_B);
-    prob[t] = lum * texel_sin_theta<R>(t / MAP_RES) + R(1e-8);
+    sm.prob[v * SHADE_PITCH + lane] = lum * sm.sin_v[v] + R(1e-8);
   }
-  __syncthreads();
-  R wsum = pairwise1024(prob, scratch);
-  for (int t = threadIdx.x; t < MAP_TEXELS; t += blockDim.x) prob[t] = prob[t] / wsum;
-  __syncthreads();
-  if (threadIdx.x < MAP_RES) rows[threadIdx.x] = pairwise32(prob + MAP_RES * threadIdx.x);
-  __syncthreads();
-  if (threadIdx.x < MAP_RES) {
-    int v = threadIdx.x;
+  __syncwarp();
+  // numpy pairwise sum of the 1,024 weights: 8 blocks of 128, each 8
+  // strided accumulators of 16 terms, then the fixed trees
+  for (int h = 0; h < 2; ++h) {
+    const int t = lane + 32 * h, blk = t >> 3, j = t & 7;
     R acc = R(0);
-    for (int u = 0; u < MAP_RES; ++u) {
-      R c = prob[v * MAP_RES + u] / rows[v];
-      acc = (u == 0) ? c : acc + c;
-      colcdf[v * MAP_RES + u] = acc;
+    for (int k = 0; k < 16; ++k) {
+      const int f = 128 * blk + 8 * k + j;  // flat texel index
+      const R w = sm.prob[(f >> 5) * SHADE_PITCH + (f & 31)];
+      acc = (k == 0) ? w : acc + w;
     }
-    colcdf[v * MAP_RES + MAP_RES - 1] = R(1);
+    sm.part[t] = acc;
   }
-  if (threadIdx.x == 32) {
-    R acc = R(0);
-    for (int v = 0; v < MAP_RES; ++v) {
-      acc = (v == 0) ? rows[0] : acc + rows[v];
-      rowcdf[v] = acc;
-    }
-    rowcdf[MAP_RES - 1] = R(1);
+  __syncwarp();
+  R B[8];
+  for (int blk = 0; blk < 8; ++blk) {
+    const R* q = sm.part + 8 * blk;
+    B[blk] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
   }
-  __syncthreads();
+  const R wsum = ((B[0] + B[1]) + (B[2] + B[3])) + ((B[4] + B[5]) + (B[6] + B[7]));
+  __syncwarp();
+  for (int v = 0; v < MAP_RES; ++v) sm.prob[v * SHADE_PITCH + lane] = sm.prob[v * SHADE_PITCH + lane] / wsum;
+  __syncwarp();
+  {  // row masses: numpy pairwise sum of 32 (8 accumulators, fixed tree)
+    const R* a = sm.prob + lane * SHADE_PITCH;
+    R q[8];
+    for (int j = 0; j < 8; ++j) q[j] = a[j];
+    for (int k = 8; k < 32; k += 8)
+      for (int j = 0; j < 8; ++j) q[j] = q[j] + a[k + j];
+    sm.rows[lane] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+  }
+  __syncwarp();
   const R* F = frames + 9 * p;
   Frame<R> fr{ldr3(F), ldr3(F + 3), ldr3(F + 6)};
   V3<R> wo_local = fr.to_local(ldr3(wo + 3 * p));
-  int mat = mats[p];
+  const int mat = mats[p];
   const int n_map = cfg.mis_samples / 2;
   const int n_bsdf = cfg.mis_samples - n_map;
   const R omega0 = (R(2.0 * PI) / R(MAP_RES)) * (R(PI) / (R(2) * R(MAP_RES)));
-  int i = threadIdx.x;
   PathRng rng;
+  // map samples (lanes < n_map <= 32)
   V3<R> c = {R(0), R(0), R(0)};
-  if (i < n_map && i < 64) {
-    rng.init(cfg.seed, keys[p], uint64_t(i), cfg.sampler_kind, 1u);
+  if (lane < n_map) {
+    rng.init(cfg.seed, keys[p], uint64_t(lane), cfg.sampler_kind, 1u);
     R u1 = to_unit<R>(rng.sample(SHADE_DIM_BASE + 0));
     R u2 = to_unit<R>(rng.sample(SHADE_DIM_BASE + 1));
+    // row: searchsorted(cumsum(rows), u1, side="right") with cdf[-1] = 1
     int v = 0;
-    while (v < MAP_RES && rowcdf[v] <= u1) ++v;
+    R acc = sm.rows[0];
+    while (v < MAP_RES && (v == MAP_RES - 1 ? R(1) : acc) <= u1) {
+      ++v;
+      if (v < MAP_RES) acc = acc + sm.rows[v];
+    }
     v = min(v, MAP_RES - 1);
+    // column: count(cumsum(prob[v] / rows[v]) <= u2) with cdf[-1] = 1
+    const R* row = sm.prob + v * SHADE_PITCH;
+    const R rv = sm.rows[v];
     int u = 0;
-    for (int k = 0; k < MAP_RES; ++k) u += (colcdf[v * MAP_RES + k] <= u2);
+    R cacc = R(0);
+    for (int k = 0; k < MAP_RES; ++k) {
+      R cc = row[k] / rv;
+      cacc = (k == 0) ? cc : cacc + cc;
+      u += ((k == MAP_RES - 1 ? R(1) : cacc) <= u2);
+    }
     u = min(u, MAP_RES - 1);
-    R pr = prob[v * MAP_RES + u];
+    R pr = row[u];
     V3<R> dir = fr.to_world(texel_local<R>(u, v));
-    R pdf = pr / (omega0 * texel_sin_theta<R>(v));
+    R pdf = pr / (omega0 * sm.sin_v[v]);
     V3<R> radv = {R(pd[v * MAP_RES + u]) * scale, R(pd[MAP_TEXELS + v * MAP_RES + u]) * scale,
                   R(pd[2 * MAP_TEXELS + v * MAP_RES + u]) * scale};
     V3<R> li = fr.to_local(dir);
@@ -695,9 +731,11 @@ __global__ void __launch_bounds__(256) k_shade(DevScene S, DrcbRenderCfg cfg,
     R w = power_heuristic(pdf, pdf_b);
     R k = (w * cos_i) / pdf;
     c = (f * radv) * mk<R>(k, k, k);
-  } else if (i >= 32 && i - 32 < n_bsdf && i - 32 < 32) {
-    int j = i - 32;
-    rng.init(cfg.seed, keys[p], uint64_t(j), cfg.sampler_kind, 1u);
+  }
+  // BSDF samples (lanes < n_bsdf <= 32)
+  V3<R> cb = {R(0), R(0), R(0)};
+  if (lane < n_bsdf) {
+    rng.init(cfg.seed, keys[p], uint64_t(lane), cfg.sampler_kind, 1u);
     R u1 = to_unit<R>(rng.sample(SHADE_DIM_BASE + 2));
     R u2 = to_unit<R>(rng.sample(SHADE_DIM_BASE + 3));
     BsdfSample<R> bs = bsdf_sample(S, mat, wo_local, u1, u2, true);
@@ -708,25 +746,23 @@ __global__ void __launch_bounds__(256) k_shade(DevScene S, DrcbRenderCfg cfg,
     if (valid) {
       int q = v * MAP_RES + u;
       radv = {R(pd[q]) * scale, R(pd[MAP_TEXELS + q]) * scale, R(pd[2 * MAP_TEXELS + q]) * scale};
-      pdf_m = prob[q] / (omega0 * texel_sin_theta<R>(v));
+      pdf_m = sm.prob[v * SHADE_PITCH + u] / (omega0 * sm.sin_v[v]);
     }
     R cos_i = fmax(bs.li.z, R(0));
     R w = power_heuristic(bs.pdf, pdf_m);
     R k = (w * cos_i) / bs.pdf;
-    c = (bs.value * radv) * mk<R>(k, k, k);
+    cb = (bs.value * radv) * mk<R>(k, k, k);
   }
-  if (i < 64) {
-    contrib[i][0] = c.x;
-    contrib[i][1] = c.y;
-    contrib[i][2] = c.z;
+  // sequential sums in sample order (lane 0 collects)
+  V3<R> sm_ = {R(0), R(0), R(0)}, sb = {R(0), R(0), R(0)};
+  for (int k = 0; k < 32; ++k) {
+    V3<R> a = {__shfl_sync(FULL, c.x, k), __shfl_sync(FULL, c.y, k), __shfl_sync(FULL, c.z, k)};
+    V3<R> b = {__shfl_sync(FULL, cb.x, k), __shfl_sync(FULL, cb.y, k), __shfl_sync(FULL, cb.z, k)};
+    if (k < n_map) sm_ = (k == 0) ? a : sm_ + a;
+    if (k < n_bsdf) sb = (k == 0) ? b : sb + b;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    V3<R> sm = {contrib[0][0], contrib[0][1], contrib[0][2]};
-    for (int k = 1; k < n_map; ++k) sm = sm + mk<R>(contrib[k][0], contrib[k][1], contrib[k][2]);
-    V3<R> sb = {contrib[32][0], contrib[32][1], contrib[32][2]};
-    for (int k = 1; k < n_bsdf; ++k) sb = sb + mk<R>(contrib[32 + k][0], contrib[32 + k][1], contrib[32 + k][2]);
-    V3<R> total = divs(sm, R(n_map));
+  if (lane == 0) {
+    V3<R> total = divs(sm_, R(n_map));
     total = total + divs(sb, R(n_bsdf));
     if (!all_finite(total)) total = {R(0), R(0), R(0)};
     st3(Lout + 3 * p, total);
@@ -772,6 +808,10 @@ __global__ void k_bucket_sort(const int* offsets, int nb, int* items) {
   }
 }
 
+// `items` is bucket-major and the buckets of a grid row are consecutive, so
+// the entries of buckets [bx0, bx1] of row yy are ONE contiguous range of
+// items: the gather loops run per bucket row, in exactly the bucket/entry
+// order of a per-bucket loop (same sums), without per-bucket loop overhead.
 template <typename R>
 __global__ void __launch_bounds__(TPB) k_interp(DevScene S, int W, int H, DrcbGBuffer gb,
                                                  const int32_t* __restrict__ epx,
@@ -782,62 +822,70 @@ __global__ void __launch_bounds__(TPB) k_interp(DevScene S, int W, int H, DrcbGB
                                                  int nbx, int nby, const int* __restrict__ off,
                                                  const int* __restrict__ items,
                                                  const R* __restrict__ direct, R* image) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= int64_t(W) * H) return;
-  int x = int(i % W), y = int(i / W);
+  // a block is a 16 x (TPB/16) pixel tile inside one bucket column: a warp's
+  // 16x2 pixels share their bucket ranges (uniform loop bounds)
+  const int x = int(blockIdx.x) * BUCKET + int(threadIdx.x % BUCKET);
+  const int y = int(blockIdx.y) * (TPB / BUCKET) + int(threadIdx.x / BUCKET);
+  if (x >= W || y >= H) return;
+  const int64_t i = int64_t(y) * W + x;
   const int64_t m = m_dev ? int64_t(*m_dev) : m_cap;
   V3<R> layer = {R(0), R(0), R(0)};
   V3<R> thr = ldr3(static_cast<const R*>(gb.throughput) + 3 * i);
   if (gb.escaped[i] && S.has_env) layer = thr * ld3<R>(S.env);
   if (gb.found[i] && m > 0) {
-    int bx = x / BUCKET, by = y / BUCKET;
+    const int bx = x / BUCKET, by = y / BUCKET;
     // nearest entry by expanding Chebyshev rings of buckets
     long long best = LLONG_MAX;
-    int maxring = max(nbx, nby);
+    const int maxring = max(nbx, nby);
+    auto scan = [&](int q0, int q1) {
+#pragma unroll 1
+      for (int q = q0; q < q1; ++q) {
+        const int e = items[q];
+        const long long dx = epx[e] - x, dy = epy[e] - y;
+        const long long d2 = dx * dx + dy * dy;
+        if (d2 < best) best = d2;
+      }
+    };
     for (int k = 0; k <= maxring; ++k) {
-      for (int yy = by - k; yy <= by + k; ++yy) {
-        if (yy < 0 || yy >= nby) continue;
-        for (int xx = bx - k; xx <= bx + k; ++xx) {
-          if (xx < 0 || xx >= nbx) continue;
-          if (max(abs(yy - by), abs(xx - bx)) != k) continue;
-          int b = yy * nbx + xx;
-          for (int q = off[b]; q < off[b + 1]; ++q) {
-            int e = items[q];
-            long long dx = epx[e] - x, dy = epy[e] - y;
-            long long d2 = dx * dx + dy * dy;
-            if (d2 < best) best = d2;
-          }
+      const int xa = max(bx - k, 0), xb = min(bx + k, nbx - 1);
+      for (int yy = max(by - k, 0); yy <= min(by + k, nby - 1); ++yy) {
+        const int row = yy * nbx;
+        if (yy == by - k || yy == by + k) {
+          scan(off[row + xa], off[row + xb + 1]);  // a whole ring row
+        } else {
+          if (bx - k >= 0) scan(off[row + bx - k], off[row + bx - k + 1]);
+          if (k > 0 && bx + k < nbx) scan(off[row + bx + k], off[row + bx + k + 1]);
         }
       }
-      long long lim = (long long)k * BUCKET + 1;
+      const long long lim = (long long)k * BUCKET + 1;
       if (best != LLONG_MAX && best <= lim * lim) break;
     }
-    R d1 = sqrt(R(best));
-    R r_eff = fmax(R(r), R(1.5) * d1);
-    R rad = R(2) * r_eff;
-    R rad2 = rad * rad;
-    V3<R> npx = ldr3(static_cast<const R*>(gb.normal) + 3 * i);
-    int reach = int(ceil(double(rad))) + 1;
-    int bx0 = max(0, (x - reach) / BUCKET), bx1 = min(nbx - 1, (x + reach) / BUCKET);
-    int by0 = max(0, (y - reach) / BUCKET), by1 = min(nby - 1, (y + reach) / BUCKET);
+    const R d1 = sqrt(R(best));
+    const R r_eff = fmax(R(r), R(1.5) * d1);
+    const R rad = R(2) * r_eff;
+    const R rad2 = rad * rad;
+    const V3<R> npx = ldr3(static_cast<const R*>(gb.normal) + 3 * i);
+    const int reach = int(ceil(double(rad))) + 1;
+    const int bx0 = max(0, (x - reach) / BUCKET), bx1 = min(nbx - 1, (x + reach) / BUCKET);
+    const int by0 = max(0, (y - reach) / BUCKET), by1 = min(nby - 1, (y + reach) / BUCKET);
     V3<R> num = {R(0), R(0), R(0)};
     R den = R(0);
-    for (int yy = by0; yy <= by1; ++yy)
-      for (int xx = bx0; xx <= bx1; ++xx) {
-        int b = yy * nbx + xx;
-        for (int q = off[b]; q < off[b + 1]; ++q) {
-          int e = items[q];
-          R dx = R(epx[e] - x), dy = R(epy[e] - y);
-          R d2 = dx * dx + dy * dy;
-          if (!(d2 <= rad2)) continue;
-          R dist = sqrt(d2);
-          R w_p = fmax(R(0), R(1) - dist / r_eff);
-          R w_n = fmax(R(0), dot(ldr3(en + 3 * e), npx));
-          R wgt = (w_p * w_n + w_p) + R(1e-4);
-          num = num + wgt * ldr3(erad + 3 * e);
-          den = den + wgt;
-        }
+    for (int yy = by0; yy <= by1; ++yy) {
+      const int q1 = off[yy * nbx + bx1 + 1];
+#pragma unroll 1
+      for (int q = off[yy * nbx + bx0]; q < q1; ++q) {
+        const int e = items[q];
+        const R dx = R(epx[e] - x), dy = R(epy[e] - y);
+        const R d2 = dx * dx + dy * dy;
+        if (!(d2 <= rad2)) continue;
+        const R dist = sqrt(d2);
+        const R w_p = fmax(R(0), R(1) - dist / r_eff);
+        const R w_n = fmax(R(0), dot(ldr3(en + 3 * e), npx));
+        const R wgt = (w_p * w_n + w_p) + R(1e-4);
+        num = num + wgt * ldr3(erad + 3 * e);
+        den = den + wgt;
       }
+    }
     if (den > R(0)) layer = thr * divs(num, den);
   }
   V3<R> out = layer;
@@ -961,7 +1009,9 @@ int launch_shade(const DevScene& S, const DrcbRenderCfg& cfg, const float* pred,
   if (n <= 0) return 0;
   if (cfg.mis_samples < 2 || cfg.mis_samples > 64)
     return fail(DRCB_ECONFIG, "mis_samples must be in [2, 64]");
-  k_shade<R><<<int(n), 256, 0, st>>>(S, cfg, pred, s_r, frames, wo, mat, keys, live, n, L);
+  constexpr int wpb = shade_warps<R>();
+  k_shade<R><<<int((n + wpb - 1) / wpb), 32 * wpb, 0, st>>>(S, cfg, pred, s_r, frames, wo, mat,
+                                                          keys, live, n, L);
   LAUNCH_CHECK();
   return 0;
 }
@@ -996,7 +1046,8 @@ int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& 
     k_bucket_sort<<<nblocks(nb), TPB, 0, st>>>(offsets, nb, items);
     LAUNCH_CHECK();
   }
-  k_interp<R><<<nblocks(int64_t(W) * H), TPB, 0, st>>>(S, W, H, gb, e_px, e_py, e_n, e_rad, m, m_dev, r,
+  const dim3 igrid(unsigned(nbx), unsigned((H + TPB / BUCKET - 1) / (TPB / BUCKET)));
+  k_interp<R><<<igrid, TPB, 0, st>>>(S, W, H, gb, e_px, e_py, e_n, e_rad, m, m_dev, r,
                                                        nbx, nby, offsets, items, direct, image);
   LAUNCH_CHECK();
   DRCB_CUDA(cudaFreeAsync(buf, st));
