@@ -623,6 +623,9 @@ __device__ __forceinline__ uint4 max4(uint4 a, uint4 b, uint4 c, uint4 d) {
 
 constexpr int RT_EPI_WARPS = 8;
 constexpr int RT_THREADS = 64 + 32 * RT_EPI_WARPS;
+// k_conv_rows adds a pool warp (warp 10) for the fused 2x2 max-pool layers
+constexpr int RT_POOL_WARP = 2 + RT_EPI_WARPS;
+constexpr int ROWS_THREADS = RT_THREADS + 32;
 // the two epilogue warps of TMEM lane quarter q (32 pixel rows)
 __device__ __forceinline__ void quarter_bar(int q) {
   asm volatile("bar.sync %0, 64;" ::"r"(8 + q) : "memory");
@@ -638,6 +641,7 @@ struct RowArgs {
   int o_bytes;    // one output staging tile (BM * BN * elem); 0 = direct stores (head)
   int p_bytes;    // fused 2x2 max-pool staging tile (BM/4 * BN * elem); 0 = no pool
   int up2;        // MH = 2 at 16x16 (a tile = one whole map): store up2x(out) at 32x32 instead
+  int pool_cta;   // fused pool by the epilogue warps on whole staged tiles (A/B switch)
 };
 
 // Row-tile implicit GEMM for hw in {16, 32}: an M tile is BM/W whole image
@@ -656,8 +660,8 @@ struct RowArgs {
 // RES: the whole weight matrix stays resident in SMEM ([chunk][dy][dx]
 // tiles). 8 epilogue warps (two per TMEM lane quarter) stage the tile in
 // SMEM in the output map's swizzled layout; one thread TMA-stores it.
-template <int KIND, int BN, bool RES, bool DX, int MH>
-__global__ void __launch_bounds__(RT_THREADS, 1)
+template <int KIND, int BN, bool RES, bool DX, int MH, bool PW = false>
+__global__ void __launch_bounds__(PW ? ROWS_THREADS : RT_THREADS, 1)
     k_conv_rows(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapP,
                 const __grid_constant__ ConvArgs p, const __grid_constant__ RowArgs h) {
@@ -694,6 +698,12 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   uint64_t* tempty = bars + 36;
   uint64_t* wfull = bars + 40;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 41);
+  uint64_t* pfull = bars + 48;   // fused pool: the 4 lane quarters staged obuf
+  uint64_t* pempty = bars + 50;  // fused pool: the pool warp has read obuf
+  // fused 2x2 max-pool on the pool warp (single-block tiles, no up2): the
+  // epilogue keeps its per-quarter staging and stores
+  // (PW instantiations only: launched with the extra warp)
+  constexpr bool POOL_WARP = PW;
   // the fused head epilogue (16 channels -> 3) is one 16-column chunk: the two
   // epilogue warp groups take alternate tiles (accumulator buffer = group)
   // instead of one group idling
@@ -715,6 +725,10 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
       mbar_init(&tempty[a], HEAD_SPLIT ? RT_EPI_WARPS / 2 : RT_EPI_WARPS);
     }
     mbar_init(wfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&pfull[b], 4);
+      mbar_init(&pempty[b], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -851,6 +865,57 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
         }
       }
     }
+  } else if (warp == RT_POOL_WARP) {
+    if constexpr (PW) {
+      // fused 2x2 max-pool (cnn.py:152-156) of each staged, already rounded
+      // tile once its four lane quarters have staged it: BM/4 pooled pixels x
+      // BN channels in the same swizzled layout, TMA-stored to the next level
+      const int hw = p.hw, ho = hw >> 1, lho = __ffs(ho) - 1;
+      constexpr int PPR = ROW_BYTES / 16;  // 16-B pieces per sub-tile row
+      int obuf = 0, kt = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int nt = tile % p.num_n_tiles, mt = tile / p.num_n_tiles;
+        const int n0 = mt / p.tiles_per_map;
+        const int y0 = (mt % p.tiles_per_map) * p.rows_per_tile;
+        mbar_wait(&pfull[obuf], (kt >> 1) & 1);
+        uint8_t* ot = ostage + obuf * h.o_bytes;
+        uint8_t* pt = pstage + obuf * h.p_bytes;
+        if (lane == 0) bulk_wait_read1();  // the pool store of 2 tiles ago has read pt
+        __syncwarp();
+        constexpr int PIECES = BN * ELEM / 16;  // 16-B pieces per pooled pixel
+#pragma unroll
+        for (int it = 0; it < (BM / 4) * PIECES / 32; ++it) {
+          const int e = lane + 32 * it;
+          const int pr = e / PIECES, pc = e % PIECES;
+          const int sub = pc / PPR, jj = pc % PPR;
+          const int py = pr >> lho, px = pr & (ho - 1);  // ho is a power of two
+          const int r00 = (2 * py) * hw + 2 * px;
+          const uint32_t base = smem_u32(ot + sub * BM * ROW_BYTES);
+          uint4 v[4];
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const int rr = r00 + (w >> 1) * hw + (w & 1);
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v[w].x), "=r"(v[w].y), "=r"(v[w].z), "=r"(v[w].w)
+                         : "r"(base + rr * ROW_BYTES + ((jj ^ (rr & 7)) << 4)));
+          }
+          uint4 m4 = max4<KIND>(v[0], v[1], v[2], v[3]);
+          sts128(smem_u32(pt + sub * (BM / 4) * ROW_BYTES) + pr * ROW_BYTES + ((jj ^ (pr & 7)) << 4),
+                 m4.x, m4.y, m4.z, m4.w);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&pempty[obuf]);  // ot may be restaged
+          for (int sb2 = 0; sb2 < BN / CEL; ++sb2)
+            tma_store_4d(&mapP, pt + sb2 * (BM / 4) * ROW_BYTES, nt * BN + sb2 * CEL, 0, y0 >> 1, n0);
+          bulk_commit();
+        }
+        obuf ^= 1;
+        ++kt;
+      }
+      if (lane == 0) bulk_wait_all();
+    }
   } else {
     const int q = warp & 3;
     const int row = q * 32 + lane;
@@ -865,7 +930,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
       stage_ep(p, ncout, s_ep, threadIdx.x - 64, 32 * RT_EPI_WARPS);
       epi_bar_rt();
     }
-    int acc = 0, obuf = 0;
+    int acc = 0, obuf = 0, kt = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       int nt = tile % p.num_n_tiles, mt = tile / p.num_n_tiles;
@@ -945,12 +1010,16 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
             bulk_commit();
           }
         }
-      } else if (h.o_bytes && !h.p_bytes) {
+      } else if (h.o_bytes && (!h.p_bytes || POOL_WARP)) {
         // per lane quarter: its two warps stage their 32 pixel rows and one
-        // thread stores them (mapP: 32-pixel boxes); no CTA-wide barrier
+        // thread stores them (mapO: 32-pixel boxes); no CTA-wide barrier
         uint8_t* ot = ostage + obuf * h.o_bytes;
         const bool issuer = grp == 0 && lane == 0;
-        if (issuer) bulk_wait_read1();  // this quarter's store of 2 tiles ago has read ot
+        if (issuer) {
+          bulk_wait_read1();  // this quarter's store of 2 tiles ago has read ot
+          // and the pool warp has read it (its use before this one)
+          if (POOL_WARP && kt >= 2) mbar_wait(&pempty[obuf], ((kt >> 1) - 1) & 1);
+        }
         quarter_bar(q);
 #pragma unroll
         for (int mh = 0; mh < MH; ++mh)
@@ -970,8 +1039,10 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
               tma_store_4d(&mapO, ot + (sb2 * MH * BM + mh * BM + q * 32) * ROW_BYTES,
                            p.cout_off + nt * BN + sb2 * CEL, 0, y0 + (mh * BM + q * 32) / p.hw, n0);
           bulk_commit();
+          if (POOL_WARP) mbar_arrive(&pfull[obuf]);  // this quarter's rows are staged
         }
         obuf ^= 1;
+        ++kt;
       } else if (h.o_bytes) {
         uint8_t* ot = ostage + obuf * h.o_bytes;
         if (threadIdx.x == 64) bulk_wait_read1();  // the store issued 2 tiles ago has read ot
@@ -1929,11 +2000,11 @@ int launch_bn(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, c
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_tc");
 }
 
-template <int KIND, int BN, bool RES, bool DX, int MH = 1>
+template <int KIND, int BN, bool RES, bool DX, int MH = 1, bool PW = false>
 int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
                    const CUtensorMap& mP, const ConvArgs& a, const RowArgs& h, size_t smem,
                    cudaStream_t st) {
-  auto kern = k_conv_rows<KIND, BN, RES, DX, MH>;
+  auto kern = k_conv_rows<KIND, BN, RES, DX, MH, PW>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1943,7 +2014,7 @@ int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorM
   if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   int tiles = a.num_m_tiles * a.num_n_tiles;
   int grid = tiles < nsm ? tiles : nsm;
-  kern<<<grid, RT_THREADS, smem, st>>>(mA, mB, mO, mP, a, h);
+  kern<<<grid, PW ? ROWS_THREADS : RT_THREADS, smem, st>>>(mA, mB, mO, mP, a, h);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_rows");
@@ -1971,6 +2042,14 @@ template <int KIND, bool DX>
 int launch_rows(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
                 const CUtensorMap& mP, const ConvArgs& a, const RowArgs& h, bool res, size_t smem,
                 cudaStream_t st) {
+  // the fused-pool skip convs (enc1.conv2: resident dx, BN 64; enc2.conv2:
+  // streamed halo, BN 128) with the pool warp
+  if (h.o_bytes && h.p_bytes && !h.up2 && !h.pool_cta) {
+    if (DX && res && a.bn == 64) return launch_rows_bn<KIND, 64, true, DX, 1, true>(mA, mB, mO, mP, a, h, smem, st);
+    if (!DX && !res && a.bn == 128)
+      return launch_rows_bn<KIND, 128, false, DX, 1, true>(mA, mB, mO, mP, a, h, smem, st);
+    return fail(DRCB_ECONFIG, "fused pool: no pool-warp instantiation for this layer shape");
+  }
 #define ROWS_CASE(BNV)                                                                  \
   case BNV:                                                                             \
     return res ? launch_rows_bn<KIND, BNV, true, DX>(mA, mB, mO, mP, a, h, smem, st)    \
@@ -2128,6 +2207,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     a.num_n_tiles = L.cout_pad / a.bn;
     RowArgs rz;
     rz.up2 = 0;
+    rz.pool_cta = 0;
     rz.row_bytes = hw * ROW_BYTES;
     rz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
     int b_tile = a.bn * ROW_BYTES;
@@ -2234,6 +2314,13 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       rz.up2 = 1;
       rz.sb = 2;  // room for the low-res tile + two output chunk buffers
     }
+    // fused pools run on the kernel's pool warp (per-quarter output stores);
+    // DRCB_POOL_CTA: the CTA-wide staged-tile pool of the epilogue warps
+    const bool pool_cta = getenv("DRCB_POOL_CTA") != nullptr;
+    // pool-warp instantiations: enc1.conv2 (resident dx, BN 64) and enc2.conv2
+    // (streamed halo, BN 128); other shapes keep the CTA-wide pool
+    const bool pw_shape = (dx && res && a.bn == 64) || (!dx && !res && a.bn == 128);
+    rz.pool_cta = (pool_cta || !pw_shape) ? 1 : 0;
     if (rz.sa >= 2 && (res || rz.sb >= 2)) {
       rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, hw, a.rows_per_tile + 2, 1);
       if (rc) return rc;
@@ -2245,7 +2332,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
         if (rc) return rc;
       } else if (rz.o_bytes) {
         // whole-tile boxes with the fused pool, else per-lane-quarter (32 px)
-        rc = encode_act(&mO, out.p, KIND, out.c, hw, nmaps, hw, rz.p_bytes ? a.rows_per_tile : 32 / hw, 1);
+        rc = encode_act(&mO, out.p, KIND, out.c, hw, nmaps, hw, (rz.p_bytes && rz.pool_cta) ? a.rows_per_tile : 32 / hw, 1);
         if (rc) return rc;
       }
       if (rz.p_bytes) {
