@@ -1120,6 +1120,237 @@ __global__ void __launch_bounds__(PW ? ROWS_THREADS : RT_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// The decoder head fused (bf16): head.deconv1 (64 -> 32) + BN + LeakyReLU,
+// head.deconv2 (32 -> 16) + BN + LeakyReLU, conv_out (1x1, 16 -> 3) + ReLU,
+// with head.deconv1's output living only in SMEM: the 32x32 layer's 64-channel
+// padded output (537 MB per 4,096 maps) is neither written nor re-read.
+// A CTA walks whole maps, 8 items of 4 output rows each, in row order, so
+// every head.deconv1 row is computed once: item t computes rows 4t+1..4t+4
+// (one M block, dx taps stacked along N = 96) and reuses rows 4t-1, 4t from
+// item t-1; item 0 computes rows 0..7 (two blocks, rows 5..7 unused). The
+// six rows 4t-1..4t+4 that head.deconv2 (N = 48, K = the 32 real channels)
+// reads at dy offsets form A2[t & 1], written in the 128B-swizzled layout a
+// TMA load would produce; rows outside the map are zero (head.deconv2's
+// padding). A reused row stays in the registers of the warp that computed it
+// and is written into the next item's buffer with that item's rows. Same products, fp32 accumulation groups and bf16 rounding of the
+// intermediate as the two-kernel path (bit-identical, DRCB_NO_HEAD_FUSE).
+//   warp 0: TMA (weights once; per item one input box, two stages)
+//   warp 1: MMA: head.deconv1 of item i, then head.deconv2 of item i-1
+//   warps 2-9: head.deconv1 epilogue of item i (two warps per lane quarter,
+//              16 channels each), then the head.deconv2 + conv_out epilogue
+//              of item i-1 (the warp group of i-1's parity)
+constexpr int HF_ROW = 32 * ROW_BYTES;       // one 32-px row of 128-B pixels
+constexpr int HF_A1 = 10 * HF_ROW;           // input box: 10 rows (item 0) / 6 rows
+constexpr int HF_A2 = 6 * HF_ROW;            // rows 4t-1 .. 4t+4
+constexpr int HF_W1 = 9 * 32 * ROW_BYTES;    // 9 tiles [dy][dx] of 32 rows
+constexpr int HF_W2 = 9 * 16 * ROW_BYTES;    // 9 tiles of 16 rows
+constexpr int HF_ACC1 = 2 * 96;              // TMEM columns per head.deconv1 accumulator
+constexpr int HF_ACC2 = 2 * HF_ACC1;         // first head.deconv2 accumulator column
+
+__global__ void __launch_bounds__(RT_THREADS, 1)
+    k_head_fused(const __grid_constant__ CUtensorMap mapA10, const __grid_constant__ CUtensorMap mapA6,
+                 const __grid_constant__ CUtensorMap mapW1, const __grid_constant__ CUtensorMap mapW2,
+                 const __grid_constant__ ConvArgs p1, const __grid_constant__ ConvArgs p2, int nmaps) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* w1 = smem;
+  uint8_t* w2 = w1 + HF_W1;
+  uint8_t* a1 = w2 + HF_W2;      // 2 stages
+  uint8_t* a2 = a1 + 2 * HF_A1;  // 2 buffers
+  uint64_t* bars = reinterpret_cast<uint64_t*>(a2 + 2 * HF_A2);
+  uint64_t* a1full = bars;         // [2]
+  uint64_t* a1empty = bars + 2;    // [2]
+  uint64_t* acc1full = bars + 4;   // [2]
+  uint64_t* acc1empty = bars + 6;  // [2]
+  uint64_t* a2full = bars + 8;     // [2]
+  uint64_t* a2empty = bars + 10;   // [2]
+  uint64_t* acc2full = bars + 12;  // [2]
+  uint64_t* acc2empty = bars + 14; // [2]
+  uint64_t* wfull = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&mapA10);
+    prefetch_map(&mapA6);
+    prefetch_map(&mapW1);
+    prefetch_map(&mapW2);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&a1full[i], 1);
+      mbar_init(&a1empty[i], 1);
+      mbar_init(&acc1full[i], 1);
+      mbar_init(&acc1empty[i], RT_EPI_WARPS);
+      mbar_init(&a2full[i], RT_EPI_WARPS);
+      mbar_init(&a2empty[i], 1);
+      mbar_init(&acc2full[i], 1);
+      mbar_init(&acc2empty[i], RT_EPI_WARPS / 2);
+    }
+    mbar_init(wfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int my_maps = nmaps > int(blockIdx.x) ? (nmaps - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+  const int items = 8 * my_maps;
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(wfull, uint32_t(HF_W1 + HF_W2));
+      for (int t = 0; t < 9; ++t) {
+        tma_load_2d(&mapW1, wfull, w1 + t * 32 * ROW_BYTES, t * 64, 0);
+        tma_load_2d(&mapW2, wfull, w2 + t * 16 * ROW_BYTES, t * 64, 0);
+      }
+      for (int kt = 0; kt < items; ++kt) {
+        const int s = kt & 1, t = kt & 7, n0 = int(blockIdx.x) + (kt >> 3) * int(gridDim.x);
+        mbar_wait(&a1empty[s], ((kt >> 1) & 1) ^ 1);
+        if (t == 0) {  // rows -1 .. 8
+          mbar_expect_tx(&a1full[s], uint32_t(10 * HF_ROW));
+          tma_load_4d(&mapA10, &a1full[s], a1 + s * HF_A1, 0, 0, -1, n0);
+        } else {       // rows 4t .. 4t+5
+          mbar_expect_tx(&a1full[s], uint32_t(6 * HF_ROW));
+          tma_load_4d(&mapA6, &a1full[s], a1 + s * HF_A1, 0, 0, 4 * t, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc1 = make_idesc(0, BM, 96);
+      constexpr uint32_t idesc2 = make_idesc(0, BM, 48);
+      mbar_wait(wfull, 0);
+      const uint32_t w1a = smem_u32(w1), w2a = smem_u32(w2);
+      auto mma2 = [&](int kt) {  // head.deconv2 of item kt: 3 dy x 2 K steps
+        const int b = kt & 1;
+        mbar_wait(&a2full[b], (kt >> 1) & 1);
+        mbar_wait(&acc2empty[b], ((kt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t a2a = smem_u32(a2 + b * HF_A2);
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            tc_mma<0>(tmem_base + HF_ACC2 + b * 48, sw128_desc(a2a + dy * HF_ROW + 32 * k),
+                      sw128_desc(w2a + dy * 3 * 16 * ROW_BYTES + 32 * k), idesc2, (dy | k) ? 1u : 0u);
+        tc_commit(&a2empty[b]);
+        tc_commit(&acc2full[b]);
+      };
+      for (int kt = 0; kt < items; ++kt) {
+        const int s = kt & 1, t = kt & 7;
+        // head.deconv1 of item kt: 1 (item 0: 2) M blocks x 3 dy x 4 K steps
+        mbar_wait(&a1full[s], (kt >> 1) & 1);
+        mbar_wait(&acc1empty[s], ((kt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t a1a = smem_u32(a1 + s * HF_A1);
+        const int nblk = t == 0 ? 2 : 1;
+#pragma unroll 1
+        for (int b = 0; b < nblk; ++b)
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int k = 0; k < ROW_BYTES / 32; ++k)
+              tc_mma<0>(tmem_base + s * HF_ACC1 + b * 96,
+                        sw128_desc(a1a + (4 * b + dy) * HF_ROW + 32 * k),
+                        sw128_desc(w1a + dy * 3 * 32 * ROW_BYTES + 32 * k), idesc1, (dy | k) ? 1u : 0u);
+        tc_commit(&a1empty[s]);
+        tc_commit(&acc1full[s]);
+        if (kt > 0) mma2(kt - 1);
+      }
+      if (items > 0) mma2(items - 1);
+    }
+  } else {
+    const int q = warp & 3, grp = (warp - 2) / 4;
+    const uint32_t tq = tmem_base + (uint32_t(q * 32) << 16);
+    const uint32_t a2s = smem_u32(a2);
+    const int c0 = 16 * grp, jb = 2 * grp;
+    // one row of head.deconv1 outputs (this warp's 16 channels) into A2 slot
+    auto put = [&](int buf, int slot, const uint32_t (&pk)[8]) {
+      const int r = slot * 32 + lane;
+      const uint32_t rowa = a2s + buf * HF_A2 + r * ROW_BYTES;
+      sts128(rowa + (((jb + 0) ^ (r & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+      sts128(rowa + (((jb + 1) ^ (r & 7)) << 4), pk[4], pk[5], pk[6], pk[7]);
+    };
+    auto epi2 = [&](int kt) {  // head.deconv2 + conv_out of item kt (warp group kt & 1)
+      const int b = kt & 1;
+      if (grp != b) return;
+      const int t = kt & 7, n0 = int(blockIdx.x) + (kt >> 3) * int(gridDim.x);
+      mbar_wait(&acc2full[b], (kt >> 1) & 1);
+      tc_fence_after();
+      const int64_t m = int64_t(n0) * 1024 + (4 * t + q) * 32 + lane;
+      epilogue_tile<0, 16, true>(p2, tq + HF_ACC2 + b * 48, m, 0, 0, 16);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc2empty[b]);
+    };
+    // a row of item kt-1 that item kt reuses (slot 4 / 5 -> slot 0 / 1),
+    // kept in registers by the warp that computed it
+    uint32_t carry[8];
+    int carry_slot = -1;
+    for (int kt = 0; kt < items; ++kt) {
+      const int s = kt & 1, t = kt & 7;
+      mbar_wait(&acc1full[s], (kt >> 1) & 1);
+      mbar_wait(&a2empty[s], ((kt >> 1) & 1) ^ 1);  // head.deconv2 of item kt-2 has read A2[s]
+      tc_fence_after();
+      if (carry_slot >= 0) put(s, carry_slot, carry);
+      carry_slot = -1;
+      const int nblk = t == 0 ? 2 : 1;
+#pragma unroll 1
+      for (int b = 0; b < nblk; ++b) {
+        // this quarter's head.deconv1 row: item 0 block b -> row 4b + q,
+        // else row 4t + 1 + q
+        const int row = t == 0 ? 4 * b + q : 4 * t + 1 + q;
+        if (t == 0 && b == 1 && q > 0) {
+          if (q == 1) {  // row -1 (slot 0 of item 0) is the map's zero padding
+            const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            put(s, 0, z);
+          }
+          continue;  // rows 5..7 of item 0 are recomputed by item 1
+        }
+        float acc[16], v[16];
+        acc_chunk<32, true>(tq + s * HF_ACC1 + b * 96, c0, lane, 32, acc);
+        bn_lrelu16(acc, p1.ep_a + c0, p1.ep_b + c0, p1.slope, v);
+        const bool inside = row < 32;
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(inside ? v[2 * i] : 0.f, inside ? v[2 * i + 1] : 0.f);
+          pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        const int slot = row - (4 * t - 1);  // slot in this item's A2 (rows 4t-1 ..)
+        put(s, slot, pk);
+        // rows 4t+3, 4t+4 are rows 4(t+1)-1, 4(t+1) of the next item
+        if (t < 7 && (slot == 4 || slot == 5)) {
+          carry_slot = slot - 4;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) carry[i] = pk[i];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc1empty[s]);
+      fence_proxy_async();  // A2 is read by the tensor core (async proxy)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a2full[s]);
+      if (kt > 0) epi2(kt - 1);
+    }
+    if (items > 0) epi2(items - 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u));
+  }
+}
+constexpr size_t head_fused_smem() {
+  return 1024 + size_t(HF_W1) + HF_W2 + 2 * size_t(HF_A1) + 2 * size_t(HF_A2) + 256;
+}
+
+// ---------------------------------------------------------------------------
 // CTA-pair row-tile conv (tcgen05.mma.cta_group::2, M = 256): the
 // streamed-weight dx layers (dec1.deconv1 @32x32, dec2.deconv1 @16x16).
 // A work tile is 256 output pixels; CTA rank r of the pair owns M rows
@@ -2377,6 +2608,58 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
                           static_cast<T*>(pool->p), nmaps, st);
 }
 
+// head.deconv1 + head.deconv2 + conv_out in one kernel (bf16; see k_head_fused)
+int run_head_fused(NetImpl& net, ConvLayer& L1, ConvLayer& L2, const Buf& in, int64_t nmaps,
+                   float* pred, cudaStream_t st) {
+  int rc = prepare_layer(net, L1, 0);
+  if (rc) return rc;
+  rc = prepare_layer(net, L2, 0);
+  if (rc) return rc;
+  if (in.c != 64 || in.hw != 32 || L1.cin_pad != 64 || L1.cout_pad != 32 || L2.cin_pad != 64 ||
+      L2.cout_pad != 16)
+    return fail(DRCB_ECONTRACT, "fused head expects 64 -> 32 -> 16 channels at 32x32");
+  ConvArgs p1, p2;
+  std::memset(&p1, 0, sizeof(p1));
+  std::memset(&p2, 0, sizeof(p2));
+  p1.hw = p2.hw = 32;
+  p1.ep_a = L1.d_ep_a;
+  p1.ep_b = L1.d_ep_b;
+  p1.slope = p2.slope = net.slope;
+  p1.cout = 32;
+  p2.ep_a = L2.d_ep_a;
+  p2.ep_b = L2.d_ep_b;
+  p2.cout = 16;
+  p2.head = 1;
+  p2.pred = pred;
+  const ConvLayer& H = net.layers[16];
+  for (int o = 0; o < 3; ++o) {
+    for (int j = 0; j < 16; ++j) p2.hw_w[o * 16 + j] = j < H.cin ? H.w[o * H.cin + j] : 0.f;
+    p2.hw_b[o] = H.bias[o];
+  }
+  CUtensorMap mA10, mA6, mW1, mW2;
+  rc = encode_act(&mA10, in.p, 0, in.c, 32, nmaps, 32, 10, 1);
+  if (rc) return rc;
+  rc = encode_act(&mA6, in.p, 0, in.c, 32, nmaps, 32, 6, 1);
+  if (rc) return rc;
+  rc = encode_w(&mW1, L1.d_wtc, 0, int64_t(9) * L1.cin_pad, L1.cout_pad, 32);
+  if (rc) return rc;
+  rc = encode_w(&mW2, L2.d_wtc, 0, int64_t(9) * L2.cin_pad, L2.cout_pad, 16);
+  if (rc) return rc;
+  constexpr size_t smem = head_fused_smem();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_head_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = nmaps < nsm ? int(nmaps) : nsm;  // whole maps per CTA
+  k_head_fused<<<grid, RT_THREADS, smem, st>>>(mA10, mA6, mW1, mW2, p1, p2, int(nmaps));
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : cuda_fail(e, "k_head_fused");
+}
+
 template <int KIND>
 int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t st,
                  const void* x_nhwc = nullptr) {
@@ -2461,19 +2744,25 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
   if (!fup16) up(B[13], 2 * k, B[2]);
   rc |= run_layer<KIND>(net, Ls[12], B[2], B[1], 0, np, st);
   rc |= run_layer<KIND>(net, Ls[13], B[1], B[14], 0, np, st);
-  rc |= run_layer<KIND>(net, Ls[14], B[14], B[15], 0, np, st);
   if (rc) {
     cudaFreeAsync(base, st);
     return rc;
   }
-  // head.deconv2 + conv_out + ReLU fused; predictions for the n real maps
+  // predictions for the n real maps
   float* pred = y;
   float* tmp = nullptr;
   if (np != n) {
     DRCB_CUDA(cudaMallocAsync((void**)&tmp, size_t(np) * 3 * 1024 * 4, st));
     pred = tmp;
   }
-  rc = run_layer<KIND>(net, Ls[15], B[15], B[14], 0, np, st, pred);
+  if (KIND == 0 && getenv("DRCB_NO_HEAD_FUSE") == nullptr) {
+    // head.deconv1 + head.deconv2 + conv_out + ReLU in one kernel
+    rc = run_head_fused(net, Ls[14], Ls[15], B[14], np, pred, st);
+  } else {
+    rc = run_layer<KIND>(net, Ls[14], B[14], B[15], 0, np, st);
+    // head.deconv2 + conv_out + ReLU fused
+    if (!rc) rc = run_layer<KIND>(net, Ls[15], B[15], B[14], 0, np, st, pred);
+  }
   if (tmp) {
     DRCB_CUDA(cudaMemcpyAsync(y, tmp, size_t(n) * 3 * 1024 * 4, cudaMemcpyDeviceToDevice, st));
     DRCB_CUDA(cudaFreeAsync(tmp, st));

@@ -84,11 +84,12 @@ def test_tc_batch_sizes_and_padding():
 
 
 @pytest.mark.parametrize("mode", ["bf16", "tf32"])
-@pytest.mark.parametrize("env", ["DRCB_NO_FUSED_POOL", "DRCB_NO_UP16"])
+@pytest.mark.parametrize("env", ["DRCB_NO_FUSED_POOL", "DRCB_NO_UP16", "DRCB_POOL_CTA", "DRCB_NO_HEAD_FUSE"])
 def test_fused_pool_and_upsample_bit_identical(mode, env, monkeypatch):
-    # the encoder pools fused into the skip convs' epilogues and the 16 -> 32
-    # upsample fused into dec2.deconv2's whole-map epilogue must reproduce
-    # the separate passes exactly (they act on the stored, rounded values)
+    # the encoder pools fused into the skip convs (pool warp or CTA-wide), the
+    # 16 -> 32 upsample fused into dec2.deconv2's whole-map epilogue and the
+    # fused head (head.deconv1's output kept in SMEM) must reproduce the
+    # separate passes exactly (they act on the stored, rounded values)
     rng = np.random.default_rng(8)
     x = rng.uniform(0, 1, (9, 7, 32, 32)).astype(np.float32)
     net = cnn.random_network(64, 2)
