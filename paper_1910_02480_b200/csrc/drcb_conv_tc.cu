@@ -1274,17 +1274,42 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
       sts128(rowa + (((jb + 0) ^ (r & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
       sts128(rowa + (((jb + 1) ^ (r & 7)) << 4), pk[4], pk[5], pk[6], pk[7]);
     };
+    // folded BN vectors in registers: head.deconv1's 16 channels of this
+    // warp, head.deconv2's 16 channels
+    float e1a[16], e1b[16], e2a[16], e2b[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      e1a[i] = p1.ep_a[c0 + i];
+      e1b[i] = p1.ep_b[c0 + i];
+      e2a[i] = p2.ep_a[i];
+      e2b[i] = p2.ep_b[i];
+    }
     auto epi2 = [&](int kt) {  // head.deconv2 + conv_out of item kt (warp group kt & 1)
       const int b = kt & 1;
       if (grp != b) return;
       const int t = kt & 7, n0 = int(blockIdx.x) + (kt >> 3) * int(gridDim.x);
       mbar_wait(&acc2full[b], (kt >> 1) & 1);
       tc_fence_after();
-      const int64_t m = int64_t(n0) * 1024 + (4 * t + q) * 32 + lane;
-      epilogue_tile<0, 16, true>(p2, tq + HF_ACC2 + b * 48, m, 0, 0, 16);
+      float acc[16];
+      acc_chunk<16, true>(tq + HF_ACC2 + b * 48, 0, lane, 32, acc);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc2empty[b]);
+      // BN + LeakyReLU, then conv_out + ReLU (epilogue_tile's head branch)
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float x = acc[i] * e2a[i] + e2b[i];
+        v[i] = x >= 0.f ? x : p2.slope * x;
+      }
+      const int pix = (4 * t + q) * 32 + lane;
+#pragma unroll
+      for (int o = 0; o < 3; ++o) {
+        float sum = p2.hw_b[o];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sum += p2.hw_w[o * 16 + i] * v[i];
+        p2.pred[(int64_t(n0) * 3 + o) * 1024 + pix] = fmaxf(sum, 0.f);
+      }
     };
     // a row of item kt-1 that item kt reuses (slot 4 / 5 -> slot 0 / 1),
     // kept in registers by the warp that computed it
@@ -1312,7 +1337,11 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
         }
         float acc[16], v[16];
         acc_chunk<32, true>(tq + s * HF_ACC1 + b * 96, c0, lane, 32, acc);
-        bn_lrelu16(acc, p1.ep_a + c0, p1.ep_b + c0, p1.slope, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float x = acc[i] * e1a[i] + e1b[i];
+          v[i] = x >= 0.f ? x : p1.slope * x;
+        }
         const bool inside = row < 32;
         uint32_t pk[8];
 #pragma unroll
