@@ -10,7 +10,7 @@ mkdir -p gpurun_out
 B="python bench.py --steps 1 --warmup 3 --no-train --no-secondary --no-cpu-baseline --no-graph"
 timeout 600 python bench.py > gpurun_out/prof_bench.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 300 -c 400 --csv \
-  $B > gpurun_out/prof_launches.csv 2> gpurun_out/prof_launches.err
+  --log-file gpurun_out/prof_launches.csv $B > gpurun_out/prof_launches.out 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   --clock-control none --csv python tools/net_time.py --iters 1 > gpurun_out/prof_net.csv 2>&1
 full() {  # name, kernel regex, launches to skip
@@ -21,6 +21,6 @@ full map_paths 'k_map_paths' 3
 full direct_samples 'k_direct_samples' 3
 full conv_pair 'k_conv_pair' 3
 full conv_tc_dec3 'k_conv_tc' 34
-full conv_rows_dec1 'k_conv_rows<0, 64, 1, 1, 1, 0>' 3
+full conv_rows_dec1 'k_conv_rows' 5   # 6 row-conv launches per frame: dec1.deconv2 is the 6th
 full head_fused 'k_head_fused' 3
 ls -la gpurun_out

@@ -22,9 +22,10 @@ PROF = os.path.join(REPO, "profiles")
 
 
 def ncu_rows(path):
-    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
-    hdr = rows[0]
-    return hdr, rows[1:]
+    rows = list(csv.reader(open(path)))
+    h = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[h]
+    return hdr, [r for r in rows[h + 1:] if len(r) == len(hdr)]
 
 
 def short(name):
