@@ -1769,10 +1769,13 @@ __global__ void __launch_bounds__(IN8_THREADS, 1)
         mbar_wait(&afull[st], ph);
         tc_fence_after();
         const uint32_t a0 = smem_u32(sa + st * A_BYTES), b0 = smem_u32(sw);
+        // K steps of 32 B that hold real taps: the last chunk holds only tap 8
+        // (its other steps would multiply zero padding)
+        constexpr int KLAST = (72 * ELEM - (NCH - 1) * ROW_BYTES + 31) / 32;
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
-          for (int k = 0; k < ROW_BYTES / 32; ++k)
+          for (int k = 0; k < (c == NCH - 1 ? KLAST : ROW_BYTES / 32); ++k)
             tc_mma<KIND>(tmem_base + acc * BN, sw128_desc(a0 + c * BM * ROW_BYTES + 32 * k),
                          sw128_desc(b0 + c * BN * ROW_BYTES + 32 * k), idesc, (c | k) ? 1u : 0u);
         tc_commit(&aempty[st]);
