@@ -1842,19 +1842,21 @@ __global__ void __launch_bounds__(IN8_THREADS, 1)
       tc_fence_after();
       const int64_t m = int64_t(tile) * BM + row;
       uint8_t* ot = so + obuf * O_BYTES;
-      if (threadIdx.x == 192) bulk_wait_read1();
-      asm volatile("bar.sync 3, 128;" ::: "memory");
+      // one warp per lane quarter = one image row: the warp stages and
+      // TMA-stores its own 32 pixels (no barrier across the epilogue warps)
+      if (lane == 0) bulk_wait_read1();  // this warp's store of 2 tiles ago has read ot
+      __syncwarp();
       epilogue_stage<KIND, BN, false, 16>(p, tmem_base + (uint32_t(q * 32) << 16) + acc * BN, m, 0,
                                           ot, 0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       fence_proxy_async();
-      asm volatile("bar.sync 3, 128;" ::: "memory");
-      if (threadIdx.x == 192) {
+      __syncwarp();
+      if (lane == 0) {
         for (int sb = 0; sb < BN / CEL; ++sb)
-          tma_store_4d(&mapO, ot + sb * BM * ROW_BYTES, p.cout_off + sb * CEL, 0, (tile & 7) * 4,
-                       tile >> 3);
+          tma_store_4d(&mapO, ot + (sb * BM + q * 32) * ROW_BYTES, p.cout_off + sb * CEL, 0,
+                       (tile & 7) * 4 + q, tile >> 3);
         bulk_commit();
       }
       obuf ^= 1;
@@ -1863,7 +1865,7 @@ __global__ void __launch_bounds__(IN8_THREADS, 1)
         aph ^= 1;
       }
     }
-    if (threadIdx.x == 192) bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -2401,7 +2403,7 @@ int run_in8(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cout_
   if (r != CUDA_SUCCESS) return fail(DRCB_ECUDA, "cuTensorMapEncodeTiled(in8) failed: " + std::to_string(int(r)));
   int rc = encode_w(&mB, L.d_wtc, KIND, L.cin_pad, 64, 64);
   if (rc) return rc;
-  rc = encode_act(&mO, out.p, KIND, out.c, 32, nmaps, 32, 4, 1);
+  rc = encode_act(&mO, out.p, KIND, out.c, 32, nmaps, 32, 1, 1);  // one row per lane quarter
   if (rc) return rc;
   auto kern = k_conv_in8<KIND>;
   constexpr size_t smem = in8_smem<KIND>();
