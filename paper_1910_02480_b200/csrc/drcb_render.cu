@@ -207,6 +207,33 @@ __global__ void __launch_bounds__(TPB, DIRECT_CTAS) k_direct_samples(DevScene S,
   if (nonfinite) add_nonfinite(nonfinite, nf);
 }
 
+// direct_spp == 1: the G-buffer centre chain and the pixel's one li_direct
+// path in one thread (one launch, no per-sample buffer; the jittered camera
+// ray re-walks the BVH nodes the centre ray just brought into L1). The
+// result is exactly k_direct_reduce's for one sample: (0 + L) / 1.
+template <typename R>
+__global__ void __launch_bounds__(TPB, DIRECT_CTAS) k_gbuffer_direct1(DevScene S, DevCamera C,
+                                                                     DrcbRenderCfg cfg,
+                                                                     DrcbGBuffer gb, R* direct,
+                                                                     int64_t* nonfinite) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int nf = 0;
+  if (k < int64_t(C.W) * C.H) {
+    const int64_t i = pixel_of(C, k);
+    const int x = int(i % C.W), y = int(i / C.W);
+    const V3<R> cam = ld3<R>(C.pos);
+    store_chain(gb, i, primary_chain(S, cam, camera_dir<R>(C, R(x) + R(0.5), R(y) + R(0.5))));
+    PathRng rng;
+    rng.init(cfg.seed, uint64_t(i), 0ull, cfg.sampler_kind, 1u);
+    const R jx = to_unit<R>(rng.sample(0)), jy = to_unit<R>(rng.sample(1));
+    const V3<R> d = camera_dir<R>(C, R(x) + jx, R(y) + jy);
+    const V3<R> l = direct_path(S, cam, d, rng, cfg.include_background != 0, nf);
+    const V3<R> acc = mk<R>(R(0), R(0), R(0)) + l;
+    st3(direct + 3 * i, divs(acc, R(1)));
+  }
+  if (nonfinite) add_nonfinite(nonfinite, nf);
+}
+
 template <typename R>
 __global__ void k_direct_reduce(DevCamera C, int spp, int tile, const R* __restrict__ samples,
                                 R* direct) {
@@ -954,9 +981,14 @@ int launch_gbuffer_direct(const DevScene& S, const DevCamera& C, const DrcbRende
                           cudaStream_t st) {
   int64_t n = int64_t(C.W) * C.H;
   if (n <= 0) return 0;
+  const int spp = cfg.direct_spp;
+  if (spp == 1 && getenv("DRCB_SPLIT_DIRECT") == nullptr) {
+    k_gbuffer_direct1<R><<<nblocks(n), TPB, 0, st>>>(S, C, cfg, gb, direct, nonfinite);
+    LAUNCH_CHECK();
+    return 0;
+  }
   k_gbuffer<R><<<nblocks(n), TPB, 0, st>>>(S, C, gb);
   LAUNCH_CHECK();
-  const int spp = cfg.direct_spp;
   R* samples = nullptr;
   DRCB_CUDA(cudaMallocAsync((void**)&samples, sizeof(R) * 3 * size_t(n) * spp, st));
   k_direct_samples<R><<<nblocks(n * spp), TPB, 0, st>>>(S, C, cfg, samples, nonfinite);

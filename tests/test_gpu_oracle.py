@@ -113,6 +113,25 @@ def test_frames_bit_identical_across_runs_and_streams(c1):
     assert np.array_equal(out.double().cpu().numpy(), a)
 
 
+@pytest.mark.parametrize("precision", [32, 64])
+def test_fused_gbuffer_direct_bit_identical_to_split_passes(c1, precision, monkeypatch):
+    # direct_spp = 1: centre chain + li_direct path in one kernel vs the
+    # k_gbuffer / k_direct_samples / k_direct_reduce passes (direct_spp > 1
+    # always takes the split passes)
+    cfg = render.RenderConfig(direct_spp=1, indirect_tasks=2, precision=precision, net_mode="fp32")
+    net = cnn.random_network(64, 0)
+    fused, tf = render.render_drc(c1, cfg, net)
+    monkeypatch.setenv("DRCB_SPLIT_DIRECT", "1")
+    split, ts = render.render_drc(c1, cfg, net)
+    assert tf["entries"] == ts["entries"] and tf["nonfinite"] == ts["nonfinite"]
+    if precision == 64:  # -fmad=false build: the same operations bit for bit
+        assert np.array_equal(fused, split)
+    else:  # the fp32 build contracts FMAs per kernel: last-ulp differences only
+        rel = np.abs(fused - split) / np.maximum(np.abs(split), 1e-3)
+        assert (rel > 1e-4).any(axis=2).mean() <= 1e-3
+        assert np.linalg.norm(fused - split) <= 1e-5 * np.linalg.norm(split)
+
+
 def test_bf16_and_tf32_frames_within_bar(c1):
     """Whole frame with the tensor-core U-Net vs the fp32 engine (config 3's
     bench weights, seed 2): relative L2 of the image."""
