@@ -1722,13 +1722,19 @@ __global__ void __launch_bounds__(IN8_THREADS, 1)
     fence_barrier_init();
   }
   if (warp >= 2 && warp < 6) {
-    // K padding pieces (never rewritten): zero them once in every A stage
-    const int r = threadIdx.x - 64;
+    // pieces no input pixel is scattered to (never rewritten): the K padding
+    // and the x-border taps (dx = -1 at x = 0, dx = +1 at x = 31, the conv's
+    // zero padding); zero them once in every A stage
+    const int r = threadIdx.x - 64, x = r & 31;
     for (int st = 0; st < IN8_SA; ++st)
-      for (int j = 9 * PPT; j < NCH * 8; ++j)
-        sts128(smem_u32(sa + st * A_BYTES + (j >> 3) * (BM * ROW_BYTES) + r * ROW_BYTES) +
-                   (((j & 7) ^ (r & 7)) << 4),
-               0u, 0u, 0u, 0u);
+      for (int j = 0; j < NCH * 8; ++j) {
+        const int t = j / PPT;
+        const bool pad = j >= 9 * PPT || (x == 0 && t % 3 == 0) || (x == 31 && t % 3 == 2);
+        if (pad)
+          sts128(smem_u32(sa + st * A_BYTES + (j >> 3) * (BM * ROW_BYTES) + r * ROW_BYTES) +
+                     (((j & 7) ^ (r & 7)) << 4),
+                 0u, 0u, 0u, 0u);
+      }
     fence_proxy_async();
   }
   if (warp == 1) {
@@ -1791,29 +1797,38 @@ __global__ void __launch_bounds__(IN8_THREADS, 1)
       }
     }
   } else if (warp < 6) {
-    // im2col builders: thread r = tile pixel (row r / 32, column r % 32)
-    const int r = threadIdx.x - 64, ry = r >> 5, x = r & 31;
+    // im2col builders, scatter form: each input pixel (6 rows y0-1 .. y0+4 of
+    // 32) is read once and written to the (up to) 9 output pixels whose taps
+    // it feeds: output (ry, x) tap t = (dy, dx) is input (ry + dy, x + dx - 1);
+    // the x-border taps stay zero (zeroed once above), the y border comes
+    // zero from the TMA (OOB rows)
+    const int b = threadIdx.x - 64;
     int ist = 0, ast = 0;
     uint32_t iph = 0, aph = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       mbar_wait(&ifull[ist], iph);
       mbar_wait(&aempty[ast], aph ^ 1);
       const uint32_t src = smem_u32(si + ist * IN_BYTES);
-      const uint32_t dst = smem_u32(sa + ast * A_BYTES) + r * ROW_BYTES;
+      const uint32_t dst = smem_u32(sa + ast * A_BYTES);
 #pragma unroll
-      for (int t = 0; t < 9; ++t) {
-        const int xs = x + t % 3 - 1;
-        const bool ok = xs >= 0 && xs < 32;
-        const uint32_t a = src + ((ry + t / 3) * 32 + (ok ? xs : 0)) * PX_BYTES;
+      for (int h = 0; h < 2; ++h) {
+        const int k = b + 128 * h;  // input pixel of the tile's 6 x 32 window
+        if (k >= 6 * 32) break;     // warp-uniform (k multiple of 32 per warp)
+        const int iy = k >> 5, ix = k & 31;
 #pragma unroll
-        for (int q = 0; q < PPT; ++q) {
-          uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-          if (ok)
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
-                         : "r"(a + 16 * q));
-          const int j = t * PPT + q;
-          sts128(dst + (j >> 3) * (BM * ROW_BYTES) + (((j & 7) ^ (r & 7)) << 4), v0, v1, v2, v3);
+        for (int qq = 0; qq < PPT; ++qq) {
+          uint32_t v0, v1, v2, v3;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                       : "r"(src + k * PX_BYTES + 16 * qq));
+#pragma unroll
+          for (int t = 0; t < 9; ++t) {
+            const int ry = iy - t / 3, x = ix - t % 3 + 1;
+            if (ry < 0 || ry > 3 || x < 0 || x > 31) continue;
+            const int r = ry * 32 + x, j = t * PPT + qq;
+            sts128(dst + (j >> 3) * (BM * ROW_BYTES) + r * ROW_BYTES + (((j & 7) ^ (r & 7)) << 4), v0, v1,
+                   v2, v3);
+          }
         }
       }
       fence_proxy_async();
