@@ -243,7 +243,10 @@ def train_throughput(cnn, world=1, batches=(64, 256, 1024), global_batch=4096, s
                     "batch_per_rank": b, "global_batch": b * world}
         del x, y
     for tr in trainers.values():
+        comm = getattr(tr, "_comm", None)
         tr.close()
+        if comm is not None:
+            comm.close()
     return out
 
 
