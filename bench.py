@@ -317,6 +317,17 @@ def secondary_frames(config, tasks, frames, rank, world, steps=2, warmup=1, stre
             "stage_ms_per_frame": {k: v / 1e3 for k, v in tel["stage_us"].items()}}
 
 
+def traversal_traffic():
+    """Per-launch memory traffic of the casting kernels from the committed ncu
+    capture (profiles/*_traversal_traffic.json), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(REPO, "profiles", "*_traversal_traffic.json")))
+    if not files:
+        return None
+    return json.load(open(files[-1])).get("kernels")
+
+
 def network_traffic(n_maps):
     """DRAM bytes (read + write) of one U-Net forward over n_maps, scaled from
     the committed ncu capture (profiles/*_network_traffic.json, 4,096 maps);
@@ -606,6 +617,21 @@ def main():
         trav["mrays_per_s"] = trav["casts_per_frame"] / (tr_ms * 1e-3) / 1e6
         trav["note"] = ("BVH + triangles (76 MB) stay L2/L1-resident: the casting kernels are bound "
                         "by SIMT issue and divergence, not HBM (profiles/*_ncu_full_summary.md)")
+        # achieved memory bandwidth of the map-path stage: bytes per launch from
+        # the committed full capture (profiles/*_traversal_traffic.json) over the
+        # live stage time
+        tt = traversal_traffic()
+        if tt and "map_paths" in tt:
+            mp = tt["map_paths"]
+            sec = avg["maps"] * 1e-6
+            trav["maps_stage"] = {
+                "l2_to_l1_gbs": mp["l2_to_l1_bytes"] / sec / 1e9,
+                "l1_to_l2_write_gbs": mp["l1_to_l2_write_bytes"] / sec / 1e9,
+                "dram_gbs": (mp["dram_read_bytes"] + mp["dram_write_bytes"]) / sec / 1e9,
+                "frac_hbm": (mp["dram_read_bytes"] + mp["dram_write_bytes"]) / sec / 1e9 /
+                            peaks.get("hbm_gbs", 6650.0),
+                "l1_hit_pct": mp.get("l1_hit_pct"), "l2_hit_pct": mp.get("l2_hit_pct"),
+                "source": "bytes per launch: ncu full capture; time: live CUDA events"}
 
     cb = None
     if rank == 0 and not args.no_cpu_baseline:

@@ -18,7 +18,7 @@ full() {  # name, kernel regex, launches to skip
     -o "gpurun_out/prof_full_$1" $B > "gpurun_out/prof_full_$1.log" 2>&1
 }
 full map_paths 'k_map_paths' 3
-full direct_samples 'k_direct_samples' 3
+full gbuffer_direct1 'k_gbuffer_direct1' 3
 full conv_pair 'k_conv_pair' 3
 full conv_tc_dec3 'k_conv_tc' 34
 full conv_rows_dec1 'k_conv_rows' 5   # 6 row-conv launches per frame: dec1.deconv2 is the 6th

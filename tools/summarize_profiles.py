@@ -127,6 +127,42 @@ def full(rnd):
     return path
 
 
+def traversal(rnd):
+    """Memory traffic of the casting kernels (one launch = one frame's stage)
+    from the full captures: L2 -> L1 bytes, L1 -> L2 write bytes, DRAM bytes."""
+    out = {"what": "per-launch memory traffic of the ray-casting kernels (one 1024^2 c3 frame), "
+                   "ncu --set full, --clock-control none",
+           "kernels": {}}
+    keys = {"us": "gpu__time_duration.sum", "l2_to_l1_bytes": "l1tex__m_xbar2l1tex_read_bytes.sum",
+            "l1_to_l2_write_bytes": "l1tex__m_l1tex2xbar_write_bytes.sum",
+            "dram_read_bytes": "dram__bytes_read.sum", "dram_write_bytes": "dram__bytes_write.sum",
+            "l1_hit_pct": "l1tex__t_sector_hit_rate.pct", "l2_hit_pct": "lts__t_sector_hit_rate.pct"}
+    scale = {"us": 1e-3, "l2_to_l1_bytes": 1e9, "l1_to_l2_write_bytes": 1e9,
+             "dram_read_bytes": 1e6, "dram_write_bytes": 1e6}
+    for name in ("map_paths", "gbuffer_direct1"):
+        rep = os.path.join(OUT, f"prof_full_{name}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout.splitlines()
+        rows = list(csv.reader(raw))
+        hdr, units, v = rows[0], rows[1], rows[2]
+        d = {}
+        for k, m in keys.items():
+            if m in hdr:
+                val = float(v[hdr.index(m)].replace(",", ""))
+                unit = units[hdr.index(m)]
+                if k.endswith("bytes"):  # normalise to bytes
+                    val *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+                elif k == "us":
+                    val *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3}.get(unit, 1)
+                d[k] = val
+        out["kernels"][name] = d
+    path = os.path.join(PROF, f"{rnd}_traversal_traffic.json")
+    json.dump(out, open(path, "w"), indent=1)
+    return path
+
+
 def bench(rnd):
     for line in open(os.path.join(OUT, "prof_bench.log")):
         if line.startswith("{"):
@@ -140,7 +176,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--round", default="r01")
     a = ap.parse_args()
-    for fn in (bench, launches, network, full):
+    for fn in (bench, launches, network, full, traversal):
         try:
             print(fn(a.round))
         except Exception as e:  # keep the others
