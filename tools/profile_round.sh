@@ -23,4 +23,9 @@ full conv_pair 'k_conv_pair' 3
 full conv_tc_dec3 'k_conv_tc' 34
 full conv_rows_dec1 'k_conv_rows' 5   # 6 row-conv launches per frame: dec1.deconv2 is the 6th
 full head_fused 'k_head_fused' 3
-ls -la gpurun_out
+# summarise on the box (the ncu reports are large), keep two reports
+python tools/summarize_profiles.py --out gpurun_out/profiles_new
+for f in gpurun_out/prof_full_*.ncu-rep; do
+  case "$f" in *map_paths*|*head_fused*) ;; *) rm -f "$f" ;; esac
+done
+ls -la gpurun_out gpurun_out/profiles_new

@@ -175,7 +175,12 @@ def bench(rnd):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--round", default="r01")
+    ap.add_argument("--out", default=None, help="output directory (default profiles/)")
     a = ap.parse_args()
+    global PROF
+    if a.out:
+        PROF = a.out
+        os.makedirs(PROF, exist_ok=True)
     for fn in (bench, launches, network, full, traversal):
         try:
             print(fn(a.round))
