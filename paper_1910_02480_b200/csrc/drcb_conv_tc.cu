@@ -577,7 +577,8 @@ __device__ __forceinline__ void unpack8_bf16(const uint4& u, float (&f)[8]) {
 }
 
 // bilinear mix of four 16-B bf16 vectors (p00, p10, p01, p11) in packed bf16x2
-// arithmetic: t0 = p00*omr + p10*fr, t1 = p01*omr + p11*fr, v = t0*omc + t1*fc
+// arithmetic: t0 = fma(p00, omr, p10*fr), t1 = fma(p01, omr, p11*fr),
+// v = fma(t0, omc, t1*fc)
 // (the weights 0, 0.25, 0.75, 1 are exact in bf16)
 __device__ __forceinline__ void up_mix_bf16x2(const uint4 (&q)[4], float omr, float fr, float omc,
                                               float fc, uint32_t (&out)[4]) {
@@ -589,9 +590,12 @@ __device__ __forceinline__ void up_mix_bf16x2(const uint4 (&q)[4], float omr, fl
   const __nv_bfloat162* d = reinterpret_cast<const __nv_bfloat162*>(&q[3]);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const __nv_bfloat162 t0 = __hadd2(__hmul2(a[i], wr0), __hmul2(b[i], wr1));
-    const __nv_bfloat162 t1 = __hadd2(__hmul2(c[i], wr0), __hmul2(d[i], wr1));
-    const __nv_bfloat162 v = __hadd2(__hmul2(t0, wc0), __hmul2(t1, wc1));
+    // explicit fused forms (one rounded product, one fma): the compiler may
+    // not contract them differently per call site, so every caller (the
+    // upsample kernel, the fused dec2.deconv2 epilogue) computes the same bits
+    const __nv_bfloat162 t0 = __hfma2(a[i], wr0, __hmul2_rn(b[i], wr1));
+    const __nv_bfloat162 t1 = __hfma2(c[i], wr0, __hmul2_rn(d[i], wr1));
+    const __nv_bfloat162 v = __hfma2(t0, wc0, __hmul2_rn(t1, wc1));
     out[i] = *reinterpret_cast<const uint32_t*>(&v);
   }
 }
@@ -969,15 +973,17 @@ __global__ void __launch_bounds__(PW ? ROWS_THREADS : RT_THREADS, 1)
             if (threadIdx.x == 64) bulk_wait_read1();
             epi_bar_rt();
           }
-          // one item = a 2x2 output block from its 3x3 low-res neighbourhood
-          // (k_up_nhwc's blocking: 9 SMEM reads per 4 outputs, not 16)
-          for (int e = et; e < 64 * 8; e += 32 * RT_EPI_WARPS) {
-            const int j = e & 7, blk = e >> 3;
-            const int bi = 4 * chk + (blk >> 4), bj = blk & 15;  // low-res pixel
-            uint4 nbq[3][3];
+          // one item = two vertically adjacent 2x2 output blocks (low-res
+          // rows bi0, bi0 + 1) from their 4x3 low-res neighbourhood: 12 SMEM
+          // reads per 8 outputs; each output mixes its four neighbours exactly
+          // as k_up_nhwc does
+          for (int e = et; e < 2 * 16 * 8; e += 32 * RT_EPI_WARPS) {
+            const int j = e & 7, bj = (e >> 3) & 15;
+            const int bi0 = 4 * chk + 2 * (e >> 7);  // low-res rows bi0, bi0 + 1
+            uint4 nbq[4][3];
 #pragma unroll
-            for (int dr = 0; dr < 3; ++dr) {
-              const int r = min(max(bi + dr - 1, 0), 15);
+            for (int dr = 0; dr < 4; ++dr) {
+              const int r = min(max(bi0 + dr - 1, 0), 15);
 #pragma unroll
               for (int dc = 0; dc < 3; ++dc) {
                 const int c = min(max(bj + dc - 1, 0), 15);
@@ -988,18 +994,24 @@ __global__ void __launch_bounds__(PW ? ROWS_THREADS : RT_THREADS, 1)
                              : "r"(L0 + rr * ROW_BYTES + ((j ^ (rr & 7)) << 4)));
               }
             }
-            const float fr_even = bi == 0 ? 0.f : 0.75f, fc_even = bj == 0 ? 0.f : 0.75f;
+            const float fc_even = bj == 0 ? 0.f : 0.75f;
 #pragma unroll
-            for (int a2 = 0; a2 < 2; ++a2) {
-              const float fr = a2 ? 0.25f : fr_even;
+            for (int hb = 0; hb < 2; ++hb) {
+              const int bi = bi0 + hb;
+              const float fr_even = bi == 0 ? 0.f : 0.75f;
 #pragma unroll
-              for (int b2 = 0; b2 < 2; ++b2) {
-                const float fc = b2 ? 0.25f : fc_even;
-                const uint4 q[4] = {nbq[a2][b2], nbq[a2 + 1][b2], nbq[a2][b2 + 1], nbq[a2 + 1][b2 + 1]};
-                uint32_t pk[4];
-                up_mix_bf16x2(q, 1.f - fr, fr, 1.f - fc, fc, pk);
-                const int opx = ((2 * bi + a2) & 7) * 32 + 2 * bj + b2;  // pixel in the chunk
-                sts128(U0 + opx * ROW_BYTES + ((j ^ (opx & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+              for (int a2 = 0; a2 < 2; ++a2) {
+                const float fr = a2 ? 0.25f : fr_even;
+#pragma unroll
+                for (int b2 = 0; b2 < 2; ++b2) {
+                  const float fc = b2 ? 0.25f : fc_even;
+                  const uint4 q[4] = {nbq[hb + a2][b2], nbq[hb + a2 + 1][b2], nbq[hb + a2][b2 + 1],
+                                      nbq[hb + a2 + 1][b2 + 1]};
+                  uint32_t pk[4];
+                  up_mix_bf16x2(q, 1.f - fr, fr, 1.f - fc, fc, pk);
+                  const int opx = ((2 * bi + a2) & 7) * 32 + 2 * bj + b2;  // pixel in the chunk
+                  sts128(U0 + opx * ROW_BYTES + ((j ^ (opx & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+                }
               }
             }
           }
