@@ -254,6 +254,22 @@ __global__ void k_direct_reduce(DevCamera C, int spp, int tile, const R* __restr
   st3(direct + 3 * i, divs(acc, R(spp)));
 }
 
+// local texel directions (texel_local) tabulated once per precision by the
+// same device function: the path kernel's fresh lanes read 3 values instead
+// of evaluating three precise sin/cos
+template <typename R>
+__device__ R g_texel_dirs[3 * MAP_TEXELS];
+
+template <typename R>
+__global__ void k_texel_dirs() {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= MAP_TEXELS) return;
+  const V3<R> d = texel_local<R>(t % MAP_RES, t / MAP_RES);
+  g_texel_dirs<R>[3 * t] = d.x;
+  g_texel_dirs<R>[3 * t + 1] = d.y;
+  g_texel_dirs<R>[3 * t + 2] = d.z;
+}
+
 // Map paths of all cache points (hemimap.py:236-262 + integrators.py:175-302)
 // as a persistent kernel with per-lane path regeneration: a lane whose path
 // terminates (escape, RR, max depth) immediately takes the next texel from a
@@ -275,7 +291,7 @@ __global__ void __launch_bounds__(MAP_TPB, MAP_CTAS) k_map_paths(DevScene S, Drc
                                                           const uint8_t* __restrict__ live,
                                                           int64_t total, unsigned long long* counter,
                                                           R* rad, R* dist, R* nloc,
-                                                          int64_t* nonfinite) {
+                                                          int64_t* nonfinite, int tab) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   bool have = false, done_all = false;
@@ -320,7 +336,7 @@ __global__ void __launch_bounds__(MAP_TPB, MAP_CTAS) k_map_paths(DevScene S, Drc
       slot = p * MAP_TEXELS + tex;
       V3<R> hp = ldr3(pos + 3 * p), hn = ldr3(nrm + 3 * p);
       Frame<R> fr = frame_scalar(S, hn);
-      D = fr.to_world(texel_local<R>(tex % MAP_RES, tex / MAP_RES));
+      D = fr.to_world(tab ? ldr3(g_texel_dirs<R> + 3 * tex) : texel_local<R>(tex % MAP_RES, tex / MAP_RES));
       O = hp + R(T_EPS) * hn;
     }
     // single traversal call site for fresh and continuing lanes
@@ -1015,6 +1031,20 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
   DRCB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   k_point_frames<R><<<nblocks(n), TPB, 0, st>>>(S, nrm, n, frames);
   LAUNCH_CHECK();
+  // the table is filled once, synchronously, outside any graph capture (the
+  // path kernel evaluates texel_local itself until then: frames on other
+  // streams must never see a half-written table)
+  static bool dirs_ready = false;  // per precision (one instantiation each)
+  if (!dirs_ready) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusNone) {
+      k_texel_dirs<R><<<nblocks(MAP_TEXELS), TPB, 0, st>>>();
+      LAUNCH_CHECK();
+      DRCB_CUDA(cudaStreamSynchronize(st));
+      dirs_ready = true;
+    }
+  }
   static int grid = 0;
   if (!grid) {
     int nsm = 0, per_sm = 0;
@@ -1025,7 +1055,7 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
   int64_t total = int64_t(per);
   int g = int(std::min<int64_t>(grid, (total + MAP_TPB - 1) / MAP_TPB));
   k_map_paths<R><<<g, MAP_TPB, 0, st>>>(S, cfg, pos, nrm, keys, live, total, counter, rad, dist,
-                                         nloc, nonfinite);
+                                         nloc, nonfinite, dirs_ready ? 1 : 0);
   LAUNCH_CHECK();
   k_stack_normalize<R><<<int(n), 256, 0, st>>>(rad, dist, nloc, live, n, stacks, s_r, s_d, nhwc,
                                                 nhwc_kind, cpad);
