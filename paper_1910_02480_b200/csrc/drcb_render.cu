@@ -291,7 +291,8 @@ __global__ void __launch_bounds__(MAP_TPB, MAP_CTAS) k_map_paths(DevScene S, Drc
                                                           const uint8_t* __restrict__ live,
                                                           int64_t total, unsigned long long* counter,
                                                           R* rad, R* dist, R* nloc,
-                                                          int64_t* nonfinite, int tab) {
+                                                          int64_t* nonfinite, int tab,
+                                                          const R* __restrict__ frames) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   bool have = false, done_all = false;
@@ -335,7 +336,8 @@ __global__ void __launch_bounds__(MAP_TPB, MAP_CTAS) k_map_paths(DevScene S, Drc
       tex = ((blk >> 2) * 4 + (w >> 3)) * MAP_RES + (blk & 3) * 8 + (w & 7);
       slot = p * MAP_TEXELS + tex;
       V3<R> hp = ldr3(pos + 3 * p), hn = ldr3(nrm + 3 * p);
-      Frame<R> fr = frame_scalar(S, hn);
+      const R* F = frames + 9 * p;  // k_point_frames: frame_scalar of the point normal
+      Frame<R> fr{ldr3(F), ldr3(F + 3), ldr3(F + 6)};
       D = fr.to_world(tab ? ldr3(g_texel_dirs<R> + 3 * tex) : texel_local<R>(tex % MAP_RES, tex / MAP_RES));
       O = hp + R(T_EPS) * hn;
     }
@@ -343,7 +345,8 @@ __global__ void __launch_bounds__(MAP_TPB, MAP_CTAS) k_map_paths(DevScene S, Drc
     SurfHit<R> h = intersect(S, O, D);
     if (fresh) {
       // first-hit features: distance and front-facing normal in the map frame
-      Frame<R> fr = frame_scalar(S, ldr3(nrm + 3 * p));
+      const R* F = frames + 9 * p;
+      Frame<R> fr{ldr3(F), ldr3(F + 3), ldr3(F + 6)};
       bool facing = dot(h.normal, D) > R(0);
       V3<R> nf3 = facing ? -h.normal : h.normal;
       dist[slot] = h.hit ? h.t : R(0);
@@ -1055,7 +1058,7 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
   int64_t total = int64_t(per);
   int g = int(std::min<int64_t>(grid, (total + MAP_TPB - 1) / MAP_TPB));
   k_map_paths<R><<<g, MAP_TPB, 0, st>>>(S, cfg, pos, nrm, keys, live, total, counter, rad, dist,
-                                         nloc, nonfinite, dirs_ready ? 1 : 0);
+                                         nloc, nonfinite, dirs_ready ? 1 : 0, frames);
   LAUNCH_CHECK();
   k_stack_normalize<R><<<int(n), 256, 0, st>>>(rad, dist, nloc, live, n, stacks, s_r, s_d, nhwc,
                                                 nhwc_kind, cpad);
