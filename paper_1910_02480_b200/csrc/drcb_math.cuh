@@ -95,6 +95,12 @@ struct PathRng {
     seed = seed_; pix = pix_; smp = smp_; kind = kind_; spp = spp_;
     prefix = hash_step(hash_step(hash_step(SEED0, seed), pix), smp);
   }
+  // the same, with hash_step(hash_step(SEED0, seed), pix) precomputed
+  DRCB_HD void init_pre(uint64_t pre2, uint64_t seed_, uint64_t pix_, uint64_t smp_, int kind_,
+                        uint32_t spp_) {
+    seed = seed_; pix = pix_; smp = smp_; kind = kind_; spp = spp_;
+    prefix = hash_step(pre2, smp);
+  }
   DRCB_HD double sample(uint64_t dim) const {
     double jitter = u53(hash_step(prefix, dim));
     if (kind == 0 || spp == 1) return jitter;

@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(MAP_TPB, MAP_CTAS) k_map_paths(DevScene S, Drc
                                                           int64_t total, unsigned long long* counter,
                                                           R* rad, R* dist, R* nloc,
                                                           int64_t* nonfinite, int tab,
-                                                          const R* __restrict__ frames) {
+                                                          const R* __restrict__ frames,
+                                                          const uint64_t* __restrict__ pre2) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   bool have = false, done_all = false;
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(MAP_TPB, MAP_CTAS) k_map_paths(DevScene S, Drc
       V3<R> nf3 = facing ? -h.normal : h.normal;
       dist[slot] = h.hit ? h.t : R(0);
       st3(nloc + 3 * slot, h.hit ? fr.to_local(nf3) : mk<R>(R(0), R(0), R(0)));
-      rng.init(cfg.seed, keys[p], uint64_t(tex), cfg.sampler_kind,
+      rng.init_pre(pre2[p], cfg.seed, keys[p], uint64_t(tex), cfg.sampler_kind,
                uint32_t(cfg.map_spp > 1 ? cfg.map_spp : 1));
       L = mk<R>(R(0), R(0), R(0));
       beta = mk<R>(R(1), R(1), R(1));
@@ -420,9 +421,13 @@ __global__ void __launch_bounds__(MAP_TPB, MAP_CTAS) k_map_paths(DevScene S, Drc
 
 // cache-point frames (build_frame of the front normal, hemimap.py:238)
 template <typename R>
-__global__ void k_point_frames(DevScene S, const R* __restrict__ nrm, int64_t n, R* frames) {
+__global__ void k_point_frames(DevScene S, const R* __restrict__ nrm, int64_t n, R* frames,
+                               const uint64_t* __restrict__ keys = nullptr, uint64_t seed = 0,
+                               uint64_t* pre2 = nullptr) {
   int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n) return;
+  // the per-point part of the path samplers' hash prefix (PathRng::init_pre)
+  if (pre2) pre2[p] = hash_step(hash_step(SEED0, seed), keys[p]);
   Frame<R> fr = frame_scalar(S, ldr3(nrm + 3 * p));
   st3(frames + 9 * p, fr.t);
   st3(frames + 9 * p + 3, fr.b);
@@ -1026,13 +1031,14 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
   if (n <= 0) return 0;
   size_t per = size_t(n) * MAP_TEXELS;
   R* scratch = nullptr;
-  DRCB_CUDA(cudaMallocAsync((void**)&scratch, per * 7 * sizeof(R) + 64, st));
+  DRCB_CUDA(cudaMallocAsync((void**)&scratch, per * 7 * sizeof(R) + 64 + size_t(n) * 8, st));
   R* rad = scratch;
   R* dist = scratch + 3 * per;
   R* nloc = scratch + 4 * per;
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(scratch + 7 * per);
+  uint64_t* pre2 = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(scratch + 7 * per) + 64);
   DRCB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
-  k_point_frames<R><<<nblocks(n), TPB, 0, st>>>(S, nrm, n, frames);
+  k_point_frames<R><<<nblocks(n), TPB, 0, st>>>(S, nrm, n, frames, keys, cfg.seed, pre2);
   LAUNCH_CHECK();
   // the table is filled once, synchronously, outside any graph capture (the
   // path kernel evaluates texel_local itself until then: frames on other
@@ -1058,7 +1064,7 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
   int64_t total = int64_t(per);
   int g = int(std::min<int64_t>(grid, (total + MAP_TPB - 1) / MAP_TPB));
   k_map_paths<R><<<g, MAP_TPB, 0, st>>>(S, cfg, pos, nrm, keys, live, total, counter, rad, dist,
-                                         nloc, nonfinite, dirs_ready ? 1 : 0, frames);
+                                         nloc, nonfinite, dirs_ready ? 1 : 0, frames, pre2);
   LAUNCH_CHECK();
   k_stack_normalize<R><<<int(n), 256, 0, st>>>(rad, dist, nloc, live, n, stacks, s_r, s_d, nhwc,
                                                 nhwc_kind, cpad);
