@@ -336,11 +336,11 @@ __global__ void __launch_bounds__(MAP_TPB, MAP_CTAS) k_map_paths(DevScene S, Drc
       const int k = int(job % MAP_TEXELS), blk = k >> 5, w = k & 31;
       tex = ((blk >> 2) * 4 + (w >> 3)) * MAP_RES + (blk & 3) * 8 + (w & 7);
       slot = p * MAP_TEXELS + tex;
-      V3<R> hp = ldr3(pos + 3 * p), hn = ldr3(nrm + 3 * p);
+      const V3<R> hp = ldr3(pos + 3 * p);
       const R* F = frames + 9 * p;  // k_point_frames: frame_scalar of the point normal
-      Frame<R> fr{ldr3(F), ldr3(F + 3), ldr3(F + 6)};
+      Frame<R> fr{ldr3(F), ldr3(F + 3), ldr3(F + 6)};  // fr.n is the point normal itself
       D = fr.to_world(tab ? ldr3(g_texel_dirs<R> + 3 * tex) : texel_local<R>(tex % MAP_RES, tex / MAP_RES));
-      O = hp + R(T_EPS) * hn;
+      O = hp + R(T_EPS) * fr.n;
     }
     // single traversal call site for fresh and continuing lanes
     SurfHit<R> h = intersect(S, O, D);
