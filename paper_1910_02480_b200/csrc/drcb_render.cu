@@ -1043,7 +1043,12 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
   // the table is filled once, synchronously, outside any graph capture (the
   // path kernel evaluates texel_local itself until then: frames on other
   // streams must never see a half-written table)
-  static bool dirs_ready = false;  // per precision (one instantiation each)
+  // per precision (one instantiation each) and per device (each device has
+  // its own copy of the __device__ table)
+  static bool dirs_ready_dev[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  bool& dirs_ready = dirs_ready_dev[dev & 63];
   if (!dirs_ready) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);
