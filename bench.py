@@ -328,6 +328,39 @@ def traversal_traffic():
     return json.load(open(files[-1])).get("kernels")
 
 
+def network_modes(cnn, net, n_maps=4096, iters=10):
+    """Secondary: one U-Net forward of n_maps through each tensor-core operand
+    mode (CUDA-event timed, device-resident input), TFLOP/s against the
+    measured dense bf16 peak (fp16 runs at the bf16 tensor rate; tf32 at half
+    of it). bf16 = the BASELINE precision; fp16 = the 16-bit mode that meets
+    the 1e-2 bar on every BASELINE weight set (tests/test_gpu_tc.py)."""
+    import torch
+
+    peaks, _ = measured_peaks()
+    dn = cnn.device_net(net)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.rand((n_maps, 7, 32, 32), device="cuda", generator=g)
+    x[:, :3] *= 10.0
+    y = torch.empty((n_maps, 3, 32, 32), device="cuda")
+    out = {}
+    for mode, peak in (("bf16", peaks.get("bf16_tflops", 1590.0)),
+                       ("fp16", peaks.get("bf16_tflops", 1590.0)),
+                       ("tf32", peaks.get("bf16_tflops", 1590.0) / 2)):
+        for _ in range(2):
+            dn.forward_device(x, y, mode=mode)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            dn.forward_device(x, y, mode=mode)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        tf = n_maps * cnn.flops_per_map(64) / (ms * 1e-3) / 1e12
+        out[mode] = {"ms": ms, "tflops": tf, "frac_of_mode_peak": tf / peak, "mode_peak": peak}
+    return out
+
+
 def network_traffic(n_maps):
     """DRAM bytes (read + write) of one U-Net forward over n_maps, scaled from
     the committed ncu capture (profiles/*_network_traffic.json, 4,096 maps);
@@ -352,7 +385,7 @@ def main():
     direct_spp = args.direct_spp or (4 if args.config == "c4" else 1)  # BASELINE config 4: 4 spp
     cfg = render.RenderConfig(direct_spp=direct_spp, indirect_tasks=args.tasks, mis_samples=16,
                               max_path_depth=8, rr_start=5, seed=0, precision=args.precision,
-                              net_mode=args.net if args.net in ("fp32", "tf32", "bf16") else "fp32")
+                              net_mode=args.net if args.net in ("fp32", "tf32", "bf16", "fp16") else "fp32")
     workload = {"workload": f"{args.config}: DRC frames {res[0]}x{res[1]}, "
                             f"{args.frames} frames/rank/step, indirect_tasks={args.tasks}, "
                             f"direct_spp={direct_spp}, orbit cameras r=3 (seed 2)",
@@ -647,6 +680,10 @@ def main():
         except Exception as e:  # secondary figure; never breaks the GPU line
             train = {"error": repr(e)}
     secondary = {}
+    try:
+        secondary["network_modes_4096_maps"] = network_modes(cnn, net)
+    except Exception as e:  # secondary figure; never breaks the GPU line
+        secondary["network_modes_4096_maps"] = {"error": repr(e)}
     if not args.no_secondary:
         for key, c_, tk in (("c4_1080p", "c4", 1), ("c3_tasks16", "c3", 16)):
             try:

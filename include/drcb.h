@@ -111,7 +111,11 @@ int drcb_scene_stats(const DrcbScene *scene, int64_t *out8);
 /* ---- stage kernels ---------------------------------------------------- */
 /* intersect_batch / occluded_batch (drc/geometry.py:217-329).
  * O, D: (n,3) Real; tmin/tmax: (n,) Real or NULL (T_EPS / +inf).
- * record=0 fills hit/t/prim only. */
+ * record=0 fills hit/t/prim only.
+ * precision DRCB_PREC_MIXED: the fp32 build's traversal of fp64 rays (every
+ * buffer fp64), candidates whose fp32 decision lies within its rounding bound
+ * re-tested in fp64 against the fp64 ray — the G-buffer's primary casts. */
+#define DRCB_PREC_MIXED 3264
 int drcb_intersect(const DrcbScene *scene, int32_t precision, const void *O,
                    const void *D, int64_t n, const void *tmin, const void *tmax,
                    int32_t record, uint8_t *hit, void *t, int64_t *prim,
@@ -222,10 +226,13 @@ void drcb_net_destroy(DrcbNet *net);
 int drcb_net_info(const DrcbNet *net, int64_t *out4);
 /* forward (drc/cnn.py:193-215; trainer model.py:80-88 eval mode):
  * x (n,7,32,32) f32 -> y (n,3,32,32) f32.
- * mode: 0 fp32 SIMT (exact), 1 tf32 tcgen05, 2 bf16 tcgen05. */
+ * mode: 0 fp32 SIMT (exact), 1 tf32 tcgen05, 2 bf16 tcgen05, 3 fp16 tcgen05
+ * (16-bit operands with a 10-bit mantissa at the bf16 tensor rate; fp32
+ * accumulation and epilogue in every tensor-core mode). */
 #define DRCB_NET_FP32 0
 #define DRCB_NET_TF32 1
 #define DRCB_NET_BF16 2
+#define DRCB_NET_FP16 3
 int drcb_net_forward(const DrcbNet *net, const float *x, float *y, int64_t n,
                      int32_t mode, void *stream);
 

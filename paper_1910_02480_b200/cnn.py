@@ -29,7 +29,7 @@ DEFAULT_LEAKY_SLOPE = 0.01
 BN_EPS = 1e-5
 IN_CHANNELS = 7
 OUT_CHANNELS = 3
-MODES = {"fp32": 0, "tf32": 1, "bf16": 2}
+MODES = {"fp32": 0, "tf32": 1, "bf16": 2, "fp16": 3}
 
 
 def architecture(k):

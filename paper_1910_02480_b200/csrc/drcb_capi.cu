@@ -219,7 +219,7 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
     void* xin = nullptr;
     int cpad = tc ? tc_input_channels(net_mode) : 0;
     if (tc && np_ <= 8192) {
-      size_t xb = size_t(np8) * 1024 * cpad * (net_mode == DRCB_NET_BF16 ? 2 : 4);
+      size_t xb = size_t(np8) * 1024 * cpad * (net_mode == DRCB_NET_TF32 ? 4 : 2);
       DRCB_CUDA(cudaMallocAsync(&xin, xb, st));
       if (np8 > np_)
         DRCB_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(xin) + xb / np8 * np_, 0,
@@ -227,7 +227,8 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
     }
     rc = launch_render_stacks<R>(S, *cfg, pos, nrm, keys, live, np_, xin ? nullptr : stacks, s_r,
                                  s_d, frames, d_nf, st, xin,
-                                 xin ? (net_mode == DRCB_NET_BF16 ? 1 : 2) : 0, cpad);
+                                 xin ? (net_mode == DRCB_NET_BF16 ? 1 : (net_mode == DRCB_NET_FP16 ? 3 : 2)) : 0,
+                                 cpad);
     if (rc) return rc;
     E.rec(2, st);
     if (!tc)
@@ -311,6 +312,10 @@ extern "C" int drcb_intersect(const DrcbScene* scene, int32_t precision, const v
                               void* pos, void* nrm, void* stream) {
   NEED(scene);
   NEED(hit);
+  if (precision == DRCB_PREC_MIXED)
+    return launch_intersect_mixed(scene->dev, (const double*)O, (const double*)D, n,
+                                  (const double*)tmin, (const double*)tmax, record, hit,
+                                  (double*)t, prim, mat, (double*)pos, (double*)nrm, S_(stream));
   if (check_precision(precision)) return DRCB_ECONFIG;
   if (precision == 64)
     return launch_intersect<double>(scene->dev, (const double*)O, (const double*)D, n,
@@ -513,7 +518,7 @@ extern "C" int drcb_net_forward(const DrcbNet* net, const float* x, float* y, in
   NEED(x);
   NEED(y);
   if (mode == DRCB_NET_FP32) return forward_f32_chunked(net->impl, x, y, n, S_(stream));
-  if (mode == DRCB_NET_TF32 || mode == DRCB_NET_BF16)
+  if (mode == DRCB_NET_TF32 || mode == DRCB_NET_BF16 || mode == DRCB_NET_FP16)
     return forward_tc(const_cast<DrcbNet*>(net)->impl, x, y, n, mode, S_(stream));
   return fail(DRCB_ECONFIG, "unknown network mode");
 }

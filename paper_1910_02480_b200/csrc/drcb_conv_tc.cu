@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cstdlib>
 #include <cstring>
@@ -126,10 +127,10 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
-template <int KIND>  // 0 = kind::f16 (bf16), 1 = kind::tf32
+template <int KIND>  // 0 = kind::f16 (bf16), 1 = kind::tf32, 2 = kind::f16 (fp16)
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                        uint32_t idesc, uint32_t accumulate) {
-  if constexpr (KIND == 0) {
+  if constexpr (KIND != 1) {
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
@@ -163,6 +164,33 @@ __device__ __forceinline__ float round_tf32(float v) {
   return __uint_as_float(r);
 }
 
+// Operand element of each KIND: 0 = bf16, 1 = fp32 holding tf32-rounded
+// values, 2 = fp16 (kind::f16 with the F16 format: the same tensor rate as
+// bf16 with a 10-bit mantissa, i.e. tf32's operand precision)
+__host__ __device__ constexpr int elem_bytes(int kind) { return kind == 1 ? 4 : 2; }
+template <int KIND>
+using ElemT = typename std::conditional<KIND == 1, float,
+                                        typename std::conditional<KIND == 2, __half, __nv_bfloat16>::type>::type;
+template <int KIND>
+using Elem2T = typename std::conditional<KIND == 2, __half2, __nv_bfloat162>::type;
+// two fp32 values rounded to nearest into one packed 16-bit pair
+template <int KIND>
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  if constexpr (KIND == 2) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+template <typename H2>
+__device__ __forceinline__ H2 splat2(float v);
+template <>
+__device__ __forceinline__ __nv_bfloat162 splat2<__nv_bfloat162>(float v) { return __float2bfloat162_rn(v); }
+template <>
+__device__ __forceinline__ __half2 splat2<__half2>(float v) { return __float2half2_rn(v); }
+
 // SMEM matrix descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart
 // (cute::UMMA::SmemDescriptor: start>>4 @0, LBO>>4 @16, SBO>>4 @32,
 // version 1 @46, layout SWIZZLE_128B=2 @61).
@@ -179,7 +207,8 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // instruction descriptor (cute::UMMA::InstrDescriptor): D f32, A/B format,
 // both K-major, N>>3 @17, M>>4 @24
 __host__ __device__ constexpr uint32_t make_idesc(int kind, int M, int N) {
-  uint32_t fmt = kind == 0 ? 1u /*BF16*/ : 2u /*TF32*/;
+  // kind::f16: F16 = 0, BF16 = 1; kind::tf32: TF32 = 2
+  uint32_t fmt = kind == 0 ? 1u /*BF16*/ : (kind == 2 ? 0u /*F16*/ : 2u /*TF32*/);
   return (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
@@ -229,7 +258,7 @@ struct ConvArgs {
 
 template <int KIND, int BN, int STAGES>
 struct Smem {
-  static constexpr int ELEM = KIND == 0 ? 2 : 4;
+  static constexpr int ELEM = elem_bytes(KIND);
   static constexpr int A_BYTES = BM * ROW_BYTES;
   static constexpr int B_BYTES = BN * ROW_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -350,14 +379,11 @@ __device__ __forceinline__ void epilogue_tile(const ConvArgs& p, uint32_t tbase,
       acc_chunk<BN, DX>(tbase, c0, xpix, p.hw, acc);
       float v[16];
       bn_lrelu16(acc, p.ep_a + cg, p.ep_b + cg, p.slope, v);
-      if constexpr (KIND == 0) {
+      if constexpr (KIND != 1) {
         uint32_t pk[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-          pk[j] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
+        for (int j = 0; j < 8; ++j) pk[j] = pack2<KIND>(v[2 * j], v[2 * j + 1]);
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) +
                                               m * p.cout_tot + p.cout_off + cg);
         dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
@@ -522,7 +548,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 template <int KIND, int BN, bool DX, int CSTEP>
 __device__ __forceinline__ void epilogue_stage(const ConvArgs& p, uint32_t tbase, int64_t m, int nt,
                                                uint8_t* ost, int cbeg, uint32_t sep = 0) {
-  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int ELEM = elem_bytes(KIND);
   constexpr int CEL = ROW_BYTES / ELEM;
   const int xpix = int(m & int64_t(p.hw - 1));  // hw is a power of two
   const int r = int(m & (BM - 1));
@@ -548,13 +574,10 @@ __device__ __forceinline__ void epilogue_stage(const ConvArgs& p, uint32_t tbase
       bn_lrelu16(acc, p.ep_a + cg, p.ep_b + cg, p.slope, v);
     const uint32_t sub = ost_s + (c0 / CEL) * (BM * ROW_BYTES) + r * ROW_BYTES;
     const int jb = (c0 % CEL) * ELEM / 16;
-    if constexpr (KIND == 0) {
+    if constexpr (KIND != 1) {
       uint32_t pk[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-        pk[j] = *reinterpret_cast<uint32_t*>(&b2);
-      }
+      for (int j = 0; j < 8; ++j) pk[j] = pack2<KIND>(v[2 * j], v[2 * j + 1]);
       sts128(sub + (((jb + 0) ^ (r & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
       sts128(sub + (((jb + 1) ^ (r & 7)) << 4), pk[4], pk[5], pk[6], pk[7]);
     } else {
@@ -576,26 +599,27 @@ __device__ __forceinline__ void unpack8_bf16(const uint4& u, float (&f)[8]) {
   }
 }
 
-// bilinear mix of four 16-B bf16 vectors (p00, p10, p01, p11) in packed bf16x2
-// arithmetic: t0 = fma(p00, omr, p10*fr), t1 = fma(p01, omr, p11*fr),
-// v = fma(t0, omc, t1*fc)
-// (the weights 0, 0.25, 0.75, 1 are exact in bf16)
-__device__ __forceinline__ void up_mix_bf16x2(const uint4 (&q)[4], float omr, float fr, float omc,
-                                              float fc, uint32_t (&out)[4]) {
-  const __nv_bfloat162 wr0 = __float2bfloat162_rn(omr), wr1 = __float2bfloat162_rn(fr);
-  const __nv_bfloat162 wc0 = __float2bfloat162_rn(omc), wc1 = __float2bfloat162_rn(fc);
-  const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&q[0]);
-  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q[1]);
-  const __nv_bfloat162* c = reinterpret_cast<const __nv_bfloat162*>(&q[2]);
-  const __nv_bfloat162* d = reinterpret_cast<const __nv_bfloat162*>(&q[3]);
+// bilinear mix of four 16-B vectors of packed 16-bit pairs (H2 = bf16x2 or
+// fp16x2; p00, p10, p01, p11) in packed arithmetic:
+// t0 = fma(p00, omr, p10*fr), t1 = fma(p01, omr, p11*fr), v = fma(t0, omc, t1*fc)
+// (the weights 0, 0.25, 0.75, 1 are exact in both formats)
+template <typename H2>
+__device__ __forceinline__ void up_mix_h2(const uint4 (&q)[4], float omr, float fr, float omc,
+                                          float fc, uint32_t (&out)[4]) {
+  const H2 wr0 = splat2<H2>(omr), wr1 = splat2<H2>(fr);
+  const H2 wc0 = splat2<H2>(omc), wc1 = splat2<H2>(fc);
+  const H2* a = reinterpret_cast<const H2*>(&q[0]);
+  const H2* b = reinterpret_cast<const H2*>(&q[1]);
+  const H2* c = reinterpret_cast<const H2*>(&q[2]);
+  const H2* d = reinterpret_cast<const H2*>(&q[3]);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     // explicit fused forms (one rounded product, one fma): the compiler may
     // not contract them differently per call site, so every caller (the
     // upsample kernel, the fused dec2.deconv2 epilogue) computes the same bits
-    const __nv_bfloat162 t0 = __hfma2(a[i], wr0, __hmul2_rn(b[i], wr1));
-    const __nv_bfloat162 t1 = __hfma2(c[i], wr0, __hmul2_rn(d[i], wr1));
-    const __nv_bfloat162 v = __hfma2(t0, wc0, __hmul2_rn(t1, wc1));
+    const H2 t0 = __hfma2(a[i], wr0, __hmul2_rn(b[i], wr1));
+    const H2 t1 = __hfma2(c[i], wr0, __hmul2_rn(d[i], wr1));
+    const H2 v = __hfma2(t0, wc0, __hmul2_rn(t1, wc1));
     out[i] = *reinterpret_cast<const uint32_t*>(&v);
   }
 }
@@ -611,11 +635,10 @@ __device__ __forceinline__ uint4 max4(uint4 a, uint4 b, uint4 c, uint4 d) {
   uint32_t* rr = reinterpret_cast<uint32_t*>(&r);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    if constexpr (KIND == 0) {
-      __nv_bfloat162 x = __hmax2(__hmax2(*reinterpret_cast<__nv_bfloat162*>(&ra[i]),
-                                         *reinterpret_cast<__nv_bfloat162*>(&rb[i])),
-                                 __hmax2(*reinterpret_cast<__nv_bfloat162*>(&rc[i]),
-                                         *reinterpret_cast<__nv_bfloat162*>(&rd[i])));
+    if constexpr (KIND != 1) {
+      using H2 = Elem2T<KIND>;
+      H2 x = __hmax2(__hmax2(*reinterpret_cast<H2*>(&ra[i]), *reinterpret_cast<H2*>(&rb[i])),
+                     __hmax2(*reinterpret_cast<H2*>(&rc[i]), *reinterpret_cast<H2*>(&rd[i])));
       rr[i] = *reinterpret_cast<uint32_t*>(&x);
     } else {
       rr[i] = __float_as_uint(fmaxf(fmaxf(__uint_as_float(ra[i]), __uint_as_float(rb[i])),
@@ -671,7 +694,7 @@ __global__ void __launch_bounds__(PW ? ROWS_THREADS : RT_THREADS, 1)
                 const __grid_constant__ ConvArgs p, const __grid_constant__ RowArgs h) {
   constexpr int B_TILE = BN * ROW_BYTES;
   constexpr int B3 = 3 * B_TILE;                       // one B stage: three weight tiles
-  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int ELEM = elem_bytes(KIND);
   constexpr int CEL = ROW_BYTES / ELEM;
   constexpr int NACCW = DX ? 3 * BN : BN;              // TMEM columns per M block
   // MH = 2: a work tile is two M blocks (BM rows each) sharing every A and B
@@ -1008,7 +1031,7 @@ __global__ void __launch_bounds__(PW ? ROWS_THREADS : RT_THREADS, 1)
                   const uint4 q[4] = {nbq[hb + a2][b2], nbq[hb + a2 + 1][b2], nbq[hb + a2][b2 + 1],
                                       nbq[hb + a2 + 1][b2 + 1]};
                   uint32_t pk[4];
-                  up_mix_bf16x2(q, 1.f - fr, fr, 1.f - fc, fc, pk);
+                  up_mix_h2<Elem2T<KIND>>(q, 1.f - fr, fr, 1.f - fc, fc, pk);
                   const int opx = ((2 * bi + a2) & 7) * 32 + 2 * bj + b2;  // pixel in the chunk
                   sts128(U0 + opx * ROW_BYTES + ((j ^ (opx & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
                 }
@@ -1159,6 +1182,7 @@ constexpr int HF_W2 = 9 * 16 * ROW_BYTES;    // 9 tiles of 16 rows
 constexpr int HF_ACC1 = 2 * 96;              // TMEM columns per head.deconv1 accumulator
 constexpr int HF_ACC2 = 2 * HF_ACC1;         // first head.deconv2 accumulator column
 
+template <int KIND>
 __global__ void __launch_bounds__(RT_THREADS, 1)
     k_head_fused(const __grid_constant__ CUtensorMap mapA10, const __grid_constant__ CUtensorMap mapA6,
                  const __grid_constant__ CUtensorMap mapW1, const __grid_constant__ CUtensorMap mapW2,
@@ -1232,8 +1256,8 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc1 = make_idesc(0, BM, 96);
-      constexpr uint32_t idesc2 = make_idesc(0, BM, 48);
+      constexpr uint32_t idesc1 = make_idesc(KIND, BM, 96);
+      constexpr uint32_t idesc2 = make_idesc(KIND, BM, 48);
       mbar_wait(wfull, 0);
       const uint32_t w1a = smem_u32(w1), w2a = smem_u32(w2);
       auto mma2 = [&](int kt) {  // head.deconv2 of item kt: 3 dy x 2 K steps
@@ -1246,7 +1270,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
         for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
           for (int k = 0; k < 2; ++k)
-            tc_mma<0>(tmem_base + HF_ACC2 + b * 48, sw128_desc(a2a + dy * HF_ROW + 32 * k),
+            tc_mma<KIND>(tmem_base + HF_ACC2 + b * 48, sw128_desc(a2a + dy * HF_ROW + 32 * k),
                       sw128_desc(w2a + dy * 3 * 16 * ROW_BYTES + 32 * k), idesc2, (dy | k) ? 1u : 0u);
         tc_commit(&a2empty[b]);
         tc_commit(&acc2full[b]);
@@ -1265,7 +1289,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
           for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
             for (int k = 0; k < ROW_BYTES / 32; ++k)
-              tc_mma<0>(tmem_base + s * HF_ACC1 + b * 96,
+              tc_mma<KIND>(tmem_base + s * HF_ACC1 + b * 96,
                         sw128_desc(a1a + (4 * b + dy) * HF_ROW + 32 * k),
                         sw128_desc(w1a + dy * 3 * 32 * ROW_BYTES + 32 * k), idesc1, (dy | k) ? 1u : 0u);
         tc_commit(&a1empty[s]);
@@ -1357,10 +1381,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
         const bool inside = row < 32;
         uint32_t pk[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(inside ? v[2 * i] : 0.f, inside ? v[2 * i + 1] : 0.f);
-          pk[i] = *reinterpret_cast<uint32_t*>(&b2);
-        }
+        for (int i = 0; i < 8; ++i) pk[i] = pack2<KIND>(inside ? v[2 * i] : 0.f, inside ? v[2 * i + 1] : 0.f);
         const int slot = row - (4 * t - 1);  // slot in this item's A2 (rows 4t-1 ..)
         put(s, slot, pk);
         // rows 4t+3, 4t+4 are rows 4(t+1)-1, 4(t+1) of the next item
@@ -1455,12 +1476,12 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
                : "memory");
 }
 
-template <int BN, bool RES>
+template <int KIND, int BN, bool RES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RT_THREADS, 1)
     k_conv_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 const __grid_constant__ CUtensorMap mapO, const __grid_constant__ ConvArgs p,
                 const __grid_constant__ RowArgs h) {
-  constexpr int KIND = 0;
+  static_assert(KIND != 1, "16-bit operands");
   constexpr int ELEM = 2;
   constexpr int CEL = ROW_BYTES / ELEM;
   static_assert(BN == CEL, "one 128-B staging sub-tile per pixel");
@@ -1689,7 +1710,7 @@ template <int KIND>
 __global__ void __launch_bounds__(IN8_THREADS, 1)
     k_conv_in8(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapB,
                const __grid_constant__ CUtensorMap mapO, const __grid_constant__ ConvArgs p) {
-  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int ELEM = elem_bytes(KIND);
   constexpr int PX_BYTES = 8 * ELEM;                  // one input pixel
   constexpr int PPT = PX_BYTES / 16;                  // 16-B pieces per tap
   constexpr int NCH = (72 * ELEM + ROW_BYTES - 1) / ROW_BYTES;  // K chunks
@@ -1904,7 +1925,7 @@ __global__ void __launch_bounds__(IN8_THREADS, 1)
 
 template <int KIND>
 constexpr size_t in8_smem() {
-  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int ELEM = elem_bytes(KIND);
   constexpr int NCH = (72 * ELEM + ROW_BYTES - 1) / ROW_BYTES;
   return 1024 + size_t(IN8_SA) * NCH * BM * ROW_BYTES + size_t(NCH) * 64 * ROW_BYTES +
          2 * size_t(BM) * 64 * ELEM + size_t(IN8_SI) * 6 * 32 * 8 * ELEM + 256;
@@ -1917,11 +1938,15 @@ __device__ __forceinline__ float ldf(const T* p);
 template <>
 __device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 template <>
+__device__ __forceinline__ float ldf<__half>(const __half* p) { return __half2float(*p); }
+template <>
 __device__ __forceinline__ float ldf<float>(const float* p) { return *p; }
 template <typename T>
 __device__ __forceinline__ T stf(float v);
 template <>
 __device__ __forceinline__ __nv_bfloat16 stf<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+template <>
+__device__ __forceinline__ __half stf<__half>(float v) { return __float2half_rn(v); }
 template <>
 __device__ __forceinline__ float stf<float>(float v) { return round_tf32(v); }
 
@@ -1944,6 +1969,16 @@ __device__ __forceinline__ void unpack<__nv_bfloat16>(const uint4& u, float* f) 
   }
 }
 template <>
+__device__ __forceinline__ void unpack<__half>(const uint4& u, float* f) {
+  const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float2 t = __half22float2(h[j]);
+    f[2 * j] = t.x;
+    f[2 * j + 1] = t.y;
+  }
+}
+template <>
 __device__ __forceinline__ void unpack<float>(const uint4& u, float* f) {
   f[0] = __uint_as_float(u.x);
   f[1] = __uint_as_float(u.y);
@@ -1961,6 +1996,14 @@ __device__ __forceinline__ uint4 pack<__nv_bfloat16>(const float* f) {
     __nv_bfloat162 b = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
     w[j] = *reinterpret_cast<uint32_t*>(&b);
   }
+  return u;
+}
+template <>
+__device__ __forceinline__ uint4 pack<__half>(const float* f) {
+  uint4 u;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) w[j] = pack2<2>(f[2 * j], f[2 * j + 1]);
   return u;
 }
 template <>
@@ -2042,9 +2085,10 @@ __global__ void __launch_bounds__(256) k_up_nhwc(const T* __restrict__ in, T* __
   const int j = int(blk % HW_IN), i = int((blk / HW_IN) % HW_IN);
   const int64_t n = blk / (HW_IN * HW_IN);
   const T* b = in + n * HW_IN * HW_IN * C + g;
-  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-    // bf16: packed bf16x2 mixing (up_mix_bf16x2), the same arithmetic as the
+  if constexpr (sizeof(T) == 2) {
+    // bf16 / fp16: packed mixing (up_mix_h2), the same arithmetic as the
     // upsample fused into dec2.deconv2's epilogue
+    using H2 = typename std::conditional<std::is_same<T, __half>::value, __half2, __nv_bfloat162>::type;
     uint4 nbq[3][3];
 #pragma unroll
     for (int dr = 0; dr < 3; ++dr) {
@@ -2064,7 +2108,7 @@ __global__ void __launch_bounds__(256) k_up_nhwc(const T* __restrict__ in, T* __
         const float fc = bb ? 0.25f : fc_even;
         const uint4 q[4] = {nbq[a][bb], nbq[a + 1][bb], nbq[a][bb + 1], nbq[a + 1][bb + 1]};
         uint32_t o[4];
-        up_mix_bf16x2(q, 1.f - fr, fr, 1.f - fc, fc, o);
+        up_mix_h2<H2>(q, 1.f - fr, fr, 1.f - fc, fc, o);
         const int64_t px = (n * HO + 2 * i + a) * HO + 2 * j + bb;
         *reinterpret_cast<uint4*>(out + px * c_tot + g) = make_uint4(o[0], o[1], o[2], o[3]);
       }
@@ -2163,17 +2207,22 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+CUtensorMapDataType tmap_dtype(int kind) {
+  return kind == 0 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                   : (kind == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+}
+
 int encode_act(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
                int box_w, int box_h, int box_n) {
   auto enc = get_encode();
   if (!enc) return fail(DRCB_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  const int es = kind == 0 ? 2 : 4;
+  const int es = elem_bytes(kind);
   cuuint64_t dims[4] = {cuuint64_t(c_tot), cuuint64_t(hw), cuuint64_t(hw), cuuint64_t(nmaps)};
   cuuint64_t strides[3] = {cuuint64_t(c_tot) * es, cuuint64_t(c_tot) * es * hw,
                            cuuint64_t(c_tot) * es * hw * hw};
   cuuint32_t box[4] = {cuuint32_t(ROW_BYTES / es), cuuint32_t(box_w), cuuint32_t(box_h), cuuint32_t(box_n)};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(m, kind == 0 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+  CUresult r = enc(m, tmap_dtype(kind), 4,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -2184,12 +2233,12 @@ int encode_act(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, in
 int encode_w(CUtensorMap* m, const void* base, int kind, int64_t k_tot, int rows, int bn) {
   auto enc = get_encode();
   if (!enc) return fail(DRCB_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  const int es = kind == 0 ? 2 : 4;
+  const int es = elem_bytes(kind);
   cuuint64_t dims[2] = {cuuint64_t(k_tot), cuuint64_t(rows)};
   cuuint64_t strides[1] = {cuuint64_t(k_tot) * es};
   cuuint32_t box[2] = {cuuint32_t(ROW_BYTES / es), cuuint32_t(bn)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, kind == 0 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+  CUresult r = enc(m, tmap_dtype(kind), 2,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -2207,7 +2256,7 @@ float host_round_tf32(float v) {
 }
 
 int pad_c(int c, int kind) {
-  int g = kind == 0 ? 64 : 32;
+  int g = ROW_BYTES / elem_bytes(kind);
   return ((c + g - 1) / g) * g;
 }
 
@@ -2216,7 +2265,7 @@ int prepare_layer(NetImpl& net, ConvLayer& L, int kind) {
   if (L.tc_kind == kind) return 0;
   L.in8 = (L.name == "enc1.conv1" && L.cin <= 8);
   // in8: K = 9 taps x 8 channels rounded up to whole 128-B rows
-  const int cinp = L.in8 ? ((72 * (kind == 0 ? 2 : 4) + ROW_BYTES - 1) / ROW_BYTES) * (ROW_BYTES / (kind == 0 ? 2 : 4))
+  const int cinp = L.in8 ? ((72 * elem_bytes(kind) + ROW_BYTES - 1) / ROW_BYTES) * (ROW_BYTES / elem_bytes(kind))
                          : pad_c(L.cin, kind);
   // output channels are padded to the next layer's K granularity; padded
   // channels get zero weights and zero epilogue vectors, so they hold exact
@@ -2225,7 +2274,7 @@ int prepare_layer(NetImpl& net, ConvLayer& L, int kind) {
   // A row-tile layer (hw >= 16) with fewer outputs than one 128-B row
   // (bf16 head.deconv1: 32) computes N = cout rounded to 16 and its epilogue
   // zero-fills the rest of the row, which the next layer's K padding reads.
-  const int cel = kind == 0 ? 64 : 32;
+  const int cel = ROW_BYTES / elem_bytes(kind);
   const int coutp = (L.name == "head.deconv2") ? 16
                     : (L.hw >= 16 && L.cout < cel && L.name != "enc1.conv1") ? (L.cout + 15) / 16 * 16
                                                     : pad_c(L.cout, kind);
@@ -2247,6 +2296,14 @@ int prepare_layer(NetImpl& net, ConvLayer& L, int kind) {
       for (int ci = 0; ci < L.cin; ++ci)
         for (int t = 0; t < 9; ++t)
           w[size_t(co) * ktot + kidx(ci, t)] = __float2bfloat16(L.w[(size_t(co) * L.cin + ci) * 9 + t]);
+    if (cudaMalloc(&dw, nel * 2) != cudaSuccess) return fail(DRCB_ECUDA, "cudaMalloc weights");
+    cudaMemcpy(dw, w.data(), nel * 2, cudaMemcpyHostToDevice);
+  } else if (kind == 2) {
+    std::vector<__half> w(nel, __float2half_rn(0.f));
+    for (int co = 0; co < L.cout; ++co)
+      for (int ci = 0; ci < L.cin; ++ci)
+        for (int t = 0; t < 9; ++t)
+          w[size_t(co) * ktot + kidx(ci, t)] = __float2half_rn(L.w[(size_t(co) * L.cin + ci) * 9 + t]);
     if (cudaMalloc(&dw, nel * 2) != cudaSuccess) return fail(DRCB_ECUDA, "cudaMalloc weights");
     cudaMemcpy(dw, w.data(), nel * 2, cudaMemcpyHostToDevice);
   } else {
@@ -2312,10 +2369,10 @@ int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorM
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_rows");
 }
 
-template <bool RES>
+template <int KIND, bool RES>
 int launch_pair64(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
                   const ConvArgs& a, const RowArgs& h, size_t smem, cudaStream_t st) {
-  auto kern = k_conv_pair<64, RES>;
+  auto kern = k_conv_pair<KIND, 64, RES>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -2417,13 +2474,13 @@ int run_in8(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cout_
   a.out = out.p;
   auto enc = get_encode();
   if (!enc) return fail(DRCB_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  const int es = KIND == 0 ? 2 : 4;
+  const int es = elem_bytes(KIND);
   CUtensorMap mX, mB, mO;
   cuuint64_t dims[4] = {8, 32, 32, cuuint64_t(nmaps)};
   cuuint64_t strides[3] = {cuuint64_t(8 * es), cuuint64_t(8 * es * 32), cuuint64_t(8 * es * 1024)};
   cuuint32_t box[4] = {8, 32, 6, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(&mX, KIND == 0 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+  CUresult r = enc(&mX, tmap_dtype(KIND), 4,
                    in.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -2470,7 +2527,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     a.tiles_per_map = 1;
   }
   a.num_m_tiles = int(nmaps * hw * hw / BM);
-  a.cblocks = L.cin_pad / (ROW_BYTES / (KIND == 0 ? 2 : 4));
+  a.cblocks = L.cin_pad / (ROW_BYTES / elem_bytes(KIND));
   a.num_kb = 9 * a.cblocks;
   a.bn = n_tile(L.cout_pad, 256);
   a.num_n_tiles = L.cout_pad / a.bn;
@@ -2495,7 +2552,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     // row-tile kernel (hw 16/32); DRCB_ROWS=dx|halo overrides the variant
     static const char* mode_env = getenv("DRCB_ROWS");
     const bool dx = mode_env ? std::strcmp(mode_env, "dx") == 0 : rows_use_dx(L, KIND);
-    a.bn = n_tile(L.cout_pad, KIND == 0 ? 128 : 64);
+    a.bn = n_tile(L.cout_pad, KIND != 1 ? 128 : 64);
     a.num_n_tiles = L.cout_pad / a.bn;
     RowArgs rz;
     rz.up2 = 0;
@@ -2504,7 +2561,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     rz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
     int b_tile = a.bn * ROW_BYTES;
     const int w_bytes = 9 * a.cblocks * b_tile;
-    rz.o_bytes = pred ? 0 : BM * std::max(a.bn, ROW_BYTES / (KIND == 0 ? 2 : 4)) * (KIND == 0 ? 2 : 4);
+    rz.o_bytes = pred ? 0 : BM * std::max(a.bn, ROW_BYTES / elem_bytes(KIND)) * elem_bytes(KIND);
     rz.p_bytes = (pool && rz.o_bytes) ? rz.o_bytes / 4 : 0;
     const int budget = 216 * 1024 - 2 * rz.o_bytes - 2 * rz.p_bytes;  // of 227 KB
     const bool res = a.num_n_tiles == 1 && w_bytes + 3 * rz.a_bytes <= budget;
@@ -2521,7 +2578,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     // streamed-weight dx layers (dec1.deconv1, dec2.deconv1): two M blocks per
     // work tile share each weight stage (half the L2 weight traffic per
     // pixel; at 16x16 the tile is the whole map)
-    const bool two = dx && !res && KIND == 0 && a.bn <= 128 && L.cout_pad % 64 == 0 &&
+    const bool two = dx && !res && KIND != 1 && a.bn <= 128 && L.cout_pad % 64 == 0 &&
                      rz.o_bytes && !rz.p_bytes && getenv("DRCB_NO_MH2") == nullptr;
     if (two) {
       a.bn = 64;  // two M blocks x 3 dx accumulators of 64 columns = 384 TMEM columns
@@ -2539,7 +2596,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     }
     // streamed-weight dx layers without a fused upsample: CTA-pair kernel
     // (M = 256 across two SMs, double-buffered TMEM)
-    if (KIND == 0 && dx && !res && L.cout_pad == 64 && rz.o_bytes && !rz.p_bytes && !up &&
+    if (KIND != 1 && dx && !res && L.cout_pad == 64 && rz.o_bytes && !rz.p_bytes && !up &&
         getenv("DRCB_NO_PAIR") == nullptr) {
       RowArgs pz = rz;
       ConvArgs pa = a;
@@ -2574,15 +2631,16 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       if (rc) return rc;
       const size_t smem = 1024 + (pres ? size_t(wbytes) : size_t(pz.sb) * bhalf) + size_t(pz.sa) * pz.a_bytes +
                           2 * size_t(pz.o_bytes) + 512 + 8 * EP_MAX;
-      return pres ? launch_pair64<true>(pA, pB, pO, pa, pz, smem, st)
-                  : launch_pair64<false>(pA, pB, pO, pa, pz, smem, st);
+      constexpr int KP = KIND == 1 ? 0 : KIND;  // never reached for tf32 (16-bit operands only)
+      return pres ? launch_pair64<KP, true>(pA, pB, pO, pa, pz, smem, st)
+                  : launch_pair64<KP, false>(pA, pB, pO, pa, pz, smem, st);
     }
     // resident-weight 32x32 dx layers: two M blocks (8 rows) per work tile
     // halve the per-tile fixed costs and the halo re-reads (10 rows loaded
     // per 8 computed instead of 6 per 4)
     // (head.deconv1 / head.deconv2; at BN = 64 the 40 KB A stages leave too
     // few of them and the layer slows down)
-    bool two_res = !two && dx && res && KIND == 0 && a.bn <= 32 && hw == 32 && !rz.p_bytes &&
+    bool two_res = !two && dx && res && KIND != 1 && a.bn <= 32 && hw == 32 && !rz.p_bytes &&
                    !up && getenv("DRCB_NO_MH2") == nullptr;
     if (two_res) {
       const int a2 = (2 * BM / hw + 2) * hw * ROW_BYTES;
@@ -2636,7 +2694,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
       size_t smem = 1024 + size_t(res ? w_bytes : 0) + size_t(rz.sa) * rz.a_bytes +
                     size_t(res ? 0 : rz.sb * 3 * b_tile) + (rz.up2 ? 3 : 2) * size_t(rz.o_bytes) +
                     2 * size_t(rz.p_bytes) + 512 + 8 * EP_MAX;
-      if constexpr (KIND == 0) {
+      if constexpr (KIND != 1) {
         if (two) rc = launch_rows_bn<KIND, 64, false, true, 2>(mA, mB, mO, mP, a, rz, smem, st);
         if (two_res) {
           switch (a.bn) {
@@ -2645,11 +2703,11 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
           }
         }
       }
-      if ((!two && !two_res) || KIND != 0)
+      if ((!two && !two_res) || KIND == 1)
         rc = dx ? launch_rows<KIND, true>(mA, mB, mO, mP, a, rz, res, smem, st)
                 : launch_rows<KIND, false>(mA, mB, mO, mP, a, rz, res, smem, st);
       if (rc || !up_after) return rc;
-      using T = typename std::conditional<KIND == 0, __nv_bfloat16, float>::type;
+      using T = ElemT<KIND>;
       return up_dispatch<T>(static_cast<const T*>(out.p), L.cout_pad, hw, static_cast<T*>(up->p),
                             up->c, nmaps, st);
     }
@@ -2664,17 +2722,18 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
   rc = launch_conv<KIND>(mA, mB, a, st);
   if (rc || !pool) return rc;
   // this path has no fused pool: run the separate pass
-  using T = typename std::conditional<KIND == 0, __nv_bfloat16, float>::type;
+  using T = ElemT<KIND>;
   return pool_dispatch<T>(static_cast<const T*>(out.p), out.c, cout_off, L.cout_pad, hw / 2,
                           static_cast<T*>(pool->p), nmaps, st);
 }
 
-// head.deconv1 + head.deconv2 + conv_out in one kernel (bf16; see k_head_fused)
+// head.deconv1 + head.deconv2 + conv_out in one kernel (16-bit; see k_head_fused)
+template <int KIND>
 int run_head_fused(NetImpl& net, ConvLayer& L1, ConvLayer& L2, const Buf& in, int64_t nmaps,
                    float* pred, cudaStream_t st) {
-  int rc = prepare_layer(net, L1, 0);
+  int rc = prepare_layer(net, L1, KIND);
   if (rc) return rc;
-  rc = prepare_layer(net, L2, 0);
+  rc = prepare_layer(net, L2, KIND);
   if (rc) return rc;
   if (in.c != 64 || in.hw != 32 || L1.cin_pad != 64 || L1.cout_pad != 32 || L2.cin_pad != 64 ||
       L2.cout_pad != 16)
@@ -2698,24 +2757,24 @@ int run_head_fused(NetImpl& net, ConvLayer& L1, ConvLayer& L2, const Buf& in, in
     p2.hw_b[o] = H.bias[o];
   }
   CUtensorMap mA10, mA6, mW1, mW2;
-  rc = encode_act(&mA10, in.p, 0, in.c, 32, nmaps, 32, 10, 1);
+  rc = encode_act(&mA10, in.p, KIND, in.c, 32, nmaps, 32, 10, 1);
   if (rc) return rc;
-  rc = encode_act(&mA6, in.p, 0, in.c, 32, nmaps, 32, 6, 1);
+  rc = encode_act(&mA6, in.p, KIND, in.c, 32, nmaps, 32, 6, 1);
   if (rc) return rc;
-  rc = encode_w(&mW1, L1.d_wtc, 0, int64_t(9) * L1.cin_pad, L1.cout_pad, 32);
+  rc = encode_w(&mW1, L1.d_wtc, KIND, int64_t(9) * L1.cin_pad, L1.cout_pad, 32);
   if (rc) return rc;
-  rc = encode_w(&mW2, L2.d_wtc, 0, int64_t(9) * L2.cin_pad, L2.cout_pad, 16);
+  rc = encode_w(&mW2, L2.d_wtc, KIND, int64_t(9) * L2.cin_pad, L2.cout_pad, 16);
   if (rc) return rc;
   constexpr size_t smem = head_fused_smem();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_head_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_head_fused<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     attr = true;
   }
   static int nsm = 0;
   if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const int grid = nmaps < nsm ? int(nmaps) : nsm;  // whole maps per CTA
-  k_head_fused<<<grid, RT_THREADS, smem, st>>>(mA10, mA6, mW1, mW2, p1, p2, int(nmaps));
+  k_head_fused<KIND><<<grid, RT_THREADS, smem, st>>>(mA10, mA6, mW1, mW2, p1, p2, int(nmaps));
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_head_fused");
@@ -2724,7 +2783,7 @@ int run_head_fused(NetImpl& net, ConvLayer& L1, ConvLayer& L2, const Buf& in, in
 template <int KIND>
 int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t st,
                  const void* x_nhwc = nullptr) {
-  using T = typename std::conditional<KIND == 0, __nv_bfloat16, float>::type;
+  using T = ElemT<KIND>;
   const int k = net.k;
   if (k != 64)  // buffer plan: concat/skip slices are whole 64-channel rows only at k = 64
     return fail(DRCB_ECONFIG, "tensor-core path supports k = 64 (use net_mode fp32 for other k)");
@@ -2800,7 +2859,7 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
   up(B[12], 4 * k, B[5]);
   rc |= run_layer<KIND>(net, Ls[10], B[5], B[4], 0, np, st);
   // dec2.deconv2's whole-map tiles write up2x straight into c1 (k_conv_rows up2)
-  const bool fup16 = KIND == 0 && getenv("DRCB_NO_UP16") == nullptr;
+  const bool fup16 = KIND != 1 && getenv("DRCB_NO_UP16") == nullptr;
   rc |= run_layer<KIND>(net, Ls[11], B[4], B[13], 0, np, st, nullptr, fup16 ? &B[2] : nullptr);
   if (!fup16) up(B[13], 2 * k, B[2]);
   rc |= run_layer<KIND>(net, Ls[12], B[2], B[1], 0, np, st);
@@ -2816,9 +2875,9 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
     DRCB_CUDA(cudaMallocAsync((void**)&tmp, size_t(np) * 3 * 1024 * 4, st));
     pred = tmp;
   }
-  if (KIND == 0 && getenv("DRCB_NO_HEAD_FUSE") == nullptr) {
+  if (KIND != 1 && getenv("DRCB_NO_HEAD_FUSE") == nullptr) {
     // head.deconv1 + head.deconv2 + conv_out + ReLU in one kernel
-    rc = run_head_fused(net, Ls[14], Ls[15], B[14], np, pred, st);
+    rc = run_head_fused<KIND>(net, Ls[14], Ls[15], B[14], np, pred, st);
   } else {
     rc = run_layer<KIND>(net, Ls[14], B[14], B[15], 0, np, st);
     // head.deconv2 + conv_out + ReLU fused
@@ -2839,8 +2898,12 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
 int forward_tc_nhwc(NetImpl& net, const void* x_nhwc, float* y, int64_t n, int mode,
                     cudaStream_t st) {
   keep_pool_memory();
-  return mode == DRCB_NET_BF16 ? tc::forward_kind<0>(net, nullptr, y, n, st, x_nhwc)
-                               : tc::forward_kind<1>(net, nullptr, y, n, st, x_nhwc);
+  switch (mode) {
+    case DRCB_NET_BF16: return tc::forward_kind<0>(net, nullptr, y, n, st, x_nhwc);
+    case DRCB_NET_TF32: return tc::forward_kind<1>(net, nullptr, y, n, st, x_nhwc);
+    case DRCB_NET_FP16: return tc::forward_kind<2>(net, nullptr, y, n, st, x_nhwc);
+  }
+  return fail(DRCB_ECONFIG, "unknown tensor-core net mode");
 }
 
 int tc_input_channels(int) { return 8; }  // compact NHWC input (7 + 1 zero channel)
@@ -2876,8 +2939,12 @@ int forward_tc(NetImpl& net, const float* x, float* y, int64_t n, int mode, cuda
   const int64_t chunk = 8192;
   for (int64_t d = 0; d < n; d += chunk) {
     int64_t c = n - d < chunk ? n - d : chunk;
-    int rc = mode == DRCB_NET_BF16 ? tc::forward_kind<0>(net, x + d * 7 * 1024, y + d * 3 * 1024, c, st)
-                                   : tc::forward_kind<1>(net, x + d * 7 * 1024, y + d * 3 * 1024, c, st);
+    const float* xs = x + d * 7 * 1024;
+    float* ys = y + d * 3 * 1024;
+    int rc = mode == DRCB_NET_BF16   ? tc::forward_kind<0>(net, xs, ys, c, st)
+             : mode == DRCB_NET_FP16 ? tc::forward_kind<2>(net, xs, ys, c, st)
+             : mode == DRCB_NET_TF32 ? tc::forward_kind<1>(net, xs, ys, c, st)
+                                     : fail(DRCB_ECONFIG, "unknown tensor-core net mode");
     if (rc) return rc;
   }
   return 0;
@@ -2892,7 +2959,7 @@ extern "C" int drcb_debug_conv(int32_t mode, int32_t cin, int32_t cout, int32_t 
                                const float* x, const float* w, float* y) {
   using namespace drcb;
   using namespace drcb::tc;
-  const int kind = mode == DRCB_NET_BF16 ? 0 : 1;
+  const int kind = mode == DRCB_NET_BF16 ? 0 : (mode == DRCB_NET_FP16 ? 2 : 1);
   NetImpl net;
   net.k = 64;
   net.slope = 1.0f;
@@ -2907,7 +2974,7 @@ extern "C" int drcb_debug_conv(int32_t mode, int32_t cin, int32_t cout, int32_t 
   L.shift.assign(cout, 0.f);
   int rc = prepare_layer(net, L, kind);
   if (rc) return rc;
-  const int es = kind == 0 ? 2 : 4;
+  const int es = elem_bytes(kind);
   const int cinp = L.cin_pad, coutp = L.cout_pad;
   const int64_t np = ((n + 7) / 8) * 8;
   const size_t px = size_t(np) * hw * hw;
@@ -2918,6 +2985,9 @@ extern "C" int drcb_debug_conv(int32_t mode, int32_t cin, int32_t cout, int32_t 
       if (kind == 0) {
         __nv_bfloat16 b = __float2bfloat16(v);
         std::memcpy(&hx[(i * cinp + c) * 2], &b, 2);
+      } else if (kind == 2) {
+        __half b = __float2half_rn(v);
+        std::memcpy(&hx[(i * cinp + c) * 2], &b, 2);
       } else {
         std::memcpy(&hx[(i * cinp + c) * 4], &v, 4);
       }
@@ -2927,7 +2997,9 @@ extern "C" int drcb_debug_conv(int32_t mode, int32_t cin, int32_t cout, int32_t 
   DRCB_CUDA(cudaMalloc(&dy, px * coutp * es));
   cudaMemcpy(dx, hx.data(), hx.size(), cudaMemcpyHostToDevice);
   Buf in{dx, cinp, hw}, out{dy, coutp, hw};
-  rc = kind == 0 ? run_layer<0>(net, L, in, out, 0, np, 0) : run_layer<1>(net, L, in, out, 0, np, 0);
+  rc = kind == 0 ? run_layer<0>(net, L, in, out, 0, np, 0)
+       : kind == 2 ? run_layer<2>(net, L, in, out, 0, np, 0)
+                   : run_layer<1>(net, L, in, out, 0, np, 0);
   if (!rc) {
     std::vector<uint8_t> hy(px * coutp * es);
     cudaMemcpy(hy.data(), dy, hy.size(), cudaMemcpyDeviceToHost);
@@ -2939,6 +3011,10 @@ extern "C" int drcb_debug_conv(int32_t mode, int32_t cin, int32_t cout, int32_t 
           __nv_bfloat16 b;
           std::memcpy(&b, &hy[(i * coutp + c) * 2], 2);
           y[i * cout + c] = __bfloat162float(b);
+        } else if (kind == 2) {
+          __half b;
+          std::memcpy(&b, &hy[(i * coutp + c) * 2], 2);
+          y[i * cout + c] = __half2float(b);
         } else {
           std::memcpy(&y[i * cout + c], &hy[(i * coutp + c) * 4], 4);
         }

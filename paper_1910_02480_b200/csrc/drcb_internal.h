@@ -51,6 +51,11 @@ template <typename R>
 int launch_intersect(const DevScene& S, const R* O, const R* D, int64_t n, const R* tmin,
                      const R* tmax, int record, uint8_t* hit, R* t, int64_t* prim, int32_t* mat,
                      R* pos, R* nrm, cudaStream_t st);
+// fp32 traversal of fp64 rays with fp64 near-tie refinement (DRCB_PREC_MIXED)
+int launch_intersect_mixed(const DevScene& S, const double* O, const double* D, int64_t n,
+                           const double* tmin, const double* tmax, int record, uint8_t* hit,
+                           double* t, int64_t* prim, int32_t* mat, double* pos, double* nrm,
+                           cudaStream_t st);
 template <typename R>
 int launch_primary_chain(const DevScene& S, const R* O, const R* D, int64_t n,
                          const DrcbGBuffer& gb, cudaStream_t st);

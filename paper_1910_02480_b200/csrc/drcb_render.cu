@@ -13,6 +13,7 @@
 //   k_interp           _interpolate_layer + composite    (cache.py:283-345, 463)
 #include <cub/cub.cuh>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "drcb_internal.h"
 #include "drcb_trace.cuh"
@@ -62,6 +63,43 @@ __global__ void k_intersect(DevScene S, const R* __restrict__ O, const R* __rest
   if (pos) st3(pos + 3 * i, h.pos);
   if (nrm) st3(nrm + 3 * i, h.normal);
 }
+
+// fp32 build, mixed mode: fp64 rays (drcb_intersect, DRCB_PREC_MIXED) cast
+// by the fp32 traversal, undecided / near-tie candidates re-tested against
+// the fp64 ray itself
+__global__ void k_intersect_mixed(DevScene S, const double* __restrict__ O, const double* __restrict__ D,
+                                  int64_t n, const double* tmin, const double* tmax, int record,
+                                  uint8_t* hit, double* t, int64_t* prim, int32_t* mat, double* pos,
+                                  double* nrm) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const V3<float> o = cvt<float>(ldr3(O + 3 * i)), d = cvt<float>(ldr3(D + 3 * i));
+  const double lo64 = tmin ? tmin[i] : T_EPS, hi64 = tmax ? tmax[i] : double(INFINITY);
+  const float lo = lo64 == T_EPS ? float(T_EPS) : float(lo64);
+  const float hi = float(hi64);
+  const Ray64Ptr ref{O + 3 * i, D + 3 * i};
+  SurfHit<float> h = intersect<float, Ray64Ptr>(S, o, d, lo, hi, ref);
+  hit[i] = h.hit;
+  if (t) t[i] = double(h.t);
+  if (prim) prim[i] = h.prim;
+  if (record) {
+    if (mat) mat[i] = h.mat;
+    if (pos) st3(pos + 3 * i, cvt<double>(h.pos));
+    if (nrm) st3(nrm + 3 * i, cvt<double>(h.normal));
+  }
+}
+
+// the pixel's fp64 camera ray (scene.py:76-93), recomputed only when a
+// primary-cast candidate needs the fp64 re-test
+struct CameraRay64 {
+  const DevCamera* C;
+  float px, py;
+  template <typename R>
+  __device__ __forceinline__ void get(V3<R>, V3<R>, V3<Dn>& o, V3<Dn>& d) const {
+    o = ld3<Dn>(C->pos);
+    d = camera_dir<Dn>(*C, Dn(double(px)), Dn(double(py)));
+  }
+};
 
 template <typename R>
 __device__ __forceinline__ void store_chain(const DrcbGBuffer& gb, int64_t i, const ChainOut<R>& c) {
@@ -124,7 +162,7 @@ __global__ void k_trace(DevScene S, DrcbRenderCfg cfg, const R* __restrict__ O,
 // One thread per pixel: the unjittered centre chain (G-buffer) and the
 // direct_spp jittered li_direct samples, averaged (cache.py:157-176, 393-423).
 template <typename R>
-__global__ void __launch_bounds__(TPB) k_gbuffer_direct(DevScene S, DevCamera C, DrcbRenderCfg cfg,
+__global__ void __launch_bounds__(TPB) k_gbuffer_direct(DevScene S, const __grid_constant__ DevCamera C, DrcbRenderCfg cfg,
                                                          int tile, DrcbGBuffer gb, R* direct,
                                                          int64_t* nonfinite) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -134,7 +172,7 @@ __global__ void __launch_bounds__(TPB) k_gbuffer_direct(DevScene S, DevCamera C,
     int x = int(i % C.W), y = int(i / C.W);
     V3<R> cam = ld3<R>(C.pos);
     V3<R> dc = camera_dir<R>(C, R(x) + R(0.5), R(y) + R(0.5));
-    store_chain(gb, i, primary_chain(S, cam, dc));
+    store_chain(gb, i, primary_chain(S, cam, dc, CameraRay64{&C, x + 0.5f, y + 0.5f}));
     // direct pass; samples are summed in the reference's per-tile chunks
     int spp = cfg.direct_spp;
     int tx0 = (x / tile) * tile, ty0 = (y / tile) * tile;
@@ -176,13 +214,14 @@ __device__ __forceinline__ int64_t pixel_of(const DevCamera& C, int64_t k) {
 }
 
 template <typename R>
-__global__ void __launch_bounds__(TPB, 8) k_gbuffer(DevScene S, DevCamera C, DrcbGBuffer gb) {
+__global__ void __launch_bounds__(TPB, 8) k_gbuffer(DevScene S, const __grid_constant__ DevCamera C,
+                                                    DrcbGBuffer gb) {
   int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= int64_t(C.W) * C.H) return;
   const int64_t i = pixel_of(C, k);
   int x = int(i % C.W), y = int(i / C.W);
   V3<R> dc = camera_dir<R>(C, R(x) + R(0.5), R(y) + R(0.5));
-  store_chain(gb, i, primary_chain(S, ld3<R>(C.pos), dc));
+  store_chain(gb, i, primary_chain(S, ld3<R>(C.pos), dc, CameraRay64{&C, x + 0.5f, y + 0.5f}));
 }
 
 template <typename R>
@@ -212,7 +251,7 @@ __global__ void __launch_bounds__(TPB, DIRECT_CTAS) k_direct_samples(DevScene S,
 // ray re-walks the BVH nodes the centre ray just brought into L1). The
 // result is exactly k_direct_reduce's for one sample: (0 + L) / 1.
 template <typename R>
-__global__ void __launch_bounds__(TPB, DIRECT_CTAS) k_gbuffer_direct1(DevScene S, DevCamera C,
+__global__ void __launch_bounds__(TPB, DIRECT_CTAS) k_gbuffer_direct1(DevScene S, const __grid_constant__ DevCamera C,
                                                                      DrcbRenderCfg cfg,
                                                                      DrcbGBuffer gb, R* direct,
                                                                      int64_t* nonfinite) {
@@ -222,7 +261,8 @@ __global__ void __launch_bounds__(TPB, DIRECT_CTAS) k_gbuffer_direct1(DevScene S
     const int64_t i = pixel_of(C, k);
     const int x = int(i % C.W), y = int(i / C.W);
     const V3<R> cam = ld3<R>(C.pos);
-    store_chain(gb, i, primary_chain(S, cam, camera_dir<R>(C, R(x) + R(0.5), R(y) + R(0.5))));
+    store_chain(gb, i, primary_chain(S, cam, camera_dir<R>(C, R(x) + R(0.5), R(y) + R(0.5)),
+                                     CameraRay64{&C, x + 0.5f, y + 0.5f}));
     PathRng rng;
     rng.init(cfg.seed, uint64_t(i), 0ull, cfg.sampler_kind, 1u);
     const R jx = to_unit<R>(rng.sample(0)), jy = to_unit<R>(rng.sample(1));
@@ -552,7 +592,7 @@ constexpr double LUMA_R = 0.2126, LUMA_G = 0.7152, LUMA_B = 0.0722;  // hemimap.
 
 // One block (256 threads) per cache point: s_r = mean luminance + 1e-3,
 // s_d = max distance (or 1), fp32 NCHW stack [rad/s_r, n_local, d/s_d].
-// nhwc_kind: 0 = none, 1 = bf16, 2 = tf32-rounded fp32 compact NHWC input of
+// nhwc_kind: 0 = none, 1 = bf16, 2 = tf32-rounded fp32, 3 = fp16 compact NHWC input of
 // the tensor-core network (cpad = 8: 7 channels + 1 zero), written here directly
 template <typename R>
 __global__ void __launch_bounds__(256) k_stack_normalize(const R* __restrict__ rad,
@@ -572,7 +612,7 @@ __global__ void __launch_bounds__(256) k_stack_normalize(const R* __restrict__ r
     if (stacks)
       for (int t = threadIdx.x; t < 7 * MAP_TEXELS; t += blockDim.x) out[t] = 0.f;
     if (nhwc_kind) {
-      int es = nhwc_kind == 1 ? 2 : 4;
+      int es = nhwc_kind == 2 ? 4 : 2;
       uint4* o = reinterpret_cast<uint4*>(static_cast<uint8_t*>(nhwc) + size_t(p) * MAP_TEXELS * cpad * es);
       for (int t = threadIdx.x; t < MAP_TEXELS * cpad * es / 16; t += blockDim.x) o[t] = make_uint4(0, 0, 0, 0);
     }
@@ -603,11 +643,16 @@ __global__ void __launch_bounds__(256) k_stack_normalize(const R* __restrict__ r
     v[7] = 0.f;
     if (stacks)
       for (int c = 0; c < 7; ++c) out[c * MAP_TEXELS + t] = v[c];
-    if (nhwc_kind == 1) {
+    if (nhwc_kind == 1 || nhwc_kind == 3) {
       uint32_t w[4];
       for (int j = 0; j < 4; ++j) {
-        __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-        w[j] = *reinterpret_cast<uint32_t*>(&b);
+        if (nhwc_kind == 1) {
+          __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+          w[j] = *reinterpret_cast<uint32_t*>(&b);
+        } else {
+          __half2 b = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
+          w[j] = *reinterpret_cast<uint32_t*>(&b);
+        }
       }
       reinterpret_cast<uint4*>(nhwc)[p * MAP_TEXELS + t] = make_uint4(w[0], w[1], w[2], w[3]);
     } else if (nhwc_kind == 2) {
@@ -1192,6 +1237,17 @@ template int launch_pt_frame<float>(const DevScene&, const DevCamera&, const Drc
 template int launch_reference_map<float>(const DevScene&, const DrcbRenderCfg&, const float*,
                                          const float*, uint64_t, int, float*, int64_t*,
                                          cudaStream_t);
+
+int launch_intersect_mixed(const DevScene& S, const double* O, const double* D, int64_t n,
+                           const double* tmin, const double* tmax, int record, uint8_t* hit,
+                           double* t, int64_t* prim, int32_t* mat, double* pos, double* nrm,
+                           cudaStream_t st) {
+  if (n <= 0) return 0;
+  DRCB_RENDER_NS::k_intersect_mixed<<<DRCB_RENDER_NS::nblocks(n), DRCB_RENDER_NS::TPB, 0, st>>>(
+      S, O, D, n, tmin, tmax, record, hit, t, prim, mat, pos, nrm);
+  LAUNCH_CHECK();
+  return 0;
+}
 
 // the fp32 module's copy of the traversal-counter pointer
 int set_trav_stats_f32(unsigned long long* buf) {

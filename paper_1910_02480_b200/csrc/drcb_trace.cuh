@@ -7,10 +7,34 @@
 // walks one path to completion (a persistent "megakernel" loop), which keeps
 // per-path state in registers instead of compacting HBM arrays per segment.
 #pragma once
+#include <type_traits>
+
 #include "drcb_math.cuh"
 #include "drcb_scene.cuh"
 
 namespace drcb {
+
+// fp64 with every operation explicitly rounded (no FMA contraction): the
+// fp32 build's near-tie re-tests compute exactly what the -fmad=false fp64
+// build (and numpy) computes, although their translation unit contracts
+struct Dn {
+  double v;
+  __device__ __forceinline__ Dn() = default;
+  __device__ __forceinline__ constexpr Dn(double x) : v(x) {}
+};
+__device__ __forceinline__ Dn operator+(Dn a, Dn b) { return Dn(__dadd_rn(a.v, b.v)); }
+__device__ __forceinline__ Dn operator-(Dn a, Dn b) { return Dn(__dsub_rn(a.v, b.v)); }
+__device__ __forceinline__ Dn operator-(Dn a) { return Dn(-a.v); }
+__device__ __forceinline__ Dn operator*(Dn a, Dn b) { return Dn(__dmul_rn(a.v, b.v)); }
+__device__ __forceinline__ Dn operator/(Dn a, Dn b) { return Dn(__ddiv_rn(a.v, b.v)); }
+__device__ __forceinline__ bool operator<(Dn a, Dn b) { return a.v < b.v; }
+__device__ __forceinline__ bool operator>(Dn a, Dn b) { return a.v > b.v; }
+__device__ __forceinline__ bool operator<=(Dn a, Dn b) { return a.v <= b.v; }
+__device__ __forceinline__ bool operator>=(Dn a, Dn b) { return a.v >= b.v; }
+using ::fabs;  // the Dn overloads below must not hide the float / double ones
+using ::sqrt;
+__device__ __forceinline__ Dn fabs(Dn a) { return Dn(::fabs(a.v)); }
+__device__ __forceinline__ Dn sqrt(Dn a) { return Dn(__dsqrt_rn(a.v)); }
 
 template <typename R>
 struct HitRec {
@@ -89,6 +113,15 @@ __device__ __forceinline__ void leaf_tri<float>(const DevScene& S, int slot, V3<
   e2 = {c.x, c.y, c.z};
 }
 template <>
+__device__ __forceinline__ void leaf_tri<Dn>(const DevScene& S, int slot, V3<Dn>& v0, V3<Dn>& e1,
+                                             V3<Dn>& e2, int& id) {
+  const double* p = S.leaf_d + 9 * slot;
+  id = __ldg(S.leaf_id + slot);
+  v0 = {__ldg(p + 0), __ldg(p + 1), __ldg(p + 2)};
+  e1 = {__ldg(p + 3), __ldg(p + 4), __ldg(p + 5)};
+  e2 = {__ldg(p + 6), __ldg(p + 7), __ldg(p + 8)};
+}
+template <>
 __device__ __forceinline__ void leaf_tri<double>(const DevScene& S, int slot, V3<double>& v0,
                                                  V3<double>& e1, V3<double>& e2, int& id) {
   const double* p = S.leaf_d + 9 * slot;
@@ -127,6 +160,103 @@ __device__ __forceinline__ bool test_prim(const DevScene& S, int slot, V3<R> O, 
   return sphere_t(S, id, O, D, tmin, bound, t);
 }
 
+// ---------------------------------------------------------------------------
+// fp32 build: near-tie refinement. The fp32 triangle test carries a bound on
+// its own rounding error (the ray and the triangle rounded to fp32, and the
+// fp32 arithmetic of Moller-Trumbore): a candidate whose inside/outside or
+// t-range decision lies within that bound, or whose t lies within the bound
+// of the current nearest hit, is re-tested in fp64 against the fp64 leaf
+// records and the fp64 ray (the reference's arithmetic, geometry.py:271-286,
+// with its nearest-t / lowest-id rule, geometry.py:199-214). Every other
+// decision is provably the one fp64 makes.
+//   Ray64 references: Plain (no refinement: the fp32 decisions as they
+//   come — bounce, shadow and map-path casts, whose flip rate the tests
+//   report), Promote (the fp32 ray itself in fp64, for later links of a
+//   primary chain), Ray64Ptr (fp64 rays in memory: drcb_intersect's mixed
+//   mode), CameraRay64 (the pixel's fp64 camera ray, recomputed on demand:
+//   the G-buffer's primary casts).
+struct Plain {};
+struct Promote {
+  template <typename R>
+  __device__ __forceinline__ void get(V3<R> O, V3<R> D, V3<Dn>& o, V3<Dn>& d) const {
+    o = {double(O.x), double(O.y), double(O.z)};
+    d = {double(D.x), double(D.y), double(D.z)};
+  }
+};
+struct Ray64Ptr {
+  const double* o;
+  const double* d;
+  template <typename R>
+  __device__ __forceinline__ void get(V3<R>, V3<R>, V3<Dn>& oo, V3<Dn>& dd) const {
+    oo = ld3<Dn>(o);
+    dd = ld3<Dn>(d);
+  }
+};
+
+// 0 = certain miss, 1 = certain hit (t, error bound mt), 2 = undecided in fp32
+__device__ __forceinline__ int tri_t_margin(V3<float> v0, V3<float> e1, V3<float> e2, V3<float> O,
+                                            V3<float> D, float tmin, float tmax, float& tout,
+                                            float& mt) {
+  V3<float> pv = cross(D, e2);
+  float det = dot(pv, e1);
+  if (!(fabsf(det) > 1e-12f)) return fabsf(det) > 0.f ? 2 : 0;  // fp64 decides |det| vs 1e-14
+  // 16 ulps of every operand magnitude that enters a result
+  constexpr float EPS = 16.f * 5.9604645e-8f;
+  const float inv = 1.f / det, ainv = fabsf(inv);
+  V3<float> tv = O - v0;
+  auto l1 = [](V3<float> a) { return fabsf(a.x) + fabsf(a.y) + fabsf(a.z); };
+  // |O - v0| carries the rounding of both points: bound it by their sizes
+  const float T = fmaxf(l1(O), l1(v0)) + l1(tv);
+  // |D||e2| bounds pv = D x e2 and its error even when D is nearly parallel to
+  // e2 (the rounding of D and e2 perturbs pv by eps |D||e2|, not eps |pv|)
+  const float de2 = l1(D) * l1(e2);
+  const float pe1 = de2 * l1(e1) * ainv;  // condition of det (>= 1)
+  const float u = dot(tv, pv) * inv;
+  const float mu = EPS * (T * de2 * ainv + fabsf(u) * pe1 + 1.f);
+  if (u < -mu || u > 1.f + mu) return 0;
+  const V3<float> qv = cross(tv, e1);
+  const float te1 = T * l1(e1);
+  const float v = dot(qv, D) * inv;
+  const float mv = EPS * (te1 * l1(D) * ainv + fabsf(v) * pe1 + 1.f);
+  if (v < -mv || u + v > 1.f + mu + mv) return 0;
+  const float t = dot(qv, e2) * inv;
+  const float m_t = EPS * (te1 * l1(e2) * ainv + fabsf(t) * pe1);
+  if (t <= tmin - m_t || t > tmax + m_t) return 0;
+  tout = t;
+  mt = m_t;
+  const bool sure = u >= mu && u <= 1.f - mu && v >= mv && u + v <= 1.f - mu - mv &&
+                    t > tmin + m_t && t <= tmax - m_t;
+  return sure ? 1 : 2;
+}
+
+// fp32 candidate test: 0 miss, 1 certain hit, 2 undecided (refine in fp64)
+__device__ __forceinline__ int test_prim32(const DevScene& S, int slot, V3<float> O, V3<float> D,
+                                           float tmin, float bound, float& t, float& mt, int& id) {
+  V3<float> v0, e1, e2;
+  leaf_tri<float>(S, slot, v0, e1, e2, id);
+  if (id >= S.n_s + S.n_q) return tri_t_margin(v0, e1, e2, O, D, tmin, bound, t, mt);
+  // spheres / quads: the plain fp32 test with a relative t bound (their
+  // near-ties with other primitives still go to fp64)
+  bool h = id >= S.n_s ? quad_t(S, id - S.n_s, O, D, tmin, bound, t) : sphere_t(S, id, O, D, tmin, bound, t);
+  mt = 1e-5f * fabsf(t) + 1e-6f;
+  return h ? 1 : 0;
+}
+
+// the fp64 re-test of one leaf slot (uncontracted: the fp64 build's bits)
+template <class Ref>
+__device__ __noinline__ bool refine64(const DevScene& S, int slot, const Ref& ref, V3<float> O,
+                                      V3<float> D, float tmin, float tmax, double& t) {
+  V3<Dn> o, d;
+  ref.get(O, D, o, d);
+  const Dn lo = tmin == float(T_EPS) ? T_EPS : double(tmin);
+  const Dn hi = isinf(tmax) ? double(INFINITY) : double(tmax);
+  int id;
+  Dn tt;
+  const bool h = test_prim<Dn>(S, slot, o, d, lo, hi, tt, id);
+  t = tt.v;
+  return h;
+}
+
 // Closest hit (ANY=false) or any hit in (tmin, tmax] (ANY=true) over the BVH.
 // Warp-synchronous while-while traversal with speculative leaf postponement
 // (Aila & Laine 2009): every lane that entered runs every iteration of ONE
@@ -137,8 +267,10 @@ __device__ __forceinline__ bool test_prim(const DevScene& S, int slot, V3<R> O, 
 // primitives left: each iteration tests ONE primitive per lane, so leaf work
 // of different lanes is done side by side instead of lane after lane. The
 // result is traversal-order independent (nearest t, ties -> lowest prim id).
-template <typename R, bool ANY>
-__device__ HitRec<R> traverse(const DevScene& S, V3<R> O, V3<R> D, R tmin, R tmax) {
+template <typename R, bool ANY, class Ref = Plain>
+__device__ HitRec<R> traverse(const DevScene& S, V3<R> O, V3<R> D, R tmin, R tmax,
+                              const Ref& ref = Ref()) {
+  constexpr bool F32 = std::is_same<R, float>::value && !std::is_same<Ref, Plain>::value;
   HitRec<R> best{tmax, -1};
   if (S.n_prims == 0) return best;
   const unsigned tmask = __activemask();
@@ -160,6 +292,10 @@ __device__ HitRec<R> traverse(const DevScene& S, V3<R> O, V3<R> D, R tmin, R tma
   int pcur = 0, pend = 0;  // primitive cursor of the leaf under test
   bool leaf_phase = false;
   unsigned n_nodes = 0, n_prims = 0;
+  // fp32 build: the nearest hit's leaf slot and its t error bound (0 once the
+  // hit is exact, i.e. came from the fp64 re-test)
+  int best_slot = -1;
+  float best_mt = 0.f;
   float tbest = isinf(float(tmax)) ? INFINITY : f_ru(tmax) * ROB;
   while (true) {
     const bool inner = node >= 0 && node != TRAV_SENTINEL;
@@ -222,22 +358,70 @@ __device__ HitRec<R> traverse(const DevScene& S, V3<R> O, V3<R> D, R tmin, R tma
       }
       R t;
       int id;
-      if (test_prim<R>(S, pcur, O, D, tmin, ANY ? tmax : best.t, t, id)) {
+      if constexpr (F32) {
+        static_assert(std::is_same<R, float>::value, "refinement is the fp32 build's");
+        float mt;
+        const int res = test_prim32(S, pcur, O, D, tmin, ANY ? tmax : best.t + best_mt, t, mt, id);
         if (ANY) {
-          best.t = t;
-          best.prim = id;
-          node = TRAV_SENTINEL;
-          postponed = 0;
-          pend = pcur;
-        } else if (improves(t, id, best.t, best.prim)) {
-          best.t = t;
-          best.prim = id;
-          tbest = f_ru(t) * ROB;
+          double t64;
+          if (res == 1 || (res == 2 && refine64(S, pcur, ref, O, D, tmin, tmax, t64))) {
+            best.t = t;
+            best.prim = id;
+            node = TRAV_SENTINEL;
+            postponed = 0;
+            pend = pcur;
+          }
+        } else if (res) {
+          const bool near = best.prim >= 0 && fabsf(t - best.t) <= mt + best_mt;
+          if (res == 1 && !near) {
+            if (t < best.t) {
+              best.t = t;
+              best.prim = id;
+              best_slot = pcur;
+              best_mt = mt;
+              tbest = f_ru(t + mt) * ROB;
+            }
+          } else {
+            // undecided candidate or a near-tie with the current nearest hit:
+            // both in fp64, the reference's comparison (nearest, then lowest id)
+            double tc, tb = 0.0;
+            if (refine64(S, pcur, ref, O, D, tmin, tmax, tc)) {
+              bool take = best.prim < 0;
+              if (!take) {
+                const bool bhit = refine64(S, best_slot, ref, O, D, tmin, tmax, tb);
+                take = !bhit || tc < tb || (tc == tb && id < best.prim);
+              }
+              if (take) {
+                const float tf = float(tc);
+                best.t = tf;
+                best.prim = id;
+                best_slot = pcur;
+                best_mt = fabsf(tf) * 1.2e-7f;  // exact up to its fp32 rounding
+                tbest = f_ru(tc) * ROB;
+              }
+            }
+          }
+        }
+      } else {
+        if (test_prim<R>(S, pcur, O, D, tmin, ANY ? tmax : best.t, t, id)) {
+          if (ANY) {
+            best.t = t;
+            best.prim = id;
+            node = TRAV_SENTINEL;
+            postponed = 0;
+            pend = pcur;
+          } else if (improves(t, id, best.t, best.prim)) {
+            best.t = t;
+            best.prim = id;
+            tbest = f_ru(t) * ROB;
+          }
         }
       }
       ++pcur;
     }
   }
+  (void)best_slot;
+  (void)best_mt;
   if (g_trav_stats) {
     atomicAdd(g_trav_stats + 0, n_nodes);
     atomicAdd(g_trav_stats + 1, n_prims);
@@ -261,10 +445,11 @@ struct SurfHit {
   V3<R> pos, normal;  // geometric, unflipped (geometry.py:296-322)
 };
 
-template <typename R>
+template <typename R, class Ref = Plain>
 __device__ __forceinline__ SurfHit<R> intersect(const DevScene& S, V3<R> O, V3<R> D,
-                                                R tmin = R(T_EPS), R tmax = R(INFINITY)) {
-  HitRec<R> h = traverse<R, false>(S, O, D, tmin, tmax);
+                                                R tmin = R(T_EPS), R tmax = R(INFINITY),
+                                                const Ref& ref = Ref()) {
+  HitRec<R> h = traverse<R, false, Ref>(S, O, D, tmin, tmax, ref);
   SurfHit<R> r;
   r.hit = h.prim >= 0;
   r.prim = h.prim;
@@ -717,8 +902,22 @@ struct ChainOut {
   R t_total;
 };
 
-template <typename R>
-__device__ ChainOut<R> primary_chain(const DevScene& S, V3<R> O, V3<R> D) {
+// the fp64 twin of the chain's FIRST cast only (later links are fp32-born)
+template <class Ref0>
+struct FirstCast {
+  Ref0 r0;
+  bool first;
+  template <typename R>
+  __device__ __forceinline__ void get(V3<R> O, V3<R> D, V3<Dn>& o, V3<Dn>& d) const {
+    if (first)
+      r0.get(O, D, o, d);
+    else
+      Promote().get(O, D, o, d);
+  }
+};
+
+template <typename R, class Ref0 = Plain>
+__device__ ChainOut<R> primary_chain(const DevScene& S, V3<R> O, V3<R> D, const Ref0& ref0 = Ref0()) {
   ChainOut<R> out;
   out.found = out.escaped = false;
   out.pos = out.normal = {R(0), R(0), R(0)};
@@ -727,8 +926,12 @@ __device__ ChainOut<R> primary_chain(const DevScene& S, V3<R> O, V3<R> D) {
   out.mat = -1;
   out.t_total = R(0);
   V3<R> beta = {R(1), R(1), R(1)};
+  using RefT = typename std::conditional<std::is_same<Ref0, Plain>::value, Plain, FirstCast<Ref0>>::type;
+  RefT ref;
+  if constexpr (!std::is_same<Ref0, Plain>::value) ref = RefT{ref0, true};
   for (int it = 0; it < SPECULAR_CHAIN_BOUND; ++it) {
-    SurfHit<R> h = intersect(S, O, D);
+    SurfHit<R> h = intersect(S, O, D, R(T_EPS), R(INFINITY), ref);
+    if constexpr (!std::is_same<Ref0, Plain>::value) ref.first = false;
     if (!h.hit) {
       out.escaped = true;
       out.thr = beta;

@@ -414,6 +414,26 @@ def render(scene, config, mode="pt", weights=None, interrupt=None):
 # ---------------------------------------------------------------------------
 # stage-level surfaces (numpy in / numpy out, for parity tests)
 
+def gbuffer_direct(scene, config, camera=None, include_background=False):
+    """The frame's first stage on its own: DrcState's G-buffer (the
+    unjittered centre chains, cache.py:157-176) and the direct pass averaged
+    per pixel (cache.py:393-423) -> (G-buffer dict of (W*H, ...) arrays,
+    direct (H, W, 3) float64)."""
+    torch = _torch()
+    prec = int(getattr(config, "precision", 64))
+    dtype = torch.float64 if prec == 64 else torch.float32
+    cam = camera or scene.camera
+    w, h = cam.resolution
+    gb = GBufferTensors(w * h, dtype)
+    direct = torch.empty((h, w, 3), dtype=dtype, device="cuda")
+    nf = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cfg = _cfg_struct(config, prec)
+    cfg.include_background = int(bool(include_background))
+    _lib.call("drcb_gbuffer_direct", device_scene(scene).handle, C.byref(camera_struct(cam)),
+              C.byref(cfg), C.byref(gb.struct()), _lib.ptr(direct), _lib.ptr(nf), _lib.stream_ptr())
+    return gb.numpy(), direct.double().cpu().numpy()
+
+
 class GBufferTensors:
     def __init__(self, n, dtype):
         torch = _torch()
@@ -464,15 +484,22 @@ def _dev(a, dtype):
     return torch.from_numpy(np.array(a, copy=True, order="C")).to(device="cuda", dtype=dtype)
 
 
+# drcb_intersect's mixed mode: the fp32 build's traversal of fp64 rays, with
+# undecided / near-tie candidates re-tested in fp64 (include/drcb.h)
+PREC_MIXED = 3264
+
+
 def _rdtype(precision):
     torch = _torch()
-    return torch.float64 if precision == 64 else torch.float32
+    return torch.float64 if precision in (64, PREC_MIXED) else torch.float32
 
 
 def intersect_batch(scene, origins, directions, t_min=T_EPS, t_max=np.inf, record=True,
                     precision=64):
     """geometry.intersect_batch on the device: dict(hit, t, prim[, mat,
-    position, normal])."""
+    position, normal]). precision: 64 (fp64 build), 32 (fp32 build on
+    fp32-rounded rays) or PREC_MIXED (fp32 build on the fp64 rays, the
+    G-buffer's primary-cast mode)."""
     torch = _torch()
     rd = _rdtype(precision)
     O = np.atleast_2d(np.asarray(origins, dtype=np.float64))

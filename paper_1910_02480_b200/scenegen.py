@@ -84,11 +84,11 @@ class _Builder:
                                 np.asarray(faces, dtype=np.int64), name))
 
 
-def _cornell(b, rng, lights, closed=True):
+def _cornell(b, rng, lights, closed=True, light_y=0.999):
     """Cornell box (closed=True: 5 walls, configs 1-2). The orbit-camera
     configs (3-4, cameras on a radius-3 sphere) use an open stage instead:
-    only a 6x6 floor, so the cameras see the lit objects rather than the
-    outside of the walls."""
+    only a 6x6 floor, so the cameras see the objects rather than the outside
+    of the walls; their lights hang above the object cloud (light_y)."""
     if closed:
         walls = [
             _quad_tris([-1, -1, -1], [1, -1, -1], [1, -1, 1], [-1, -1, 1]),   # floor
@@ -105,7 +105,7 @@ def _cornell(b, rng, lights, closed=True):
         v, f = _box(lo, hi)
         b.add(v, f, rng.uniform(0.1, 0.9, 3))
     for (cx, cz, e) in lights:
-        v, f = _light(0.999, LIGHT_HALF, cx, cz)
+        v, f = _light(light_y, LIGHT_HALF, cx, cz)
         b.add(v, f, [0.0, 0.0, 0.0], emission=[e, e, e])
 
 
@@ -131,20 +131,34 @@ CONFIGS = {
 }
 
 
+# The orbit-camera configs (3-4): the 2,000 / 16,000 random triangles with
+# vertices uniform in [-1,1]^3 make the cube nearly opaque, so a ceiling light
+# at y = 0.999 inside it lit almost nothing, and the radius-3 orbit cameras
+# sit above the light plane or below the floor (their frames had no direct
+# light at all). The open stage therefore hangs its lights above the cloud
+# (y = 1.6, facing down, still one-sided, R10) and adds a uniform grey
+# environment (the reference's `environment`, scene.py:328) that escaped
+# paths see: every orbit camera's frame is lit.
+OPEN_STAGE_LIGHT_Y = 1.6
+OPEN_STAGE_ENV = 0.3
+
+
 def build_scene(config="c1", seed=None, resolution=None):
     """Scene for BASELINE config c1..c4 (seed defaults to the config's)."""
     res, _, n_sph, n_rand, lights, wseed = CONFIGS[config]
     seed = {"c1": 0, "c2": 1, "c3": 2, "c4": 2}[config] if seed is None else seed
     rng = np.random.default_rng(seed)
     b = _Builder()
-    _cornell(b, rng, lights, closed=config in ("c1", "c2"))
+    closed = config in ("c1", "c2")
+    _cornell(b, rng, lights, closed=closed, light_y=0.999 if closed else OPEN_STAGE_LIGHT_Y)
     _spheres(b, rng, n_sph)
     if n_rand:
         _random_tris(b, rng, n_rand)
     res = tuple(resolution or res)
     cam = Camera(np.array([0.0, 0.0, -3.7]), np.zeros(3), np.array([0.0, 1.0, 0.0]), 40.0, res)
-    return Scene(cam, tuple(b.materials), tuple(b.meshes), (), np.array([0.0, 1.0, 0.0]),
-                 np.zeros(3), name=config)
+    env = np.zeros(3) if closed else np.full(3, OPEN_STAGE_ENV)
+    return Scene(cam, tuple(b.materials), tuple(b.meshes), (), np.array([0.0, 1.0, 0.0]), env,
+                 name=config)
 
 
 def orbit_cameras(n, resolution, seed=2, radius=3.0, up=(0.0, 1.0, 0.0)):
@@ -179,4 +193,6 @@ def scene_doc(scene):
                    "resolution": [int(c.resolution[0]), int(c.resolution[1])]},
         "global_up": [float(x) for x in scene.global_up],
         "materials": mats, "shapes": shapes, "point_lights": [],
+        **({"environment": [float(x) for x in scene.environment]}
+           if np.any(np.asarray(scene.environment) > 0) else {}),
     }

@@ -110,3 +110,71 @@ def test_row_tile_kernels_agree_with_per_tap_kernel(mode, bar, monkeypatch):
     monkeypatch.setenv("DRCB_NO_ROWS", "1")
     tap = cnn.forward_batch(net, x, mode=mode)
     assert _rel(rows, tap) <= bar
+
+
+def _per_map_rel(y, ref):
+    num = np.linalg.norm((y - ref).reshape(len(y), -1), axis=1)
+    den = np.linalg.norm(ref.reshape(len(ref), -1), axis=1)
+    keep = den > 1e-6 * den.max()
+    return num[keep] / den[keep]
+
+
+@pytest.mark.parametrize("mode", [2, 3])
+@pytest.mark.parametrize("shape", [(64, 64, 32, 8), (7, 64, 32, 8), (128, 256, 8, 16),
+                                   (256, 512, 4, 16), (192, 64, 32, 8), (32, 16, 32, 8)])
+def test_fp16_single_layer_implicit_gemm(mode, shape):
+    # fp16 operands (kind::f16, F16 format): exact to operand rounding at every
+    # output position, like the bf16 / tf32 kinds above
+    if mode == 2:
+        pytest.skip("bf16 covered by test_single_layer_implicit_gemm")
+    cin, cout, hw, n = shape
+    rng = np.random.default_rng(hash(shape) % 1000 + 7)
+    x = rng.normal(size=(n, hw, hw, cin)).astype(np.float32)
+    w = rng.normal(size=(cout, cin, 3, 3)).astype(np.float32)
+    y = np.zeros((n, hw, hw, cout), np.float32)
+    _lib.call("drcb_debug_conv", mode, cin, cout, hw, n, x.ctypes.data_as(C.c_void_p),
+              w.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p))
+    ref = _conv_ref(x.astype(np.float16).astype(np.float64), w.astype(np.float16).astype(np.float64))
+    assert np.abs(y - ref).max() <= 2e-3 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("config,wseed", [("c2", 1), ("c3", 2), ("c1", 0)])
+def test_16bit_network_on_rendered_stacks(config, wseed):
+    """BASELINE bar for the 16-bit U-Net: relative L2 <= 1e-2 against the
+    fp32 engine, here per map (the MAX over maps) on stacks rendered by the
+    map path tracer at the config's own scene, with the config's weights
+    (C1 seed 0, C2 seed 1, C3 seed 2). fp16 operands must pass on every
+    weight set; bf16 operands (8-bit mantissa) pass on C3's weights only —
+    on C1/C2's the rounding of 17 chained layers leaves ~1.2-1.5e-2 (measured
+    here and by the CPU emulation), which the test records."""
+    from stacks_util import rendered_stacks
+
+    x, _ = rendered_stacks(config, 256)
+    assert len(x) >= 64 and float(x[:, :3].max()) > 5.0  # real radiance range (C1: 64 points)
+    net = cnn.random_network(64, wseed)
+    ref = cnn.forward_batch(net, x, mode="fp32")
+    e16 = _per_map_rel(cnn.forward_batch(net, x, mode="fp16"), ref)
+    ebf = _per_map_rel(cnn.forward_batch(net, x, mode="bf16"), ref)
+    print(f"{config}: fp16 median {np.median(e16):.2e} max {e16.max():.2e}; "
+          f"bf16 median {np.median(ebf):.2e} max {ebf.max():.2e}")
+    assert e16.max() <= 1e-2 / 2, e16.max()  # measured 2.5e-3 (C2) by emulation
+    if wseed == 2:
+        assert ebf.max() <= 1e-2, ebf.max()
+    # the tf32 kind for reference (10-bit mantissa like fp16)
+    etf = _per_map_rel(cnn.forward_batch(net, x, mode="tf32"), ref)
+    assert etf.max() <= 1e-2 / 2, etf.max()
+
+
+def test_fp16_batching_and_fusions_bit_identical(monkeypatch):
+    # batching invariance and the fused pool / upsample / head variants in fp16
+    rng = np.random.default_rng(11)
+    x = rng.uniform(0, 1, (13, 7, 32, 32)).astype(np.float32)
+    x[:, :3] *= 20
+    net = cnn.random_network(64, 1)
+    y13 = cnn.forward_batch(net, x, mode="fp16")
+    y1 = np.concatenate([cnn.forward_batch(net, x[i:i + 1], mode="fp16") for i in range(13)])
+    assert np.array_equal(y13, y1)
+    for env in ("DRCB_NO_FUSED_POOL", "DRCB_NO_UP16", "DRCB_NO_HEAD_FUSE"):
+        monkeypatch.setenv(env, "1")
+        assert np.array_equal(cnn.forward_batch(net, x, mode="fp16"), y13), env
+        monkeypatch.delenv(env)
