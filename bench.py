@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--tasks", type=int, default=1)
     ap.add_argument("--precision", type=int, default=32)
-    ap.add_argument("--net", default=os.environ.get("DRCB_BENCH_NET", "bf16"))
+    ap.add_argument("--net", default=os.environ.get("DRCB_BENCH_NET", "fp16"))
     ap.add_argument("--frames", type=int, default=FRAMES_PER_RANK)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-points", type=int, default=16)

@@ -36,16 +36,15 @@ namespace drcb {
 // synchronisation (release threshold 0), turning each frame's multi-GB
 // activation workspace into a fresh cudaMalloc; keep them cached.
 void keep_pool_memory() {
-  static int done_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (done_dev == dev) return;
+  static DeviceFlags done;
+  const int dev = current_device();
+  if (done.test(dev)) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  done_dev = dev;
+  done.set(dev);
 }
 
 namespace tc {
@@ -2334,13 +2333,9 @@ template <int KIND, int BN, int STAGES>
 int launch_bn(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, cudaStream_t st) {
   using SM = Smem<KIND, BN, STAGES>;
   auto kern = k_conv_tc<KIND, BN, STAGES>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
-    attr = true;
-  }
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  static DeviceFlags attr;
+  smem_attr_once(attr, kern, SM::TOTAL);
+  const int nsm = sm_count();
   int tiles = a.num_m_tiles * a.num_n_tiles;
   int grid = tiles < nsm ? tiles : nsm;
   kern<<<grid, NUM_THREADS, SM::TOTAL, st>>>(mA, mB, a);
@@ -2354,13 +2349,9 @@ int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorM
                    const CUtensorMap& mP, const ConvArgs& a, const RowArgs& h, size_t smem,
                    cudaStream_t st) {
   auto kern = k_conv_rows<KIND, BN, RES, DX, MH, PW>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  static DeviceFlags attr;
+  smem_attr_once(attr, kern, 227 * 1024);
+  const int nsm = sm_count();
   int tiles = a.num_m_tiles * a.num_n_tiles;
   int grid = tiles < nsm ? tiles : nsm;
   kern<<<grid, PW ? ROWS_THREADS : RT_THREADS, smem, st>>>(mA, mB, mO, mP, a, h);
@@ -2373,13 +2364,9 @@ template <int KIND, bool RES>
 int launch_pair64(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO,
                   const ConvArgs& a, const RowArgs& h, size_t smem, cudaStream_t st) {
   auto kern = k_conv_pair<KIND, 64, RES>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  static DeviceFlags attr;
+  smem_attr_once(attr, kern, 227 * 1024);
+  const int nsm = sm_count();
   const int pairs = std::min(a.num_m_tiles, nsm / 2);
   kern<<<2 * pairs, RT_THREADS, smem, st>>>(mA, mB, mO, a, h);
   count_launch();
@@ -2491,13 +2478,9 @@ int run_in8(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cout_
   if (rc) return rc;
   auto kern = k_conv_in8<KIND>;
   constexpr size_t smem = in8_smem<KIND>();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
-  }
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  static DeviceFlags attr;
+  smem_attr_once(attr, kern, int(smem));
+  const int nsm = sm_count();
   int grid = a.num_m_tiles < nsm ? a.num_m_tiles : nsm;
   kern<<<grid, IN8_THREADS, smem, st>>>(mX, mB, mO, a);
   count_launch();
@@ -2766,13 +2749,9 @@ int run_head_fused(NetImpl& net, ConvLayer& L1, ConvLayer& L2, const Buf& in, in
   rc = encode_w(&mW2, L2.d_wtc, KIND, int64_t(9) * L2.cin_pad, L2.cout_pad, 16);
   if (rc) return rc;
   constexpr size_t smem = head_fused_smem();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_head_fused<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
-  }
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  static DeviceFlags attr;
+  smem_attr_once(attr, k_head_fused<KIND>, int(smem));
+  const int nsm = sm_count();
   const int grid = nmaps < nsm ? int(nmaps) : nsm;  // whole maps per CTA
   k_head_fused<KIND><<<grid, RT_THREADS, smem, st>>>(mA10, mA6, mW1, mW2, p1, p2, int(nmaps));
   count_launch();

@@ -3,6 +3,7 @@
 // no link-time NCCL dependency and shares the process's NCCL instance with
 // torch when torch already loaded it.
 #include <dlfcn.h>
+#include <mutex>
 #include <nccl.h>
 
 #include <cstring>
@@ -25,9 +26,8 @@ struct Nccl {
 
 Nccl* nccl() {
   static Nccl n;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static std::once_flag once;  // several host threads may build communicators
+  std::call_once(once, [] {
     n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (n.h) {
       n.get_unique_id = reinterpret_cast<decltype(n.get_unique_id)>(dlsym(n.h, "ncclGetUniqueId"));
@@ -36,7 +36,7 @@ Nccl* nccl() {
       n.comm_destroy = reinterpret_cast<decltype(n.comm_destroy)>(dlsym(n.h, "ncclCommDestroy"));
       n.error_string = reinterpret_cast<decltype(n.error_string)>(dlsym(n.h, "ncclGetErrorString"));
     }
-  }
+  });
   if (!n.h || !n.get_unique_id || !n.comm_init_rank || !n.all_reduce || !n.comm_destroy)
     return nullptr;
   return &n;

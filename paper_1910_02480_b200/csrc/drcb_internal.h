@@ -2,6 +2,7 @@
 // units. Not part of the ABI.
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -17,6 +18,42 @@ int cuda_fail(cudaError_t e, const char* where);
 void count_launch(int n = 1);
 void keep_pool_memory();
 int allreduce_sum(void* comm, void* buf, size_t count, int is_double, cudaStream_t st);
+
+// Per-device launch state: kernel attributes and SM counts are
+// properties of a device, and several host threads may launch on several
+// devices. A flag word per kernel remembers which devices are set up; the
+// attribute call is idempotent, so two threads racing on a first launch
+// both set it and neither launches before its own call returned.
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+struct DeviceFlags {
+  std::atomic<uint64_t> bits{0};
+  bool test(int dev) const { return (bits.load(std::memory_order_acquire) >> (dev & 63)) & 1; }
+  void set(int dev) { bits.fetch_or(uint64_t(1) << (dev & 63), std::memory_order_release); }
+};
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+template <class K>
+inline void smem_attr_once(DeviceFlags& f, K kern, int bytes) {
+  const int dev = current_device();
+  if (!f.test(dev)) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    f.set(dev);
+  }
+}
+// SM count of the current device (cached per device)
+inline int sm_count() {
+  static std::atomic<int> cache[64];
+  const int dev = current_device();
+  int v = cache[dev & 63].load(std::memory_order_relaxed);
+  if (!v) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev & 63].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 
 #define DRCB_CUDA(call)                                      \
   do {                                                       \

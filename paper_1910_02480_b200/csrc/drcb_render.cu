@@ -1090,10 +1090,9 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
   // streams must never see a half-written table)
   // per precision (one instantiation each) and per device (each device has
   // its own copy of the __device__ table)
-  static bool dirs_ready_dev[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  bool& dirs_ready = dirs_ready_dev[dev & 63];
+  static DeviceFlags dirs_flags;
+  const int dev = current_device();
+  bool dirs_ready = dirs_flags.test(dev);
   if (!dirs_ready) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);
@@ -1101,15 +1100,18 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
       k_texel_dirs<R><<<nblocks(MAP_TEXELS), TPB, 0, st>>>();
       LAUNCH_CHECK();
       DRCB_CUDA(cudaStreamSynchronize(st));
+      dirs_flags.set(dev);
       dirs_ready = true;
     }
   }
-  static int grid = 0;
+  // persistent grid: resident CTAs per SM x SMs of this device
+  static std::atomic<int> grid_dev[64];
+  int grid = grid_dev[dev & 63].load(std::memory_order_relaxed);
   if (!grid) {
-    int nsm = 0, per_sm = 0;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_paths<R>, MAP_TPB, 0);
-    grid = nsm * (per_sm > 0 ? per_sm : 1);
+    grid = sm_count() * (per_sm > 0 ? per_sm : 1);
+    grid_dev[dev & 63].store(grid, std::memory_order_relaxed);
   }
   int64_t total = int64_t(per);
   int g = int(std::min<int64_t>(grid, (total + MAP_TPB - 1) / MAP_TPB));

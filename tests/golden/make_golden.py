@@ -183,6 +183,53 @@ def cnn_fixture():
     save("cnn.npz", **out)
 
 
+def glass_fixtures():
+    """Transmission (dielectric) materials: the reference's cornell box with
+    two glass spheres as a whole frame, and the lens scene of the reference's
+    refraction test (pkg/tests/test_integrators.py:132-170) with a lamp, for
+    chains / paths / direct estimates through glass (bsdf.py:198-215, 257-319;
+    integrators.py:427-518)."""
+    doc = ref_scene_doc("cornell", 32)
+    doc["materials"]["glass"] = {"kind": "transmission", "albedo": [0.95, 0.95, 0.95], "ior": 1.5}
+    doc["materials"]["tint"] = {"kind": "transmission", "albedo": [0.9, 0.7, 0.5], "ior": 1.33}
+    doc["shapes"].append({"type": "sphere", "center": [1.9, 1.2, 2.2], "radius": 1.0,
+                          "material": "glass"})
+    doc["shapes"].append({"type": "sphere", "center": [3.9, 0.8, 1.5], "radius": 0.7,
+                          "material": "tint"})
+    frame_fixture("frame_glass.npz", doc, 8, 6, dict(direct_spp=2, indirect_tasks=2, mis_samples=8),
+                  n_points=8)
+    lens = {"camera": {"position": [0, 0, -5], "look_at": [0, 0, 0], "up": [0, 1, 0], "fov": 40.0,
+                       "resolution": [16, 16]},
+            "global_up": [0, 1, 0],
+            "materials": {"glass": {"kind": "transmission", "albedo": [0.95, 0.95, 0.95], "ior": 1.5},
+                          "gray": {"kind": "diffuse", "albedo": [0.5, 0.5, 0.5]},
+                          "lamp": {"kind": "diffuse", "albedo": [0.5, 0.5, 0.5],
+                                   "emission": [6.0, 6.0, 6.0]}},
+            "shapes": [{"type": "sphere", "center": [0, 0, 0], "radius": 1.0, "material": "glass"},
+                       {"type": "quad", "corner": [-50, -3, -50], "edge_u": [100, 0, 0],
+                        "edge_v": [0, 0, 100], "material": "gray"},
+                       {"type": "quad", "corner": [-1, 4, -1], "edge_u": [2, 0, 0],
+                        "edge_v": [0, 0, 2], "material": "lamp"}],
+            "point_lights": []}
+    rscene = parse_scene(json.dumps(lens))
+    rng = np.random.default_rng(17)
+    n = 2048
+    gx, gy = np.meshgrid(np.linspace(-0.95, 0.95, 32), np.linspace(-0.95, 0.95, 32))
+    O = np.concatenate([np.stack([gx.ravel(), gy.ravel(), np.full(gx.size, -5.0)], axis=1),
+                        rng.uniform(-2.5, 2.5, (n - gx.size, 3)) + np.array([0, 0, -4.0])])
+    D = np.concatenate([np.tile([0.0, 0.0, 1.0], (gx.size, 1)),
+                        rng.normal(size=(n - gx.size, 3)) * 0.3 + np.array([0, 0, 1.0])])
+    D /= np.linalg.norm(D, axis=1, keepdims=True)
+    pix = rng.integers(0, 1 << 40, n).astype(np.uint64)
+    smp = rng.integers(0, 1024, n).astype(np.uint64)
+    ch = rint.primary_chain_batch(rscene, O, D)
+    s = Sampler("independent", 3, 1)
+    L = rint.trace_radiance_batch(rscene, O, D, pix, smp, s, 8, skip_first_emission=False, rr_start=5)
+    Ld = rint.li_direct_batch(rscene, O, D, pix, smp, s, include_background=True)
+    save("glass_chain.npz", doc=doc_array(lens), O=O, D=D, pix=pix, smp=smp,
+         **{f"chain_{k}": np.asarray(v) for k, v in ch.items()}, L=L, L_direct=Ld)
+
+
 def main():
     geometry_fixture()
     trace_fixture()
@@ -204,8 +251,11 @@ def main():
     frame_fixture("frame_furnace.npz", env, 8, 1, dict(direct_spp=2, indirect_tasks=1, mis_samples=8))
 
 
-if __name__ == "__main__" and not ({"--train", "--pt", "--data", "--drcc"} & set(sys.argv)):
+if __name__ == "__main__" and not ({"--train", "--pt", "--data", "--drcc", "--glass"} & set(sys.argv)):
     main()
+    glass_fixtures()
+if __name__ == "__main__" and "--glass" in sys.argv:
+    glass_fixtures()
 
 
 def train_fixture():

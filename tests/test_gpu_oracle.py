@@ -165,3 +165,31 @@ def test_config3_frame_properties():
     assert np.all(np.isfinite(a)) and a.min() >= 0
     assert out[32][1]["entries"] == out[64][1]["entries"] > 0
     assert _rel_l2(a, b) <= 2e-2, _rel_l2(a, b)
+
+
+def test_frames_from_concurrent_host_threads_bit_identical(c1):
+    """Two host threads render on their own streams at once (the C-ABI's
+    per-device launch state is shared): same bits as a
+    sequential render."""
+    import threading
+
+    cfg = render.RenderConfig(direct_spp=1, indirect_tasks=2, precision=32, net_mode="fp16")
+    net = cnn.random_network(64, 0)
+    ref, _ = render.render_drc(c1, cfg, net)
+    out = [None, None]
+
+    def work(i):
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            img, _ = render.render_drc_device(c1, cfg, net)
+            res = img.double().cpu().numpy()
+        s.synchronize()
+        out[i] = res
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert np.array_equal(out[0], ref) and np.array_equal(out[1], ref)

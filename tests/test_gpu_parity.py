@@ -54,7 +54,7 @@ def test_intersect_fp32_prims_match_except_near_ties():
 
 
 @pytest.mark.parametrize("name", ["frame_c1.npz", "frame_cornell.npz", "frame_glossybox.npz",
-                                  "frame_room.npz", "frame_furnace.npz"])
+                                  "frame_room.npz", "frame_furnace.npz", "frame_glass.npz"])
 def test_gbuffer_and_direct_fp64(name):
     g = load_golden(name)
     sc = _scene(g)
@@ -79,7 +79,7 @@ def test_gbuffer_and_direct_fp64(name):
 
 
 @pytest.mark.parametrize("name", ["frame_c1.npz", "frame_cornell.npz", "frame_glossybox.npz",
-                                  "frame_room.npz"])
+                                  "frame_room.npz", "frame_glass.npz"])
 def test_stacks_cnn_shade_fp64(name):
     g = load_golden(name)
     sc = _scene(g)
@@ -103,7 +103,7 @@ def test_stacks_cnn_shade_fp64(name):
 
 
 @pytest.mark.parametrize("name", ["frame_c1.npz", "frame_cornell.npz", "frame_glossybox.npz",
-                                  "frame_room.npz", "frame_furnace.npz"])
+                                  "frame_room.npz", "frame_furnace.npz", "frame_glass.npz"])
 def test_render_drc_fp64_image(name):
     g = load_golden(name)
     sc = _scene(g)
@@ -146,3 +146,56 @@ def test_cnn_fp32_matches_reference_k8_k64():
     blur = cnn.make_blur_network(16)
     y = cnn.forward_batch(blur, g["blur_x"], mode="fp32")
     assert np.allclose(y, g["blur_y"], rtol=1e-5, atol=1e-6)
+
+
+def test_glass_chains_paths_direct_fp64():
+    """Transmission: chains, paths and direct estimates through the glass
+    sphere of the reference's refraction test scene (plus a lamp) against the
+    reference's own batch functions (golden glass_chain.npz)."""
+    g = load_golden("glass_chain.npz")
+    sc = _scene(g)
+    ch = render.primary_chain_batch(sc, g["O"], g["D"], precision=64)
+    for k in ("found", "escaped", "mat"):
+        assert np.array_equal(ch[k], g[f"chain_{k}"]), k
+    for k in ("position", "normal", "throughput", "direction", "t_total"):
+        assert np.allclose(ch[k], g[f"chain_{k}"], rtol=1e-9, atol=1e-12), k
+
+    class S:
+        kind, seed, spp = "independent", 3, 1
+
+    L = render.trace_radiance_batch(sc, g["O"], g["D"], g["pix"], g["smp"], S, 8, False, 5)
+    assert np.allclose(L, g["L"], rtol=1e-9, atol=1e-12)
+    Ld = render.li_direct_batch(sc, g["O"], g["D"], g["pix"], g["smp"], S, True)
+    assert np.allclose(Ld, g["L_direct"], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_refraction_chain_matches_manual_snell_walk(precision):
+    """pkg/tests/test_integrators.py:132-170: a ray entering the unit glass
+    sphere above its centre is bent down and lands on the floor (y = -3)
+    where an independent step-by-step Snell walk says (atol 1e-3)."""
+    g = load_golden("glass_chain.npz")
+    sc = _scene(g)
+    origin = np.array([0.0, 0.3, -5.0])
+    direction = np.array([0.0, 0.0, 1.0])
+    res = render.primary_chain_batch(sc, origin[None], direction[None], precision=precision)
+    assert res["found"][0]
+
+    def refract(d, n, eta):
+        ci = -d @ n
+        s2 = eta * eta * (1 - ci * ci)
+        if s2 >= 1:
+            return d + 2 * ci * n
+        return eta * d + (eta * ci - np.sqrt(1 - s2)) * n
+
+    p1 = origin + direction * (5.0 - np.sqrt(1 - 0.09))
+    n1 = p1 / np.linalg.norm(p1)
+    d1 = refract(direction, n1, 1 / 1.5)
+    d1 /= np.linalg.norm(d1)
+    p2 = p1 + (-2.0 * (p1 @ d1)) * d1
+    n2 = -(p2 / np.linalg.norm(p2))
+    d2 = refract(d1, n2, 1.5)
+    d2 /= np.linalg.norm(d2)
+    target = p2 + ((-3.0 - p2[1]) / d2[1]) * d2
+    assert np.allclose(res["position"][0], target, atol=1e-3)
+    assert np.all(res["throughput"][0] < 0.95)  # two transmission links (1 - Fresnel) * albedo

@@ -32,7 +32,7 @@ def test_intersect_matches_reference_exactly():
 
 
 FRAMES = ["frame_c1.npz", "frame_cornell.npz", "frame_glossybox.npz", "frame_room.npz",
-          "frame_furnace.npz"]
+          "frame_furnace.npz", "frame_glass.npz"]
 
 
 @pytest.mark.parametrize("name", FRAMES)
@@ -53,7 +53,7 @@ def test_gbuffer_direct(name):
         assert np.allclose(direct.reshape(h, w, 3), g["direct"], rtol=1e-9, atol=1e-12)
 
 
-@pytest.mark.parametrize("name", FRAMES[:4])
+@pytest.mark.parametrize("name", FRAMES[:4] + ["frame_glass.npz"])
 def test_stacks_shade(name):
     g = load_golden(name)
     osc = _osc(g)
@@ -100,7 +100,28 @@ def test_cnn_k8_and_blur():
     assert np.allclose(y, g["blur_y"], rtol=1e-5, atol=1e-6)
 
 
-@pytest.mark.parametrize("name", ["frame_c1.npz", "frame_cornell.npz", "frame_furnace.npz"])
+def test_glass_chains_paths_direct():
+    """Transmission (dielectric) rays through the reference's refraction-test
+    lens scene (pkg/tests/test_integrators.py:132-170, plus a lamp)."""
+    g = load_golden("glass_chain.npz")
+    osc = _osc(g)
+
+    class S:
+        kind, seed, spp = "independent", 3, 1
+
+    ch = O.primary_chain_batch(osc, g["O"], g["D"])
+    for k in ("found", "escaped", "mat"):
+        assert np.array_equal(ch[k], g[f"chain_{k}"]), k
+    for k in ("position", "normal", "throughput", "direction", "t_total"):
+        assert np.allclose(ch[k], g[f"chain_{k}"], rtol=1e-9, atol=1e-12), k
+    assert np.allclose(O.trace_radiance_batch(osc, g["O"], g["D"], g["pix"], g["smp"], S, 8),
+                       g["L"], rtol=1e-9, atol=1e-12)
+    assert np.allclose(O.li_direct_batch(osc, g["O"], g["D"], g["pix"], g["smp"], S),
+                       g["L_direct"], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["frame_c1.npz", "frame_cornell.npz", "frame_furnace.npz",
+                                  "frame_glass.npz"])
 def test_render_drc_frame(name):
     g = load_golden(name)
     osc = _osc(g)
