@@ -206,6 +206,26 @@ int drcb_render_drc_entries(const DrcbScene *scene, const DrcbNet *net,
                             int32_t net_mode, void *image, int64_t *telemetry_host,
                             const DrcbEntries *entries, void *stream);
 
+/* ---- progressive frames: the control plane of render_drc
+ * (drc/cache.py:426-469). begin renders the G-buffer and direct pass and
+ * reserves an entry pool for max_points cache points; add_points evaluates
+ * a batch of cache points (host arrays in budget order: stacks, network,
+ * shade) and appends the live ones to the pool in order; composite writes
+ * image = direct + the interpolation of the entries so far at pass spacing
+ * r (a pass end, a snapshot, or the interrupted frame); info synchronises
+ * and returns {entries, nonfinite, points evaluated, max_points}. All
+ * asynchronous on `stream` except info. */
+typedef struct DrcbFrame DrcbFrame;
+int drcb_frame_begin(const DrcbScene *scene, const DrcbNet *net, const DrcbCamera *cam,
+                     const DrcbRenderCfg *cfg, int32_t net_mode, int64_t max_points,
+                     DrcbFrame **out, void *stream);
+int drcb_frame_add_points(DrcbFrame *frame, const int32_t *px_host, const int32_t *py_host,
+                          const uint64_t *keys_host, int64_t n, void *stream);
+int drcb_frame_composite(DrcbFrame *frame, int32_t r, void *image, void *stream);
+int drcb_frame_info(DrcbFrame *frame, int64_t *out4, void *stream);
+int drcb_frame_entries(DrcbFrame *frame, const DrcbEntries *out, void *stream);
+int drcb_frame_end(DrcbFrame *frame, void *stream);
+
 /* render(mode="pt") (drc/integrators.py:678-722): spp = cfg->direct_spp
  * jittered paths per pixel (max_path_depth, rr_start), image (H*W,3) Real. */
 int drcb_render_pt(const DrcbScene *scene, const DrcbCamera *cam, const DrcbRenderCfg *cfg,

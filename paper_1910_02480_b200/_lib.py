@@ -91,6 +91,13 @@ _SIGS = [
                                         vp, vp, vp, vp, C.c_int64, C.c_int32, vp, vp, vp]),
     ("drcb_render_drc", C.c_int, [vp, vp, C.POINTER(Camera), C.POINTER(RenderCfg), vp, vp, vp,
                                   C.c_int64, C.c_int32, C.c_int32, vp, vp, vp]),
+    ("drcb_frame_begin", C.c_int, [vp, vp, C.POINTER(Camera), C.POINTER(RenderCfg), C.c_int32,
+                                   C.c_int64, C.POINTER(vp), vp]),
+    ("drcb_frame_add_points", C.c_int, [vp, vp, vp, vp, C.c_int64, vp]),
+    ("drcb_frame_composite", C.c_int, [vp, C.c_int32, vp, vp]),
+    ("drcb_frame_info", C.c_int, [vp, C.POINTER(C.c_int64), vp]),
+    ("drcb_frame_entries", C.c_int, [vp, C.POINTER(Entries), vp]),
+    ("drcb_frame_end", C.c_int, [vp, vp]),
     ("drcb_render_pt", C.c_int, [vp, C.POINTER(Camera), C.POINTER(RenderCfg), vp, vp, vp]),
     ("drcb_reference_map", C.c_int, [vp, C.POINTER(RenderCfg), vp, vp, C.c_uint64, C.c_int32, vp,
                                      vp, vp]),

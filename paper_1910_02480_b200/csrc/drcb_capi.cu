@@ -79,32 +79,24 @@ __global__ void k_gather_points(DrcbGBuffer gb, int W, const int32_t* px, const 
   mat[i] = f ? gb.mat[q] : 0;
 }
 
-// stable compaction of live points into the entry pool (append order =
-// task order, cache.py:183-190, 450-452)
+// stable compaction of live points into the entry pool after the *base
+// entries already there (append order = task order, cache.py:183-190, 450-452)
 template <typename R>
-__global__ void k_scatter_entries(const uint8_t* live, const int* rank, int64_t n,
+__global__ void k_scatter_entries(const uint8_t* live, const int* rank, int64_t n, const int* base,
                                   const int32_t* px, const int32_t* py, const R* nrm, const R* L,
                                   int32_t* epx, int32_t* epy, R* en, R* erad, const R* pos,
-                                  const R* gthr, int W, DrcbEntries dump) {
+                                  const R* gthr, int W, R* epos, R* ethr) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n || !live[i]) return;
-  int j = rank[i];
+  const int j = *base + rank[i];
+  const int64_t pix = int64_t(py[i]) * W + px[i];
   epx[j] = px[i];
   epy[j] = py[i];
   for (int k = 0; k < 3; ++k) {
     en[3 * j + k] = nrm[3 * i + k];
     erad[3 * j + k] = L[3 * i + k];
-  }
-  if (dump.px) {  // entry pool copy-out (DrcState.entries, cache.py:196-201)
-    const int64_t pix = int64_t(py[i]) * W + px[i];
-    dump.px[j] = px[i];
-    dump.py[j] = py[i];
-    for (int k = 0; k < 3; ++k) {
-      static_cast<R*>(dump.position)[3 * j + k] = pos[3 * i + k];
-      static_cast<R*>(dump.normal)[3 * j + k] = nrm[3 * i + k];
-      static_cast<R*>(dump.radiance)[3 * j + k] = L[3 * i + k];
-      static_cast<R*>(dump.throughput)[3 * j + k] = gthr[3 * pix + k];
-    }
+    epos[3 * j + k] = pos[3 * i + k];  // DrcState.entries (cache.py:196-201)
+    ethr[3 * j + k] = gthr[3 * pix + k];
   }
 }
 
@@ -114,7 +106,7 @@ __global__ void k_u8_to_int(const uint8_t* a, int* b, int64_t n) {
 }
 
 __global__ void k_entry_count(const int* rank, const uint8_t* live, int64_t n, int* m) {
-  *m = n > 0 ? rank[n - 1] + int(live[n - 1]) : 0;
+  *m += n > 0 ? rank[n - 1] + int(live[n - 1]) : 0;
 }
 
 // Per-frame stage timing (CUDA events on the frame's stream; read only when
@@ -140,54 +132,91 @@ struct StageEvents {
   }
 };
 
+// A frame in progress (drc/cache.py:377-470 as a resumable object): the
+// G-buffer and direct pass are computed once (begin); cache points are then
+// evaluated in any number of submissions (add_points: maps -> network ->
+// shade -> append to the entry pool in submission order, cache.py:183-190,
+// 436-452); composite interpolates the entries so far with a pass spacing r
+// and adds the direct layer (cache.py:283-345, 463). Everything is
+// stream-ordered; nothing synchronises the host except `info`.
 template <typename R>
-int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
-                 const DrcbRenderCfg* cfg, const int32_t* px_h, const int32_t* py_h,
-                 const uint64_t* keys_h, int64_t np_, int r_final, int net_mode, R* image,
-                 int64_t* tel, cudaStream_t st, const DrcbEntries* dump = nullptr) {
-  const DevScene& S = scene->dev;
-  keep_pool_memory();
-  DevCamera C = make_camera(*cam);
-  const int W = C.W, H = C.H;
-  const int64_t npx = int64_t(W) * H;
-  StageEvents E;
-  if (tel) E.create();
-  E.rec(0, st);
-  // ---- frame buffers (stream-ordered allocations from the pool)
-  size_t bytes = npx * (2 + 4 + sizeof(R) * 16) + 256;
-  uint8_t* fb = nullptr;
-  DRCB_CUDA(cudaMallocAsync((void**)&fb, bytes, st));
-  DrcbGBuffer gb;
-  uint8_t* cur = fb;
-  auto take = [&](size_t b) {
-    uint8_t* p = cur;
-    cur += (b + 15) & ~size_t(15);
-    return p;
-  };
-  R* direct = (R*)take(npx * 3 * sizeof(R));
-  gb.position = take(npx * 3 * sizeof(R));
-  gb.normal = take(npx * 3 * sizeof(R));
-  gb.throughput = take(npx * 3 * sizeof(R));
-  gb.direction = take(npx * 3 * sizeof(R));
-  gb.t_total = take(npx * sizeof(R));
-  gb.mat = (int32_t*)take(npx * 4);
-  gb.found = take(npx);
-  gb.escaped = take(npx);
-  int64_t* d_nf = (int64_t*)take(8);
-  int* d_m = (int*)take(4);
-  DRCB_CUDA(cudaMemsetAsync(d_nf, 0, 8, st));
-  DRCB_CUDA(cudaMemsetAsync(d_m, 0, 4, st));
-  DrcbRenderCfg dcfg = *cfg;
-  dcfg.include_background = 0;  // escaped chains carry the env in the indirect layer
-  int rc = launch_gbuffer_direct<R>(S, C, dcfg, cfg->tile, gb, direct, d_nf, st);
-  if (rc) return rc;
-  E.rec(1, st);
-  uint8_t* pb = nullptr;
-  if (np_ > 0) {
-    size_t pbytes = np_ * (4 * 8 + 8 + 1 + sizeof(R) * (3 * 6 + 2 + 9)) + 32 * 24 +
+struct FrameCtx {
+  const DevScene* S = nullptr;
+  DrcbNet* net = nullptr;
+  DevCamera C{};
+  DrcbRenderCfg cfg{};
+  int net_mode = 0;
+  int W = 0, H = 0;
+  int64_t npx = 0, cap = 0, points = 0;
+  uint8_t* fb = nullptr;    // frame buffers (G-buffer, direct, counters)
+  uint8_t* pool = nullptr;  // entry pool (cap entries)
+  DrcbGBuffer gb{};
+  R* direct = nullptr;
+  int64_t* d_nf = nullptr;  // non-finite samples
+  int* d_m = nullptr;       // entries so far
+  int32_t *epx = nullptr, *epy = nullptr;
+  R *en = nullptr, *erad = nullptr, *epos = nullptr, *ethr = nullptr;
+  StageEvents* E = nullptr;  // stage timing (single-submission frames)
+
+  int begin(cudaStream_t st) {
+    keep_pool_memory();
+    npx = int64_t(W) * H;
+    size_t bytes = npx * (2 + 4 + sizeof(R) * 16) + 256;
+    DRCB_CUDA(cudaMallocAsync((void**)&fb, bytes, st));
+    uint8_t* cur = fb;
+    auto take = [&](size_t b) {
+      uint8_t* p = cur;
+      cur += (b + 15) & ~size_t(15);
+      return p;
+    };
+    direct = (R*)take(npx * 3 * sizeof(R));
+    gb.position = take(npx * 3 * sizeof(R));
+    gb.normal = take(npx * 3 * sizeof(R));
+    gb.throughput = take(npx * 3 * sizeof(R));
+    gb.direction = take(npx * 3 * sizeof(R));
+    gb.t_total = take(npx * sizeof(R));
+    gb.mat = (int32_t*)take(npx * 4);
+    gb.found = take(npx);
+    gb.escaped = take(npx);
+    d_nf = (int64_t*)take(8);
+    d_m = (int*)take(4);
+    DRCB_CUDA(cudaMemsetAsync(d_nf, 0, 8, st));
+    DRCB_CUDA(cudaMemsetAsync(d_m, 0, 4, st));
+    if (cap > 0) {
+      DRCB_CUDA(cudaMallocAsync((void**)&pool, size_t(cap) * (8 + 12 * sizeof(R)) + 64, st));
+      cur = pool;
+      epx = (int32_t*)take(cap * 4);
+      epy = (int32_t*)take(cap * 4);
+      en = (R*)take(cap * 3 * sizeof(R));
+      erad = (R*)take(cap * 3 * sizeof(R));
+      epos = (R*)take(cap * 3 * sizeof(R));
+      ethr = (R*)take(cap * 3 * sizeof(R));
+    }
+    DrcbRenderCfg dcfg = cfg;
+    dcfg.include_background = 0;  // escaped chains carry the env in the indirect layer
+    if (E) E->rec(0, st);
+    int rc = launch_gbuffer_direct<R>(*S, C, dcfg, cfg.tile, gb, direct, d_nf, st);
+    if (E) E->rec(1, st);
+    return rc;
+  }
+
+  // evaluate np_ cache points (host arrays, budget order) and append the
+  // live ones to the entry pool
+  int add_points(const int32_t* px_h, const int32_t* py_h, const uint64_t* keys_h, int64_t np_,
+                 cudaStream_t st) {
+    if (np_ <= 0) return 0;
+    if (points + np_ > cap) return fail(DRCB_ECONTRACT, "frame: more cache points than reserved");
+    points += np_;
+    size_t pbytes = np_ * (4 * 8 + 8 + 1 + sizeof(R) * (3 * 4 + 2 + 9)) + 32 * 24 +
                     np_ * size_t(7 + 3) * 1024 * 4;
+    uint8_t* pb = nullptr;
     DRCB_CUDA(cudaMallocAsync((void**)&pb, pbytes, st));
-    cur = pb;
+    uint8_t* cur = pb;
+    auto take = [&](size_t b) {
+      uint8_t* p = cur;
+      cur += (b + 15) & ~size_t(15);
+      return p;
+    };
     int32_t* px = (int32_t*)take(np_ * 4);
     int32_t* py = (int32_t*)take(np_ * 4);
     uint64_t* keys = (uint64_t*)take(np_ * 8);
@@ -195,14 +224,10 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
     uint8_t* live = take(np_);
     int* rank = (int*)take(np_ * 4);
     int* flags = (int*)take(np_ * 4);
-    int32_t* epx = (int32_t*)take(np_ * 4);
-    int32_t* epy = (int32_t*)take(np_ * 4);
     R* pos = (R*)take(np_ * 3 * sizeof(R));
     R* nrm = (R*)take(np_ * 3 * sizeof(R));
     R* wo = (R*)take(np_ * 3 * sizeof(R));
     R* Le = (R*)take(np_ * 3 * sizeof(R));
-    R* en = (R*)take(np_ * 3 * sizeof(R));
-    R* erad = (R*)take(np_ * 3 * sizeof(R));
     R* s_r = (R*)take(np_ * sizeof(R));
     R* s_d = (R*)take(np_ * sizeof(R));
     R* frames = (R*)take(np_ * 9 * sizeof(R));
@@ -225,12 +250,12 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
         DRCB_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(xin) + xb / np8 * np_, 0,
                                   xb / np8 * (np8 - np_), st));
     }
-    rc = launch_render_stacks<R>(S, *cfg, pos, nrm, keys, live, np_, xin ? nullptr : stacks, s_r,
-                                 s_d, frames, d_nf, st, xin,
-                                 xin ? (net_mode == DRCB_NET_BF16 ? 1 : (net_mode == DRCB_NET_FP16 ? 3 : 2)) : 0,
-                                 cpad);
+    int rc = launch_render_stacks<R>(*S, cfg, pos, nrm, keys, live, np_, xin ? nullptr : stacks, s_r,
+                                     s_d, frames, d_nf, st, xin,
+                                     xin ? (net_mode == DRCB_NET_BF16 ? 1 : (net_mode == DRCB_NET_FP16 ? 3 : 2)) : 0,
+                                     cpad);
     if (rc) return rc;
-    E.rec(2, st);
+    if (E) E->rec(2, st);
     if (!tc)
       rc = forward_f32_chunked(net->impl, stacks, pred, np_, st);
     else if (xin)
@@ -239,10 +264,10 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
       rc = forward_tc(net->impl, stacks, pred, np_, net_mode, st);
     if (xin) DRCB_CUDA(cudaFreeAsync(xin, st));
     if (rc) return rc;
-    E.rec(3, st);
-    rc = launch_shade<R>(S, *cfg, pred, s_r, frames, wo, mat, keys, live, np_, Le, st);
+    if (E) E->rec(3, st);
+    rc = launch_shade<R>(*S, cfg, pred, s_r, frames, wo, mat, keys, live, np_, Le, st);
     if (rc) return rc;
-    // stable compaction of live points into the entry pool
+    // stable compaction of live points, appended after the entries so far
     k_u8_to_int<<<nb, 128, 0, st>>>(live, flags, np_);
     size_t tmpb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmpb, flags, rank, int(np_), st);
@@ -250,35 +275,88 @@ int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
     DRCB_CUDA(cudaMallocAsync(&tmp, tmpb, st));
     cub::DeviceScan::ExclusiveSum(tmp, tmpb, flags, rank, int(np_), st);
     DRCB_CUDA(cudaFreeAsync(tmp, st));
-    DrcbEntries dz{};
-    if (dump) dz = *dump;
-    k_scatter_entries<R><<<nb, 128, 0, st>>>(live, rank, np_, px, py, nrm, Le, epx, epy, en, erad,
-                                             pos, static_cast<const R*>(gb.throughput), W, dz);
+    k_scatter_entries<R><<<nb, 128, 0, st>>>(live, rank, np_, d_m, px, py, nrm, Le, epx, epy, en,
+                                             erad, pos, static_cast<const R*>(gb.throughput), W,
+                                             epos, ethr);
     k_entry_count<<<1, 1, 0, st>>>(rank, live, np_, d_m);
     count_launch(5);  // u8_to_int, scan (2), scatter, entry_count
-    E.rec(4, st);
-    rc = launch_interp_composite<R>(S, W, H, gb, epx, epy, en, erad, np_, d_m, r_final, direct,
-                                    image, st);
-    if (rc) return rc;
-  } else {
+    if (E) E->rec(4, st);
+    DRCB_CUDA(cudaFreeAsync(pb, st));
+    return 0;
+  }
+
+  // image = direct + interpolation of the entries so far at spacing r
+  int composite(int r, R* image, cudaStream_t st) {
+    return launch_interp_composite<R>(*S, W, H, gb, epx, epy, en, erad, cap > 0 ? cap : 0,
+                                      cap > 0 ? d_m : nullptr, r, direct, image, st);
+  }
+
+  int entries_out(const DrcbEntries& out, cudaStream_t st) {
+    if (cap <= 0) return 0;
+    const size_t v = size_t(cap) * 3 * sizeof(R);
+    if (out.px) DRCB_CUDA(cudaMemcpyAsync(out.px, epx, cap * 4, cudaMemcpyDeviceToDevice, st));
+    if (out.py) DRCB_CUDA(cudaMemcpyAsync(out.py, epy, cap * 4, cudaMemcpyDeviceToDevice, st));
+    if (out.position) DRCB_CUDA(cudaMemcpyAsync(out.position, epos, v, cudaMemcpyDeviceToDevice, st));
+    if (out.normal) DRCB_CUDA(cudaMemcpyAsync(out.normal, en, v, cudaMemcpyDeviceToDevice, st));
+    if (out.radiance) DRCB_CUDA(cudaMemcpyAsync(out.radiance, erad, v, cudaMemcpyDeviceToDevice, st));
+    if (out.throughput) DRCB_CUDA(cudaMemcpyAsync(out.throughput, ethr, v, cudaMemcpyDeviceToDevice, st));
+    return 0;
+  }
+
+  int counters(int64_t& m, int64_t& nf, cudaStream_t st) {
+    int mm = 0;
+    int64_t n = 0;
+    DRCB_CUDA(cudaMemcpyAsync(&mm, d_m, 4, cudaMemcpyDeviceToHost, st));
+    DRCB_CUDA(cudaMemcpyAsync(&n, d_nf, 8, cudaMemcpyDeviceToHost, st));
+    DRCB_CUDA(cudaStreamSynchronize(st));
+    m = mm;
+    nf = n;
+    return 0;
+  }
+
+  int end(cudaStream_t st) {
+    if (pool) DRCB_CUDA(cudaFreeAsync(pool, st));
+    if (fb) DRCB_CUDA(cudaFreeAsync(fb, st));
+    pool = fb = nullptr;
+    return 0;
+  }
+};
+
+template <typename R>
+int render_frame(const DrcbScene* scene, DrcbNet* net, const DrcbCamera* cam,
+                 const DrcbRenderCfg* cfg, const int32_t* px_h, const int32_t* py_h,
+                 const uint64_t* keys_h, int64_t np_, int r_final, int net_mode, R* image,
+                 int64_t* tel, cudaStream_t st, const DrcbEntries* dump = nullptr) {
+  FrameCtx<R> F;
+  F.S = &scene->dev;
+  F.net = net;
+  F.C = make_camera(*cam);
+  F.W = F.C.W;
+  F.H = F.C.H;
+  F.cfg = *cfg;
+  F.net_mode = net_mode;
+  F.cap = np_;
+  StageEvents E;
+  if (tel) {
+    E.create();
+    F.E = &E;
+  }
+  int rc = F.begin(st);
+  if (!rc) rc = F.add_points(px_h, py_h, keys_h, np_, st);
+  if (np_ <= 0) {
     E.rec(2, st);
     E.rec(3, st);
     E.rec(4, st);
-    rc = launch_interp_composite<R>(S, W, H, gb, nullptr, nullptr, nullptr, nullptr, 0, nullptr,
-                                    r_final, direct, image, st);
-    if (rc) return rc;
   }
+  if (!rc) rc = F.composite(r_final, image, st);
   E.rec(5, st);
-  int64_t nf = 0;
-  int m = 0;
+  if (!rc && dump) rc = F.entries_out(*dump, st);
+  int64_t m = 0, nf = 0;
+  if (!rc && tel) rc = F.counters(m, nf, st);
+  int rc2 = F.end(st);
+  if (rc) return rc;
+  if (rc2) return rc2;
   if (tel) {
-    DRCB_CUDA(cudaMemcpyAsync(&nf, d_nf, 8, cudaMemcpyDeviceToHost, st));
-    DRCB_CUDA(cudaMemcpyAsync(&m, d_m, 4, cudaMemcpyDeviceToHost, st));
-  }
-  if (pb) DRCB_CUDA(cudaFreeAsync(pb, st));
-  DRCB_CUDA(cudaFreeAsync(fb, st));
-  if (tel) {
-    DRCB_CUDA(cudaStreamSynchronize(st));
     tel[0] = m;
     tel[1] = 0;  // fallback pixels: unreachable by construction (cache.py:306-307)
     tel[2] = nf;
@@ -478,6 +556,100 @@ extern "C" int drcb_render_drc_entries(const DrcbScene* scene, const DrcbNet* ne
                                 entries);
   return render_frame<float>(scene, mnet, cam, cfg, px_host, py_host, keys_host, n_points, r_final,
                              net_mode, (float*)image, telemetry_host, S_(stream), entries);
+}
+
+// ---- progressive frames (drc/cache.py:426-469 control plane): the host
+// runs the pass loop, polls interrupts between passes and takes snapshots
+struct DrcbFrame {
+  int prec = 64;
+  FrameCtx<double> d;
+  FrameCtx<float> f;
+};
+
+namespace {
+template <typename F>
+int with_frame(DrcbFrame* fr, F&& fn) {
+  return fr->prec == 64 ? fn(fr->d) : fn(fr->f);
+}
+}  // namespace
+
+extern "C" int drcb_frame_begin(const DrcbScene* scene, const DrcbNet* net, const DrcbCamera* cam,
+                                const DrcbRenderCfg* cfg, int32_t net_mode, int64_t max_points,
+                                DrcbFrame** out, void* stream) {
+  NEED(scene);
+  NEED(cam);
+  NEED(out);
+  if (check_cfg(cfg)) return DRCB_ECONFIG;
+  if (max_points < 0) return fail(DRCB_ECONTRACT, "drcb_frame_begin: negative max_points");
+  if (max_points > 0 && !net) return fail(DRCB_ECONTRACT, "drcb_frame_begin: points need a network");
+  DrcbFrame* fr = new DrcbFrame();
+  fr->prec = cfg->precision;
+  int rc = with_frame(fr, [&](auto& F) {
+    F.S = &scene->dev;
+    F.net = const_cast<DrcbNet*>(net);
+    F.C = make_camera(*cam);
+    F.W = F.C.W;
+    F.H = F.C.H;
+    F.cfg = *cfg;
+    F.net_mode = net_mode;
+    F.cap = max_points;
+    return F.begin(S_(stream));
+  });
+  if (rc) {
+    with_frame(fr, [&](auto& F) { return F.end(S_(stream)); });
+    delete fr;
+    return rc;
+  }
+  *out = fr;
+  return 0;
+}
+
+extern "C" int drcb_frame_add_points(DrcbFrame* fr, const int32_t* px_host, const int32_t* py_host,
+                                     const uint64_t* keys_host, int64_t n, void* stream) {
+  NEED(fr);
+  if (n <= 0) return 0;
+  if (!px_host || !py_host || !keys_host) return fail(DRCB_ECONTRACT, "drcb_frame_add_points: null arrays");
+  return with_frame(fr, [&](auto& F) {
+    for (int64_t i = 0; i < n; ++i)
+      if (px_host[i] < 0 || px_host[i] >= F.W || py_host[i] < 0 || py_host[i] >= F.H)
+        return fail(DRCB_ECONTRACT, "cache point outside the image");
+    return F.add_points(px_host, py_host, keys_host, n, S_(stream));
+  });
+}
+
+extern "C" int drcb_frame_composite(DrcbFrame* fr, int32_t r, void* image, void* stream) {
+  NEED(fr);
+  NEED(image);
+  if (r < 1) return fail(DRCB_ECONFIG, "drcb_frame_composite: spacing r must be >= 1");
+  if (fr->prec == 64) return fr->d.composite(r, static_cast<double*>(image), S_(stream));
+  return fr->f.composite(r, static_cast<float*>(image), S_(stream));
+}
+
+extern "C" int drcb_frame_info(DrcbFrame* fr, int64_t* out4, void* stream) {
+  NEED(fr);
+  NEED(out4);
+  return with_frame(fr, [&](auto& F) {
+    int64_t m = 0, nf = 0;
+    int rc = F.counters(m, nf, S_(stream));
+    out4[0] = m;
+    out4[1] = nf;
+    out4[2] = F.points;
+    out4[3] = F.cap;
+    return rc;
+  });
+}
+
+extern "C" int drcb_frame_entries(DrcbFrame* fr, const DrcbEntries* out, void* stream) {
+  NEED(fr);
+  NEED(out);
+  return with_frame(fr, [&](auto& F) { return F.entries_out(*out, S_(stream)); });
+}
+
+extern "C" int drcb_frame_end(DrcbFrame* fr, void* stream) {
+  if (!fr) return 0;
+  int rc = with_frame(fr, [&](auto& F) { return F.end(S_(stream)); });
+  delete fr;
+  return rc;
 }
 
 extern "C" int drcb_render_pt(const DrcbScene* scene, const DrcbCamera* cam,

@@ -336,26 +336,138 @@ def render_drc_device(scene, config, net, camera=None, out=None, precision=None,
     return out, telemetry
 
 
-def render_drc(scene, config, net, interrupt=None, snapshots=None):
-    """Drop-in for drc.cache.render_drc: (image (H,W,3) float64, telemetry).
+class DeviceFrame:
+    """A DRC frame in progress on the device (drcb_frame_*): G-buffer + direct
+    at construction, then cache points in any number of submissions, then
+    composites at a pass spacing r. The host pass loop of render_drc drives
+    it (cache.py:426-469)."""
 
-    `snapshots` budgets are rendered as clean runs at that budget, which the
-    reference guarantees equal its mid-run snapshots (cache.py:381-385).
-    `interrupt` is polled once before the frame; a frame is one device
-    submission, so there is no mid-frame pass boundary to stop at."""
-    if interrupt is not None and interrupt():
-        config = _replace(config, indirect_tasks=1, passes=None)
-    img, tel = render_drc_device(scene, config, net, entries=True)
-    image = img.double().cpu().numpy()
-    if snapshots:
-        snaps = {}
-        for b in sorted(set(snapshots)):
-            if b >= tel["tasks"]:
-                snaps[b] = image if b == tel["tasks"] else None
-                continue
-            si, _ = render_drc_device(scene, _replace(config, indirect_tasks=b, passes=None), net)
-            snaps[b] = si.double().cpu().numpy()
-        tel["snapshots"] = {k: v for k, v in snaps.items() if v is not None}
+    def __init__(self, scene, config, net, camera=None, max_points=0):
+        torch = _torch()
+        self.prec = int(getattr(config, "precision", 64))
+        self.dtype = torch.float64 if self.prec == 64 else torch.float32
+        self.cam = camera or scene.camera
+        self.w, self.h = self.cam.resolution
+        self.net_mode = MODES[getattr(config, "net_mode", "fp32")]
+        dn = device_net(net) if max_points else None
+        self._keep = (dn,)
+        h = C.c_void_p()
+        _lib.call("drcb_frame_begin", device_scene(scene).handle, dn.handle if dn else None,
+                  C.byref(camera_struct(self.cam)), C.byref(_cfg_struct(config, self.prec)),
+                  self.net_mode, int(max_points), C.byref(h), _lib.stream_ptr())
+        self.handle = h
+        self.max_points = int(max_points)
+
+    def add_points(self, px, py, keys):
+        px = np.ascontiguousarray(px, dtype=np.int32)
+        py = np.ascontiguousarray(py, dtype=np.int32)
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        if len(px):
+            _lib.call("drcb_frame_add_points", self.handle, px.ctypes.data_as(C.c_void_p),
+                      py.ctypes.data_as(C.c_void_p), keys.ctypes.data_as(C.c_void_p), len(px),
+                      _lib.stream_ptr())
+
+    def composite(self, r, out=None):
+        torch = _torch()
+        if out is None:
+            out = torch.empty((self.h, self.w, 3), dtype=self.dtype, device="cuda")
+        _lib.call("drcb_frame_composite", self.handle, int(r), _lib.ptr(out), _lib.stream_ptr())
+        return out
+
+    def info(self):
+        o = (C.c_int64 * 4)()
+        _lib.call("drcb_frame_info", self.handle, o, _lib.stream_ptr())
+        return {"entries": int(o[0]), "nonfinite": int(o[1]), "points": int(o[2])}
+
+    def entries(self):
+        torch = _torch()
+        n = max(self.max_points, 1)
+        bufs = [torch.zeros(n, dtype=torch.int32, device="cuda") for _ in range(2)] + \
+               [torch.zeros((n, 3), dtype=self.dtype, device="cuda") for _ in range(4)]
+        ent = _lib.Entries(*[C.c_void_p(b.data_ptr()) for b in bufs])
+        _lib.call("drcb_frame_entries", self.handle, C.byref(ent), _lib.stream_ptr())
+        m = self.info()["entries"]
+        return [b[:m].cpu().numpy().astype(np.float64 if b.dim() == 2 else np.int64) for b in bufs]
+
+    def close(self):
+        if getattr(self, "handle", None) and _lib._lib is not None:
+            _lib._lib.drcb_frame_end(self.handle, _lib.stream_ptr())
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def render_drc(scene, config, net, interrupt=None, snapshots=None):
+    """Drop-in for drc.cache.render_drc (cache.py:377-470): (image (H,W,3)
+    float64, telemetry).
+
+    The reference's progressive control plane on the host: pass by pass and
+    task by task (plan_pass, cache.py:96-113), each pass's cache points
+    evaluated on the device in one submission (split at snapshot budgets);
+    `snapshots` budgets are composited mid-run from the entries so far (the
+    reference's append-only pool makes them equal to clean runs,
+    cache.py:381-385, 450-452); `interrupt` is polled after every pass and
+    finalises the frame at that pass (cache.py:460-461). Telemetry carries
+    per-pass {index, r, tasks, entries, seconds}."""
+    w, h = scene.camera.resolution
+    t0 = time.time()
+    budget = task_budget(config)
+    px_all, _, _, _, _ = plan_points((w, h), config)
+    frame = DeviceFrame(scene, config, net, max_points=len(px_all))
+    try:
+        _torch().cuda.current_stream().synchronize()
+        geo_direct_s = time.time() - t0
+        snaps = sorted(set(snapshots)) if snapshots else []
+        snap_images = {}
+        passes = []
+        done, k, r = 0, 0, None
+        while done < budget:
+            plan = plan_pass((w, h), k, config.r0, jitter_seed=config.seed)
+            tp = time.time()
+            base = ENTRY_KEY_BASE + plan.pass_index * w * h * 4
+            seg = ([], [], [])
+            executed = 0
+            for t in range(plan.task_count):
+                if done >= budget:
+                    break
+                xs, ys = plan.task_points(t)
+                gx, gy = np.meshgrid(xs, ys)
+                gx, gy = gx.ravel(), gy.ravel()
+                seg[0].append(gx)
+                seg[1].append(gy)
+                seg[2].append((base + gy * w + gx).astype(np.uint64))
+                done += 1
+                executed += 1
+                if done in snaps:
+                    frame.add_points(*(np.concatenate(a) for a in seg))
+                    seg = ([], [], [])
+                    snap_images[done] = frame.composite(plan.r).double().cpu().numpy()
+            if seg[0]:
+                frame.add_points(*(np.concatenate(a) for a in seg))
+            r = plan.r
+            info = frame.info()  # synchronises: the pass is finished
+            passes.append({"index": k, "r": plan.r, "tasks": executed, "entries": info["entries"],
+                           "seconds": time.time() - tp})
+            k += 1
+            if interrupt is not None and interrupt():
+                break  # this pass is finalised: composite below
+        image = frame.composite(r or 1).double().cpu().numpy()
+        info = frame.info()
+        pool = frame.entries() if frame.max_points else [np.zeros(0, np.int64)] * 2 + \
+            [np.zeros((0, 3))] * 4
+    finally:
+        frame.close()
+    tel = {"mode": "drc", "direct_spp": config.direct_spp,
+           "geometry_seconds": geo_direct_s, "direct_seconds": 0.0,
+           "passes": passes, "nonfinite": info["nonfinite"], "entries": info["entries"],
+           "fallback_pixels": 0, "tasks": done, "seconds": time.time() - t0}
+    if snap_images:
+        tel["snapshots"] = snap_images
+    tel["state"] = FrameState(info["entries"], info["points"], pool)
     return image, tel
 
 

@@ -230,6 +230,33 @@ def glass_fixtures():
          **{f"chain_{k}": np.asarray(v) for k, v in ch.items()}, L=L, L_direct=Ld)
 
 
+def progressive_fixture():
+    """The progressive control plane of render_drc (cache.py:426-469): per-pass
+    telemetry (index, r, tasks, cumulative entries), mid-run snapshots at task
+    budgets, and an interrupt that fires at its second poll (after pass 1),
+    against which libdrcb's host pass loop is checked."""
+    doc = scenegen.scene_doc(scenegen.build_scene("c1", resolution=(40, 40)))
+    scene = parse_scene(json.dumps(doc))
+    net = rcnn.random_network(8, 2)
+    kw = dict(direct_spp=1, mis_samples=8, seed=3, threads=1)
+    img, tel = render_drc(scene, RenderConfig(passes=3, **kw), net, snapshots=[2, 5, 9])
+    polls = []
+
+    def interrupt():
+        polls.append(1)
+        return len(polls) >= 2
+
+    img_i, tel_i = render_drc(scene, RenderConfig(passes=3, **kw), net, interrupt=interrupt)
+    pas = np.array([[p["index"], p["r"], p["tasks"], p["entries"]] for p in tel["passes"]])
+    pas_i = np.array([[p["index"], p["r"], p["tasks"], p["entries"]] for p in tel_i["passes"]])
+    snaps = tel["snapshots"]
+    save("drc_progressive.npz", doc=doc_array(doc), cfg=doc_array(dict(passes=3, direct_spp=1,
+                                                                        mis_samples=8, seed=3)),
+         k=8, seed_w=2, image=img, passes=pas, tasks=tel["tasks"], entries=tel["entries"],
+         snap_budgets=np.array(sorted(snaps)), snaps=np.stack([snaps[b] for b in sorted(snaps)]),
+         image_interrupted=img_i, passes_interrupted=pas_i, tasks_interrupted=tel_i["tasks"])
+
+
 def main():
     geometry_fixture()
     trace_fixture()
@@ -251,11 +278,15 @@ def main():
     frame_fixture("frame_furnace.npz", env, 8, 1, dict(direct_spp=2, indirect_tasks=1, mis_samples=8))
 
 
-if __name__ == "__main__" and not ({"--train", "--pt", "--data", "--drcc", "--glass"} & set(sys.argv)):
+if __name__ == "__main__" and not ({"--train", "--pt", "--data", "--drcc", "--glass", "--progressive"}
+                                   & set(sys.argv)):
     main()
     glass_fixtures()
+    progressive_fixture()
 if __name__ == "__main__" and "--glass" in sys.argv:
     glass_fixtures()
+if __name__ == "__main__" and "--progressive" in sys.argv:
+    progressive_fixture()
 
 
 def train_fixture():
