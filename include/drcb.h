@@ -262,6 +262,13 @@ int drcb_net_forward(const DrcbNet *net, const float *x, float *y, int64_t n,
 int drcb_debug_conv(int32_t mode, int32_t cin, int32_t cout, int32_t hw, int64_t n,
                     const float *x, const float *w, float *y);
 
+/* weight gradient of one 3x3 layer on the tensor cores (the training step's
+ * wgrad), HOST arrays (unit-test harness): x (n,hw,hw,cin) NHWC, dz
+ * (n,hw,hw,cout) NHWC, both rounded to bf16; dw (cout,cin,3,3) fp32 with
+ * dw[co][ci][ky][kx] = sum_p dz[p][co] * x[p + (ky-1, kx-1)][ci]. */
+int drcb_debug_wgrad(int32_t cin, int32_t cout, int32_t hw, int64_t n, const float *x,
+                     const float *dz, float *dw);
+
 /* traversal counters for roofline accounting: buf = device u64[12]
  * {inner nodes visited, primitives tested, casts, max nodes, max prims,
  * prims-tested histogram [5], sum of converged lanes at cast entry, any-hit

@@ -109,6 +109,7 @@ _SIGS = [
     ("drcb_trav_stats", C.c_int, [vp]),
     ("drcb_debug_conv", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, vp, vp,
                                   vp]),
+    ("drcb_debug_wgrad", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int64, vp, vp, vp]),
     ("drcb_trainer_create", C.c_int, [C.c_char_p, C.c_size_t, C.c_float, C.c_float, C.c_float,
                                       C.c_float, C.POINTER(vp)]),
     ("drcb_trainer_destroy", None, [vp]),

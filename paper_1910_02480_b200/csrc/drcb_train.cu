@@ -11,17 +11,9 @@
 #include <string>
 #include <vector>
 
-#include <cublas_v2.h>
-#include <cuda_bf16.h>
-#include <dlfcn.h>
-
-#include "drcb_net.h"
+#include "drcb_train.h"
 
 namespace drcb {
-
-int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int cin_pad, void* out,
-                 int out_ctot, int out_coff, const void* wpacked, int cout_pad, const float* ep_a,
-                 const float* ep_b, float slope, cudaStream_t st);
 
 int conv_f32(const ConvLayer& L, const float* in, int cin_tot, int cin_off, float* out,
              int cout_tot, int cout_off, int64_t n, float slope, cudaStream_t st);
@@ -31,19 +23,6 @@ int upsample_f32(const float* in, int c, int hw_in, float* out, int c_tot, int64
                  cudaStream_t st);
 
 namespace train {
-
-constexpr int NL = 17;  // 16 conv/deconv + BN layers and head.conv_out
-constexpr float MOMENTUM = 0.1f;
-constexpr float EPS = 1e-5f;
-
-struct TL {
-  std::string name, bn;
-  int cin, cout, hw, ks;
-  bool deconv, has_bn;
-  int64_t w, b, g, be;  // offsets in the flat parameter buffer
-  int64_t rm, rv;       // offsets in the running-stats buffer
-  int64_t nw;           // weight element count
-};
 
 __global__ void k_fill(float* p, int64_t n, float v) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -71,9 +50,24 @@ __global__ void k_wforms(const float* __restrict__ w, int cin, int cout, int ks,
   wt[((int64_t(ci) * cout + co) * ks + (ks - 1 - ky)) * ks + (ks - 1 - kx)] = v;
 }
 
-// per-channel sum / sum of squares (double accumulation) of an NCHW slice
+// Deterministic reductions: every block writes its partial sums to its own
+// slot (part[(slot * gridDim.x + block) ...]); k_reduce_partials adds a
+// slot's partials in block order. No floating-point atomics anywhere, so a
+// step is bit-reproducible run to run (the reference's determinism, SURVEY
+// §8(b)).
+__global__ void k_reduce_partials(const double* __restrict__ part, int nparts, int nslots,
+                                  double* __restrict__ out) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslots) return;
+  double a = 0.0;
+  for (int b = 0; b < nparts; ++b) a += part[int64_t(s) * nparts + b];
+  out[s] = a;
+}
+
+// per-channel sum / sum of squares (double accumulation) of an NCHW slice:
+// partial slots (2c, 2c+1) of block blockIdx.x
 __global__ void k_chan_stats(const float* __restrict__ x, int c_tot, int c_off, int hw2, int64_t n,
-                             double* acc) {
+                             double* part) {
   int c = blockIdx.y;
   int64_t total = n * hw2;
   double s = 0, ss = 0;
@@ -101,8 +95,8 @@ __global__ void k_chan_stats(const float* __restrict__ x, int c_tot, int c_off, 
       s += red[0][k];
       ss += red[1][k];
     }
-    atomicAdd(acc + 2 * c, s);
-    atomicAdd(acc + 2 * c + 1, ss);
+    part[int64_t(2 * c) * gridDim.x + blockIdx.x] = s;
+    part[int64_t(2 * c + 1) * gridDim.x + blockIdx.x] = ss;
   }
 }
 
@@ -138,7 +132,7 @@ __global__ void k_bn_act(const float* __restrict__ z, int c, int hw2, int64_t n,
 
 // L1 loss (mean |pred - target|) and its gradient through the final ReLU
 __global__ void k_l1(const float* __restrict__ pred, const float* __restrict__ tgt, int64_t n,
-                     double* loss, float* __restrict__ dpre) {
+                     double* part, float* __restrict__ dpre) {
   double s = 0;
   float inv = 1.f / float(n);
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -149,7 +143,13 @@ __global__ void k_l1(const float* __restrict__ pred, const float* __restrict__ t
     dpre[i] = pred[i] > 0.f ? sg * inv : 0.f;
   }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(loss, s);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < int(blockDim.x / 32); ++k) s += red[k];
+    part[blockIdx.x] = s;
+  }
 }
 
 // LeakyReLU + BN backward, pass 1: per-channel sums of dyb and dyb * xhat
@@ -157,7 +157,7 @@ __global__ void k_bn_bwd_stats(const float* __restrict__ z, const float* __restr
                                int da_tot, int da_off, int c, int hw2, int64_t n,
                                const float* __restrict__ mean, const float* __restrict__ invstd,
                                const float* __restrict__ gamma, const float* __restrict__ beta,
-                               float slope, double* acc) {
+                               float slope, double* part) {
   int ch = blockIdx.y;
   int64_t total = n * hw2;
   double s = 0, sx = 0;
@@ -188,8 +188,8 @@ __global__ void k_bn_bwd_stats(const float* __restrict__ z, const float* __restr
       s += red[0][k];
       sx += red[1][k];
     }
-    atomicAdd(acc + 2 * ch, s);
-    atomicAdd(acc + 2 * ch + 1, sx);
+    part[int64_t(2 * ch) * gridDim.x + blockIdx.x] = s;
+    part[int64_t(2 * ch + 1) * gridDim.x + blockIdx.x] = sx;
   }
 }
 
@@ -392,88 +392,10 @@ __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float
 
 inline unsigned nb(int64_t n, int t = 256) { return unsigned((n + t - 1) / t); }
 
-// ---------------------------------------------------------------------------
-// bf16 tensor-core path (drcb_trainer_set_mode(T, 2)): the 3x3 convs of the
-// forward and the dgrad run on the sm_100a implicit-GEMM kernels
-// (tc_conv_bf16) over NHWC bf16 copies, the weight gradient is one GEMM over
-// all pixels (im2col bf16 x dz bf16 -> fp32, cuBLAS), everything else (batch
-// norm, LeakyReLU, pools, upsample, Adam, fp32 master weights) is unchanged.
-
-inline int pad64(int c) { return (c + 63) / 64 * 64; }
-
-// conv-form fp32 weights [cout][cin][9] -> packed bf16 [coutp][9 * cinp]
-__global__ void k_pack_w(const float* __restrict__ w, int cout, int cin, int cinp, int coutp,
-                         __nv_bfloat16* __restrict__ out) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t kt = int64_t(9) * cinp;
-  if (i >= int64_t(coutp) * kt) return;
-  const int co = int(i / kt), r = int(i % kt), tap = r / cinp, ci = r % cinp;
-  out[i] = __float2bfloat16_rn((co < cout && ci < cin) ? w[(int64_t(co) * cin + ci) * 9 + tap] : 0.f);
-}
-
-// padded epilogue vector: v[c] (or fill when v == NULL) for c < n, 0 beyond
-__global__ void k_pad_vec(const float* __restrict__ v, int n, int np, float fill, float* out) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < np) out[c] = c < n ? (v ? v[c] : fill) : 0.f;
-}
-
-
-
-// Tiled layout conversions (32 pixels x 64 channels per block through SMEM,
-// both sides coalesced). Pixels are flattened over (map, pixel); `pad` = 1
-// writes the (hw+2)^2 zero-bordered layout used by the weight-gradient GEMMs
-// (its border is cleared by the caller), `mbase` shifts by a margin.
-__global__ void __launch_bounds__(256) k_nchw2nhwc_t(const float* __restrict__ in, int ctot, int coff,
-                                                     int c, int hw, int64_t n, int cpad, int pad,
-                                                     int64_t mbase, __nv_bfloat16* __restrict__ out) {
-  __shared__ float tile[64][33];
-  const int hw2 = hw * hw;
-  const int64_t P0 = int64_t(blockIdx.x) * 32;
-  const int c0 = blockIdx.y * 64;
-  for (int k = 0; k < 8; ++k) {
-    const int idx = threadIdx.x + 256 * k, ch = idx >> 5, px = idx & 31;
-    const int64_t P = P0 + px, m = P / hw2;
-    const int p = int(P % hw2);
-    float v = 0.f;
-    if (m < n && c0 + ch < c) v = __ldg(in + (m * ctot + coff + c0 + ch) * hw2 + p);
-    tile[ch][px] = v;
-  }
-  __syncthreads();
-  const int px = threadIdx.x >> 3, piece = threadIdx.x & 7;
-  const int64_t P = P0 + px, m = P / hw2;
-  const int p = int(P % hw2);
-  __align__(16) __nv_bfloat16 v[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) v[j] = __float2bfloat16_rn(tile[piece * 8 + j][px]);
-  const int64_t q = pad ? mbase + (m * (hw + 2) + p / hw + 1) * (hw + 2) + p % hw + 1 : P;
-  *reinterpret_cast<uint4*>(out + q * cpad + c0 + piece * 8) = *reinterpret_cast<uint4*>(v);
-}
-
-__global__ void __launch_bounds__(256) k_nhwc2nchw_t(const __nv_bfloat16* __restrict__ in, int cpad,
-                                                     int c, int hw2, int64_t n,
-                                                     float* __restrict__ out, int ctot, int coff) {
-  __shared__ float tile[64][33];
-  const int64_t P0 = int64_t(blockIdx.x) * 32;
-  const int c0 = blockIdx.y * 64;
-  {
-    const int px = threadIdx.x >> 3, piece = threadIdx.x & 7;
-    const uint4 u = __ldg(reinterpret_cast<const uint4*>(in + (P0 + px) * cpad + c0 + piece * 8));
-    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) tile[piece * 8 + j][px] = __bfloat162float(b[j]);
-  }
-  __syncthreads();
-  for (int k = 0; k < 8; ++k) {
-    const int idx = threadIdx.x + 256 * k, ch = idx >> 5, px = idx & 31;
-    const int64_t P = P0 + px, m = P / hw2;
-    if (m < n && c0 + ch < c) out[(m * ctot + coff + c0 + ch) * hw2 + int(P % hw2)] = tile[ch][px];
-  }
-}
-
 // 1x1 conv weight gradient (head.conv_out): dW[co][ci] = sum_p dz x, grid
-// (chunks, cout * cin), double accumulation
-__global__ void k_wgrad1_acc(const float* __restrict__ dz, int cout, const float* __restrict__ in,
-                             int cin, int hw2, int64_t n, double* acc) {
+// (chunks, cout * cin), double accumulation, partial slot blockIdx.y
+__global__ void k_wgrad1_part(const float* __restrict__ dz, int cout, const float* __restrict__ in,
+                              int cin, int hw2, int64_t n, double* part) {
   const int co = blockIdx.y / cin, ci = blockIdx.y % cin;
   double s = 0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * hw2;
@@ -483,23 +405,17 @@ __global__ void k_wgrad1_acc(const float* __restrict__ dz, int cout, const float
     s += double(dz[(m * cout + co) * hw2 + p]) * in[(m * cin + ci) * hw2 + p];
   }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(acc + blockIdx.y, s);
-}
-
-
-// GEMM result C (col-major coutp x 9*cinp) -> conv-form gradient [co][ci][9]
-__global__ void k_wgrad_from_gemm(const float* __restrict__ C, int coutp, int cout, int cin,
-                                  int cinp, float* __restrict__ dwf) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= int64_t(cout) * cin * 9) return;
-  const int tap = int(i % 9);
-  const int ci = int((i / 9) % cin);
-  const int co = int(i / (int64_t(9) * cin));
-  dwf[i] = C[co + (int64_t(tap) * cinp + ci) * coutp];
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < int(blockDim.x / 32); ++k) s += red[k];
+    part[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = s;
+  }
 }
 
 // per-channel sum of an NCHW tensor (conv bias gradient), grid (chunks, c)
-__global__ void k_chan_sum_acc(const float* __restrict__ x, int c, int hw2, int64_t n, double* acc) {
+__global__ void k_chan_sum_part(const float* __restrict__ x, int c, int hw2, int64_t n, double* part) {
   const int ch = blockIdx.y;
   double s = 0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * hw2;
@@ -508,62 +424,22 @@ __global__ void k_chan_sum_acc(const float* __restrict__ x, int c, int hw2, int6
     s += x[(m * c + ch) * hw2 + int(i % hw2)];
   }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(acc + ch, s);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < int(blockDim.x / 32); ++k) s += red[k];
+    part[int64_t(ch) * gridDim.x + blockIdx.x] = s;
+  }
 }
 __global__ void k_acc_to_float(const double* acc, int c, float* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < c) out[i] = float(acc[i]);
 }
 
-// cuBLAS, opened at first use (shares the process's instance with torch)
-struct Blas {
-  void* h = nullptr;
-  cublasStatus_t (*create)(cublasHandle_t*) = nullptr;
-  cublasStatus_t (*set_stream)(cublasHandle_t, cudaStream_t) = nullptr;
-  cublasStatus_t (*gemm_ex)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int,
-                            const void*, const void*, cudaDataType, int, const void*, cudaDataType,
-                            int, const void*, void*, cudaDataType, int, cublasComputeType_t,
-                            cublasGemmAlgo_t) = nullptr;
-};
-
-Blas* blas() {
-  static Blas b;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    b.h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
-    if (b.h) {
-      b.create = reinterpret_cast<decltype(b.create)>(dlsym(b.h, "cublasCreate_v2"));
-      b.set_stream = reinterpret_cast<decltype(b.set_stream)>(dlsym(b.h, "cublasSetStream_v2"));
-      b.gemm_ex = reinterpret_cast<decltype(b.gemm_ex)>(dlsym(b.h, "cublasGemmEx"));
-    }
-  }
-  return (b.create && b.set_stream && b.gemm_ex) ? &b : nullptr;
-}
-
 }  // namespace train
 }  // namespace drcb
 
-struct DrcbTrainer {
-  int k = 0;
-  float slope = 0.01f;
-  uint32_t slope_bits = 0;
-  std::vector<drcb::train::TL> L;
-  int64_t n_params = 0, n_running = 0;
-  float *params = nullptr, *grads = nullptr, *m = nullptr, *v = nullptr, *running = nullptr;
-  float *wf = nullptr, *wt = nullptr;  // conv-form / dgrad-form weights (all layers)
-  std::vector<int64_t> wf_off;
-  float lr = 1e-4f, b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
-  int64_t step = 0;
-  void* comm = nullptr;  // ncclComm_t or NULL
-  int world = 1;
-  std::vector<void*> allocs;
-  // bf16 tensor-core path
-  int mode = 0;  // 0 = fp32 CUDA cores (parity), 2 = bf16 tensor cores
-  void* blas = nullptr;                     // cublasHandle_t
-  std::vector<__nv_bfloat16*> wpk_f, wpk_t;  // packed fwd / dgrad weights per layer
-  std::vector<float*> ep_one_f, ep_one_t, ep_b, ep_zero;
-};
 
 namespace drcb {
 namespace train {
@@ -610,10 +486,13 @@ struct Work {
   // gradients
   float *d0, *da1, *dp1, *d2, *da3, *dp2, *d4, *da5, *dp3, *d6, *d7, *d8, *d9, *d10, *d11, *d12,
       *d13, *d14, *d15, *dc1, *dc2, *dc3, *dpre, *dz, *dwf;
-  double* acc;
+  double* acc;   // reduced sums (2 x channels)
+  double* part;  // per-block partial sums (see k_reduce_partials)
   double* loss;
   void* base = nullptr;
 };
+
+constexpr int GX = 64;  // partial blocks of the per-channel reductions
 
 }  // namespace train
 }  // namespace drcb
@@ -645,7 +524,8 @@ int alloc_work(DrcbTrainer* T, int64_t n, Work& W, cudaStream_t st) {
   for (auto& r : req) per += (r.second + 63) / 64 * 64;
   int64_t maxw = 0;
   for (const auto& l : T->L) maxw = std::max(maxw, l.nw);
-  size_t bytes = per * n * 4 + size_t(maxw) * 4 + (16 * 2 * 1024 + 4096) * 8 + 1024 * 1024;
+  size_t bytes = per * n * 4 + size_t(maxw) * 4 + (16 * 2 * 1024 + 4096) * 8 + 1024 * 1024 +
+                 size_t(GX) * 2 * 1024 * 8 + 1024 * 8;
   DRCB_CUDA(cudaMallocAsync(&W.base, bytes, st));
   float* cur = static_cast<float*>(W.base);
   for (auto& r : req) {
@@ -665,6 +545,7 @@ int alloc_work(DrcbTrainer* T, int64_t n, Work& W, cudaStream_t st) {
   uintptr_t a = (reinterpret_cast<uintptr_t>(cur) + 7) & ~uintptr_t(7);
   W.acc = reinterpret_cast<double*>(a);
   W.loss = W.acc + 2 * 1024;
+  W.part = W.loss + 8;
 
   return 0;
 }
@@ -773,55 +654,20 @@ extern "C" int drcb_trainer_create(const void* drcw, size_t len, float lr, float
 }
 
 // Select the conv engine: 0 = fp32 CUDA cores (the parity engine, default),
-// 2 = bf16 tensor cores (forward + dgrad on the implicit-GEMM kernels,
-// weight gradient via one bf16 GEMM; fp32 master weights, batch norm,
-// activations and Adam unchanged).
+// 2 = the NHWC bf16 tensor-core engine (drcb_train_tc.cu: forward, dgrad and
+// wgrad on tcgen05, fp32 master weights, batch statistics and Adam).
 extern "C" int drcb_trainer_set_mode(DrcbTrainer* T, int32_t mode) {
   if (!T) return fail(DRCB_ECONTRACT, "drcb_trainer_set_mode: null trainer");
   if (mode != 0 && mode != 2) return fail(DRCB_ECONFIG, "trainer mode must be 0 (fp32) or 2 (bf16)");
-  if (mode == 2 && T->wpk_f.empty()) {
-    if (!blas()) return fail(DRCB_ECUDA, "libcublas.so.12 not available");
-    cublasHandle_t h = nullptr;
-    if (blas()->create(&h) != CUBLAS_STATUS_SUCCESS) return fail(DRCB_ECUDA, "cublasCreate failed");
-    T->blas = h;
-    size_t bytes = 0;
-    std::vector<size_t> off;
-    for (int l = 0; l < 16; ++l) {
-      const TL& t = T->L[l];
-      const size_t cinp = pad64(t.cin), coutp = pad64(t.cout);
-      const size_t sz[6] = {coutp * 9 * cinp * 2, cinp * 9 * coutp * 2, coutp * 4, cinp * 4,
-                            coutp * 4, cinp * 4};
-      for (size_t z : sz) {
-        off.push_back(bytes);
-        bytes += (z + 255) / 256 * 256;
-      }
-    }
-    void* base = nullptr;
-    if (cudaMalloc(&base, bytes) != cudaSuccess) return fail(DRCB_ECUDA, "cudaMalloc bf16 state");
-    T->allocs.push_back(base);
-    uint8_t* b = static_cast<uint8_t*>(base);
-    for (int l = 0; l < 16; ++l) {
-      const TL& t = T->L[l];
-      const int cinp = pad64(t.cin), coutp = pad64(t.cout);
-      T->wpk_f.push_back(reinterpret_cast<__nv_bfloat16*>(b + off[6 * l]));
-      T->wpk_t.push_back(reinterpret_cast<__nv_bfloat16*>(b + off[6 * l + 1]));
-      T->ep_one_f.push_back(reinterpret_cast<float*>(b + off[6 * l + 2]));
-      T->ep_one_t.push_back(reinterpret_cast<float*>(b + off[6 * l + 3]));
-      T->ep_b.push_back(reinterpret_cast<float*>(b + off[6 * l + 4]));
-      T->ep_zero.push_back(reinterpret_cast<float*>(b + off[6 * l + 5]));
-      k_pad_vec<<<nb(coutp), 256>>>(nullptr, t.cout, coutp, 1.f, T->ep_one_f[l]);
-      k_pad_vec<<<nb(cinp), 256>>>(nullptr, t.cin, cinp, 1.f, T->ep_one_t[l]);
-      k_pad_vec<<<nb(cinp), 256>>>(nullptr, 0, cinp, 0.f, T->ep_zero[l]);
-    }
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) return cuda_fail(e, "drcb_trainer_set_mode");
-  }
+  if (mode == 2 && T->k != 64)
+    return fail(DRCB_ECONFIG, "the tensor-core trainer is built for k = 64 (use mode 0 for other k)");
   T->mode = mode;
   return 0;
 }
 
 extern "C" void drcb_trainer_destroy(DrcbTrainer* T) {
   if (!T) return;
+  if (T->tc) tc_engine_destroy(T->tc);
   for (void* p : T->allocs) cudaFree(p);
   delete T;
 }
@@ -851,10 +697,10 @@ namespace {
 int bn_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& out, cudaStream_t st) {
   const TL& t = T->L[l];
   const int hw2 = t.hw * t.hw;
-  DRCB_CUDA(cudaMemsetAsync(W.acc, 0, sizeof(double) * 2 * t.cout, st));
-  dim3 g(std::min<int64_t>(64, nb(n * hw2)), t.cout);
-  k_chan_stats<<<g, 256, 0, st>>>(W.z[l], t.cout, 0, hw2, n, W.acc);
+  k_chan_stats<<<dim3(GX, t.cout), 256, 0, st>>>(W.z[l], t.cout, 0, hw2, n, W.part);
   TCHECK("k_chan_stats");
+  k_reduce_partials<<<nb(2 * t.cout), 256, 0, st>>>(W.part, GX, 2 * t.cout, W.acc);
+  TCHECK("k_reduce_partials");
   // SyncBN: batch statistics over all data-parallel ranks (NVLink all-reduce)
   int rc = allreduce_sum(T->comm, W.acc, size_t(2) * t.cout, 1, st);
   if (rc) return rc;
@@ -868,119 +714,12 @@ int bn_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& out, cudaS
   return 0;
 }
 
-// NCHW fp32 slice -> NHWC bf16 (np maps, cpad channels); pad = 1: the
-// zero-bordered (hw+2)^2 layout with `margin` zero pixels before the first map
-int to_nhwc(const View& in, int c, int hw, int64_t n, int64_t np, int cpad, int pad, int64_t margin,
-            __nv_bfloat16* out, cudaStream_t st) {
-  dim3 g(unsigned(np * hw * hw / 32), unsigned(cpad / 64));
-  k_nchw2nhwc_t<<<g, 256, 0, st>>>(in.p, in.ctot, in.coff, c, hw, n, cpad, pad, margin, out);
-  count_launch();
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : cuda_fail(e, "k_nchw2nhwc_t");
-}
-
-int to_nchw(const __nv_bfloat16* in, int cpad, int c, int hw, int64_t n, int64_t np, float* out,
-            int ctot, int coff, cudaStream_t st) {
-  dim3 g(unsigned(np * hw * hw / 32), unsigned(cpad / 64));
-  k_nhwc2nchw_t<<<g, 256, 0, st>>>(in, cpad, c, hw * hw, n, out, ctot, coff);
-  count_launch();
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : cuda_fail(e, "k_nhwc2nchw_t");
-}
-
-// bf16 tensor-core conv of layer l: in (NCHW fp32 slice) -> W.z[l] (NCHW fp32)
-int conv_tc_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, cudaStream_t st) {
-  const TL& t = T->L[l];
-  const int hw2 = t.hw * t.hw, cinp = pad64(t.cin), coutp = pad64(t.cout);
-  const int64_t np = (n + 7) / 8 * 8;
-  __nv_bfloat16 *xi = nullptr, *zo = nullptr;
-  DRCB_CUDA(cudaMallocAsync((void**)&xi, size_t(np) * hw2 * cinp * 2, st));
-  DRCB_CUDA(cudaMallocAsync((void**)&zo, size_t(np) * hw2 * coutp * 2, st));
-  int rc = to_nhwc(in, t.cin, t.hw, n, np, cinp, 0, 0, xi, st);
-  if (!rc)
-    rc = tc_conv_bf16(t.cin, t.cout, t.hw, np, xi, cinp, zo, coutp, 0, T->wpk_f[l], coutp,
-                      T->ep_one_f[l], T->ep_b[l], 1.0f, st);
-  if (!rc) rc = to_nchw(zo, coutp, t.cout, t.hw, n, np, W.z[l], t.cout, 0, st);
-  if (rc) return rc;
-  DRCB_CUDA(cudaFreeAsync(xi, st));
-  DRCB_CUDA(cudaFreeAsync(zo, st));
-  return 0;
-}
-
-// bf16 tensor-core backward of layer l's conv. dgrad: the transposed conv on
-// the tensor cores (W.dz -> din). Weight gradient without an im2col buffer:
-// with dz and x in the zero-bordered (hw+2)^2 layout, every tap is a constant
-// offset s = (ky-1)(hw+2) + (kx-1) in the flattened padded pixel index, so
-//   dW_tap[co][ci] = sum_q dz_pad[q][co] * x_pad[q + s][ci]
-// is one plain GEMM per tap over all padded pixels (dz is zero on the border,
-// so border rows add nothing and shifted rows never leave x's zero margins).
-int conv_tc_backward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, float* din,
-                     int din_ctot, cudaStream_t st) {
-  const TL& t = T->L[l];
-  const int hw = t.hw, hw2 = hw * hw, cinp = pad64(t.cin), coutp = pad64(t.cout);
-  const int64_t np = (n + 7) / 8 * 8;
-  const View dzv{W.dz, t.cout, 0};
-  int rc = 0;
-  if (din) {
-    __nv_bfloat16 *dzh = nullptr, *dih = nullptr;
-    DRCB_CUDA(cudaMallocAsync((void**)&dzh, size_t(np) * hw2 * coutp * 2, st));
-    DRCB_CUDA(cudaMallocAsync((void**)&dih, size_t(np) * hw2 * cinp * 2, st));
-    rc = to_nhwc(dzv, t.cout, hw, n, np, coutp, 0, 0, dzh, st);
-    if (!rc)
-      rc = tc_conv_bf16(t.cout, t.cin, hw, np, dzh, coutp, dih, cinp, 0, T->wpk_t[l], cinp,
-                        T->ep_one_t[l], T->ep_zero[l], 1.0f, st);
-    if (!rc) rc = to_nchw(dih, cinp, t.cin, hw, n, np, din, din_ctot, 0, st);
-    if (rc) return rc;
-    DRCB_CUDA(cudaFreeAsync(dzh, st));
-    DRCB_CUDA(cudaFreeAsync(dih, st));
-  }
-  const int wp = hw + 2;
-  const int64_t Q = np * wp * wp, margin = wp + 1;
-  __nv_bfloat16 *dzp = nullptr, *xp = nullptr;
-  float* C = nullptr;
-  DRCB_CUDA(cudaMallocAsync((void**)&dzp, size_t(Q) * coutp * 2, st));
-  DRCB_CUDA(cudaMallocAsync((void**)&xp, size_t(Q + 2 * margin) * cinp * 2, st));
-  DRCB_CUDA(cudaMallocAsync((void**)&C, size_t(9) * coutp * cinp * 4, st));
-  DRCB_CUDA(cudaMemsetAsync(dzp, 0, size_t(Q) * coutp * 2, st));
-  DRCB_CUDA(cudaMemsetAsync(xp, 0, size_t(Q + 2 * margin) * cinp * 2, st));
-  rc = to_nhwc(dzv, t.cout, hw, n, np, coutp, 1, 0, dzp, st);
-  if (!rc) rc = to_nhwc(in, t.cin, hw, n, np, cinp, 1, margin, xp, st);
-  if (rc) return rc;
-  Blas* B = blas();
-  if (!B) return fail(DRCB_ECUDA, "libcublas.so.12 not available");
-  cublasHandle_t h = static_cast<cublasHandle_t>(T->blas);
-  if (B->set_stream(h, st) != CUBLAS_STATUS_SUCCESS) return fail(DRCB_ECUDA, "cublasSetStream");
-  const float one = 1.f, zero = 0.f;
-  for (int tap = 0; tap < 9; ++tap) {
-    const int64_t shift = int64_t(tap / 3 - 1) * wp + (tap % 3 - 1);
-    // column-major: C_tap (coutp x cinp) = dz_pad (coutp x Q) * x_pad[+s]^T (Q x cinp)
-    cublasStatus_t bs = B->gemm_ex(h, CUBLAS_OP_N, CUBLAS_OP_T, coutp, cinp, int(Q), &one, dzp,
-                                   CUDA_R_16BF, coutp, xp + (margin + shift) * cinp, CUDA_R_16BF,
-                                   cinp, &zero, C + int64_t(tap) * coutp * cinp, CUDA_R_32F, coutp,
-                                   CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-    if (bs != CUBLAS_STATUS_SUCCESS) return fail(DRCB_ECUDA, "cublasGemmEx (wgrad) failed");
-    count_launch();
-  }
-  k_wgrad_from_gemm<<<nb(int64_t(t.cout) * t.cin * 9), 256, 0, st>>>(C, coutp, t.cout, t.cin, cinp,
-                                                                      W.dwf);
-  TCHECK("k_wgrad_from_gemm");
-  DRCB_CUDA(cudaFreeAsync(dzp, st));
-  DRCB_CUDA(cudaFreeAsync(xp, st));
-  DRCB_CUDA(cudaFreeAsync(C, st));
-  return 0;
-}
-
 // conv/deconv + train BN + LeakyReLU layer l: in -> out slice
 int layer_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, const View& out,
                   cudaStream_t st) {
-  int rc;
-  if (T->mode == 2) {
-    rc = conv_tc_forward(T, l, W, n, in, st);
-  } else {
-    ConvLayer L;
-    conv_layer_view(T, l, T->wf + T->wf_off[l], L);
-    rc = conv_f32(L, in.p, in.ctot, in.coff, W.z[l], T->L[l].cout, 0, n, T->slope, st);
-  }
+  ConvLayer L;
+  conv_layer_view(T, l, T->wf + T->wf_off[l], L);
+  int rc = conv_f32(L, in.p, in.ctot, in.coff, W.z[l], T->L[l].cout, 0, n, T->slope, st);
   if (rc) return rc;
   return bn_forward(T, l, W, n, out, st);
 }
@@ -991,12 +730,12 @@ int layer_backward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, co
                    float* din, int din_ctot, cudaStream_t st) {
   const TL& t = T->L[l];
   const int hw2 = t.hw * t.hw;
-  DRCB_CUDA(cudaMemsetAsync(W.acc, 0, sizeof(double) * 2 * t.cout, st));
-  dim3 g(std::min<int64_t>(64, nb(n * hw2)), t.cout);
-  k_bn_bwd_stats<<<g, 256, 0, st>>>(W.z[l], dout.p, dout.ctot, dout.coff, t.cout, hw2, n,
-                                     W.mean[l], W.invstd[l], T->params + t.g, T->params + t.be,
-                                     T->slope, W.acc);
+  k_bn_bwd_stats<<<dim3(GX, t.cout), 256, 0, st>>>(W.z[l], dout.p, dout.ctot, dout.coff, t.cout, hw2,
+                                                  n, W.mean[l], W.invstd[l], T->params + t.g,
+                                                  T->params + t.be, T->slope, W.part);
   TCHECK("k_bn_bwd_stats");
+  k_reduce_partials<<<nb(2 * t.cout), 256, 0, st>>>(W.part, GX, 2 * t.cout, W.acc);
+  TCHECK("k_reduce_partials");
   // local gamma/beta gradients first (they join the gradient all-reduce)
   k_bn_param_grads<<<nb(t.cout), 256, 0, st>>>(W.acc, t.cout, T->grads + t.g, T->grads + t.be);
   TCHECK("k_bn_param_grads");
@@ -1011,52 +750,12 @@ int layer_backward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, co
                                                         T->slope, W.acc, double(n) * hw2 * T->world,
                                                         W.dz);
   TCHECK("k_bn_bwd_apply");
-  DRCB_CUDA(cudaMemsetAsync(W.acc, 0, sizeof(double) * t.cout, st));
-  k_chan_sum_acc<<<dim3(std::min<int64_t>(64, nb(n * hw2)), t.cout), 256, 0, st>>>(W.dz, t.cout,
-                                                                                  hw2, n, W.acc);
-  TCHECK("k_chan_sum_acc");
+  k_chan_sum_part<<<dim3(GX, t.cout), 256, 0, st>>>(W.dz, t.cout, hw2, n, W.part);
+  TCHECK("k_chan_sum_part");
+  k_reduce_partials<<<nb(t.cout), 256, 0, st>>>(W.part, GX, t.cout, W.acc);
+  TCHECK("k_reduce_partials");
   k_acc_to_float<<<nb(t.cout), 256, 0, st>>>(W.acc, t.cout, T->grads + t.b);
   TCHECK("k_acc_to_float");
-  if (T->mode == 2) {
-    int rc = conv_tc_backward(T, l, W, n, in, din, din_ctot, st);
-    if (rc) return rc;
-    if (getenv("DRCB_TRAIN_CHECK")) {
-      // self-check: the tensor-core dgrad / wgrad of this layer against the
-      // fp32 CUDA-core kernels on the SAME inputs (bf16 operand rounding:
-      // ~3e-3 relative L2); fails the step beyond 2e-2
-      std::vector<float> a(t.cout * t.cin * 9), b(t.cout * t.cin * 9);
-      cudaMemcpyAsync(a.data(), W.dwf, a.size() * 4, cudaMemcpyDeviceToHost, st);
-      k_wgrad<3><<<t.cout * t.cin, 256, 0, st>>>(W.dz, t.cout, in.p, in.ctot, in.coff, t.cin, t.hw, n,
-                                                  W.dwf);
-      cudaMemcpyAsync(b.data(), W.dwf, b.size() * 4, cudaMemcpyDeviceToHost, st);
-      double num = 0, den = 0;
-      if (din) {
-        int64_t nd = n * din_ctot * t.hw * t.hw;
-        std::vector<float> c(nd), d(nd);
-        cudaMemcpyAsync(c.data(), din, nd * 4, cudaMemcpyDeviceToHost, st);
-        ConvLayer D;
-        D.cin = t.cout; D.cout = t.cin; D.hw = t.hw; D.ksize = 3; D.act = false; D.mode = 0;
-        D.d_w = T->wt + T->wf_off[l]; D.d_bias = nullptr;
-        conv_f32(D, W.dz, t.cout, 0, din, din_ctot, 0, n, T->slope, st);
-        cudaMemcpyAsync(d.data(), din, nd * 4, cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        for (int64_t i = 0; i < nd; ++i) { num += (c[i]-d[i])*(c[i]-d[i]); den += d[i]*d[i]; }
-        cudaMemcpyAsync(din, c.data(), nd * 4, cudaMemcpyHostToDevice, st);
-        if (!(sqrt(num / (den + 1e-30)) <= 2e-2))
-          return fail(DRCB_ECUDA, "bf16 dgrad self-check failed at layer " + std::to_string(l));
-      }
-      cudaStreamSynchronize(st);
-      num = den = 0;
-      for (size_t i = 0; i < a.size(); ++i) { num += (a[i]-b[i])*(a[i]-b[i]); den += b[i]*b[i]; }
-      cudaMemcpyAsync(W.dwf, a.data(), a.size() * 4, cudaMemcpyHostToDevice, st);
-      cudaStreamSynchronize(st);
-      if (!(sqrt(num / (den + 1e-30)) <= 2e-2))
-        return fail(DRCB_ECUDA, "bf16 wgrad self-check failed at layer " + std::to_string(l));
-    }
-    k_wgrad_to_param<<<nb(t.nw), 256, 0, st>>>(W.dwf, t.cin, t.cout, 3, t.deconv, T->grads + t.w);
-    TCHECK("k_wgrad_to_param");
-    return 0;
-  }
   k_wgrad<3><<<t.cout * t.cin, 256, 0, st>>>(W.dz, t.cout, in.p, in.ctot, in.coff, t.cin, t.hw, n,
                                               W.dwf);
   TCHECK("k_wgrad");
@@ -1082,6 +781,22 @@ int layer_backward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, co
 
 extern "C" int drcb_trainer_apply(DrcbTrainer* T, float grad_scale, void* stream);
 
+namespace drcb {
+namespace train {
+// conv-form (forward) and transposed-flipped (dgrad) fp32 weights of every
+// layer from the master parameters
+int weight_forms(DrcbTrainer* T, cudaStream_t st) {
+  for (int l = 0; l < NL; ++l) {
+    const TL& t = T->L[l];
+    k_wforms<<<nb(t.nw), 256, 0, st>>>(T->params + t.w, t.cin, t.cout, t.ks, t.deconv,
+                                        T->wf + T->wf_off[l], T->wt + T->wf_off[l]);
+    TCHECK("k_wforms");
+  }
+  return 0;
+}
+}  // namespace train
+}  // namespace drcb
+
 // One optimisation step (train.py:97-103) on n examples: x (n,7,32,32),
 // y (n,3,32,32) device fp32. loss_host (optional) receives the batch L1 loss
 // (synchronises). apply_adam = 0 leaves parameters untouched (grads only).
@@ -1091,28 +806,28 @@ extern "C" int drcb_trainer_step(DrcbTrainer* T, const float* x, const float* y,
   if (n < 1) return fail(DRCB_ECONFIG, "training step needs n >= 1 examples");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   keep_pool_memory();
+  int rc = weight_forms(T, st);
+  if (rc) return rc;
+  const int64_t nout = n * 3 * 1024;
+  if (T->mode == 2) {
+    // the NHWC tensor-core engine: forward, loss and backward into T->grads
+    double* loss_dev = nullptr;
+    rc = tc_step(T, x, y, n, &loss_dev, st);
+    if (!rc) rc = allreduce_sum(T->comm, T->grads, size_t(T->n_params), 0, st);
+    if (!rc && apply_adam) rc = drcb_trainer_apply(T, 1.0f / float(T->world), stream);
+    if (rc) return rc;
+    if (loss_host) {
+      double loss = 0;
+      DRCB_CUDA(cudaMemcpyAsync(&loss, loss_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+      DRCB_CUDA(cudaStreamSynchronize(st));
+      *loss_host = loss / double(nout);
+    }
+    return 0;
+  }
   const int k = T->k;
   Work W;
-  int rc = alloc_work(T, n, W, st);
+  rc = alloc_work(T, n, W, st);
   if (rc) return rc;
-  // weight forms
-  for (int l = 0; l < NL; ++l) {
-    const TL& t = T->L[l];
-    k_wforms<<<nb(t.nw), 256, 0, st>>>(T->params + t.w, t.cin, t.cout, t.ks, t.deconv,
-                                        T->wf + T->wf_off[l], T->wt + T->wf_off[l]);
-    TCHECK("k_wforms");
-    if (T->mode == 2 && l < 16) {
-      const int cinp = pad64(t.cin), coutp = pad64(t.cout);
-      k_pack_w<<<nb(int64_t(coutp) * 9 * cinp), 256, 0, st>>>(T->wf + T->wf_off[l], t.cout, t.cin,
-                                                               cinp, coutp, T->wpk_f[l]);
-      TCHECK("k_pack_w");
-      k_pack_w<<<nb(int64_t(cinp) * 9 * coutp), 256, 0, st>>>(T->wt + T->wf_off[l], t.cin, t.cout,
-                                                               coutp, cinp, T->wpk_t[l]);
-      TCHECK("k_pack_w");
-      k_pad_vec<<<nb(coutp), 256, 0, st>>>(T->params + t.b, t.cout, coutp, 0.f, T->ep_b[l]);
-      TCHECK("k_pad_vec");
-    }
-  }
   float* xin = const_cast<float*>(x);
   // ---- forward (model.py:80-88)
   rc |= layer_forward(T, 0, W, n, {xin, 7, 0}, {W.a0, k, 0}, st);
@@ -1148,23 +863,22 @@ extern "C" int drcb_trainer_step(DrcbTrainer* T, const float* x, const float* y,
     return rc;
   }
   // ---- L1 loss (train.py:88) + gradient through the final ReLU
-  DRCB_CUDA(cudaMemsetAsync(W.loss, 0, sizeof(double), st));
-  const int64_t nout = n * 3 * 1024;
-  k_l1<<<std::min<int64_t>(1024, nb(nout)), 256, 0, st>>>(W.pred, y, nout, W.loss, W.dpre);
+  k_l1<<<1024, 256, 0, st>>>(W.pred, y, nout, W.part, W.dpre);
+  TCHECK("k_l1");
+  k_reduce_partials<<<1, 32, 0, st>>>(W.part, 1024, 1, W.loss);
   TCHECK("k_l1");
   // ---- backward
   {
     const TL& t = T->L[16];
     // conv_out: dW, db, d(a15)
-    DRCB_CUDA(cudaMemsetAsync(W.acc, 0, sizeof(double) * (3 + 3 * t.cin), st));
-    k_chan_sum_acc<<<dim3(std::min<int64_t>(64, nb(n * 1024)), 3), 256, 0, st>>>(W.dpre, 3, 1024, n,
-                                                                                 W.acc);
-    TCHECK("k_chan_sum_acc");
+    k_chan_sum_part<<<dim3(GX, 3), 256, 0, st>>>(W.dpre, 3, 1024, n, W.part);
+    TCHECK("k_chan_sum_part");
+    k_reduce_partials<<<1, 32, 0, st>>>(W.part, GX, 3, W.acc);
     k_acc_to_float<<<1, 32, 0, st>>>(W.acc, 3, T->grads + t.b);
     TCHECK("k_acc_to_float");
-    k_wgrad1_acc<<<dim3(std::min<int64_t>(32, nb(n * 1024)), 3 * t.cin), 256, 0, st>>>(
-        W.dpre, 3, W.a15, t.cin, 1024, n, W.acc + 3);
-    TCHECK("k_wgrad1_acc");
+    k_wgrad1_part<<<dim3(GX, 3 * t.cin), 256, 0, st>>>(W.dpre, 3, W.a15, t.cin, 1024, n, W.part);
+    TCHECK("k_wgrad1_part");
+    k_reduce_partials<<<nb(3 * t.cin), 256, 0, st>>>(W.part, GX, 3 * t.cin, W.acc + 3);
     k_acc_to_float<<<nb(3 * t.cin), 256, 0, st>>>(W.acc + 3, 3 * t.cin, W.dwf);
     TCHECK("k_acc_to_float");
     k_wgrad_to_param<<<nb(t.nw), 256, 0, st>>>(W.dwf, t.cin, 3, 1, 0, T->grads + t.w);

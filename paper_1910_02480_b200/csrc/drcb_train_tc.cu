@@ -1,0 +1,816 @@
+// drcb_train_tc.cu — the autoencoder's training step on the tensor cores,
+// NHWC bf16 end to end (trainer/src/drc_trainer/train.py:97-103 with
+// MapAutoencoder in train mode, model.py:20-88; BASELINE config 5: bf16
+// compute, fp32 master weights).
+//
+// Per 3x3 layer, forward: conv (tcgen05 implicit GEMM, epilogue = bias) ->
+// Z (bf16) -> batch statistics (deterministic per-block partials) -> BN +
+// LeakyReLU (+ the fused 2x2 max-pool of the encoder skips) straight into
+// the next layer's input buffer or the decoder's concat slice. Backward:
+// BN/LeakyReLU backward (two passes: per-channel sums, then dZ), dgrad
+// (tcgen05 transposed conv into the input-gradient buffer / concat slices),
+// wgrad (tcgen05 with MN-major operands read from the same NHWC tensors,
+// drcb_wgrad.cu), pool / upsample backward as NHWC gathers, the 1x1 head +
+// L1 loss fused in one kernel. Activations never leave NHWC bf16; every
+// buffer is allocated once per batch capacity (no per-step allocations); no
+// floating-point atomics (the step is bit-reproducible). The fp32 master
+// weights, gradients, running statistics and Adam live in drcb_train.cu.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "drcb_train.h"
+
+namespace drcb {
+
+int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int cin_pad, void* out,
+                 int out_ctot, int out_coff, const void* wpacked, int cout_pad, const float* ep_a,
+                 const float* ep_b, float slope, cudaStream_t st);
+int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, int cout_pad, int hw,
+               int64_t nmaps, float* dwf, void* ws, size_t* ws_bytes, cudaStream_t st);
+
+namespace train {
+
+using bf16 = __nv_bfloat16;
+
+inline int pad64(int c) { return (c + 63) / 64 * 64; }
+inline unsigned nbk(int64_t n, int t = 256) { return unsigned((n + t - 1) / t); }
+
+#define TC_CHECK(name)                                      \
+  do {                                                      \
+    count_launch();                                         \
+    cudaError_t _e = cudaGetLastError();                    \
+    if (_e != cudaSuccess) return cuda_fail(_e, name);      \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// 16-B vectors of 8 bf16 channels
+__device__ __forceinline__ void ld8(const bf16* p, float (&f)[8]) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 t = __bfloat1622float2(h[j]);
+    f[2 * j] = t.x;
+    f[2 * j + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void st8(bf16* p, const float (&f)[8]) {
+  uint4 u;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+    w[j] = *reinterpret_cast<uint32_t*>(&b);
+  }
+  *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ void round8(float (&f)[8]) {  // the stored (bf16) values
+#pragma unroll
+  for (int j = 0; j < 8; ++j) f[j] = __bfloat162float(__float2bfloat16_rn(f[j]));
+}
+
+// ---------------------------------------------------------------------------
+// input (n,7,32,32) fp32 NCHW -> X0 (np,32,32,64) bf16 NHWC: channels 0..6,
+// zeros in channel 7 and in the maps beyond n (channels 8..63 are zeroed once)
+__global__ void k_x_in(const float* __restrict__ x, int64_t n, int64_t np, bf16* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= np * 1024) return;
+  const int64_t m = i / 1024;
+  const int p = int(i % 1024);
+  float f[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) f[c] = (c < 7 && m < n) ? __ldg(x + (m * 7 + c) * 1024 + p) : 0.f;
+  st8(out + i * 64, f);
+}
+
+// conv-form fp32 weights [cout][cin][9] -> packed bf16 [coutp][9 * cinp]
+__global__ void k_pack_w(const float* __restrict__ w, int cout, int cin, int cinp, int coutp,
+                         bf16* __restrict__ out) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t kt = int64_t(9) * cinp;
+  if (i >= int64_t(coutp) * kt) return;
+  const int co = int(i / kt), r = int(i % kt), tap = r / cinp, ci = r % cinp;
+  out[i] = __float2bfloat16_rn((co < cout && ci < cin) ? w[(int64_t(co) * cin + ci) * 9 + tap] : 0.f);
+}
+
+// padded epilogue vector: v[c] (or fill when v == NULL) for c < n, 0 beyond
+__global__ void k_pad_vec(const float* __restrict__ v, int n, int np, float fill, float* out) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < np) out[c] = c < n ? (v ? v[c] : fill) : 0.f;
+}
+
+// Per-channel reductions over the first npx pixels of an NHWC tensor: block
+// (bx, channel tile of 64) covers pixels [bx*ppb, (bx+1)*ppb); thread = (8-ch
+// group, one of 32 pixel lanes); the 32 lanes' sums are combined in lane
+// order in double. Partial slot (q*cpad + c) of block bx at
+// part[(q*cpad + c)*gx + bx], q = 0..NQ-1.
+template <int NQ, class F>
+__device__ __forceinline__ void chan_reduce(int64_t npx, int64_t ppb, int cpad, double* part, F&& f) {
+  const int cg = threadIdx.x & 7, pl = threadIdx.x >> 3;
+  const int c0 = blockIdx.y * 64 + cg * 8;
+  float acc[NQ][8];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[q][j] = 0.f;
+  const int64_t p0 = int64_t(blockIdx.x) * ppb, p1 = min(npx, p0 + ppb);
+  for (int64_t p = p0 + pl; p < p1; p += 32) f(p, c0, acc);
+  __shared__ float red[NQ][32][65];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[q][pl][cg * 8 + j] = acc[q][j];
+  __syncthreads();
+  if (threadIdx.x < 64 * NQ) {
+    const int q = threadIdx.x / 64, c = threadIdx.x % 64;
+    double s = 0.0;
+    for (int l = 0; l < 32; ++l) s += double(red[q][l][c]);
+    part[(int64_t(q) * cpad + blockIdx.y * 64 + c) * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+__global__ void k_reduce_parts(const double* __restrict__ part, int nparts, int nslots,
+                               double* __restrict__ out) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslots) return;
+  double a = 0.0;
+  for (int b = 0; b < nparts; ++b) a += part[int64_t(s) * nparts + b];
+  out[s] = a;
+}
+
+// forward batch statistics: sum z, sum z^2 per channel
+__global__ void __launch_bounds__(256) k_bn_stats(const bf16* __restrict__ z, int cpad, int64_t npx,
+                                                  int64_t ppb, double* part) {
+  chan_reduce<2>(npx, ppb, cpad, part, [&](int64_t p, int c0, float (&acc)[2][8]) {
+    float v[8];
+    ld8(z + p * cpad + c0, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      acc[0][j] += v[j];
+      acc[1][j] = fmaf(v[j], v[j], acc[1][j]);
+    }
+  });
+}
+
+// BN finalize (torch BatchNorm2d train mode: biased variance normalises,
+// unbiased variance updates the running estimate, momentum 0.1):
+// y = z * s + t with s = gamma * invstd, t = beta - mean * s
+__global__ void k_bn_fin(const double* sums, int c, int cpad, double count, const float* gamma,
+                         const float* beta, float* rm, float* rv, float* bnv) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c) return;
+  double mu = sums[i] / count;
+  double var = sums[cpad + i] / count - mu * mu;
+  if (var < 0) var = 0;
+  const float invstd = float(1.0 / sqrt(var + double(EPS)));
+  const float s = gamma[i] * invstd;
+  bnv[i] = s;                           // scale
+  bnv[cpad + i] = beta[i] - float(mu) * s;  // shift
+  bnv[2 * cpad + i] = float(mu);        // mean
+  bnv[3 * cpad + i] = invstd;           // invstd
+  rm[i] = (1.f - MOMENTUM) * rm[i] + MOMENTUM * float(mu);
+  rv[i] = (1.f - MOMENTUM) * rv[i] + MOMENTUM * float(var * count / (count - 1.0));
+}
+
+// a = LeakyReLU(z * s + t) into out[.., c_off + c] (all np maps)
+__global__ void k_bn_apply(const bf16* __restrict__ z, int cpad, int64_t npx, const float* __restrict__ bnv,
+                           float slope, bf16* __restrict__ out, int c_tot, int c_off) {
+  const int g = cpad / 8;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= npx * g) return;
+  const int64_t p = i / g;
+  const int c0 = int(i % g) * 8;
+  float v[8];
+  ld8(z + p * cpad + c0, v);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float y = fmaf(v[j], bnv[c0 + j], bnv[cpad + c0 + j]);
+    v[j] = y >= 0.f ? y : slope * y;
+  }
+  st8(out + p * c_tot + c_off + c0, v);
+}
+
+// the same with the encoder's fused 2x2 max-pool (cnn.py:152-156) of the
+// stored values into pool (hw/2 maps, cpad channels)
+__global__ void k_bn_apply_pool(const bf16* __restrict__ z, int cpad, int hw, int64_t np,
+                                const float* __restrict__ bnv, float slope, bf16* __restrict__ out,
+                                int c_tot, int c_off, bf16* __restrict__ pool) {
+  const int g = cpad / 8, ho = hw / 2;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= np * ho * ho * g) return;
+  const int c0 = int(i % g) * 8;
+  const int64_t pp = i / g;
+  const int px = int(pp % ho), py = int((pp / ho) % ho);
+  const int64_t m = pp / (ho * ho);
+  float mx[8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t p = (m * hw + 2 * py + (k >> 1)) * hw + 2 * px + (k & 1);
+    float v[8];
+    ld8(z + p * cpad + c0, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float y = fmaf(v[j], bnv[c0 + j], bnv[cpad + c0 + j]);
+      v[j] = y >= 0.f ? y : slope * y;
+    }
+    round8(v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) mx[j] = k == 0 ? v[j] : fmaxf(mx[j], v[j]);
+    st8(out + p * c_tot + c_off + c0, v);
+  }
+  st8(pool + pp * cpad + c0, mx);
+}
+
+// bilinear 2x upsample (align_corners=False, cnn.py:159-174) of an NHWC map
+// into the leading channel slice of a concat buffer
+__device__ __forceinline__ void up_src(int o, int n, int& i0, int& i1, float& fr) {
+  const float s = fmaxf((o + 0.5f) * 0.5f - 0.5f, 0.f);
+  i0 = int(s);
+  i1 = min(i0 + 1, n - 1);
+  fr = s - float(i0);
+}
+__global__ void k_up_fwd(const bf16* __restrict__ in, int c, int hw_in, int64_t np, bf16* __restrict__ out,
+                         int c_tot) {
+  const int g = c / 8, ho = 2 * hw_in;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= np * ho * ho * g) return;
+  const int c0 = int(i % g) * 8;
+  const int64_t op = i / g;
+  const int ox = int(op % ho), oy = int((op / ho) % ho);
+  const int64_t m = op / (ho * ho);
+  int r0, r1, q0, q1;
+  float fr, fc;
+  up_src(oy, hw_in, r0, r1, fr);
+  up_src(ox, hw_in, q0, q1, fc);
+  const bf16* b = in + m * hw_in * hw_in * c + c0;
+  float a00[8], a01[8], a10[8], a11[8], v[8];
+  ld8(b + (r0 * hw_in + q0) * c, a00);
+  ld8(b + (r0 * hw_in + q1) * c, a01);
+  ld8(b + (r1 * hw_in + q0) * c, a10);
+  ld8(b + (r1 * hw_in + q1) * c, a11);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float t0 = a00[j] * (1.f - fr) + a10[j] * fr;
+    const float t1 = a01[j] * (1.f - fr) + a11[j] * fr;
+    v[j] = t0 * (1.f - fc) + t1 * fc;
+  }
+  st8(out + op * c_tot + c0, v);
+}
+
+// adjoint of the upsample: d_low[i] = sum over outputs of weight(o -> i) * d_high[o]
+__device__ __forceinline__ float up_wt(int o, int i, int n) {
+  int i0, i1;
+  float fr;
+  up_src(o, n, i0, i1, fr);
+  return (i0 == i ? 1.f - fr : 0.f) + (i1 == i ? fr : 0.f);
+}
+__global__ void k_up_bwd(const bf16* __restrict__ dhigh, int c_tot, int c, int hw_in, int64_t np,
+                         bf16* __restrict__ dlow) {
+  const int g = c / 8, ho = 2 * hw_in;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= np * hw_in * hw_in * g) return;
+  const int c0 = int(i % g) * 8;
+  const int64_t lp = i / g;
+  const int x = int(lp % hw_in), y = int((lp / hw_in) % hw_in);
+  const int64_t m = lp / (hw_in * hw_in);
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int oy = max(0, 2 * y - 2); oy <= min(ho - 1, 2 * y + 3); ++oy) {
+    const float wy = up_wt(oy, y, hw_in);
+    if (wy == 0.f) continue;
+    for (int ox = max(0, 2 * x - 2); ox <= min(ho - 1, 2 * x + 3); ++ox) {
+      const float wx = up_wt(ox, x, hw_in);
+      if (wx == 0.f) continue;
+      float d[8];
+      ld8(dhigh + ((m * ho + oy) * ho + ox) * c_tot + c0, d);
+      const float w = wy * wx;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s[j] = fmaf(w, d[j], s[j]);
+    }
+  }
+  st8(dlow + lp * c + c0, s);
+}
+
+// max-pool backward + the skip-connection gradient: ds = dskip + dp at the
+// window's first maximum in scan order (torch's tie rule)
+__global__ void k_pool_bwd(const bf16* __restrict__ a, int a_tot, int a_off, int c, int hw_out,
+                           int64_t np, const bf16* __restrict__ dp, const bf16* __restrict__ dskip,
+                           int ds_tot, int ds_off, bf16* __restrict__ ds) {
+  const int g = c / 8, hi = 2 * hw_out;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= np * hw_out * hw_out * g) return;
+  const int c0 = int(i % g) * 8;
+  const int64_t pp = i / g;
+  const int px = int(pp % hw_out), py = int((pp / hw_out) % hw_out);
+  const int64_t m = pp / (hw_out * hw_out);
+  float v[4][8], dpv[8];
+  int64_t q[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    q[k] = (m * hi + 2 * py + (k >> 1)) * hi + 2 * px + (k & 1);
+    ld8(a + q[k] * a_tot + a_off + c0, v[k]);
+  }
+  ld8(dp + pp * c + c0, dpv);
+  int best[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    best[j] = 0;
+#pragma unroll
+    for (int k = 1; k < 4; ++k)
+      if (v[k][j] > v[best[j]][j]) best[j] = k;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float d[8];
+    ld8(dskip + q[k] * ds_tot + ds_off + c0, d);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (best[j] == k) d[j] += dpv[j];
+    st8(ds + q[k] * c + c0, d);
+  }
+}
+
+// LeakyReLU + BN backward, pass 1: per-channel sums of dyb and dyb * xhat
+__global__ void __launch_bounds__(256) k_bnb_stats(const bf16* __restrict__ z, const bf16* __restrict__ da,
+                                                   int cpad, int64_t npx, int64_t ppb,
+                                                   const float* __restrict__ bnv, float slope,
+                                                   double* part) {
+  chan_reduce<2>(npx, ppb, cpad, part, [&](int64_t p, int c0, float (&acc)[2][8]) {
+    float zv[8], dv[8];
+    ld8(z + p * cpad + c0, zv);
+    ld8(da + p * cpad + c0, dv);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = c0 + j;
+      const float y = fmaf(zv[j], bnv[c], bnv[cpad + c]);
+      const float dyb = y > 0.f ? dv[j] : slope * dv[j];
+      const float xh = (zv[j] - bnv[2 * cpad + c]) * bnv[3 * cpad + c];
+      acc[0][j] += dyb;
+      acc[1][j] = fmaf(dyb, xh, acc[1][j]);
+    }
+  });
+}
+
+// bwd finalize: local gamma/beta gradients (before the SyncBN all-reduce)
+__global__ void k_bnb_param(const double* sums, int c, int cpad, float* dgamma, float* dbeta) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c) return;
+  dbeta[i] = float(sums[i]);
+  dgamma[i] = float(sums[cpad + i]);
+}
+// means of dyb and dyb * xhat over the (global) batch, and gamma * invstd
+__global__ void k_bnb_coef(const double* sums, int c, int cpad, double count, const float* gamma,
+                           float* bnv) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cpad) return;
+  const bool real = i < c;
+  bnv[4 * cpad + i] = real ? float(sums[i] / count) : 0.f;          // m1
+  bnv[5 * cpad + i] = real ? float(sums[cpad + i] / count) : 0.f;   // m2
+  bnv[6 * cpad + i] = real ? gamma[i] * bnv[3 * cpad + i] : 0.f;    // gamma * invstd
+}
+
+// pass 2: dz = gamma * invstd * (dyb - m1 - xhat * m2) (zero beyond n maps
+// and in padded channels), plus per-block partial sums of dz (bias gradient)
+__global__ void __launch_bounds__(256) k_bnb_apply(const bf16* __restrict__ z, const bf16* __restrict__ da,
+                                                   int cpad, int64_t npx_all, int64_t npx, int64_t ppb,
+                                                   const float* __restrict__ bnv, float slope,
+                                                   bf16* __restrict__ dz, double* part) {
+  chan_reduce<1>(npx_all, ppb, cpad, part, [&](int64_t p, int c0, float (&acc)[1][8]) {
+    float zv[8], dv[8], o[8];
+    ld8(z + p * cpad + c0, zv);
+    ld8(da + p * cpad + c0, dv);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = c0 + j;
+      const float y = fmaf(zv[j], bnv[c], bnv[cpad + c]);
+      const float dyb = y > 0.f ? dv[j] : slope * dv[j];
+      const float xh = (zv[j] - bnv[2 * cpad + c]) * bnv[3 * cpad + c];
+      const float g = p < npx ? bnv[6 * cpad + c] * (dyb - bnv[4 * cpad + c] - xh * bnv[5 * cpad + c]) : 0.f;
+      o[j] = g;
+      acc[0][j] += g;
+    }
+    st8(dz + p * cpad + c0, o);
+  });
+}
+
+// head: conv_out (1x1, 16 -> 3) + ReLU, L1 loss against y (n,3,32,32) fp32,
+// d(pred) = sign / n_out through the ReLU, d(a15) = W^T d(pred) and the
+// partials of loss (slot 0), d bias (1..3) and d W (4..51) per block
+constexpr int HEAD_SLOTS = 52;
+__global__ void __launch_bounds__(256) k_head(const bf16* __restrict__ a15, const float* __restrict__ w,
+                                              const float* __restrict__ b, const float* __restrict__ y,
+                                              int64_t n, int64_t np, double inv_n, bf16* __restrict__ da15,
+                                              double* part) {
+  float wl[48], bl[3];
+#pragma unroll
+  for (int i = 0; i < 48; ++i) wl[i] = w[i];
+#pragma unroll
+  for (int o = 0; o < 3; ++o) bl[o] = b[o];
+  double acc[HEAD_SLOTS];
+#pragma unroll
+  for (int s = 0; s < HEAD_SLOTS; ++s) acc[s] = 0.0;
+  const float ginv = float(inv_n);
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < np * 1024;
+       p += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t m = p / 1024;
+    const int px = int(p % 1024);
+    float a[16];
+    {
+      float t[8];
+      ld8(a15 + p * 64, t);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = t[j];
+      ld8(a15 + p * 64 + 8, t);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[8 + j] = t[j];
+    }
+    float gpre[3] = {0.f, 0.f, 0.f};
+    if (m < n) {
+#pragma unroll
+      for (int o = 0; o < 3; ++o) {
+        float s = bl[o];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) s = fmaf(wl[o * 16 + c], a[c], s);
+        const float pred = fmaxf(s, 0.f);
+        const float d = pred - y[(m * 3 + o) * 1024 + px];
+        acc[0] += fabs(double(d));
+        const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+        gpre[o] = pred > 0.f ? sg * ginv : 0.f;
+        acc[1 + o] += gpre[o];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc[4 + o * 16 + c] += double(gpre[o]) * a[c];
+      }
+    }
+    float da[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        da[j] = wl[h * 8 + j] * gpre[0] + wl[16 + h * 8 + j] * gpre[1] + wl[32 + h * 8 + j] * gpre[2];
+      st8(da15 + p * 64 + 8 * h, da);
+    }
+  }
+  // block reduction of the 52 slots in a fixed order
+  __shared__ double red[8][HEAD_SLOTS];
+  const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
+#pragma unroll
+  for (int s = 0; s < HEAD_SLOTS; ++s) {
+    double v = acc[s];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid][s] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < HEAD_SLOTS) {
+    double v = 0.0;
+    for (int k = 0; k < int(blockDim.x / 32); ++k) v += red[k][threadIdx.x];
+    part[int64_t(threadIdx.x) * gridDim.x + blockIdx.x] = v;
+  }
+}
+
+__global__ void k_sums_to_float(const double* sums, int c, float* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < c) out[i] = float(sums[i]);
+}
+
+__global__ void k_head_out(const double* sums, float* gw, float* gb, double* loss) {
+  const int i = threadIdx.x;
+  if (i == 0) *loss = sums[0];
+  if (i < 3) gb[i] = float(sums[1 + i]);
+  if (i < 48) gw[i] = float(sums[4 + i]);
+}
+
+// conv-form weight gradient -> parameter layout (deconv: back-transpose + flip)
+__global__ void k_wgrad_to_param(const float* __restrict__ dwf, int cin, int cout, int deconv,
+                                 float* __restrict__ g) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(cin) * cout * 9) return;
+  const int kx = int(i % 3), ky = int((i / 3) % 3);
+  const int64_t r = i / 9;
+  const int ci = int(r % cin), co = int(r / cin);
+  const float v = dwf[i];
+  if (deconv)
+    g[((int64_t(ci) * cout + co) * 3 + (2 - ky)) * 3 + (2 - kx)] = v;
+  else
+    g[i] = v;
+}
+
+// ---------------------------------------------------------------------------
+struct Buf {
+  bf16* p = nullptr;
+  int c = 0, hw = 0;
+};
+
+enum BufId {
+  X0, A0, C1, P1, A2, C2, P2, A4, C3, P3, A6, A7, A8, A9, A10, A11, A12, A13, A14, A15,
+  DZ, DA15, DA14, DA13, DA12, DC1, DA11, DA10, DC2, DA9, DA8, DC3, DA7, DA6, DP3, DS3, DA4, DP2,
+  DS2, DA2, DP1, DS1, DA0, NBUF
+};
+
+struct LayerPlan {
+  int in;           // input buffer
+  int out, off;     // BN output buffer and channel offset
+  int pool;         // fused-pool destination or -1
+  int up;           // upsample destination (concat buffer) after the layer, or -1
+  int dA;           // gradient of the layer output (BN backward input)
+  int din;          // dgrad destination or -1 (enc1.conv1)
+};
+
+struct TcEngine {
+  int64_t cap = 0;  // maps the buffers hold (a multiple of 8)
+  Buf B[NBUF];
+  bf16* Z[16] = {};
+  bf16 *wpf[16] = {}, *wpt[16] = {};
+  float *ep_one_f[16] = {}, *ep_b[16] = {}, *ep_one_t[16] = {}, *ep_zero[16] = {};
+  float* bnv[16] = {};  // per layer: s, t, mean, invstd, m1, m2, coef (7 x cout_pad)
+  float* dwf = nullptr;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  double *part = nullptr, *sums = nullptr, *loss = nullptr;
+  std::vector<void*> allocs;
+  ~TcEngine() {
+    for (void* p : allocs) cudaFree(p);
+  }
+};
+
+void tc_engine_destroy(TcEngine* e) { delete e; }
+
+const LayerPlan PLAN[16] = {
+    {X0, A0, 0, -1, -1, DA0, -1},      {A0, C1, 128, P1, -1, DS1, DA0},
+    {P1, A2, 0, -1, -1, DA2, DP1},     {A2, C2, 256, P2, -1, DS2, DA2},
+    {P2, A4, 0, -1, -1, DA4, DP2},     {A4, C3, 512, P3, -1, DS3, DA4},
+    {P3, A6, 0, -1, -1, DA6, DP3},     {A6, A7, 0, -1, C3, DA7, DA6},
+    {C3, A8, 0, -1, -1, DA8, DC3},     {A8, A9, 0, -1, C2, DA9, DA8},
+    {C2, A10, 0, -1, -1, DA10, DC2},   {A10, A11, 0, -1, C1, DA11, DA10},
+    {C1, A12, 0, -1, -1, DA12, DC1},   {A12, A13, 0, -1, -1, DA13, DA12},
+    {A13, A14, 0, -1, -1, DA14, DA13}, {A14, A15, 0, -1, -1, DA15, DA14},
+};
+
+int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
+  TcEngine* E = T->tc;
+  if (E && E->cap >= np) return 0;
+  if (E) {
+    DRCB_CUDA(cudaStreamSynchronize(st));
+    delete E;
+  }
+  E = T->tc = new TcEngine();
+  E->cap = np;
+  const int spec[NBUF][2] = {
+      {64, 32}, {64, 32}, {192, 32}, {64, 16}, {128, 16}, {384, 16}, {128, 8}, {256, 8}, {768, 8},
+      {256, 4}, {512, 4}, {512, 4}, {256, 8}, {256, 8}, {128, 16}, {128, 16}, {64, 32}, {64, 32},
+      {64, 32}, {64, 32},
+      {64, 32},  // DZ: the largest cout_pad * hw^2 (64 * 1024)
+      {64, 32}, {64, 32}, {64, 32}, {64, 32}, {192, 32}, {128, 16}, {128, 16}, {384, 16}, {256, 8},
+      {256, 8}, {768, 8}, {512, 4}, {512, 4}, {256, 4}, {256, 8}, {256, 8}, {128, 8}, {128, 16},
+      {128, 16}, {64, 16}, {64, 32}, {64, 32}};
+  size_t total = 0;
+  std::vector<size_t> off(NBUF + 16);
+  for (int i = 0; i < NBUF; ++i) {
+    off[i] = total;
+    total += (size_t(np) * spec[i][1] * spec[i][1] * spec[i][0] * 2 + 1023) & ~size_t(1023);
+  }
+  for (int l = 0; l < 16; ++l) {
+    const TL& t = T->L[l];
+    off[NBUF + l] = total;
+    total += (size_t(np) * t.hw * t.hw * pad64(t.cout) * 2 + 1023) & ~size_t(1023);
+  }
+  void* base = nullptr;
+  if (cudaMalloc(&base, total) != cudaSuccess) return fail(DRCB_ECUDA, "cudaMalloc tensor-core trainer activations");
+  E->allocs.push_back(base);
+  DRCB_CUDA(cudaMemsetAsync(base, 0, total, st));
+  uint8_t* b = static_cast<uint8_t*>(base);
+  for (int i = 0; i < NBUF; ++i) E->B[i] = Buf{reinterpret_cast<bf16*>(b + off[i]), spec[i][0], spec[i][1]};
+  for (int l = 0; l < 16; ++l) E->Z[l] = reinterpret_cast<bf16*>(b + off[NBUF + l]);
+  // weights, epilogue vectors, BN vectors
+  size_t wb = 0;
+  std::vector<size_t> wo;
+  for (int l = 0; l < 16; ++l) {
+    const TL& t = T->L[l];
+    const size_t cinp = pad64(t.cin), coutp = pad64(t.cout);
+    const size_t sz[7] = {coutp * 9 * cinp * 2, cinp * 9 * coutp * 2, coutp * 4, coutp * 4,
+                          cinp * 4, cinp * 4, 7 * coutp * 4};
+    for (size_t z : sz) {
+      wo.push_back(wb);
+      wb += (z + 255) & ~size_t(255);
+    }
+  }
+  // conv-form gradient scratch, wgrad split-K partials, reduction partials
+  int64_t maxw = 0;
+  size_t wsb = 0;
+  for (int l = 0; l < 16; ++l) {
+    const TL& t = T->L[l];
+    maxw = std::max<int64_t>(maxw, t.nw);
+    size_t q = 0;
+    int rc = wgrad_bf16(nullptr, t.cin, E->B[PLAN[l].in].c, nullptr, t.cout, pad64(t.cout), t.hw, np,
+                        nullptr, nullptr, &q, st);
+    if (rc) return rc;
+    wsb = std::max(wsb, q);
+  }
+  const size_t dwf_off = wb;
+  wb += (size_t(maxw) * 4 + 255) & ~size_t(255);
+  const size_t ws_off = wb;
+  wb += (wsb + 255) & ~size_t(255);
+  const size_t part_off = wb;
+  wb += size_t(256) * 2 * 1024 * 8 + size_t(1024) * HEAD_SLOTS * 8;
+  const size_t sums_off = wb;
+  wb += 2 * 1024 * 8 + 64 * 8;
+  void* wbase = nullptr;
+  if (cudaMalloc(&wbase, wb) != cudaSuccess) return fail(DRCB_ECUDA, "cudaMalloc tensor-core trainer state");
+  E->allocs.push_back(wbase);
+  DRCB_CUDA(cudaMemsetAsync(wbase, 0, wb, st));
+  uint8_t* w = static_cast<uint8_t*>(wbase);
+  for (int l = 0; l < 16; ++l) {
+    const TL& t = T->L[l];
+    E->wpf[l] = reinterpret_cast<bf16*>(w + wo[7 * l]);
+    E->wpt[l] = reinterpret_cast<bf16*>(w + wo[7 * l + 1]);
+    E->ep_one_f[l] = reinterpret_cast<float*>(w + wo[7 * l + 2]);
+    E->ep_b[l] = reinterpret_cast<float*>(w + wo[7 * l + 3]);
+    E->ep_one_t[l] = reinterpret_cast<float*>(w + wo[7 * l + 4]);
+    E->ep_zero[l] = reinterpret_cast<float*>(w + wo[7 * l + 5]);
+    E->bnv[l] = reinterpret_cast<float*>(w + wo[7 * l + 6]);
+    const int cinp = pad64(t.cin), coutp = pad64(t.cout);
+    k_pad_vec<<<nbk(coutp), 256, 0, st>>>(nullptr, t.cout, coutp, 1.f, E->ep_one_f[l]);
+    k_pad_vec<<<nbk(cinp), 256, 0, st>>>(nullptr, t.cin, cinp, 1.f, E->ep_one_t[l]);
+  }
+  E->dwf = reinterpret_cast<float*>(w + dwf_off);
+  E->ws = w + ws_off;
+  E->ws_bytes = wsb;
+  E->part = reinterpret_cast<double*>(w + part_off);
+  E->sums = reinterpret_cast<double*>(w + sums_off);
+  E->loss = E->sums + 2 * 1024;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : cuda_fail(e, "trainer engine setup");
+}
+
+// reduction geometry over npx pixels: pixels per block and blocks
+inline void red_geom(int64_t npx, int64_t& ppb, int& gx) {
+  ppb = std::max<int64_t>(1024, (npx + 255) / 256);
+  ppb = (ppb + 31) / 32 * 32;
+  gx = int((npx + ppb - 1) / ppb);
+}
+
+int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
+  TcEngine* E = T->tc;
+  const TL& t = T->L[l];
+  const LayerPlan& P = PLAN[l];
+  const int coutp = pad64(t.cout), hw2 = t.hw * t.hw;
+  const Buf& in = E->B[P.in];
+  int rc = tc_conv_bf16(t.cin, t.cout, t.hw, np, in.p, in.c, E->Z[l], coutp, 0, E->wpf[l], coutp,
+                        E->ep_one_f[l], E->ep_b[l], 1.0f, st);
+  if (rc) return rc;
+  int64_t ppb;
+  int gx;
+  red_geom(n * hw2, ppb, gx);
+  k_bn_stats<<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], coutp, n * hw2, ppb, E->part);
+  TC_CHECK("k_bn_stats");
+  k_reduce_parts<<<nbk(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
+  TC_CHECK("k_reduce_parts");
+  rc = allreduce_sum(T->comm, E->sums, size_t(2) * coutp, 1, st);  // SyncBN
+  if (rc) return rc;
+  k_bn_fin<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, coutp, double(n) * hw2 * T->world,
+                                         T->params + t.g, T->params + t.be, T->running + t.rm,
+                                         T->running + t.rv, E->bnv[l]);
+  TC_CHECK("k_bn_fin");
+  const Buf& out = E->B[P.out];
+  if (P.pool >= 0) {
+    const int64_t tot = np * (hw2 / 4) * (coutp / 8);
+    k_bn_apply_pool<<<nbk(tot), 256, 0, st>>>(E->Z[l], coutp, t.hw, np, E->bnv[l], T->slope, out.p,
+                                              out.c, P.off, E->B[P.pool].p);
+    TC_CHECK("k_bn_apply_pool");
+  } else {
+    const int64_t tot = np * hw2 * (coutp / 8);
+    k_bn_apply<<<nbk(tot), 256, 0, st>>>(E->Z[l], coutp, np * hw2, E->bnv[l], T->slope, out.p, out.c,
+                                         P.off);
+    TC_CHECK("k_bn_apply");
+  }
+  if (P.up >= 0) {
+    const Buf& cat = E->B[P.up];
+    const int64_t tot = np * 4 * hw2 * (coutp / 8);
+    k_up_fwd<<<nbk(tot), 256, 0, st>>>(out.p, coutp, t.hw, np, cat.p, cat.c);
+    TC_CHECK("k_up_fwd");
+  }
+  return 0;
+}
+
+int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
+  TcEngine* E = T->tc;
+  const TL& t = T->L[l];
+  const LayerPlan& P = PLAN[l];
+  const int coutp = pad64(t.cout), hw2 = t.hw * t.hw;
+  const bf16* da = E->B[P.dA].p;
+  int64_t ppb;
+  int gx;
+  red_geom(n * hw2, ppb, gx);
+  k_bnb_stats<<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], da, coutp, n * hw2, ppb, E->bnv[l],
+                                                    T->slope, E->part);
+  TC_CHECK("k_bnb_stats");
+  k_reduce_parts<<<nbk(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
+  TC_CHECK("k_reduce_parts");
+  k_bnb_param<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, coutp, T->grads + t.g, T->grads + t.be);
+  TC_CHECK("k_bnb_param");
+  int rc = allreduce_sum(T->comm, E->sums, size_t(2) * coutp, 1, st);  // SyncBN backward
+  if (rc) return rc;
+  k_bnb_coef<<<nbk(coutp), 256, 0, st>>>(E->sums, t.cout, coutp, double(n) * hw2 * T->world,
+                                          T->params + t.g, E->bnv[l]);
+  TC_CHECK("k_bnb_coef");
+  int64_t ppb2;
+  int gx2;
+  red_geom(np * hw2, ppb2, gx2);
+  bf16* dz = E->B[DZ].p;
+  k_bnb_apply<<<dim3(gx2, coutp / 64), 256, 0, st>>>(E->Z[l], da, coutp, np * hw2, n * hw2, ppb2,
+                                                     E->bnv[l], T->slope, dz, E->part);
+  TC_CHECK("k_bnb_apply");
+  k_reduce_parts<<<nbk(t.cout), 256, 0, st>>>(E->part, gx2, t.cout, E->sums);
+  TC_CHECK("k_reduce_parts");
+  k_sums_to_float<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, T->grads + t.b);  // conv bias
+  TC_CHECK("k_sums_to_float");
+  // dgrad: the transposed conv of dz into the input-gradient buffer
+  if (P.din >= 0) {
+    const Buf& din = E->B[P.din];
+    rc = tc_conv_bf16(t.cout, t.cin, t.hw, np, dz, coutp, din.p, din.c, 0, E->wpt[l], din.c,
+                      E->ep_one_t[l], E->ep_zero[l], 1.0f, st);
+    if (rc) return rc;
+  }
+  // wgrad from the layer input and dz (both NHWC, straight from the buffers)
+  const Buf& in = E->B[P.in];
+  size_t wsb = E->ws_bytes;
+  rc = wgrad_bf16(in.p, t.cin, in.c, dz, t.cout, coutp, t.hw, np, E->dwf, E->ws, &wsb, st);
+  if (rc) return rc;
+  k_wgrad_to_param<<<nbk(t.nw), 256, 0, st>>>(E->dwf, t.cin, t.cout, t.deconv ? 1 : 0, T->grads + t.w);
+  TC_CHECK("k_wgrad_to_param");
+  return 0;
+}
+
+int up_bwd(TcEngine* E, int dcat, int c, int hw_in, int dlow, int64_t np, cudaStream_t st) {
+  const int64_t tot = np * hw_in * hw_in * (c / 8);
+  k_up_bwd<<<nbk(tot), 256, 0, st>>>(E->B[dcat].p, E->B[dcat].c, c, hw_in, np, E->B[dlow].p);
+  TC_CHECK("k_up_bwd");
+  return 0;
+}
+
+int pool_bwd(TcEngine* E, int cat, int off, int c, int hw_out, int dp, int dcat, int ds, int64_t np,
+             cudaStream_t st) {
+  const int64_t tot = np * hw_out * hw_out * (c / 8);
+  k_pool_bwd<<<nbk(tot), 256, 0, st>>>(E->B[cat].p, E->B[cat].c, off, c, hw_out, np, E->B[dp].p,
+                                        E->B[dcat].p, E->B[dcat].c, off, E->B[ds].p);
+  TC_CHECK("k_pool_bwd");
+  return 0;
+}
+
+// One step's forward, L1 loss and backward (gradients of every parameter in
+// T->grads, local to this rank); *loss_dev receives the device sum |pred - y|.
+int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** loss_dev,
+            cudaStream_t st) {
+  if (T->k != 64) return fail(DRCB_ECONFIG, "the tensor-core trainer is built for k = 64");
+  const int64_t np = (n + 7) / 8 * 8;
+  int rc = engine_setup(T, np, st);
+  if (rc) return rc;
+  TcEngine* E = T->tc;
+  // packed bf16 operands of this step's weights (forward and dgrad forms)
+  for (int l = 0; l < 16; ++l) {
+    const TL& t = T->L[l];
+    const int cinp = pad64(t.cin), coutp = pad64(t.cout);
+    k_pack_w<<<nbk(int64_t(coutp) * 9 * cinp), 256, 0, st>>>(T->wf + T->wf_off[l], t.cout, t.cin,
+                                                              cinp, coutp, E->wpf[l]);
+    TC_CHECK("k_pack_w");
+    k_pack_w<<<nbk(int64_t(cinp) * 9 * coutp), 256, 0, st>>>(T->wt + T->wf_off[l], t.cin, t.cout,
+                                                              coutp, cinp, E->wpt[l]);
+    TC_CHECK("k_pack_w");
+    k_pad_vec<<<nbk(coutp), 256, 0, st>>>(T->params + t.b, t.cout, coutp, 0.f, E->ep_b[l]);
+    TC_CHECK("k_pad_vec");
+  }
+  k_x_in<<<nbk(np * 1024), 256, 0, st>>>(x, n, np, E->B[X0].p);
+  TC_CHECK("k_x_in");
+  // ---- forward (model.py:80-88)
+  for (int l = 0; l < 16 && !rc; ++l) rc = layer_fwd(T, l, n, np, st);
+  if (rc) return rc;
+  // ---- head.conv_out + ReLU + L1 loss (train.py:88) and its backward
+  {
+    const TL& t = T->L[16];
+    const int gx = 1024;
+    k_head<<<gx, 256, 0, st>>>(E->B[A15].p, T->params + t.w, T->params + t.b, y, n, np,
+                               1.0 / double(n * 3 * 1024), E->B[DA15].p, E->part);
+    TC_CHECK("k_head");
+    k_reduce_parts<<<1, 64, 0, st>>>(E->part, gx, HEAD_SLOTS, E->sums);
+    TC_CHECK("k_reduce_parts");
+    k_head_out<<<1, 64, 0, st>>>(E->sums, T->grads + t.w, T->grads + t.b, E->loss);
+    TC_CHECK("k_head_out");
+  }
+  // ---- backward
+  const int order[] = {15, 14, 13, 12, -1, 11, 10, -2, 9, 8, -3, 7, 6, -4, 5, 4, -5, 3, 2, -6, 1, 0};
+  for (int o : order) {
+    if (o >= 0) rc = layer_bwd(T, o, n, np, st);
+    else if (o == -1) rc = up_bwd(E, DC1, 128, 16, DA11, np, st);
+    else if (o == -2) rc = up_bwd(E, DC2, 256, 8, DA9, np, st);
+    else if (o == -3) rc = up_bwd(E, DC3, 512, 4, DA7, np, st);
+    else if (o == -4) rc = pool_bwd(E, C3, 512, 256, 4, DP3, DC3, DS3, np, st);
+    else if (o == -5) rc = pool_bwd(E, C2, 256, 128, 8, DP2, DC2, DS2, np, st);
+    else rc = pool_bwd(E, C1, 128, 64, 16, DP1, DC1, DS1, np, st);
+    if (rc) return rc;
+  }
+  *loss_dev = E->loss;
+  return 0;
+}
+
+}  // namespace train
+}  // namespace drcb

@@ -54,10 +54,11 @@ def param_layout(k):
 
 
 class DeviceTrainer:
-    """mode "fp32": CUDA-core engine (the parity engine); "bf16": the 3x3
-    convs' forward and dgrad on the tcgen05 implicit-GEMM kernels and the
-    weight gradient as one bf16 GEMM, with fp32 master weights, batch norm,
-    activations and Adam (BASELINE config 5: bf16 compute, fp32 master)."""
+    """mode "fp32": CUDA-core engine (the parity engine); "bf16": the NHWC
+    tensor-core engine (drcb_train_tc.cu: forward, dgrad and wgrad of every
+    3x3 layer on tcgen05, activations and gradients NHWC bf16, batch
+    statistics / Adam / master weights fp32; BASELINE config 5: bf16 compute,
+    fp32 master weights; k = 64)."""
 
     def __init__(self, net_or_drcw, lr=6e-5, betas=(0.9, 0.999), eps=1e-8, mode="fp32"):
         lib = _lib.load()
