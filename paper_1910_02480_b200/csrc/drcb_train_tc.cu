@@ -107,16 +107,21 @@ __global__ void k_pad_vec(const float* __restrict__ v, int n, int np, float fill
 // order in double. Partial slot (q*cpad + c) of block bx at
 // part[(q*cpad + c)*gx + bx], q = 0..NQ-1.
 template <int NQ, class F>
-__device__ __forceinline__ void chan_reduce(int64_t npx, int64_t ppb, int cpad, double* part, F&& f) {
+__device__ __forceinline__ void chan_reduce(int64_t npx, int64_t ppb, int cpad, double* part, F f) {
   const int cg = threadIdx.x & 7, pl = threadIdx.x >> 3;
   const int c0 = blockIdx.y * 64 + cg * 8;
+  f.init(c0);  // this thread's 8 channels are fixed: per-channel constants once
   float acc[NQ][8];
 #pragma unroll
   for (int q = 0; q < NQ; ++q)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[q][j] = 0.f;
   const int64_t p0 = int64_t(blockIdx.x) * ppb, p1 = min(npx, p0 + ppb);
-  for (int64_t p = p0 + pl; p < p1; p += 32) f(p, c0, acc);
+  // four pixels per lane in flight (the loads of one iteration are issued
+  // before their arithmetic: enough bytes in flight per SM for HBM rate)
+  int64_t p = p0 + pl;
+  for (; p + 96 < p1; p += 128) f.template go<4>(p, c0, acc);
+  for (; p < p1; p += 32) f.template go<1>(p, c0, acc);
   __shared__ float red[NQ][32][65];
 #pragma unroll
   for (int q = 0; q < NQ; ++q)
@@ -131,27 +136,41 @@ __device__ __forceinline__ void chan_reduce(int64_t npx, int64_t ppb, int cpad, 
   }
 }
 
+// one warp per slot: lane l adds parts l, l+32, ... in order, then a fixed
+// butterfly combines the lanes (deterministic)
 __global__ void k_reduce_parts(const double* __restrict__ part, int nparts, int nslots,
                                double* __restrict__ out) {
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   if (s >= nslots) return;
   double a = 0.0;
-  for (int b = 0; b < nparts; ++b) a += part[int64_t(s) * nparts + b];
-  out[s] = a;
+  for (int b = lane; b < nparts; b += 32) a += part[int64_t(s) * nparts + b];
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if (lane == 0) out[s] = a;
 }
+inline unsigned nb_slots(int nslots) { return unsigned((int64_t(nslots) * 32 + 255) / 256); }
 
 // forward batch statistics: sum z, sum z^2 per channel
+struct StatsF {
+  const bf16* z;
+  int cpad;
+  __device__ __forceinline__ void init(int) {}
+  template <int U>
+  __device__ __forceinline__ void go(int64_t p, int c0, float (&acc)[2][8]) const {
+    float v[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) ld8(z + (p + 32 * u) * cpad + c0, v[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        acc[0][j] += v[u][j];
+        acc[1][j] = fmaf(v[u][j], v[u][j], acc[1][j]);
+      }
+  }
+};
 __global__ void __launch_bounds__(256) k_bn_stats(const bf16* __restrict__ z, int cpad, int64_t npx,
                                                   int64_t ppb, double* part) {
-  chan_reduce<2>(npx, ppb, cpad, part, [&](int64_t p, int c0, float (&acc)[2][8]) {
-    float v[8];
-    ld8(z + p * cpad + c0, v);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      acc[0][j] += v[j];
-      acc[1][j] = fmaf(v[j], v[j], acc[1][j]);
-    }
-  });
+  chan_reduce<2>(npx, ppb, cpad, part, StatsF{z, cpad});
 }
 
 // BN finalize (torch BatchNorm2d train mode: biased variance normalises,
@@ -174,45 +193,63 @@ __global__ void k_bn_fin(const double* sums, int c, int cpad, double count, cons
   rv[i] = (1.f - MOMENTUM) * rv[i] + MOMENTUM * float(var * count / (count - 1.0));
 }
 
+// Elementwise NHWC kernels: one thread per (pixel, 8-channel group); every
+// extent is a power of two (lg* = log2) except the concat buffers' channel
+// totals, which only multiply: 32-bit shift / mask indexing (no 64-bit
+// division in the address math).
+__device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
+
 // a = LeakyReLU(z * s + t) into out[.., c_off + c] (all np maps)
-__global__ void k_bn_apply(const bf16* __restrict__ z, int cpad, int64_t npx, const float* __restrict__ bnv,
-                           float slope, bf16* __restrict__ out, int c_tot, int c_off) {
-  const int g = cpad / 8;
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= npx * g) return;
-  const int64_t p = i / g;
-  const int c0 = int(i % g) * 8;
+__global__ void __launch_bounds__(256) k_bn_apply(const bf16* __restrict__ z, int cpad, int npx,
+                                                  const float* __restrict__ bnv, float slope,
+                                                  bf16* __restrict__ out, int c_tot, int c_off) {
+  const int lg = ilog2(cpad / 8);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (npx << lg)) return;
+  const int p = i >> lg, c0 = (i & ((1 << lg) - 1)) * 8;
   float v[8];
-  ld8(z + p * cpad + c0, v);
+  ld8(z + int64_t(p) * cpad + c0, v);
+  const float4 s0 = __ldg(reinterpret_cast<const float4*>(bnv + c0));
+  const float4 s1 = __ldg(reinterpret_cast<const float4*>(bnv + c0 + 4));
+  const float4 t0 = __ldg(reinterpret_cast<const float4*>(bnv + cpad + c0));
+  const float4 t1 = __ldg(reinterpret_cast<const float4*>(bnv + cpad + c0 + 4));
+  const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+  const float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const float y = fmaf(v[j], bnv[c0 + j], bnv[cpad + c0 + j]);
+    const float y = fmaf(v[j], sv[j], tv[j]);
     v[j] = y >= 0.f ? y : slope * y;
   }
-  st8(out + p * c_tot + c_off + c0, v);
+  st8(out + int64_t(p) * c_tot + c_off + c0, v);
 }
 
 // the same with the encoder's fused 2x2 max-pool (cnn.py:152-156) of the
 // stored values into pool (hw/2 maps, cpad channels)
-__global__ void k_bn_apply_pool(const bf16* __restrict__ z, int cpad, int hw, int64_t np,
-                                const float* __restrict__ bnv, float slope, bf16* __restrict__ out,
-                                int c_tot, int c_off, bf16* __restrict__ pool) {
-  const int g = cpad / 8, ho = hw / 2;
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= np * ho * ho * g) return;
-  const int c0 = int(i % g) * 8;
-  const int64_t pp = i / g;
-  const int px = int(pp % ho), py = int((pp / ho) % ho);
-  const int64_t m = pp / (ho * ho);
+__global__ void __launch_bounds__(256) k_bn_apply_pool(const bf16* __restrict__ z, int cpad, int hw, int np,
+                                                       const float* __restrict__ bnv, float slope,
+                                                       bf16* __restrict__ out, int c_tot, int c_off,
+                                                       bf16* __restrict__ pool) {
+  const int lg = ilog2(cpad / 8), lho = ilog2(hw / 2), hw_ = hw;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (np << (2 * lho + lg))) return;
+  const int c0 = (i & ((1 << lg) - 1)) * 8;
+  const int pp = i >> lg;
+  const int px = pp & ((1 << lho) - 1), py = (pp >> lho) & ((1 << lho) - 1), m = pp >> (2 * lho);
+  float sv[8], tv[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sv[j] = __ldg(bnv + c0 + j);
+    tv[j] = __ldg(bnv + cpad + c0 + j);
+  }
   float mx[8];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const int64_t p = (m * hw + 2 * py + (k >> 1)) * hw + 2 * px + (k & 1);
+    const int64_t p = (int64_t(m) * hw_ + 2 * py + (k >> 1)) * hw_ + 2 * px + (k & 1);
     float v[8];
     ld8(z + p * cpad + c0, v);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float y = fmaf(v[j], bnv[c0 + j], bnv[cpad + c0 + j]);
+      const float y = fmaf(v[j], sv[j], tv[j]);
       v[j] = y >= 0.f ? y : slope * y;
     }
     round8(v);
@@ -220,31 +257,40 @@ __global__ void k_bn_apply_pool(const bf16* __restrict__ z, int cpad, int hw, in
     for (int j = 0; j < 8; ++j) mx[j] = k == 0 ? v[j] : fmaxf(mx[j], v[j]);
     st8(out + p * c_tot + c_off + c0, v);
   }
-  st8(pool + pp * cpad + c0, mx);
+  st8(pool + int64_t(pp) * cpad + c0, mx);
 }
 
-// bilinear 2x upsample (align_corners=False, cnn.py:159-174) of an NHWC map
-// into the leading channel slice of a concat buffer
+// bilinear 2x upsample (align_corners=False, cnn.py:159-174): output index o
+// reads low-res i0 = (o-1)/2, i1 = i0 + 1 (clamped) with weight 0.25 / 0.75
+// (the closed form of src = max((o + 0.5)/2 - 0.5, 0))
 __device__ __forceinline__ void up_src(int o, int n, int& i0, int& i1, float& fr) {
-  const float s = fmaxf((o + 0.5f) * 0.5f - 0.5f, 0.f);
-  i0 = int(s);
-  i1 = min(i0 + 1, n - 1);
-  fr = s - float(i0);
+  if (o == 0) {
+    i0 = 0;
+    i1 = min(1, n - 1);
+    fr = 0.f;
+  } else if (o & 1) {
+    i0 = o >> 1;
+    i1 = min(i0 + 1, n - 1);
+    fr = 0.25f;
+  } else {
+    i0 = (o >> 1) - 1;
+    i1 = o >> 1;
+    fr = 0.75f;
+  }
 }
-__global__ void k_up_fwd(const bf16* __restrict__ in, int c, int hw_in, int64_t np, bf16* __restrict__ out,
-                         int c_tot) {
-  const int g = c / 8, ho = 2 * hw_in;
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= np * ho * ho * g) return;
-  const int c0 = int(i % g) * 8;
-  const int64_t op = i / g;
-  const int ox = int(op % ho), oy = int((op / ho) % ho);
-  const int64_t m = op / (ho * ho);
+__global__ void __launch_bounds__(256) k_up_fwd(const bf16* __restrict__ in, int c, int hw_in, int np,
+                                                bf16* __restrict__ out, int c_tot) {
+  const int lg = ilog2(c / 8), lho = ilog2(2 * hw_in), ho = 2 * hw_in;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (np << (2 * lho + lg))) return;
+  const int c0 = (i & ((1 << lg) - 1)) * 8;
+  const int op = i >> lg;
+  const int ox = op & (ho - 1), oy = (op >> lho) & (ho - 1), m = op >> (2 * lho);
   int r0, r1, q0, q1;
   float fr, fc;
   up_src(oy, hw_in, r0, r1, fr);
   up_src(ox, hw_in, q0, q1, fc);
-  const bf16* b = in + m * hw_in * hw_in * c + c0;
+  const bf16* b = in + int64_t(m) * hw_in * hw_in * c + c0;
   float a00[8], a01[8], a10[8], a11[8], v[8];
   ld8(b + (r0 * hw_in + q0) * c, a00);
   ld8(b + (r0 * hw_in + q1) * c, a01);
@@ -256,62 +302,78 @@ __global__ void k_up_fwd(const bf16* __restrict__ in, int c, int hw_in, int64_t 
     const float t1 = a01[j] * (1.f - fr) + a11[j] * fr;
     v[j] = t0 * (1.f - fc) + t1 * fc;
   }
-  st8(out + op * c_tot + c0, v);
+  st8(out + int64_t(op) * c_tot + c0, v);
 }
 
-// adjoint of the upsample: d_low[i] = sum over outputs of weight(o -> i) * d_high[o]
-__device__ __forceinline__ float up_wt(int o, int i, int n) {
-  int i0, i1;
-  float fr;
-  up_src(o, n, i0, i1, fr);
-  return (i0 == i ? 1.f - fr : 0.f) + (i1 == i ? fr : 0.f);
+// adjoint of the upsample: low index i receives from outputs 2i-1 .. 2i+2
+// with weights (0.25, 0.75, 0.75, 0.25), folded at the map borders (output 0
+// and 2n-1 give both of their taps to the border sample)
+__device__ __forceinline__ void up_adj(int i, int n, int (&o)[4], float (&w)[4]) {
+  o[0] = 2 * i - 1; o[1] = 2 * i; o[2] = 2 * i + 1; o[3] = 2 * i + 2;
+  w[0] = 0.25f; w[1] = 0.75f; w[2] = 0.75f; w[3] = 0.25f;
+  if (i == 0) {         // output 0 reads (0, 1) with weights (1, 0)
+    w[0] = 0.f;
+    w[1] = 1.f;
+  }
+  if (i == n - 1) {     // output 2n-1 reads (n-1, n-1): 0.75 + 0.25
+    w[2] = 1.f;
+    w[3] = 0.f;
+  }
+  if (n == 1) {         // a 1-pixel map: both outputs copy it
+    w[1] = 1.f;
+    w[2] = 1.f;
+  }
 }
-__global__ void k_up_bwd(const bf16* __restrict__ dhigh, int c_tot, int c, int hw_in, int64_t np,
-                         bf16* __restrict__ dlow) {
-  const int g = c / 8, ho = 2 * hw_in;
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= np * hw_in * hw_in * g) return;
-  const int c0 = int(i % g) * 8;
-  const int64_t lp = i / g;
-  const int x = int(lp % hw_in), y = int((lp / hw_in) % hw_in);
-  const int64_t m = lp / (hw_in * hw_in);
+__global__ void __launch_bounds__(256) k_up_bwd(const bf16* __restrict__ dhigh, int c_tot, int c, int hw_in,
+                                                int np, bf16* __restrict__ dlow) {
+  const int lg = ilog2(c / 8), lhi = ilog2(hw_in), ho = 2 * hw_in;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (np << (2 * lhi + lg))) return;
+  const int c0 = (i & ((1 << lg) - 1)) * 8;
+  const int lp = i >> lg;
+  const int x = lp & (hw_in - 1), y = (lp >> lhi) & (hw_in - 1), m = lp >> (2 * lhi);
+  int oy[4], ox[4];
+  float wy[4], wx[4];
+  up_adj(y, hw_in, oy, wy);
+  up_adj(x, hw_in, ox, wx);
   float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int oy = max(0, 2 * y - 2); oy <= min(ho - 1, 2 * y + 3); ++oy) {
-    const float wy = up_wt(oy, y, hw_in);
-    if (wy == 0.f) continue;
-    for (int ox = max(0, 2 * x - 2); ox <= min(ho - 1, 2 * x + 3); ++ox) {
-      const float wx = up_wt(ox, x, hw_in);
-      if (wx == 0.f) continue;
+  const bf16* base = dhigh + int64_t(m) * ho * ho * c_tot + c0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    if (wy[a] == 0.f || oy[a] < 0 || oy[a] >= ho) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (wx[b] == 0.f || ox[b] < 0 || ox[b] >= ho) continue;
       float d[8];
-      ld8(dhigh + ((m * ho + oy) * ho + ox) * c_tot + c0, d);
-      const float w = wy * wx;
+      ld8(base + int64_t(oy[a] * ho + ox[b]) * c_tot, d);
+      const float w = wy[a] * wx[b];
 #pragma unroll
       for (int j = 0; j < 8; ++j) s[j] = fmaf(w, d[j], s[j]);
     }
   }
-  st8(dlow + lp * c + c0, s);
+  st8(dlow + int64_t(lp) * c + c0, s);
 }
 
 // max-pool backward + the skip-connection gradient: ds = dskip + dp at the
 // window's first maximum in scan order (torch's tie rule)
-__global__ void k_pool_bwd(const bf16* __restrict__ a, int a_tot, int a_off, int c, int hw_out,
-                           int64_t np, const bf16* __restrict__ dp, const bf16* __restrict__ dskip,
-                           int ds_tot, int ds_off, bf16* __restrict__ ds) {
-  const int g = c / 8, hi = 2 * hw_out;
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= np * hw_out * hw_out * g) return;
-  const int c0 = int(i % g) * 8;
-  const int64_t pp = i / g;
-  const int px = int(pp % hw_out), py = int((pp / hw_out) % hw_out);
-  const int64_t m = pp / (hw_out * hw_out);
+__global__ void __launch_bounds__(256) k_pool_bwd(const bf16* __restrict__ a, int a_tot, int a_off, int c,
+                                                  int hw_out, int np, const bf16* __restrict__ dp,
+                                                  const bf16* __restrict__ dskip, int ds_tot, int ds_off,
+                                                  bf16* __restrict__ ds) {
+  const int lg = ilog2(c / 8), lho = ilog2(hw_out), hi = 2 * hw_out;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (np << (2 * lho + lg))) return;
+  const int c0 = (i & ((1 << lg) - 1)) * 8;
+  const int pp = i >> lg;
+  const int px = pp & (hw_out - 1), py = (pp >> lho) & (hw_out - 1), m = pp >> (2 * lho);
   float v[4][8], dpv[8];
   int64_t q[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    q[k] = (m * hi + 2 * py + (k >> 1)) * hi + 2 * px + (k & 1);
+    q[k] = (int64_t(m) * hi + 2 * py + (k >> 1)) * hi + 2 * px + (k & 1);
     ld8(a + q[k] * a_tot + a_off + c0, v[k]);
   }
-  ld8(dp + pp * c + c0, dpv);
+  ld8(dp + int64_t(pp) * c + c0, dpv);
   int best[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -332,24 +394,46 @@ __global__ void k_pool_bwd(const bf16* __restrict__ a, int a_tot, int a_off, int
 }
 
 // LeakyReLU + BN backward, pass 1: per-channel sums of dyb and dyb * xhat
+struct BnbStatsF {
+  const bf16 *z, *da;
+  const float* bnv;
+  int cpad;
+  float slope;
+  float s[8], t[8], mu[8], is[8];
+  __device__ __forceinline__ void init(int c0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s[j] = __ldg(bnv + c0 + j);
+      t[j] = __ldg(bnv + cpad + c0 + j);
+      mu[j] = __ldg(bnv + 2 * cpad + c0 + j);
+      is[j] = __ldg(bnv + 3 * cpad + c0 + j);
+    }
+  }
+  template <int U>
+  __device__ __forceinline__ void go(int64_t p, int c0, float (&acc)[2][8]) const {
+    float zv[U][8], dv[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ld8(z + (p + 32 * u) * cpad + c0, zv[u]);
+      ld8(da + (p + 32 * u) * cpad + c0, dv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float y = fmaf(zv[u][j], s[j], t[j]);
+        const float dyb = y > 0.f ? dv[u][j] : slope * dv[u][j];
+        const float xh = (zv[u][j] - mu[j]) * is[j];
+        acc[0][j] += dyb;
+        acc[1][j] = fmaf(dyb, xh, acc[1][j]);
+      }
+  }
+};
 __global__ void __launch_bounds__(256) k_bnb_stats(const bf16* __restrict__ z, const bf16* __restrict__ da,
                                                    int cpad, int64_t npx, int64_t ppb,
                                                    const float* __restrict__ bnv, float slope,
                                                    double* part) {
-  chan_reduce<2>(npx, ppb, cpad, part, [&](int64_t p, int c0, float (&acc)[2][8]) {
-    float zv[8], dv[8];
-    ld8(z + p * cpad + c0, zv);
-    ld8(da + p * cpad + c0, dv);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = c0 + j;
-      const float y = fmaf(zv[j], bnv[c], bnv[cpad + c]);
-      const float dyb = y > 0.f ? dv[j] : slope * dv[j];
-      const float xh = (zv[j] - bnv[2 * cpad + c]) * bnv[3 * cpad + c];
-      acc[0][j] += dyb;
-      acc[1][j] = fmaf(dyb, xh, acc[1][j]);
-    }
-  });
+  chan_reduce<2>(npx, ppb, cpad, part, BnbStatsF{z, da, bnv, cpad, slope});
 }
 
 // bwd finalize: local gamma/beta gradients (before the SyncBN all-reduce)
@@ -372,26 +456,59 @@ __global__ void k_bnb_coef(const double* sums, int c, int cpad, double count, co
 
 // pass 2: dz = gamma * invstd * (dyb - m1 - xhat * m2) (zero beyond n maps
 // and in padded channels), plus per-block partial sums of dz (bias gradient)
+// dz = coef * (dyb - m1 - xhat * m2) = coef * dyb + (k0 + k1 * z) with
+// k1 = -coef * m2 * invstd, k0 = -coef * (m1 - m2 * mean * invstd): three
+// FMAs per element from constants held in registers
+struct BnbApplyF {
+  const bf16 *z, *da;
+  const float* bnv;
+  bf16* dz;
+  int64_t npx;  // real pixels (maps beyond n get dz = 0)
+  int cpad;
+  float slope;
+  float s[8], t[8], cf[8], k0[8], k1[8];
+  __device__ __forceinline__ void init(int c0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = c0 + j;
+      s[j] = __ldg(bnv + c);
+      t[j] = __ldg(bnv + cpad + c);
+      const float mu = __ldg(bnv + 2 * cpad + c), is = __ldg(bnv + 3 * cpad + c);
+      const float m1 = __ldg(bnv + 4 * cpad + c), m2 = __ldg(bnv + 5 * cpad + c);
+      cf[j] = __ldg(bnv + 6 * cpad + c);
+      k1[j] = -cf[j] * m2 * is;
+      k0[j] = -cf[j] * (m1 - m2 * mu * is);
+    }
+  }
+  template <int U>
+  __device__ __forceinline__ void go(int64_t p, int c0, float (&acc)[1][8]) const {
+    float zv[U][8], dv[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ld8(z + (p + 32 * u) * cpad + c0, zv[u]);
+      ld8(da + (p + 32 * u) * cpad + c0, dv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float o[8];
+      const bool real = p + 32 * u < npx;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float y = fmaf(zv[u][j], s[j], t[j]);
+        const float dyb = y > 0.f ? dv[u][j] : slope * dv[u][j];
+        const float g = real ? fmaf(cf[j], dyb, fmaf(k1[j], zv[u][j], k0[j])) : 0.f;
+        o[j] = g;
+        acc[0][j] += g;
+      }
+      st8(dz + (p + 32 * u) * cpad + c0, o);
+    }
+  }
+};
 __global__ void __launch_bounds__(256) k_bnb_apply(const bf16* __restrict__ z, const bf16* __restrict__ da,
                                                    int cpad, int64_t npx_all, int64_t npx, int64_t ppb,
                                                    const float* __restrict__ bnv, float slope,
                                                    bf16* __restrict__ dz, double* part) {
-  chan_reduce<1>(npx_all, ppb, cpad, part, [&](int64_t p, int c0, float (&acc)[1][8]) {
-    float zv[8], dv[8], o[8];
-    ld8(z + p * cpad + c0, zv);
-    ld8(da + p * cpad + c0, dv);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = c0 + j;
-      const float y = fmaf(zv[j], bnv[c], bnv[cpad + c]);
-      const float dyb = y > 0.f ? dv[j] : slope * dv[j];
-      const float xh = (zv[j] - bnv[2 * cpad + c]) * bnv[3 * cpad + c];
-      const float g = p < npx ? bnv[6 * cpad + c] * (dyb - bnv[4 * cpad + c] - xh * bnv[5 * cpad + c]) : 0.f;
-      o[j] = g;
-      acc[0][j] += g;
-    }
-    st8(dz + p * cpad + c0, o);
-  });
+  chan_reduce<1>(npx_all, ppb, cpad, part, BnbApplyF{z, da, bnv, dz, npx, cpad, slope});
 }
 
 // head: conv_out (1x1, 16 -> 3) + ReLU, L1 loss against y (n,3,32,32) fp32,
@@ -611,7 +728,7 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
   const size_t ws_off = wb;
   wb += (wsb + 255) & ~size_t(255);
   const size_t part_off = wb;
-  wb += size_t(256) * 2 * 1024 * 8 + size_t(1024) * HEAD_SLOTS * 8;
+  wb += size_t(2048) * 2 * 1024 * 8 + size_t(1024) * HEAD_SLOTS * 8;
   const size_t sums_off = wb;
   wb += 2 * 1024 * 8 + 64 * 8;
   void* wbase = nullptr;
@@ -643,9 +760,10 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
 }
 
 // reduction geometry over npx pixels: pixels per block and blocks
-inline void red_geom(int64_t npx, int64_t& ppb, int& gx) {
-  ppb = std::max<int64_t>(1024, (npx + 255) / 256);
-  ppb = (ppb + 31) / 32 * 32;
+inline void red_geom(int64_t npx, int ctiles, int64_t& ppb, int& gx) {
+  const int64_t target = std::max<int64_t>(1, int64_t(sm_count()) * 8 / ctiles);
+  ppb = std::max<int64_t>(128, (npx + target - 1) / target);
+  ppb = (ppb + 127) / 128 * 128;
   gx = int((npx + ppb - 1) / ppb);
 }
 
@@ -660,10 +778,10 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   if (rc) return rc;
   int64_t ppb;
   int gx;
-  red_geom(n * hw2, ppb, gx);
+  red_geom(n * hw2, coutp / 64, ppb, gx);
   k_bn_stats<<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], coutp, n * hw2, ppb, E->part);
   TC_CHECK("k_bn_stats");
-  k_reduce_parts<<<nbk(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
+  k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
   TC_CHECK("k_reduce_parts");
   rc = allreduce_sum(T->comm, E->sums, size_t(2) * coutp, 1, st);  // SyncBN
   if (rc) return rc;
@@ -700,11 +818,11 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   const bf16* da = E->B[P.dA].p;
   int64_t ppb;
   int gx;
-  red_geom(n * hw2, ppb, gx);
+  red_geom(n * hw2, coutp / 64, ppb, gx);
   k_bnb_stats<<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], da, coutp, n * hw2, ppb, E->bnv[l],
                                                     T->slope, E->part);
   TC_CHECK("k_bnb_stats");
-  k_reduce_parts<<<nbk(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
+  k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
   TC_CHECK("k_reduce_parts");
   k_bnb_param<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, coutp, T->grads + t.g, T->grads + t.be);
   TC_CHECK("k_bnb_param");
@@ -715,12 +833,12 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   TC_CHECK("k_bnb_coef");
   int64_t ppb2;
   int gx2;
-  red_geom(np * hw2, ppb2, gx2);
+  red_geom(np * hw2, coutp / 64, ppb2, gx2);
   bf16* dz = E->B[DZ].p;
   k_bnb_apply<<<dim3(gx2, coutp / 64), 256, 0, st>>>(E->Z[l], da, coutp, np * hw2, n * hw2, ppb2,
                                                      E->bnv[l], T->slope, dz, E->part);
   TC_CHECK("k_bnb_apply");
-  k_reduce_parts<<<nbk(t.cout), 256, 0, st>>>(E->part, gx2, t.cout, E->sums);
+  k_reduce_parts<<<nb_slots(t.cout), 256, 0, st>>>(E->part, gx2, t.cout, E->sums);
   TC_CHECK("k_reduce_parts");
   k_sums_to_float<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, T->grads + t.b);  // conv bias
   TC_CHECK("k_sums_to_float");
@@ -791,7 +909,7 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
     k_head<<<gx, 256, 0, st>>>(E->B[A15].p, T->params + t.w, T->params + t.b, y, n, np,
                                1.0 / double(n * 3 * 1024), E->B[DA15].p, E->part);
     TC_CHECK("k_head");
-    k_reduce_parts<<<1, 64, 0, st>>>(E->part, gx, HEAD_SLOTS, E->sums);
+    k_reduce_parts<<<nb_slots(HEAD_SLOTS), 256, 0, st>>>(E->part, gx, HEAD_SLOTS, E->sums);
     TC_CHECK("k_reduce_parts");
     k_head_out<<<1, 64, 0, st>>>(E->sums, T->grads + t.w, T->grads + t.b, E->loss);
     TC_CHECK("k_head_out");

@@ -29,6 +29,7 @@
 //   warps 2-5: epilogue (tcgen05.ld -> fp32 partial tiles)
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "drcb_net.h"
@@ -61,6 +62,9 @@ struct WgArgs {
   int rb, mb, cpm;        // box rows, box maps, chunks per map (hw >= 16)
   int dz_stages, x_stages;
   float* partial;         // [splits][units][n_acc][128][n_tile]
+  // dx-in-N variant (hw >= 16)
+  int xbox;               // bytes of the X box (rb + 2 rows)
+  int zero_off;           // byte offset of the zero block from the SMEM base
 };
 
 __device__ __forceinline__ void chunk_origin(const WgArgs& a, int c, int& map0, int& row0) {
@@ -227,6 +231,166 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// dx-in-N variant (hw in {16, 32}: an image row is a whole number of
+// 1024-B swizzle atoms). With the identity
+//   dW_(dy,dx) = sum_q X[q + (dy, 0)] * dZ[q - (0, dx)]
+// (exact: the terms it adds or drops have X or dZ out of the map = zero),
+// a K chunk of rb image rows needs ONE X box of rb + 2 rows (the dy shift
+// is a row offset inside it) and three dZ boxes shifted by dx = -1, 0, +1
+// (TMA zero fill at the row ends). Two MMAs per K step cover the nine taps:
+//   acc 0: M = [X(dy=-1) | X(dy=0)] (two 64-channel blocks, LBO = one row)
+//          x N = [dZ(dx=-1) | dZ(0) | dZ(+1)] = 192 columns: six taps,
+//   acc 1: M = [X(dy=+1) | zero block] x the same N: three taps.
+// N = 192 per MMA (the small-N layers' 64-column MMAs ran at ~45 % of the
+// tensor rate). A CTA owns one 64-channel input block x one 64-channel
+// output block and a range of K chunks.
+__global__ void __launch_bounds__(THREADS, 1)
+    k_wgrad_dxn(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapDZ,
+                const __grid_constant__ WgArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int STB = 3 * BOX + a.xbox;  // one stage: dZ boxes (dx = -1, 0, +1), then the X box
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.zero_off + BOX);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + 4;
+  uint64_t* tfull = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  const int unit = int(blockIdx.x) % a.units, split = int(blockIdx.x) / a.units;
+  const int cob = unit / a.cb, cb = unit % a.cb;  // output / input channel blocks of 64
+  const int c0 = int(int64_t(a.chunks) * split / a.splits);
+  const int c1 = int(int64_t(a.chunks) * (split + 1) / a.splits);
+  constexpr uint32_t NCOL = 192, TCOLS = 512;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&mapX);
+    prefetch_map(&mapDZ);
+    for (int s = 0; s < a.dz_stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp >= 2) {  // the zero block (the M partner of the dy = +1 block)
+    uint4* z = reinterpret_cast<uint4*>(smem + a.zero_off);
+    for (int i = threadIdx.x - 64; i < BOX / 16; i += THREADS - 64) z[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int rowb = a.hw * 128;  // one image row of 64 channels
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int c = c0; c < c1; ++c) {
+        const int map0 = c / a.cpm, row0 = (c % a.cpm) * a.rb;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], uint32_t(STB));
+        uint8_t* st = smem + s * STB;
+        for (int j = 0; j < 3; ++j)  // dZ[q - (0, dx)], dx = j - 1: box at x = 1 - j
+          tma_load_4d(&mapDZ, &full[s], st + j * BOX, 64 * cob, 1 - j, row0, map0);
+        tma_load_4d(&mapX, &full[s], st + 3 * BOX, 64 * cb, 0, row0 - 1, map0);
+        if (++s == a.dz_stages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_mn(0, 128, NCOL);
+      const uint32_t zero = smem_u32(smem + a.zero_off);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int c = c0; c < c1; ++c) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t bz = smem_u32(smem + s * STB);
+        const uint32_t xs = bz + 3 * BOX;
+        const uint32_t acc_flag = c > c0 ? 1u : 0u;
+#pragma unroll
+        for (int k = 0; k < KPX / 16; ++k) {
+          const uint64_t bd = mn128_desc(bz + k * 2048, BOX, 1024);
+          // rows dy = -1, 0 of the X box: offsets 0, one row
+          tc_mma<0>(tmem_base, mn128_desc(xs + k * 2048, rowb, 1024), bd, idesc, (acc_flag | k) ? 1u : 0u);
+          // dy = +1 (offset two rows) and the zero block
+          const uint32_t a1 = xs + 2 * rowb + k * 2048;
+          tc_mma<0>(tmem_base + NCOL, mn128_desc(a1, zero - (xs + 2 * rowb), 1024), bd, idesc,
+                    (acc_flag | k) ? 1u : 0u);
+        }
+        tc_commit(&empty[s]);
+        if (++s == a.dz_stages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      tc_commit(tfull);
+    }
+  } else {
+    const int q = warp & 3, row = q * 32 + lane;
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    float* out = a.partial + (int64_t(split) * a.units + unit) * 2 * 128 * NCOL;
+    for (int j = 0; j < 2; ++j) {
+      float* o = out + (int64_t(j) * 128 + row) * NCOL;
+      for (int c = 0; c < int(NCOL); c += 16) {
+        float v[16];
+        if (c1 > c0) {
+          uint32_t r[16];
+          tmem_ld16(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(j * NCOL + c), r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 16; e += 4)
+          *reinterpret_cast<float4*>(o + c + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TCOLS));
+  }
+}
+
+// dx-in-N partials -> dwf: unit (output block, input block), acc j, row m
+// (dy of the X block: acc 0 rows -1 / 0, acc 1 row +1), column n (dx, co)
+__global__ void k_wgrad_reduce_dxn(const WgArgs a, int cin, int cout, float* __restrict__ dwf) {
+  const int64_t per = int64_t(2) * 128 * 192;
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= per * a.units) return;
+  const int unit = int(e / per);
+  int64_t r = e % per;
+  const int n = int(r % 192);
+  r /= 192;
+  const int m = int(r % 128), j = int(r / 128);
+  if (j == 1 && m >= 64) return;  // the zero block
+  const int dy = j == 0 ? (m < 64 ? -1 : 0) : 1, dx = n / 64 - 1;
+  const int cob = unit / a.cb, cb = unit % a.cb;
+  const int ci = 64 * cb + (m & 63), co = 64 * cob + (n & 63);
+  if (ci >= cin || co >= cout) return;
+  const int64_t stride = int64_t(a.units) * 2 * 128 * 192;
+  const float* p = a.partial + int64_t(unit) * per + (int64_t(j) * 128 + m) * 192 + n;
+  float s = 0.f;
+  for (int k = 0; k < a.splits; ++k) s += p[k * stride];
+  dwf[(int64_t(co) * cin + ci) * 9 + (dy + 1) * 3 + (dx + 1)] = s;
+}
+
 // split-K partials -> conv-form fp32 weight gradient dwf[co][ci][tap], summed
 // over the splits in order (deterministic). One thread per (n tile, M tile,
 // row, column) accumulator element.
@@ -271,10 +435,16 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
   a.n_tile = cout_pad >= 256 ? 256 : cout_pad;
   while (cout_pad % a.n_tile) a.n_tile -= 64;
   a.nb_n = a.n_tile / 64;
-  a.npairs = (9 * a.cb + 1) / 2;
-  a.n_acc = std::min(a.npairs, 512 / a.n_tile);
-  a.groups = (a.npairs + a.n_acc - 1) / a.n_acc;
-  a.units = (cout_pad / a.n_tile) * a.groups;
+  const bool taps_env = getenv("DRCB_WGRAD_TAPS") != nullptr;  // A/B: a box per tap
+  const bool dxn = hw >= 16 && !taps_env;
+  if (dxn) {
+    a.units = (cout_pad / 64) * a.cb;
+  } else {
+    a.npairs = (9 * a.cb + 1) / 2;
+    a.n_acc = std::min(a.npairs, 512 / a.n_tile);
+    a.groups = (a.npairs + a.n_acc - 1) / a.n_acc;
+    a.units = (cout_pad / a.n_tile) * a.groups;
+  }
   const int px_map = hw * hw;
   if (hw >= 16) {
     a.rb = KPX / hw;
@@ -290,7 +460,8 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
   }
   const int nsm = sm_count();
   a.splits = std::max(1, std::min(a.chunks, (2 * nsm + a.units - 1) / a.units));
-  const size_t part = size_t(a.splits) * a.units * a.n_acc * 128 * a.n_tile * 4;
+  const size_t part = dxn ? size_t(a.splits) * a.units * 2 * 128 * 192 * 4
+                          : size_t(a.splits) * a.units * a.n_acc * 128 * a.n_tile * 4;
   if (!ws) {
     *ws_bytes = part;
     return 0;
@@ -298,6 +469,30 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
   if (*ws_bytes < part) return fail(DRCB_ECONTRACT, "wgrad: scratch too small");
   a.partial = static_cast<float*>(ws);
   const int DZB = a.nb_n * BOX;
+  static DeviceFlags attr_dxn;
+  if (dxn) {
+    a.xbox = (a.rb + 2) * hw * 128;
+    const int stb = 3 * BOX + a.xbox;
+    a.dz_stages = std::min(4, (222 * 1024 - BOX) / stb);
+    if (a.dz_stages < 2) return fail(DRCB_ECONFIG, "wgrad dx-in-N: SMEM plan");
+    a.zero_off = a.dz_stages * stb;
+    const size_t smem = 1024 + size_t(a.zero_off) + BOX + 256;
+    CUtensorMap mX, mDZ;
+    int rc = tc::encode_act(&mX, x, 0, cin_pad, hw, nmaps, hw, a.rb + 2, 1);
+    if (rc) return rc;
+    rc = tc::encode_act(&mDZ, dz, 0, cout_pad, hw, nmaps, hw, a.rb, 1);
+    if (rc) return rc;
+    smem_attr_once(attr_dxn, k_wgrad_dxn, 227 * 1024);
+    k_wgrad_dxn<<<a.units * a.splits, THREADS, smem, st>>>(mX, mDZ, a);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "k_wgrad_dxn");
+    const int64_t total = int64_t(2) * 128 * 192 * a.units;
+    k_wgrad_reduce_dxn<<<unsigned((total + 255) / 256), 256, 0, st>>>(a, cin, cout, dwf);
+    count_launch();
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : cuda_fail(e, "k_wgrad_reduce_dxn");
+  }
   a.dz_stages = 2;
   const int budget = 220 * 1024;
   a.x_stages = std::min(8, (budget - a.dz_stages * DZB) / (2 * BOX));

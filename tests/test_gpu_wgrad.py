@@ -61,3 +61,23 @@ def test_wgrad_deterministic():
                   dz.ctypes.data_as(C.c_void_p), dw.ctypes.data_as(C.c_void_p))
         outs.append(dw)
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 32, 2), (192, 64, 32, 2), (64, 128, 16, 2)])
+def test_wgrad_box_per_tap_variant_agrees(shape, monkeypatch):
+    """The 32x32 / 16x16 layers run the dx-in-N variant (one X box with the dy
+    shift as a row offset, three dx-shifted dZ boxes, N = 192);
+    DRCB_WGRAD_TAPS forces one X box per tap."""
+    cin, cout, hw, n = shape
+    rng = np.random.default_rng(7)
+    x = rng.normal(size=(n, hw, hw, cin)).astype(np.float32)
+    dz = rng.normal(size=(n, hw, hw, cout)).astype(np.float32)
+    out = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("DRCB_WGRAD_TAPS", env)
+        dw = np.zeros((cout, cin, 3, 3), np.float32)
+        _lib.call("drcb_debug_wgrad", cin, cout, hw, n, x.ctypes.data_as(C.c_void_p),
+                  dz.ctypes.data_as(C.c_void_p), dw.ctypes.data_as(C.c_void_p))
+        out.append(dw)
+    assert np.abs(out[0] - out[1]).max() <= 1e-5 * np.abs(out[1]).max()
