@@ -325,6 +325,11 @@ int drcb_trainer_apply(DrcbTrainer *t, float grad_scale, void *stream);
  * the step uses SyncBN (batch statistics all-reduced over NVLink/NVSwitch)
  * and all-reduces the gradient buffer; Adam averages by 1/world. */
 int drcb_trainer_set_comm(DrcbTrainer *t, void *nccl_comm, int32_t world);
+/* test hook (tensor-core trainer): the bf16 pre-BN conv output Z of one of
+ * the 16 3x3 layers from the last step, device NHWC (batch rounded up to 8,
+ * hw, hw, cout rounded up to 64) -> dst (device); layer 16: the head's input
+ * activation (head.deconv2's BN + LeakyReLU output, 32x32 x 64 channels). */
+int drcb_trainer_debug_z(DrcbTrainer *t, int32_t layer, void *dst, void *stream);
 
 /* ---- NCCL plumbing (libnccl.so.2 opened at first use) ------------------ */
 int drcb_nccl_unique_id(void *out128);

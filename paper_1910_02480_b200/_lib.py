@@ -124,6 +124,7 @@ _SIGS = [
     ("drcb_trainer_apply", C.c_int, [vp, C.c_float, vp]),
     ("drcb_trainer_export", C.c_int64, [vp, vp, C.c_int64]),
     ("drcb_trainer_set_comm", C.c_int, [vp, vp, C.c_int32]),
+    ("drcb_trainer_debug_z", C.c_int, [vp, C.c_int32, vp, vp]),
     ("drcb_nccl_unique_id", C.c_int, [vp]),
     ("drcb_nccl_comm_create", C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(vp)]),
     ("drcb_nccl_comm_destroy", C.c_int, [vp]),

@@ -932,3 +932,22 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
 
 }  // namespace train
 }  // namespace drcb
+
+// Test hook: the bf16 pre-BN conv output Z of layer `layer` (0..15) from the
+// last tensor-core step, NHWC (capacity maps, hw, hw, pad64(cout)) -> dst.
+extern "C" int drcb_trainer_debug_z(DrcbTrainer* T, int32_t layer, void* dst, void* stream) {
+  using namespace drcb;
+  using namespace drcb::train;
+  if (!T || !dst || layer < 0 || layer > 16) return fail(DRCB_ECONTRACT, "drcb_trainer_debug_z: bad arguments");
+  if (!T->tc) return fail(DRCB_ECONTRACT, "drcb_trainer_debug_z: no tensor-core step has run");
+  if (layer == 16) {  // the head's input (head.deconv2's BN + LeakyReLU output, 64-channel padded)
+    DRCB_CUDA(cudaMemcpyAsync(dst, T->tc->B[A15].p, size_t(T->tc->cap) * 1024 * 64 * 2,
+                              cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+    return 0;
+  }
+  const TL& t = T->L[layer];
+  const size_t bytes = size_t(T->tc->cap) * t.hw * t.hw * pad64(t.cout) * 2;
+  DRCB_CUDA(cudaMemcpyAsync(dst, T->tc->Z[layer], bytes, cudaMemcpyDeviceToDevice,
+                            static_cast<cudaStream_t>(stream)));
+  return 0;
+}

@@ -88,9 +88,26 @@ class DeviceTrainer:
         xd = xd.to(device="cuda", dtype=torch.float32).contiguous()
         yd = yd.to(device="cuda", dtype=torch.float32).contiguous()
         loss = C.c_double(0.0)
+        self._last_n_pad = (int(xd.shape[0]) + 7) // 8 * 8
         _lib.call("drcb_trainer_step", self.handle, _lib.ptr(xd), _lib.ptr(yd), int(xd.shape[0]),
                   C.byref(loss) if want_loss else None, int(bool(apply)), _lib.stream_ptr())
         return float(loss.value) if want_loss else None
+
+    def debug_z(self, layer):
+        """(test hook, bf16 engine) the pre-BN conv output of 3x3 layer
+        `layer` (0..15) from the last step, or (16) the head's input
+        activation: float32 CUDA tensor (n_pad, hw, hw, c_pad)."""
+        import torch
+
+        cout = [self.k, self.k, 2 * self.k, 2 * self.k, 4 * self.k, 4 * self.k, 8 * self.k,
+                8 * self.k, 4 * self.k, 4 * self.k, 2 * self.k, 2 * self.k, self.k, self.k,
+                self.k // 2, self.k // 4, self.k // 4][layer]
+        hw = [32, 32, 16, 16, 8, 8, 4, 4, 8, 8, 16, 16, 32, 32, 32, 32, 32][layer]
+        cpad = (cout + 63) // 64 * 64
+        n = self._last_n_pad
+        out = torch.empty((n, hw, hw, cpad), dtype=torch.bfloat16, device="cuda")
+        _lib.call("drcb_trainer_debug_z", self.handle, int(layer), _lib.ptr(out), _lib.stream_ptr())
+        return out.float()
 
     def apply(self, grad_scale=1.0):
         _lib.call("drcb_trainer_apply", self.handle, float(grad_scale), _lib.stream_ptr())
