@@ -1,10 +1,12 @@
 """Benchmark: predicted-radiance DRC frames/s at 1024^2 (BASELINE.json config 3).
 
-One step = one batch of 8 complete DRC frames per rank (G-buffer + direct,
-cache-point map path tracing, U-Net, MIS shading, interpolation, composite)
-over the 258,036-triangle config-3 scene, each frame from its own orbit camera.
-Frames shard across ranks with no collective (weak scaling: every rank renders
-its own 8 frames; value = all frames / max-over-ranks time).
+One step = one batch of 8 complete DRC frames (G-buffer + direct, cache-point
+map path tracing, U-Net, MIS shading, interpolation, composite) over the
+258,028-triangle config-3 scene, each frame from its own orbit camera.
+BASELINE config 3 shards that 8-frame batch across the ranks with the scene
+replicated and no collective (strong scaling: 8 / N frames per rank, one
+frame per GPU at N = 8; value = 8 frames x steps / max-over-ranks time);
+--weak gives every rank its own 8 frames instead.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
   python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
@@ -45,7 +47,10 @@ def parse():
     ap.add_argument("--tasks", type=int, default=1)
     ap.add_argument("--precision", type=int, default=32)
     ap.add_argument("--net", default=os.environ.get("DRCB_BENCH_NET", "fp16"))
-    ap.add_argument("--frames", type=int, default=FRAMES_PER_RANK)
+    ap.add_argument("--frames", type=int, default=FRAMES_PER_RANK,
+                    help="frames per step (the whole job's; per rank with --weak)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank renders --frames frames per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-points", type=int, default=16)
     ap.add_argument("--cpu-pixels", type=int, default=4096)
@@ -387,7 +392,8 @@ def main():
                               max_path_depth=8, rr_start=5, seed=0, precision=args.precision,
                               net_mode=args.net if args.net in ("fp32", "tf32", "bf16", "fp16") else "fp32")
     workload = {"workload": f"{args.config}: DRC frames {res[0]}x{res[1]}, "
-                            f"{args.frames} frames/rank/step, indirect_tasks={args.tasks}, "
+                            f"{args.frames} frames/{'rank/' if args.weak else ''}step, "
+                            f"indirect_tasks={args.tasks}, "
                             f"direct_spp={direct_spp}, orbit cameras r=3 (seed 2)",
                 "scene_tris": None, "cache_points_per_frame": None,
                 "precision": f"rays fp{args.precision}, U-Net {cfg.net_mode}",
@@ -395,8 +401,10 @@ def main():
     scene = scenegen.build_scene(args.config)
     from paper_1910_02480_b200.dist import frame_shard
 
-    cams = scenegen.orbit_cameras(args.frames * max(world, 1), res, seed=2)
+    n_frames = args.frames * max(world, 1) if args.weak else args.frames
+    cams = scenegen.orbit_cameras(n_frames, res, seed=2)
     my_cams = [cams[i] for i in frame_shard(len(cams), rank, max(world, 1))]
+    scaling = "weak" if args.weak else "strong"
     net = cnn.random_network(64, seed=wseed)
     plan = render.plan_points(res, cfg)
     n_pts = len(plan[0])
@@ -418,7 +426,7 @@ def main():
         cb["value"] = v
         line = {"metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * args.frames / v,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded procedural scene, SURVEY §8d)", "config": workload,
                 "impl": "reference", "cpu_baseline": cb,
                 "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
@@ -577,7 +585,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    frames_total = args.steps * len(my_cams) * world
+    frames_total = args.steps * n_frames
     value = frames_total / (ms / 1e3)
 
     # ---- e2e: public API with host buffers (plan H2D inside the call, image D2H)
@@ -606,8 +614,8 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = frames_total / (float(te.item()) / 1e3)
-    h2d = len(my_cams) * n_pts * (4 + 4 + 8)
-    d2h = len(my_cams) * h * w * 3 * (4 if args.precision == 32 else 8)
+    h2d = n_frames * n_pts * (4 + 4 + 8)  # the whole job's plan uploads
+    d2h = n_frames * h * w * 3 * (4 if args.precision == 32 else 8)
 
     # ---- roofline of the dominant stage (live CUDA-event stage times)
     peaks, src = measured_peaks()
@@ -695,7 +703,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": f"f{args.precision} rays / {cfg.net_mode} U-Net",
             "data": "synthetic (seeded procedural scene + random-init U-Net, SURVEY §8d)",
             "config": workload, "clocks": clk, "roofline": roof, "cpu_baseline": cb,

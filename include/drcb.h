@@ -331,6 +331,23 @@ int drcb_trainer_set_comm(DrcbTrainer *t, void *nccl_comm, int32_t world);
  * activation (head.deconv2's BN + LeakyReLU output, 32x32 x 64 channels). */
 int drcb_trainer_debug_z(DrcbTrainer *t, int32_t layer, void *dst, void *stream);
 
+/* reduction hook replacing NCCL for the trainer's SyncBN statistics and
+ * gradient all-reduce: fn(user, device buffer, count, is_double, stream)
+ * leaves the sum over the `world` ranks in buf. */
+typedef int (*DrcbReduceFn)(void *user, void *buf, int64_t count, int32_t is_double, void *stream);
+int drcb_trainer_set_reducer(DrcbTrainer *t, DrcbReduceFn fn, void *user, int32_t world);
+
+/* loopback communicator: `world` ranks as host threads of one process
+ * (half-batch trainers on one GPU), reduced in rank order; per-rank ctx for
+ * drcb_loopback_reduce (a DrcbReduceFn). */
+int drcb_loopback_create(int32_t world, void **out);
+int drcb_loopback_rank(void *lb, int32_t rank, void **ctx);
+int drcb_loopback_reduce(void *ctx, void *buf, int64_t count, int32_t is_double, void *stream);
+void drcb_loopback_destroy(void *lb, void **ranks, int32_t n);
+/* synchronous byte copy between host / device addresses on `stream` (the
+ * host-staged reduction hooks, e.g. a gloo all-reduce). */
+int drcb_copy_sync(void *dst, const void *src, int64_t bytes, void *stream);
+
 /* ---- NCCL plumbing (libnccl.so.2 opened at first use) ------------------ */
 int drcb_nccl_unique_id(void *out128);
 int drcb_nccl_comm_create(const void *id128, int32_t world, int32_t rank, void **comm);

@@ -668,6 +668,11 @@ extern "C" int drcb_trainer_set_mode(DrcbTrainer* T, int32_t mode) {
 extern "C" void drcb_trainer_destroy(DrcbTrainer* T) {
   if (!T) return;
   if (T->tc) tc_engine_destroy(T->tc);
+  if (T->comm_stream) {
+    for (cudaEvent_t e : T->comm_ev)
+      if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(T->comm_stream);
+  }
   for (void* p : T->allocs) cudaFree(p);
   delete T;
 }
@@ -702,7 +707,7 @@ int bn_forward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& out, cudaS
   k_reduce_partials<<<nb(2 * t.cout), 256, 0, st>>>(W.part, GX, 2 * t.cout, W.acc);
   TCHECK("k_reduce_partials");
   // SyncBN: batch statistics over all data-parallel ranks (NVLink all-reduce)
-  int rc = allreduce_sum(T->comm, W.acc, size_t(2) * t.cout, 1, st);
+  int rc = trainer_allreduce(T, W.acc, size_t(2) * t.cout, 1, st);
   if (rc) return rc;
   k_bn_finalize<<<nb(t.cout), 256, 0, st>>>(W.acc, t.cout, double(n) * hw2 * T->world, W.mean[l],
                                                W.invstd[l], T->running + t.rm, T->running + t.rv);
@@ -741,7 +746,7 @@ int layer_backward(DrcbTrainer* T, int l, Work& W, int64_t n, const View& in, co
   TCHECK("k_bn_param_grads");
   // SyncBN backward: global means of dyb and dyb * xhat
   {
-    int rc = allreduce_sum(T->comm, W.acc, size_t(2) * t.cout, 1, st);
+    int rc = trainer_allreduce(T, W.acc, size_t(2) * t.cout, 1, st);
     if (rc) return rc;
   }
   k_bn_bwd_apply<<<nb(n * t.cout * hw2), 256, 0, st>>>(W.z[l], dout.p, dout.ctot, dout.coff,
@@ -783,6 +788,20 @@ extern "C" int drcb_trainer_apply(DrcbTrainer* T, float grad_scale, void* stream
 
 namespace drcb {
 namespace train {
+int trainer_allreduce(DrcbTrainer* T, void* buf, size_t count, int is_double, cudaStream_t st) {
+  if (T->reduce_fn) {
+    int rc = T->reduce_fn(T->reduce_user, buf, int64_t(count), is_double, st);
+    return rc ? fail(DRCB_ENCCL, "reduction hook failed") : 0;
+  }
+  return allreduce_sum(T->comm, buf, count, is_double, st);
+}
+
+void layer_param_range(const DrcbTrainer* T, int l, int64_t& off, int64_t& count) {
+  const TL& t = T->L[l];
+  off = t.w;
+  count = (t.has_bn ? t.be + t.cout : t.b + t.cout) - t.w;
+}
+
 // conv-form (forward) and transposed-flipped (dgrad) fp32 weights of every
 // layer from the master parameters
 int weight_forms(DrcbTrainer* T, cudaStream_t st) {
@@ -813,7 +832,9 @@ extern "C" int drcb_trainer_step(DrcbTrainer* T, const float* x, const float* y,
     // the NHWC tensor-core engine: forward, loss and backward into T->grads
     double* loss_dev = nullptr;
     rc = tc_step(T, x, y, n, &loss_dev, st);
-    if (!rc) rc = allreduce_sum(T->comm, T->grads, size_t(T->n_params), 0, st);
+    // NCCL: the gradients were all-reduced layer by layer inside the step
+    // (bucketed, overlapping the backward); a reduction hook gets one call
+    if (!rc && (T->reduce_fn || !T->comm)) rc = trainer_allreduce(T, T->grads, size_t(T->n_params), 0, st);
     if (!rc && apply_adam) rc = drcb_trainer_apply(T, 1.0f / float(T->world), stream);
     if (rc) return rc;
     if (loss_host) {
@@ -933,7 +954,7 @@ extern "C" int drcb_trainer_step(DrcbTrainer* T, const float* x, const float* y,
   // (drcb_trainer_apply after an external all-reduce, or apply_adam below)
   // gradient all-reduce over the data-parallel ranks (sum); the per-rank
   // loss is a local mean, so the average is sum / world
-  rc = allreduce_sum(T->comm, T->grads, size_t(T->n_params), 0, st);
+  rc = trainer_allreduce(T, T->grads, size_t(T->n_params), 0, st);
   if (rc) {
     cudaFreeAsync(W.base, st);
     return rc;
@@ -978,7 +999,21 @@ extern "C" int drcb_trainer_apply(DrcbTrainer* T, float grad_scale, void* stream
 extern "C" int drcb_trainer_set_comm(DrcbTrainer* T, void* comm, int32_t world) {
   if (!T || world < 1) return fail(DRCB_ECONTRACT, "drcb_trainer_set_comm: bad arguments");
   T->comm = comm;
+  T->reduce_fn = nullptr;
+  T->reduce_user = nullptr;
   T->world = comm ? world : 1;
+  return 0;
+}
+
+// a reduction hook in place of NCCL: fn(user, device buffer, count, is_double,
+// stream) must leave the sum over the `world` ranks in the buffer (the
+// SyncBN statistics and the gradients of the data-parallel step go through it)
+extern "C" int drcb_trainer_set_reducer(DrcbTrainer* T, DrcbReduceFn fn, void* user, int32_t world) {
+  if (!T || world < 1) return fail(DRCB_ECONTRACT, "drcb_trainer_set_reducer: bad arguments");
+  T->comm = nullptr;
+  T->reduce_fn = fn;
+  T->reduce_user = user;
+  T->world = fn ? world : 1;
   return 0;
 }
 

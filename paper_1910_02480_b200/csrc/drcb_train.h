@@ -46,6 +46,13 @@ struct DrcbTrainer {
   std::vector<void*> allocs;
   int mode = 0;  // 0 = fp32 CUDA cores (parity), 2 = bf16 tensor cores (NHWC engine)
   drcb::train::TcEngine* tc = nullptr;
+  // a reduction hook replacing NCCL (loopback ranks in one process, or a
+  // host callback such as a gloo all-reduce): drcb_trainer_set_reducer
+  DrcbReduceFn reduce_fn = nullptr;
+  void* reduce_user = nullptr;
+  // bucketed gradient all-reduce (NCCL): a side stream + one event per layer
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t comm_ev[18] = {};
 };
 
 namespace drcb {
@@ -56,5 +63,10 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
             cudaStream_t st);
 // weight-form kernels shared by both engines (drcb_train.cu)
 int weight_forms(DrcbTrainer* T, cudaStream_t st);
+// sum-all-reduce over the data-parallel ranks through the trainer's
+// communicator: the reduction hook if set, else NCCL (no-op for one rank)
+int trainer_allreduce(DrcbTrainer* T, void* buf, size_t count, int is_double, cudaStream_t st);
+// the flat-buffer range [off, off + count) of layer l's parameters
+void layer_param_range(const DrcbTrainer* T, int l, int64_t& off, int64_t& count);
 }  // namespace train
 }  // namespace drcb

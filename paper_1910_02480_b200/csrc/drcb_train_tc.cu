@@ -783,7 +783,7 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   TC_CHECK("k_bn_stats");
   k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
   TC_CHECK("k_reduce_parts");
-  rc = allreduce_sum(T->comm, E->sums, size_t(2) * coutp, 1, st);  // SyncBN
+  rc = trainer_allreduce(T, E->sums, size_t(2) * coutp, 1, st);  // SyncBN
   if (rc) return rc;
   k_bn_fin<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, coutp, double(n) * hw2 * T->world,
                                          T->params + t.g, T->params + t.be, T->running + t.rm,
@@ -826,7 +826,7 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   TC_CHECK("k_reduce_parts");
   k_bnb_param<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, coutp, T->grads + t.g, T->grads + t.be);
   TC_CHECK("k_bnb_param");
-  int rc = allreduce_sum(T->comm, E->sums, size_t(2) * coutp, 1, st);  // SyncBN backward
+  int rc = trainer_allreduce(T, E->sums, size_t(2) * coutp, 1, st);  // SyncBN backward
   if (rc) return rc;
   k_bnb_coef<<<nbk(coutp), 256, 0, st>>>(E->sums, t.cout, coutp, double(n) * hw2 * T->world,
                                           T->params + t.g, E->bnv[l]);
@@ -915,9 +915,32 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
     TC_CHECK("k_head_out");
   }
   // ---- backward
+  // NCCL (world > 1): each layer's gradients are all-reduced on a side stream
+  // as soon as its backward is done (buckets = layers, in backward order),
+  // overlapping the all-reduce with the remaining layers' backward
+  const bool bucket = T->comm && !T->reduce_fn && T->world > 1;
+  if (bucket && !T->comm_stream) {
+    DRCB_CUDA(cudaStreamCreateWithFlags(&T->comm_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : T->comm_ev) DRCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  int nev = 0;
+  auto reduce_layer = [&](int l) -> int {
+    if (!bucket) return 0;
+    int64_t off, cnt;
+    layer_param_range(T, l, off, cnt);
+    DRCB_CUDA(cudaEventRecord(T->comm_ev[nev], st));
+    DRCB_CUDA(cudaStreamWaitEvent(T->comm_stream, T->comm_ev[nev], 0));
+    ++nev;
+    return allreduce_sum(T->comm, T->grads + off, size_t(cnt), 0, T->comm_stream);
+  };
+  rc = reduce_layer(16);  // the head (its gradients came with the loss)
+  if (rc) return rc;
   const int order[] = {15, 14, 13, 12, -1, 11, 10, -2, 9, 8, -3, 7, 6, -4, 5, 4, -5, 3, 2, -6, 1, 0};
   for (int o : order) {
-    if (o >= 0) rc = layer_bwd(T, o, n, np, st);
+    if (o >= 0) {
+      rc = layer_bwd(T, o, n, np, st);
+      if (!rc) rc = reduce_layer(o);
+    }
     else if (o == -1) rc = up_bwd(E, DC1, 128, 16, DA11, np, st);
     else if (o == -2) rc = up_bwd(E, DC2, 256, 8, DA9, np, st);
     else if (o == -3) rc = up_bwd(E, DC3, 512, 4, DA7, np, st);
@@ -925,6 +948,10 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
     else if (o == -5) rc = pool_bwd(E, C2, 256, 128, 8, DP2, DC2, DS2, np, st);
     else rc = pool_bwd(E, C1, 128, 64, 16, DP1, DC1, DS1, np, st);
     if (rc) return rc;
+  }
+  if (bucket) {  // the step's stream waits for the last bucket
+    DRCB_CUDA(cudaEventRecord(T->comm_ev[nev], T->comm_stream));
+    DRCB_CUDA(cudaStreamWaitEvent(st, T->comm_ev[nev], 0));
   }
   *loss_dev = E->loss;
   return 0;

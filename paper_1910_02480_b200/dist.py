@@ -95,3 +95,80 @@ def dp_step(trainer, x, y, group=None):
         dist.all_reduce(trainer.grad_tensor(), op=dist.ReduceOp.SUM, group=group)
     trainer.apply(1.0 / world)
     return loss
+
+
+# ---------------------------------------------------------------------------
+# reduction hooks (drcb_trainer_set_reducer): the same SyncBN + gradient
+# all-reduce points NCCL serves, through another transport
+
+# int fn(void* user, void* buf, int64_t count, int32_t is_double, void* stream)
+REDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p)
+
+
+def attach_reducer(trainer, fn, user, world):
+    """Route the trainer's reductions through `fn` (a REDUCE_FN or the address
+    of a C function) with context `user`."""
+    _lib.call("drcb_trainer_set_reducer", trainer.handle,
+              C.cast(fn, C.c_void_p) if not isinstance(fn, int) else C.c_void_p(fn),
+              C.c_void_p(user) if not isinstance(user, C.c_void_p) else user, int(world))
+    trainer._reducer = fn  # keep a Python callback alive
+
+
+class LoopbackGroup:
+    """`world` data-parallel ranks as host threads of one process (e.g. two
+    half-batch trainers on one GPU): libdrcb's loopback all-reduce sums the
+    ranks' buffers in rank order — SyncBN and the gradient all-reduce exactly
+    where NCCL would run them."""
+
+    def __init__(self, world):
+        lib = _lib.load()
+        h = C.c_void_p()
+        _lib.check(lib.drcb_loopback_create(int(world), C.byref(h)), "drcb_loopback_create")
+        self.handle, self.world = h, int(world)
+        self._ranks = []
+
+    def attach(self, trainer, rank):
+        lib = _lib.load()
+        ctx = C.c_void_p()
+        _lib.call("drcb_loopback_rank", self.handle, int(rank), C.byref(ctx))
+        self._ranks.append(ctx)
+        addr = C.cast(lib.drcb_loopback_reduce, C.c_void_p).value
+        attach_reducer(trainer, addr, ctx, self.world)
+
+    def close(self):
+        if self.handle:
+            arr = (C.c_void_p * len(self._ranks))(*[r.value for r in self._ranks])
+            _lib.load().drcb_loopback_destroy(self.handle, arr, len(self._ranks))
+            self.handle = None
+
+
+def host_reducer(group=None, device=True):
+    """A REDUCE_FN doing a host-staged torch.distributed all-reduce (sum):
+    device buffer -> host -> all_reduce (gloo or any backend) -> device. With
+    device=False the buffer is host memory (CPU tests call it directly)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    def reduce(user, buf, count, is_double, stream):
+        try:
+            dt = np.float64 if is_double else np.float32
+            host = np.empty(int(count), dtype=dt)
+            nbytes = host.nbytes
+            if device:
+                _lib.call("drcb_copy_sync", host.ctypes.data_as(C.c_void_p), C.c_void_p(buf), nbytes,
+                          C.c_void_p(stream))
+            else:
+                C.memmove(host.ctypes.data, buf, nbytes)
+            t = torch.from_numpy(host)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            if device:
+                _lib.call("drcb_copy_sync", C.c_void_p(buf), host.ctypes.data_as(C.c_void_p), nbytes,
+                          C.c_void_p(stream))
+            else:
+                C.memmove(buf, host.ctypes.data, nbytes)
+            return 0
+        except Exception:  # the library reports a failed hook as an error
+            return 1
+
+    return REDUCE_FN(reduce)

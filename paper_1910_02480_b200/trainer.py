@@ -133,6 +133,14 @@ class DeviceTrainer:
         flat = self._host(0)
         return {n: flat[o:o + int(np.prod(s))].reshape(s).copy() for n, _, s, o in self.layout}
 
+    def running(self):
+        """Batch-norm running statistics, flat fp32 (DRCW order of the layers)."""
+        import torch
+
+        ptr = self._buffers()[2]
+        torch.cuda.current_stream().synchronize()
+        return _device_view(ptr, self.n_running).cpu().numpy()
+
     def grads(self):
         flat = self._host(1)
         return {n: flat[o:o + int(np.prod(s))].reshape(s).copy() for n, _, s, o in self.layout}

@@ -89,3 +89,38 @@ def test_dp_step_matches_full_batch_gloo():
     # equal shards of an L1 mean: full-batch gradient == mean of shard grads
     assert np.allclose(res[0][1], ref.w.numpy(), atol=1e-6)
     assert np.array_equal(res[0][1], res[1][1])
+
+
+def _host_reducer_worker(rank, world, port, out):
+    import ctypes as C
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1910_02480_b200.dist import host_reducer
+
+        fn = host_reducer(device=False)  # the REDUCE_FN libdrcb calls (host buffers here)
+        for dt, is_double in ((np.float32, 0), (np.float64, 1)):
+            buf = (np.arange(10, dtype=dt) + 100 * rank).copy()
+            rc = fn(None, buf.ctypes.data_as(C.c_void_p).value, len(buf), is_double, None)
+            out.put((rank, str(dt), rc, buf.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_staged_reduction_hook_world2_gloo():
+    """The reduction hook the trainer calls at every SyncBN / gradient
+    reduction point (drcb_trainer_set_reducer), backed by a gloo all-reduce:
+    both ranks receive the sum, in both precisions."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_host_reducer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(4)]
+    for p in ps:
+        p.join(timeout=60)
+    want = (2 * np.arange(10) + 100).tolist()
+    for rank, dt, rc, buf in res:
+        assert rc == 0 and buf == want, (rank, dt, rc, buf)
