@@ -21,7 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--maps", type=int, default=4096)
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--mode", default="bf16")
+    ap.add_argument("--mode", default="fp16")
     args = ap.parse_args()
     import torch
 

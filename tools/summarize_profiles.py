@@ -72,7 +72,7 @@ def network(rnd):
             continue
         layers.append({"kernel": d["kernel"], "us": round(d["gpu__time_duration.sum"] / 1e3, 1),
                        "dram_bytes": int(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"])})
-    out = {"what": "U-Net forward of 4,096 maps (bf16), DRAM bytes per kernel from ncu --metrics "
+    out = {"what": "U-Net forward of 4,096 maps (bench precision), DRAM bytes per kernel from ncu --metrics "
                    "dram__bytes_read.sum,dram__bytes_write.sum (--clock-control none, serialised)",
            "maps": 4096, "dram_bytes_total": sum(x["dram_bytes"] for x in layers),
            "kernel_us_total": round(sum(x["us"] for x in layers), 1), "layers": layers}
@@ -163,6 +163,34 @@ def traversal(rnd):
     return path
 
 
+def train(rnd):
+    """Kernel shares of one B = 4,096 tensor-core training step (the second of
+    two: tools/train_time.py --warmup 1 --iters 1) with DRAM bytes."""
+    hdr, rows = ncu_rows(os.path.join(OUT, "prof_train.csv"))
+    iN, iM, iV, iID = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("ID")
+    per = collections.OrderedDict()
+    for r in rows:
+        d = per.setdefault(int(r[iID]), {"kernel": short(r[iN])})
+        d[r[iM]] = float(r[iV].replace(",", ""))
+    seq = list(per.values())
+    seq = seq[len(seq) // 2:]
+    tot, cnt, dram = collections.Counter(), collections.Counter(), collections.Counter()
+    for d in seq:
+        k = d["kernel"]
+        tot[k] += d.get("gpu__time_duration.sum", 0.0) / 1e3
+        cnt[k] += 1
+        dram[k] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+    s = sum(tot.values())
+    path = os.path.join(PROF, f"{rnd}_train_launches_summary.csv")
+    with open(path, "w") as f:
+        f.write("# ncu launch list of one bf16 tensor-core training step, B = 4,096 (the second of two), "
+                "--clock-control none, serialised\n")
+        f.write("kernel,launches,total_us,share,dram_gb\n")
+        for k, v in tot.most_common():
+            f.write(f"{k},{cnt[k]},{v:.1f},{v / s:.3f},{dram[k] / 1e9:.3f}\n")
+    return path
+
+
 def bench(rnd):
     for line in open(os.path.join(OUT, "prof_bench.log")):
         if line.startswith("{"):
@@ -181,7 +209,7 @@ def main():
     if a.out:
         PROF = a.out
         os.makedirs(PROF, exist_ok=True)
-    for fn in (bench, launches, network, full, traversal):
+    for fn in (bench, launches, network, train, full, traversal):
         try:
             print(fn(a.round))
         except Exception as e:  # keep the others
