@@ -181,10 +181,24 @@ def cpu_baseline(scene, cams, cfg, net_host, npts_total, n_pixels, n_points, ran
     t_pt = (time.perf_counter() - t1) / max(1, len(pos))
     frame_s = w * h * t_px + npts_total * t_pt
     return {"value": 1.0 / frame_s, "unit": "frames/s", "cores": nthreads, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"oracle on {n_pixels} px (G-buffer+direct) + {len(pos)} cache points "
                       f"(maps+U-Net fp32+shade) of config {cfg_name()} frame 0; frame time "
                       f"extrapolated = {w}x{h}*{t_px*1e6:.1f}us + {npts_total}*{t_pt*1e3:.1f}ms",
             "seconds_per_frame": frame_s}
+
+
+def cpu_model():
+    """The host CPU the baseline ran on (SURVEY §8(d) asks for it)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or platform.machine()
 
 
 _CFG_NAME = ["c3"]
