@@ -227,31 +227,39 @@ def train_throughput(cnn, world=1, batches=(64, 256, 1024), global_batch=4096, s
     net = cnn.random_network(64, seed=3)
     out = {"model": "MapAutoencoder k=64 (7,32,32)->(3,32,32)", "unit": "samples/s",
            "world": world, "allreduce": "libdrcb NCCL (grads + SyncBN)" if world > 1 else None}
-    runs = [("bf16", b, f"bf16_b{b}") for b in batches]
+    # one process: the bf16 step is replayed from a captured CUDA graph
+    # (DeviceTrainer.step_graph, bit-identical to the eager step); the eager
+    # launch sequence is timed beside it at the smallest batch
+    graphs = world == 1
+    runs = [("bf16", b, f"bf16_b{b}", graphs) for b in batches]
+    if graphs:
+        runs.append(("bf16", batches[0], f"bf16_b{batches[0]}_eager", False))
     if global_batch and global_batch % world == 0:
-        runs.append(("bf16", global_batch // world, f"bf16_global{global_batch}"))
+        runs.append(("bf16", global_batch // world, f"bf16_global{global_batch}", graphs))
     if world == 1:
-        runs.append(("fp32", batches[0], f"fp32_b{batches[0]}"))
+        runs.append(("fp32", batches[0], f"fp32_b{batches[0]}", False))
+    out["graph_replay"] = graphs
     trainers = {}
-    for mode, b, key in runs:
-        if mode not in trainers:
+    for mode, b, key, graph in runs:
+        if (mode, graph) not in trainers:
             tr = DeviceTrainer(net, lr=1e-4, mode=mode)
             if world > 1:
                 attach_nccl(tr)
-            trainers[mode] = tr
-        tr = trainers[mode]
+            trainers[(mode, graph)] = tr
+        tr = trainers[(mode, graph)]
         g = torch.Generator(device="cuda").manual_seed(3)
         x = torch.rand((b, 7, 32, 32), device="cuda", generator=g)
         y = torch.rand((b, 3, 32, 32), device="cuda", generator=g)
+        step = (lambda: tr.step_graph(x, y)) if graph else (lambda: tr.step(x, y, want_loss=False))
         for _ in range(warmup):
-            tr.step(x, y, want_loss=False)
+            step()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0.record()
         for _ in range(steps):
-            tr.step(x, y, want_loss=False)
+            step()
         e1.record()
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device="cuda")

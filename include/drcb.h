@@ -331,6 +331,13 @@ int drcb_trainer_set_comm(DrcbTrainer *t, void *nccl_comm, int32_t world);
  * activation (head.deconv2's BN + LeakyReLU output, 32x32 x 64 channels). */
 int drcb_trainer_debug_z(DrcbTrainer *t, int32_t layer, void *dst, void *stream);
 
+/* The batch L1 loss of the last bf16 (mode 2) step, read on `stream`
+ * (synchronises). drcb_trainer_step is graph-capture safe in mode 2 after one
+ * eager step at the same batch size (no allocation, no host sync when
+ * loss_host is NULL; the Adam step counter lives on the device), so a
+ * captured step can be replayed and its loss read here. */
+int drcb_trainer_last_loss(DrcbTrainer *t, double *loss, void *stream);
+
 /* reduction hook replacing NCCL for the trainer's SyncBN statistics and
  * gradient all-reduce: fn(user, device buffer, count, is_double, stream)
  * leaves the sum over the `world` ranks in buf. */

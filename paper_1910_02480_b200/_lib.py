@@ -125,6 +125,7 @@ _SIGS = [
     ("drcb_trainer_export", C.c_int64, [vp, vp, C.c_int64]),
     ("drcb_trainer_set_comm", C.c_int, [vp, vp, C.c_int32]),
     ("drcb_trainer_debug_z", C.c_int, [vp, C.c_int32, vp, vp]),
+    ("drcb_trainer_last_loss", C.c_int, [vp, C.POINTER(C.c_double), vp]),
     ("drcb_trainer_set_reducer", C.c_int, [vp, vp, vp, C.c_int32]),
     ("drcb_loopback_create", C.c_int, [C.c_int32, C.POINTER(vp)]),
     ("drcb_loopback_rank", C.c_int, [vp, C.c_int32, C.POINTER(vp)]),

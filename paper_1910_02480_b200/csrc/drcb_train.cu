@@ -376,11 +376,24 @@ __global__ void k_up_bwd(const float* __restrict__ dhigh, int c_tot, int c, int 
 
 // torch.optim.Adam (amsgrad=False, weight_decay=0): m, v, bias corrections,
 // p -= lr/bc1 * m / (sqrt(v)/sqrt(bc2) + eps)
+// The step counter and the bias corrections live on the device (double, as
+// torch computes them on the host) so that a captured step graph replays
+// with the right step number: coef = {lr / bc1, sqrt(bc2)}.
+__global__ void k_adam_coef(int64_t* step, float lr, float b1, float b2, float* coef) {
+  const int64_t s = *step + 1;
+  *step = s;
+  const double bc1 = 1.0 - pow(double(b1), double(s));
+  const double bc2 = 1.0 - pow(double(b2), double(s));
+  coef[0] = float(double(lr) / bc1);
+  coef[1] = float(sqrt(bc2));
+}
+
 __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
-                       float* __restrict__ v, int64_t n, float step_size, float b1, float b2,
-                       float eps, float bc2_sqrt, float gscale) {
+                       float* __restrict__ v, int64_t n, const float* __restrict__ coef, float b1,
+                       float b2, float eps, float gscale) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const float step_size = coef[0], bc2_sqrt = coef[1];
   float gi = g[i] * gscale;
   float mi = m[i] + (1.f - b1) * (gi - m[i]);  // exp_avg.lerp_(grad, 1 - beta1)
   float vi = b2 * v[i] + (1.f - b2) * (gi * gi);
@@ -633,7 +646,8 @@ extern "C" int drcb_trainer_create(const void* drcw, size_t len, float lr, float
   }
   size_t pbytes = size_t(T->n_params) * 4;
   void* p = nullptr;
-  if (cudaMalloc(&p, pbytes * 4 + size_t(T->n_running) * 4 + size_t(wtot) * 8) != cudaSuccess) {
+  const size_t sbytes = (pbytes * 4 + size_t(T->n_running) * 4 + size_t(wtot) * 8 + 15) & ~size_t(15);
+  if (cudaMalloc(&p, sbytes + 16) != cudaSuccess) {
     delete T;
     return fail(DRCB_ECUDA, "cudaMalloc trainer state");
   }
@@ -646,6 +660,9 @@ extern "C" int drcb_trainer_create(const void* drcw, size_t len, float lr, float
   T->running = f + 4 * T->n_params;
   T->wf = T->running + T->n_running;
   T->wt = T->wf + wtot;
+  T->d_step = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(p) + sbytes);
+  T->d_coef = reinterpret_cast<float*>(T->d_step + 1);
+  cudaMemset(T->d_step, 0, 16);
   cudaMemcpy(T->params, hp.data(), pbytes, cudaMemcpyHostToDevice);
   cudaMemset(T->grads, 0, pbytes * 3);
   cudaMemcpy(T->running, hr.data(), size_t(T->n_running) * 4, cudaMemcpyHostToDevice);
@@ -682,7 +699,10 @@ extern "C" int drcb_trainer_info(const DrcbTrainer* T, int64_t* out4) {
   out4[0] = T->k;
   out4[1] = T->n_params;
   out4[2] = T->n_running;
-  out4[3] = T->step;
+  int64_t step = 0;  // the device counter (graph replays advance it too)
+  if (cudaMemcpy(&step, T->d_step, sizeof(step), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(DRCB_ECUDA, "drcb_trainer_info: step counter");
+  out4[3] = step;
   return 0;
 }
 
@@ -825,11 +845,11 @@ extern "C" int drcb_trainer_step(DrcbTrainer* T, const float* x, const float* y,
   if (n < 1) return fail(DRCB_ECONFIG, "training step needs n >= 1 examples");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   keep_pool_memory();
-  int rc = weight_forms(T, st);
-  if (rc) return rc;
   const int64_t nout = n * 3 * 1024;
+  int rc = 0;
   if (T->mode == 2) {
     // the NHWC tensor-core engine: forward, loss and backward into T->grads
+    // (it packs its bf16 operands straight from the master parameters)
     double* loss_dev = nullptr;
     rc = tc_step(T, x, y, n, &loss_dev, st);
     // NCCL: the gradients were all-reduced layer by layer inside the step
@@ -845,6 +865,8 @@ extern "C" int drcb_trainer_step(DrcbTrainer* T, const float* x, const float* y,
     }
     return 0;
   }
+  rc = weight_forms(T, st);
+  if (rc) return rc;
   const int k = T->k;
   Work W;
   rc = alloc_work(T, n, W, st);
@@ -983,13 +1005,10 @@ extern "C" int drcb_trainer_step(DrcbTrainer* T, const float* x, const float* y,
 extern "C" int drcb_trainer_apply(DrcbTrainer* T, float grad_scale, void* stream) {
   if (!T) return fail(DRCB_ECONTRACT, "drcb_trainer_apply: null trainer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  T->step += 1;
-  // bias corrections in double on the host, as torch.optim.Adam computes them
-  double bc1 = 1.0 - std::pow(double(T->b1), double(T->step));
-  double bc2 = 1.0 - std::pow(double(T->b2), double(T->step));
-  float step_size = float(double(T->lr) / bc1);
-  k_adam<<<nb(T->n_params), 256, 0, st>>>(T->params, T->grads, T->m, T->v, T->n_params, step_size,
-                                           T->b1, T->b2, T->eps, float(std::sqrt(bc2)), grad_scale);
+  k_adam_coef<<<1, 1, 0, st>>>(T->d_step, T->lr, T->b1, T->b2, T->d_coef);
+  TCHECK("k_adam_coef");
+  k_adam<<<nb(T->n_params), 256, 0, st>>>(T->params, T->grads, T->m, T->v, T->n_params, T->d_coef,
+                                           T->b1, T->b2, T->eps, grad_scale);
   TCHECK("k_adam");
   return 0;
 }

@@ -40,7 +40,8 @@ struct DrcbTrainer {
   float *wf = nullptr, *wt = nullptr;  // conv-form / dgrad-form weights (all layers)
   std::vector<int64_t> wf_off;
   float lr = 1e-4f, b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
-  int64_t step = 0;
+  int64_t* d_step = nullptr;  // Adam step counter (device; graph-replay safe)
+  float* d_coef = nullptr;     // {lr / bc1, sqrt(bc2)} of the current step
   void* comm = nullptr;  // ncclComm_t or NULL
   int world = 1;
   std::vector<void*> allocs;
@@ -61,8 +62,6 @@ namespace train {
 // into T->grads (gradient all-reduce and Adam stay with the caller)
 int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** loss_dev_sum,
             cudaStream_t st);
-// weight-form kernels shared by both engines (drcb_train.cu)
-int weight_forms(DrcbTrainer* T, cudaStream_t st);
 // sum-all-reduce over the data-parallel ranks through the trainer's
 // communicator: the reduction hook if set, else NCCL (no-op for one rank)
 int trainer_allreduce(DrcbTrainer* T, void* buf, size_t count, int is_double, cudaStream_t st);

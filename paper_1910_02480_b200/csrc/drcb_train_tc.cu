@@ -28,7 +28,7 @@ int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int c
                  int out_ctot, int out_coff, const void* wpacked, int cout_pad, const float* ep_a,
                  const float* ep_b, float slope, cudaStream_t st);
 int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, int cout_pad, int hw,
-               int64_t nmaps, float* dwf, void* ws, size_t* ws_bytes, cudaStream_t st);
+               int64_t nmaps, float* dwf, int deconv, void* ws, size_t* ws_bytes, cudaStream_t st);
 
 namespace train {
 
@@ -85,14 +85,51 @@ __global__ void k_x_in(const float* __restrict__ x, int64_t n, int64_t np, bf16*
   st8(out + i * 64, f);
 }
 
-// conv-form fp32 weights [cout][cin][9] -> packed bf16 [coutp][9 * cinp]
-__global__ void k_pack_w(const float* __restrict__ w, int cout, int cin, int cinp, int coutp,
-                         bf16* __restrict__ out) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t kt = int64_t(9) * cinp;
-  if (i >= int64_t(coutp) * kt) return;
-  const int co = int(i / kt), r = int(i % kt), tap = r / cinp, ci = r % cinp;
-  out[i] = __float2bfloat16_rn((co < cout && ci < cin) ? w[(int64_t(co) * cin + ci) * 9 + tap] : 0.f);
+// Every layer's step operands straight from the fp32 master parameters, in
+// one launch (a flat index over the layers' concatenated segments): the
+// forward form wpf[co][tap][ci] (a deconv's weight flipped and transposed,
+// model.py:33-34), the dgrad form wpt[ci][tap][co] = wf[co][ci][8 - tap],
+// both bf16 and zero-padded to 64 channels, and the padded conv bias.
+struct PrepLayer {
+  const float *w, *b;
+  bf16 *wpf, *wpt;
+  float* ep_b;
+  int cin, cout, cinp, coutp, deconv;
+};
+struct PrepArgs {
+  PrepLayer L[16];
+  int64_t start[17];  // segment starts; segment = wpf, wpt, bias
+};
+
+__device__ __forceinline__ float wf_at(const PrepLayer& t, int co, int ci, int tap) {
+  if (co >= t.cout || ci >= t.cin) return 0.f;
+  if (t.deconv) return t.w[(int64_t(ci) * t.cout + co) * 9 + (8 - tap)];
+  return t.w[(int64_t(co) * t.cin + ci) * 9 + tap];
+}
+
+__global__ void k_prep_weights(const __grid_constant__ PrepArgs a) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= a.start[16]) return;
+  int l = 0;
+  while (i >= a.start[l + 1]) ++l;
+  const PrepLayer& t = a.L[l];
+  int64_t j = i - a.start[l];
+  const int64_t nf = int64_t(t.coutp) * 9 * t.cinp;
+  if (j < nf) {
+    const int64_t kt = int64_t(9) * t.cinp;
+    const int co = int(j / kt), r = int(j % kt), tap = r / t.cinp, ci = r % t.cinp;
+    t.wpf[j] = __float2bfloat16_rn(wf_at(t, co, ci, tap));
+    return;
+  }
+  j -= nf;
+  if (j < nf) {
+    const int64_t kt = int64_t(9) * t.coutp;
+    const int ci = int(j / kt), r = int(j % kt), tap = r / t.coutp, co = r % t.coutp;
+    t.wpt[j] = __float2bfloat16_rn(wf_at(t, co, ci, 8 - tap));
+    return;
+  }
+  j -= nf;
+  t.ep_b[j] = j < t.cout ? t.b[j] : 0.f;
 }
 
 // padded epilogue vector: v[c] (or fill when v == NULL) for c < n, 0 beyond
@@ -138,14 +175,21 @@ __device__ __forceinline__ void chan_reduce(int64_t npx, int64_t ppb, int cpad, 
 
 // one warp per slot: lane l adds parts l, l+32, ... in order, then a fixed
 // butterfly combines the lanes (deterministic)
+// Optional fp32 copies of two slot ranges (gradients that are these sums):
+// f0[i] = out[i] and f1[i] = out[cpad + i] for i < c.
 __global__ void k_reduce_parts(const double* __restrict__ part, int nparts, int nslots,
-                               double* __restrict__ out) {
+                               double* __restrict__ out, int c = 0, int cpad = 0,
+                               float* __restrict__ f0 = nullptr, float* __restrict__ f1 = nullptr) {
   const int s = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   if (s >= nslots) return;
   double a = 0.0;
   for (int b = lane; b < nparts; b += 32) a += part[int64_t(s) * nparts + b];
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  if (lane == 0) out[s] = a;
+  if (lane == 0) {
+    out[s] = a;
+    if (f0 && s < c) f0[s] = float(a);
+    if (f1 && s >= cpad && s < cpad + c) f1[s - cpad] = float(a);
+  }
 }
 inline unsigned nb_slots(int nslots) { return unsigned((int64_t(nslots) * 32 + 255) / 256); }
 
@@ -436,13 +480,6 @@ __global__ void __launch_bounds__(256) k_bnb_stats(const bf16* __restrict__ z, c
   chan_reduce<2>(npx, ppb, cpad, part, BnbStatsF{z, da, bnv, cpad, slope});
 }
 
-// bwd finalize: local gamma/beta gradients (before the SyncBN all-reduce)
-__global__ void k_bnb_param(const double* sums, int c, int cpad, float* dgamma, float* dbeta) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= c) return;
-  dbeta[i] = float(sums[i]);
-  dgamma[i] = float(sums[cpad + i]);
-}
 // means of dyb and dyb * xhat over the (global) batch, and gamma * invstd
 __global__ void k_bnb_coef(const double* sums, int c, int cpad, double count, const float* gamma,
                            float* bnv) {
@@ -585,31 +622,11 @@ __global__ void __launch_bounds__(256) k_head(const bf16* __restrict__ a15, cons
   }
 }
 
-__global__ void k_sums_to_float(const double* sums, int c, float* out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < c) out[i] = float(sums[i]);
-}
-
 __global__ void k_head_out(const double* sums, float* gw, float* gb, double* loss) {
   const int i = threadIdx.x;
   if (i == 0) *loss = sums[0];
   if (i < 3) gb[i] = float(sums[1 + i]);
   if (i < 48) gw[i] = float(sums[4 + i]);
-}
-
-// conv-form weight gradient -> parameter layout (deconv: back-transpose + flip)
-__global__ void k_wgrad_to_param(const float* __restrict__ dwf, int cin, int cout, int deconv,
-                                 float* __restrict__ g) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= int64_t(cin) * cout * 9) return;
-  const int kx = int(i % 3), ky = int((i / 3) % 3);
-  const int64_t r = i / 9;
-  const int ci = int(r % cin), co = int(r / cin);
-  const float v = dwf[i];
-  if (deconv)
-    g[((int64_t(ci) * cout + co) * 3 + (2 - ky)) * 3 + (2 - kx)] = v;
-  else
-    g[i] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -640,10 +657,10 @@ struct TcEngine {
   bf16 *wpf[16] = {}, *wpt[16] = {};
   float *ep_one_f[16] = {}, *ep_b[16] = {}, *ep_one_t[16] = {}, *ep_zero[16] = {};
   float* bnv[16] = {};  // per layer: s, t, mean, invstd, m1, m2, coef (7 x cout_pad)
-  float* dwf = nullptr;
   void* ws = nullptr;
   size_t ws_bytes = 0;
   double *part = nullptr, *sums = nullptr, *loss = nullptr;
+  int64_t last_n = 0;  // examples in the last step (the loss normaliser)
   std::vector<void*> allocs;
   ~TcEngine() {
     for (void* p : allocs) cudaFree(p);
@@ -711,20 +728,16 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
       wb += (z + 255) & ~size_t(255);
     }
   }
-  // conv-form gradient scratch, wgrad split-K partials, reduction partials
-  int64_t maxw = 0;
+  // wgrad split-K partials, reduction partials
   size_t wsb = 0;
   for (int l = 0; l < 16; ++l) {
     const TL& t = T->L[l];
-    maxw = std::max<int64_t>(maxw, t.nw);
     size_t q = 0;
     int rc = wgrad_bf16(nullptr, t.cin, E->B[PLAN[l].in].c, nullptr, t.cout, pad64(t.cout), t.hw, np,
-                        nullptr, nullptr, &q, st);
+                        nullptr, 0, nullptr, &q, st);
     if (rc) return rc;
     wsb = std::max(wsb, q);
   }
-  const size_t dwf_off = wb;
-  wb += (size_t(maxw) * 4 + 255) & ~size_t(255);
   const size_t ws_off = wb;
   wb += (wsb + 255) & ~size_t(255);
   const size_t part_off = wb;
@@ -749,7 +762,6 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
     k_pad_vec<<<nbk(coutp), 256, 0, st>>>(nullptr, t.cout, coutp, 1.f, E->ep_one_f[l]);
     k_pad_vec<<<nbk(cinp), 256, 0, st>>>(nullptr, t.cin, cinp, 1.f, E->ep_one_t[l]);
   }
-  E->dwf = reinterpret_cast<float*>(w + dwf_off);
   E->ws = w + ws_off;
   E->ws_bytes = wsb;
   E->part = reinterpret_cast<double*>(w + part_off);
@@ -822,10 +834,10 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   k_bnb_stats<<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], da, coutp, n * hw2, ppb, E->bnv[l],
                                                     T->slope, E->part);
   TC_CHECK("k_bnb_stats");
-  k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
+  // (sums of dyb and dyb * xhat: the local beta and gamma gradients)
+  k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums, t.cout, coutp,
+                                                      T->grads + t.be, T->grads + t.g);
   TC_CHECK("k_reduce_parts");
-  k_bnb_param<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, coutp, T->grads + t.g, T->grads + t.be);
-  TC_CHECK("k_bnb_param");
   int rc = trainer_allreduce(T, E->sums, size_t(2) * coutp, 1, st);  // SyncBN backward
   if (rc) return rc;
   k_bnb_coef<<<nbk(coutp), 256, 0, st>>>(E->sums, t.cout, coutp, double(n) * hw2 * T->world,
@@ -838,10 +850,9 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   k_bnb_apply<<<dim3(gx2, coutp / 64), 256, 0, st>>>(E->Z[l], da, coutp, np * hw2, n * hw2, ppb2,
                                                      E->bnv[l], T->slope, dz, E->part);
   TC_CHECK("k_bnb_apply");
-  k_reduce_parts<<<nb_slots(t.cout), 256, 0, st>>>(E->part, gx2, t.cout, E->sums);
+  k_reduce_parts<<<nb_slots(t.cout), 256, 0, st>>>(E->part, gx2, t.cout, E->sums, t.cout, 0,
+                                                   T->grads + t.b);  // conv bias
   TC_CHECK("k_reduce_parts");
-  k_sums_to_float<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, T->grads + t.b);  // conv bias
-  TC_CHECK("k_sums_to_float");
   // dgrad: the transposed conv of dz into the input-gradient buffer
   if (P.din >= 0) {
     const Buf& din = E->B[P.din];
@@ -852,11 +863,9 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   // wgrad from the layer input and dz (both NHWC, straight from the buffers)
   const Buf& in = E->B[P.in];
   size_t wsb = E->ws_bytes;
-  rc = wgrad_bf16(in.p, t.cin, in.c, dz, t.cout, coutp, t.hw, np, E->dwf, E->ws, &wsb, st);
-  if (rc) return rc;
-  k_wgrad_to_param<<<nbk(t.nw), 256, 0, st>>>(E->dwf, t.cin, t.cout, t.deconv ? 1 : 0, T->grads + t.w);
-  TC_CHECK("k_wgrad_to_param");
-  return 0;
+  // (straight into the parameter layout of T->grads)
+  return wgrad_bf16(in.p, t.cin, in.c, dz, t.cout, coutp, t.hw, np, T->grads + t.w, t.deconv ? 1 : 0,
+                    E->ws, &wsb, st);
 }
 
 int up_bwd(TcEngine* E, int dcat, int c, int hw_in, int dlow, int64_t np, cudaStream_t st) {
@@ -884,18 +893,22 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
   int rc = engine_setup(T, np, st);
   if (rc) return rc;
   TcEngine* E = T->tc;
+  E->last_n = n;
   // packed bf16 operands of this step's weights (forward and dgrad forms)
-  for (int l = 0; l < 16; ++l) {
-    const TL& t = T->L[l];
-    const int cinp = pad64(t.cin), coutp = pad64(t.cout);
-    k_pack_w<<<nbk(int64_t(coutp) * 9 * cinp), 256, 0, st>>>(T->wf + T->wf_off[l], t.cout, t.cin,
-                                                              cinp, coutp, E->wpf[l]);
-    TC_CHECK("k_pack_w");
-    k_pack_w<<<nbk(int64_t(cinp) * 9 * coutp), 256, 0, st>>>(T->wt + T->wf_off[l], t.cin, t.cout,
-                                                              coutp, cinp, E->wpt[l]);
-    TC_CHECK("k_pack_w");
-    k_pad_vec<<<nbk(coutp), 256, 0, st>>>(T->params + t.b, t.cout, coutp, 0.f, E->ep_b[l]);
-    TC_CHECK("k_pad_vec");
+  {
+    PrepArgs a;
+    int64_t tot = 0;
+    for (int l = 0; l < 16; ++l) {
+      const TL& t = T->L[l];
+      const int cinp = pad64(t.cin), coutp = pad64(t.cout);
+      a.L[l] = PrepLayer{T->params + t.w, T->params + t.b, E->wpf[l], E->wpt[l], E->ep_b[l],
+                         t.cin, t.cout, cinp, coutp, t.deconv ? 1 : 0};
+      a.start[l] = tot;
+      tot += 2 * int64_t(coutp) * 9 * cinp + coutp;
+    }
+    a.start[16] = tot;
+    k_prep_weights<<<nbk(tot), 256, 0, st>>>(a);
+    TC_CHECK("k_prep_weights");
   }
   k_x_in<<<nbk(np * 1024), 256, 0, st>>>(x, n, np, E->B[X0].p);
   TC_CHECK("k_x_in");
@@ -959,6 +972,21 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
 
 }  // namespace train
 }  // namespace drcb
+
+// The batch L1 loss of the last tensor-core step (device sum / n*3*1024),
+// read on `stream` (synchronises): the loss of a replayed step graph.
+extern "C" int drcb_trainer_last_loss(DrcbTrainer* T, double* loss, void* stream) {
+  using namespace drcb;
+  if (!T || !loss) return fail(DRCB_ECONTRACT, "drcb_trainer_last_loss: null argument");
+  if (!T->tc || T->tc->last_n < 1)
+    return fail(DRCB_ECONFIG, "drcb_trainer_last_loss: no tensor-core step has run");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double s = 0;
+  DRCB_CUDA(cudaMemcpyAsync(&s, T->tc->loss, sizeof(double), cudaMemcpyDeviceToHost, st));
+  DRCB_CUDA(cudaStreamSynchronize(st));
+  *loss = s / double(T->tc->last_n * 3 * 1024);
+  return 0;
+}
 
 // Test hook: the bf16 pre-BN conv output Z of layer `layer` (0..15) from the
 // last tensor-core step, NHWC (capacity maps, hw, hw, pad64(cout)) -> dst.

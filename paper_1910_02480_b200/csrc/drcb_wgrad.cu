@@ -368,9 +368,17 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// the output element (co, ci, tap): conv form dwf[co][ci][tap], or with
+// `deconv` the ConvTranspose2d parameter layout w[ci][co][8 - tap] (the
+// transposed, flipped conv form; model.py:33-34)
+__device__ __forceinline__ int64_t wg_out(int co, int ci, int tap, int cin, int cout, int deconv) {
+  return deconv ? (int64_t(ci) * cout + co) * 9 + (8 - tap) : (int64_t(co) * cin + ci) * 9 + tap;
+}
+
 // dx-in-N partials -> dwf: unit (output block, input block), acc j, row m
 // (dy of the X block: acc 0 rows -1 / 0, acc 1 row +1), column n (dx, co)
-__global__ void k_wgrad_reduce_dxn(const WgArgs a, int cin, int cout, float* __restrict__ dwf) {
+__global__ void k_wgrad_reduce_dxn(const WgArgs a, int cin, int cout, int deconv,
+                                   float* __restrict__ dwf) {
   const int64_t per = int64_t(2) * 128 * 192;
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= per * a.units) return;
@@ -388,13 +396,13 @@ __global__ void k_wgrad_reduce_dxn(const WgArgs a, int cin, int cout, float* __r
   const float* p = a.partial + int64_t(unit) * per + (int64_t(j) * 128 + m) * 192 + n;
   float s = 0.f;
   for (int k = 0; k < a.splits; ++k) s += p[k * stride];
-  dwf[(int64_t(co) * cin + ci) * 9 + (dy + 1) * 3 + (dx + 1)] = s;
+  dwf[wg_out(co, ci, (dy + 1) * 3 + (dx + 1), cin, cout, deconv)] = s;
 }
 
 // split-K partials -> conv-form fp32 weight gradient dwf[co][ci][tap], summed
 // over the splits in order (deterministic). One thread per (n tile, M tile,
 // row, column) accumulator element.
-__global__ void k_wgrad_reduce(const WgArgs a, int cin, int cout, float* __restrict__ dwf) {
+__global__ void k_wgrad_reduce(const WgArgs a, int cin, int cout, int deconv, float* __restrict__ dwf) {
   const int64_t per_nt = int64_t(a.npairs) * 128 * a.n_tile;
   const int64_t total = per_nt * (int64_t(a.units) / a.groups);
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -414,17 +422,18 @@ __global__ void k_wgrad_reduce(const WgArgs a, int cin, int cout, float* __restr
   const float* p = a.partial + ((int64_t(unit) * a.n_acc + j) * 128 + m) * a.n_tile + n;
   float s = 0.f;
   for (int k = 0; k < a.splits; ++k) s += p[k * stride];
-  dwf[(int64_t(co) * cin + ci) * 9 + tap] = s;
+  dwf[wg_out(co, ci, tap, cin, cout, deconv)] = s;
 }
 
 }  // namespace wg
 
 // Plan + launch the weight gradient of one 3x3 layer. x: NHWC bf16 (nmaps,
 // hw, hw, cin_pad); dz: NHWC bf16 (nmaps, hw, hw, cout_pad); dwf: conv-form
-// fp32 (cout, cin, 3, 3). `ws` / `ws_bytes`: scratch for the split-K partials
-// (query with ws == nullptr: ws_bytes receives the size).
+// fp32 (cout, cin, 3, 3), or with `deconv` the transposed conv's parameter
+// layout (cin, cout, 3, 3) flipped. `ws` / `ws_bytes`: scratch for the
+// split-K partials (query with ws == nullptr: ws_bytes receives the size).
 int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, int cout_pad, int hw,
-               int64_t nmaps, float* dwf, void* ws, size_t* ws_bytes, cudaStream_t st) {
+               int64_t nmaps, float* dwf, int deconv, void* ws, size_t* ws_bytes, cudaStream_t st) {
   using namespace wg;
   if (cin_pad % 64 || cout_pad % 64 || (hw != 4 && hw != 8 && hw != 16 && hw != 32))
     return fail(DRCB_ECONFIG, "wgrad: channels must be padded to 64, hw in {4, 8, 16, 32}");
@@ -488,7 +497,7 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "k_wgrad_dxn");
     const int64_t total = int64_t(2) * 128 * 192 * a.units;
-    k_wgrad_reduce_dxn<<<unsigned((total + 255) / 256), 256, 0, st>>>(a, cin, cout, dwf);
+    k_wgrad_reduce_dxn<<<unsigned((total + 255) / 256), 256, 0, st>>>(a, cin, cout, deconv, dwf);
     count_launch();
     e = cudaGetLastError();
     return e == cudaSuccess ? 0 : cuda_fail(e, "k_wgrad_reduce_dxn");
@@ -511,7 +520,7 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "k_wgrad");
   const int64_t total = int64_t(a.npairs) * 128 * a.n_tile * (cout_pad / a.n_tile);
-  k_wgrad_reduce<<<unsigned((total + 255) / 256), 256, 0, st>>>(a, cin, cout, dwf);
+  k_wgrad_reduce<<<unsigned((total + 255) / 256), 256, 0, st>>>(a, cin, cout, deconv, dwf);
   count_launch();
   e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_wgrad_reduce");
@@ -540,11 +549,11 @@ extern "C" int drcb_debug_wgrad(int32_t cin, int32_t cout, int32_t hw, int64_t n
   cudaMemcpy(dx, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dd, hz.data(), hz.size() * 2, cudaMemcpyHostToDevice);
   size_t wsb = 0;
-  int rc = wgrad_bf16(dx, cin, cinp, dd, cout, coutp, hw, n, dwf, nullptr, &wsb, 0);
+  int rc = wgrad_bf16(dx, cin, cinp, dd, cout, coutp, hw, n, dwf, 0, nullptr, &wsb, 0);
   if (!rc) {
     if (cudaMalloc(&ws, wsb) != cudaSuccess) rc = fail(DRCB_ECUDA, "cudaMalloc wgrad scratch");
   }
-  if (!rc) rc = wgrad_bf16(dx, cin, cinp, dd, cout, coutp, hw, n, dwf, ws, &wsb, 0);
+  if (!rc) rc = wgrad_bf16(dx, cin, cinp, dd, cout, coutp, hw, n, dwf, 0, ws, &wsb, 0);
   if (!rc) {
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) rc = cuda_fail(e, "drcb_debug_wgrad");

@@ -93,6 +93,45 @@ class DeviceTrainer:
                   C.byref(loss) if want_loss else None, int(bool(apply)), _lib.stream_ptr())
         return float(loss.value) if want_loss else None
 
+    def step_graph(self, x, y, want_loss=False):
+        """One full step (apply=True) replayed from a captured CUDA graph —
+        the bf16 engine's ~350 launches per step cost one graph launch, which
+        is what small batches (BASELINE config 5's 64) are bound by. x, y are
+        device fp32 contiguous tensors the caller refills in place; the first
+        call with a new (x, y, n) runs the step eagerly (engine setup) and
+        captures the next one. Bit-identical to step(x, y): same kernels, same
+        order; the Adam step counter is on the device."""
+        import torch
+
+        if self.mode != "bf16":
+            raise ValueError("step_graph needs the bf16 tensor-core engine")
+        if not (x.is_cuda and y.is_cuda and x.dtype == torch.float32 and y.dtype == torch.float32
+                and x.is_contiguous() and y.is_contiguous()):
+            raise ValueError("step_graph takes contiguous float32 CUDA tensors")
+        key = (x.data_ptr(), y.data_ptr(), int(x.shape[0]))
+        if getattr(self, "_graph_key", None) != key:
+            loss = self.step(x, y, apply=True, want_loss=want_loss)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                _lib.call("drcb_trainer_step", self.handle, _lib.ptr(x), _lib.ptr(y),
+                          int(x.shape[0]), None, 1, _lib.stream_ptr())
+            self._graph, self._graph_key = g, key
+            return loss
+        self._graph.replay()
+        return self.last_loss() if want_loss else None
+
+    def steps_taken(self):
+        """Adam steps applied so far (the device counter; synchronises)."""
+        info = (C.c_int64 * 4)()
+        _lib.call("drcb_trainer_info", self.handle, info)
+        return int(info[3])
+
+    def last_loss(self):
+        """The batch L1 loss of the last bf16 step (synchronises)."""
+        loss = C.c_double(0.0)
+        _lib.call("drcb_trainer_last_loss", self.handle, C.byref(loss), _lib.stream_ptr())
+        return float(loss.value)
+
     def debug_z(self, layer):
         """(test hook, bf16 engine) the pre-BN conv output of 3x3 layer
         `layer` (0..15) from the last step, or (16) the head's input
@@ -155,6 +194,7 @@ class DeviceTrainer:
         return load_weights(self.export())
 
     def close(self):
+        self._graph = self._graph_key = None
         if getattr(self, "handle", None) and _lib._lib is not None:
             _lib._lib.drcb_trainer_destroy(self.handle)
             self.handle = None

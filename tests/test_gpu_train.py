@@ -147,3 +147,27 @@ def test_fp32_trainer_is_bit_reproducible():
     ga, gb = a.grads(), b.grads()
     for name in ga:
         assert np.array_equal(ga[name], gb[name]), name
+
+
+def test_bf16_step_graph_replays_the_eager_step():
+    """step_graph (one captured CUDA graph per step, BASELINE config 5's
+    batch 64) gives the eager engine's exact bits: same kernels, same order,
+    the Adam step counter advanced on the device by each replay. The batch is
+    refilled in place between replays."""
+    xs, ys = zip(*(_batch(64, s) for s in range(4)))
+    net = cnn.random_network(64, 6)
+    a = DeviceTrainer(net, lr=1e-3, mode="bf16")
+    b = DeviceTrainer(net, lr=1e-3, mode="bf16")
+    xd = torch.empty((64, 7, 32, 32), device="cuda")
+    yd = torch.empty((64, 3, 32, 32), device="cuda")
+    for x, y in zip(xs, ys):
+        la = a.step(x, y)
+        xd.copy_(x)
+        yd.copy_(y)
+        lb = b.step_graph(xd, yd, want_loss=True)
+        assert la == lb
+    assert b._graph is not None
+    pa, pb = a.params(), b.params()
+    for name in pa:
+        assert np.array_equal(pa[name], pb[name]), name
+    assert a.steps_taken() == b.steps_taken() == 4

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--mode", default="bf16")
+    ap.add_argument("--graph", action="store_true", help="replay a captured step graph")
     args = ap.parse_args()
     import torch
 
@@ -31,18 +32,19 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(3)
     x = torch.rand((args.batch, 7, 32, 32), device="cuda", generator=g)
     y = torch.rand((args.batch, 3, 32, 32), device="cuda", generator=g)
+    step = (lambda: tr.step_graph(x, y)) if args.graph else (lambda: tr.step(x, y, want_loss=False))
     for _ in range(args.warmup):
-        tr.step(x, y, want_loss=False)
+        step()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.iters):
-        tr.step(x, y, want_loss=False)
+        step()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.iters
     tf = args.batch * 3 * cnn.flops_per_map(64) / (ms * 1e-3) / 1e12
-    print(json.dumps({"batch": args.batch, "mode": args.mode, "ms": ms,
+    print(json.dumps({"batch": args.batch, "mode": args.mode, "graph": args.graph, "ms": ms,
                       "samples_per_s": args.batch / ms * 1e3, "tflops": tf}))
 
 
