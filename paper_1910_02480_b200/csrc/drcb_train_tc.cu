@@ -86,10 +86,12 @@ __global__ void k_x_in(const float* __restrict__ x, int64_t n, int64_t np, bf16*
 }
 
 // Every layer's step operands straight from the fp32 master parameters, in
-// one launch (a flat index over the layers' concatenated segments): the
-// forward form wpf[co][tap][ci] (a deconv's weight flipped and transposed,
-// model.py:33-34), the dgrad form wpt[ci][tap][co] = wf[co][ci][8 - tap],
-// both bf16 and zero-padded to 64 channels, and the padded conv bias.
+// one launch: the forward form wpf[co][tap][ci] (a deconv's weight flipped
+// and transposed, model.py:33-34), the dgrad form wpt[ci][tap][co] =
+// wf[co][ci][8 - tap], both bf16 and zero-padded to 64 channels, and the
+// padded conv bias. One thread per (layer, form, output row, input channel)
+// moves the 9 taps; the fastest index is the packed layout's contiguous one
+// so the 2-byte stores coalesce (the 36-byte tap runs are read whole).
 struct PrepLayer {
   const float *w, *b;
   bf16 *wpf, *wpt;
@@ -98,14 +100,8 @@ struct PrepLayer {
 };
 struct PrepArgs {
   PrepLayer L[16];
-  int64_t start[17];  // segment starts; segment = wpf, wpt, bias
+  int64_t start[17];  // thread-segment starts; segment = wpf rows, wpt rows, bias
 };
-
-__device__ __forceinline__ float wf_at(const PrepLayer& t, int co, int ci, int tap) {
-  if (co >= t.cout || ci >= t.cin) return 0.f;
-  if (t.deconv) return t.w[(int64_t(ci) * t.cout + co) * 9 + (8 - tap)];
-  return t.w[(int64_t(co) * t.cin + ci) * 9 + tap];
-}
 
 __global__ void k_prep_weights(const __grid_constant__ PrepArgs a) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -114,21 +110,37 @@ __global__ void k_prep_weights(const __grid_constant__ PrepArgs a) {
   while (i >= a.start[l + 1]) ++l;
   const PrepLayer& t = a.L[l];
   int64_t j = i - a.start[l];
-  const int64_t nf = int64_t(t.coutp) * 9 * t.cinp;
-  if (j < nf) {
-    const int64_t kt = int64_t(9) * t.cinp;
-    const int co = int(j / kt), r = int(j % kt), tap = r / t.cinp, ci = r % t.cinp;
-    t.wpf[j] = __float2bfloat16_rn(wf_at(t, co, ci, tap));
+  const int64_t nf = int64_t(t.coutp) * t.cinp;
+  if (j < 2 * nf) {
+    const bool fwd = j < nf;
+    if (!fwd) j -= nf;
+    // forward rows: (co, ci) ci fastest; dgrad rows: (ci, co) co fastest
+    const int inner = fwd ? t.cinp : t.coutp;
+    const int r = int(j / inner), c = int(j % inner);
+    const int co = fwd ? r : c, ci = fwd ? c : r;
+    float v[9];
+    if (co < t.cout && ci < t.cin) {
+      // wf[co][ci][tap]: conv w[co][ci][tap], deconv w[ci][co][8 - tap]
+      const float* src = t.deconv ? t.w + (int64_t(ci) * t.cout + co) * 9
+                                  : t.w + (int64_t(co) * t.cin + ci) * 9;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) v[k] = src[t.deconv ? 8 - k : k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) v[k] = 0.f;
+    }
+    if (fwd) {
+      bf16* dst = t.wpf + int64_t(co) * 9 * t.cinp + ci;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) dst[int64_t(k) * t.cinp] = __float2bfloat16_rn(v[k]);
+    } else {
+      bf16* dst = t.wpt + int64_t(ci) * 9 * t.coutp + co;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) dst[int64_t(k) * t.coutp] = __float2bfloat16_rn(v[8 - k]);
+    }
     return;
   }
-  j -= nf;
-  if (j < nf) {
-    const int64_t kt = int64_t(9) * t.coutp;
-    const int ci = int(j / kt), r = int(j % kt), tap = r / t.coutp, co = r % t.coutp;
-    t.wpt[j] = __float2bfloat16_rn(wf_at(t, co, ci, 8 - tap));
-    return;
-  }
-  j -= nf;
+  j -= 2 * nf;
   t.ep_b[j] = j < t.cout ? t.b[j] : 0.f;
 }
 
@@ -220,21 +232,72 @@ __global__ void __launch_bounds__(256) k_bn_stats(const bf16* __restrict__ z, in
 // BN finalize (torch BatchNorm2d train mode: biased variance normalises,
 // unbiased variance updates the running estimate, momentum 0.1):
 // y = z * s + t with s = gamma * invstd, t = beta - mean * s
-__global__ void k_bn_fin(const double* sums, int c, int cpad, double count, const float* gamma,
-                         const float* beta, float* rm, float* rv, float* bnv) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= c) return;
-  double mu = sums[i] / count;
-  double var = sums[cpad + i] / count - mu * mu;
-  if (var < 0) var = 0;
-  const float invstd = float(1.0 / sqrt(var + double(EPS)));
-  const float s = gamma[i] * invstd;
-  bnv[i] = s;                           // scale
-  bnv[cpad + i] = beta[i] - float(mu) * s;  // shift
-  bnv[2 * cpad + i] = float(mu);        // mean
-  bnv[3 * cpad + i] = invstd;           // invstd
-  rm[i] = (1.f - MOMENTUM) * rm[i] + MOMENTUM * float(mu);
-  rv[i] = (1.f - MOMENTUM) * rv[i] + MOMENTUM * float(var * count / (count - 1.0));
+struct BnFin {  // forward: batch mean / invstd -> scale, shift, running stats
+  int c, cpad;
+  double count;
+  const float *gamma, *beta;
+  float *rm, *rv, *bnv;
+  __device__ void operator()(int i, double s0, double s1) const {
+    if (i >= c) return;
+    double mu = s0 / count;
+    double var = s1 / count - mu * mu;
+    if (var < 0) var = 0;
+    const float invstd = float(1.0 / sqrt(var + double(EPS)));
+    const float s = gamma[i] * invstd;
+    bnv[i] = s;                               // scale
+    bnv[cpad + i] = beta[i] - float(mu) * s;  // shift
+    bnv[2 * cpad + i] = float(mu);            // mean
+    bnv[3 * cpad + i] = invstd;               // invstd
+    rm[i] = (1.f - MOMENTUM) * rm[i] + MOMENTUM * float(mu);
+    rv[i] = (1.f - MOMENTUM) * rv[i] + MOMENTUM * float(var * count / (count - 1.0));
+  }
+};
+
+// backward: means of dyb and dyb * xhat over the (global) batch, and
+// gamma * invstd; with `dbeta` set (one rank: the sums are already the
+// batch's) also the beta / gamma gradients
+struct BnbCoef {
+  int c, cpad;
+  double count;
+  const float* gamma;
+  float* bnv;
+  float *dbeta, *dgamma;
+  __device__ void operator()(int i, double s0, double s1) const {
+    const bool real = i < c;
+    if (real && dbeta) {
+      dbeta[i] = float(s0);
+      dgamma[i] = float(s1);
+    }
+    bnv[4 * cpad + i] = real ? float(s0 / count) : 0.f;              // m1
+    bnv[5 * cpad + i] = real ? float(s1 / count) : 0.f;              // m2
+    bnv[6 * cpad + i] = real ? gamma[i] * bnv[3 * cpad + i] : 0.f;  // gamma * invstd
+  }
+};
+
+// finalise from all-reduced sums (sum slot i, square/product slot cpad + i)
+template <class F>
+__global__ void k_fin(const double* sums, int n, F f) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f(i, sums[i], sums[f.cpad + i]);
+}
+
+// one rank (nothing to all-reduce): the partial reduction and the
+// finalisation in one launch, a warp per channel, partials summed in block
+// order exactly as k_reduce_parts does
+template <class F>
+__global__ void k_reduce_fin(const double* __restrict__ part, int nparts, int n, F f) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
+  if (i >= n) return;
+  double a = 0.0, b = 0.0;
+  for (int k = lane; k < nparts; k += 32) {
+    a += part[int64_t(i) * nparts + k];
+    b += part[int64_t(f.cpad + i) * nparts + k];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) f(i, a, b);
 }
 
 // Elementwise NHWC kernels: one thread per (pixel, 8-channel group); every
@@ -480,16 +543,6 @@ __global__ void __launch_bounds__(256) k_bnb_stats(const bf16* __restrict__ z, c
   chan_reduce<2>(npx, ppb, cpad, part, BnbStatsF{z, da, bnv, cpad, slope});
 }
 
-// means of dyb and dyb * xhat over the (global) batch, and gamma * invstd
-__global__ void k_bnb_coef(const double* sums, int c, int cpad, double count, const float* gamma,
-                           float* bnv) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= cpad) return;
-  const bool real = i < c;
-  bnv[4 * cpad + i] = real ? float(sums[i] / count) : 0.f;          // m1
-  bnv[5 * cpad + i] = real ? float(sums[cpad + i] / count) : 0.f;   // m2
-  bnv[6 * cpad + i] = real ? gamma[i] * bnv[3 * cpad + i] : 0.f;    // gamma * invstd
-}
 
 // pass 2: dz = gamma * invstd * (dyb - m1 - xhat * m2) (zero beyond n maps
 // and in padded channels), plus per-block partial sums of dz (bias gradient)
@@ -779,6 +832,9 @@ inline void red_geom(int64_t npx, int ctiles, int64_t& ppb, int& gx) {
   gx = int((npx + ppb - 1) / ppb);
 }
 
+// nothing to all-reduce: the SyncBN sums are already the batch's
+inline bool one_rank(const DrcbTrainer* T) { return !T->reduce_fn && T->world == 1; }
+
 int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   TcEngine* E = T->tc;
   const TL& t = T->L[l];
@@ -793,14 +849,19 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   red_geom(n * hw2, coutp / 64, ppb, gx);
   k_bn_stats<<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], coutp, n * hw2, ppb, E->part);
   TC_CHECK("k_bn_stats");
-  k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
-  TC_CHECK("k_reduce_parts");
-  rc = trainer_allreduce(T, E->sums, size_t(2) * coutp, 1, st);  // SyncBN
-  if (rc) return rc;
-  k_bn_fin<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, coutp, double(n) * hw2 * T->world,
-                                         T->params + t.g, T->params + t.be, T->running + t.rm,
-                                         T->running + t.rv, E->bnv[l]);
-  TC_CHECK("k_bn_fin");
+  const BnFin fin{t.cout,           coutp,       double(n) * hw2 * T->world, T->params + t.g,
+                  T->params + t.be, T->running + t.rm, T->running + t.rv,  E->bnv[l]};
+  if (one_rank(T)) {
+    k_reduce_fin<<<nb_slots(t.cout), 256, 0, st>>>(E->part, gx, t.cout, fin);
+    TC_CHECK("k_reduce_fin");
+  } else {
+    k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
+    TC_CHECK("k_reduce_parts");
+    rc = trainer_allreduce(T, E->sums, size_t(2) * coutp, 1, st);  // SyncBN
+    if (rc) return rc;
+    k_fin<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, fin);
+    TC_CHECK("k_fin");
+  }
   const Buf& out = E->B[P.out];
   if (P.pool >= 0) {
     const int64_t tot = np * (hw2 / 4) * (coutp / 8);
@@ -835,14 +896,22 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
                                                     T->slope, E->part);
   TC_CHECK("k_bnb_stats");
   // (sums of dyb and dyb * xhat: the local beta and gamma gradients)
-  k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums, t.cout, coutp,
-                                                      T->grads + t.be, T->grads + t.g);
-  TC_CHECK("k_reduce_parts");
-  int rc = trainer_allreduce(T, E->sums, size_t(2) * coutp, 1, st);  // SyncBN backward
-  if (rc) return rc;
-  k_bnb_coef<<<nbk(coutp), 256, 0, st>>>(E->sums, t.cout, coutp, double(n) * hw2 * T->world,
-                                          T->params + t.g, E->bnv[l]);
-  TC_CHECK("k_bnb_coef");
+  BnbCoef coef{t.cout, coutp, double(n) * hw2 * T->world, T->params + t.g, E->bnv[l],
+               T->grads + t.be, T->grads + t.g};
+  int rc = 0;
+  if (one_rank(T)) {
+    k_reduce_fin<<<nb_slots(coutp), 256, 0, st>>>(E->part, gx, coutp, coef);
+    TC_CHECK("k_reduce_fin");
+  } else {
+    k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums, t.cout,
+                                                        coutp, T->grads + t.be, T->grads + t.g);
+    TC_CHECK("k_reduce_parts");
+    rc = trainer_allreduce(T, E->sums, size_t(2) * coutp, 1, st);  // SyncBN backward
+    if (rc) return rc;
+    coef.dbeta = coef.dgamma = nullptr;  // (written above from the local sums)
+    k_fin<<<nbk(coutp), 256, 0, st>>>(E->sums, coutp, coef);
+    TC_CHECK("k_fin");
+  }
   int64_t ppb2;
   int gx2;
   red_geom(np * hw2, coutp / 64, ppb2, gx2);
@@ -904,7 +973,7 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
       a.L[l] = PrepLayer{T->params + t.w, T->params + t.b, E->wpf[l], E->wpt[l], E->ep_b[l],
                          t.cin, t.cout, cinp, coutp, t.deconv ? 1 : 0};
       a.start[l] = tot;
-      tot += 2 * int64_t(coutp) * 9 * cinp + coutp;
+      tot += 2 * int64_t(coutp) * cinp + coutp;
     }
     a.start[16] = tot;
     k_prep_weights<<<nbk(tot), 256, 0, st>>>(a);

@@ -468,7 +468,15 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
     a.chunks = int(nmaps / a.mb);
   }
   const int nsm = sm_count();
-  a.splits = std::max(1, std::min(a.chunks, (2 * nsm + a.units - 1) / a.units));
+  // split-K over the pixel chunks: two CTAs per SM, but at least
+  // `min_chunks` chunks per split (small batches: fewer, longer splits beat
+  // a partial buffer the reduction then has to stream)
+  static const int min_chunks = [] {
+    const char* e = getenv("DRCB_WGRAD_MINCHUNKS");
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
+  a.splits = std::max(1, std::min((a.chunks + min_chunks - 1) / min_chunks,
+                                  (2 * nsm + a.units - 1) / a.units));
   const size_t part = dxn ? size_t(a.splits) * a.units * 2 * 128 * 192 * 4
                           : size_t(a.splits) * a.units * a.n_acc * 128 * a.n_tile * 4;
   if (!ws) {
