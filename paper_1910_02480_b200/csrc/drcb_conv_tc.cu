@@ -2536,6 +2536,14 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     a.bn = n_tile(L.cout_pad, 256);
     a.num_n_tiles = L.cout_pad / a.bn;
   }
+  // few M tiles (small batches of the 4x4 / 8x8 layers): narrower N tiles
+  // until the work tiles cover the SMs; each output's K order is unchanged
+  // (same bits), the A tiles are re-read per N tile from L2
+  static const bool no_nsplit = getenv("DRCB_NO_NSPLIT") != nullptr;
+  if (!pred && !no_nsplit) {
+    while (a.bn > 64 && int64_t(a.num_m_tiles) * (L.cout_pad / a.bn) < sm_count()) a.bn /= 2;
+    a.num_n_tiles = L.cout_pad / a.bn;
+  }
   int box_w = hw, box_h = a.maps_per_tile == 1 ? a.rows_per_tile : hw, box_n = a.maps_per_tile;
   rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, box_w, box_h, box_n);
   if (rc) return rc;
