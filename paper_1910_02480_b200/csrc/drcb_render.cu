@@ -1110,6 +1110,7 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
   if (!grid) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_paths<R>, MAP_TPB, 0);
+    if (const char* e = getenv("DRCB_MAP_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     grid = sm_count() * (per_sm > 0 ? per_sm : 1);
     grid_dev[dev & 63].store(grid, std::memory_order_relaxed);
   }
