@@ -385,31 +385,46 @@ __device__ __forceinline__ void up_src(int o, int n, int& i0, int& i1, float& fr
     fr = 0.75f;
   }
 }
+// one thread = two horizontally adjacent outputs (2k, 2k + 1) of one output
+// row and 8 channels: they share the source columns k - 1, k, k + 1, so six
+// 16-byte loads serve two outputs (eight before)
 __global__ void __launch_bounds__(256) k_up_fwd(const bf16* __restrict__ in, int c, int hw_in, int np,
                                                 bf16* __restrict__ out, int c_tot) {
-  const int lg = ilog2(c / 8), lho = ilog2(2 * hw_in), ho = 2 * hw_in;
+  const int lg = ilog2(c / 8), lhi = ilog2(hw_in), lho = lhi + 1, ho = 2 * hw_in;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (np << (2 * lho + lg))) return;
+  if (i >= (np << (lho + lhi + lg))) return;
   const int c0 = (i & ((1 << lg) - 1)) * 8;
-  const int op = i >> lg;
-  const int ox = op & (ho - 1), oy = (op >> lho) & (ho - 1), m = op >> (2 * lho);
-  int r0, r1, q0, q1;
-  float fr, fc;
+  const int rest = i >> lg;
+  const int k = rest & (hw_in - 1), oy = (rest >> lhi) & (ho - 1), m = rest >> (lhi + lho);
+  int r0, r1;
+  float fr;
   up_src(oy, hw_in, r0, r1, fr);
-  up_src(ox, hw_in, q0, q1, fc);
+  const int kl = k > 0 ? k - 1 : 0, kr = min(k + 1, hw_in - 1);
   const bf16* b = in + int64_t(m) * hw_in * hw_in * c + c0;
-  float a00[8], a01[8], a10[8], a11[8], v[8];
-  ld8(b + (r0 * hw_in + q0) * c, a00);
-  ld8(b + (r0 * hw_in + q1) * c, a01);
-  ld8(b + (r1 * hw_in + q0) * c, a10);
-  ld8(b + (r1 * hw_in + q1) * c, a11);
+  float l0[8], l1[8], m0[8], m1[8], h0[8], h1[8];  // (row r0 / r1) x (col kl / k / kr)
+  ld8(b + (r0 * hw_in + kl) * c, l0);
+  ld8(b + (r1 * hw_in + kl) * c, l1);
+  ld8(b + (r0 * hw_in + k) * c, m0);
+  ld8(b + (r1 * hw_in + k) * c, m1);
+  ld8(b + (r0 * hw_in + kr) * c, h0);
+  ld8(b + (r1 * hw_in + kr) * c, h1);
+  // output 2k: columns (k-1, k) at 0.75, or (0, min(1, n-1)) at 0 on the
+  // left border; output 2k+1: columns (k, min(k+1, n-1)) at 0.25
+  const bool left = k == 0;
+  const float fe = left ? 0.f : 0.75f;
+  float ve[8], vo[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const float t0 = a00[j] * (1.f - fr) + a10[j] * fr;
-    const float t1 = a01[j] * (1.f - fr) + a11[j] * fr;
-    v[j] = t0 * (1.f - fc) + t1 * fc;
+    const float tm = m0[j] * (1.f - fr) + m1[j] * fr;
+    const float th = h0[j] * (1.f - fr) + h1[j] * fr;
+    const float tl = l0[j] * (1.f - fr) + l1[j] * fr;
+    const float e0 = left ? tm : tl, e1 = left ? th : tm;
+    ve[j] = e0 * (1.f - fe) + e1 * fe;
+    vo[j] = tm * (1.f - 0.25f) + th * 0.25f;
   }
-  st8(out + int64_t(op) * c_tot + c0, v);
+  bf16* o = out + (int64_t(m) * ho * ho + int64_t(oy) * ho + 2 * k) * c_tot + c0;
+  st8(o, ve);
+  st8(o + c_tot, vo);
 }
 
 // adjoint of the upsample: low index i receives from outputs 2i-1 .. 2i+2
@@ -443,19 +458,27 @@ __global__ void __launch_bounds__(256) k_up_bwd(const bf16* __restrict__ dhigh, 
   float wy[4], wx[4];
   up_adj(y, hw_in, oy, wy);
   up_adj(x, hw_in, ox, wx);
+  // taps outside the map carry weight 0: clamp their index and load anyway,
+  // so every thread issues its loads back to back
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    if (oy[a] < 0 || oy[a] >= ho) wy[a] = 0.f;
+    if (ox[a] < 0 || ox[a] >= ho) wx[a] = 0.f;
+    oy[a] = min(max(oy[a], 0), ho - 1);
+    ox[a] = min(max(ox[a], 0), ho - 1);
+  }
   float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const bf16* base = dhigh + int64_t(m) * ho * ho * c_tot + c0;
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    if (wy[a] == 0.f || oy[a] < 0 || oy[a] >= ho) continue;
+    float d[4][8];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) ld8(base + int64_t(oy[a] * ho + ox[b]) * c_tot, d[b]);
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      if (wx[b] == 0.f || ox[b] < 0 || ox[b] >= ho) continue;
-      float d[8];
-      ld8(base + int64_t(oy[a] * ho + ox[b]) * c_tot, d);
       const float w = wy[a] * wx[b];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) s[j] = fmaf(w, d[j], s[j]);
+      for (int j = 0; j < 8; ++j) s[j] = fmaf(w, d[b][j], s[j]);
     }
   }
   st8(dlow + int64_t(lp) * c + c0, s);
@@ -876,7 +899,7 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   }
   if (P.up >= 0) {
     const Buf& cat = E->B[P.up];
-    const int64_t tot = np * 4 * hw2 * (coutp / 8);
+    const int64_t tot = np * 2 * hw2 * (coutp / 8);  // two outputs per thread
     k_up_fwd<<<nbk(tot), 256, 0, st>>>(out.p, coutp, t.hw, np, cat.p, cat.c);
     TC_CHECK("k_up_fwd");
   }
