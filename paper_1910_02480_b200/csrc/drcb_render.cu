@@ -1109,6 +1109,10 @@ int launch_render_stacks(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
   int grid = grid_dev[dev & 63].load(std::memory_order_relaxed);
   if (!grid) {
     int per_sm = 0;
+    // the casting kernels use no shared memory and live on L1 hits: ask for
+    // the largest L1 (maps 3.58 ms at 0 % shared, 3.71 at 50 %, 4.27 at 100 %)
+    cudaFuncSetAttribute(k_map_paths<R>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    cudaFuncSetAttribute(k_gbuffer_direct1<R>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_map_paths<R>, MAP_TPB, 0);
     if (const char* e = getenv("DRCB_MAP_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     grid = sm_count() * (per_sm > 0 ? per_sm : 1);
