@@ -20,6 +20,7 @@ extrapolates frames/s.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -274,6 +275,116 @@ def train_throughput(cnn, world=1, batches=(64, 256, 1024), global_batch=4096, s
         tr.close()
         if comm is not None:
             comm.close()
+    return out
+
+
+class _Sampler:  # the oracle's sampler argument (kind, spp, seed)
+    def __init__(self, kind="independent", spp=1, seed=0):
+        self.kind, self.spp, self.seed = kind, spp, seed
+
+
+def next_rows(scene, cam, cpu=True, spp=4, grid=(8, 8), ref_spp=256):
+    """SURVEY §8(f) rows beside the headline (rank 0, one GPU): f2 render(mode="pt")
+    frames/s at config 3's scene and camera (fp32 rays, `spp` paths per pixel,
+    depth 8, RR from 5; CUDA events around drcb_render_pt), and f1 reference-mode
+    dataset generation (dataset.generate_examples, `grid` points at `ref_spp`,
+    wall clock through the public API). With `cpu`, the oracle's path tracer on
+    the host cores over a bounded sample (camera paths; one reference map)."""
+    import ctypes as C
+    import math
+
+    import torch
+
+    from paper_1910_02480_b200 import _lib, dataset, render
+    from paper_1910_02480_b200.scene import device_scene
+
+    out = {}
+    w, h = cam.resolution
+    rc = render.RenderConfig(spp=spp, max_path_depth=8, rr_start=5, seed=0, precision=32)
+    cs = render._cfg_struct(rc, 32)
+    cs.direct_spp = spp
+    ds = device_scene(scene)
+    img = torch.empty((h, w, 3), dtype=torch.float32, device="cuda")
+    nf = torch.zeros(1, dtype=torch.int64, device="cuda")
+    camst = render.camera_struct(cam)
+
+    def pt():
+        _lib.call("drcb_render_pt", ds.handle, C.byref(camst), C.byref(cs), _lib.ptr(img),
+                  _lib.ptr(nf), _lib.stream_ptr())
+
+    pt()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        pt()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 3
+    paths = w * h * spp
+    out["pt"] = {"what": f"render(mode='pt') {w}x{h}, {spp} spp, depth 8 (f2)", "ms_per_frame": ms,
+                 "frames_per_s": 1e3 / ms, "mpaths_per_s": paths / ms / 1e3}
+    sc = dataclasses.replace(scene, camera=cam) if dataclasses.is_dataclass(scene) else scene
+    dataset.generate_examples(sc, (1, 1), ref_spp, seed=0, precision=32)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ex = dataset.generate_examples(sc, grid, ref_spp, seed=0, precision=32)
+    dt = time.perf_counter() - t0
+    out["dataset"] = {"what": f"generate_examples grid {grid[0]}x{grid[1]}, ref_spp {ref_spp}, "
+                              f"fp32 (f1; through the public API, one read-back per call)",
+                      "examples": len(ex), "seconds": dt, "examples_per_s": len(ex) / dt,
+                      "mpaths_per_s": len(ex) * 1024 * ref_spp / dt / 1e6}
+    if cpu:
+        from oracle import oracle as O
+
+        O.set_threads(os.cpu_count() or 1)
+        osc = O.OracleScene(scene)
+        f, r, u = cam.basis()
+        th = math.tan(math.radians(cam.fov) * 0.5)
+        n = 8192
+        ys = np.full(n, h // 2, dtype=np.int64)
+        xs = np.arange(n, dtype=np.int64) % w
+        ndc_x = ((xs + 0.5) / w * 2.0 - 1.0) * th * (w / h)
+        ndc_y = (1.0 - (ys + 0.5) / h * 2.0) * th
+        d = np.asarray(f) + ndc_x[:, None] * np.asarray(r) + ndc_y[:, None] * np.asarray(u)
+        d /= np.linalg.norm(d, axis=-1, keepdims=True)
+        o = np.broadcast_to(np.asarray(cam.position, dtype=np.float64), d.shape)
+        t0 = time.perf_counter()
+        O.trace_radiance_batch(osc, o, d, (ys * w + xs).astype(np.uint64), np.zeros(n, np.uint64),
+                               _Sampler(), 8, False, 5)
+        cpu_pps = n / (time.perf_counter() - t0)
+        out["pt"]["cpu_oracle"] = {"paths_per_s": cpu_pps, "cores": os.cpu_count() or 1,
+                                   "frames_per_s": cpu_pps / paths,
+                                   "sample": f"{n} camera paths of the frame's middle rows"}
+        out["pt"]["vs_cpu_oracle"] = out["pt"]["frames_per_s"] / (cpu_pps / paths)
+        # one reference map (1,024 texels x ref_spp paths) on the oracle
+        geo = render.primary_chain_batch(scene, np.asarray(cam.position, np.float64)[None],
+                                         d[w // 2][None], precision=64)
+        if geo["found"][0]:
+            pos, nrm = geo["position"][0], geo["normal"][0]
+            tex = np.arange(1024)
+            phi = 2 * np.pi * ((tex % 32) + 0.5) / 32
+            theta = 0.5 * np.pi * ((tex // 32) + 0.5) / 32
+            loc = np.stack([np.sin(theta) * np.cos(phi), np.sin(theta) * np.sin(phi), np.cos(theta)], 1)
+            a = np.array([0.0, 1.0, 0.0]) if abs(nrm[1]) < 0.9 else np.array([1.0, 0.0, 0.0])
+            t_ = np.cross(a, nrm)
+            t_ /= np.linalg.norm(t_)
+            b_ = np.cross(nrm, t_)
+            dirs = loc[:, :1] * t_ + loc[:, 1:2] * b_ + loc[:, 2:] * nrm
+            k = 64  # a bounded share of the ref_spp paths per texel, scaled below
+            oo = np.repeat(pos[None] + 1e-4 * nrm, 1024 * k, 0)
+            dd = np.repeat(dirs, k, 0)
+            t0 = time.perf_counter()
+            O.trace_radiance_batch(osc, oo, dd, np.repeat(tex, k).astype(np.uint64),
+                                   np.tile(np.arange(k), 1024).astype(np.uint64),
+                                   _Sampler(spp=k), 8, True, 5)
+            per_ex = (time.perf_counter() - t0) * ref_spp / k
+            out["dataset"]["cpu_oracle"] = {"seconds_per_example": per_ex,
+                                            "examples_per_s": 1.0 / per_ex,
+                                            "cores": os.cpu_count() or 1,
+                                            "sample": f"1024 texels x {k} of {ref_spp} paths of one "
+                                                      f"reference map, scaled"}
+            out["dataset"]["vs_cpu_oracle"] = out["dataset"]["examples_per_s"] * per_ex
     return out
 
 
@@ -715,6 +826,11 @@ def main():
     except Exception as e:  # secondary figure; never breaks the GPU line
         secondary["network_modes_4096_maps"] = {"error": repr(e)}
     if not args.no_secondary:
+        if world <= 1:
+            try:
+                secondary["next_rows_c3"] = next_rows(scene, cams[0], cpu=not args.no_cpu_baseline)
+            except Exception as e:  # secondary figure; never breaks the GPU line
+                secondary["next_rows_c3"] = {"error": repr(e)}
         for key, c_, tk in (("c4_1080p", "c4", 1), ("c3_tasks16", "c3", 16)):
             try:
                 secondary[key] = secondary_frames(c_, tk, 8 if c_ == "c4" else 1, rank,

@@ -509,46 +509,53 @@ __global__ void __launch_bounds__(TPB) k_pt_frame(DevScene S, DevCamera C, DrcbR
 }
 
 // _reference_map (dataset.py:107-127): ref_spp paths per texel of one cache
-// point (pixel key = texel + key * 4096, sample key = s), skip first emission;
-// one thread per (texel, 16-sample chunk) writes the chunk's sequential sum.
+// point (pixel key = texel + key * 4096, sample key = s), skip first emission.
+// One thread per path (sample s, texel) of a group of samples writes its
+// radiance; the reduction then adds them in the reference's order.
 template <typename R>
-__global__ void __launch_bounds__(TPB) k_reference_chunks(DevScene S, DrcbRenderCfg cfg,
-                                                           const R* __restrict__ pos,
-                                                           const R* __restrict__ nrm,
-                                                           uint64_t key, int ref_spp, int chunk,
-                                                           int nchunks, R* partial,
-                                                           int64_t* nonfinite) {
+__global__ void __launch_bounds__(TPB) k_reference_paths(DevScene S, DrcbRenderCfg cfg,
+                                                          const R* __restrict__ pos,
+                                                          const R* __restrict__ nrm,
+                                                          uint64_t key, int ref_spp, int s_begin,
+                                                          int s_count, R* paths,
+                                                          int64_t* nonfinite) {
   int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   int nf = 0;
-  if (g < int64_t(nchunks) * MAP_TEXELS) {
-    int tex = int(g % MAP_TEXELS), c = int(g / MAP_TEXELS);
+  if (g < int64_t(s_count) * MAP_TEXELS) {
+    const int tex = int(g % MAP_TEXELS), s = s_begin + int(g / MAP_TEXELS);
     V3<R> hp = ldr3(pos), hn = ldr3(nrm);
     Frame<R> fr = frame_scalar(S, hn);
     V3<R> D = fr.to_world(texel_local<R>(tex % MAP_RES, tex / MAP_RES));
     V3<R> O = hp + R(T_EPS) * hn;
     uint64_t pix = uint64_t(tex) + key * uint64_t(1 << 12);
-    int s0 = c * chunk, ns = min(chunk, ref_spp - s0);
     PathRng rng;
-    V3<R> part = {R(0), R(0), R(0)};
-    for (int s = s0; s < s0 + ns; ++s) {
-      rng.init(cfg.seed, pix, uint64_t(s), cfg.sampler_kind, uint32_t(ref_spp > 1 ? ref_spp : 1));
-      V3<R> l = trace_path<R>(S, O, D, rng, cfg.max_path_depth, true, cfg.rr_start, nullptr, nf);
-      part = (s == s0) ? l : part + l;
-    }
-    st3(partial + 3 * g, part);
+    rng.init(cfg.seed, pix, uint64_t(s), cfg.sampler_kind, uint32_t(ref_spp > 1 ? ref_spp : 1));
+    st3(paths + 3 * g, trace_path<R>(S, O, D, rng, cfg.max_path_depth, true, cfg.rr_start, nullptr, nf));
   }
   if (nonfinite) add_nonfinite(nonfinite, nf);
 }
 
-// total = ((0 + chunk_0) + chunk_1) + ... ; map = total / ref_spp
+// the reference's sums: per chunk of `chunk` samples the sequential sum
+// (numpy's axis-0 sum), total = ((0 + chunk_0) + chunk_1) + ...; the group's
+// chunks [c_begin, c_end) continue `tot`; the last group writes total / ref_spp
 template <typename R>
-__global__ void k_reference_reduce(const R* __restrict__ partial, int nchunks, int ref_spp,
-                                   R* out) {
+__global__ void k_reference_reduce(const R* __restrict__ paths, int s_begin, int chunk,
+                                   int c_begin, int c_end, int ref_spp, R* tot_buf, R* out,
+                                   int last) {
   int tex = blockIdx.x * blockDim.x + threadIdx.x;
   if (tex >= MAP_TEXELS) return;
-  V3<R> tot = {R(0), R(0), R(0)};
-  for (int c = 0; c < nchunks; ++c) tot = tot + ldr3(partial + 3 * (int64_t(c) * MAP_TEXELS + tex));
-  st3(out + 3 * tex, divs(tot, R(ref_spp)));
+  V3<R> tot = c_begin == 0 ? mk<R>(R(0), R(0), R(0)) : ldr3(tot_buf + 3 * tex);
+  for (int c = c_begin; c < c_end; ++c) {
+    const int s0 = c * chunk, ns = min(chunk, ref_spp - s0);
+    V3<R> part = ldr3(paths + 3 * (int64_t(s0 - s_begin) * MAP_TEXELS + tex));
+    for (int s = s0 + 1; s < s0 + ns; ++s)
+      part = part + ldr3(paths + 3 * (int64_t(s - s_begin) * MAP_TEXELS + tex));
+    tot = tot + part;
+  }
+  if (last)
+    st3(out + 3 * tex, divs(tot, R(ref_spp)));
+  else
+    st3(tot_buf + 3 * tex, tot);
 }
 
 // numpy pairwise summation of 1024 contiguous values (8-accumulator blocks of
@@ -1197,14 +1204,24 @@ int launch_reference_map(const DevScene& S, const DrcbRenderCfg& cfg, const R* p
                          uint64_t key, int ref_spp, R* out, int64_t* nonfinite, cudaStream_t st) {
   const int chunk = std::max(1, (1 << 14) / MAP_TEXELS);  // dataset.py:114
   const int nchunks = (ref_spp + chunk - 1) / chunk;
-  R* partial = nullptr;
-  DRCB_CUDA(cudaMallocAsync((void**)&partial, sizeof(R) * 3 * size_t(nchunks) * MAP_TEXELS, st));
-  k_reference_chunks<R><<<nblocks(int64_t(nchunks) * MAP_TEXELS), TPB, 0, st>>>(
-      S, cfg, pos, nrm, key, ref_spp, chunk, nchunks, partial, nonfinite);
-  LAUNCH_CHECK();
-  k_reference_reduce<R><<<nblocks(MAP_TEXELS), TPB, 0, st>>>(partial, nchunks, ref_spp, out);
-  LAUNCH_CHECK();
-  DRCB_CUDA(cudaFreeAsync(partial, st));
+  // groups of whole chunks whose per-path radiance fits 256 MB
+  const int64_t per_chunk = int64_t(chunk) * MAP_TEXELS * 3 * int64_t(sizeof(R));
+  const int gchunks = int(std::max<int64_t>(1, std::min<int64_t>(nchunks, (int64_t(256) << 20) / per_chunk)));
+  const int gs = std::min(ref_spp, gchunks * chunk);
+  R* paths = nullptr;
+  DRCB_CUDA(cudaMallocAsync((void**)&paths, sizeof(R) * 3 * (size_t(gs) + 1) * MAP_TEXELS, st));
+  R* tot = paths + 3 * size_t(gs) * MAP_TEXELS;
+  for (int c0 = 0; c0 < nchunks; c0 += gchunks) {
+    const int c1 = std::min(nchunks, c0 + gchunks);
+    const int s0 = c0 * chunk, s1 = std::min(ref_spp, c1 * chunk);
+    k_reference_paths<R><<<nblocks(int64_t(s1 - s0) * MAP_TEXELS), TPB, 0, st>>>(
+        S, cfg, pos, nrm, key, ref_spp, s0, s1 - s0, paths, nonfinite);
+    LAUNCH_CHECK();
+    k_reference_reduce<R><<<nblocks(MAP_TEXELS), TPB, 0, st>>>(paths, s0, chunk, c0, c1, ref_spp,
+                                                               tot, out, c1 == nchunks ? 1 : 0);
+    LAUNCH_CHECK();
+  }
+  DRCB_CUDA(cudaFreeAsync(paths, st));
   return 0;
 }
 

@@ -68,39 +68,46 @@ def generate_examples(scene, grid, ref_spp, sampler_variants=None, seed=0, confi
 
     ds = device_scene(scene)
     rd = torch.float64 if precision == 64 else torch.float32
+    found = [i for i in range(len(gx)) if geo["found"][i]]
+    n = len(found)
     examples = []
-    found_total = int(geo["found"].sum())
-    for i in range(len(gx)):
-        if not geo["found"][i]:
-            continue
+    if n == 0:
+        return examples
+    # every point's stacks and reference map are enqueued back to back and
+    # read back once (no host round trip per example)
+    P = torch.from_numpy(np.ascontiguousarray(geo["position"][found])).to("cuda", rd)
+    N = torch.from_numpy(np.ascontiguousarray(geo["normal"][found])).to("cuda", rd)
+    keys = torch.tensor([DATASET_KEY_BASE + i for i in found], dtype=torch.int64, device="cuda")
+    stacks = torch.zeros((n, 7, 32, 32), dtype=torch.float32, device="cuda")
+    s_r = torch.zeros(n, dtype=rd, device="cuda")
+    s_d = torch.zeros(n, dtype=rd, device="cuda")
+    frames = torch.zeros((n, 9), dtype=rd, device="cuda")
+    ref = torch.zeros((n, 1024, 3), dtype=rd, device="cuda")
+    nf = torch.zeros(1, dtype=torch.int64, device="cuda")
+    fields = [k for k in render.RenderConfig.__dataclass_fields__ if hasattr(cfg, k)]
+    for j, i in enumerate(found):
         kind = kinds[i % len(kinds)]
-        key = DATASET_KEY_BASE + i
-        c = render.RenderConfig(**{k: getattr(cfg, k) for k in render.RenderConfig.__dataclass_fields__
-                                   if hasattr(cfg, k)})
+        c = render.RenderConfig(**{k: getattr(cfg, k) for k in fields})
         c.sampler_kind, c.seed, c.precision = kind, seed + i, precision
         st = render._cfg_struct(c, precision)
         st.map_spp = int(ref_spp)
-        pos = torch.from_numpy(geo["position"][i].copy()).to("cuda", rd)
-        nrm = torch.from_numpy(geo["normal"][i].copy()).to("cuda", rd)
-        keys = torch.tensor([key], dtype=torch.int64, device="cuda")
-        stacks = torch.zeros((1, 7, 32, 32), dtype=torch.float32, device="cuda")
-        s_r = torch.zeros(1, dtype=rd, device="cuda")
-        s_d = torch.zeros(1, dtype=rd, device="cuda")
-        frames = torch.zeros((1, 9), dtype=rd, device="cuda")
-        nf = torch.zeros(1, dtype=torch.int64, device="cuda")
-        _lib.call("drcb_render_stacks", ds.handle, C.byref(st), _lib.ptr(pos), _lib.ptr(nrm),
-                  _lib.ptr(keys), 1, _lib.ptr(stacks), _lib.ptr(s_r), _lib.ptr(s_d),
-                  _lib.ptr(frames), _lib.ptr(nf), _lib.stream_ptr())
-        ref = torch.zeros((1024, 3), dtype=rd, device="cuda")
-        _lib.call("drcb_reference_map", ds.handle, C.byref(st), _lib.ptr(pos), _lib.ptr(nrm),
-                  C.c_uint64(key), int(ref_spp), _lib.ptr(ref), _lib.ptr(nf), _lib.stream_ptr())
-        sr = float(s_r.item())
-        target = (ref.double().cpu().numpy().reshape(32, 32, 3) / sr)
+        _lib.call("drcb_render_stacks", ds.handle, C.byref(st), _lib.ptr(P[j]), _lib.ptr(N[j]),
+                  _lib.ptr(keys[j:j + 1]), 1, _lib.ptr(stacks[j]), _lib.ptr(s_r[j]),
+                  _lib.ptr(s_d[j]), _lib.ptr(frames[j]), _lib.ptr(nf), _lib.stream_ptr())
+        _lib.call("drcb_reference_map", ds.handle, C.byref(st), _lib.ptr(P[j]), _lib.ptr(N[j]),
+                  C.c_uint64(DATASET_KEY_BASE + i), int(ref_spp), _lib.ptr(ref[j]), _lib.ptr(nf),
+                  _lib.stream_ptr())
+    stacks_h = stacks.cpu().numpy()
+    s_r_h, s_d_h = s_r.double().cpu().numpy(), s_d.double().cpu().numpy()
+    ref_h = ref.double().cpu().numpy()
+    for j, i in enumerate(found):
+        sr = float(s_r_h[j])
+        target = ref_h[j].reshape(32, 32, 3) / sr
         examples.append(TrainingExample(
-            input=stacks[0].cpu().numpy(),
+            input=stacks_h[j],
             target=np.moveaxis(target, -1, 0).astype(np.float32),
-            s_r=sr, s_d=float(s_d.item()), scene_id=getattr(scene, "name", "scene"),
+            s_r=sr, s_d=float(s_d_h[j]), scene_id=getattr(scene, "name", "scene"),
             pixel=(int(gx[i]), int(gy[i]))))
         if progress is not None:
-            progress(len(examples), found_total)
+            progress(len(examples), n)
     return examples
