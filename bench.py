@@ -53,8 +53,12 @@ def parse():
     ap.add_argument("--weak", action="store_true",
                     help="weak scaling: every rank renders --frames frames per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-points", type=int, default=16)
-    ap.add_argument("--cpu-pixels", type=int, default=4096)
+    ap.add_argument("--cpu-points", type=int, default=256,
+                    help="cache points of the CPU baseline's sample (~10 s of oracle work)")
+    ap.add_argument("--cpu-pixels", type=int, default=65536)
+    ap.add_argument("--ref-points", type=int, default=64,
+                    help="cache points per --impl reference step (~3 s each)")
+    ap.add_argument("--ref-pixels", type=int, default=16384)
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--direct-spp", type=int, default=0)
     ap.add_argument("--no-graph", action="store_true",
@@ -552,7 +556,7 @@ def main():
         vals = []
         cb = None
         for i in range(args.warmup + args.steps):
-            cb = cpu_baseline(scene, cams, cfg, net, n_pts, args.cpu_pixels, args.cpu_points, rank)
+            cb = cpu_baseline(scene, cams, cfg, net, n_pts, args.ref_pixels, args.ref_points, rank)
             if i >= args.warmup:
                 vals.append(cb["value"])
         v = float(np.mean(vals))
