@@ -35,7 +35,7 @@ def main():
     cams = scenegen.orbit_cameras(args.frames, res, seed=2)
     net = cnn.random_network(64, seed=wseed)
     plan = render.plan_points(res, cfg)
-    hashes, maps = [], []
+    hashes, maps, gbuf = [], [], []
     for rep in range(args.reps):
         for i, cam in enumerate(cams):
             img, tel = render.render_drc_device(scene, cfg, net, camera=cam, plan=plan, telemetry=True)
@@ -44,8 +44,10 @@ def main():
                 hashes.append(hashlib.sha256(img.cpu().numpy().tobytes()).hexdigest()[:16])
             elif tel and "stage_us" in tel:
                 maps.append(tel["stage_us"]["maps"])
+                gbuf.append(tel["stage_us"]["gbuffer_direct"])
     print(json.dumps({"env": {k: v for k, v in os.environ.items() if k.startswith("DRCB_")},
-                      "maps_ms": sum(maps) / max(len(maps), 1) / 1e3, "hashes": hashes}))
+                      "maps_ms": sum(maps) / max(len(maps), 1) / 1e3,
+                      "gbuffer_direct_ms": sum(gbuf) / max(len(gbuf), 1) / 1e3, "hashes": hashes}))
 
 
 if __name__ == "__main__":
