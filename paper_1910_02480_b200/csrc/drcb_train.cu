@@ -688,6 +688,8 @@ extern "C" void drcb_trainer_destroy(DrcbTrainer* T) {
   if (T->comm_stream) {
     for (cudaEvent_t e : T->comm_ev)
       if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : T->sync_ev)
+      if (e) cudaEventDestroy(e);
     cudaStreamDestroy(T->comm_stream);
   }
   for (void* p : T->allocs) cudaFree(p);

@@ -54,6 +54,7 @@ struct DrcbTrainer {
   // bucketed gradient all-reduce (NCCL): a side stream + one event per layer
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t comm_ev[18] = {};
+  cudaEvent_t sync_ev[2] = {};  // SyncBN all-reduces routed through comm_stream
 };
 
 namespace drcb {

@@ -858,6 +858,24 @@ inline void red_geom(int64_t npx, int ctiles, int64_t& ppb, int& gx) {
 // nothing to all-reduce: the SyncBN sums are already the batch's
 inline bool one_rank(const DrcbTrainer* T) { return !T->reduce_fn && T->world == 1; }
 
+// SyncBN sums. With the bucketed gradient all-reduce (NCCL, several ranks)
+// every NCCL call of the step goes through comm_stream in host order: one
+// communicator must see its collectives in the same order on every rank, and
+// the device's order between two streams is not fixed. The compute stream
+// forks into comm_stream and joins back (the BN statistics are on the
+// critical path either way).
+int syncbn_allreduce(DrcbTrainer* T, double* buf, size_t count, cudaStream_t st) {
+  if (!T->comm_stream || !T->comm || T->reduce_fn || T->world <= 1)
+    return trainer_allreduce(T, buf, count, 1, st);
+  DRCB_CUDA(cudaEventRecord(T->sync_ev[0], st));
+  DRCB_CUDA(cudaStreamWaitEvent(T->comm_stream, T->sync_ev[0], 0));
+  int rc = allreduce_sum(T->comm, buf, count, 1, T->comm_stream);
+  if (rc) return rc;
+  DRCB_CUDA(cudaEventRecord(T->sync_ev[1], T->comm_stream));
+  DRCB_CUDA(cudaStreamWaitEvent(st, T->sync_ev[1], 0));
+  return 0;
+}
+
 int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   TcEngine* E = T->tc;
   const TL& t = T->L[l];
@@ -880,7 +898,7 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   } else {
     k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
     TC_CHECK("k_reduce_parts");
-    rc = trainer_allreduce(T, E->sums, size_t(2) * coutp, 1, st);  // SyncBN
+    rc = syncbn_allreduce(T, E->sums, size_t(2) * coutp, st);  // SyncBN
     if (rc) return rc;
     k_fin<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, fin);
     TC_CHECK("k_fin");
@@ -929,7 +947,7 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
     k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums, t.cout,
                                                         coutp, T->grads + t.be, T->grads + t.g);
     TC_CHECK("k_reduce_parts");
-    rc = trainer_allreduce(T, E->sums, size_t(2) * coutp, 1, st);  // SyncBN backward
+    rc = syncbn_allreduce(T, E->sums, size_t(2) * coutp, st);  // SyncBN backward
     if (rc) return rc;
     coef.dbeta = coef.dgamma = nullptr;  // (written above from the local sums)
     k_fin<<<nbk(coutp), 256, 0, st>>>(E->sums, coutp, coef);
@@ -986,6 +1004,13 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
   if (rc) return rc;
   TcEngine* E = T->tc;
   E->last_n = n;
+  // NCCL over several ranks: the side stream every collective of the step
+  // goes through (bucketed gradients overlap the backward; SyncBN joins)
+  if (T->comm && !T->reduce_fn && T->world > 1 && !T->comm_stream) {
+    DRCB_CUDA(cudaStreamCreateWithFlags(&T->comm_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : T->comm_ev) DRCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (cudaEvent_t& e : T->sync_ev) DRCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   // packed bf16 operands of this step's weights (forward and dgrad forms)
   {
     PrepArgs a;
@@ -1024,10 +1049,6 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
   // as soon as its backward is done (buckets = layers, in backward order),
   // overlapping the all-reduce with the remaining layers' backward
   const bool bucket = T->comm && !T->reduce_fn && T->world > 1;
-  if (bucket && !T->comm_stream) {
-    DRCB_CUDA(cudaStreamCreateWithFlags(&T->comm_stream, cudaStreamNonBlocking));
-    for (cudaEvent_t& e : T->comm_ev) DRCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
   int nev = 0;
   auto reduce_layer = [&](int l) -> int {
     if (!bucket) return 0;
