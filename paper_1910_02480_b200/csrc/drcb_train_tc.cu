@@ -855,6 +855,12 @@ inline void red_geom(int64_t npx, int ctiles, int64_t& ppb, int& gx) {
   gx = int((npx + ppb - 1) / ppb);
 }
 
+// N of a conv whose output has fewer than 64 real channels (head.deconv1 /
+// deconv2 and their dgrads, 32x32): the row kernels compute N = channels
+// rounded to 16 and zero-fill the rest of each 64-channel row (the padding
+// the next layer's K reads), instead of multiplying zero weight rows
+inline int narrow_n(int hw, int c, int c_pad) { return hw >= 16 && c < 64 ? (c + 15) / 16 * 16 : c_pad; }
+
 // nothing to all-reduce: the SyncBN sums are already the batch's
 inline bool one_rank(const DrcbTrainer* T) { return !T->reduce_fn && T->world == 1; }
 
@@ -882,7 +888,7 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   const LayerPlan& P = PLAN[l];
   const int coutp = pad64(t.cout), hw2 = t.hw * t.hw;
   const Buf& in = E->B[P.in];
-  int rc = tc_conv_bf16(t.cin, t.cout, t.hw, np, in.p, in.c, E->Z[l], coutp, 0, E->wpf[l], coutp,
+  int rc = tc_conv_bf16(t.cin, t.cout, t.hw, np, in.p, in.c, E->Z[l], coutp, 0, E->wpf[l], narrow_n(t.hw, t.cout, coutp),
                         E->ep_one_f[l], E->ep_b[l], 1.0f, st);
   if (rc) return rc;
   int64_t ppb;
@@ -966,7 +972,7 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   // dgrad: the transposed conv of dz into the input-gradient buffer
   if (P.din >= 0) {
     const Buf& din = E->B[P.din];
-    rc = tc_conv_bf16(t.cout, t.cin, t.hw, np, dz, coutp, din.p, din.c, 0, E->wpt[l], din.c,
+    rc = tc_conv_bf16(t.cout, t.cin, t.hw, np, dz, coutp, din.p, din.c, 0, E->wpt[l], narrow_n(t.hw, t.cin, din.c),
                       E->ep_one_t[l], E->ep_zero[l], 1.0f, st);
     if (rc) return rc;
   }
