@@ -389,6 +389,8 @@ extern "C" int drcb_intersect(const DrcbScene* scene, int32_t precision, const v
                               int32_t record, uint8_t* hit, void* t, int64_t* prim, int32_t* mat,
                               void* pos, void* nrm, void* stream) {
   NEED(scene);
+  if (n < 0) return fail(DRCB_ECONTRACT, "drcb_intersect: negative ray count");
+  if (n == 0) return 0;  // an empty batch (the reference returns empty arrays)
   NEED(hit);
   if (precision == DRCB_PREC_MIXED)
     return launch_intersect_mixed(scene->dev, (const double*)O, (const double*)D, n,
