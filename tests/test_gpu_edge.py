@@ -3,7 +3,9 @@ test_all_rays_escape_yields_background / test_drc_smoke_nonnegative_and_
 tile_invariant, pkg/tests/test_geometry.py test_batch_respects_bounds), on the
 device path: empty scenes (no cache points at all), the (t_min, t_max]
 bound, the direct-pass tile only splitting work, a ragged frame size against
-the oracle, and zero-length batches."""
+the oracle, zero-length batches; and the analytic cases of
+pkg/tests/test_integrators.py / test_dataset.py (furnace, no light = exact
+zero, point light under a Lambertian floor, unlit dataset = zero targets)."""
 
 import numpy as np
 import pytest
@@ -109,3 +111,77 @@ def test_ragged_frame_matches_oracle():
     assert tel["entries"] == otel["entries"] > 0
     err = np.abs(img - ref).max() / max(np.abs(ref).max(), 1e-30)
     assert err <= 1e-4, err
+
+
+class _Sampler:
+    def __init__(self, kind="independent", spp=1, seed=0):
+        self.kind, self.spp, self.seed = kind, spp, seed
+
+
+def _ball(env=(0.0, 0.0, 0.0), lights=()):
+    doc = _doc([{"type": "sphere", "center": [0, 0, 0], "radius": 1.0, "material": "half"}],
+               env=env, lights=lights)
+    doc["materials"] = {"half": {"kind": "diffuse", "albedo": [0.5, 0.5, 0.5]}}
+    return scene_from_doc(doc, name="ball")
+
+
+def _centre_rays(n):
+    o = np.tile([0.0, 0.0, -5.0], (n, 1))
+    d = np.tile([0.0, 0.0, 1.0], (n, 1))
+    return o, d, np.zeros(n, np.uint64), np.arange(n, dtype=np.uint64)
+
+
+@pytest.mark.parametrize("precision,tol", [(64, 1e-12), (32, 1e-6)])
+def test_furnace_every_path_reflects_the_albedo(precision, tol):
+    """A convex Lambertian ball (albedo 0.5) in a unit environment: cosine
+    sampling makes every path's throughput exactly the albedo and the bounce
+    escapes, so every path (not just the mean) returns 0.5."""
+    o, d, pix, smp = _centre_rays(4096)
+    L = render.trace_radiance_batch(_ball(env=(1.0, 1.0, 1.0)), o, d, pix, smp, _Sampler(seed=1),
+                                    max_depth=4, precision=precision)
+    assert np.allclose(L, 0.5, rtol=tol, atol=0)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_no_lights_no_environment_is_exactly_zero(precision):
+    o, d, pix, smp = _centre_rays(1024)
+    L = render.trace_radiance_batch(_ball(), o, d, pix, smp, _Sampler(), max_depth=6,
+                                    precision=precision)
+    assert np.all(L == 0.0)
+
+
+@pytest.mark.parametrize("precision,tol", [(64, 1e-9), (32, 1e-5)])
+def test_direct_point_light_analytic(precision, tol):
+    """A Lambertian floor point straight below a point light: L = albedo/pi *
+    I / d^2 (the NEE estimate of a delta light is exact)."""
+    doc = _doc([{"type": "quad", "corner": [-40, 0, -40], "edge_u": [80, 0, 0],
+                 "edge_v": [0, 0, 80], "material": "half"}],
+               lights=[{"position": [0.0, 2.5, 0.0], "intensity": [6.0, 5.0, 4.0]}])
+    doc["materials"] = {"half": {"kind": "diffuse", "albedo": [0.5, 0.5, 0.5]}}
+    sc = scene_from_doc(doc, name="floor")
+    o = np.array([[0.0, 2.0, -2.0]])
+    d = np.array([[0.0, -2.0, 2.0]]) / np.sqrt(8.0)
+    L = render.li_direct_batch(sc, o, d, np.zeros(1, np.uint64), np.zeros(1, np.uint64),
+                               _Sampler(seed=3), precision=precision)
+    want = 0.5 / np.pi * np.array([6.0, 5.0, 4.0]) / 2.5 ** 2
+    assert np.allclose(L[0], want, rtol=tol, atol=0)
+
+
+def test_dataset_of_an_unlit_scene_has_zero_targets():
+    from paper_1910_02480_b200 import dataset
+
+    ex = dataset.generate_examples(_room_unlit(), (2, 2), 256, seed=2,
+                                   config=render.RenderConfig(max_path_depth=3, rr_start=3))
+    assert len(ex) > 0
+    for e in ex:
+        assert e.target.shape == (3, 32, 32) and np.all(e.target == 0.0)
+        assert np.all(e.input[:3] == 0.0)  # radiance channels
+
+
+def _room_unlit():
+    doc = _doc([
+        {"type": "quad", "corner": [-2.5, 0, -1], "edge_u": [5, 0, 0], "edge_v": [0, 0, 4],
+         "material": "matte"},
+        {"type": "sphere", "center": [0.5, 0.6, 1.2], "radius": 0.6, "material": "rust"},
+    ], res=(24, 24))
+    return scene_from_doc(doc, name="unlit")
