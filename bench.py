@@ -470,6 +470,33 @@ def traversal_traffic():
     return json.load(open(files[-1])).get("kernels")
 
 
+def l2_read_peak(mb=48, iters=100):
+    """Measured L2 -> SM read bandwidth (GB/s): libdrcb's probe kernel
+    streams an L2-resident buffer (48 MB of the 126 MB L2) with 16-B
+    ld.global.cg loads, CUDA-event timed after a warm-up pass; best of 3."""
+    import torch
+
+    from paper_1910_02480_b200 import _lib
+
+    buf = torch.ones(mb * (1 << 20) // 4, dtype=torch.int32, device="cuda")
+    sink = torch.zeros(1, dtype=torch.int64, device="cuda")
+    nbytes = buf.numel() * 4
+
+    def run(k):
+        _lib.call("drcb_l2_read_probe", _lib.ptr(buf), nbytes, k, _lib.ptr(sink), _lib.stream_ptr())
+
+    run(2)
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run(iters)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes * iters / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    return best
+
+
 def network_modes(cnn, net, n_maps=4096, iters=10):
     """Secondary: one U-Net forward of n_maps through each tensor-core operand
     mode (CUDA-event timed, device-resident input), TFLOP/s against the
@@ -814,6 +841,15 @@ def main():
                             peaks.get("hbm_gbs", 6650.0),
                 "l1_hit_pct": mp.get("l1_hit_pct"), "l2_hit_pct": mp.get("l2_hit_pct"),
                 "source": "bytes per launch: ncu full capture; time: live CUDA events"}
+            try:  # the L2 side of the roofline (SIMT-issue-bound, not L2-bound)
+                l2 = l2_read_peak()
+                ms_ = trav["maps_stage"]
+                ms_["l2_read_peak_gbs"] = l2
+                ms_["frac_l2_read"] = ms_["l2_to_l1_gbs"] / l2
+                ms_["frac_l2_total"] = (ms_["l2_to_l1_gbs"] + ms_["l1_to_l2_write_gbs"]) / l2
+                ms_["l2_peak_source"] = "measured live: drcb_l2_read_probe (48 MB, 16-B ld.global.cg)"
+            except Exception as e:  # secondary figure
+                trav["maps_stage"]["l2_read_peak_error"] = repr(e)
 
     cb = None
     if rank == 0 and not args.no_cpu_baseline:

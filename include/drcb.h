@@ -279,6 +279,12 @@ int drcb_trav_stats(unsigned long long *buf);
 /* number of kernels this library has launched so far (process-wide) */
 int64_t drcb_kernel_launches(void);
 
+/* Profiling hook: streams an L2-resident buffer `iters` times through L2 ->
+ * SM loads on `stream` (time it with events): the measured L2 read peak the
+ * ray-casting stages are reported against. `sink`: one device word. */
+int drcb_l2_read_probe(const void *buf, int64_t bytes, int32_t iters,
+                       unsigned long long *sink, void *stream);
+
 /* ---- trainer input pipeline (trainer/src/drc_trainer/data.py:77-121) -- */
 /* numpy cos/sin of 2*pi*shift/32 for shift = 0, 8, 16, 24 (host-computed so
  * the float64 normal re-expression matches _rotate_normals_xy bit for bit) */

@@ -106,6 +106,7 @@ _SIGS = [
     ("drcb_net_info", C.c_int, [vp, C.POINTER(C.c_int64)]),
     ("drcb_net_forward", C.c_int, [vp, vp, vp, C.c_int64, C.c_int32, vp]),
     ("drcb_kernel_launches", C.c_int64, []),
+    ("drcb_l2_read_probe", C.c_int, [vp, C.c_int64, C.c_int32, vp, vp]),
     ("drcb_trav_stats", C.c_int, [vp]),
     ("drcb_debug_conv", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, vp, vp,
                                   vp]),

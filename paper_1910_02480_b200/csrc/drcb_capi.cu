@@ -384,6 +384,43 @@ extern "C" const char* drcb_last_error(void) { return g_err.c_str(); }
 extern "C" int drcb_version(void) { return 1; }
 extern "C" int64_t drcb_kernel_launches(void) { return g_launches.load(); }
 
+namespace drcb {
+namespace probe {
+// L2 read bandwidth probe: every thread streams 16-B loads over an
+// L2-resident buffer `iters` times (ld.global.cg: L2, not L1) and folds them
+// into one word, so the loads cannot be elided
+__global__ void __launch_bounds__(512) k_l2_read(const uint4* __restrict__ buf, int64_t n16,
+                                                 int iters, unsigned long long* sink) {
+  uint32_t acc = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int it = 0; it < iters; ++it)
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride) {
+      uint4 v;
+      asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                   : "l"(buf + i));
+      acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+  if (acc == 0x9e3779b9u) atomicAdd(sink, 1ull);  // practically never; keeps the loads live
+}
+}  // namespace probe
+}  // namespace drcb
+
+// Profiling hook: stream `bytes` (a buffer that fits in L2) `iters` times
+// through L2 -> SM loads on `stream` (the caller times it with events):
+// the measured L2 read peak the traversal stages are compared against.
+extern "C" int drcb_l2_read_probe(const void* buf, int64_t bytes, int32_t iters,
+                                  unsigned long long* sink, void* stream) {
+  NEED(buf);
+  NEED(sink);
+  if (bytes < 16 || iters < 1) return fail(DRCB_ECONTRACT, "drcb_l2_read_probe: bad size");
+  drcb::probe::k_l2_read<<<unsigned(drcb::sm_count() * 4), 512, 0, S_(stream)>>>(
+      static_cast<const uint4*>(buf), bytes / 16, iters, sink);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : cuda_fail(e, "k_l2_read");
+}
+
 extern "C" int drcb_intersect(const DrcbScene* scene, int32_t precision, const void* O,
                               const void* D, int64_t n, const void* tmin, const void* tmax,
                               int32_t record, uint8_t* hit, void* t, int64_t* prim, int32_t* mat,
