@@ -2050,6 +2050,29 @@ CUtensorMapDataType tmap_dtype(int kind) {
                    : (kind == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
 }
 
+// NHWC activation box of `box_c` channels (box_c * elem bytes = 32 / 64 /
+// 128 B rows, swizzled at that width) x box_w x box_h x box_n
+int encode_act_c(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
+                 int box_c, int box_w, int box_h, int box_n) {
+  auto enc = get_encode();
+  if (!enc) return fail(DRCB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const int es = elem_bytes(kind);
+  const int rb = box_c * es;
+  if (rb != 32 && rb != 64 && rb != 128) return fail(DRCB_ECONFIG, "activation box rows must be 32, 64 or 128 B");
+  cuuint64_t dims[4] = {cuuint64_t(c_tot), cuuint64_t(hw), cuuint64_t(hw), cuuint64_t(nmaps)};
+  cuuint64_t strides[3] = {cuuint64_t(c_tot) * es, cuuint64_t(c_tot) * es * hw,
+                           cuuint64_t(c_tot) * es * hw * hw};
+  cuuint32_t box[4] = {cuuint32_t(box_c), cuuint32_t(box_w), cuuint32_t(box_h), cuuint32_t(box_n)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUtensorMapSwizzle sw = rb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUresult r = enc(m, tmap_dtype(kind), 4,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DRCB_ECUDA, "cuTensorMapEncodeTiled(activation) failed: " + std::to_string(int(r)));
+  return 0;
+}
+
 int encode_act(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
                int box_w, int box_h, int box_n) {
   auto enc = get_encode();

@@ -190,6 +190,18 @@ __device__ __forceinline__ uint64_t mn128_desc(uint32_t saddr, uint32_t lbo, uin
   d |= uint64_t(2) << 61;  // SWIZZLE_128B
   return d;
 }
+// the same for the narrower swizzles (rows of W = 32 / 64 / 128 bytes:
+// W / 2 16-bit MN elements per row, 8-row atoms of 8 W bytes; layout type
+// SWIZZLE_32B = 6, SWIZZLE_64B = 4, SWIZZLE_128B = 2)
+__device__ __forceinline__ uint64_t mn_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, int w) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(w == 128 ? 2 : w == 64 ? 4 : 6) << 61;
+  return d;
+}
 // instruction descriptor with MN-major A and B operands
 __host__ __device__ constexpr uint32_t make_idesc_mn(int kind, int M, int N) {
   return make_idesc(kind, M, N) | (1u << 15) | (1u << 16);

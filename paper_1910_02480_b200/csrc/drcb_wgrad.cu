@@ -39,6 +39,8 @@ namespace drcb {
 namespace tc {
 int encode_act(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
                int box_w, int box_h, int box_n);
+int encode_act_c(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
+                 int box_c, int box_w, int box_h, int box_n);
 }  // namespace tc
 
 namespace wg {
@@ -244,12 +246,18 @@ __global__ void __launch_bounds__(THREADS, 1)
 // N = 192 per MMA (the small-N layers' 64-column MMAs ran at ~45 % of the
 // tensor rate). A CTA owns one 64-channel input block x one 64-channel
 // output block and a range of K chunks.
+// NB = output channels per dZ box: 64 (128-B swizzled rows), or 32 / 16 for
+// layers with fewer outputs (head.deconv1 / deconv2: N = 96 / 48 instead of
+// multiplying 64-channel boxes that are mostly zero padding)
+template <int NB>
 __global__ void __launch_bounds__(THREADS, 1)
     k_wgrad_dxn(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapDZ,
                 const __grid_constant__ WgArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int STB = 3 * BOX + a.xbox;  // one stage: dZ boxes (dx = -1, 0, +1), then the X box
+  constexpr int W = NB * 2;          // dZ row bytes (one pixel)
+  constexpr int BOXZ = W * KPX;      // one dZ box
+  const int STB = 3 * BOXZ + a.xbox;  // one stage: dZ boxes (dx = -1, 0, +1), then the X box
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.zero_off + BOX);
   uint64_t* full = bars;
   uint64_t* empty = bars + 4;
@@ -259,7 +267,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int cob = unit / a.cb, cb = unit % a.cb;  // output / input channel blocks of 64
   const int c0 = int(int64_t(a.chunks) * split / a.splits);
   const int c1 = int(int64_t(a.chunks) * (split + 1) / a.splits);
-  constexpr uint32_t NCOL = 192, TCOLS = 512;
+  constexpr uint32_t NCOL = 3 * NB, TCOLS = 512;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (warp == 0 && lane == 0) {
     prefetch_map(&mapX);
@@ -297,8 +305,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_expect_tx(&full[s], uint32_t(STB));
         uint8_t* st = smem + s * STB;
         for (int j = 0; j < 3; ++j)  // dZ[q - (0, dx)], dx = j - 1: box at x = 1 - j
-          tma_load_4d(&mapDZ, &full[s], st + j * BOX, 64 * cob, 1 - j, row0, map0);
-        tma_load_4d(&mapX, &full[s], st + 3 * BOX, 64 * cb, 0, row0 - 1, map0);
+          tma_load_4d(&mapDZ, &full[s], st + j * BOXZ, NB * cob, 1 - j, row0, map0);
+        tma_load_4d(&mapX, &full[s], st + 3 * BOXZ, 64 * cb, 0, row0 - 1, map0);
         if (++s == a.dz_stages) {
           s = 0;
           ph ^= 1;
@@ -315,11 +323,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint32_t bz = smem_u32(smem + s * STB);
-        const uint32_t xs = bz + 3 * BOX;
+        const uint32_t xs = bz + 3 * BOXZ;
         const uint32_t acc_flag = c > c0 ? 1u : 0u;
 #pragma unroll
         for (int k = 0; k < KPX / 16; ++k) {
-          const uint64_t bd = mn128_desc(bz + k * 2048, BOX, 1024);
+          const uint64_t bd = mn_desc(bz + k * 16 * W, BOXZ, 8 * W, W);
           // rows dy = -1, 0 of the X box: offsets 0, one row
           tc_mma<0>(tmem_base, mn128_desc(xs + k * 2048, rowb, 1024), bd, idesc, (acc_flag | k) ? 1u : 0u);
           // dy = +1 (offset two rows) and the zero block
@@ -377,23 +385,24 @@ __device__ __forceinline__ int64_t wg_out(int co, int ci, int tap, int cin, int 
 
 // dx-in-N partials -> dwf: unit (output block, input block), acc j, row m
 // (dy of the X block: acc 0 rows -1 / 0, acc 1 row +1), column n (dx, co)
-__global__ void k_wgrad_reduce_dxn(const WgArgs a, int cin, int cout, int deconv,
+__global__ void k_wgrad_reduce_dxn(const WgArgs a, int nb, int cin, int cout, int deconv,
                                    float* __restrict__ dwf) {
-  const int64_t per = int64_t(2) * 128 * 192;
+  const int ncol = 3 * nb;
+  const int64_t per = int64_t(2) * 128 * ncol;
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= per * a.units) return;
   const int unit = int(e / per);
   int64_t r = e % per;
-  const int n = int(r % 192);
-  r /= 192;
+  const int n = int(r % ncol);
+  r /= ncol;
   const int m = int(r % 128), j = int(r / 128);
   if (j == 1 && m >= 64) return;  // the zero block
-  const int dy = j == 0 ? (m < 64 ? -1 : 0) : 1, dx = n / 64 - 1;
+  const int dy = j == 0 ? (m < 64 ? -1 : 0) : 1, dx = n / nb - 1;
   const int cob = unit / a.cb, cb = unit % a.cb;
-  const int ci = 64 * cb + (m & 63), co = 64 * cob + (n & 63);
+  const int ci = 64 * cb + (m & 63), co = nb * cob + n % nb;
   if (ci >= cin || co >= cout) return;
-  const int64_t stride = int64_t(a.units) * 2 * 128 * 192;
-  const float* p = a.partial + int64_t(unit) * per + (int64_t(j) * 128 + m) * 192 + n;
+  const int64_t stride = int64_t(a.units) * per;
+  const float* p = a.partial + int64_t(unit) * per + (int64_t(j) * 128 + m) * ncol + n;
   float s = 0.f;
   for (int k = 0; k < a.splits; ++k) s += p[k * stride];
   dwf[wg_out(co, ci, (dy + 1) * 3 + (dx + 1), cin, cout, deconv)] = s;
@@ -446,8 +455,11 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
   a.nb_n = a.n_tile / 64;
   const bool taps_env = getenv("DRCB_WGRAD_TAPS") != nullptr;  // A/B: a box per tap
   const bool dxn = hw >= 16 && !taps_env;
+  // dZ box width: the real output channels when there are fewer than 64
+  static const bool no_narrow = getenv("DRCB_WGRAD_NO_NARROW") != nullptr;
+  const int nb = (dxn && !no_narrow && cout <= 16) ? 16 : (dxn && !no_narrow && cout <= 32) ? 32 : 64;
   if (dxn) {
-    a.units = (cout_pad / 64) * a.cb;
+    a.units = ((cout + nb - 1) / nb) * a.cb;
   } else {
     a.npairs = (9 * a.cb + 1) / 2;
     a.n_acc = std::min(a.npairs, 512 / a.n_tile);
@@ -477,7 +489,7 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
   }();
   a.splits = std::max(1, std::min((a.chunks + min_chunks - 1) / min_chunks,
                                   (2 * nsm + a.units - 1) / a.units));
-  const size_t part = dxn ? size_t(a.splits) * a.units * 2 * 128 * 192 * 4
+  const size_t part = dxn ? size_t(a.splits) * a.units * 2 * 128 * (3 * nb) * 4
                           : size_t(a.splits) * a.units * a.n_acc * 128 * a.n_tile * 4;
   if (!ws) {
     *ws_bytes = part;
@@ -486,10 +498,10 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
   if (*ws_bytes < part) return fail(DRCB_ECONTRACT, "wgrad: scratch too small");
   a.partial = static_cast<float*>(ws);
   const int DZB = a.nb_n * BOX;
-  static DeviceFlags attr_dxn;
+  static DeviceFlags attr_dxn[3];
   if (dxn) {
     a.xbox = (a.rb + 2) * hw * 128;
-    const int stb = 3 * BOX + a.xbox;
+    const int stb = 3 * (nb * 2 * KPX) + a.xbox;
     a.dz_stages = std::min(4, (222 * 1024 - BOX) / stb);
     if (a.dz_stages < 2) return fail(DRCB_ECONFIG, "wgrad dx-in-N: SMEM plan");
     a.zero_off = a.dz_stages * stb;
@@ -497,15 +509,24 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
     CUtensorMap mX, mDZ;
     int rc = tc::encode_act(&mX, x, 0, cin_pad, hw, nmaps, hw, a.rb + 2, 1);
     if (rc) return rc;
-    rc = tc::encode_act(&mDZ, dz, 0, cout_pad, hw, nmaps, hw, a.rb, 1);
+    rc = tc::encode_act_c(&mDZ, dz, 0, cout_pad, hw, nmaps, nb, hw, a.rb, 1);
     if (rc) return rc;
-    smem_attr_once(attr_dxn, k_wgrad_dxn, 227 * 1024);
-    k_wgrad_dxn<<<a.units * a.splits, THREADS, smem, st>>>(mX, mDZ, a);
+    const unsigned grid = unsigned(a.units * a.splits);
+    if (nb == 16) {
+      smem_attr_once(attr_dxn[0], k_wgrad_dxn<16>, 227 * 1024);
+      k_wgrad_dxn<16><<<grid, THREADS, smem, st>>>(mX, mDZ, a);
+    } else if (nb == 32) {
+      smem_attr_once(attr_dxn[1], k_wgrad_dxn<32>, 227 * 1024);
+      k_wgrad_dxn<32><<<grid, THREADS, smem, st>>>(mX, mDZ, a);
+    } else {
+      smem_attr_once(attr_dxn[2], k_wgrad_dxn<64>, 227 * 1024);
+      k_wgrad_dxn<64><<<grid, THREADS, smem, st>>>(mX, mDZ, a);
+    }
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "k_wgrad_dxn");
-    const int64_t total = int64_t(2) * 128 * 192 * a.units;
-    k_wgrad_reduce_dxn<<<unsigned((total + 255) / 256), 256, 0, st>>>(a, cin, cout, deconv, dwf);
+    const int64_t total = int64_t(2) * 128 * (3 * nb) * a.units;
+    k_wgrad_reduce_dxn<<<unsigned((total + 255) / 256), 256, 0, st>>>(a, nb, cin, cout, deconv, dwf);
     count_launch();
     e = cudaGetLastError();
     return e == cudaSuccess ? 0 : cuda_fail(e, "k_wgrad_reduce_dxn");

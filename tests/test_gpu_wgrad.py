@@ -36,7 +36,7 @@ def _wgrad_ref(x, dz):
                                    (128, 128, 16, 2), (128, 256, 8, 4), (256, 256, 8, 2),
                                    (256, 512, 4, 8), (512, 512, 4, 8), (768, 256, 8, 2),
                                    (384, 128, 16, 2), (192, 64, 32, 2), (64, 32, 32, 2),
-                                   (32, 16, 32, 2)])
+                                   (32, 16, 32, 2), (64, 16, 16, 2), (128, 32, 16, 2)])
 def test_wgrad_matches_fp64(shape):
     cin, cout, hw, n = shape
     rng = np.random.default_rng(sum(shape))
