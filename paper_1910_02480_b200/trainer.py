@@ -88,6 +88,10 @@ class DeviceTrainer:
         xd = xd.to(device="cuda", dtype=torch.float32).contiguous()
         yd = yd.to(device="cuda", dtype=torch.float32).contiguous()
         loss = C.c_double(0.0)
+        key = getattr(self, "_graph_key", None)
+        if key is not None and int(xd.shape[0]) > key[2]:
+            # a larger batch can regrow the engine's buffers under the graph
+            self._graph = self._graph_key = None
         self._last_n_pad = (int(xd.shape[0]) + 7) // 8 * 8
         _lib.call("drcb_trainer_step", self.handle, _lib.ptr(xd), _lib.ptr(yd), int(xd.shape[0]),
                   C.byref(loss) if want_loss else None, int(bool(apply)), _lib.stream_ptr())
