@@ -13,7 +13,8 @@ import os
 from .errors import STATUS_TO_ERROR, CudaError, DrcError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdrcb.so")
+# DRCB_LIB: another build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("DRCB_LIB") or os.path.join(_HERE, "libdrcb.so")
 
 c_dp = C.POINTER(C.c_double)
 c_ip = C.POINTER(C.c_int32)

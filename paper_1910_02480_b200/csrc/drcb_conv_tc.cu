@@ -2073,12 +2073,15 @@ int encode_act_c(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, 
   return 0;
 }
 
+// c_dim (0 = c_tot): channels that hold data; the box's channels beyond it
+// are the TMA unit's out-of-bounds zero fill (not read from HBM)
 int encode_act(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
-               int box_w, int box_h, int box_n) {
+               int box_w, int box_h, int box_n, int c_dim = 0) {
   auto enc = get_encode();
   if (!enc) return fail(DRCB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const int es = elem_bytes(kind);
-  cuuint64_t dims[4] = {cuuint64_t(c_tot), cuuint64_t(hw), cuuint64_t(hw), cuuint64_t(nmaps)};
+  cuuint64_t dims[4] = {cuuint64_t(c_dim > 0 ? c_dim : c_tot), cuuint64_t(hw), cuuint64_t(hw),
+                        cuuint64_t(nmaps)};
   cuuint64_t strides[3] = {cuuint64_t(c_tot) * es, cuuint64_t(c_tot) * es * hw,
                            cuuint64_t(c_tot) * es * hw * hw};
   cuuint32_t box[4] = {cuuint32_t(ROW_BYTES / es), cuuint32_t(box_w), cuuint32_t(box_h), cuuint32_t(box_n)};
@@ -2279,6 +2282,7 @@ struct Buf {
   void* p;
   int c;   // channels (NHWC)
   int hw;
+  int c_real = 0;  // channels holding data when fewer than c (0: all), see encode_act
 };
 
 // one conv layer: in (NHWC, c_in_tot == layer cin_pad) -> out slice
@@ -2468,7 +2472,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
         pz.sb = std::min(8, (216 * 1024 - 2 * pz.o_bytes - pz.sa * pz.a_bytes) / bhalf);
       }
       CUtensorMap pA, pB, pO;
-      rc = encode_act(&pA, in.p, KIND, in.c, hw, nmaps, hw, BM / hw + 2, 1);
+      rc = encode_act(&pA, in.p, KIND, in.c, hw, nmaps, hw, BM / hw + 2, 1, in.c_real);
       if (rc) return rc;
       rc = encode_w(&pB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, 32);
       if (rc) return rc;
@@ -2517,7 +2521,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     const bool pw_shape = (dx && res && a.bn == 64) || (!dx && !res && a.bn == 128);
     rz.pool_cta = (pool_cta || !pw_shape) ? 1 : 0;
     if (rz.sa >= 2 && (res || rz.sb >= 2)) {
-      rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, hw, a.rows_per_tile + 2, 1);
+      rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, hw, a.rows_per_tile + 2, 1, in.c_real);
       if (rc) return rc;
       rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
       if (rc) return rc;
@@ -2568,7 +2572,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     a.num_n_tiles = L.cout_pad / a.bn;
   }
   int box_w = hw, box_h = a.maps_per_tile == 1 ? a.rows_per_tile : hw, box_n = a.maps_per_tile;
-  rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, box_w, box_h, box_n);
+  rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, box_w, box_h, box_n, in.c_real);
   if (rc) return rc;
   rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
   if (rc) return rc;
@@ -2777,7 +2781,10 @@ int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int c
   L.d_ep_a = const_cast<float*>(ep_a);
   L.d_ep_b = const_cast<float*>(ep_b);
   L.tc_kind = 0;
-  tc::Buf bi{const_cast<void*>(in), cin_pad, hw}, bo{out, out_ctot, hw};
+  // channels past cin (rounded to 8) hold zeros (or a shared buffer's stale
+  // values) that meet zero weights: not read (TMA zero fill)
+  const int c_real = cin < cin_pad ? (cin + 7) / 8 * 8 : 0;
+  tc::Buf bi{const_cast<void*>(in), cin_pad, hw, c_real}, bo{out, out_ctot, hw};
   return tc::run_layer<0>(net, L, bi, bo, out_coff, nmaps, st);
 }
 

@@ -150,14 +150,18 @@ __global__ void k_pad_vec(const float* __restrict__ v, int n, int np, float fill
   if (c < np) out[c] = c < n ? (v ? v[c] : fill) : 0.f;
 }
 
-// Per-channel reductions over the first npx pixels of an NHWC tensor: block
-// (bx, channel tile of 64) covers pixels [bx*ppb, (bx+1)*ppb); thread = (8-ch
-// group, one of 32 pixel lanes); the 32 lanes' sums are combined in lane
-// order in double. Partial slot (q*cpad + c) of block bx at
-// part[(q*cpad + c)*gx + bx], q = 0..NQ-1.
-template <int NQ, class F>
+// Per-channel reductions over the first npx pixels of an NHWC tensor (pixel
+// pitch cpad): block (bx, channel tile of 64) covers pixels [bx*ppb,
+// (bx+1)*ppb); thread = (8-ch group, one of 256/CG pixel lanes); the lanes'
+// sums are combined in lane order in double. CG = 8 groups cover a 64-channel
+// tile; a layer with fewer real channels (head.deconv1 / deconv2: 32 / 16)
+// runs CG = 4 / 2 and never touches the padding (a quarter / half of the
+// bytes). Partial slot (q*cpad + c) of block bx at part[(q*cpad + c)*gx + bx],
+// q = 0..NQ-1.
+template <int NQ, int CG, class F>
 __device__ __forceinline__ void chan_reduce(int64_t npx, int64_t ppb, int cpad, double* part, F f) {
-  const int cg = threadIdx.x & 7, pl = threadIdx.x >> 3;
+  constexpr int PL = 256 / CG, CT = 8 * CG;
+  const int cg = threadIdx.x % CG, pl = threadIdx.x / CG;
   const int c0 = blockIdx.y * 64 + cg * 8;
   f.init(c0);  // this thread's 8 channels are fixed: per-channel constants once
   float acc[NQ][8];
@@ -169,18 +173,18 @@ __device__ __forceinline__ void chan_reduce(int64_t npx, int64_t ppb, int cpad, 
   // four pixels per lane in flight (the loads of one iteration are issued
   // before their arithmetic: enough bytes in flight per SM for HBM rate)
   int64_t p = p0 + pl;
-  for (; p + 96 < p1; p += 128) f.template go<4>(p, c0, acc);
-  for (; p < p1; p += 32) f.template go<1>(p, c0, acc);
-  __shared__ float red[NQ][32][65];
+  for (; p + 3 * PL < p1; p += 4 * PL) f.template go<4, PL>(p, c0, acc);
+  for (; p < p1; p += PL) f.template go<1, PL>(p, c0, acc);
+  __shared__ float red[NQ][PL][CT + 1];
 #pragma unroll
   for (int q = 0; q < NQ; ++q)
 #pragma unroll
     for (int j = 0; j < 8; ++j) red[q][pl][cg * 8 + j] = acc[q][j];
   __syncthreads();
-  if (threadIdx.x < 64 * NQ) {
-    const int q = threadIdx.x / 64, c = threadIdx.x % 64;
+  if (threadIdx.x < CT * NQ) {
+    const int q = threadIdx.x / CT, c = threadIdx.x % CT;
     double s = 0.0;
-    for (int l = 0; l < 32; ++l) s += double(red[q][l][c]);
+    for (int l = 0; l < PL; ++l) s += double(red[q][l][c]);
     part[(int64_t(q) * cpad + blockIdx.y * 64 + c) * gridDim.x + blockIdx.x] = s;
   }
 }
@@ -210,11 +214,11 @@ struct StatsF {
   const bf16* z;
   int cpad;
   __device__ __forceinline__ void init(int) {}
-  template <int U>
+  template <int U, int PS>
   __device__ __forceinline__ void go(int64_t p, int c0, float (&acc)[2][8]) const {
     float v[U][8];
 #pragma unroll
-    for (int u = 0; u < U; ++u) ld8(z + (p + 32 * u) * cpad + c0, v[u]);
+    for (int u = 0; u < U; ++u) ld8(z + (p + PS * u) * cpad + c0, v[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -224,9 +228,10 @@ struct StatsF {
       }
   }
 };
+template <int CG>
 __global__ void __launch_bounds__(256) k_bn_stats(const bf16* __restrict__ z, int cpad, int64_t npx,
                                                   int64_t ppb, double* part) {
-  chan_reduce<2>(npx, ppb, cpad, part, StatsF{z, cpad});
+  chan_reduce<2, CG>(npx, ppb, cpad, part, StatsF{z, cpad});
 }
 
 // BN finalize (torch BatchNorm2d train mode: biased variance normalises,
@@ -307,10 +312,13 @@ __global__ void k_reduce_fin(const double* __restrict__ part, int nparts, int n,
 __device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
 
 // a = LeakyReLU(z * s + t) into out[.., c_off + c] (all np maps)
+// (the first `groups` 8-channel groups of each pixel: the padding of a
+// layer with fewer than 64 channels keeps its zeros)
 __global__ void __launch_bounds__(256) k_bn_apply(const bf16* __restrict__ z, int cpad, int npx,
                                                   const float* __restrict__ bnv, float slope,
-                                                  bf16* __restrict__ out, int c_tot, int c_off) {
-  const int lg = ilog2(cpad / 8);
+                                                  bf16* __restrict__ out, int c_tot, int c_off,
+                                                  int groups) {
+  const int lg = ilog2(groups);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (npx << lg)) return;
   const int p = i >> lg, c0 = (i & ((1 << lg) - 1)) * 8;
@@ -539,13 +547,13 @@ struct BnbStatsF {
       is[j] = __ldg(bnv + 3 * cpad + c0 + j);
     }
   }
-  template <int U>
+  template <int U, int PS>
   __device__ __forceinline__ void go(int64_t p, int c0, float (&acc)[2][8]) const {
     float zv[U][8], dv[U][8];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      ld8(z + (p + 32 * u) * cpad + c0, zv[u]);
-      ld8(da + (p + 32 * u) * cpad + c0, dv[u]);
+      ld8(z + (p + PS * u) * cpad + c0, zv[u]);
+      ld8(da + (p + PS * u) * cpad + c0, dv[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -559,11 +567,12 @@ struct BnbStatsF {
       }
   }
 };
+template <int CG>
 __global__ void __launch_bounds__(256) k_bnb_stats(const bf16* __restrict__ z, const bf16* __restrict__ da,
                                                    int cpad, int64_t npx, int64_t ppb,
                                                    const float* __restrict__ bnv, float slope,
                                                    double* part) {
-  chan_reduce<2>(npx, ppb, cpad, part, BnbStatsF{z, da, bnv, cpad, slope});
+  chan_reduce<2, CG>(npx, ppb, cpad, part, BnbStatsF{z, da, bnv, cpad, slope});
 }
 
 
@@ -593,18 +602,18 @@ struct BnbApplyF {
       k0[j] = -cf[j] * (m1 - m2 * mu * is);
     }
   }
-  template <int U>
+  template <int U, int PS>
   __device__ __forceinline__ void go(int64_t p, int c0, float (&acc)[1][8]) const {
     float zv[U][8], dv[U][8];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      ld8(z + (p + 32 * u) * cpad + c0, zv[u]);
-      ld8(da + (p + 32 * u) * cpad + c0, dv[u]);
+      ld8(z + (p + PS * u) * cpad + c0, zv[u]);
+      ld8(da + (p + PS * u) * cpad + c0, dv[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       float o[8];
-      const bool real = p + 32 * u < npx;
+      const bool real = p + PS * u < npx;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float y = fmaf(zv[u][j], s[j], t[j]);
@@ -613,15 +622,16 @@ struct BnbApplyF {
         o[j] = g;
         acc[0][j] += g;
       }
-      st8(dz + (p + 32 * u) * cpad + c0, o);
+      st8(dz + (p + PS * u) * cpad + c0, o);
     }
   }
 };
+template <int CG>
 __global__ void __launch_bounds__(256) k_bnb_apply(const bf16* __restrict__ z, const bf16* __restrict__ da,
                                                    int cpad, int64_t npx_all, int64_t npx, int64_t ppb,
                                                    const float* __restrict__ bnv, float slope,
                                                    bf16* __restrict__ dz, double* part) {
-  chan_reduce<1>(npx_all, ppb, cpad, part, BnbApplyF{z, da, bnv, dz, npx, cpad, slope});
+  chan_reduce<1, CG>(npx_all, ppb, cpad, part, BnbApplyF{z, da, bnv, dz, npx, cpad, slope});
 }
 
 // head: conv_out (1x1, 16 -> 3) + ReLU, L1 loss against y (n,3,32,32) fp32,
@@ -861,6 +871,10 @@ inline void red_geom(int64_t npx, int ctiles, int64_t& ppb, int& gx) {
 // the next layer's K reads), instead of multiplying zero weight rows
 inline int narrow_n(int hw, int c, int c_pad) { return hw >= 16 && c < 64 ? (c + 15) / 16 * 16 : c_pad; }
 
+// 8-channel groups a per-channel pass covers per 64-channel tile: 8, or the
+// real channels of a layer with fewer than 64 (head.deconv1 / deconv2)
+inline int chan_groups(int cout) { return cout <= 16 ? 2 : (cout <= 32 ? 4 : 8); }
+
 // nothing to all-reduce: the SyncBN sums are already the batch's
 inline bool one_rank(const DrcbTrainer* T) { return !T->reduce_fn && T->world == 1; }
 
@@ -893,8 +907,13 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   if (rc) return rc;
   int64_t ppb;
   int gx;
+  const int cg = chan_groups(t.cout);
   red_geom(n * hw2, coutp / 64, ppb, gx);
-  k_bn_stats<<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], coutp, n * hw2, ppb, E->part);
+  switch (cg) {
+    case 2: k_bn_stats<2><<<dim3(gx, 1), 256, 0, st>>>(E->Z[l], coutp, n * hw2, ppb, E->part); break;
+    case 4: k_bn_stats<4><<<dim3(gx, 1), 256, 0, st>>>(E->Z[l], coutp, n * hw2, ppb, E->part); break;
+    default: k_bn_stats<8><<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], coutp, n * hw2, ppb, E->part);
+  }
   TC_CHECK("k_bn_stats");
   const BnFin fin{t.cout,           coutp,       double(n) * hw2 * T->world, T->params + t.g,
                   T->params + t.be, T->running + t.rm, T->running + t.rv,  E->bnv[l]};
@@ -916,9 +935,10 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
                                               out.c, P.off, E->B[P.pool].p);
     TC_CHECK("k_bn_apply_pool");
   } else {
-    const int64_t tot = np * hw2 * (coutp / 8);
+    const int groups = cg < 8 ? cg : coutp / 8;
+    const int64_t tot = np * hw2 * groups;
     k_bn_apply<<<nbk(tot), 256, 0, st>>>(E->Z[l], coutp, np * hw2, E->bnv[l], T->slope, out.p, out.c,
-                                         P.off);
+                                         P.off, groups);
     TC_CHECK("k_bn_apply");
   }
   if (P.up >= 0) {
@@ -938,9 +958,14 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   const bf16* da = E->B[P.dA].p;
   int64_t ppb;
   int gx;
+  const int cg = chan_groups(t.cout);
   red_geom(n * hw2, coutp / 64, ppb, gx);
-  k_bnb_stats<<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], da, coutp, n * hw2, ppb, E->bnv[l],
-                                                    T->slope, E->part);
+  const dim3 gs(gx, cg < 8 ? 1 : coutp / 64);
+  switch (cg) {
+    case 2: k_bnb_stats<2><<<gs, 256, 0, st>>>(E->Z[l], da, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
+    case 4: k_bnb_stats<4><<<gs, 256, 0, st>>>(E->Z[l], da, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
+    default: k_bnb_stats<8><<<gs, 256, 0, st>>>(E->Z[l], da, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part);
+  }
   TC_CHECK("k_bnb_stats");
   // (sums of dyb and dyb * xhat: the local beta and gamma gradients)
   BnbCoef coef{t.cout, coutp, double(n) * hw2 * T->world, T->params + t.g, E->bnv[l],
@@ -963,8 +988,14 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   int gx2;
   red_geom(np * hw2, coutp / 64, ppb2, gx2);
   bf16* dz = E->B[DZ].p;
-  k_bnb_apply<<<dim3(gx2, coutp / 64), 256, 0, st>>>(E->Z[l], da, coutp, np * hw2, n * hw2, ppb2,
-                                                     E->bnv[l], T->slope, dz, E->part);
+  // (a narrow layer's dz padding is not written: its dgrad reads the real
+  // channels only, tc_conv_bf16, and its wgrad loads narrow dz boxes)
+  const dim3 ga(gx2, cg < 8 ? 1 : coutp / 64);
+  switch (cg) {
+    case 2: k_bnb_apply<2><<<ga, 256, 0, st>>>(E->Z[l], da, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
+    case 4: k_bnb_apply<4><<<ga, 256, 0, st>>>(E->Z[l], da, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
+    default: k_bnb_apply<8><<<ga, 256, 0, st>>>(E->Z[l], da, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part);
+  }
   TC_CHECK("k_bnb_apply");
   k_reduce_parts<<<nb_slots(t.cout), 256, 0, st>>>(E->part, gx2, t.cout, E->sums, t.cout, 0,
                                                    T->grads + t.b);  // conv bias

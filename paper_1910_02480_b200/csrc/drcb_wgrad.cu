@@ -38,7 +38,7 @@
 namespace drcb {
 namespace tc {
 int encode_act(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
-               int box_w, int box_h, int box_n);
+               int box_w, int box_h, int box_n, int c_dim = 0);
 int encode_act_c(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
                  int box_c, int box_w, int box_h, int box_n);
 }  // namespace tc
