@@ -273,6 +273,16 @@ def train_throughput(cnn, world=1, batches=(64, 256, 1024), global_batch=4096, s
         ms = float(t.item())
         out[key] = {"samples_per_s": b * world / (ms / 1e3), "ms_per_step": ms,
                     "batch_per_rank": b, "global_batch": b * world}
+        if mode == "bf16":
+            # forward + dgrad + wgrad = 3x the forward's multiply-adds per sample,
+            # against the measured dense bf16 peaks (burst, and sustained: the
+            # step runs back to back under the power cap)
+            tf = 3 * cnn.flops_per_map(64) * b / (ms * 1e-3) / 1e12
+            pk = measured_peaks()[0]
+            out[key]["tflops_per_gpu"] = tf
+            out[key]["frac_bf16_peak"] = tf / pk["bf16_tflops"]
+            if pk.get("bf16_tflops_sustained"):
+                out[key]["frac_bf16_peak_sustained"] = tf / pk["bf16_tflops_sustained"]
         del x, y
     for tr in trainers.values():
         comm = getattr(tr, "_comm", None)
