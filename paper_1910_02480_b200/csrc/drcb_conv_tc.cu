@@ -2052,16 +2052,18 @@ CUtensorMapDataType tmap_dtype(int kind) {
 
 // NHWC activation box of `box_c` channels (box_c * elem bytes = 32 / 64 /
 // 128 B rows, swizzled at that width) x box_w x box_h x box_n
+// (pitch: elements between pixels when the tensor is stored narrower than
+// c_tot; 0 = c_tot)
 int encode_act_c(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
-                 int box_c, int box_w, int box_h, int box_n) {
+                 int box_c, int box_w, int box_h, int box_n, int pitch = 0) {
   auto enc = get_encode();
   if (!enc) return fail(DRCB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const int es = elem_bytes(kind);
   const int rb = box_c * es;
   if (rb != 32 && rb != 64 && rb != 128) return fail(DRCB_ECONFIG, "activation box rows must be 32, 64 or 128 B");
-  cuuint64_t dims[4] = {cuuint64_t(c_tot), cuuint64_t(hw), cuuint64_t(hw), cuuint64_t(nmaps)};
-  cuuint64_t strides[3] = {cuuint64_t(c_tot) * es, cuuint64_t(c_tot) * es * hw,
-                           cuuint64_t(c_tot) * es * hw * hw};
+  const int pc = pitch > 0 ? pitch : c_tot;
+  cuuint64_t dims[4] = {cuuint64_t(std::min(c_tot, pc)), cuuint64_t(hw), cuuint64_t(hw), cuuint64_t(nmaps)};
+  cuuint64_t strides[3] = {cuuint64_t(pc) * es, cuuint64_t(pc) * es * hw, cuuint64_t(pc) * es * hw * hw};
   cuuint32_t box[4] = {cuuint32_t(box_c), cuuint32_t(box_w), cuuint32_t(box_h), cuuint32_t(box_n)};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUtensorMapSwizzle sw = rb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
@@ -2074,16 +2076,19 @@ int encode_act_c(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, 
 }
 
 // c_dim (0 = c_tot): channels that hold data; the box's channels beyond it
-// are the TMA unit's out-of-bounds zero fill (not read from HBM)
+// are the TMA unit's out-of-bounds zero fill on loads (not read from HBM)
+// and are dropped on stores. pitch (0 = c_tot): elements between pixels, for
+// a tensor stored narrower than the 64-channel boxes (the training engine's
+// 32- / 16-channel head layers)
 int encode_act(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
-               int box_w, int box_h, int box_n, int c_dim = 0) {
+               int box_w, int box_h, int box_n, int c_dim = 0, int pitch = 0) {
   auto enc = get_encode();
   if (!enc) return fail(DRCB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const int es = elem_bytes(kind);
-  cuuint64_t dims[4] = {cuuint64_t(c_dim > 0 ? c_dim : c_tot), cuuint64_t(hw), cuuint64_t(hw),
-                        cuuint64_t(nmaps)};
-  cuuint64_t strides[3] = {cuuint64_t(c_tot) * es, cuuint64_t(c_tot) * es * hw,
-                           cuuint64_t(c_tot) * es * hw * hw};
+  const int pc = pitch > 0 ? pitch : c_tot;
+  const int cd = std::min(c_dim > 0 ? c_dim : c_tot, pc);
+  cuuint64_t dims[4] = {cuuint64_t(cd), cuuint64_t(hw), cuuint64_t(hw), cuuint64_t(nmaps)};
+  cuuint64_t strides[3] = {cuuint64_t(pc) * es, cuuint64_t(pc) * es * hw, cuuint64_t(pc) * es * hw * hw};
   cuuint32_t box[4] = {cuuint32_t(ROW_BYTES / es), cuuint32_t(box_w), cuuint32_t(box_h), cuuint32_t(box_n)};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(m, tmap_dtype(kind), 4,
@@ -2283,6 +2288,7 @@ struct Buf {
   int c;   // channels (NHWC)
   int hw;
   int c_real = 0;  // channels holding data when fewer than c (0: all), see encode_act
+  int pitch = 0;   // elements between pixels when stored narrower than c (0: c)
 };
 
 // one conv layer: in (NHWC, c_in_tot == layer cin_pad) -> out slice
@@ -2472,7 +2478,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
         pz.sb = std::min(8, (216 * 1024 - 2 * pz.o_bytes - pz.sa * pz.a_bytes) / bhalf);
       }
       CUtensorMap pA, pB, pO;
-      rc = encode_act(&pA, in.p, KIND, in.c, hw, nmaps, hw, BM / hw + 2, 1, in.c_real);
+      rc = encode_act(&pA, in.p, KIND, in.c, hw, nmaps, hw, BM / hw + 2, 1, in.c_real, in.pitch);
       if (rc) return rc;
       rc = encode_w(&pB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, 32);
       if (rc) return rc;
@@ -2521,7 +2527,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     const bool pw_shape = (dx && res && a.bn == 64) || (!dx && !res && a.bn == 128);
     rz.pool_cta = (pool_cta || !pw_shape) ? 1 : 0;
     if (rz.sa >= 2 && (res || rz.sb >= 2)) {
-      rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, hw, a.rows_per_tile + 2, 1, in.c_real);
+      rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, hw, a.rows_per_tile + 2, 1, in.c_real, in.pitch);
       if (rc) return rc;
       rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
       if (rc) return rc;
@@ -2572,7 +2578,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     a.num_n_tiles = L.cout_pad / a.bn;
   }
   int box_w = hw, box_h = a.maps_per_tile == 1 ? a.rows_per_tile : hw, box_n = a.maps_per_tile;
-  rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, box_w, box_h, box_n, in.c_real);
+  rc = encode_act(&mA, in.p, KIND, in.c, hw, nmaps, box_w, box_h, box_n, in.c_real, in.pitch);
   if (rc) return rc;
   rc = encode_w(&mB, L.d_wtc, KIND, int64_t(9) * L.cin_pad, L.cout_pad, a.bn);
   if (rc) return rc;
@@ -2765,9 +2771,12 @@ int tc_input_channels(int) { return 8; }  // compact NHWC input (7 + 1 zero chan
 // dgrad): NHWC bf16 in (nmaps a multiple of 8, cin_pad channels), packed
 // K-major weights [cout_pad][9 * cin_pad], epilogue y = acc * a + b then
 // LeakyReLU(slope) (slope 1 = identity) into out's channel slice.
+// in_pitch (0 = cin_pad): elements between input pixels when the input is
+// stored narrower than its 64-channel K blocks; out_ctot below 64 likewise
+// stores the output narrow (the TMA store drops the box's other channels)
 int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int cin_pad, void* out,
                  int out_ctot, int out_coff, const void* wpacked, int cout_pad, const float* ep_a,
-                 const float* ep_b, float slope, cudaStream_t st) {
+                 const float* ep_b, float slope, cudaStream_t st, int in_pitch) {
   NetImpl net;
   net.slope = slope;
   ConvLayer L;
@@ -2784,7 +2793,7 @@ int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int c
   // channels past cin (rounded to 8) hold zeros (or a shared buffer's stale
   // values) that meet zero weights: not read (TMA zero fill)
   const int c_real = cin < cin_pad ? (cin + 7) / 8 * 8 : 0;
-  tc::Buf bi{const_cast<void*>(in), cin_pad, hw, c_real}, bo{out, out_ctot, hw};
+  tc::Buf bi{const_cast<void*>(in), cin_pad, hw, c_real, in_pitch}, bo{out, out_ctot, hw};
   return tc::run_layer<0>(net, L, bi, bo, out_coff, nmaps, st);
 }
 

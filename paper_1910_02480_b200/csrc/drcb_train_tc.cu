@@ -26,15 +26,25 @@ namespace drcb {
 
 int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int cin_pad, void* out,
                  int out_ctot, int out_coff, const void* wpacked, int cout_pad, const float* ep_a,
-                 const float* ep_b, float slope, cudaStream_t st);
+                 const float* ep_b, float slope, cudaStream_t st, int in_pitch);
 int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, int cout_pad, int hw,
-               int64_t nmaps, float* dwf, int deconv, void* ws, size_t* ws_bytes, cudaStream_t st);
+               int64_t nmaps, float* dwf, int deconv, void* ws, size_t* ws_bytes, cudaStream_t st,
+               int x_pitch, int dz_pitch);
 
 namespace train {
 
 using bf16 = __nv_bfloat16;
 
 inline int pad64(int c) { return (c + 63) / 64 * 64; }
+// 8-channel groups a per-channel pass covers per 64-channel tile: 8, or the
+// real channels of a layer with fewer than 64 (head.deconv1 / deconv2)
+inline int chan_groups(int cout) { return cout <= 16 ? 2 : (cout <= 32 ? 4 : 8); }
+// elements between pixels of a layer's Z / activation / gradient tensors:
+// 64-channel multiples, except the head's 32- and 16-channel layers, which
+// are stored at that width (a quarter / half of the bytes of every pass over
+// them; the tensor-core kernels load them into 64-channel boxes through the
+// TMA zero fill and store them through box clipping)
+inline int zpitch(int cout) { return cout < 64 ? 8 * chan_groups(cout) : pad64(cout); }
 inline unsigned nbk(int64_t n, int t = 256) { return unsigned((n + t - 1) / t); }
 
 #define TC_CHECK(name)                                      \
@@ -212,13 +222,13 @@ inline unsigned nb_slots(int nslots) { return unsigned((int64_t(nslots) * 32 + 2
 // forward batch statistics: sum z, sum z^2 per channel
 struct StatsF {
   const bf16* z;
-  int cpad;
+  int pitch;
   __device__ __forceinline__ void init(int) {}
   template <int U, int PS>
   __device__ __forceinline__ void go(int64_t p, int c0, float (&acc)[2][8]) const {
     float v[U][8];
 #pragma unroll
-    for (int u = 0; u < U; ++u) ld8(z + (p + PS * u) * cpad + c0, v[u]);
+    for (int u = 0; u < U; ++u) ld8(z + (p + PS * u) * pitch + c0, v[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -229,9 +239,9 @@ struct StatsF {
   }
 };
 template <int CG>
-__global__ void __launch_bounds__(256) k_bn_stats(const bf16* __restrict__ z, int cpad, int64_t npx,
-                                                  int64_t ppb, double* part) {
-  chan_reduce<2, CG>(npx, ppb, cpad, part, StatsF{z, cpad});
+__global__ void __launch_bounds__(256) k_bn_stats(const bf16* __restrict__ z, int pitch, int cpad,
+                                                  int64_t npx, int64_t ppb, double* part) {
+  chan_reduce<2, CG>(npx, ppb, cpad, part, StatsF{z, pitch});
 }
 
 // BN finalize (torch BatchNorm2d train mode: biased variance normalises,
@@ -314,7 +324,7 @@ __device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
 // a = LeakyReLU(z * s + t) into out[.., c_off + c] (all np maps)
 // (the first `groups` 8-channel groups of each pixel: the padding of a
 // layer with fewer than 64 channels keeps its zeros)
-__global__ void __launch_bounds__(256) k_bn_apply(const bf16* __restrict__ z, int cpad, int npx,
+__global__ void __launch_bounds__(256) k_bn_apply(const bf16* __restrict__ z, int zp, int cpad, int npx,
                                                   const float* __restrict__ bnv, float slope,
                                                   bf16* __restrict__ out, int c_tot, int c_off,
                                                   int groups) {
@@ -323,7 +333,7 @@ __global__ void __launch_bounds__(256) k_bn_apply(const bf16* __restrict__ z, in
   if (i >= (npx << lg)) return;
   const int p = i >> lg, c0 = (i & ((1 << lg) - 1)) * 8;
   float v[8];
-  ld8(z + int64_t(p) * cpad + c0, v);
+  ld8(z + int64_t(p) * zp + c0, v);
   const float4 s0 = __ldg(reinterpret_cast<const float4*>(bnv + c0));
   const float4 s1 = __ldg(reinterpret_cast<const float4*>(bnv + c0 + 4));
   const float4 t0 = __ldg(reinterpret_cast<const float4*>(bnv + cpad + c0));
@@ -535,7 +545,7 @@ __global__ void __launch_bounds__(256) k_pool_bwd(const bf16* __restrict__ a, in
 struct BnbStatsF {
   const bf16 *z, *da;
   const float* bnv;
-  int cpad;
+  int cpad, pitch;  // bnv vector stride; elements between pixels
   float slope;
   float s[8], t[8], mu[8], is[8];
   __device__ __forceinline__ void init(int c0) {
@@ -552,8 +562,8 @@ struct BnbStatsF {
     float zv[U][8], dv[U][8];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      ld8(z + (p + PS * u) * cpad + c0, zv[u]);
-      ld8(da + (p + PS * u) * cpad + c0, dv[u]);
+      ld8(z + (p + PS * u) * pitch + c0, zv[u]);
+      ld8(da + (p + PS * u) * pitch + c0, dv[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -569,10 +579,10 @@ struct BnbStatsF {
 };
 template <int CG>
 __global__ void __launch_bounds__(256) k_bnb_stats(const bf16* __restrict__ z, const bf16* __restrict__ da,
-                                                   int cpad, int64_t npx, int64_t ppb,
+                                                   int pitch, int cpad, int64_t npx, int64_t ppb,
                                                    const float* __restrict__ bnv, float slope,
                                                    double* part) {
-  chan_reduce<2, CG>(npx, ppb, cpad, part, BnbStatsF{z, da, bnv, cpad, slope});
+  chan_reduce<2, CG>(npx, ppb, cpad, part, BnbStatsF{z, da, bnv, cpad, pitch, slope});
 }
 
 
@@ -585,8 +595,8 @@ struct BnbApplyF {
   const bf16 *z, *da;
   const float* bnv;
   bf16* dz;
-  int64_t npx;  // real pixels (maps beyond n get dz = 0)
-  int cpad;
+  int64_t npx;      // real pixels (maps beyond n get dz = 0)
+  int cpad, pitch;  // bnv vector stride; elements between pixels
   float slope;
   float s[8], t[8], cf[8], k0[8], k1[8];
   __device__ __forceinline__ void init(int c0) {
@@ -607,8 +617,8 @@ struct BnbApplyF {
     float zv[U][8], dv[U][8];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      ld8(z + (p + PS * u) * cpad + c0, zv[u]);
-      ld8(da + (p + PS * u) * cpad + c0, dv[u]);
+      ld8(z + (p + PS * u) * pitch + c0, zv[u]);
+      ld8(da + (p + PS * u) * pitch + c0, dv[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -622,16 +632,16 @@ struct BnbApplyF {
         o[j] = g;
         acc[0][j] += g;
       }
-      st8(dz + (p + PS * u) * cpad + c0, o);
+      st8(dz + (p + PS * u) * pitch + c0, o);
     }
   }
 };
 template <int CG>
 __global__ void __launch_bounds__(256) k_bnb_apply(const bf16* __restrict__ z, const bf16* __restrict__ da,
-                                                   int cpad, int64_t npx_all, int64_t npx, int64_t ppb,
-                                                   const float* __restrict__ bnv, float slope,
-                                                   bf16* __restrict__ dz, double* part) {
-  chan_reduce<1, CG>(npx_all, ppb, cpad, part, BnbApplyF{z, da, bnv, dz, npx, cpad, slope});
+                                                   int pitch, int cpad, int64_t npx_all, int64_t npx,
+                                                   int64_t ppb, const float* __restrict__ bnv,
+                                                   float slope, bf16* __restrict__ dz, double* part) {
+  chan_reduce<1, CG>(npx_all, ppb, cpad, part, BnbApplyF{z, da, bnv, dz, npx, cpad, pitch, slope});
 }
 
 // head: conv_out (1x1, 16 -> 3) + ReLU, L1 loss against y (n,3,32,32) fp32,
@@ -641,7 +651,7 @@ constexpr int HEAD_SLOTS = 52;
 __global__ void __launch_bounds__(256) k_head(const bf16* __restrict__ a15, const float* __restrict__ w,
                                               const float* __restrict__ b, const float* __restrict__ y,
                                               int64_t n, int64_t np, double inv_n, bf16* __restrict__ da15,
-                                              double* part) {
+                                              double* part, int pitch) {
   float wl[48], bl[3];
 #pragma unroll
   for (int i = 0; i < 48; ++i) wl[i] = w[i];
@@ -658,10 +668,10 @@ __global__ void __launch_bounds__(256) k_head(const bf16* __restrict__ a15, cons
     float a[16];
     {
       float t[8];
-      ld8(a15 + p * 64, t);
+      ld8(a15 + p * pitch, t);
 #pragma unroll
       for (int j = 0; j < 8; ++j) a[j] = t[j];
-      ld8(a15 + p * 64 + 8, t);
+      ld8(a15 + p * pitch + 8, t);
 #pragma unroll
       for (int j = 0; j < 8; ++j) a[8 + j] = t[j];
     }
@@ -688,7 +698,7 @@ __global__ void __launch_bounds__(256) k_head(const bf16* __restrict__ a15, cons
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         da[j] = wl[h * 8 + j] * gpre[0] + wl[16 + h * 8 + j] * gpre[1] + wl[32 + h * 8 + j] * gpre[2];
-      st8(da15 + p * 64 + 8 * h, da);
+      st8(da15 + p * pitch + 8 * h, da);
     }
   }
   // block reduction of the 52 slots in a fixed order
@@ -778,9 +788,9 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
   const int spec[NBUF][2] = {
       {64, 32}, {64, 32}, {192, 32}, {64, 16}, {128, 16}, {384, 16}, {128, 8}, {256, 8}, {768, 8},
       {256, 4}, {512, 4}, {512, 4}, {256, 8}, {256, 8}, {128, 16}, {128, 16}, {64, 32}, {64, 32},
-      {64, 32}, {64, 32},
-      {64, 32},  // DZ: the largest cout_pad * hw^2 (64 * 1024)
-      {64, 32}, {64, 32}, {64, 32}, {64, 32}, {192, 32}, {128, 16}, {128, 16}, {384, 16}, {256, 8},
+      {32, 32}, {16, 32},  // A14, A15: the head's 32- / 16-channel layers stored at that width
+      {64, 32},            // DZ: the largest cout_pad * hw^2 (64 * 1024)
+      {16, 32}, {32, 32}, {64, 32}, {64, 32}, {192, 32}, {128, 16}, {128, 16}, {384, 16}, {256, 8},
       {256, 8}, {768, 8}, {512, 4}, {512, 4}, {256, 4}, {256, 8}, {256, 8}, {128, 8}, {128, 16},
       {128, 16}, {64, 16}, {64, 32}, {64, 32}};
   size_t total = 0;
@@ -792,7 +802,7 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
   for (int l = 0; l < 16; ++l) {
     const TL& t = T->L[l];
     off[NBUF + l] = total;
-    total += (size_t(np) * t.hw * t.hw * pad64(t.cout) * 2 + 1023) & ~size_t(1023);
+    total += (size_t(np) * t.hw * t.hw * zpitch(t.cout) * 2 + 1023) & ~size_t(1023);
   }
   void* base = nullptr;
   if (cudaMalloc(&base, total) != cudaSuccess) return fail(DRCB_ECUDA, "cudaMalloc tensor-core trainer activations");
@@ -819,8 +829,8 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
   for (int l = 0; l < 16; ++l) {
     const TL& t = T->L[l];
     size_t q = 0;
-    int rc = wgrad_bf16(nullptr, t.cin, E->B[PLAN[l].in].c, nullptr, t.cout, pad64(t.cout), t.hw, np,
-                        nullptr, 0, nullptr, &q, st);
+    int rc = wgrad_bf16(nullptr, t.cin, pad64(E->B[PLAN[l].in].c), nullptr, t.cout, pad64(t.cout), t.hw,
+                        np, nullptr, 0, nullptr, &q, st, 0, 0);
     if (rc) return rc;
     wsb = std::max(wsb, q);
   }
@@ -871,10 +881,6 @@ inline void red_geom(int64_t npx, int ctiles, int64_t& ppb, int& gx) {
 // the next layer's K reads), instead of multiplying zero weight rows
 inline int narrow_n(int hw, int c, int c_pad) { return hw >= 16 && c < 64 ? (c + 15) / 16 * 16 : c_pad; }
 
-// 8-channel groups a per-channel pass covers per 64-channel tile: 8, or the
-// real channels of a layer with fewer than 64 (head.deconv1 / deconv2)
-inline int chan_groups(int cout) { return cout <= 16 ? 2 : (cout <= 32 ? 4 : 8); }
-
 // nothing to all-reduce: the SyncBN sums are already the batch's
 inline bool one_rank(const DrcbTrainer* T) { return !T->reduce_fn && T->world == 1; }
 
@@ -900,19 +906,20 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   TcEngine* E = T->tc;
   const TL& t = T->L[l];
   const LayerPlan& P = PLAN[l];
-  const int coutp = pad64(t.cout), hw2 = t.hw * t.hw;
+  const int coutp = pad64(t.cout), hw2 = t.hw * t.hw, zp = zpitch(t.cout);
   const Buf& in = E->B[P.in];
-  int rc = tc_conv_bf16(t.cin, t.cout, t.hw, np, in.p, in.c, E->Z[l], coutp, 0, E->wpf[l], narrow_n(t.hw, t.cout, coutp),
-                        E->ep_one_f[l], E->ep_b[l], 1.0f, st);
+  // (K blocks of 64 channels; a narrow input is read at its own pitch)
+  int rc = tc_conv_bf16(t.cin, t.cout, t.hw, np, in.p, pad64(in.c), E->Z[l], zp, 0, E->wpf[l],
+                        narrow_n(t.hw, t.cout, coutp), E->ep_one_f[l], E->ep_b[l], 1.0f, st, in.c);
   if (rc) return rc;
   int64_t ppb;
   int gx;
   const int cg = chan_groups(t.cout);
   red_geom(n * hw2, coutp / 64, ppb, gx);
   switch (cg) {
-    case 2: k_bn_stats<2><<<dim3(gx, 1), 256, 0, st>>>(E->Z[l], coutp, n * hw2, ppb, E->part); break;
-    case 4: k_bn_stats<4><<<dim3(gx, 1), 256, 0, st>>>(E->Z[l], coutp, n * hw2, ppb, E->part); break;
-    default: k_bn_stats<8><<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], coutp, n * hw2, ppb, E->part);
+    case 2: k_bn_stats<2><<<dim3(gx, 1), 256, 0, st>>>(E->Z[l], zp, coutp, n * hw2, ppb, E->part); break;
+    case 4: k_bn_stats<4><<<dim3(gx, 1), 256, 0, st>>>(E->Z[l], zp, coutp, n * hw2, ppb, E->part); break;
+    default: k_bn_stats<8><<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], zp, coutp, n * hw2, ppb, E->part);
   }
   TC_CHECK("k_bn_stats");
   const BnFin fin{t.cout,           coutp,       double(n) * hw2 * T->world, T->params + t.g,
@@ -937,8 +944,8 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   } else {
     const int groups = cg < 8 ? cg : coutp / 8;
     const int64_t tot = np * hw2 * groups;
-    k_bn_apply<<<nbk(tot), 256, 0, st>>>(E->Z[l], coutp, np * hw2, E->bnv[l], T->slope, out.p, out.c,
-                                         P.off, groups);
+    k_bn_apply<<<nbk(tot), 256, 0, st>>>(E->Z[l], zp, coutp, np * hw2, E->bnv[l], T->slope, out.p,
+                                         out.c, P.off, groups);
     TC_CHECK("k_bn_apply");
   }
   if (P.up >= 0) {
@@ -954,7 +961,7 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   TcEngine* E = T->tc;
   const TL& t = T->L[l];
   const LayerPlan& P = PLAN[l];
-  const int coutp = pad64(t.cout), hw2 = t.hw * t.hw;
+  const int coutp = pad64(t.cout), hw2 = t.hw * t.hw, zp = zpitch(t.cout);
   const bf16* da = E->B[P.dA].p;
   int64_t ppb;
   int gx;
@@ -962,9 +969,9 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   red_geom(n * hw2, coutp / 64, ppb, gx);
   const dim3 gs(gx, cg < 8 ? 1 : coutp / 64);
   switch (cg) {
-    case 2: k_bnb_stats<2><<<gs, 256, 0, st>>>(E->Z[l], da, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
-    case 4: k_bnb_stats<4><<<gs, 256, 0, st>>>(E->Z[l], da, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
-    default: k_bnb_stats<8><<<gs, 256, 0, st>>>(E->Z[l], da, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part);
+    case 2: k_bnb_stats<2><<<gs, 256, 0, st>>>(E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
+    case 4: k_bnb_stats<4><<<gs, 256, 0, st>>>(E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
+    default: k_bnb_stats<8><<<gs, 256, 0, st>>>(E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part);
   }
   TC_CHECK("k_bnb_stats");
   // (sums of dyb and dyb * xhat: the local beta and gamma gradients)
@@ -988,13 +995,13 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   int gx2;
   red_geom(np * hw2, coutp / 64, ppb2, gx2);
   bf16* dz = E->B[DZ].p;
-  // (a narrow layer's dz padding is not written: its dgrad reads the real
-  // channels only, tc_conv_bf16, and its wgrad loads narrow dz boxes)
+  // (a narrow layer's dz is stored at its own width: its dgrad and wgrad
+  // load it into 64-channel / narrow boxes through the TMA zero fill)
   const dim3 ga(gx2, cg < 8 ? 1 : coutp / 64);
   switch (cg) {
-    case 2: k_bnb_apply<2><<<ga, 256, 0, st>>>(E->Z[l], da, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
-    case 4: k_bnb_apply<4><<<ga, 256, 0, st>>>(E->Z[l], da, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
-    default: k_bnb_apply<8><<<ga, 256, 0, st>>>(E->Z[l], da, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part);
+    case 2: k_bnb_apply<2><<<ga, 256, 0, st>>>(E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
+    case 4: k_bnb_apply<4><<<ga, 256, 0, st>>>(E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
+    default: k_bnb_apply<8><<<ga, 256, 0, st>>>(E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part);
   }
   TC_CHECK("k_bnb_apply");
   k_reduce_parts<<<nb_slots(t.cout), 256, 0, st>>>(E->part, gx2, t.cout, E->sums, t.cout, 0,
@@ -1003,16 +1010,16 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   // dgrad: the transposed conv of dz into the input-gradient buffer
   if (P.din >= 0) {
     const Buf& din = E->B[P.din];
-    rc = tc_conv_bf16(t.cout, t.cin, t.hw, np, dz, coutp, din.p, din.c, 0, E->wpt[l], narrow_n(t.hw, t.cin, din.c),
-                      E->ep_one_t[l], E->ep_zero[l], 1.0f, st);
+    rc = tc_conv_bf16(t.cout, t.cin, t.hw, np, dz, coutp, din.p, din.c, 0, E->wpt[l],
+                      narrow_n(t.hw, t.cin, din.c), E->ep_one_t[l], E->ep_zero[l], 1.0f, st, zp);
     if (rc) return rc;
   }
   // wgrad from the layer input and dz (both NHWC, straight from the buffers)
   const Buf& in = E->B[P.in];
   size_t wsb = E->ws_bytes;
   // (straight into the parameter layout of T->grads)
-  return wgrad_bf16(in.p, t.cin, in.c, dz, t.cout, coutp, t.hw, np, T->grads + t.w, t.deconv ? 1 : 0,
-                    E->ws, &wsb, st);
+  return wgrad_bf16(in.p, t.cin, pad64(in.c), dz, t.cout, coutp, t.hw, np, T->grads + t.w,
+                    t.deconv ? 1 : 0, E->ws, &wsb, st, in.c, zp);
 }
 
 int up_bwd(TcEngine* E, int dcat, int c, int hw_in, int dlow, int64_t np, cudaStream_t st) {
@@ -1074,7 +1081,7 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
     const TL& t = T->L[16];
     const int gx = 1024;
     k_head<<<gx, 256, 0, st>>>(E->B[A15].p, T->params + t.w, T->params + t.b, y, n, np,
-                               1.0 / double(n * 3 * 1024), E->B[DA15].p, E->part);
+                               1.0 / double(n * 3 * 1024), E->B[DA15].p, E->part, E->B[A15].c);
     TC_CHECK("k_head");
     k_reduce_parts<<<nb_slots(HEAD_SLOTS), 256, 0, st>>>(E->part, gx, HEAD_SLOTS, E->sums);
     TC_CHECK("k_reduce_parts");
@@ -1145,14 +1152,15 @@ extern "C" int drcb_trainer_debug_z(DrcbTrainer* T, int32_t layer, void* dst, vo
   using namespace drcb::train;
   if (!T || !dst || layer < 0 || layer > 16) return fail(DRCB_ECONTRACT, "drcb_trainer_debug_z: bad arguments");
   if (!T->tc) return fail(DRCB_ECONTRACT, "drcb_trainer_debug_z: no tensor-core step has run");
-  if (layer == 16) {  // the head's input (head.deconv2's BN + LeakyReLU output, 64-channel padded)
-    DRCB_CUDA(cudaMemcpyAsync(dst, T->tc->B[A15].p, size_t(T->tc->cap) * 1024 * 64 * 2,
-                              cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
-    return 0;
-  }
-  const TL& t = T->L[layer];
-  const size_t bytes = size_t(T->tc->cap) * t.hw * t.hw * pad64(t.cout) * 2;
-  DRCB_CUDA(cudaMemcpyAsync(dst, T->tc->Z[layer], bytes, cudaMemcpyDeviceToDevice,
-                            static_cast<cudaStream_t>(stream)));
+  // (the tensor unpacked into 64-channel padded rows, zeros in the padding)
+  const bool head = layer == 16;
+  const TL& t = T->L[head ? 15 : layer];
+  const int cp = pad64(t.cout), zp = zpitch(t.cout);
+  const size_t rows = size_t(T->tc->cap) * t.hw * t.hw;
+  const void* src = head ? static_cast<const void*>(T->tc->B[A15].p) : T->tc->Z[layer];
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (zp < cp) DRCB_CUDA(cudaMemsetAsync(dst, 0, rows * cp * 2, s));
+  DRCB_CUDA(cudaMemcpy2DAsync(dst, size_t(cp) * 2, src, size_t(zp) * 2, size_t(zp) * 2, rows,
+                              cudaMemcpyDeviceToDevice, s));
   return 0;
 }

@@ -38,9 +38,9 @@
 namespace drcb {
 namespace tc {
 int encode_act(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
-               int box_w, int box_h, int box_n, int c_dim = 0);
+               int box_w, int box_h, int box_n, int c_dim = 0, int pitch = 0);
 int encode_act_c(CUtensorMap* m, const void* base, int kind, int c_tot, int hw, int64_t nmaps,
-                 int box_c, int box_w, int box_h, int box_n);
+                 int box_c, int box_w, int box_h, int box_n, int pitch = 0);
 }  // namespace tc
 
 namespace wg {
@@ -441,8 +441,12 @@ __global__ void k_wgrad_reduce(const WgArgs a, int cin, int cout, int deconv, fl
 // fp32 (cout, cin, 3, 3), or with `deconv` the transposed conv's parameter
 // layout (cin, cout, 3, 3) flipped. `ws` / `ws_bytes`: scratch for the
 // split-K partials (query with ws == nullptr: ws_bytes receives the size).
+// x_pitch / dz_pitch (0 = cin_pad / cout_pad): elements between pixels of a
+// tensor stored narrower than its 64-channel blocks (the missing channels
+// load as zeros)
 int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, int cout_pad, int hw,
-               int64_t nmaps, float* dwf, int deconv, void* ws, size_t* ws_bytes, cudaStream_t st) {
+               int64_t nmaps, float* dwf, int deconv, void* ws, size_t* ws_bytes, cudaStream_t st,
+               int x_pitch, int dz_pitch) {
   using namespace wg;
   if (cin_pad % 64 || cout_pad % 64 || (hw != 4 && hw != 8 && hw != 16 && hw != 32))
     return fail(DRCB_ECONFIG, "wgrad: channels must be padded to 64, hw in {4, 8, 16, 32}");
@@ -507,9 +511,9 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
     a.zero_off = a.dz_stages * stb;
     const size_t smem = 1024 + size_t(a.zero_off) + BOX + 256;
     CUtensorMap mX, mDZ;
-    int rc = tc::encode_act(&mX, x, 0, cin_pad, hw, nmaps, hw, a.rb + 2, 1);
+    int rc = tc::encode_act(&mX, x, 0, cin_pad, hw, nmaps, hw, a.rb + 2, 1, 0, x_pitch);
     if (rc) return rc;
-    rc = tc::encode_act_c(&mDZ, dz, 0, cout_pad, hw, nmaps, nb, hw, a.rb, 1);
+    rc = tc::encode_act_c(&mDZ, dz, 0, cout_pad, hw, nmaps, nb, hw, a.rb, 1, dz_pitch);
     if (rc) return rc;
     const unsigned grid = unsigned(a.units * a.splits);
     if (nb == 16) {
@@ -538,9 +542,9 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
   const size_t smem = 1024 + size_t(a.dz_stages) * DZB + size_t(a.x_stages) * 2 * BOX + 256;
   CUtensorMap mX, mDZ;
   const int bw = hw, bh = a.rb, bn = a.mb;
-  int rc = tc::encode_act(&mX, x, 0, cin_pad, hw, nmaps, bw, bh, bn);
+  int rc = tc::encode_act(&mX, x, 0, cin_pad, hw, nmaps, bw, bh, bn, 0, x_pitch);
   if (rc) return rc;
-  rc = tc::encode_act(&mDZ, dz, 0, cout_pad, hw, nmaps, bw, bh, bn);
+  rc = tc::encode_act(&mDZ, dz, 0, cout_pad, hw, nmaps, bw, bh, bn, 0, dz_pitch);
   if (rc) return rc;
   static DeviceFlags attr;
   smem_attr_once(attr, k_wgrad, 227 * 1024);
@@ -578,11 +582,11 @@ extern "C" int drcb_debug_wgrad(int32_t cin, int32_t cout, int32_t hw, int64_t n
   cudaMemcpy(dx, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dd, hz.data(), hz.size() * 2, cudaMemcpyHostToDevice);
   size_t wsb = 0;
-  int rc = wgrad_bf16(dx, cin, cinp, dd, cout, coutp, hw, n, dwf, 0, nullptr, &wsb, 0);
+  int rc = wgrad_bf16(dx, cin, cinp, dd, cout, coutp, hw, n, dwf, 0, nullptr, &wsb, 0, 0, 0);
   if (!rc) {
     if (cudaMalloc(&ws, wsb) != cudaSuccess) rc = fail(DRCB_ECUDA, "cudaMalloc wgrad scratch");
   }
-  if (!rc) rc = wgrad_bf16(dx, cin, cinp, dd, cout, coutp, hw, n, dwf, 0, ws, &wsb, 0);
+  if (!rc) rc = wgrad_bf16(dx, cin, cinp, dd, cout, coutp, hw, n, dwf, 0, ws, &wsb, 0, 0, 0);
   if (!rc) {
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) rc = cuda_fail(e, "drcb_debug_wgrad");
