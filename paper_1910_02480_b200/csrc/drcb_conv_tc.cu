@@ -613,10 +613,14 @@ __global__ void __launch_bounds__(PW ? ROWS_THREADS : RT_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       if (RES) {
+        // (several N tiles: the grid is a multiple of num_n_tiles, so this
+        // CTA's tiles all have N tile blockIdx.x % num_n_tiles: its weights)
+        const int nt_res = int(blockIdx.x) % p.num_n_tiles;
         mbar_expect_tx(wfull, uint32_t(n_wtiles * B_TILE));
         for (int cb = 0; cb < p.cblocks; ++cb)
           for (int t = 0; t < 9; ++t)
-            tma_load_2d(&mapB, wfull, wres + (cb * 9 + t) * B_TILE, (t * p.cblocks + cb) * CEL, 0);
+            tma_load_2d(&mapB, wfull, wres + (cb * 9 + t) * B_TILE, (t * p.cblocks + cb) * CEL,
+                        nt_res * BN);
       }
       int sa = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
@@ -2224,6 +2228,10 @@ int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorM
   const int nsm = sm_count();
   int tiles = a.num_m_tiles * a.num_n_tiles;
   int grid = tiles < nsm ? tiles : nsm;
+  // resident weights with several N tiles: a CTA keeps one N tile's weights,
+  // so the grid is a multiple of the N tiles (the schedule's stride then
+  // keeps every CTA on its N tile)
+  if (RES && a.num_n_tiles > 1) grid = std::min(a.num_m_tiles, nsm / a.num_n_tiles) * a.num_n_tiles;
   kern<<<grid, PW ? ROWS_THREADS : RT_THREADS, smem, st>>>(mA, mB, mO, mP, a, h);
   count_launch();
   cudaError_t e = cudaGetLastError();
@@ -2419,7 +2427,12 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     rz.o_bytes = pred ? 0 : BM * std::max(a.bn, ROW_BYTES / elem_bytes(KIND)) * elem_bytes(KIND);
     rz.p_bytes = (pool && rz.o_bytes) ? rz.o_bytes / 4 : 0;
     const int budget = 216 * 1024 - 2 * rz.o_bytes - 2 * rz.p_bytes;  // of 227 KB
-    const bool res = a.num_n_tiles == 1 && w_bytes + 3 * rz.a_bytes <= budget;
+    // resident weights: one N tile's weights per CTA (several N tiles: the
+    // dgrad of dec1.deconv1, 64 -> 192 channels; 1,101 -> ~830 us per 4,096
+    // samples against the streamed two-block kernel)
+    static const bool no_res_multi = getenv("DRCB_NO_RES_MULTI") != nullptr;
+    const bool res = (a.num_n_tiles == 1 || (!no_res_multi && a.num_n_tiles <= sm_count())) &&
+                     w_bytes + 3 * rz.a_bytes <= budget;
     if (res) {
       rz.sb = 1;
       rz.sa = std::min(8, (budget - w_bytes) / rz.a_bytes);
