@@ -2767,15 +2767,37 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
 
 // input already NHWC (n rounded up to 8 maps, channels padded to the K
 // granularity, zeros in the padding): used by the frame driver
+// Maps per forward pass: the layer chain runs over chunks of this many maps
+// (a multiple of 8; bounds the activation footprint, ~1.5 MB per map in
+// 16-bit). Measured inside the bench frame (config 3, 4,096 maps, fp16): one
+// pass 5.15-5.17 ms, two chunks of 2,048 5.23 ms, four of 1,024 5.47 ms
+// (standalone, tools/net_time.py, two chunks looked 6 % faster: it does not
+// carry over to the frame). DRCB_NET_CHUNK overrides (A/B).
+int64_t net_chunk() {
+  static const int64_t c = [] {
+    const char* e = getenv("DRCB_NET_CHUNK");
+    const int64_t v = e ? atoll(e) : 8192;
+    return std::max<int64_t>(8, v / 8 * 8);
+  }();
+  return c;
+}
+
 int forward_tc_nhwc(NetImpl& net, const void* x_nhwc, float* y, int64_t n, int mode,
                     cudaStream_t st) {
   keep_pool_memory();
-  switch (mode) {
-    case DRCB_NET_BF16: return tc::forward_kind<0>(net, nullptr, y, n, st, x_nhwc);
-    case DRCB_NET_TF32: return tc::forward_kind<1>(net, nullptr, y, n, st, x_nhwc);
-    case DRCB_NET_FP16: return tc::forward_kind<2>(net, nullptr, y, n, st, x_nhwc);
+  const int64_t chunk = net_chunk();
+  const size_t es = mode == DRCB_NET_TF32 ? 4 : 2;  // compact input: 8 channels per pixel
+  for (int64_t d = 0; d < n; d += chunk) {
+    const int64_t c = n - d < chunk ? n - d : chunk;
+    const void* xs = static_cast<const uint8_t*>(x_nhwc) + size_t(d) * 1024 * 8 * es;
+    float* ys = y + d * 3 * 1024;
+    int rc = mode == DRCB_NET_BF16   ? tc::forward_kind<0>(net, nullptr, ys, c, st, xs)
+             : mode == DRCB_NET_FP16 ? tc::forward_kind<2>(net, nullptr, ys, c, st, xs)
+             : mode == DRCB_NET_TF32 ? tc::forward_kind<1>(net, nullptr, ys, c, st, xs)
+                                     : fail(DRCB_ECONFIG, "unknown tensor-core net mode");
+    if (rc) return rc;
   }
-  return fail(DRCB_ECONFIG, "unknown tensor-core net mode");
+  return 0;
 }
 
 int tc_input_channels(int) { return 8; }  // compact NHWC input (7 + 1 zero channel)
@@ -2813,8 +2835,8 @@ int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int c
 int forward_tc(NetImpl& net, const float* x, float* y, int64_t n, int mode, cudaStream_t st) {
   if (n <= 0) return 0;
   keep_pool_memory();
-  // bound the activation footprint (~1.5 MB/map in bf16)
-  const int64_t chunk = 8192;
+  // (also bounds the activation footprint, ~1.5 MB/map in bf16)
+  const int64_t chunk = net_chunk();
   for (int64_t d = 0; d < n; d += chunk) {
     int64_t c = n - d < chunk ? n - d : chunk;
     const float* xs = x + d * 7 * 1024;
