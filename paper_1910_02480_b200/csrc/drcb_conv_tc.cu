@@ -2430,7 +2430,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     // resident weights: one N tile's weights per CTA (several N tiles: the
     // dgrad of dec1.deconv1, 64 -> 192 channels; 1,101 -> ~830 us per 4,096
     // samples against the streamed two-block kernel)
-    static const bool no_res_multi = getenv("DRCB_NO_RES_MULTI") != nullptr;
+    const bool no_res_multi = getenv("DRCB_NO_RES_MULTI") != nullptr;
     const bool res = (a.num_n_tiles == 1 || (!no_res_multi && a.num_n_tiles <= sm_count())) &&
                      w_bytes + 3 * rz.a_bytes <= budget;
     if (res) {

@@ -171,3 +171,22 @@ def test_bf16_step_graph_replays_the_eager_step():
     for name in pa:
         assert np.array_equal(pa[name], pb[name]), name
     assert a.steps_taken() == b.steps_taken() == 4
+
+
+def test_bf16_multi_n_resident_dgrad_is_bit_identical(monkeypatch):
+    """dec1.deconv1's dgrad (64 -> 192 channels, three N tiles) keeps one N
+    tile's weights resident per CTA; DRCB_NO_RES_MULTI streams them through
+    the two-block kernel instead. Same K order per output: identical bits
+    (loss, every gradient)."""
+    x, y = _batch(32, 3)
+    net = cnn.random_network(64, 8)
+    a = DeviceTrainer(net, lr=1e-3, mode="bf16")
+    la = a.step(x, y)
+    ga = a.grads()
+    monkeypatch.setenv("DRCB_NO_RES_MULTI", "1")
+    b = DeviceTrainer(net, lr=1e-3, mode="bf16")
+    lb = b.step(x, y)
+    gb = b.grads()
+    assert la == lb
+    for name in ga:
+        assert np.array_equal(ga[name], gb[name]), name
