@@ -2423,7 +2423,7 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     rz.row_bytes = hw * ROW_BYTES;
     rz.a_bytes = (a.rows_per_tile + 2) * hw * ROW_BYTES;
     int b_tile = a.bn * ROW_BYTES;
-    const int w_bytes = 9 * a.cblocks * b_tile;
+    int w_bytes = 9 * a.cblocks * b_tile;
     rz.o_bytes = pred ? 0 : BM * std::max(a.bn, ROW_BYTES / elem_bytes(KIND)) * elem_bytes(KIND);
     rz.p_bytes = (pool && rz.o_bytes) ? rz.o_bytes / 4 : 0;
     const int budget = 216 * 1024 - 2 * rz.o_bytes - 2 * rz.p_bytes;  // of 227 KB
@@ -2431,11 +2431,31 @@ int run_layer(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cou
     // dgrad of dec1.deconv1, 64 -> 192 channels; 1,101 -> ~830 us per 4,096
     // samples against the streamed two-block kernel)
     const bool no_res_multi = getenv("DRCB_NO_RES_MULTI") != nullptr;
-    const bool res = (a.num_n_tiles == 1 || (!no_res_multi && a.num_n_tiles <= sm_count())) &&
-                     w_bytes + 3 * rz.a_bytes <= budget;
+    bool res = (a.num_n_tiles == 1 || (!no_res_multi && a.num_n_tiles <= sm_count())) &&
+               w_bytes + 3 * rz.a_bytes <= budget;
+    int budget_res = budget;
+    // weights that do not fit at 3 A stages: 64-wide N tiles with at least
+    // DRCB_RES_STAGES A stages (default 2) may (the 16x16 convs with 128
+    // input channels: 144 KB per N tile; dec2.deconv1's dgrad, 128 -> 384
+    // channels, 880 -> 695 us; the 128 -> 128 ones 293 -> 234 us, B = 4,096)
+    if (!res && !no_res_multi && KIND != 1 && dx && a.bn >= 64 && !pool && !pred && !up) {
+      const char* e = getenv("DRCB_RES_STAGES");
+      const int min_st = e ? std::max(1, atoi(e)) : 2;
+      const int o64 = BM * 64 * elem_bytes(KIND), w64 = 9 * a.cblocks * 64 * ROW_BYTES;
+      const int bud64 = 216 * 1024 - 2 * o64;
+      if (w64 + min_st * rz.a_bytes <= bud64) {
+        a.bn = 64;
+        a.num_n_tiles = L.cout_pad / 64;
+        b_tile = 64 * ROW_BYTES;
+        rz.o_bytes = o64;
+        budget_res = bud64;
+        w_bytes = w64;
+        res = true;
+      }
+    }
     if (res) {
       rz.sb = 1;
-      rz.sa = std::min(8, (budget - w_bytes) / rz.a_bytes);
+      rz.sa = std::min(8, (budget_res - w_bytes) / rz.a_bytes);
     } else if (dx) {
       // B triples are consumed three per A box
       rz.sa = std::min(4, std::max(2, budget / (4 * rz.a_bytes)));
