@@ -18,7 +18,11 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "drcb_train.h"
 
@@ -916,8 +920,32 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
 }
 
 // reduction geometry over npx pixels: pixels per block and blocks
-inline void red_geom(int64_t npx, int ctiles, int64_t& ppb, int& gx) {
-  const int64_t target = std::max<int64_t>(1, int64_t(sm_count()) * 8 / ctiles);
+// resident blocks per SM of a 256-thread reduction kernel on this device
+inline int resident_blocks(const void* kern) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find({dev, kern});
+  if (it != cache.end()) return it->second;
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0) != cudaSuccess || b < 1) b = 1;
+  cache[{dev, kern}] = b;
+  return b;
+}
+
+// reduction geometry over npx pixels: pixels per block and blocks. With
+// `kern` given, the grid is whole waves of that kernel's resident blocks
+// (DRCB_RED_WAVES, default 2) instead of 8 blocks per SM: a partial last wave
+// left SMs idle at the end of every pass.
+inline void red_geom(int64_t npx, int ctiles, int64_t& ppb, int& gx, const void* kern = nullptr) {
+  static const int waves = [] {
+    const char* e = getenv("DRCB_RED_WAVES");
+    return e ? atoi(e) : 2;
+  }();
+  const int per_sm = (kern && waves > 0) ? waves * resident_blocks(kern) : 8;
+  const int64_t target = std::max<int64_t>(1, int64_t(sm_count()) * per_sm / ctiles);
   ppb = std::max<int64_t>(128, (npx + target - 1) / target);
   ppb = (ppb + 127) / 128 * 128;
   gx = int((npx + ppb - 1) / ppb);
@@ -963,7 +991,7 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   int64_t ppb;
   int gx;
   const int cg = chan_groups(t.cout);
-  red_geom(n * hw2, coutp / 64, ppb, gx);
+  red_geom(n * hw2, coutp / 64, ppb, gx, reinterpret_cast<const void*>(k_bn_stats<8>));
   switch (cg) {
     case 2: k_bn_stats<2><<<dim3(gx, 1), 256, 0, st>>>(E->Z[l], zp, coutp, n * hw2, ppb, E->part); break;
     case 4: k_bn_stats<4><<<dim3(gx, 1), 256, 0, st>>>(E->Z[l], zp, coutp, n * hw2, ppb, E->part); break;
@@ -1014,7 +1042,7 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   int64_t ppb;
   int gx;
   const int cg = chan_groups(t.cout);
-  red_geom(n * hw2, coutp / 64, ppb, gx);
+  red_geom(n * hw2, coutp / 64, ppb, gx, reinterpret_cast<const void*>(k_bnb_stats<8>));
   const dim3 gs(gx, cg < 8 ? 1 : coutp / 64);
   switch (cg) {
     case 2: k_bnb_stats<2><<<gs, 256, 0, st>>>(E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
@@ -1041,7 +1069,7 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   }
   int64_t ppb2;
   int gx2;
-  red_geom(np * hw2, coutp / 64, ppb2, gx2);
+  red_geom(np * hw2, coutp / 64, ppb2, gx2, reinterpret_cast<const void*>(k_bnb_apply<8>));
   bf16* dz = E->B[DZ].p;
   // (a narrow layer's dz is stored at its own width: its dgrad and wgrad
   // load it into 64-channel / narrow boxes through the TMA zero fill)
