@@ -213,7 +213,19 @@ __global__ void k_reduce_parts(const double* __restrict__ part, int nparts, int 
   const int s = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   if (s >= nslots) return;
   double a = 0.0;
-  for (int b = lane; b < nparts; b += 32) a += part[int64_t(s) * nparts + b];
+  {
+    // (four loads in flight ahead of the in-order adds: same sums, same bits)
+    const double* q = part + int64_t(s) * nparts;
+    int b = lane;
+    for (; b + 96 < nparts; b += 128) {
+      const double v0 = q[b], v1 = q[b + 32], v2 = q[b + 64], v3 = q[b + 96];
+      a += v0;
+      a += v1;
+      a += v2;
+      a += v3;
+    }
+    for (; b < nparts; b += 32) a += q[b];
+  }
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
   if (lane == 0) {
     out[s] = a;
@@ -308,9 +320,27 @@ __global__ void k_reduce_fin(const double* __restrict__ part, int nparts, int n,
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   if (i >= n) return;
   double a = 0.0, b = 0.0;
-  for (int k = lane; k < nparts; k += 32) {
-    a += part[int64_t(i) * nparts + k];
-    b += part[int64_t(f.cpad + i) * nparts + k];
+  {
+    // (four loads per sum in flight ahead of the in-order adds: same bits)
+    const double* qa = part + int64_t(i) * nparts;
+    const double* qb = part + int64_t(f.cpad + i) * nparts;
+    int k = lane;
+    for (; k + 96 < nparts; k += 128) {
+      const double a0 = qa[k], a1 = qa[k + 32], a2 = qa[k + 64], a3 = qa[k + 96];
+      const double b0 = qb[k], b1 = qb[k + 32], b2 = qb[k + 64], b3 = qb[k + 96];
+      a += a0;
+      a += a1;
+      a += a2;
+      a += a3;
+      b += b0;
+      b += b1;
+      b += b2;
+      b += b3;
+    }
+    for (; k < nparts; k += 32) {
+      a += qa[k];
+      b += qb[k];
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     a += __shfl_xor_sync(0xffffffffu, a, o);
