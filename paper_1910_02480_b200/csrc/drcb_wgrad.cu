@@ -505,8 +505,28 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
     const char* e = getenv("DRCB_WGRAD_MINCHUNKS");
     return e ? std::max(1, atoi(e)) : 8;
   }();
-  a.splits = std::max(1, std::min((a.chunks + min_chunks - 1) / min_chunks,
-                                  (2 * nsm + a.units - 1) / a.units));
+  // Both kernels hold one CTA per SM (their SMEM plans): the grid runs in
+  // waves of nsm CTAs, so the split count is chosen for the fewest waves per
+  // unit of work, ceil(units * s / nsm) / s, over s up to two waves' worth
+  // (the old rounding, ceil(2 nsm / units) splits, left a one-CTA third wave
+  // for 297 = 2 x 148 + 1 CTAs: dec1.deconv1 with 3 units, dec3.deconv1 27)
+  const int s_chunks = std::max(1, (a.chunks + min_chunks - 1) / min_chunks);
+  static const bool old_splits = getenv("DRCB_WGRAD_OLD_SPLITS") != nullptr;
+  if (old_splits) {
+    a.splits = std::max(1, std::min(s_chunks, (2 * nsm + a.units - 1) / a.units));
+  } else {
+    const int s_max = std::max(1, std::min(s_chunks, (2 * nsm + a.units - 1) / a.units));
+    int best = 1;
+    double best_cost = 1e30;
+    for (int sp = 1; sp <= s_max; ++sp) {
+      const double cost = double((int64_t(a.units) * sp + nsm - 1) / nsm) / sp;
+      if (cost < best_cost * (1.0 - 1e-9)) {
+        best_cost = cost;
+        best = sp;
+      }
+    }
+    a.splits = best;
+  }
   const size_t part = dxn ? size_t(a.splits) * a.units * 2 * 128 * (3 * nb) * 4
                           : size_t(a.splits) * a.units * a.n_acc * 128 * a.n_tile * 4;
   if (!ws) {
