@@ -86,8 +86,9 @@ __device__ __forceinline__ void round8(float (&f)[8]) {  // the stored (bf16) va
 }
 
 // ---------------------------------------------------------------------------
-// input (n,7,32,32) fp32 NCHW -> X0 (np,32,32,64) bf16 NHWC: channels 0..6,
-// zeros in channel 7 and in the maps beyond n (channels 8..63 are zeroed once)
+// input (n,7,32,32) fp32 NCHW -> X0 (np,32,32,8) bf16 NHWC: channels 0..6,
+// zeros in channel 7 and in the maps beyond n (stored 8 channels wide: the
+// convs load it into 64-channel boxes through the TMA zero fill)
 __global__ void k_x_in(const float* __restrict__ x, int64_t n, int64_t np, bf16* __restrict__ out) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= np * 1024) return;
@@ -96,7 +97,7 @@ __global__ void k_x_in(const float* __restrict__ x, int64_t n, int64_t np, bf16*
   float f[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) f[c] = (c < 7 && m < n) ? __ldg(x + (m * 7 + c) * 1024 + p) : 0.f;
-  st8(out + i * 64, f);
+  st8(out + i * 8, f);
 }
 
 // Every layer's step operands straight from the fp32 master parameters, in
@@ -868,7 +869,7 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
   E = T->tc = new TcEngine();
   E->cap = np;
   const int spec[NBUF][2] = {
-      {64, 32}, {64, 32}, {192, 32}, {64, 16}, {128, 16}, {384, 16}, {128, 8}, {256, 8}, {768, 8},
+      {8, 32}, {64, 32}, {192, 32}, {64, 16}, {128, 16}, {384, 16}, {128, 8}, {256, 8}, {768, 8},
       {256, 4}, {512, 4}, {512, 4}, {256, 8}, {256, 8}, {128, 16}, {128, 16}, {64, 32}, {64, 32},
       {32, 32}, {16, 32},  // A14, A15: the head's 32- / 16-channel layers stored at that width
       {64, 32},            // DZ: the largest cout_pad * hw^2 (64 * 1024)
