@@ -2203,13 +2203,24 @@ int prepare_layer(NetImpl& net, ConvLayer& L, int kind) {
   return 0;
 }
 
+// SMs the persistent tensor-core kernels spread over (DRCB_CONV_SMS caps it:
+// an A/B of the U-Net's throughput on fewer SMs under the power limit)
+inline int conv_sms() {
+  const int nsm = sm_count();
+  static const int cap = [] {
+    const char* e = getenv("DRCB_CONV_SMS");
+    return e ? atoi(e) : 0;
+  }();
+  return cap > 0 ? std::min(cap, nsm) : nsm;
+}
+
 template <int KIND, int BN, int STAGES>
 int launch_bn(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, cudaStream_t st) {
   using SM = Smem<KIND, BN, STAGES>;
   auto kern = k_conv_tc<KIND, BN, STAGES>;
   static DeviceFlags attr;
   smem_attr_once(attr, kern, SM::TOTAL);
-  const int nsm = sm_count();
+  const int nsm = conv_sms();
   int tiles = a.num_m_tiles * a.num_n_tiles;
   int grid = tiles < nsm ? tiles : nsm;
   kern<<<grid, NUM_THREADS, SM::TOTAL, st>>>(mA, mB, a);
@@ -2225,7 +2236,7 @@ int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorM
   auto kern = k_conv_rows<KIND, BN, RES, DX, MH, PW>;
   static DeviceFlags attr;
   smem_attr_once(attr, kern, 227 * 1024);
-  const int nsm = sm_count();
+  const int nsm = conv_sms();
   int tiles = a.num_m_tiles * a.num_n_tiles;
   int grid = tiles < nsm ? tiles : nsm;
   // resident weights with several N tiles: a CTA keeps one N tile's weights,
@@ -2244,7 +2255,7 @@ int launch_pair64(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMa
   auto kern = k_conv_pair<KIND, 64, RES>;
   static DeviceFlags attr;
   smem_attr_once(attr, kern, 227 * 1024);
-  const int nsm = sm_count();
+  const int nsm = conv_sms();
   const int pairs = std::min(a.num_m_tiles, nsm / 2);
   kern<<<2 * pairs, RT_THREADS, smem, st>>>(mA, mB, mO, a, h);
   count_launch();
@@ -2360,7 +2371,7 @@ int run_in8(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cout_
   constexpr size_t smem = in8_smem<KIND>();
   static DeviceFlags attr;
   smem_attr_once(attr, kern, int(smem));
-  const int nsm = sm_count();
+  const int nsm = conv_sms();
   int grid = a.num_m_tiles < nsm ? a.num_m_tiles : nsm;
   kern<<<grid, IN8_THREADS, smem, st>>>(mX, mB, mO, a);
   count_launch();
@@ -2664,7 +2675,7 @@ int run_head_fused(NetImpl& net, ConvLayer& L1, ConvLayer& L2, const Buf& in, in
   constexpr size_t smem = head_fused_smem();
   static DeviceFlags attr;
   smem_attr_once(attr, k_head_fused<KIND>, int(smem));
-  const int nsm = sm_count();
+  const int nsm = conv_sms();
   const int grid = nmaps < nsm ? int(nmaps) : nsm;  // whole maps per CTA
   k_head_fused<KIND><<<grid, RT_THREADS, smem, st>>>(mA10, mA6, mW1, mW2, p1, p2, int(nmaps));
   count_launch();
