@@ -968,12 +968,13 @@ inline int resident_blocks(const void* kern) {
 
 // reduction geometry over npx pixels: pixels per block and blocks. With
 // `kern` given, the grid is whole waves of that kernel's resident blocks
-// (DRCB_RED_WAVES, default 2) instead of 8 blocks per SM: a partial last wave
-// left SMs idle at the end of every pass.
+// (DRCB_RED_WAVES, default 1; 2 / 4 waves measured 0.1 / 0.4 ms slower per
+// B = 4,096 step) instead of 8 blocks per SM: a partial last wave left SMs
+// idle at the end of every pass.
 inline void red_geom(int64_t npx, int ctiles, int64_t& ppb, int& gx, const void* kern = nullptr) {
   static const int waves = [] {
     const char* e = getenv("DRCB_RED_WAVES");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 1;
   }();
   const int per_sm = (kern && waves > 0) ? waves * resident_blocks(kern) : 8;
   const int64_t target = std::max<int64_t>(1, int64_t(sm_count()) * per_sm / ctiles);
