@@ -2863,6 +2863,29 @@ int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int c
   return tc::run_layer<0>(net, L, bi, bo, out_coff, nmaps, st);
 }
 
+// enc1.conv1 of the training engine through the inference in8 kernel: the
+// 8-channel NHWC input (x0), weights packed [64][128] with K index tap * 8 +
+// channel (zeros beyond 72), epilogue y = acc * a + b then LeakyReLU(slope)
+int tc_conv_in8_bf16(int64_t nmaps, const void* in, void* out, int out_ctot, const void* w8,
+                     const float* ep_a, const float* ep_b, float slope, cudaStream_t st) {
+  NetImpl net;
+  net.slope = slope;
+  ConvLayer L;
+  L.name = "enc1.conv1";
+  L.cin = 8;
+  L.cout = 64;
+  L.hw = 32;
+  L.in8 = true;
+  L.cin_pad = 128;
+  L.cout_pad = 64;
+  L.tc_kind = 0;
+  L.d_wtc = const_cast<void*>(w8);
+  L.d_ep_a = const_cast<float*>(ep_a);
+  L.d_ep_b = const_cast<float*>(ep_b);
+  tc::Buf bi{const_cast<void*>(in), 8, 32}, bo{out, out_ctot, 32};
+  return tc::run_in8<0>(net, L, bi, bo, 0, nmaps, st);
+}
+
 int forward_tc(NetImpl& net, const float* x, float* y, int64_t n, int mode, cudaStream_t st) {
   if (n <= 0) return 0;
   keep_pool_memory();

@@ -31,6 +31,8 @@ namespace drcb {
 int tc_conv_bf16(int cin, int cout, int hw, int64_t nmaps, const void* in, int cin_pad, void* out,
                  int out_ctot, int out_coff, const void* wpacked, int cout_pad, const float* ep_a,
                  const float* ep_b, float slope, cudaStream_t st, int in_pitch);
+int tc_conv_in8_bf16(int64_t nmaps, const void* in, void* out, int out_ctot, const void* w8,
+                     const float* ep_a, const float* ep_b, float slope, cudaStream_t st);
 int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, int cout_pad, int hw,
                int64_t nmaps, float* dwf, int deconv, void* ws, size_t* ws_bytes, cudaStream_t st,
                int x_pitch, int dz_pitch);
@@ -157,6 +159,16 @@ __global__ void k_prep_weights(const __grid_constant__ PrepArgs a) {
   }
   j -= 2 * nf;
   t.ep_b[j] = j < t.cout ? t.b[j] : 0.f;
+}
+
+// enc1.conv1's weights in the in8 kernel's layout: w8[co][tap * 8 + ci]
+// (bf16, zeros for ci >= cin and K >= 72), from the conv-form fp32 w[co][ci][tap]
+__global__ void k_prep_in8(const float* __restrict__ w, int cin, int cout, bf16* __restrict__ w8) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 64 * 128) return;
+  const int co = i / 128, kk = i % 128, t = kk / 8, ci = kk % 8;
+  const float v = (co < cout && t < 9 && ci < cin) ? w[(int64_t(co) * cin + ci) * 9 + t] : 0.f;
+  w8[i] = __float2bfloat16_rn(v);
 }
 
 // padded epilogue vector: v[c] (or fill when v == NULL) for c < n, 0 beyond
@@ -834,6 +846,7 @@ struct TcEngine {
   Buf B[NBUF];
   bf16* Z[16] = {};
   bf16 *wpf[16] = {}, *wpt[16] = {};
+  bf16* w8 = nullptr;  // enc1.conv1 in the in8 kernel's layout
   float *ep_one_f[16] = {}, *ep_b[16] = {}, *ep_one_t[16] = {}, *ep_zero[16] = {};
   float* bnv[16] = {};  // per layer: s, t, mean, invstd, m1, m2, coef (7 x cout_pad)
   void* ws = nullptr;
@@ -917,6 +930,8 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
     if (rc) return rc;
     wsb = std::max(wsb, q);
   }
+  const size_t w8_off = wb;
+  wb += 64 * 128 * 2;
   const size_t ws_off = wb;
   wb += (wsb + 255) & ~size_t(255);
   const size_t part_off = wb;
@@ -941,6 +956,7 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
     k_pad_vec<<<nbk(coutp), 256, 0, st>>>(nullptr, t.cout, coutp, 1.f, E->ep_one_f[l]);
     k_pad_vec<<<nbk(cinp), 256, 0, st>>>(nullptr, t.cin, cinp, 1.f, E->ep_one_t[l]);
   }
+  E->w8 = reinterpret_cast<bf16*>(w + w8_off);
   E->ws = w + ws_off;
   E->ws_bytes = wsb;
   E->part = reinterpret_cast<double*>(w + part_off);
@@ -989,6 +1005,13 @@ inline void red_geom(int64_t npx, int ctiles, int64_t& ppb, int& gx, const void*
 // the next layer's K reads), instead of multiplying zero weight rows
 inline int narrow_n(int hw, int c, int c_pad) { return hw >= 16 && c < 64 ? (c + 15) / 16 * 16 : c_pad; }
 
+// enc1.conv1 forward through the in8 kernel (DRCB_TRAIN_NO_IN8: the row
+// kernel over a zero-filled 64-channel K block)
+inline bool use_in8(const DrcbTrainer* T) {
+  return T->L[0].cin <= 8 && T->L[0].cout == 64 && T->L[0].hw == 32 &&
+         getenv("DRCB_TRAIN_NO_IN8") == nullptr;
+}
+
 // nothing to all-reduce: the SyncBN sums are already the batch's
 inline bool one_rank(const DrcbTrainer* T) { return !T->reduce_fn && T->world == 1; }
 
@@ -1016,9 +1039,14 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   const LayerPlan& P = PLAN[l];
   const int coutp = pad64(t.cout), hw2 = t.hw * t.hw, zp = zpitch(t.cout);
   const Buf& in = E->B[P.in];
-  // (K blocks of 64 channels; a narrow input is read at its own pitch)
-  int rc = tc_conv_bf16(t.cin, t.cout, t.hw, np, in.p, pad64(in.c), E->Z[l], zp, 0, E->wpf[l],
-                        narrow_n(t.hw, t.cout, coutp), E->ep_one_f[l], E->ep_b[l], 1.0f, st, in.c);
+  // (K blocks of 64 channels; a narrow input is read at its own pitch;
+  // enc1.conv1 through the in8 kernel: K = 72 instead of a 64-channel block
+  // per tap of which 8 channels hold data)
+  int rc = (l == 0 && use_in8(T))
+               ? tc_conv_in8_bf16(np, in.p, E->Z[l], zp, E->w8, E->ep_one_f[l], E->ep_b[l], 1.0f, st)
+               : tc_conv_bf16(t.cin, t.cout, t.hw, np, in.p, pad64(in.c), E->Z[l], zp, 0, E->wpf[l],
+                              narrow_n(t.hw, t.cout, coutp), E->ep_one_f[l], E->ep_b[l], 1.0f, st,
+                              in.c);
   if (rc) return rc;
   int64_t ppb;
   int gx;
@@ -1178,6 +1206,11 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
     a.start[16] = tot;
     k_prep_weights<<<nbk(tot), 256, 0, st>>>(a);
     TC_CHECK("k_prep_weights");
+    if (use_in8(T)) {
+      const TL& t0 = T->L[0];
+      k_prep_in8<<<nbk(64 * 128), 256, 0, st>>>(T->params + t0.w, t0.cin, t0.cout, E->w8);
+      TC_CHECK("k_prep_in8");
+    }
   }
   k_x_in<<<nbk(np * 1024), 256, 0, st>>>(x, n, np, E->B[X0].p);
   TC_CHECK("k_x_in");
