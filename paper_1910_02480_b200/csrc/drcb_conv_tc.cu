@@ -241,6 +241,7 @@ template <int KIND, int BN, int STAGES>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ ConvArgs p) {
+  pdl_wait();
   using SM = Smem<KIND, BN, STAGES>;
   constexpr int UMMA_KSTEPS = ROW_BYTES / 32;  // 32 B of K per MMA for both kinds
   constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
@@ -530,6 +531,7 @@ __global__ void __launch_bounds__(PW ? ROWS_THREADS : RT_THREADS, 1)
     k_conv_rows(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapP,
                 const __grid_constant__ ConvArgs p, const __grid_constant__ RowArgs h) {
+  pdl_wait();
   constexpr int B_TILE = BN * ROW_BYTES;
   constexpr int B3 = 3 * B_TILE;                       // one B stage: three weight tiles
   constexpr int ELEM = elem_bytes(KIND);
@@ -1029,6 +1031,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
     k_head_fused(const __grid_constant__ CUtensorMap mapA10, const __grid_constant__ CUtensorMap mapA6,
                  const __grid_constant__ CUtensorMap mapW1, const __grid_constant__ CUtensorMap mapW2,
                  const __grid_constant__ ConvArgs p1, const __grid_constant__ ConvArgs p2, int nmaps) {
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* w1 = smem;
@@ -1323,6 +1326,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RT_THREADS, 1)
     k_conv_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 const __grid_constant__ CUtensorMap mapO, const __grid_constant__ ConvArgs p,
                 const __grid_constant__ RowArgs h) {
+  pdl_wait();
   static_assert(KIND != 1, "16-bit operands");
   constexpr int ELEM = 2;
   constexpr int CEL = ROW_BYTES / ELEM;
@@ -1552,6 +1556,7 @@ template <int KIND>
 __global__ void __launch_bounds__(IN8_THREADS, 1)
     k_conv_in8(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapB,
                const __grid_constant__ CUtensorMap mapO, const __grid_constant__ ConvArgs p) {
+  pdl_wait();
   constexpr int ELEM = elem_bytes(KIND);
   constexpr int PX_BYTES = 8 * ELEM;                  // one input pixel
   constexpr int PPT = PX_BYTES / 16;                  // 16-B pieces per tap
@@ -1859,6 +1864,7 @@ __device__ __forceinline__ uint4 pack<float>(const float* f) {
 template <typename T>
 __global__ void k_stack_to_nhwc(const float* __restrict__ x, int64_t n, int64_t n_pad, int,
                                 T* __restrict__ out) {
+  pdl_wait();
   constexpr int V = Vec<T>::N;   // channels per 16-B piece
   constexpr int PP = 8 / V;      // pieces per pixel
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1882,6 +1888,7 @@ __global__ void k_stack_to_nhwc(const float* __restrict__ x, int64_t n, int64_t 
 template <typename T, int HW_OUT, int C>
 __global__ void __launch_bounds__(256) k_pool_nhwc(const T* __restrict__ in, int c_tot, int off,
                                                    T* __restrict__ out, int64_t nmaps) {
+  pdl_wait();
   constexpr int V = Vec<T>::N;
   constexpr int G = C / V;          // 16 B groups per pixel
   constexpr int GPT = G >= 4 ? 4 : G;  // groups per thread
@@ -1917,6 +1924,7 @@ __global__ void __launch_bounds__(256) k_pool_nhwc(const T* __restrict__ in, int
 template <typename T, int HW_IN, int C>
 __global__ void __launch_bounds__(256) k_up_nhwc(const T* __restrict__ in, T* __restrict__ out,
                                                  int c_tot, int64_t nmaps) {
+  pdl_wait();
   constexpr int V = Vec<T>::N;
   constexpr int G = C / V;
   constexpr int HO = 2 * HW_IN;
@@ -1997,14 +2005,14 @@ void launch_pool(const T* in, int c_tot, int off, T* out, int64_t nmaps, cudaStr
   constexpr int G = C / Vec<T>::N;
   constexpr int TPP = G / (G >= 4 ? 4 : G);
   int64_t tot = nmaps * HW_OUT * HW_OUT * TPP;
-  k_pool_nhwc<T, HW_OUT, C><<<unsigned((tot + 255) / 256), 256, 0, st>>>(in, c_tot, off, out, nmaps);
+  launch_pdl(k_pool_nhwc<T, HW_OUT, C>, unsigned((tot + 255) / 256), 256, 0, st, in, c_tot, off, out, nmaps);
   count_launch();
 }
 
 template <typename T, int HW_IN, int C>
 void launch_up(const T* in, T* out, int c_tot, int64_t nmaps, cudaStream_t st) {
   int64_t tot = nmaps * HW_IN * HW_IN * (C / Vec<T>::N);
-  k_up_nhwc<T, HW_IN, C><<<unsigned((tot + 255) / 256), 256, 0, st>>>(in, out, c_tot, nmaps);
+  launch_pdl(k_up_nhwc<T, HW_IN, C>, unsigned((tot + 255) / 256), 256, 0, st, in, out, c_tot, nmaps);
   count_launch();
 }
 
@@ -2223,7 +2231,7 @@ int launch_bn(const CUtensorMap& mA, const CUtensorMap& mB, const ConvArgs& a, c
   const int nsm = conv_sms();
   int tiles = a.num_m_tiles * a.num_n_tiles;
   int grid = tiles < nsm ? tiles : nsm;
-  kern<<<grid, NUM_THREADS, SM::TOTAL, st>>>(mA, mB, a);
+  launch_pdl(kern, grid, NUM_THREADS, SM::TOTAL, st, mA, mB, a);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_tc");
@@ -2243,7 +2251,7 @@ int launch_rows_bn(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorM
   // so the grid is a multiple of the N tiles (the schedule's stride then
   // keeps every CTA on its N tile)
   if (RES && a.num_n_tiles > 1) grid = std::min(a.num_m_tiles, nsm / a.num_n_tiles) * a.num_n_tiles;
-  kern<<<grid, PW ? ROWS_THREADS : RT_THREADS, smem, st>>>(mA, mB, mO, mP, a, h);
+  launch_pdl(kern, grid, PW ? ROWS_THREADS : RT_THREADS, smem, st, mA, mB, mO, mP, a, h);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_rows");
@@ -2257,7 +2265,7 @@ int launch_pair64(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMa
   smem_attr_once(attr, kern, 227 * 1024);
   const int nsm = conv_sms();
   const int pairs = std::min(a.num_m_tiles, nsm / 2);
-  kern<<<2 * pairs, RT_THREADS, smem, st>>>(mA, mB, mO, a, h);
+  launch_pdl(kern, 2 * pairs, RT_THREADS, smem, st, mA, mB, mO, a, h);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_pair");
@@ -2373,7 +2381,7 @@ int run_in8(NetImpl& net, ConvLayer& L, const Buf& in, const Buf& out, int cout_
   smem_attr_once(attr, kern, int(smem));
   const int nsm = conv_sms();
   int grid = a.num_m_tiles < nsm ? a.num_m_tiles : nsm;
-  kern<<<grid, IN8_THREADS, smem, st>>>(mX, mB, mO, a);
+  launch_pdl(kern, grid, IN8_THREADS, smem, st, mX, mB, mO, a);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_conv_in8");
@@ -2677,7 +2685,7 @@ int run_head_fused(NetImpl& net, ConvLayer& L1, ConvLayer& L2, const Buf& in, in
   smem_attr_once(attr, k_head_fused<KIND>, int(smem));
   const int nsm = conv_sms();
   const int grid = nmaps < nsm ? int(nmaps) : nsm;  // whole maps per CTA
-  k_head_fused<KIND><<<grid, RT_THREADS, smem, st>>>(mA10, mA6, mW1, mW2, p1, p2, int(nmaps));
+  launch_pdl(k_head_fused<KIND>, grid, RT_THREADS, smem, st, mA10, mA6, mW1, mW2, p1, p2, int(nmaps));
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_head_fused");
@@ -2730,7 +2738,7 @@ int forward_kind(NetImpl& net, const float* x, float* y, int64_t n, cudaStream_t
     B[0].p = const_cast<void*>(x_nhwc);
   } else {
     int64_t tot = np * 1024 * (8 / Vec<T>::N);
-    k_stack_to_nhwc<T><<<unsigned((tot + 255) / 256), 256, 0, st>>>(x, n, np, B[0].c, (T*)B[0].p);
+    launch_pdl(k_stack_to_nhwc<T>, unsigned((tot + 255) / 256), 256, 0, st, x, n, np, B[0].c, (T*)B[0].p);
     count_launch();
   }
   auto pool = [&](const Buf& in, int off_c, int c, const Buf& out) {

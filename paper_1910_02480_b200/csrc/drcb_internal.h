@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -34,6 +36,36 @@ struct DeviceFlags {
   bool test(int dev) const { return (bits.load(std::memory_order_acquire) >> (dev & 63)) & 1; }
   void set(int dev) { bits.fetch_or(uint64_t(1) << (dev & 63), std::memory_order_release); }
 };
+// Programmatic dependent launch: the tensor-core and training kernels are
+// launched with cudaLaunchAttributeProgrammaticStreamSerialization and begin
+// with pdl_wait() (griddepcontrol.wait: returns once the preceding kernel of
+// the stream has completed and its writes are visible), so a kernel's launch
+// and block scheduling overlap its predecessor's tail instead of following
+// it. Every kernel launched this way waits before touching memory; a kernel
+// launched plainly executes the wait as a no-op. DRCB_NO_PDL turns it off.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
+inline bool pdl_enabled() {
+  static const bool on = getenv("DRCB_NO_PDL") == nullptr;
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
 template <class K>
 inline void smem_attr_once(DeviceFlags& f, K kern, int bytes) {

@@ -92,6 +92,7 @@ __device__ __forceinline__ void round8(float (&f)[8]) {  // the stored (bf16) va
 // zeros in channel 7 and in the maps beyond n (stored 8 channels wide: the
 // convs load it into 64-channel boxes through the TMA zero fill)
 __global__ void k_x_in(const float* __restrict__ x, int64_t n, int64_t np, bf16* __restrict__ out) {
+  pdl_wait();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= np * 1024) return;
   const int64_t m = i / 1024;
@@ -121,6 +122,7 @@ struct PrepArgs {
 };
 
 __global__ void k_prep_weights(const __grid_constant__ PrepArgs a) {
+  pdl_wait();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= a.start[16]) return;
   int l = 0;
@@ -164,6 +166,7 @@ __global__ void k_prep_weights(const __grid_constant__ PrepArgs a) {
 // enc1.conv1's weights in the in8 kernel's layout: w8[co][tap * 8 + ci]
 // (bf16, zeros for ci >= cin and K >= 72), from the conv-form fp32 w[co][ci][tap]
 __global__ void k_prep_in8(const float* __restrict__ w, int cin, int cout, bf16* __restrict__ w8) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 64 * 128) return;
   const int co = i / 128, kk = i % 128, t = kk / 8, ci = kk % 8;
@@ -173,6 +176,7 @@ __global__ void k_prep_in8(const float* __restrict__ w, int cin, int cout, bf16*
 
 // padded epilogue vector: v[c] (or fill when v == NULL) for c < n, 0 beyond
 __global__ void k_pad_vec(const float* __restrict__ v, int n, int np, float fill, float* out) {
+  pdl_wait();
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < np) out[c] = c < n ? (v ? v[c] : fill) : 0.f;
 }
@@ -223,6 +227,7 @@ __device__ __forceinline__ void chan_reduce(int64_t npx, int64_t ppb, int cpad, 
 __global__ void k_reduce_parts(const double* __restrict__ part, int nparts, int nslots,
                                double* __restrict__ out, int c = 0, int cpad = 0,
                                float* __restrict__ f0 = nullptr, float* __restrict__ f1 = nullptr) {
+  pdl_wait();
   const int s = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   if (s >= nslots) return;
   double a = 0.0;
@@ -270,6 +275,7 @@ struct StatsF {
 template <int CG>
 __global__ void __launch_bounds__(256) k_bn_stats(const bf16* __restrict__ z, int pitch, int cpad,
                                                   int64_t npx, int64_t ppb, double* part) {
+  pdl_wait();
   chan_reduce<2, CG>(npx, ppb, cpad, part, StatsF{z, pitch});
 }
 
@@ -321,6 +327,7 @@ struct BnbCoef {
 // finalise from all-reduced sums (sum slot i, square/product slot cpad + i)
 template <class F>
 __global__ void k_fin(const double* sums, int n, F f) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) f(i, sums[i], sums[f.cpad + i]);
 }
@@ -330,6 +337,7 @@ __global__ void k_fin(const double* sums, int n, F f) {
 // order exactly as k_reduce_parts does
 template <class F>
 __global__ void k_reduce_fin(const double* __restrict__ part, int nparts, int n, F f) {
+  pdl_wait();
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   if (i >= n) return;
   double a = 0.0, b = 0.0;
@@ -375,6 +383,7 @@ __global__ void __launch_bounds__(256) k_bn_apply(const bf16* __restrict__ z, in
                                                   const float* __restrict__ bnv, float slope,
                                                   bf16* __restrict__ out, int c_tot, int c_off,
                                                   int groups) {
+  pdl_wait();
   const int lg = ilog2(groups);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (npx << lg)) return;
@@ -401,6 +410,7 @@ __global__ void __launch_bounds__(256) k_bn_apply_pool(const bf16* __restrict__ 
                                                        const float* __restrict__ bnv, float slope,
                                                        bf16* __restrict__ out, int c_tot, int c_off,
                                                        bf16* __restrict__ pool) {
+  pdl_wait();
   const int lg = ilog2(cpad / 8), lho = ilog2(hw / 2), hw_ = hw;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (np << (2 * lho + lg))) return;
@@ -469,6 +479,7 @@ __device__ __forceinline__ void widen(uint4 u, float (&f)[8]) {
 // 16 -> 32 upsample at B = 4,096; a whole column strip per thread 461 us.)
 __global__ void __launch_bounds__(256) k_up_fwd(const bf16* __restrict__ in, int c, int hw_in, int np,
                                                 bf16* __restrict__ out, int c_tot) {
+  pdl_wait();
   const int lg = ilog2(c / 8), lhi = ilog2(hw_in), lho = lhi + 1, ho = 2 * hw_in;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (np << (lho + lhi + lg))) return;
@@ -533,6 +544,7 @@ __device__ __forceinline__ void up_adj(int i, int n, int (&o)[4], float (&w)[4])
 // re-reads). Same taps, weights and summation order (same bits).
 __global__ void __launch_bounds__(256) k_up_bwd(const bf16* __restrict__ dhigh, int c_tot, int c, int hw_in,
                                                 int np, bf16* __restrict__ dlow) {
+  pdl_wait();
   const int lg = ilog2(c / 8), lhi = ilog2(hw_in), ho = 2 * hw_in;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (np << (lhi + lg))) return;
@@ -603,6 +615,7 @@ __global__ void __launch_bounds__(256) k_pool_bwd(const bf16* __restrict__ a, in
                                                   int hw_out, int np, const bf16* __restrict__ dp,
                                                   const bf16* __restrict__ dskip, int ds_tot, int ds_off,
                                                   bf16* __restrict__ ds) {
+  pdl_wait();
   const int lg = ilog2(c / 8), lho = ilog2(hw_out), hi = 2 * hw_out;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (np << (2 * lho + lg))) return;
@@ -677,6 +690,7 @@ __global__ void __launch_bounds__(256) k_bnb_stats(const bf16* __restrict__ z, c
                                                    int pitch, int cpad, int64_t npx, int64_t ppb,
                                                    const float* __restrict__ bnv, float slope,
                                                    double* part) {
+  pdl_wait();
   chan_reduce<2, CG>(npx, ppb, cpad, part, BnbStatsF{z, da, bnv, cpad, pitch, slope});
 }
 
@@ -736,6 +750,7 @@ __global__ void __launch_bounds__(256) k_bnb_apply(const bf16* __restrict__ z, c
                                                    int pitch, int cpad, int64_t npx_all, int64_t npx,
                                                    int64_t ppb, const float* __restrict__ bnv,
                                                    float slope, bf16* __restrict__ dz, double* part) {
+  pdl_wait();
   chan_reduce<1, CG>(npx_all, ppb, cpad, part, BnbApplyF{z, da, bnv, dz, npx, cpad, pitch, slope});
 }
 
@@ -747,6 +762,7 @@ __global__ void __launch_bounds__(256) k_head(const bf16* __restrict__ a15, cons
                                               const float* __restrict__ b, const float* __restrict__ y,
                                               int64_t n, int64_t np, double inv_n, bf16* __restrict__ da15,
                                               double* part, int pitch) {
+  pdl_wait();
   float wl[48], bl[3];
 #pragma unroll
   for (int i = 0; i < 48; ++i) wl[i] = w[i];
@@ -814,6 +830,7 @@ __global__ void __launch_bounds__(256) k_head(const bf16* __restrict__ a15, cons
 }
 
 __global__ void k_head_out(const double* sums, float* gw, float* gb, double* loss) {
+  pdl_wait();
   const int i = threadIdx.x;
   if (i == 0) *loss = sums[0];
   if (i < 3) gb[i] = float(sums[1 + i]);
@@ -953,8 +970,8 @@ int engine_setup(DrcbTrainer* T, int64_t np, cudaStream_t st) {
     E->ep_zero[l] = reinterpret_cast<float*>(w + wo[7 * l + 5]);
     E->bnv[l] = reinterpret_cast<float*>(w + wo[7 * l + 6]);
     const int cinp = pad64(t.cin), coutp = pad64(t.cout);
-    k_pad_vec<<<nbk(coutp), 256, 0, st>>>(nullptr, t.cout, coutp, 1.f, E->ep_one_f[l]);
-    k_pad_vec<<<nbk(cinp), 256, 0, st>>>(nullptr, t.cin, cinp, 1.f, E->ep_one_t[l]);
+    launch_pdl(k_pad_vec, nbk(coutp), 256, 0, st, nullptr, t.cout, coutp, 1.f, E->ep_one_f[l]);
+    launch_pdl(k_pad_vec, nbk(cinp), 256, 0, st, nullptr, t.cin, cinp, 1.f, E->ep_one_t[l]);
   }
   E->w8 = reinterpret_cast<bf16*>(w + w8_off);
   E->ws = w + ws_off;
@@ -1053,41 +1070,42 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   const int cg = chan_groups(t.cout);
   red_geom(n * hw2, coutp / 64, ppb, gx, reinterpret_cast<const void*>(k_bn_stats<8>));
   switch (cg) {
-    case 2: k_bn_stats<2><<<dim3(gx, 1), 256, 0, st>>>(E->Z[l], zp, coutp, n * hw2, ppb, E->part); break;
-    case 4: k_bn_stats<4><<<dim3(gx, 1), 256, 0, st>>>(E->Z[l], zp, coutp, n * hw2, ppb, E->part); break;
-    default: k_bn_stats<8><<<dim3(gx, coutp / 64), 256, 0, st>>>(E->Z[l], zp, coutp, n * hw2, ppb, E->part);
+    case 2: launch_pdl(k_bn_stats<2>, dim3(gx, 1), 256, 0, st, E->Z[l], zp, coutp, n * hw2, ppb, E->part); break;
+    case 4: launch_pdl(k_bn_stats<4>, dim3(gx, 1), 256, 0, st, E->Z[l], zp, coutp, n * hw2, ppb, E->part); break;
+    default: launch_pdl(k_bn_stats<8>, dim3(gx, coutp / 64), 256, 0, st, E->Z[l], zp, coutp, n * hw2, ppb, E->part);
   }
   TC_CHECK("k_bn_stats");
   const BnFin fin{t.cout,           coutp,       double(n) * hw2 * T->world, T->params + t.g,
                   T->params + t.be, T->running + t.rm, T->running + t.rv,  E->bnv[l]};
   if (one_rank(T)) {
-    k_reduce_fin<<<nb_slots(t.cout), 256, 0, st>>>(E->part, gx, t.cout, fin);
+    launch_pdl(k_reduce_fin<BnFin>, nb_slots(t.cout), 256, 0, st, E->part, gx, t.cout, fin);
     TC_CHECK("k_reduce_fin");
   } else {
-    k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums);
+    launch_pdl(k_reduce_parts, nb_slots(2 * coutp), 256, 0, st, E->part, gx, 2 * coutp, E->sums, 0, 0,
+               (float*)nullptr, (float*)nullptr);
     TC_CHECK("k_reduce_parts");
     rc = syncbn_allreduce(T, E->sums, size_t(2) * coutp, st);  // SyncBN
     if (rc) return rc;
-    k_fin<<<nbk(t.cout), 256, 0, st>>>(E->sums, t.cout, fin);
+    launch_pdl(k_fin<BnFin>, nbk(t.cout), 256, 0, st, E->sums, t.cout, fin);
     TC_CHECK("k_fin");
   }
   const Buf& out = E->B[P.out];
   if (P.pool >= 0) {
     const int64_t tot = np * (hw2 / 4) * (coutp / 8);
-    k_bn_apply_pool<<<nbk(tot), 256, 0, st>>>(E->Z[l], coutp, t.hw, np, E->bnv[l], T->slope, out.p,
+    launch_pdl(k_bn_apply_pool, nbk(tot), 256, 0, st, E->Z[l], coutp, t.hw, np, E->bnv[l], T->slope, out.p,
                                               out.c, P.off, E->B[P.pool].p);
     TC_CHECK("k_bn_apply_pool");
   } else {
     const int groups = cg < 8 ? cg : coutp / 8;
     const int64_t tot = np * hw2 * groups;
-    k_bn_apply<<<nbk(tot), 256, 0, st>>>(E->Z[l], zp, coutp, np * hw2, E->bnv[l], T->slope, out.p,
+    launch_pdl(k_bn_apply, nbk(tot), 256, 0, st, E->Z[l], zp, coutp, np * hw2, E->bnv[l], T->slope, out.p,
                                          out.c, P.off, groups);
     TC_CHECK("k_bn_apply");
   }
   if (P.up >= 0) {
     const Buf& cat = E->B[P.up];
     const int64_t tot = np * 2 * hw2 * (coutp / 8);  // two outputs per thread
-    k_up_fwd<<<nbk(tot), 256, 0, st>>>(out.p, coutp, t.hw, np, cat.p, cat.c);
+    launch_pdl(k_up_fwd, nbk(tot), 256, 0, st, out.p, coutp, t.hw, np, cat.p, cat.c);
     TC_CHECK("k_up_fwd");
   }
   return 0;
@@ -1105,9 +1123,9 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   red_geom(n * hw2, coutp / 64, ppb, gx, reinterpret_cast<const void*>(k_bnb_stats<8>));
   const dim3 gs(gx, cg < 8 ? 1 : coutp / 64);
   switch (cg) {
-    case 2: k_bnb_stats<2><<<gs, 256, 0, st>>>(E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
-    case 4: k_bnb_stats<4><<<gs, 256, 0, st>>>(E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
-    default: k_bnb_stats<8><<<gs, 256, 0, st>>>(E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part);
+    case 2: launch_pdl(k_bnb_stats<2>, gs, 256, 0, st, E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
+    case 4: launch_pdl(k_bnb_stats<4>, gs, 256, 0, st, E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
+    default: launch_pdl(k_bnb_stats<8>, gs, 256, 0, st, E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part);
   }
   TC_CHECK("k_bnb_stats");
   // (sums of dyb and dyb * xhat: the local beta and gamma gradients)
@@ -1115,16 +1133,16 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
                T->grads + t.be, T->grads + t.g};
   int rc = 0;
   if (one_rank(T)) {
-    k_reduce_fin<<<nb_slots(coutp), 256, 0, st>>>(E->part, gx, coutp, coef);
+    launch_pdl(k_reduce_fin<BnbCoef>, nb_slots(coutp), 256, 0, st, E->part, gx, coutp, coef);
     TC_CHECK("k_reduce_fin");
   } else {
-    k_reduce_parts<<<nb_slots(2 * coutp), 256, 0, st>>>(E->part, gx, 2 * coutp, E->sums, t.cout,
+    launch_pdl(k_reduce_parts, nb_slots(2 * coutp), 256, 0, st, E->part, gx, 2 * coutp, E->sums, t.cout,
                                                         coutp, T->grads + t.be, T->grads + t.g);
     TC_CHECK("k_reduce_parts");
     rc = syncbn_allreduce(T, E->sums, size_t(2) * coutp, st);  // SyncBN backward
     if (rc) return rc;
     coef.dbeta = coef.dgamma = nullptr;  // (written above from the local sums)
-    k_fin<<<nbk(coutp), 256, 0, st>>>(E->sums, coutp, coef);
+    launch_pdl(k_fin<BnbCoef>, nbk(coutp), 256, 0, st, E->sums, coutp, coef);
     TC_CHECK("k_fin");
   }
   int64_t ppb2;
@@ -1135,13 +1153,13 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   // load it into 64-channel / narrow boxes through the TMA zero fill)
   const dim3 ga(gx2, cg < 8 ? 1 : coutp / 64);
   switch (cg) {
-    case 2: k_bnb_apply<2><<<ga, 256, 0, st>>>(E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
-    case 4: k_bnb_apply<4><<<ga, 256, 0, st>>>(E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
-    default: k_bnb_apply<8><<<ga, 256, 0, st>>>(E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part);
+    case 2: launch_pdl(k_bnb_apply<2>, ga, 256, 0, st, E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
+    case 4: launch_pdl(k_bnb_apply<4>, ga, 256, 0, st, E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
+    default: launch_pdl(k_bnb_apply<8>, ga, 256, 0, st, E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part);
   }
   TC_CHECK("k_bnb_apply");
-  k_reduce_parts<<<nb_slots(t.cout), 256, 0, st>>>(E->part, gx2, t.cout, E->sums, t.cout, 0,
-                                                   T->grads + t.b);  // conv bias
+  launch_pdl(k_reduce_parts, nb_slots(t.cout), 256, 0, st, E->part, gx2, t.cout, E->sums, t.cout, 0,
+             T->grads + t.b, (float*)nullptr);  // conv bias
   TC_CHECK("k_reduce_parts");
   // dgrad: the transposed conv of dz into the input-gradient buffer
   if (P.din >= 0) {
@@ -1160,7 +1178,7 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
 
 int up_bwd(TcEngine* E, int dcat, int c, int hw_in, int dlow, int64_t np, cudaStream_t st) {
   const int64_t tot = np * hw_in * (c / 8);  // a column strip per thread
-  k_up_bwd<<<nbk(tot), 256, 0, st>>>(E->B[dcat].p, E->B[dcat].c, c, hw_in, np, E->B[dlow].p);
+  launch_pdl(k_up_bwd, nbk(tot), 256, 0, st, E->B[dcat].p, E->B[dcat].c, c, hw_in, np, E->B[dlow].p);
   TC_CHECK("k_up_bwd");
   return 0;
 }
@@ -1168,7 +1186,7 @@ int up_bwd(TcEngine* E, int dcat, int c, int hw_in, int dlow, int64_t np, cudaSt
 int pool_bwd(TcEngine* E, int cat, int off, int c, int hw_out, int dp, int dcat, int ds, int64_t np,
              cudaStream_t st) {
   const int64_t tot = np * hw_out * hw_out * (c / 8);
-  k_pool_bwd<<<nbk(tot), 256, 0, st>>>(E->B[cat].p, E->B[cat].c, off, c, hw_out, np, E->B[dp].p,
+  launch_pdl(k_pool_bwd, nbk(tot), 256, 0, st, E->B[cat].p, E->B[cat].c, off, c, hw_out, np, E->B[dp].p,
                                         E->B[dcat].p, E->B[dcat].c, off, E->B[ds].p);
   TC_CHECK("k_pool_bwd");
   return 0;
@@ -1204,15 +1222,15 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
       tot += 2 * int64_t(coutp) * cinp + coutp;
     }
     a.start[16] = tot;
-    k_prep_weights<<<nbk(tot), 256, 0, st>>>(a);
+    launch_pdl(k_prep_weights, nbk(tot), 256, 0, st, a);
     TC_CHECK("k_prep_weights");
     if (use_in8(T)) {
       const TL& t0 = T->L[0];
-      k_prep_in8<<<nbk(64 * 128), 256, 0, st>>>(T->params + t0.w, t0.cin, t0.cout, E->w8);
+      launch_pdl(k_prep_in8, nbk(64 * 128), 256, 0, st, T->params + t0.w, t0.cin, t0.cout, E->w8);
       TC_CHECK("k_prep_in8");
     }
   }
-  k_x_in<<<nbk(np * 1024), 256, 0, st>>>(x, n, np, E->B[X0].p);
+  launch_pdl(k_x_in, nbk(np * 1024), 256, 0, st, x, n, np, E->B[X0].p);
   TC_CHECK("k_x_in");
   // ---- forward (model.py:80-88)
   for (int l = 0; l < 16 && !rc; ++l) rc = layer_fwd(T, l, n, np, st);
@@ -1221,12 +1239,13 @@ int tc_step(DrcbTrainer* T, const float* x, const float* y, int64_t n, double** 
   {
     const TL& t = T->L[16];
     const int gx = 1024;
-    k_head<<<gx, 256, 0, st>>>(E->B[A15].p, T->params + t.w, T->params + t.b, y, n, np,
+    launch_pdl(k_head, gx, 256, 0, st, E->B[A15].p, T->params + t.w, T->params + t.b, y, n, np,
                                1.0 / double(n * 3 * 1024), E->B[DA15].p, E->part, E->B[A15].c);
     TC_CHECK("k_head");
-    k_reduce_parts<<<nb_slots(HEAD_SLOTS), 256, 0, st>>>(E->part, gx, HEAD_SLOTS, E->sums);
+    launch_pdl(k_reduce_parts, nb_slots(HEAD_SLOTS), 256, 0, st, E->part, gx, HEAD_SLOTS, E->sums, 0, 0,
+               (float*)nullptr, (float*)nullptr);
     TC_CHECK("k_reduce_parts");
-    k_head_out<<<1, 64, 0, st>>>(E->sums, T->grads + t.w, T->grads + t.b, E->loss);
+    launch_pdl(k_head_out, 1, 64, 0, st, E->sums, T->grads + t.w, T->grads + t.b, E->loss);
     TC_CHECK("k_head_out");
   }
   // ---- backward

@@ -82,6 +82,7 @@ __device__ __forceinline__ void chunk_origin(const WgArgs& a, int c, int& map0, 
 __global__ void __launch_bounds__(THREADS, 1)
     k_wgrad(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapDZ,
             const __grid_constant__ WgArgs a) {
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int DZB = a.nb_n * BOX;  // one dZ stage
@@ -253,6 +254,7 @@ template <int NB>
 __global__ void __launch_bounds__(THREADS, 1)
     k_wgrad_dxn(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapDZ,
                 const __grid_constant__ WgArgs a) {
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int W = NB * 2;          // dZ row bytes (one pixel)
@@ -405,6 +407,7 @@ __device__ __forceinline__ int64_t wg_out(int co, int ci, int tap, int cin, int 
 // (dy of the X block: acc 0 rows -1 / 0, acc 1 row +1), column n (dx, co)
 __global__ void k_wgrad_reduce_dxn(const WgArgs a, int nb, int cin, int cout, int deconv,
                                    float* __restrict__ dwf) {
+  pdl_wait();
   const int ncol = 3 * nb;
   const int64_t per = int64_t(2) * 128 * ncol;
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -428,6 +431,7 @@ __global__ void k_wgrad_reduce_dxn(const WgArgs a, int nb, int cin, int cout, in
 // over the splits in order (deterministic). One thread per (n tile, M tile,
 // row, column) accumulator element.
 __global__ void k_wgrad_reduce(const WgArgs a, int cin, int cout, int deconv, float* __restrict__ dwf) {
+  pdl_wait();
   const int64_t per_nt = int64_t(a.npairs) * 128 * a.n_tile;
   const int64_t total = per_nt * (int64_t(a.units) / a.groups);
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -552,19 +556,19 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
     const unsigned grid = unsigned(a.units * a.splits);
     if (nb == 16) {
       smem_attr_once(attr_dxn[0], k_wgrad_dxn<16>, 227 * 1024);
-      k_wgrad_dxn<16><<<grid, THREADS, smem, st>>>(mX, mDZ, a);
+      launch_pdl(k_wgrad_dxn<16>, grid, THREADS, smem, st, mX, mDZ, a);
     } else if (nb == 32) {
       smem_attr_once(attr_dxn[1], k_wgrad_dxn<32>, 227 * 1024);
-      k_wgrad_dxn<32><<<grid, THREADS, smem, st>>>(mX, mDZ, a);
+      launch_pdl(k_wgrad_dxn<32>, grid, THREADS, smem, st, mX, mDZ, a);
     } else {
       smem_attr_once(attr_dxn[2], k_wgrad_dxn<64>, 227 * 1024);
-      k_wgrad_dxn<64><<<grid, THREADS, smem, st>>>(mX, mDZ, a);
+      launch_pdl(k_wgrad_dxn<64>, grid, THREADS, smem, st, mX, mDZ, a);
     }
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "k_wgrad_dxn");
     const int64_t total = int64_t(2) * 128 * (3 * nb) * a.units;
-    k_wgrad_reduce_dxn<<<unsigned((total + 255) / 256), 256, 0, st>>>(a, nb, cin, cout, deconv, dwf);
+    launch_pdl(k_wgrad_reduce_dxn, unsigned((total + 255) / 256), 256, 0, st, a, nb, cin, cout, deconv, dwf);
     count_launch();
     e = cudaGetLastError();
     return e == cudaSuccess ? 0 : cuda_fail(e, "k_wgrad_reduce_dxn");
@@ -582,12 +586,12 @@ int wgrad_bf16(const void* x, int cin, int cin_pad, const void* dz, int cout, in
   if (rc) return rc;
   static DeviceFlags attr;
   smem_attr_once(attr, k_wgrad, 227 * 1024);
-  k_wgrad<<<a.units * a.splits, THREADS, smem, st>>>(mX, mDZ, a);
+  launch_pdl(k_wgrad, a.units * a.splits, THREADS, smem, st, mX, mDZ, a);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "k_wgrad");
   const int64_t total = int64_t(a.npairs) * 128 * a.n_tile * (cout_pad / a.n_tile);
-  k_wgrad_reduce<<<unsigned((total + 255) / 256), 256, 0, st>>>(a, cin, cout, deconv, dwf);
+  launch_pdl(k_wgrad_reduce, unsigned((total + 255) / 256), 256, 0, st, a, cin, cout, deconv, dwf);
   count_launch();
   e = cudaGetLastError();
   return e == cudaSuccess ? 0 : cuda_fail(e, "k_wgrad_reduce");
