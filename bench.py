@@ -835,6 +835,10 @@ def main():
         "shade": {"bytes_per_frame": pt_bytes, "us": sub["shade"],
                   "achieved_gbs": pt_bytes / (sub["shade"] * 1e3),
                   "frac_hbm": pt_bytes / (sub["shade"] * 1e3) / hbm},
+        "bound": ("issue, not HBM: per-pixel scans of the nearby cache entries (k_interp, ncu "
+                  "72 % issue-active, 26.8 active threads per warp instruction) and per-map CDF "
+                  "chains (k_shade, one warp per map, 57 % issue-active); "
+                  "profiles/r02_ncu_full_summary.md"),
     }
     if trav and "casts_per_frame" in trav:
         # every cast of a frame is made by the G-buffer/direct and map stages

@@ -29,6 +29,8 @@ full conv_pair 'k_conv_pair' 3 "$B"
 full conv_tc_dec3 'k_conv_tc' 34 "$B"
 full conv_rows_dec1 'k_conv_rows' 5 "$B"   # 6 row-conv launches per frame: dec1.deconv2 is the 6th
 full head_fused 'k_head_fused' 3 "$B"
+full interp 'k_interp' 3 "$B"   # the gather-bound elementwise stages (issue, not HBM)
+full shade 'k_shade' 3 "$B"
 full train_wgrad_dxn 'k_wgrad_dxn' 12 "$T"  # second step's first (head.deconv2)
 full train_wgrad_taps '^k_wgrad$' 6 "$T"
 full train_bnb_apply 'k_bnb_apply' 17 "$T"
