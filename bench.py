@@ -821,7 +821,8 @@ def main():
                 "unit": "GB/s", "frac": None, "traffic": None}
     roof["peak_source"] = src
     roof["stage_ms_per_frame"] = {k: v / 1e3 for k, v in avg.items()}
-    # the HBM-bound elementwise stages against the measured HBM peak:
+    # the elementwise stages against the measured HBM peak (their bound is
+    # issue, see "bound"):
     # algorithmic bytes = every distinct tensor read once + written once
     sub = {k: float(np.mean([r[k] for r in sub_rows])) for k in sub_rows[0]}
     rb = 4 if args.precision == 32 else 8
