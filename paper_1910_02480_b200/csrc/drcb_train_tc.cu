@@ -72,6 +72,26 @@ __device__ __forceinline__ void ld8(const bf16* p, float (&f)[8]) {
     f[2 * j + 1] = t.y;
   }
 }
+// the same through the streaming cache policy (evict-first), for the passes
+// that read a tensor for the last time in a while (the BN applies: Z and dA
+// are dead after the backward's apply, which leaves L2 to the dZ it writes
+// for the dgrad and wgrad; the statistics passes keep the default policy,
+// their tensors are re-read by the apply right after). DRCB_BN_NOSTREAM:
+// plain loads (A/B)
+__device__ __forceinline__ void ld8s(const bf16* p, float (&f)[8]) {
+#ifdef DRCB_BN_NOSTREAM
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+#else
+  const uint4 u = __ldcs(reinterpret_cast<const uint4*>(p));
+#endif
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 t = __bfloat1622float2(h[j]);
+    f[2 * j] = t.x;
+    f[2 * j + 1] = t.y;
+  }
+}
 __device__ __forceinline__ void st8(bf16* p, const float (&f)[8]) {
   uint4 u;
   uint32_t* w = reinterpret_cast<uint32_t*>(&u);
@@ -389,7 +409,7 @@ __global__ void __launch_bounds__(256) k_bn_apply(const bf16* __restrict__ z, in
   if (i >= (npx << lg)) return;
   const int p = i >> lg, c0 = (i & ((1 << lg) - 1)) * 8;
   float v[8];
-  ld8(z + int64_t(p) * zp + c0, v);
+  ld8s(z + int64_t(p) * zp + c0, v);  // (Z's last reader until the backward)
   const float4 s0 = __ldg(reinterpret_cast<const float4*>(bnv + c0));
   const float4 s1 = __ldg(reinterpret_cast<const float4*>(bnv + c0 + 4));
   const float4 t0 = __ldg(reinterpret_cast<const float4*>(bnv + cpad + c0));
@@ -726,8 +746,8 @@ struct BnbApplyF {
     float zv[U][8], dv[U][8];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      ld8(z + (p + PS * u) * pitch + c0, zv[u]);
-      ld8(da + (p + PS * u) * pitch + c0, dv[u]);
+      ld8s(z + (p + PS * u) * pitch + c0, zv[u]);
+      ld8s(da + (p + PS * u) * pitch + c0, dv[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
