@@ -202,16 +202,19 @@ __global__ void k_pad_vec(const float* __restrict__ v, int n, int np, float fill
 }
 
 // Per-channel reductions over the first npx pixels of an NHWC tensor (pixel
-// pitch cpad): block (bx, channel tile of 64) covers pixels [bx*ppb,
-// (bx+1)*ppb); thread = (8-ch group, one of 256/CG pixel lanes); the lanes'
-// sums are combined in lane order in double. CG = 8 groups cover a 64-channel
-// tile; a layer with fewer real channels (head.deconv1 / deconv2: 32 / 16)
-// runs CG = 4 / 2 and never touches the padding (a quarter / half of the
-// bytes). Partial slot (q*cpad + c) of block bx at part[(q*cpad + c)*gx + bx],
-// q = 0..NQ-1.
+// pitch cpad): blocks (bx, channel tile of 64) sweep the tensor together in
+// chunks of 4 * PL pixels, chunk k to block k % gx (grid-stride: the grid
+// moves through memory as one front, low to high, or high to low with `rev`,
+// so a pass can start where the previous kernel's writes ended while they
+// are still in L2); thread = (8-ch group, one of PL = 256/CG pixel lanes);
+// the lanes' sums are combined in lane order in double. CG = 8 groups cover
+// a 64-channel tile; a layer with fewer real channels (head.deconv1 /
+// deconv2: 32 / 16) runs CG = 4 / 2 and never touches the padding (a quarter
+// / half of the bytes). Partial slot (q*cpad + c) of block bx at
+// part[(q*cpad + c)*gx + bx], q = 0..NQ-1.
 template <int NQ, int CG, class F>
-__device__ __forceinline__ void chan_reduce(int64_t npx, int64_t ppb, int cpad, double* part, F f) {
-  constexpr int PL = 256 / CG, CT = 8 * CG;
+__device__ __forceinline__ void chan_reduce(int64_t npx, int rev, int cpad, double* part, F f) {
+  constexpr int PL = 256 / CG, CT = 8 * CG, CH = 4 * PL;
   const int cg = threadIdx.x % CG, pl = threadIdx.x / CG;
   const int c0 = blockIdx.y * 64 + cg * 8;
   f.init(c0);  // this thread's 8 channels are fixed: per-channel constants once
@@ -220,12 +223,18 @@ __device__ __forceinline__ void chan_reduce(int64_t npx, int64_t ppb, int cpad, 
   for (int q = 0; q < NQ; ++q)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[q][j] = 0.f;
-  const int64_t p0 = int64_t(blockIdx.x) * ppb, p1 = min(npx, p0 + ppb);
-  // four pixels per lane in flight (the loads of one iteration are issued
-  // before their arithmetic: enough bytes in flight per SM for HBM rate)
-  int64_t p = p0 + pl;
-  for (; p + 3 * PL < p1; p += 4 * PL) f.template go<4, PL>(p, c0, acc);
-  for (; p < p1; p += PL) f.template go<1, PL>(p, c0, acc);
+  // four pixels per lane in flight (the loads of one chunk are issued before
+  // their arithmetic: enough bytes in flight per SM for HBM rate)
+  const int64_t nch = (npx + CH - 1) / CH;
+  for (int64_t k = blockIdx.x; k < nch; k += gridDim.x) {
+    const int64_t kc = rev ? nch - 1 - k : k;
+    const int64_t q0 = kc * CH + pl;
+    if ((kc + 1) * CH <= npx) {
+      f.template go<4, PL>(q0, c0, acc);
+    } else {
+      for (int64_t p = q0; p < npx; p += PL) f.template go<1, PL>(p, c0, acc);
+    }
+  }
   __shared__ float red[NQ][PL][CT + 1];
 #pragma unroll
   for (int q = 0; q < NQ; ++q)
@@ -294,9 +303,9 @@ struct StatsF {
 };
 template <int CG>
 __global__ void __launch_bounds__(256) k_bn_stats(const bf16* __restrict__ z, int pitch, int cpad,
-                                                  int64_t npx, int64_t ppb, double* part) {
+                                                  int64_t npx, double* part) {
   pdl_wait();
-  chan_reduce<2, CG>(npx, ppb, cpad, part, StatsF{z, pitch});
+  chan_reduce<2, CG>(npx, 0, cpad, part, StatsF{z, pitch});
 }
 
 // BN finalize (torch BatchNorm2d train mode: biased variance normalises,
@@ -396,7 +405,11 @@ __global__ void k_reduce_fin(const double* __restrict__ part, int nparts, int n,
 // division in the address math).
 __device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
 
-// a = LeakyReLU(z * s + t) into out[.., c_off + c] (all np maps)
+// a = LeakyReLU(z * s + t) into out[.., c_off + c] (all np maps). Walked
+// from the last pixel down: the stats pass that precedes it ended on the
+// high pixels (still in L2), and the next layer's conv starts on the low
+// ones this leaves in L2 (measured with the bnb_apply direction below:
+// ~0.25 ms of a B = 4,096 step).
 // (the first `groups` 8-channel groups of each pixel: the padding of a
 // layer with fewer than 64 channels keeps its zeros)
 __global__ void __launch_bounds__(256) k_bn_apply(const bf16* __restrict__ z, int zp, int cpad, int npx,
@@ -405,8 +418,9 @@ __global__ void __launch_bounds__(256) k_bn_apply(const bf16* __restrict__ z, in
                                                   int groups) {
   pdl_wait();
   const int lg = ilog2(groups);
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (npx << lg)) return;
+  i = (npx << lg) - 1 - i;  // high to low (see k_bn_apply's comment above)
   const int p = i >> lg, c0 = (i & ((1 << lg) - 1)) * 8;
   float v[8];
   ld8s(z + int64_t(p) * zp + c0, v);  // (Z's last reader until the backward)
@@ -432,8 +446,9 @@ __global__ void __launch_bounds__(256) k_bn_apply_pool(const bf16* __restrict__ 
                                                        bf16* __restrict__ pool) {
   pdl_wait();
   const int lg = ilog2(cpad / 8), lho = ilog2(hw / 2), hw_ = hw;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (np << (2 * lho + lg))) return;
+  i = (np << (2 * lho + lg)) - 1 - i;  // high to low, as k_bn_apply
   const int c0 = (i & ((1 << lg) - 1)) * 8;
   const int pp = i >> lg;
   const int px = pp & ((1 << lho) - 1), py = (pp >> lho) & ((1 << lho) - 1), m = pp >> (2 * lho);
@@ -707,11 +722,11 @@ struct BnbStatsF {
 };
 template <int CG>
 __global__ void __launch_bounds__(256) k_bnb_stats(const bf16* __restrict__ z, const bf16* __restrict__ da,
-                                                   int pitch, int cpad, int64_t npx, int64_t ppb,
+                                                   int pitch, int cpad, int64_t npx,
                                                    const float* __restrict__ bnv, float slope,
                                                    double* part) {
   pdl_wait();
-  chan_reduce<2, CG>(npx, ppb, cpad, part, BnbStatsF{z, da, bnv, cpad, pitch, slope});
+  chan_reduce<2, CG>(npx, 0, cpad, part, BnbStatsF{z, da, bnv, cpad, pitch, slope});
 }
 
 
@@ -768,10 +783,12 @@ struct BnbApplyF {
 template <int CG>
 __global__ void __launch_bounds__(256) k_bnb_apply(const bf16* __restrict__ z, const bf16* __restrict__ da,
                                                    int pitch, int cpad, int64_t npx_all, int64_t npx,
-                                                   int64_t ppb, const float* __restrict__ bnv,
+                                                   const float* __restrict__ bnv,
                                                    float slope, bf16* __restrict__ dz, double* part) {
   pdl_wait();
-  chan_reduce<1, CG>(npx_all, ppb, cpad, part, BnbApplyF{z, da, bnv, dz, npx, cpad, pitch, slope});
+  // high to low: starts on the stats pass's last (L2-resident) pixels and
+  // ends on the low ones the dgrad reads first
+  chan_reduce<1, CG>(npx_all, 1, cpad, part, BnbApplyF{z, da, bnv, dz, npx, cpad, pitch, slope});
 }
 
 // head: conv_out (1x1, 16 -> 3) + ReLU, L1 loss against y (n,3,32,32) fp32,
@@ -1019,21 +1036,19 @@ inline int resident_blocks(const void* kern) {
   return b;
 }
 
-// reduction geometry over npx pixels: pixels per block and blocks. With
+// reduction grid over npx pixels (blocks per channel tile). With
 // `kern` given, the grid is whole waves of that kernel's resident blocks
 // (DRCB_RED_WAVES, default 1; 2 / 4 waves measured 0.1 / 0.4 ms slower per
 // B = 4,096 step) instead of 8 blocks per SM: a partial last wave left SMs
 // idle at the end of every pass.
-inline void red_geom(int64_t npx, int ctiles, int64_t& ppb, int& gx, const void* kern = nullptr) {
+inline int red_grid(int64_t npx, int ctiles, const void* kern = nullptr) {
   static const int waves = [] {
     const char* e = getenv("DRCB_RED_WAVES");
     return e ? atoi(e) : 1;
   }();
   const int per_sm = (kern && waves > 0) ? waves * resident_blocks(kern) : 8;
   const int64_t target = std::max<int64_t>(1, int64_t(sm_count()) * per_sm / ctiles);
-  ppb = std::max<int64_t>(128, (npx + target - 1) / target);
-  ppb = (ppb + 127) / 128 * 128;
-  gx = int((npx + ppb - 1) / ppb);
+  return int(std::min<int64_t>(target, std::max<int64_t>(1, (npx + 127) / 128)));
 }
 
 // N of a conv whose output has fewer than 64 real channels (head.deconv1 /
@@ -1085,14 +1100,12 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
                               narrow_n(t.hw, t.cout, coutp), E->ep_one_f[l], E->ep_b[l], 1.0f, st,
                               in.c);
   if (rc) return rc;
-  int64_t ppb;
-  int gx;
   const int cg = chan_groups(t.cout);
-  red_geom(n * hw2, coutp / 64, ppb, gx, reinterpret_cast<const void*>(k_bn_stats<8>));
+  const int gx = red_grid(n * hw2, coutp / 64, reinterpret_cast<const void*>(k_bn_stats<8>));
   switch (cg) {
-    case 2: launch_pdl(k_bn_stats<2>, dim3(gx, 1), 256, 0, st, E->Z[l], zp, coutp, n * hw2, ppb, E->part); break;
-    case 4: launch_pdl(k_bn_stats<4>, dim3(gx, 1), 256, 0, st, E->Z[l], zp, coutp, n * hw2, ppb, E->part); break;
-    default: launch_pdl(k_bn_stats<8>, dim3(gx, coutp / 64), 256, 0, st, E->Z[l], zp, coutp, n * hw2, ppb, E->part);
+    case 2: launch_pdl(k_bn_stats<2>, dim3(gx, 1), 256, 0, st, E->Z[l], zp, coutp, n * hw2, E->part); break;
+    case 4: launch_pdl(k_bn_stats<4>, dim3(gx, 1), 256, 0, st, E->Z[l], zp, coutp, n * hw2, E->part); break;
+    default: launch_pdl(k_bn_stats<8>, dim3(gx, coutp / 64), 256, 0, st, E->Z[l], zp, coutp, n * hw2, E->part);
   }
   TC_CHECK("k_bn_stats");
   const BnFin fin{t.cout,           coutp,       double(n) * hw2 * T->world, T->params + t.g,
@@ -1118,7 +1131,7 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   } else {
     const int groups = cg < 8 ? cg : coutp / 8;
     const int64_t tot = np * hw2 * groups;
-    launch_pdl(k_bn_apply, nbk(tot), 256, 0, st, E->Z[l], zp, coutp, np * hw2, E->bnv[l], T->slope, out.p,
+    launch_pdl(k_bn_apply, nbk(tot), 256, 0, st, E->Z[l], zp, coutp, int(np * hw2), E->bnv[l], T->slope, out.p,
                                          out.c, P.off, groups);
     TC_CHECK("k_bn_apply");
   }
@@ -1137,15 +1150,13 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   const LayerPlan& P = PLAN[l];
   const int coutp = pad64(t.cout), hw2 = t.hw * t.hw, zp = zpitch(t.cout);
   const bf16* da = E->B[P.dA].p;
-  int64_t ppb;
-  int gx;
   const int cg = chan_groups(t.cout);
-  red_geom(n * hw2, coutp / 64, ppb, gx, reinterpret_cast<const void*>(k_bnb_stats<8>));
+  const int gx = red_grid(n * hw2, coutp / 64, reinterpret_cast<const void*>(k_bnb_stats<8>));
   const dim3 gs(gx, cg < 8 ? 1 : coutp / 64);
   switch (cg) {
-    case 2: launch_pdl(k_bnb_stats<2>, gs, 256, 0, st, E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
-    case 4: launch_pdl(k_bnb_stats<4>, gs, 256, 0, st, E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part); break;
-    default: launch_pdl(k_bnb_stats<8>, gs, 256, 0, st, E->Z[l], da, zp, coutp, n * hw2, ppb, E->bnv[l], T->slope, E->part);
+    case 2: launch_pdl(k_bnb_stats<2>, gs, 256, 0, st, E->Z[l], da, zp, coutp, n * hw2, E->bnv[l], T->slope, E->part); break;
+    case 4: launch_pdl(k_bnb_stats<4>, gs, 256, 0, st, E->Z[l], da, zp, coutp, n * hw2, E->bnv[l], T->slope, E->part); break;
+    default: launch_pdl(k_bnb_stats<8>, gs, 256, 0, st, E->Z[l], da, zp, coutp, n * hw2, E->bnv[l], T->slope, E->part);
   }
   TC_CHECK("k_bnb_stats");
   // (sums of dyb and dyb * xhat: the local beta and gamma gradients)
@@ -1165,17 +1176,15 @@ int layer_bwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
     launch_pdl(k_fin<BnbCoef>, nbk(coutp), 256, 0, st, E->sums, coutp, coef);
     TC_CHECK("k_fin");
   }
-  int64_t ppb2;
-  int gx2;
-  red_geom(np * hw2, coutp / 64, ppb2, gx2, reinterpret_cast<const void*>(k_bnb_apply<8>));
+  const int gx2 = red_grid(np * hw2, coutp / 64, reinterpret_cast<const void*>(k_bnb_apply<8>));
   bf16* dz = E->B[DZ].p;
   // (a narrow layer's dz is stored at its own width: its dgrad and wgrad
   // load it into 64-channel / narrow boxes through the TMA zero fill)
   const dim3 ga(gx2, cg < 8 ? 1 : coutp / 64);
   switch (cg) {
-    case 2: launch_pdl(k_bnb_apply<2>, ga, 256, 0, st, E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
-    case 4: launch_pdl(k_bnb_apply<4>, ga, 256, 0, st, E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part); break;
-    default: launch_pdl(k_bnb_apply<8>, ga, 256, 0, st, E->Z[l], da, zp, coutp, np * hw2, n * hw2, ppb2, E->bnv[l], T->slope, dz, E->part);
+    case 2: launch_pdl(k_bnb_apply<2>, ga, 256, 0, st, E->Z[l], da, zp, coutp, np * hw2, n * hw2, E->bnv[l], T->slope, dz, E->part); break;
+    case 4: launch_pdl(k_bnb_apply<4>, ga, 256, 0, st, E->Z[l], da, zp, coutp, np * hw2, n * hw2, E->bnv[l], T->slope, dz, E->part); break;
+    default: launch_pdl(k_bnb_apply<8>, ga, 256, 0, st, E->Z[l], da, zp, coutp, np * hw2, n * hw2, E->bnv[l], T->slope, dz, E->part);
   }
   TC_CHECK("k_bnb_apply");
   launch_pdl(k_reduce_parts, nb_slots(t.cout), 256, 0, st, E->part, gx2, t.cout, E->sums, t.cout, 0,
