@@ -507,49 +507,96 @@ __device__ __forceinline__ void widen(uint4 u, float (&f)[8]) {
   }
 }
 
-// one thread = two horizontally adjacent outputs (2k, 2k + 1) of one output
-// row and 8 channels: they share the source columns k - 1, k, k + 1, so six
-// 16-byte loads serve two outputs (eight before). (Four output rows per
-// thread, twelve loads for 8 outputs, measured slower: 365 -> 418 us for the
-// 16 -> 32 upsample at B = 4,096; a whole column strip per thread 461 us.)
+// packed fp32 pairs (FFMA2 / FMUL2 on sm_100a: per lane the same correctly
+// rounded fma / mul as the scalar instruction, half the issue slots)
+__device__ __forceinline__ void widen2(uint4 u, float2 (&f)[4]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) f[j] = make_float2(__uint_as_float(w[j] << 16), __uint_as_float(w[j] & 0xffff0000u));
+}
+__device__ __forceinline__ uint4 narrow2(const float2 (&f)[4]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(f[j].x, f[j].y);
+    w[j] = *reinterpret_cast<uint32_t*>(&b);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+// a * (1 - f) + b * f as fma(a, 1 - f, b * f), the contraction the scalar
+// kernels compile to
+__device__ __forceinline__ float2 mix2(float2 a, float2 b, float f) {
+  return __ffma2_rn(a, make_float2(1.f - f, 1.f - f), __fmul2_rn(b, make_float2(f, f)));
+}
+
+// one thread = the 2x2 output block of low-res pixel (i, j), 8 channels:
+// rows i-1 .. i+1 x columns j-1 .. j+1 (clamped), nine 16-B loads for four
+// outputs, the row and column mixes in packed fp32 pairs. Per output the same
+// sources, weights and fma order as the reference-order scalar form (up_src:
+// rows first, then columns), so the same bits. The two-output scalar kernel
+// was issue-bound (80 % issue-active, 3.5 TB/s for the 16 -> 32 upsample);
+// this one is bit-identical and 7 % faster (639 -> 596 us for the three
+// upsamples at B = 4,096), now latency-bound at 64 registers (37 % warps
+// active; 48 or 40 registers spill and are slower, 72 is slower too).
 __global__ void __launch_bounds__(256) k_up_fwd(const bf16* __restrict__ in, int c, int hw_in, int np,
                                                 bf16* __restrict__ out, int c_tot) {
   pdl_wait();
-  const int lg = ilog2(c / 8), lhi = ilog2(hw_in), lho = lhi + 1, ho = 2 * hw_in;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (np << (lho + lhi + lg))) return;
-  const int c0 = (i & ((1 << lg) - 1)) * 8;
-  const int rest = i >> lg;
-  const int k = rest & (hw_in - 1), oy = (rest >> lhi) & (ho - 1), m = rest >> (lhi + lho);
-  int r0, r1;
-  float fr;
-  up_src(oy, hw_in, r0, r1, fr);
-  const int kl = k > 0 ? k - 1 : 0, kr = min(k + 1, hw_in - 1);
+  const int lg = ilog2(c / 8), lhi = ilog2(hw_in), ho = 2 * hw_in;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (np << (2 * lhi + lg))) return;
+  const int c0 = (t & ((1 << lg) - 1)) * 8;
+  const int rest = t >> lg;
+  const int j = rest & (hw_in - 1), i = (rest >> lhi) & (hw_in - 1), m = rest >> (2 * lhi);
   const bf16* b = in + int64_t(m) * hw_in * hw_in * c + c0;
-  float l0[8], l1[8], m0[8], m1[8], h0[8], h1[8];  // (row r0 / r1) x (col kl / k / kr)
-  ld8(b + (r0 * hw_in + kl) * c, l0);
-  ld8(b + (r1 * hw_in + kl) * c, l1);
-  ld8(b + (r0 * hw_in + k) * c, m0);
-  ld8(b + (r1 * hw_in + k) * c, m1);
-  ld8(b + (r0 * hw_in + kr) * c, h0);
-  ld8(b + (r1 * hw_in + kr) * c, h1);
-  // output 2k: columns (k-1, k) at 0.75, or (0, min(1, n-1)) at 0 on the
-  // left border; output 2k+1: columns (k, min(k+1, n-1)) at 0.25
-  const bool left = k == 0;
-  const float fe = left ? 0.f : 0.75f;
-  float ve[8], vo[8];
+  const int cl = max(j - 1, 0), cr = min(j + 1, hw_in - 1);
+  const int rt = max(i - 1, 0), rb = min(i + 1, hw_in - 1);
+  // output row 2i mixes rows (i-1, i) at 0.75 (rows (0, min(1, n-1)) at 0 for
+  // i = 0); row 2i+1 mixes rows (i, min(i+1, n-1)) at 0.25 (up_src)
+  const int a0 = i == 0 ? i : rt, a1 = i == 0 ? rb : i;
+  const float fa = i == 0 ? 0.f : 0.75f;
+  float2 ra[3][4], rbm[3][4];  // row-mixed columns (l, m, r) of output rows 2i, 2i+1
+  {
+    const int cols[3] = {cl, j, cr};
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float tm = m0[j] * (1.f - fr) + m1[j] * fr;
-    const float th = h0[j] * (1.f - fr) + h1[j] * fr;
-    const float tl = l0[j] * (1.f - fr) + l1[j] * fr;
-    const float e0 = left ? tm : tl, e1 = left ? th : tm;
-    ve[j] = e0 * (1.f - fe) + e1 * fe;
-    vo[j] = tm * (1.f - 0.25f) + th * 0.25f;
+    for (int q = 0; q < 3; ++q) {
+      float2 x0[4], x1[4], x2[4];
+      widen2(ldraw(b + (a0 * hw_in + cols[q]) * c), x0);
+      widen2(ldraw(b + (a1 * hw_in + cols[q]) * c), x1);
+      widen2(ldraw(b + (rb * hw_in + cols[q]) * c), x2);
+      if (i != 0) {  // row i (= a1) then serves output row 2i+1 as its first row
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          ra[q][e] = mix2(x0[e], x1[e], fa);
+          rbm[q][e] = mix2(x1[e], x2[e], 0.25f);
+        }
+      } else {  // i = 0: rows (0, min(1, n-1)) for both output rows
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          ra[q][e] = mix2(x0[e], x1[e], 0.f);
+          rbm[q][e] = mix2(x0[e], x1[e], 0.25f);
+        }
+      }
+    }
   }
-  bf16* o = out + (int64_t(m) * ho * ho + int64_t(oy) * ho + 2 * k) * c_tot + c0;
-  st8(o, ve);
-  st8(o + c_tot, vo);
+  // columns: output 2j mixes (j-1, j) at 0.75 or, on the left border, (0,
+  // min(1, n-1)) at 0; output 2j+1 mixes (j, min(j+1, n-1)) at 0.25
+  const bool left = j == 0;
+  const float fe = left ? 0.f : 0.75f;
+  bf16* o = out + (int64_t(m) * ho * ho + int64_t(2 * i) * ho + 2 * j) * c_tot + c0;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const float2(&v)[3][4] = r ? rbm : ra;
+    float2 ve[4], vo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 e0 = left ? v[1][e] : v[0][e], e1 = left ? v[2][e] : v[1][e];
+      ve[e] = mix2(e0, e1, fe);
+      vo[e] = mix2(v[1][e], v[2][e], 0.25f);
+    }
+    bf16* orow = o + int64_t(r) * ho * c_tot;
+    *reinterpret_cast<uint4*>(orow) = narrow2(ve);
+    *reinterpret_cast<uint4*>(orow + c_tot) = narrow2(vo);
+  }
 }
 
 // adjoint of the upsample: low index i receives from outputs 2i-1 .. 2i+2
@@ -572,11 +619,15 @@ __device__ __forceinline__ void up_adj(int i, int n, int (&o)[4], float (&w)[4])
   }
 }
 // one thread = a column strip of the low-res gradient: output (y, x) for
-// every y of one map, 8 channels. High-res rows 2y - 1 .. 2y + 2 (columns
-// 2x - 1 .. 2x + 2) are needed; the last two rows of one y are the first two
-// of the next, so they slide in registers (raw bf16): 8 loads per output
-// instead of 16 (the one-output-per-thread kernel was L2-bound on the
-// re-reads). Same taps, weights and summation order (same bits).
+// every y of one map, 8 channels, from high-res rows 2y - 1 .. 2y + 2 and
+// columns 2x - 1 .. 2x + 2 (up_adj weights, folded at the borders). The
+// adjoint is separable: each high-res row is first reduced over its four
+// columns, h(o) = sum_b wx[b] d[o][ox[b]], once (two new rows per output: the
+// last two of one y are the first two of the next), then the output is
+// sum_a wy[a] h(2y - 1 + a); both in packed fp32 pairs. (The double sum with
+// the products wy[a] wx[b] in one chain widened and multiplied every tap of
+// every row twice and was issue-bound: 346 us for the 16 -> 32 adjoint at
+// B = 4,096, 3.8 TB/s.)
 __global__ void __launch_bounds__(256) k_up_bwd(const bf16* __restrict__ dhigh, int c_tot, int c, int hw_in,
                                                 int np, bf16* __restrict__ dlow) {
   pdl_wait();
@@ -600,22 +651,38 @@ __global__ void __launch_bounds__(256) k_up_bwd(const bf16* __restrict__ dhigh, 
 #pragma unroll
     for (int b = 0; b < 4; ++b) v[b] = ldraw(base + int64_t(oc * ho + ox[b]) * c_tot);
   };
-  uint4 r0[4], r1[4], r2[4], r3[4];  // high-res rows 2y - 1 .. 2y + 2 (clamped)
-  uint4 n2[4], n3[4];                 // rows 2y + 3, 2y + 4 (prefetched)
-  row(-1, r0);
-  row(0, r1);
+  auto colsum = [&](const uint4 (&v)[4], float2 (&h)[4]) {
+    float2 d[4];
+    widen2(v[0], d);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) h[e] = __fmul2_rn(d[e], make_float2(wx[0], wx[0]));
+#pragma unroll
+    for (int b = 1; b < 4; ++b) {
+      widen2(v[b], d);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) h[e] = __ffma2_rn(d[e], make_float2(wx[b], wx[b]), h[e]);
+    }
+  };
+  float2 h0[4], h1[4], h2[4], h3[4];  // column sums of high-res rows 2y - 1 .. 2y + 2 (clamped)
+  uint4 n2[4], n3[4];                 // raw rows 2y + 3, 2y + 4 (prefetched)
+  row(-1, n2);
+  row(0, n3);
+  colsum(n2, h0);
+  colsum(n3, h1);
+  row(1, n2);
+  row(2, n3);
+  colsum(n2, h2);
+  colsum(n3, h3);
   bf16* ob = dlow + (int64_t(m) * hw_in * hw_in + x) * c + c0;
-  row(1, r2);
-  row(2, r3);
   for (int y = 0; y < hw_in; ++y) {
     if (y > 0) {
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        r0[b] = r2[b];
-        r1[b] = r3[b];
-        r2[b] = n2[b];
-        r3[b] = n3[b];
+      for (int e = 0; e < 4; ++e) {
+        h0[e] = h2[e];
+        h1[e] = h3[e];
       }
+      colsum(n2, h2);
+      colsum(n3, h3);
     }
     if (y + 1 < hw_in) {  // the next y's new rows, in flight during this y's sums
       row(2 * y + 3, n2);
@@ -627,20 +694,15 @@ __global__ void __launch_bounds__(256) k_up_bwd(const bf16* __restrict__ dhigh, 
 #pragma unroll
     for (int a = 0; a < 4; ++a)
       if (oy[a] < 0 || oy[a] >= ho) wy[a] = 0.f;
-    float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float2 s[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const uint4* ra = a == 0 ? r0 : (a == 1 ? r1 : (a == 2 ? r2 : r3));
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        float d[8];
-        widen(ra[b], d);
-        const float w = wy[a] * wx[b];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) s[j] = fmaf(w, d[j], s[j]);
-      }
+    for (int e = 0; e < 4; ++e) {
+      s[e] = __fmul2_rn(h0[e], make_float2(wy[0], wy[0]));
+      s[e] = __ffma2_rn(h1[e], make_float2(wy[1], wy[1]), s[e]);
+      s[e] = __ffma2_rn(h2[e], make_float2(wy[2], wy[2]), s[e]);
+      s[e] = __ffma2_rn(h3[e], make_float2(wy[3], wy[3]), s[e]);
     }
-    st8(ob + int64_t(y) * hw_in * c, s);
+    *reinterpret_cast<uint4*>(ob + int64_t(y) * hw_in * c) = narrow2(s);
   }
 }
 
@@ -1137,7 +1199,7 @@ int layer_fwd(DrcbTrainer* T, int l, int64_t n, int64_t np, cudaStream_t st) {
   }
   if (P.up >= 0) {
     const Buf& cat = E->B[P.up];
-    const int64_t tot = np * 2 * hw2 * (coutp / 8);  // two outputs per thread
+    const int64_t tot = np * hw2 * (coutp / 8);  // a 2x2 output block per thread
     launch_pdl(k_up_fwd, nbk(tot), 256, 0, st, out.p, coutp, t.hw, np, cat.p, cat.c);
     TC_CHECK("k_up_fwd");
   }
