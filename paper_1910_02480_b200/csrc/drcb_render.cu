@@ -911,19 +911,38 @@ __global__ void k_bucket_sort(const int* offsets, int nb, int* items) {
   }
 }
 
+// the entries' pixel, normal and radiance copied into item order once per
+// frame (m <= 65,536 entries): the interpolation's gather loops then read
+// consecutive records instead of an index followed by dependent loads of
+// three SoA tables (same values, same order: bit-identical)
+template <typename R>
+struct alignas(4 * sizeof(R)) Rec4 {
+  R x, y, z, w;
+};
+template <typename R>
+__global__ void k_bucket_gather(const int* __restrict__ items, int64_t m, const int* m_dev,
+                                const int32_t* __restrict__ epx, const int32_t* __restrict__ epy,
+                                const R* __restrict__ en, const R* __restrict__ erad, int2* ipx,
+                                Rec4<R>* inrm, Rec4<R>* irad) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= (m_dev ? int64_t(*m_dev) : m)) return;
+  const int e = items[q];
+  ipx[q] = make_int2(epx[e], epy[e]);
+  inrm[q] = Rec4<R>{en[3 * e], en[3 * e + 1], en[3 * e + 2], R(0)};
+  irad[q] = Rec4<R>{erad[3 * e], erad[3 * e + 1], erad[3 * e + 2], R(0)};
+}
+
 // `items` is bucket-major and the buckets of a grid row are consecutive, so
 // the entries of buckets [bx0, bx1] of row yy are ONE contiguous range of
 // items: the gather loops run per bucket row, in exactly the bucket/entry
 // order of a per-bucket loop (same sums), without per-bucket loop overhead.
 template <typename R>
 __global__ void __launch_bounds__(TPB) k_interp(DevScene S, int W, int H, DrcbGBuffer gb,
-                                                 const int32_t* __restrict__ epx,
-                                                 const int32_t* __restrict__ epy,
-                                                 const R* __restrict__ en,
-                                                 const R* __restrict__ erad, int64_t m_cap,
+                                                 const int2* __restrict__ ipx,
+                                                 const Rec4<R>* __restrict__ inrm,
+                                                 const Rec4<R>* __restrict__ irad, int64_t m_cap,
                                                  const int* __restrict__ m_dev, int r,
                                                  int nbx, int nby, const int* __restrict__ off,
-                                                 const int* __restrict__ items,
                                                  const R* __restrict__ direct, R* image) {
   // a block is a 16 x (TPB/16) pixel tile inside one bucket column: a warp's
   // 16x2 pixels share their bucket ranges (uniform loop bounds)
@@ -943,8 +962,8 @@ __global__ void __launch_bounds__(TPB) k_interp(DevScene S, int W, int H, DrcbGB
     auto scan = [&](int q0, int q1) {
 #pragma unroll 1
       for (int q = q0; q < q1; ++q) {
-        const int e = items[q];
-        const long long dx = epx[e] - x, dy = epy[e] - y;
+        const int2 pe = ipx[q];
+        const long long dx = pe.x - x, dy = pe.y - y;
         const long long d2 = dx * dx + dy * dy;
         if (d2 < best) best = d2;
       }
@@ -977,15 +996,17 @@ __global__ void __launch_bounds__(TPB) k_interp(DevScene S, int W, int H, DrcbGB
       const int q1 = off[yy * nbx + bx1 + 1];
 #pragma unroll 1
       for (int q = off[yy * nbx + bx0]; q < q1; ++q) {
-        const int e = items[q];
-        const R dx = R(epx[e] - x), dy = R(epy[e] - y);
+        const int2 pe = ipx[q];
+        const R dx = R(pe.x - x), dy = R(pe.y - y);
         const R d2 = dx * dx + dy * dy;
         if (!(d2 <= rad2)) continue;
         const R dist = sqrt(d2);
         const R w_p = fmax(R(0), R(1) - dist / r_eff);
-        const R w_n = fmax(R(0), dot(ldr3(en + 3 * e), npx));
+        const Rec4<R> ne = inrm[q];
+        const R w_n = fmax(R(0), dot(V3<R>{ne.x, ne.y, ne.z}, npx));
         const R wgt = (w_p * w_n + w_p) + R(1e-4);
-        num = num + wgt * ldr3(erad + 3 * e);
+        const Rec4<R> le = irad[q];
+        num = num + wgt * V3<R>{le.x, le.y, le.z};
         den = den + wgt;
       }
     }
@@ -1181,10 +1202,21 @@ int launch_interp_composite(const DevScene& S, int W, int H, const DrcbGBuffer& 
     k_bucket_sort<<<nblocks(nb), TPB, 0, st>>>(offsets, nb, items);
     LAUNCH_CHECK();
   }
+  Rec4<R>* recs = nullptr;  // inrm (m), irad (m), then ipx (m)
+  DRCB_CUDA(cudaMallocAsync((void**)&recs, (2 * sizeof(Rec4<R>) + sizeof(int2)) * mm, st));
+  Rec4<R>* inrm = recs;
+  Rec4<R>* irad = recs + mm;
+  int2* ipx = reinterpret_cast<int2*>(recs + 2 * mm);
+  if (m > 0) {
+    k_bucket_gather<R><<<nblocks(m), TPB, 0, st>>>(items, m, m_dev, e_px, e_py, e_n, e_rad, ipx, inrm,
+                                                    irad);
+    LAUNCH_CHECK();
+  }
   const dim3 igrid(unsigned(nbx), unsigned((H + TPB / BUCKET - 1) / (TPB / BUCKET)));
-  k_interp<R><<<igrid, TPB, 0, st>>>(S, W, H, gb, e_px, e_py, e_n, e_rad, m, m_dev, r,
-                                                       nbx, nby, offsets, items, direct, image);
+  k_interp<R><<<igrid, TPB, 0, st>>>(S, W, H, gb, ipx, inrm, irad, m, m_dev, r, nbx, nby, offsets,
+                                     direct, image);
   LAUNCH_CHECK();
+  DRCB_CUDA(cudaFreeAsync(recs, st));
   DRCB_CUDA(cudaFreeAsync(buf, st));
   return 0;
 }
