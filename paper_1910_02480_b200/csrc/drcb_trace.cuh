@@ -312,14 +312,26 @@ __device__ HitRec<R> traverse(const DevScene& S, V3<R> O, V3<R> D, R tmin, R tma
         float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2), d = __ldg(nd + 3);
         // explicit FMAs (this TU builds with -fmad=false for the fp64 parity
         // path; one rounding instead of two stays inside the ROB slack)
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+        // packed pairs (FFMA2: per lane the same correctly rounded fma)
+        const float2 tx = __ffma2_rn(make_float2(a.x, a.y), make_float2(ix, ix), make_float2(-oix, -oix));
+        const float2 ty = __ffma2_rn(make_float2(a.z, a.w), make_float2(iy, iy), make_float2(-oiy, -oiy));
+        const float2 tz = __ffma2_rn(make_float2(c.x, c.y), make_float2(iz, iz), make_float2(-oiz, -oiz));
+        const float2 sx = __ffma2_rn(make_float2(b.x, b.y), make_float2(ix, ix), make_float2(-oix, -oix));
+        const float2 sy = __ffma2_rn(make_float2(b.z, b.w), make_float2(iy, iy), make_float2(-oiy, -oiy));
+        const float2 sz = __ffma2_rn(make_float2(c.z, c.w), make_float2(iz, iz), make_float2(-oiz, -oiz));
+        float tx0 = tx.x, tx1 = tx.y, ty0 = ty.x, ty1 = ty.y, tz0 = tz.x, tz1 = tz.y;
+        float sx0 = sx.x, sx1 = sx.y, sy0 = sy.x, sy1 = sy.y, sz0 = sz.x, sz1 = sz.y;
+#else
         float tx0 = __fmaf_rn(a.x, ix, -oix), tx1 = __fmaf_rn(a.y, ix, -oix);
         float ty0 = __fmaf_rn(a.z, iy, -oiy), ty1 = __fmaf_rn(a.w, iy, -oiy);
         float tz0 = __fmaf_rn(c.x, iz, -oiz), tz1 = __fmaf_rn(c.y, iz, -oiz);
-        float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
-        float f0 = fminf(fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fmaxf(tz0, tz1)) * ROB, tbest);
         float sx0 = __fmaf_rn(b.x, ix, -oix), sx1 = __fmaf_rn(b.y, ix, -oix);
         float sy0 = __fmaf_rn(b.z, iy, -oiy), sy1 = __fmaf_rn(b.w, iy, -oiy);
         float sz0 = __fmaf_rn(c.z, iz, -oiz), sz1 = __fmaf_rn(c.w, iz, -oiz);
+#endif
+        float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+        float f0 = fminf(fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fmaxf(tz0, tz1)) * ROB, tbest);
         float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), 0.0f));
         float f1 = fminf(fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fmaxf(sz0, sz1)) * ROB, tbest);
         bool h0 = n0 <= f0, h1 = n1 <= f1;
